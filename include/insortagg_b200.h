@@ -1,0 +1,177 @@
+/*
+ * insortagg_b200 — C ABI of the B200 (sm_100a) sort-based grouping /
+ * duplicate-removal / aggregation operator (arXiv 2010.00152, wide-merge
+ * path of the reference package `insortagg`).
+ *
+ * Plain pointers and sizes only; no torch types.  One handle per host thread
+ * (the reference operator is single-threaded per instance,
+ * /root/reference/pkg/src/insortagg/sortagg.py:725-732).
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/pkg/src/insortagg/):
+ *   isa_create        SortAggregate.__init__          sortagg.py:734-742
+ *                     (SortAggConfig validation       sortagg.py:69-82,
+ *                      Schema slot layout             core.py:119-157)
+ *   isa_execute       SortAggregate.execute/_execute_wide sortagg.py:744-784
+ *                     = index_run_generation (read-sort-write) sortagg.py:300-376
+ *                     + wide_merge                     sortagg.py:588-674
+ *   isa_result_copy   the returned list[Row] (sorted ascending, unfinalized
+ *                     state tuples)                    sortagg.py:757, 670-672
+ *   isa_metrics       SortAggregate.ledger (MetricsLedger) core.py:224-262,
+ *                     runs_after_generation / executed_steps sortagg.py:740-742
+ *   isa_cycles        OutputEstimator.note_cycle inputs sortagg.py:116-118, 345
+ *   isa_run_rows      RunMeta.row_count per run        runstore.py:145-154
+ *   isa_last_error    the EngineError message          core.py:15-40
+ *   isa_sample_keys / isa_partition    (new: multi-GPU range partitioning;
+ *                     no reference function)
+ *
+ * Status codes map 1:1 to the reference exception classes (core.py:15-40).
+ */
+#ifndef INSORTAGG_B200_H
+#define INSORTAGG_B200_H
+
+#include <stdint.h>
+
+#ifndef ISA_API
+#define ISA_API __attribute__((visibility("default")))
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ISA_MAX_KEY_COLS 8
+#define ISA_MAX_SLOTS 16
+#define ISA_MAX_VAL_COLS 16
+
+/* status codes (0 = ok) — one per reference exception class */
+enum isa_status {
+  ISA_OK = 0,
+  ISA_ERR_INVALID_INPUT = 1,      /* InvalidInputError       core.py:19 */
+  ISA_ERR_ORDERING = 2,           /* OrderingViolationError  core.py:23 */
+  ISA_ERR_CONTRACT = 3,           /* ContractViolationError  core.py:27 */
+  ISA_ERR_CORRUPTION = 4,         /* CorruptionError         core.py:31 */
+  ISA_ERR_RESOURCE = 5,           /* ResourceError           core.py:35 */
+  ISA_ERR_PLANNING = 6,           /* PlanningError           core.py:39 */
+  ISA_ERR_CUDA = 7                /* CUDA failure (Python maps to ResourceError) */
+};
+
+/* column element types */
+enum isa_dtype {
+  ISA_U8 = 1, ISA_I8 = 2, ISA_U16 = 3, ISA_I16 = 4, ISA_U32 = 5, ISA_I32 = 6,
+  ISA_U64 = 7, ISA_I64 = 8, ISA_F32 = 9, ISA_F64 = 10
+};
+
+/* aggregate-state slot combine op (Schema.merge_states, core.py:184-208) */
+enum isa_op { ISA_OP_ADD = 0, ISA_OP_MIN = 1, ISA_OP_MAX = 2 };
+/* slot accumulator type: int64 (exact) or float64 (core.py:196 semantics) */
+enum isa_slot_type { ISA_SLOT_I64 = 0, ISA_SLOT_F64 = 1 };
+/* slot initial value (Schema.make_state, core.py:162-182):
+ * ONE = constant 1 (COUNT, AVG's count half), COLUMN = value of a column
+ * (SUM/MIN/MAX/AVG-sum, or an already-built state slot). */
+enum isa_slot_src { ISA_SRC_ONE = 0, ISA_SRC_COLUMN = 1 };
+
+/* where spilled runs live */
+enum isa_run_tier { ISA_TIER_HOST = 0, ISA_TIER_HBM = 1 };
+
+typedef struct isa_config {
+  int64_t memory_budget;     /* M: group-table budget in rows  (SortAggConfig.memory_budget) */
+  int64_t page_capacity;     /* P: rows per run page           (SortAggConfig.page_capacity) */
+  int32_t run_tier;          /* isa_run_tier */
+  int32_t device;            /* CUDA device ordinal */
+  int64_t chunk_rows_max;    /* 0 = auto: largest run-generation chunk */
+  int64_t window_rows;       /* 0 = auto: host-input staging window (rows) */
+  int64_t merge_window_rows; /* 0 = auto: wide-merge key-range window capacity (rows) */
+} isa_config;
+
+typedef struct isa_schema {
+  int32_t n_key_cols;                       /* 1..8, most significant first */
+  int32_t key_dtypes[ISA_MAX_KEY_COLS];     /* integer isa_dtype; total width <= 128 bits */
+  int32_t n_val_cols;                       /* value (payload) columns */
+  int32_t val_dtypes[ISA_MAX_VAL_COLS];
+  int32_t n_slots;                          /* aggregate-state slots (core.py:141-157) */
+  int32_t slot_op[ISA_MAX_SLOTS];           /* isa_op */
+  int32_t slot_type[ISA_MAX_SLOTS];         /* isa_slot_type */
+  int32_t slot_src[ISA_MAX_SLOTS];          /* isa_slot_src */
+  int32_t slot_col[ISA_MAX_SLOTS];          /* value column index for ISA_SRC_COLUMN */
+} isa_schema;
+
+typedef struct isa_ledger {
+  /* MetricsLedger counters (core.py:232-243); CPU comparison counters are 0 */
+  int64_t row_comparisons;
+  int64_t ovc_decided_comparisons;
+  int64_t column_value_accesses;
+  int64_t hash_computations;
+  int64_t rows_spilled;
+  int64_t rows_read_back;
+  int64_t pages_written;
+  int64_t pages_read;
+  int64_t merge_steps;
+  int64_t merge_levels;
+  /* operator state */
+  int64_t runs_after_generation;
+  int64_t rows_seen;
+  int64_t n_groups;
+  int64_t merge_windows;
+  int64_t chunks;
+  /* device-side accounting */
+  int64_t bytes_h2d;
+  int64_t bytes_d2h;
+  int64_t kernel_launches;
+  double ms_run_generation;
+  double ms_wide_merge;
+} isa_ledger;
+
+typedef struct isa_handle isa_handle;
+
+/* library version string */
+ISA_API const char* isa_version(void);
+
+/* Validate config + schema, allocate per-handle workspace lazily.
+ * Returns NULL on error; the message is then available via isa_last_error(NULL). */
+ISA_API isa_handle* isa_create(const isa_config* config, const isa_schema* schema);
+ISA_API void isa_destroy(isa_handle* h);
+
+/* Group/aggregate n_rows rows.  key_cols[i] / val_cols[j] point to n_rows
+ * elements each, on the device (input_on_host = 0) or in pinned/pageable host
+ * memory (input_on_host = 1; copied in staged windows, overlapping compute).
+ * `stream` is a cudaStream_t (NULL = legacy default).  On return the result is
+ * held by the handle; *n_groups_out receives its row count. */
+ISA_API int isa_execute(isa_handle* h, int64_t n_rows, const void* const* key_cols,
+                const void* const* val_cols, int32_t input_on_host,
+                void* stream, int64_t* n_groups_out);
+
+/* Copy the last result out: key_out[i] receives column i in its input dtype,
+ * slot_out[s] receives slot s as int64 or float64 (per slot_type).  Buffers
+ * are device memory (out_on_host = 0) or host memory (out_on_host = 1). */
+ISA_API int isa_result_copy(isa_handle* h, void* const* key_out, void* const* slot_out,
+                    int32_t out_on_host, void* stream);
+
+ISA_API int isa_metrics(isa_handle* h, isa_ledger* out);
+/* Read-sort-write fill-cycle lengths of the last execute (rows per cycle). */
+ISA_API int64_t isa_cycles(isa_handle* h, int64_t* out, int64_t cap);
+/* Row counts of the runs of the last execute. */
+ISA_API int64_t isa_run_rows(isa_handle* h, int64_t* out, int64_t cap);
+ISA_API const char* isa_last_error(isa_handle* h);
+
+/* --- multi-GPU range partitioning primitives -------------------------- */
+/* Normalized (order-preserving, 128-bit) keys of rows 0, stride, 2*stride, ...
+ * into out_lo/out_hi (device, n_out = ceil(n_rows/stride) entries). */
+ISA_API int isa_sample_keys(isa_handle* h, int64_t n_rows, const void* const* key_cols,
+                    int64_t stride, uint64_t* out_lo, uint64_t* out_hi,
+                    void* stream);
+/* Stable partition of rows by destination d = #splitters <= key (splitters
+ * sorted, normalized, device arrays of n_splitters <= 255).  Columns are
+ * gathered into key_out/val_out (device, n_rows each) grouped by destination;
+ * counts_out (host, n_splitters+1 int64) receives rows per destination. */
+ISA_API int isa_partition(isa_handle* h, int64_t n_rows, const void* const* key_cols,
+                  const void* const* val_cols, const uint64_t* split_lo,
+                  const uint64_t* split_hi, int32_t n_splitters,
+                  void* const* key_out, void* const* val_out,
+                  int64_t* counts_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* INSORTAGG_B200_H */

@@ -1,0 +1,219 @@
+"""ctypes binding of libinsortagg_b200.so (declared in include/insortagg_b200.h).
+
+The library is the product path: there is no Python or CPU fallback.  If the
+shared object is missing or cannot be loaded, every operator call raises
+ResourceError naming the file and the build command.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .core import (
+    ContractViolationError,
+    CorruptionError,
+    InvalidInputError,
+    OrderingViolationError,
+    PlanningError,
+    ResourceError,
+)
+
+LIB_NAME = "libinsortagg_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+MAX_KEY_COLS = 8
+MAX_SLOTS = 16
+MAX_VAL_COLS = 16
+
+# isa_dtype
+U8, I8, U16, I16, U32, I32, U64, I64, F32, F64 = range(1, 11)
+DTYPE_BITS = {U8: 8, I8: 8, U16: 16, I16: 16, U32: 32, I32: 32, U64: 64, I64: 64, F32: 32, F64: 64}
+OP_ADD, OP_MIN, OP_MAX = 0, 1, 2
+SLOT_I64, SLOT_F64 = 0, 1
+SRC_ONE, SRC_COLUMN = 0, 1
+TIER_HOST, TIER_HBM = 0, 1
+
+_STATUS_ERRORS = {
+    1: InvalidInputError,
+    2: OrderingViolationError,
+    3: ContractViolationError,
+    4: CorruptionError,
+    5: ResourceError,
+    6: PlanningError,
+    7: ResourceError,
+}
+
+EXPORTED_SYMBOLS = (
+    "isa_version", "isa_create", "isa_destroy", "isa_execute", "isa_result_copy",
+    "isa_metrics", "isa_cycles", "isa_run_rows", "isa_last_error",
+    "isa_sample_keys", "isa_partition",
+)
+
+
+class IsaConfig(ctypes.Structure):
+    _fields_ = [
+        ("memory_budget", ctypes.c_int64),
+        ("page_capacity", ctypes.c_int64),
+        ("run_tier", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("chunk_rows_max", ctypes.c_int64),
+        ("window_rows", ctypes.c_int64),
+        ("merge_window_rows", ctypes.c_int64),
+    ]
+
+
+class IsaSchema(ctypes.Structure):
+    _fields_ = [
+        ("n_key_cols", ctypes.c_int32),
+        ("key_dtypes", ctypes.c_int32 * MAX_KEY_COLS),
+        ("n_val_cols", ctypes.c_int32),
+        ("val_dtypes", ctypes.c_int32 * MAX_VAL_COLS),
+        ("n_slots", ctypes.c_int32),
+        ("slot_op", ctypes.c_int32 * MAX_SLOTS),
+        ("slot_type", ctypes.c_int32 * MAX_SLOTS),
+        ("slot_src", ctypes.c_int32 * MAX_SLOTS),
+        ("slot_col", ctypes.c_int32 * MAX_SLOTS),
+    ]
+
+
+class IsaLedger(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_int64) for name in (
+        "row_comparisons", "ovc_decided_comparisons", "column_value_accesses",
+        "hash_computations", "rows_spilled", "rows_read_back", "pages_written",
+        "pages_read", "merge_steps", "merge_levels", "runs_after_generation",
+        "rows_seen", "n_groups", "merge_windows", "chunks", "bytes_h2d",
+        "bytes_d2h", "kernel_launches")] + [
+        ("ms_run_generation", ctypes.c_double),
+        ("ms_wide_merge", ctypes.c_double),
+    ]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_lib = None
+_load_error = None
+
+
+def load():
+    """Load (once) and return the CDLL; raise ResourceError when absent."""
+    global _lib, _load_error
+    if _lib is not None:
+        return _lib
+    if _load_error is not None:
+        raise ResourceError(_load_error)
+    if not os.path.exists(LIB_PATH):
+        _load_error = (f"{LIB_PATH} is missing: build it with "
+                       "`make -C paper_2010_00152_b200/csrc` or __graft_entry__.build()")
+        raise ResourceError(_load_error)
+    try:
+        lib = ctypes.CDLL(LIB_PATH)
+    except OSError as exc:
+        _load_error = f"cannot load {LIB_PATH}: {exc}"
+        raise ResourceError(_load_error) from exc
+    vp = ctypes.c_void_p
+    pp = ctypes.POINTER(ctypes.c_void_p)
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    lib.isa_version.restype = ctypes.c_char_p
+    lib.isa_version.argtypes = []
+    lib.isa_create.restype = vp
+    lib.isa_create.argtypes = [ctypes.POINTER(IsaConfig), ctypes.POINTER(IsaSchema)]
+    lib.isa_destroy.restype = None
+    lib.isa_destroy.argtypes = [vp]
+    lib.isa_execute.restype = ctypes.c_int
+    lib.isa_execute.argtypes = [vp, ctypes.c_int64, pp, pp, ctypes.c_int32, vp, i64p]
+    lib.isa_result_copy.restype = ctypes.c_int
+    lib.isa_result_copy.argtypes = [vp, pp, pp, ctypes.c_int32, vp]
+    lib.isa_metrics.restype = ctypes.c_int
+    lib.isa_metrics.argtypes = [vp, ctypes.POINTER(IsaLedger)]
+    lib.isa_cycles.restype = ctypes.c_int64
+    lib.isa_cycles.argtypes = [vp, i64p, ctypes.c_int64]
+    lib.isa_run_rows.restype = ctypes.c_int64
+    lib.isa_run_rows.argtypes = [vp, i64p, ctypes.c_int64]
+    lib.isa_last_error.restype = ctypes.c_char_p
+    lib.isa_last_error.argtypes = [vp]
+    lib.isa_sample_keys.restype = ctypes.c_int
+    lib.isa_sample_keys.argtypes = [vp, ctypes.c_int64, pp, ctypes.c_int64, vp, vp, vp]
+    lib.isa_partition.restype = ctypes.c_int
+    lib.isa_partition.argtypes = [vp, ctypes.c_int64, pp, pp, vp, vp, ctypes.c_int32, pp, pp, i64p, vp]
+    _lib = lib
+    return lib
+
+
+def version():
+    return load().isa_version().decode()
+
+
+def _ptr_array(ptrs):
+    arr = (ctypes.c_void_p * max(1, len(ptrs)))()
+    for i, p in enumerate(ptrs):
+        arr[i] = p
+    return arr
+
+
+class Handle:
+    """One native operator instance (not thread-safe; one per host thread)."""
+
+    def __init__(self, config: IsaConfig, schema: IsaSchema):
+        self._lib = load()
+        self.schema = schema
+        h = self._lib.isa_create(ctypes.byref(config), ctypes.byref(schema))
+        if not h:
+            msg = self._lib.isa_last_error(None).decode()
+            raise InvalidInputError(msg) if "CUDA" not in msg and "cuda" not in msg else ResourceError(msg)
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.isa_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, status):
+        if status != 0:
+            msg = self._lib.isa_last_error(self._h).decode()
+            raise _STATUS_ERRORS.get(status, ResourceError)(msg)
+
+    def execute(self, n_rows, key_ptrs, val_ptrs, on_host, stream):
+        out = ctypes.c_int64(0)
+        self._check(self._lib.isa_execute(self._h, n_rows, _ptr_array(key_ptrs), _ptr_array(val_ptrs),
+                                          1 if on_host else 0, stream, ctypes.byref(out)))
+        return out.value
+
+    def result_copy(self, key_ptrs, slot_ptrs, on_host, stream):
+        self._check(self._lib.isa_result_copy(self._h, _ptr_array(key_ptrs), _ptr_array(slot_ptrs),
+                                              1 if on_host else 0, stream))
+
+    def metrics(self):
+        led = IsaLedger()
+        self._check(self._lib.isa_metrics(self._h, ctypes.byref(led)))
+        return led
+
+    def cycles(self):
+        n = self._lib.isa_cycles(self._h, None, 0)
+        buf = (ctypes.c_int64 * max(1, n))()
+        self._lib.isa_cycles(self._h, buf, n)
+        return [buf[i] for i in range(n)]
+
+    def run_rows(self):
+        n = self._lib.isa_run_rows(self._h, None, 0)
+        buf = (ctypes.c_int64 * max(1, n))()
+        self._lib.isa_run_rows(self._h, buf, n)
+        return [buf[i] for i in range(n)]
+
+    def sample_keys(self, n_rows, key_ptrs, stride, out_lo, out_hi, stream):
+        self._check(self._lib.isa_sample_keys(self._h, n_rows, _ptr_array(key_ptrs), stride,
+                                              out_lo, out_hi, stream))
+
+    def partition(self, n_rows, key_ptrs, val_ptrs, split_lo, split_hi, n_split, key_out, val_out, stream):
+        counts = (ctypes.c_int64 * (n_split + 1))()
+        self._check(self._lib.isa_partition(self._h, n_rows, _ptr_array(key_ptrs), _ptr_array(val_ptrs),
+                                            split_lo, split_hi, n_split, _ptr_array(key_out),
+                                            _ptr_array(val_out), counts, stream))
+        return [counts[i] for i in range(n_split + 1)]

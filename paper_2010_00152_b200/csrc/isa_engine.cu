@@ -1,0 +1,1038 @@
+// Host runtime of the B200 sort-based aggregation operator + the C ABI.
+//
+// Algorithm (exact read-sort-write semantics of the reference):
+//
+//   index_run_generation (sortagg.py:300-376, RSW branch :344-351):
+//     rows stream into an ordered index of at most M groups; duplicates are
+//     absorbed; the first row whose key is new while M groups are resident
+//     flushes the whole index as one sorted unique run and starts a new
+//     fill cycle.  Here the index is a sorted group table T in HBM and rows
+//     are processed in chunks:
+//       * |T| <= 8: the "absorb" kernel probes every row against T held in
+//         registers and aggregates hits in place; only misses are sorted.
+//       * otherwise: the chunk's (key, row) pairs are radix-sorted on their
+//         varying bits.
+//     From the sorted chunk, every key that is absent from T contributes its
+//     first row position to a bitmap; if |T| + new keys > M, the flush
+//     position f is the (M - |T| + 1)-th set bit — exactly the row at which
+//     the reference's insert_or_aggregate returns NEEDS_EVICTION.  Rows
+//     before f are collapsed (segmented reduce) and merged into T; T becomes
+//     a run of exactly M groups; the next chunk starts at f.
+//   wide_merge (sortagg.py:588-674):
+//     all runs are merged in one step.  The forecasting priority queue +
+//     strict watermark of the reference emit a key only once every run has
+//     advanced past it; on the GPU this is a partition of the key space into
+//     windows: window [s_i, s_{i+1}) is final as soon as every run's slice of
+//     it has been read.  Each window's slices are staged (H2D for host-tier
+//     runs), radix-sorted and collapsed.
+#include "isa_kernels.h"
+#include "../../include/insortagg_b200.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace {
+
+using namespace isa;
+
+struct IsaError : std::runtime_error {
+  int code;
+  IsaError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw IsaError(ISA_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
+  } while (0)
+
+static thread_local std::string g_create_error;
+
+// ------------------------------------------------------------ buffers ----
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t need) {
+    if (need <= bytes) return;
+    if (p) CK(cudaFree(p));
+    size_t nb = std::max(need, bytes + bytes / 2);
+    nb = (nb + 255) & ~(size_t)255;
+    p = nullptr;
+    CK(cudaMalloc(&p, nb));
+    bytes = nb;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T> T* as() { return (T*)p; }
+};
+
+// pinned host blocks, bump-allocated per execute and reused across executes
+struct PinnedPool {
+  struct Block { char* p; size_t bytes; size_t used; };
+  std::vector<Block> blocks;
+  void reset() { for (auto& b : blocks) b.used = 0; }
+  char* alloc(size_t bytes) {
+    bytes = (bytes + 255) & ~(size_t)255;
+    for (auto& b : blocks)
+      if (b.bytes - b.used >= bytes) { char* r = b.p + b.used; b.used += bytes; return r; }
+    size_t nb = std::max(bytes, (size_t)256 << 20);
+    void* p = nullptr;
+    CK(cudaHostAlloc(&p, nb, cudaHostAllocMapped | cudaHostAllocPortable));
+    blocks.push_back({(char*)p, nb, bytes});
+    return (char*)p;
+  }
+  void release() {
+    for (auto& b : blocks) cudaFreeHost(b.p);
+    blocks.clear();
+  }
+};
+
+// device blocks for HBM-tier runs, same discipline
+struct DevicePool {
+  struct Block { char* p; size_t bytes; size_t used; };
+  std::vector<Block> blocks;
+  void reset() { for (auto& b : blocks) b.used = 0; }
+  char* alloc(size_t bytes) {
+    bytes = (bytes + 255) & ~(size_t)255;
+    for (auto& b : blocks)
+      if (b.bytes - b.used >= bytes) { char* r = b.p + b.used; b.used += bytes; return r; }
+    size_t nb = std::max(bytes, (size_t)1 << 30);
+    void* p = nullptr;
+    CK(cudaMalloc(&p, nb));
+    blocks.push_back({(char*)p, nb, bytes});
+    return (char*)p;
+  }
+  void release() {
+    for (auto& b : blocks) cudaFree(b.p);
+    blocks.clear();
+  }
+};
+
+// sorted unique group table (keys SoA, states AoS) in device memory
+struct Table {
+  DevBuf lo, hi, st;
+  u32 n = 0;
+  u64* plo() { return lo.as<u64>(); }
+  u64* phi() { return hi.as<u64>(); }
+  u64* pst() { return st.as<u64>(); }
+  void reserve(size_t cap, int KW, int S) {
+    lo.ensure(cap * 8);
+    if (KW == 2) hi.ensure(cap * 8);
+    if (S) st.ensure(cap * 8 * S);
+  }
+  void release() { lo.release(); hi.release(); st.release(); n = 0; }
+};
+
+struct Run {
+  u64* lo = nullptr;   // host-mapped or device pointer usable by kernels
+  u64* hi = nullptr;
+  u64* st = nullptr;
+  u32 rows = 0;
+  bool host = true;
+};
+
+struct Window {      // staged host input
+  int64_t start = 0, end = 0;
+  std::vector<DevBuf> keys, vals;
+  cudaEvent_t ready = nullptr;
+  bool staged = false;
+};
+
+struct Engine {
+  isa_config cfg;
+  isa_schema sch;
+  int KW = 1, S = 0, key_bits = 0;
+  KeyDesc kd0;
+  SlotDesc sd0;
+  int ops[ISA_MAX_SLOTS], types[ISA_MAX_SLOTS];
+  int dev = 0, num_sms = 148;
+  cudaStream_t st = nullptr;          // caller's stream for the current call
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::string err;
+
+  // workspace
+  DevBuf s_lo[2], s_hi[2], s_val[2], tile_hist, scan_tmp;
+  DevBuf scal;   // small device scalars (u64 varying[2], u32 counters)
+  u32* h_scal = nullptr;   // pinned mirror (64 words)
+  DevBuf bitmap, word_tmp;
+  DevBuf cl_flags, cl_partial, cl_pslot;
+  DevBuf mg_rank_a, mg_match_a, mg_rank_b, mg_match_b;
+  DevBuf ab_partials, ab_miss_buf, ab_miss_cnt, ab_miss_off, miss_list;
+  Table T, U, Tn;   // resident table, chunk collapse, merge output
+  std::vector<cudaEvent_t> tbl_free;   // not used for now
+  TinyTable tiny;   // host mirror of T keys when |T| <= 8
+  // runs
+  PinnedPool pinned;
+  DevicePool devpool;
+  std::vector<Run> runs;
+  cudaEvent_t spill_done = nullptr;
+  // wide merge
+  DevBuf stg_lo[2], stg_hi[2], stg_st[2];
+  cudaEvent_t stg_ready[2] = {nullptr, nullptr}, stg_free[2] = {nullptr, nullptr};
+  DevBuf runref_dev, bounds_lo, bounds_hi, bounds_out;
+  Table result;
+  DevBuf out_tmp;
+  // host input windows
+  Window win[2];
+  // accounting
+  isa_ledger led;
+  std::vector<int64_t> cycles;
+  int64_t launches = 0;
+
+  Engine(const isa_config& c, const isa_schema& s) : cfg(c), sch(s) {
+    validate();
+    CK(cudaSetDevice(cfg.device));
+    dev = cfg.device;
+    CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&spill_done, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&stg_ready[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&stg_free[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&win[i].ready, cudaEventDisableTiming));
+    }
+    CK(cudaHostAlloc((void**)&h_scal, 64 * sizeof(u64), cudaHostAllocDefault));
+    scal.ensure(64 * sizeof(u64));
+    memset(&led, 0, sizeof(led));
+  }
+  ~Engine() {
+    cudaSetDevice(dev);
+    cudaDeviceSynchronize();
+    DevBuf* bufs[] = {&s_lo[0], &s_lo[1], &s_hi[0], &s_hi[1], &s_val[0], &s_val[1], &tile_hist, &scan_tmp,
+                      &scal, &bitmap, &word_tmp, &cl_flags, &cl_partial, &cl_pslot, &mg_rank_a, &mg_match_a,
+                      &mg_rank_b, &mg_match_b, &ab_partials, &ab_miss_buf, &ab_miss_cnt, &ab_miss_off,
+                      &miss_list, &stg_lo[0], &stg_lo[1], &stg_hi[0], &stg_hi[1], &stg_st[0], &stg_st[1],
+                      &runref_dev, &bounds_lo, &bounds_hi, &bounds_out, &out_tmp};
+    for (auto* b : bufs) b->release();
+    for (auto& w : win) { for (auto& b : w.keys) b.release(); for (auto& b : w.vals) b.release(); }
+    T.release(); U.release(); Tn.release(); result.release();
+    pinned.release();
+    devpool.release();
+    if (h_scal) cudaFreeHost(h_scal);
+    if (h2d) cudaStreamDestroy(h2d);
+    if (d2h) cudaStreamDestroy(d2h);
+    if (spill_done) cudaEventDestroy(spill_done);
+    for (int i = 0; i < 2; ++i) {
+      if (stg_ready[i]) cudaEventDestroy(stg_ready[i]);
+      if (stg_free[i]) cudaEventDestroy(stg_free[i]);
+      if (win[i].ready) cudaEventDestroy(win[i].ready);
+    }
+  }
+
+  // ---------------------------------------------------------- validate --
+  void validate() {
+    // SortAggConfig.__post_init__ (sortagg.py:69-82)
+    if (cfg.page_capacity < 1) throw IsaError(ISA_ERR_INVALID_INPUT, "page capacity must be positive");
+    if (cfg.memory_budget < 2 * cfg.page_capacity)
+      throw IsaError(ISA_ERR_INVALID_INPUT, "memory budget must cover two pages");
+    if (cfg.memory_budget / cfg.page_capacity < 2) throw IsaError(ISA_ERR_INVALID_INPUT, "fan-in must be at least 2");
+    if (cfg.memory_budget > (int64_t)1 << 30)
+      throw IsaError(ISA_ERR_INVALID_INPUT, "memory budget above 2^30 groups is not supported");
+    if (cfg.run_tier != ISA_TIER_HOST && cfg.run_tier != ISA_TIER_HBM)
+      throw IsaError(ISA_ERR_INVALID_INPUT, "unknown run tier");
+    if (sch.n_key_cols < 1) throw IsaError(ISA_ERR_INVALID_INPUT, "schema needs at least one key column");
+    if (sch.n_key_cols > ISA_MAX_KEY_COLS) throw IsaError(ISA_ERR_INVALID_INPUT, "too many key columns");
+    if (sch.n_slots < 0 || sch.n_slots > ISA_MAX_SLOTS) throw IsaError(ISA_ERR_INVALID_INPUT, "too many state slots");
+    if (sch.n_val_cols < 0 || sch.n_val_cols > ISA_MAX_VAL_COLS)
+      throw IsaError(ISA_ERR_INVALID_INPUT, "too many value columns");
+    key_bits = 0;
+    for (int c = 0; c < sch.n_key_cols; ++c) {
+      int dt = sch.key_dtypes[c];
+      if (dt < ISA_U8 || dt > ISA_I64) throw IsaError(ISA_ERR_INVALID_INPUT, "key columns must be integer");
+      key_bits += dtype_bits(dt);
+    }
+    if (key_bits > 128) throw IsaError(ISA_ERR_INVALID_INPUT, "composite key wider than 128 bits");
+    KW = key_bits > 64 ? 2 : 1;
+    memset(&kd0, 0, sizeof(kd0));
+    kd0.ncols = sch.n_key_cols;
+    kd0.total_bits = key_bits;
+    int pos = key_bits;
+    for (int c = 0; c < sch.n_key_cols; ++c) {
+      int w = dtype_bits(sch.key_dtypes[c]);
+      pos -= w;
+      kd0.dtype[c] = sch.key_dtypes[c];
+      kd0.width[c] = w;
+      kd0.shift[c] = pos;
+    }
+    for (int j = 0; j < sch.n_val_cols; ++j)
+      if (sch.val_dtypes[j] < ISA_U8 || sch.val_dtypes[j] > ISA_F64)
+        throw IsaError(ISA_ERR_INVALID_INPUT, "unknown value column dtype");
+    S = sch.n_slots;
+    memset(&sd0, 0, sizeof(sd0));
+    sd0.nslots = S;
+    for (int s = 0; s < S; ++s) {
+      int op = sch.slot_op[s], ty = sch.slot_type[s], src = sch.slot_src[s];
+      if (op < 0 || op > 2) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown aggregate op");
+      if (ty != ISA_SLOT_I64 && ty != ISA_SLOT_F64) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown slot type");
+      if (src != ISA_SRC_ONE && src != ISA_SRC_COLUMN) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown slot source");
+      sd0.op[s] = ops[s] = op;
+      sd0.type[s] = types[s] = ty;
+      sd0.src[s] = src;
+      if (src == ISA_SRC_COLUMN) {
+        int col = sch.slot_col[s];
+        if (col < 0 || col >= sch.n_val_cols) throw IsaError(ISA_ERR_INVALID_INPUT, "slot column out of range");
+        int dt = sch.val_dtypes[col];
+        if (ty == ISA_SLOT_I64 && dtype_float(dt))
+          throw IsaError(ISA_ERR_INVALID_INPUT, "integer aggregate slot fed by a float column");
+        sd0.dtype[s] = dt;
+      }
+    }
+  }
+
+  // ------------------------------------------------------------ helpers --
+  void sync() { CK(cudaStreamSynchronize(st)); }
+  u32 read_u32(const u32* dptr) {
+    CK(cudaMemcpyAsync(h_scal, dptr, sizeof(u32), cudaMemcpyDeviceToHost, st));
+    sync();
+    return h_scal[0];
+  }
+  u32* dscal32(int i) { return (u32*)((u64*)scal.p + 8) + i; }   // u32 counters after 8 u64
+  u64* dvary() { return (u64*)scal.p; }
+
+  KeyDesc kd_at(const void* const* key_base) const {
+    KeyDesc k = kd0;
+    for (int c = 0; c < kd0.ncols; ++c) k.ptr[c] = key_base[c];
+    return k;
+  }
+  SlotDesc sd_at(const void* const* val_base) const {
+    SlotDesc s = sd0;
+    for (int k = 0; k < S; ++k) s.ptr[k] = (sd0.src[k] == SRC_COL) ? val_base[sch.slot_col[k]] : nullptr;
+    return s;
+  }
+
+  void ensure_sort(size_t n) {
+    for (int i = 0; i < 2; ++i) {
+      s_lo[i].ensure(n * 8);
+      if (KW == 2) s_hi[i].ensure(n * 8);
+      s_val[i].ensure(n * 4);
+    }
+    tile_hist.ensure(sort_hist_words((u32)n) * 4 + 64);
+    size_t sc = std::max<size_t>(scan_tmp_words((u32)(sort_hist_words((u32)n) + 1)), scan_tmp_words((u32)n + 1));
+    scan_tmp.ensure((sc + 64) * 4);
+  }
+  void ensure_collapse(size_t m) {
+    cl_flags.ensure((m + 1) * 4);
+    cl_pslot.ensure(((m + 7) / 8 + 1) * 4);
+    if (S) cl_partial.ensure(((m + 7) / 8 + 1) * 8 * S);
+    scan_tmp.ensure((scan_tmp_words((u32)m + 1) + 64) * 4);
+  }
+  void ensure_merge(size_t na, size_t nb) {
+    mg_rank_a.ensure((na + 1) * 4);
+    mg_match_a.ensure((2 * na + 2) * 4);
+    mg_rank_b.ensure((nb + 1) * 4);
+    mg_match_b.ensure((2 * nb + 2) * 4);
+    scan_tmp.ensure((scan_tmp_words((u32)std::max(na, nb) + 1) + 64) * 4);
+  }
+
+  // Sort (key, pos) pairs of rows row0 + pos[i] (pos == nullptr: row0 + i),
+  // i < m.  Returns the buffer index holding the sorted result.
+  int sort_rows(const KeyDesc& kd, int64_t row0, const u32* pos, u32 m) {
+    ensure_sort(m);
+    CK(cudaMemsetAsync(dvary(), 0, 2 * sizeof(u64), st));
+    build_keys(KW, kd, row0, pos, m, s_lo[0].as<u64>(), s_hi[0].as<u64>(), s_val[0].as<u32>(), dvary(), st);
+    launches += 1;
+    return sort_built(m);
+  }
+  int sort_built(u32 m) {
+    CK(cudaMemcpyAsync(h_scal, dvary(), 2 * sizeof(u64), cudaMemcpyDeviceToHost, st));
+    sync();
+    u64 vlo = ((u64*)h_scal)[0], vhi = ((u64*)h_scal)[1];
+    int hb = -1, lb = 128;
+    if (vhi) { hb = 127 - __builtin_clzll(vhi); }
+    else if (vlo) { hb = 63 - __builtin_clzll(vlo); }
+    if (vlo) lb = __builtin_ctzll(vlo);
+    else if (vhi) lb = 64 + __builtin_ctzll(vhi);
+    if (hb < 0) return 0;   // all keys equal: already sorted (stable)
+    SortBufs b;
+    for (int i = 0; i < 2; ++i) { b.lo[i] = s_lo[i].as<u64>(); b.hi[i] = s_hi[i].as<u64>(); b.val[i] = s_val[i].as<u32>(); }
+    b.tile_hist = tile_hist.as<u32>();
+    b.scan_tmp = scan_tmp.as<u32>();
+    return radix_sort_pairs(KW, b, m, lb, hb + 1, st, &launches);
+  }
+
+  // Flush analysis on a sorted chunk of `span` rows: number of keys absent
+  // from T; if |T| + new > M returns the chunk-relative flush row, else span.
+  u32 flush_point(int cur, u32 m, u32 span) {
+    u32 nw = (span + 31) / 32;
+    bitmap.ensure((size_t)nw * 4 + 4);
+    word_tmp.ensure((size_t)nw * 4 + 4);
+    scan_tmp.ensure((scan_tmp_words(nw + 1) + 64) * 4);
+    CK(cudaMemsetAsync(bitmap.p, 0, (size_t)nw * 4, st));
+    CK(cudaMemsetAsync(dscal32(0), 0, sizeof(u32), st));
+    new_heads(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, T.plo(), T.phi(), T.n,
+              bitmap.as<u32>(), dscal32(0), st);
+    launches += 1;
+    u32 n_new = read_u32(dscal32(0));
+    const int64_t M = cfg.memory_budget;
+    last_new = n_new;
+    if ((int64_t)T.n + n_new <= M) return span;
+    u32 k = (u32)(M - (int64_t)T.n + 1);
+    select_kth_bit(bitmap.as<u32>(), span, k, word_tmp.as<u32>(), scan_tmp.as<u32>(), dscal32(1), st);
+    launches += 5;
+    return read_u32(dscal32(1));
+  }
+  u32 last_new = 0;
+  bool tn_busy = false;
+
+  // U <- collapse(sorted chunk restricted to positions < limit)
+  void collapse_chunk(int cur, u32 m, u32 limit, const SlotDesc& sd, int64_t row0, const u64* st_in, Table& out,
+                      size_t out_cap) {
+    ensure_collapse(m);
+    out.reserve(out_cap, KW, S);
+    CollapseTmp ct;
+    ct.flags = cl_flags.as<u32>();
+    ct.scan_tmp = scan_tmp.as<u32>();
+    ct.partial = cl_partial.as<u64>();
+    ct.partial_slot = cl_pslot.as<u32>();
+    ct.total = dscal32(2);
+    collapse(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, limit, sd, row0, st_in,
+             out.plo(), out.phi(), out.pst(), ct, st);
+    launches += 6;
+    out.n = read_u32(dscal32(2));
+  }
+
+  // Tn <- merge_combine(T, U); swap into T
+  void merge_into_T() {
+    if (U.n == 0) return;
+    if (T.n == 0) { std::swap(T, U); U.n = 0; return; }
+    ensure_merge(T.n, U.n);
+    if (tn_busy) {   // Tn's buffers are still being copied to the host tier
+      CK(cudaStreamWaitEvent(st, spill_done, 0));
+      tn_busy = false;
+    }
+    Tn.reserve((size_t)T.n + U.n, KW, S);
+    MergeTmp mt;
+    mt.rank_a = mg_rank_a.as<u32>(); mt.match_a = mg_match_a.as<u32>();
+    mt.rank_b = mg_rank_b.as<u32>(); mt.match_b = mg_match_b.as<u32>();
+    mt.scan_tmp = scan_tmp.as<u32>();
+    mt.total = dscal32(4);
+    merge_combine(KW, S, ops, types, T.plo(), T.phi(), T.pst(), T.n, U.plo(), U.phi(), U.pst(), U.n, Tn.plo(),
+                  Tn.phi(), Tn.pst(), mt, st);
+    launches += 12;
+    u32 matches = read_u32(dscal32(4));
+    Tn.n = T.n + U.n - matches;
+    std::swap(T, Tn);
+    Tn.n = 0;
+    U.n = 0;
+  }
+
+  void refresh_tiny() {
+    if (T.n == 0 || T.n > 8) return;
+    memset(&tiny, 0, sizeof(tiny));
+    CK(cudaMemcpyAsync(h_scal, T.plo(), T.n * 8, cudaMemcpyDeviceToHost, st));
+    if (KW == 2) CK(cudaMemcpyAsync((u64*)h_scal + 8, T.phi(), T.n * 8, cudaMemcpyDeviceToHost, st));
+    sync();
+    for (u32 j = 0; j < T.n; ++j) {
+      tiny.lo[j] = ((u64*)h_scal)[j];
+      tiny.hi[j] = KW == 2 ? ((u64*)h_scal)[8 + j] : 0;
+    }
+  }
+
+  // T becomes a run (RunWriter of a read-sort-write flush, sortagg.py:344-350)
+  void spill_T() {
+    if (T.n == 0) return;
+    Run r;
+    r.rows = T.n;
+    size_t nb_key = (size_t)T.n * 8, nb_st = (size_t)T.n * 8 * S;
+    if (cfg.run_tier == ISA_TIER_HOST) {
+      r.host = true;
+      char* klo = pinned.alloc(nb_key);
+      char* khi = KW == 2 ? pinned.alloc(nb_key) : nullptr;
+      char* kst = S ? pinned.alloc(nb_st) : nullptr;
+      // copy on the d2h stream after the table is complete; the table's
+      // buffers are recycled only after the copy finished (event below)
+      cudaEvent_t ev;
+      CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      CK(cudaEventRecord(ev, st));
+      CK(cudaStreamWaitEvent(d2h, ev, 0));
+      cudaEventDestroy(ev);
+      CK(cudaMemcpyAsync(klo, T.plo(), nb_key, cudaMemcpyDeviceToHost, d2h));
+      if (KW == 2) CK(cudaMemcpyAsync(khi, T.phi(), nb_key, cudaMemcpyDeviceToHost, d2h));
+      if (S) CK(cudaMemcpyAsync(kst, T.pst(), nb_st, cudaMemcpyDeviceToHost, d2h));
+      CK(cudaEventRecord(spill_done, d2h));
+      u64 *dlo = nullptr, *dhi = nullptr, *dst = nullptr;
+      CK(cudaHostGetDevicePointer((void**)&dlo, klo, 0));
+      if (khi) CK(cudaHostGetDevicePointer((void**)&dhi, khi, 0));
+      if (kst) CK(cudaHostGetDevicePointer((void**)&dst, kst, 0));
+      r.lo = dlo; r.hi = dhi; r.st = dst;
+      led.bytes_d2h += nb_key * KW + nb_st;
+      // the spilled table's buffers go to Tn (free) once the copy is done:
+      // the compute stream waits for the copy before reusing them
+      std::swap(T, Tn);
+      T.n = 0;
+      tn_busy = true;   // Tn holds the spilled buffers until spill_done
+    } else {
+      r.host = false;
+      char* klo = devpool.alloc(nb_key);
+      char* khi = KW == 2 ? devpool.alloc(nb_key) : nullptr;
+      char* kst = S ? devpool.alloc(nb_st) : nullptr;
+      CK(cudaMemcpyAsync(klo, T.plo(), nb_key, cudaMemcpyDeviceToDevice, st));
+      if (KW == 2) CK(cudaMemcpyAsync(khi, T.phi(), nb_key, cudaMemcpyDeviceToDevice, st));
+      if (S) CK(cudaMemcpyAsync(kst, T.pst(), nb_st, cudaMemcpyDeviceToDevice, st));
+      r.lo = (u64*)klo; r.hi = (u64*)khi; r.st = (u64*)kst;
+      T.n = 0;
+    }
+    runs.push_back(r);
+    led.rows_spilled += r.rows;
+    led.pages_written += (r.rows + cfg.page_capacity - 1) / cfg.page_capacity;
+  }
+
+  // ------------------------------------------------------------ chunks --
+  // Process rows [a, b) (absolute), columns addressed by (kd, sd) with
+  // row0_base = absolute row of column element 0.  Returns the absolute row
+  // at which the next chunk starts (b, or the flush row).
+  int64_t process_chunk(const KeyDesc& kd, const SlotDesc& sd, int64_t base, int64_t a, int64_t b) {
+    const u32 span = (u32)(b - a);
+    const int64_t row0 = a - base;   // column element of row a
+    led.chunks++;
+    if (T.n > 0 && T.n <= 8 && absorb_supported((int)T.n, S)) return absorb_chunk(kd, sd, row0, a, span);
+    int cur = sort_rows(kd, row0, nullptr, span);
+    u32 f = flush_point(cur, span, span);
+    collapse_chunk(cur, span, f, sd, row0, nullptr, U, std::min<int64_t>(span, cfg.memory_budget));
+    merge_into_T();
+    if (f < span) {
+      spill_T();
+      return a + f;
+    }
+    refresh_tiny();
+    return b;
+  }
+
+  int64_t absorb_chunk(const KeyDesc& kd, const SlotDesc& sd, int64_t row0, int64_t a, u32 span) {
+    const int nt = (int)T.n;
+    u32 grid, rpc;
+    absorb_geometry(span, num_sms, &grid, &rpc);
+    ab_partials.ensure((size_t)grid * nt * std::max(S, 1) * 8 + 64);
+    ab_miss_buf.ensure((size_t)grid * rpc * 4 + 64);
+    ab_miss_cnt.ensure((size_t)(grid + 1) * 4);
+    ab_miss_off.ensure((size_t)(grid + 1) * 4);
+    scan_tmp.ensure((scan_tmp_words(grid + 1) + 64) * 4);
+    absorb_tiny(KW, nt, kd, sd, row0, span, tiny, grid, rpc, ab_partials.as<u64>(), ab_miss_buf.as<u32>(),
+                ab_miss_cnt.as<u32>(), st);
+    launches += 1;
+    CK(cudaMemcpyAsync(ab_miss_off.p, ab_miss_cnt.p, (size_t)grid * 4, cudaMemcpyDeviceToDevice, st));
+    scan_exclusive_u32(ab_miss_off.as<u32>(), grid, scan_tmp.as<u32>(), dscal32(3), st);
+    launches += 3;
+    u32 nmiss = read_u32(dscal32(3));
+    if (nmiss == 0) {
+      fold_partials(nt, sd, ab_partials.as<u64>(), grid, T.pst(), st);
+      launches += 1;
+      last_new = 0;
+      return a + span;
+    }
+    miss_list.ensure((size_t)nmiss * 4 + 64);
+    compact_misses(ab_miss_buf.as<u32>(), ab_miss_cnt.as<u32>(), ab_miss_off.as<u32>(), grid, rpc,
+                   miss_list.as<u32>(), st);
+    launches += 1;
+    int cur = sort_rows(kd, row0, miss_list.as<u32>(), nmiss);
+    u32 f = flush_point(cur, nmiss, span);
+    if (f >= span) {
+      fold_partials(nt, sd, ab_partials.as<u64>(), grid, T.pst(), st);
+      launches += 1;
+      collapse_chunk(cur, nmiss, span, sd, row0, nullptr, U, std::min<int64_t>(nmiss, cfg.memory_budget));
+      merge_into_T();
+      refresh_tiny();
+      return a + span;
+    }
+    // a flush inside this chunk: the optimistic partials include hits at or
+    // after f; recompute them for [a, a + f) only
+    if (f > 0) {
+      u32 g2, r2;
+      absorb_geometry(f, num_sms, &g2, &r2);
+      ab_partials.ensure((size_t)g2 * nt * std::max(S, 1) * 8 + 64);
+      ab_miss_buf.ensure((size_t)g2 * r2 * 4 + 64);
+      ab_miss_cnt.ensure((size_t)(g2 + 1) * 4);
+      absorb_tiny(KW, nt, kd, sd, row0, f, tiny, g2, r2, ab_partials.as<u64>(), ab_miss_buf.as<u32>(),
+                  ab_miss_cnt.as<u32>(), st);
+      fold_partials(nt, sd, ab_partials.as<u64>(), g2, T.pst(), st);
+      launches += 2;
+    }
+    collapse_chunk(cur, nmiss, f, sd, row0, nullptr, U, std::min<int64_t>(nmiss, cfg.memory_budget));
+    merge_into_T();
+    spill_T();
+    return a + f;
+  }
+
+  // next chunk length (rows) for the sort path
+  int64_t chunk_len(int64_t remaining, int64_t last_len, bool last_flushed, int64_t last_cycle) {
+    const int64_t M = cfg.memory_budget;
+    int64_t cmax = cfg.chunk_rows_max > 0 ? cfg.chunk_rows_max : ((int64_t)64 << 20);
+    int64_t len;
+    if (T.n > 0 && T.n <= 8 && absorb_supported((int)T.n, S)) {
+      len = std::min<int64_t>(cmax, (int64_t)1 << 28);
+    } else if (last_len == 0) {
+      len = std::max<int64_t>(M + M / 8, 65536);
+    } else if (last_flushed) {
+      len = last_cycle + last_cycle / 8 + 4096;
+    } else if (last_new > 0) {
+      double rate = (double)last_new / (double)last_len;
+      double need = (double)(M - (int64_t)T.n + 1) / rate;
+      len = (int64_t)(need * 1.125) + 4096;
+      len = std::min(len, last_len * 4);
+    } else {
+      len = last_len * 4;
+    }
+    len = std::max<int64_t>(len, 4096);
+    len = std::min(len, cmax);
+    return std::min(len, remaining);
+  }
+
+  // ------------------------------------------------------- host windows --
+  size_t key_elem(int c) const { return dtype_bits(sch.key_dtypes[c]) / 8; }
+  size_t val_elem(int j) const { return dtype_bits(sch.val_dtypes[j]) / 8; }
+
+  void stage_window(Window& w, const void* const* key_cols, const void* const* val_cols, int64_t start,
+                    int64_t end) {
+    w.start = start;
+    w.end = end;
+    size_t rows = (size_t)(end - start);
+    w.keys.resize(sch.n_key_cols);
+    w.vals.resize(sch.n_val_cols);
+    for (int c = 0; c < sch.n_key_cols; ++c) {
+      w.keys[c].ensure(rows * key_elem(c));
+      CK(cudaMemcpyAsync(w.keys[c].p, (const char*)key_cols[c] + start * key_elem(c), rows * key_elem(c),
+                         cudaMemcpyHostToDevice, h2d));
+      led.bytes_h2d += rows * key_elem(c);
+    }
+    for (int j = 0; j < sch.n_val_cols; ++j) {
+      w.vals[j].ensure(rows * val_elem(j));
+      CK(cudaMemcpyAsync(w.vals[j].p, (const char*)val_cols[j] + start * val_elem(j), rows * val_elem(j),
+                         cudaMemcpyHostToDevice, h2d));
+      led.bytes_h2d += rows * val_elem(j);
+    }
+    CK(cudaEventRecord(w.ready, h2d));
+    w.staged = true;
+  }
+
+  // -------------------------------------------------------- wide merge --
+  void wide_merge() {
+    const int k = (int)runs.size();
+    int64_t total = 0;
+    for (auto& r : runs) total += r.rows;
+    CK(cudaStreamWaitEvent(st, spill_done, 0));
+    tn_busy = false;
+    int64_t W = cfg.merge_window_rows > 0 ? cfg.merge_window_rows : ((int64_t)48 << 20);
+    W = std::max<int64_t>(W, (int64_t)k * 64);
+    // ---- plan windows from sampled keys (every F-th row of each run)
+    int64_t F = std::max<int64_t>(1, W / (8 * (int64_t)k));
+    std::vector<std::pair<u64, u64>> samples;   // (hi, lo)
+    std::vector<u64> tmp_lo, tmp_hi;
+    for (auto& r : runs) {
+      int64_t ns = (r.rows + F - 1) / F;
+      if (ns == 0) continue;
+      tmp_lo.resize(ns);
+      tmp_hi.assign(ns, 0);
+      CK(cudaMemcpy2DAsync(tmp_lo.data(), 8, r.lo, F * 8, 8, ns, cudaMemcpyDefault, st));
+      if (KW == 2) CK(cudaMemcpy2DAsync(tmp_hi.data(), 8, r.hi, F * 8, 8, ns, cudaMemcpyDefault, st));
+      sync();
+      for (int64_t i = 0; i < ns; ++i) samples.push_back({tmp_hi[i], tmp_lo[i]});
+    }
+    std::sort(samples.begin(), samples.end());
+    std::vector<std::pair<u64, u64>> bounds;
+    int64_t acc = (int64_t)k * F;
+    for (auto& s : samples) {
+      if (acc + F > W && (bounds.empty() || bounds.back() != s)) {
+        bounds.push_back(s);
+        acc = (int64_t)k * F;
+      }
+      acc += F;
+    }
+    const int nb = (int)bounds.size();
+    const int nwin = nb + 1;
+    // ---- exact slice boundaries: lower_bound of every bound in every run
+    std::vector<u32> lb((size_t)k * std::max(nb, 1));
+    if (nb > 0) {
+      std::vector<RunRef> refs(k);
+      for (int i = 0; i < k; ++i) refs[i] = {runs[i].lo, runs[i].hi, runs[i].rows};
+      runref_dev.ensure(sizeof(RunRef) * k);
+      bounds_lo.ensure(8 * nb);
+      bounds_hi.ensure(8 * nb);
+      bounds_out.ensure(4 * (size_t)k * nb);
+      std::vector<u64> blo(nb), bhi(nb);
+      for (int i = 0; i < nb; ++i) { bhi[i] = bounds[i].first; blo[i] = bounds[i].second; }
+      CK(cudaMemcpyAsync(runref_dev.p, refs.data(), sizeof(RunRef) * k, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(bounds_lo.p, blo.data(), 8 * nb, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(bounds_hi.p, bhi.data(), 8 * nb, cudaMemcpyHostToDevice, st));
+      run_lower_bounds(KW, runref_dev.as<RunRef>(), k, bounds_lo.as<u64>(), bounds_hi.as<u64>(), nb,
+                       bounds_out.as<u32>(), st);
+      launches += 1;
+      CK(cudaMemcpyAsync(lb.data(), bounds_out.p, 4 * (size_t)k * nb, cudaMemcpyDeviceToHost, st));
+      sync();
+    }
+    auto slice = [&](int r, int w, u32& s0, u32& s1) {
+      s0 = (w == 0) ? 0 : lb[(size_t)r * nb + (w - 1)];
+      s1 = (w == nwin - 1) ? runs[r].rows : lb[(size_t)r * nb + w];
+    };
+    int64_t wmax = 0;
+    for (int w = 0; w < nwin; ++w) {
+      int64_t rows = 0;
+      for (int r = 0; r < k; ++r) { u32 s0, s1; slice(r, w, s0, s1); rows += s1 - s0; }
+      wmax = std::max(wmax, rows);
+    }
+    for (int i = 0; i < 2; ++i) {
+      stg_lo[i].ensure(wmax * 8 + 8);
+      if (KW == 2) stg_hi[i].ensure(wmax * 8 + 8);
+      if (S) stg_st[i].ensure(wmax * 8 * S + 8);
+      CK(cudaEventRecord(stg_free[i], st));
+    }
+    result.n = 0;
+    result.reserve(std::max<int64_t>(1, std::min<int64_t>(total, W)), KW, S);
+    auto stage = [&](int w, int slot) -> int64_t {
+      CK(cudaStreamWaitEvent(h2d, stg_free[slot], 0));
+      int64_t off = 0;
+      for (int r = 0; r < k; ++r) {
+        u32 s0, s1;
+        slice(r, w, s0, s1);
+        size_t cnt = s1 - s0;
+        if (!cnt) continue;
+        cudaMemcpyKind kind = runs[r].host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+        CK(cudaMemcpyAsync(stg_lo[slot].as<u64>() + off, runs[r].lo + s0, cnt * 8, cudaMemcpyDefault, h2d));
+        if (KW == 2) CK(cudaMemcpyAsync(stg_hi[slot].as<u64>() + off, runs[r].hi + s0, cnt * 8, cudaMemcpyDefault, h2d));
+        if (S) CK(cudaMemcpyAsync(stg_st[slot].as<u64>() + off * S, runs[r].st + (size_t)s0 * S, cnt * 8 * S, cudaMemcpyDefault, h2d));
+        if (kind == cudaMemcpyHostToDevice) led.bytes_h2d += cnt * 8 * (KW + S);
+        off += cnt;
+      }
+      CK(cudaEventRecord(stg_ready[slot], h2d));
+      return off;
+    };
+    std::vector<int64_t> wrows(nwin);
+    wrows[0] = stage(0, 0);
+    for (int w = 0; w < nwin; ++w) {
+      const int slot = w & 1;
+      if (w + 1 < nwin) wrows[w + 1] = stage(w + 1, slot ^ 1);
+      CK(cudaStreamWaitEvent(st, stg_ready[slot], 0));
+      const u32 m = (u32)wrows[w];
+      led.rows_read_back += m;
+      led.merge_windows++;
+      if (m == 0) { CK(cudaEventRecord(stg_free[slot], st)); continue; }
+      // sort the window's rows by key: keys copied into sort buffers, value = staged row index
+      ensure_sort(m);
+      CK(cudaMemcpyAsync(s_lo[0].p, stg_lo[slot].p, (size_t)m * 8, cudaMemcpyDeviceToDevice, st));
+      if (KW == 2) CK(cudaMemcpyAsync(s_hi[0].p, stg_hi[slot].p, (size_t)m * 8, cudaMemcpyDeviceToDevice, st));
+      iota_u32(s_val[0].as<u32>(), m, st);
+      CK(cudaMemsetAsync(dvary(), 0, 2 * sizeof(u64), st));
+      keys_varying(KW, s_lo[0].as<u64>(), s_hi[0].as<u64>(), m, dvary(), st);
+      launches += 2;
+      int cur = sort_built(m);
+      collapse_chunk(cur, m, 0xFFFFFFFFu, sd0, 0, stg_st[slot].as<u64>(), U, m);
+      CK(cudaEventRecord(stg_free[slot], st));
+      // append U to the result
+      size_t need = (size_t)result.n + U.n;
+      if (need > result.lo.bytes / 8) grow_result(need);
+      CK(cudaMemcpyAsync(result.plo() + result.n, U.plo(), (size_t)U.n * 8, cudaMemcpyDeviceToDevice, st));
+      if (KW == 2) CK(cudaMemcpyAsync(result.phi() + result.n, U.phi(), (size_t)U.n * 8, cudaMemcpyDeviceToDevice, st));
+      if (S) CK(cudaMemcpyAsync(result.pst() + (size_t)result.n * S, U.pst(), (size_t)U.n * 8 * S, cudaMemcpyDeviceToDevice, st));
+      result.n += U.n;
+    }
+    U.n = 0;
+    led.pages_read = led.pages_written;
+    led.merge_steps += 1;
+    led.merge_levels += 1;
+  }
+
+  void grow_result(size_t need) {
+    size_t cap = std::max(need, result.lo.bytes / 8 * 2);
+    Table nt;
+    nt.reserve(cap, KW, S);
+    if (result.n) {
+      CK(cudaMemcpyAsync(nt.plo(), result.plo(), (size_t)result.n * 8, cudaMemcpyDeviceToDevice, st));
+      if (KW == 2) CK(cudaMemcpyAsync(nt.phi(), result.phi(), (size_t)result.n * 8, cudaMemcpyDeviceToDevice, st));
+      if (S) CK(cudaMemcpyAsync(nt.pst(), result.pst(), (size_t)result.n * 8 * S, cudaMemcpyDeviceToDevice, st));
+    }
+    sync();
+    nt.n = result.n;
+    result.release();
+    result = nt;
+    nt.lo.p = nt.hi.p = nt.st.p = nullptr;
+  }
+
+  // ------------------------------------------------------------ execute --
+  int64_t execute(int64_t n, const void* const* key_cols, const void* const* val_cols, bool on_host,
+                  cudaStream_t stream) {
+    CK(cudaSetDevice(dev));
+    st = stream;
+    memset(&led, 0, sizeof(led));
+    cycles.clear();
+    runs.clear();
+    pinned.reset();
+    devpool.reset();
+    T.n = U.n = Tn.n = result.n = 0;
+    tn_busy = false;
+    launches = 0;
+    if (n < 0) throw IsaError(ISA_ERR_INVALID_INPUT, "negative row count");
+    led.rows_seen = n;
+    if (n == 0) return 0;
+    T.reserve(std::min<int64_t>(cfg.memory_budget, n) + 1, KW, S);
+    auto t0 = std::chrono::steady_clock::now();
+
+    int64_t wrows = on_host ? (cfg.window_rows > 0 ? cfg.window_rows : ((int64_t)32 << 20)) : n;
+    int64_t a = 0, cycle_start = 0, last_len = 0, last_cycle = 0;
+    bool last_flushed = false;
+    int wi = 0;
+    if (on_host) stage_window(win[0], key_cols, val_cols, 0, std::min(n, wrows));
+    while (a < n) {
+      const void* kb[ISA_MAX_KEY_COLS];
+      const void* vb[ISA_MAX_VAL_COLS];
+      int64_t base = 0, wend = n;
+      if (on_host) {
+        Window& w = win[wi];
+        if (a >= w.end) {
+          // advance: the next window was prefetched (or stage it now)
+          cudaEvent_t used;
+          CK(cudaEventCreateWithFlags(&used, cudaEventDisableTiming));
+          CK(cudaEventRecord(used, st));
+          wi ^= 1;
+          Window& nw = win[wi];
+          if (!(nw.staged && nw.start == a)) {
+            CK(cudaStreamWaitEvent(h2d, used, 0));
+            stage_window(nw, key_cols, val_cols, a, std::min(n, a + wrows));
+          }
+          cudaEventDestroy(used);
+          continue;
+        }
+        CK(cudaStreamWaitEvent(st, w.ready, 0));
+        // prefetch the following window into the other buffer
+        Window& ow = win[wi ^ 1];
+        if (w.end < n && !(ow.staged && ow.start == w.end)) {
+          cudaEvent_t used;
+          CK(cudaEventCreateWithFlags(&used, cudaEventDisableTiming));
+          CK(cudaEventRecord(used, st));
+          CK(cudaStreamWaitEvent(h2d, used, 0));
+          cudaEventDestroy(used);
+          stage_window(ow, key_cols, val_cols, w.end, std::min(n, w.end + wrows));
+        }
+        base = w.start;
+        wend = w.end;
+        for (int c = 0; c < sch.n_key_cols; ++c) kb[c] = w.keys[c].p;
+        for (int j = 0; j < sch.n_val_cols; ++j) vb[j] = w.vals[j].p;
+      } else {
+        for (int c = 0; c < sch.n_key_cols; ++c) kb[c] = key_cols[c];
+        for (int j = 0; j < sch.n_val_cols; ++j) vb[j] = val_cols[j];
+      }
+      KeyDesc kd = kd_at(kb);
+      SlotDesc sd = sd_at(vb);
+      int64_t len = chunk_len(std::min(n, wend) - a, last_len, last_flushed, last_cycle);
+      int64_t b = a + len;
+      int64_t nxt = process_chunk(kd, sd, base, a, b);
+      last_flushed = nxt < b;
+      if (last_flushed) {
+        last_cycle = nxt - cycle_start;
+        cycles.push_back(last_cycle);
+        cycle_start = nxt;
+      }
+      last_len = nxt - a;
+      if (last_len == 0) last_len = 1;
+      a = nxt;
+    }
+    // residue becomes the last run if anything spilled (sortagg.py:353-374)
+    if (!runs.empty()) spill_T();
+    led.runs_after_generation = (int64_t)runs.size();
+    sync();
+    auto t1 = std::chrono::steady_clock::now();
+    led.ms_run_generation = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    if (runs.empty()) {
+      std::swap(result, T);
+      T.n = 0;
+    } else {
+      wide_merge();
+      sync();
+      led.ms_wide_merge = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
+    }
+    led.n_groups = result.n;
+    led.kernel_launches = launches;
+    CK(cudaGetLastError());
+    return result.n;
+  }
+
+  void result_copy(void* const* key_out, void* const* slot_out, bool out_on_host, cudaStream_t stream) {
+    CK(cudaSetDevice(dev));
+    st = stream;
+    const u32 n = result.n;
+    if (n == 0) return;
+    for (int c = 0; c < kd0.ncols; ++c) {
+      void* dst = key_out[c];
+      size_t eb = (size_t)n * key_elem(c);
+      if (!dst) continue;
+      if (out_on_host) { out_tmp.ensure(eb); dst = out_tmp.p; }
+      export_key_col(result.plo(), KW == 2 ? result.phi() : nullptr, n, kd0.dtype[c], kd0.shift[c], kd0.width[c],
+                     dst, st);
+      if (out_on_host) {
+        CK(cudaMemcpyAsync(key_out[c], out_tmp.p, eb, cudaMemcpyDeviceToHost, st));
+        sync();
+      }
+    }
+    for (int s = 0; s < S; ++s) {
+      void* dst = slot_out[s];
+      size_t eb = (size_t)n * 8;
+      if (!dst) continue;
+      if (out_on_host) { out_tmp.ensure(eb); dst = out_tmp.p; }
+      export_slot(result.pst(), S, s, n, (u64*)dst, st);
+      if (out_on_host) {
+        CK(cudaMemcpyAsync(slot_out[s], out_tmp.p, eb, cudaMemcpyDeviceToHost, st));
+        sync();
+      }
+    }
+    sync();
+  }
+
+  // --------------------------------------------------------- partition --
+  void partition(int64_t n, const void* const* key_cols, const void* const* val_cols, const u64* sp_lo,
+                 const u64* sp_hi, int ns, void* const* key_out, void* const* val_out, int64_t* counts,
+                 cudaStream_t stream) {
+    CK(cudaSetDevice(dev));
+    st = stream;
+    if (ns < 0 || ns > 255) throw IsaError(ISA_ERR_INVALID_INPUT, "at most 255 splitters");
+    if (n > 0x7FFFFFFFll) throw IsaError(ISA_ERR_INVALID_INPUT, "partition of more than 2^31 rows per call");
+    const u32 m = (u32)n;
+    if (m == 0) { for (int d = 0; d <= ns; ++d) counts[d] = 0; return; }
+    ensure_sort(m);
+    KeyDesc kd = kd_at(key_cols);
+    partition_dest(KW, kd, m, sp_lo, sp_hi, ns, s_lo_buf(0), s_val[0].as<u32>(), st);
+    SortBufs b;
+    for (int i = 0; i < 2; ++i) { b.lo[i] = s_lo[i].as<u64>(); b.hi[i] = nullptr; b.val[i] = s_val[i].as<u32>(); }
+    b.tile_hist = tile_hist.as<u32>();
+    b.scan_tmp = scan_tmp.as<u32>();
+    int cur = radix_sort_pairs(1, b, m, 0, 8, st, &launches);
+    const u32* perm = s_val[cur].as<u32>();
+    for (int c = 0; c < sch.n_key_cols; ++c) gather_column(key_cols[c], (int)key_elem(c), perm, m, key_out[c], st);
+    for (int j = 0; j < sch.n_val_cols; ++j) gather_column(val_cols[j], (int)val_elem(j), perm, m, val_out[j], st);
+    word_tmp.ensure(4 * 256);
+    count_dest(s_lo[cur].as<u64>(), m, ns + 1, word_tmp.as<u32>(), st);
+    std::vector<u32> ub(ns + 1);
+    CK(cudaMemcpyAsync(ub.data(), word_tmp.p, 4 * (ns + 1), cudaMemcpyDeviceToHost, st));
+    sync();
+    u32 prev = 0;
+    for (int d = 0; d <= ns; ++d) { counts[d] = ub[d] - prev; prev = ub[d]; }
+  }
+  u64* s_lo_buf(int i) { return s_lo[i].as<u64>(); }
+};
+
+int fail(isa_handle* h, const std::exception& e);
+
+}  // namespace
+
+struct isa_handle {
+  Engine* eng;
+};
+
+namespace {
+int fail(isa_handle* h, const std::exception& e) {
+  const IsaError* ie = dynamic_cast<const IsaError*>(&e);
+  int code = ie ? ie->code : ISA_ERR_RESOURCE;
+  if (h && h->eng) h->eng->err = e.what();
+  else g_create_error = e.what();
+  return code;
+}
+}  // namespace
+
+extern "C" {
+
+const char* isa_version(void) { return "insortagg_b200 0.1.0 (sm_100a)"; }
+
+isa_handle* isa_create(const isa_config* config, const isa_schema* schema) {
+  if (!config || !schema) {
+    g_create_error = "null config or schema";
+    return nullptr;
+  }
+  try {
+    isa_handle* h = new isa_handle;
+    h->eng = new Engine(*config, *schema);
+    g_create_error.clear();
+    return h;
+  } catch (const std::exception& e) {
+    fail(nullptr, e);
+    return nullptr;
+  }
+}
+
+void isa_destroy(isa_handle* h) {
+  if (!h) return;
+  delete h->eng;
+  delete h;
+}
+
+int isa_execute(isa_handle* h, int64_t n_rows, const void* const* key_cols, const void* const* val_cols,
+                int32_t input_on_host, void* stream, int64_t* n_groups_out) {
+  if (!h) return ISA_ERR_CONTRACT;
+  try {
+    int64_t g = h->eng->execute(n_rows, key_cols, val_cols, input_on_host != 0, (cudaStream_t)stream);
+    if (n_groups_out) *n_groups_out = g;
+    return ISA_OK;
+  } catch (const std::exception& e) {
+    return fail(h, e);
+  }
+}
+
+int isa_result_copy(isa_handle* h, void* const* key_out, void* const* slot_out, int32_t out_on_host, void* stream) {
+  if (!h) return ISA_ERR_CONTRACT;
+  try {
+    h->eng->result_copy(key_out, slot_out, out_on_host != 0, (cudaStream_t)stream);
+    return ISA_OK;
+  } catch (const std::exception& e) {
+    return fail(h, e);
+  }
+}
+
+int isa_metrics(isa_handle* h, isa_ledger* out) {
+  if (!h || !out) return ISA_ERR_CONTRACT;
+  *out = h->eng->led;
+  return ISA_OK;
+}
+
+int64_t isa_cycles(isa_handle* h, int64_t* out, int64_t cap) {
+  if (!h) return -1;
+  auto& c = h->eng->cycles;
+  for (int64_t i = 0; i < (int64_t)c.size() && i < cap; ++i) out[i] = c[i];
+  return (int64_t)c.size();
+}
+
+int64_t isa_run_rows(isa_handle* h, int64_t* out, int64_t cap) {
+  if (!h) return -1;
+  auto& r = h->eng->runs;
+  for (int64_t i = 0; i < (int64_t)r.size() && i < cap; ++i) out[i] = r[i].rows;
+  return (int64_t)r.size();
+}
+
+const char* isa_last_error(isa_handle* h) {
+  if (!h) return g_create_error.c_str();
+  return h->eng->err.c_str();
+}
+
+int isa_sample_keys(isa_handle* h, int64_t n_rows, const void* const* key_cols, int64_t stride, uint64_t* out_lo,
+                    uint64_t* out_hi, void* stream) {
+  if (!h) return ISA_ERR_CONTRACT;
+  try {
+    if (stride < 1) throw IsaError(ISA_ERR_INVALID_INPUT, "stride must be positive");
+    CK(cudaSetDevice(h->eng->dev));
+    KeyDesc kd = h->eng->kd_at(key_cols);
+    isa::sample_keys(kd, n_rows, stride, out_lo, out_hi, (cudaStream_t)stream);
+    CK(cudaGetLastError());
+    return ISA_OK;
+  } catch (const std::exception& e) {
+    return fail(h, e);
+  }
+}
+
+int isa_partition(isa_handle* h, int64_t n_rows, const void* const* key_cols, const void* const* val_cols,
+                  const uint64_t* split_lo, const uint64_t* split_hi, int32_t n_splitters, void* const* key_out,
+                  void* const* val_out, int64_t* counts_out, void* stream) {
+  if (!h) return ISA_ERR_CONTRACT;
+  try {
+    h->eng->partition(n_rows, key_cols, val_cols, split_lo, split_hi, n_splitters, key_out, val_out, counts_out,
+                      (cudaStream_t)stream);
+    return ISA_OK;
+  } catch (const std::exception& e) {
+    return fail(h, e);
+  }
+}
+
+}  // extern "C"

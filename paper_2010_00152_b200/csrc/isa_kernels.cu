@@ -1,0 +1,765 @@
+// sm_100a kernels of the B200 sort-based aggregation operator.
+//
+// Every kernel here is HBM-bound integer/byte work (sort, scan, segmented
+// reduce, merge): no tensor cores.  Design rules followed: coalesced global
+// access, shared-memory staging of tiles, warp-synchronous ranking with
+// match.any, grids sized from the SM count for streaming kernels.
+#include "isa_kernels.h"
+#include <cstdio>
+#include <algorithm>
+
+namespace isa {
+
+// ============================================================== scan ====
+#define SC_THREADS 256
+#define SC_ITEMS 16
+#define SC_TILE (SC_THREADS * SC_ITEMS)
+
+__global__ void __launch_bounds__(SC_THREADS) k_scan_reduce(const u32* __restrict__ d, u32 n, u32* __restrict__ bsum) {
+  __shared__ u32 sw[8];
+  u32 base = blockIdx.x * SC_TILE;
+  u32 s = 0;
+#pragma unroll
+  for (int i = 0; i < SC_ITEMS; ++i) {
+    u32 idx = base + i * SC_THREADS + threadIdx.x;
+    if (idx < n) s += d[idx];
+  }
+  u32 tot;
+  block_excl_scan256(s, sw, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(SC_THREADS) k_scan_single(u32* __restrict__ bsum, u32 nb, u32* __restrict__ total) {
+  __shared__ u32 sw[8];
+  u32 carry = 0;
+  for (u32 base = 0; base < nb; base += SC_TILE) {
+    u32 v[SC_ITEMS];
+    u32 s = 0;
+#pragma unroll
+    for (int i = 0; i < SC_ITEMS; ++i) {
+      u32 idx = base + threadIdx.x * SC_ITEMS + i;
+      v[i] = idx < nb ? bsum[idx] : 0;
+      s += v[i];
+    }
+    u32 tot;
+    u32 pre = block_excl_scan256(s, sw, &tot) + carry;
+#pragma unroll
+    for (int i = 0; i < SC_ITEMS; ++i) {
+      u32 idx = base + threadIdx.x * SC_ITEMS + i;
+      if (idx < nb) bsum[idx] = pre;
+      pre += v[i];
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    bsum[nb] = carry;
+    if (total) *total = carry;
+  }
+}
+
+__global__ void __launch_bounds__(SC_THREADS) k_scan_apply(u32* __restrict__ d, u32 n, const u32* __restrict__ bsum) {
+  __shared__ u32 sw[8];
+  __shared__ u32 tile[SC_TILE];
+  u32 base = blockIdx.x * SC_TILE;
+#pragma unroll
+  for (int i = 0; i < SC_ITEMS; ++i) {
+    u32 idx = base + i * SC_THREADS + threadIdx.x;
+    tile[i * SC_THREADS + threadIdx.x] = idx < n ? d[idx] : 0;
+  }
+  __syncthreads();
+  u32 v[SC_ITEMS];
+  u32 s = 0;
+#pragma unroll
+  for (int i = 0; i < SC_ITEMS; ++i) { v[i] = tile[threadIdx.x * SC_ITEMS + i]; s += v[i]; }
+  u32 tot;
+  u32 pre = block_excl_scan256(s, sw, &tot) + bsum[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < SC_ITEMS; ++i) { tile[threadIdx.x * SC_ITEMS + i] = pre; pre += v[i]; }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < SC_ITEMS; ++i) {
+    u32 idx = base + i * SC_THREADS + threadIdx.x;
+    if (idx < n) d[idx] = tile[i * SC_THREADS + threadIdx.x];
+  }
+}
+
+size_t scan_tmp_words(u32 n) { return (size_t)(n + SC_TILE - 1) / SC_TILE + 2; }
+
+void scan_exclusive_u32(u32* data, u32 n, u32* tmp, u32* total, cudaStream_t st) {
+  u32 nb = (n + SC_TILE - 1) / SC_TILE;
+  if (n == 0) {
+    if (total) cudaMemsetAsync(total, 0, sizeof(u32), st);
+    return;
+  }
+  k_scan_reduce<<<nb, SC_THREADS, 0, st>>>(data, n, tmp);
+  k_scan_single<<<1, SC_THREADS, 0, st>>>(tmp, nb, total);
+  k_scan_apply<<<nb, SC_THREADS, 0, st>>>(data, n, tmp);
+}
+
+// ======================================================== radix sort ====
+#define RS_THREADS 256
+#define RS_ITEMS 16
+#define RS_TILE (RS_THREADS * RS_ITEMS)
+#define RS_WARPS (RS_THREADS / 32)
+#define RS_WARP_ITEMS (RS_TILE / RS_WARPS)
+
+__device__ __forceinline__ u32 digit_of(u64 hi, u64 lo, int shift) {
+  u64 v;
+  if (shift >= 64) v = hi >> (shift - 64);
+  else if (shift > 56) v = (lo >> shift) | (hi << (64 - shift));
+  else v = lo >> shift;
+  return (u32)(v & 0xFFu);
+}
+
+template <int KW>
+__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const u64* __restrict__ klo, const u64* __restrict__ khi,
+                                                      u32 n, int shift, u32* __restrict__ tile_hist, u32 ntiles) {
+  __shared__ u32 h[RS_WARPS * 256];
+  for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) h[i] = 0;
+  __syncthreads();
+  const u32 tile = blockIdx.x, base = tile * RS_TILE;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll 4
+  for (int it = 0; it < RS_ITEMS; ++it) {
+    u32 i = base + it * RS_THREADS + threadIdx.x;
+    bool valid = i < n;
+    u32 d = 256 + lane;
+    if (valid) d = digit_of(KW == 2 ? khi[i] : 0, klo[i], shift);
+    u32 peers = __match_any_sync(0xffffffffu, d);
+    if (valid && lane == __ffs(peers) - 1) atomicAdd(&h[w * 256 + d], (u32)__popc(peers));
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < 256; d += RS_THREADS) {
+    u32 s = 0;
+#pragma unroll
+    for (int ww = 0; ww < RS_WARPS; ++ww) s += h[ww * 256 + d];
+    tile_hist[(size_t)d * ntiles + tile] = s;
+  }
+}
+
+template <int KW>
+__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const u64* __restrict__ lo_in, const u64* __restrict__ hi_in,
+                                                         const u32* __restrict__ v_in, u64* __restrict__ lo_out,
+                                                         u64* __restrict__ hi_out, u32* __restrict__ v_out, u32 n,
+                                                         int shift, const u32* __restrict__ tile_off, u32 ntiles) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  u32* wcnt = (u32*)smem;               // [RS_WARPS][256]
+  u32* dstart = wcnt + RS_WARPS * 256;  // [256]
+  u32* gbase = dstart + 256;            // [256]
+  u32* sw = gbase + 256;                // [8]
+  u64* s_lo = (u64*)(sw + 8);           // [RS_TILE]
+  u64* s_hi = s_lo + RS_TILE;           // [RS_TILE] (KW == 2)
+  u32* s_v = (u32*)(s_lo + KW * RS_TILE);
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const u32 tile = blockIdx.x, base = tile * RS_TILE;
+  const u32 tile_n = min((u32)RS_TILE, n - base);
+  for (int i = tid; i < RS_WARPS * 256; i += RS_THREADS) wcnt[i] = 0;
+  __syncthreads();
+
+  u64 lo[RS_ITEMS], hi[RS_ITEMS];
+  u32 v[RS_ITEMS], off[RS_ITEMS], dg[RS_ITEMS];
+  const u32 lt = lanemask_lt();
+#pragma unroll
+  for (int it = 0; it < RS_ITEMS; ++it) {
+    u32 li = w * RS_WARP_ITEMS + it * 32 + lane;
+    bool valid = li < tile_n;
+    u32 gi = base + li;
+    lo[it] = valid ? lo_in[gi] : 0;
+    hi[it] = (KW == 2 && valid) ? hi_in[gi] : 0;
+    v[it] = valid ? v_in[gi] : 0;
+  }
+#pragma unroll
+  for (int it = 0; it < RS_ITEMS; ++it) {
+    u32 li = w * RS_WARP_ITEMS + it * 32 + lane;
+    bool valid = li < tile_n;
+    u32 d = valid ? digit_of(hi[it], lo[it], shift) : 256 + lane;
+    u32 peers = __match_any_sync(0xffffffffu, d);
+    int leader = __ffs(peers) - 1;
+    u32 cnt = 0;
+    if (valid && lane == leader) {
+      cnt = wcnt[w * 256 + d];
+      wcnt[w * 256 + d] = cnt + __popc(peers);
+    }
+    cnt = __shfl_sync(0xffffffffu, cnt, leader);
+    off[it] = cnt + __popc(peers & lt);
+    dg[it] = d;
+    __syncwarp();
+  }
+  __syncthreads();
+  {
+    // per-digit exclusive prefix over warps, then over digits
+    const int d = tid;  // RS_THREADS == 256
+    u32 run = 0;
+#pragma unroll
+    for (int ww = 0; ww < RS_WARPS; ++ww) {
+      u32 c = wcnt[ww * 256 + d];
+      wcnt[ww * 256 + d] = run;
+      run += c;
+    }
+    u32 tot;
+    u32 ds = block_excl_scan256(run, sw, &tot);
+    dstart[d] = ds;
+    gbase[d] = tile_off[(size_t)d * ntiles + tile] - ds;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < RS_ITEMS; ++it) {
+    u32 li = w * RS_WARP_ITEMS + it * 32 + lane;
+    if (li < tile_n) {
+      u32 d = dg[it];
+      u32 p = dstart[d] + wcnt[w * 256 + d] + off[it];
+      s_lo[p] = lo[it];
+      if (KW == 2) s_hi[p] = hi[it];
+      s_v[p] = v[it];
+    }
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (int it = 0; it < RS_ITEMS; ++it) {
+    u32 p = it * RS_THREADS + tid;
+    if (p < tile_n) {
+      u64 l = s_lo[p];
+      u64 h = KW == 2 ? s_hi[p] : 0;
+      u32 d = digit_of(h, l, shift);
+      u32 dst = gbase[d] + p;
+      lo_out[dst] = l;
+      if (KW == 2) hi_out[dst] = h;
+      v_out[dst] = s_v[p];
+    }
+  }
+}
+
+static size_t rs_scatter_smem(int KW) {
+  return (RS_WARPS * 256 + 256 + 256 + 8) * sizeof(u32) + (size_t)RS_TILE * (8 * KW + 4);
+}
+
+size_t sort_hist_words(u32 n) { return (size_t)256 * ((n + RS_TILE - 1) / RS_TILE); }
+
+int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStream_t st, int64_t* launches) {
+  int cur = 0;
+  if (n <= 1 || bit_hi <= bit_lo) return cur;
+  static bool attr_set[3] = {false, false, false};
+  if (!attr_set[KW]) {
+    if (KW == 2)
+      cudaFuncSetAttribute(k_rs_scatter<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_scatter_smem(2));
+    else
+      cudaFuncSetAttribute(k_rs_scatter<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_scatter_smem(1));
+    attr_set[KW] = true;
+  }
+  const u32 ntiles = (n + RS_TILE - 1) / RS_TILE;
+  const size_t smem = rs_scatter_smem(KW);
+  for (int shift = bit_lo; shift < bit_hi; shift += 8) {
+    int nxt = cur ^ 1;
+    if (KW == 2) {
+      k_rs_hist<2><<<ntiles, RS_THREADS, 0, st>>>(b.lo[cur], b.hi[cur], n, shift, b.tile_hist, ntiles);
+      scan_exclusive_u32(b.tile_hist, 256 * ntiles, b.scan_tmp, nullptr, st);
+      k_rs_scatter<2><<<ntiles, RS_THREADS, smem, st>>>(b.lo[cur], b.hi[cur], b.val[cur], b.lo[nxt], b.hi[nxt],
+                                                         b.val[nxt], n, shift, b.tile_hist, ntiles);
+    } else {
+      k_rs_hist<1><<<ntiles, RS_THREADS, 0, st>>>(b.lo[cur], nullptr, n, shift, b.tile_hist, ntiles);
+      scan_exclusive_u32(b.tile_hist, 256 * ntiles, b.scan_tmp, nullptr, st);
+      k_rs_scatter<1><<<ntiles, RS_THREADS, smem, st>>>(b.lo[cur], nullptr, b.val[cur], b.lo[nxt], nullptr,
+                                                         b.val[nxt], n, shift, b.tile_hist, ntiles);
+    }
+    if (launches) *launches += 5;
+    cur = nxt;
+  }
+  return cur;
+}
+
+// ======================================================= key building ====
+template <int KW>
+__global__ void k_build_keys(KeyDesc kd, i64 row0, const u32* __restrict__ pos, u32 n, u64* __restrict__ lo,
+                             u64* __restrict__ hi, u32* __restrict__ val, u64* __restrict__ varying) {
+  u64 r_hi, r_lo;
+  load_key(kd, row0 + (pos ? pos[0] : 0), r_hi, r_lo);
+  u64 acc_lo = 0, acc_hi = 0;
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    u32 r = pos ? pos[i] : i;
+    u64 h, l;
+    load_key(kd, row0 + r, h, l);
+    lo[i] = l;
+    if (KW == 2) hi[i] = h;
+    val[i] = r;
+    acc_lo |= l ^ r_lo;
+    acc_hi |= h ^ r_hi;
+  }
+  // warp OR-reduce, one atomic per warp
+  for (int o = 16; o; o >>= 1) {
+    acc_lo |= __shfl_xor_sync(0xffffffffu, acc_lo, o);
+    acc_hi |= __shfl_xor_sync(0xffffffffu, acc_hi, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (acc_lo) atomicOr((unsigned long long*)&varying[0], (unsigned long long)acc_lo);
+    if (acc_hi) atomicOr((unsigned long long*)&varying[1], (unsigned long long)acc_hi);
+  }
+}
+
+static int grid_for(u64 n, int threads, int cap = 148 * 16) {
+  u64 g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > (u64)cap) g = cap;
+  return (int)g;
+}
+
+void build_keys(int KW, const KeyDesc& kd, int64_t row0, const u32* pos, u32 n, u64* lo, u64* hi, u32* val,
+                u64* varying, cudaStream_t st) {
+  if (n == 0) return;
+  int g = grid_for(n, 256);
+  if (KW == 2) k_build_keys<2><<<g, 256, 0, st>>>(kd, row0, pos, n, lo, hi, val, varying);
+  else k_build_keys<1><<<g, 256, 0, st>>>(kd, row0, pos, n, lo, hi, val, varying);
+}
+
+template <int KW>
+__global__ void k_keys_varying(const u64* __restrict__ lo, const u64* __restrict__ hi, u32 n, u64* varying) {
+  u64 r_lo = lo[0], r_hi = KW == 2 ? hi[0] : 0;
+  u64 acc_lo = 0, acc_hi = 0;
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    acc_lo |= lo[i] ^ r_lo;
+    if (KW == 2) acc_hi |= hi[i] ^ r_hi;
+  }
+  for (int o = 16; o; o >>= 1) {
+    acc_lo |= __shfl_xor_sync(0xffffffffu, acc_lo, o);
+    acc_hi |= __shfl_xor_sync(0xffffffffu, acc_hi, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (acc_lo) atomicOr((unsigned long long*)&varying[0], (unsigned long long)acc_lo);
+    if (acc_hi) atomicOr((unsigned long long*)&varying[1], (unsigned long long)acc_hi);
+  }
+}
+
+void keys_varying(int KW, const u64* lo, const u64* hi, u32 n, u64* varying, cudaStream_t st) {
+  if (n == 0) return;
+  int g = grid_for(n, 256);
+  if (KW == 2) k_keys_varying<2><<<g, 256, 0, st>>>(lo, hi, n, varying);
+  else k_keys_varying<1><<<g, 256, 0, st>>>(lo, hi, n, varying);
+}
+
+__global__ void k_iota(u32* v, u32 n) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = i;
+}
+void iota_u32(u32* v, u32 n, cudaStream_t st) {
+  if (n) k_iota<<<grid_for(n, 256), 256, 0, st>>>(v, n);
+}
+
+// ==================================================== flush analysis ====
+template <int KW>
+__global__ void k_new_heads(const u64* __restrict__ lo, const u64* __restrict__ hi, const u32* __restrict__ val,
+                            u32 m, const u64* __restrict__ T_lo, const u64* __restrict__ T_hi, u32 t,
+                            u32* __restrict__ bitmap, u32* __restrict__ n_new) {
+  u32 cnt = 0;
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    u64 l = lo[i], h = KW == 2 ? hi[i] : 0;
+    bool head = (i == 0) || !key_eq<KW>(h, l, KW == 2 ? hi[i - 1] : 0, lo[i - 1]);
+    if (!head) continue;
+    bool in_t = false;
+    if (t) {
+      u32 p = lower_bound_key<KW>(T_lo, T_hi, t, h, l);
+      in_t = p < t && key_eq<KW>(KW == 2 ? T_hi[p] : 0, T_lo[p], h, l);
+    }
+    if (!in_t) {
+      u32 pos = val[i];
+      atomicOr(&bitmap[pos >> 5], 1u << (pos & 31));
+      ++cnt;
+    }
+  }
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(n_new, cnt);
+}
+
+void new_heads(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, const u64* T_lo, const u64* T_hi,
+               u32 t, u32* bitmap, u32* n_new, cudaStream_t st) {
+  if (m == 0) return;
+  int g = grid_for(m, 256);
+  if (KW == 2) k_new_heads<2><<<g, 256, 0, st>>>(lo, hi, val, m, T_lo, T_hi, t, bitmap, n_new);
+  else k_new_heads<1><<<g, 256, 0, st>>>(lo, hi, val, m, T_lo, T_hi, t, bitmap, n_new);
+}
+
+__global__ void k_popc_words(const u32* __restrict__ bm, u32 nw, u32* __restrict__ cnt) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x) cnt[i] = __popc(bm[i]);
+}
+__global__ void k_find_kth(const u32* __restrict__ bm, const u32* __restrict__ pre, u32 nw, u32 k,
+                           u32* __restrict__ out) {
+  for (u32 w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) {
+    u32 word = bm[w];
+    u32 p = pre[w], c = __popc(word);
+    if (p < k && p + c >= k) {
+      u32 need = k - p;  // 1-based within word
+      for (int b = 0; b < 32; ++b) {
+        if (word & (1u << b)) {
+          if (--need == 0) { *out = w * 32 + b; break; }
+        }
+      }
+    }
+  }
+}
+
+void select_kth_bit(const u32* bitmap, u32 nbits, u32 k, u32* word_tmp, u32* scan_tmp, u32* out, cudaStream_t st) {
+  u32 nw = (nbits + 31) / 32;
+  int g = grid_for(nw, 256);
+  k_popc_words<<<g, 256, 0, st>>>(bitmap, nw, word_tmp);
+  scan_exclusive_u32(word_tmp, nw, scan_tmp, nullptr, st);
+  k_find_kth<<<g, 256, 0, st>>>(bitmap, word_tmp, nw, k, out);
+}
+
+// ========================================================== collapse ====
+#define CL_ITEMS 8
+
+template <int KW>
+__global__ void k_head_flags(const u64* __restrict__ lo, const u64* __restrict__ hi, const u32* __restrict__ val,
+                             u32 m, u32 limit, u32* __restrict__ flags) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    bool inc = val[i] < limit;
+    bool head = inc && ((i == 0) || !key_eq<KW>(KW == 2 ? hi[i] : 0, lo[i], KW == 2 ? hi[i - 1] : 0, lo[i - 1]));
+    flags[i] = head ? 1u : 0u;
+  }
+}
+
+__device__ __forceinline__ void load_state_row(const SlotDesc& sd, i64 row0, const u64* __restrict__ st_in, u32 v,
+                                               u64* s) {
+  const int S = sd.nslots;
+  if (st_in) {
+    const u64* p = st_in + (size_t)v * S;
+    for (int k = 0; k < S; ++k) s[k] = p[k];
+  } else {
+    for (int k = 0; k < S; ++k) s[k] = load_slot_value(sd.src[k], sd.type[k], sd.dtype[k], sd.ptr[k], row0 + v);
+  }
+}
+
+template <int KW>
+__global__ void k_seg_reduce(const u64* __restrict__ lo, const u64* __restrict__ hi, const u32* __restrict__ val,
+                             u32 m, u32 limit, SlotDesc sd, i64 row0, const u64* __restrict__ st_in,
+                             const u32* __restrict__ hpos, u64* __restrict__ out_lo, u64* __restrict__ out_hi,
+                             u64* __restrict__ out_st, u64* __restrict__ partial, u32* __restrict__ partial_slot) {
+  const int S = sd.nslots;
+  const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+  const u32 i0 = t * CL_ITEMS;
+  if (i0 >= m) return;
+  const u32 i1 = min(i0 + CL_ITEMS, m);
+  u64 acc[ISA_MAX_SLOTS];
+  u64 cur[ISA_MAX_SLOTS];
+  bool have = false, lead = true;
+  u32 slot = 0;
+  u64 prev_lo = 0, prev_hi = 0;
+  if (i0 > 0) { prev_lo = lo[i0 - 1]; prev_hi = KW == 2 ? hi[i0 - 1] : 0; }
+  partial_slot[t] = 0xFFFFFFFFu;
+  for (u32 i = i0; i < i1; ++i) {
+    u64 l = lo[i], h = KW == 2 ? hi[i] : 0;
+    u32 v = val[i];
+    bool head = (i == 0) || !key_eq<KW>(h, l, prev_hi, prev_lo);
+    prev_lo = l; prev_hi = h;
+    if (v >= limit) continue;
+    if (S) load_state_row(sd, row0, st_in, v, cur);
+    if (head) {
+      if (have) {
+        if (lead) {
+          for (int k = 0; k < S; ++k) partial[(size_t)t * S + k] = acc[k];
+          partial_slot[t] = hpos[i0] - 1;
+        } else {
+          for (int k = 0; k < S; ++k) out_st[(size_t)slot * S + k] = acc[k];
+        }
+      }
+      have = true; lead = false;
+      slot = hpos[i];
+      out_lo[slot] = l;
+      if (KW == 2) out_hi[slot] = h;
+      for (int k = 0; k < S; ++k) acc[k] = cur[k];
+    } else if (!have) {
+      have = true;
+      for (int k = 0; k < S; ++k) acc[k] = cur[k];
+    } else {
+      for (int k = 0; k < S; ++k) acc[k] = combine_slot(sd.op[k], sd.type[k], acc[k], cur[k]);
+    }
+  }
+  if (have) {
+    if (lead) {
+      for (int k = 0; k < S; ++k) partial[(size_t)t * S + k] = acc[k];
+      partial_slot[t] = hpos[i0] - 1;
+    } else {
+      for (int k = 0; k < S; ++k) out_st[(size_t)slot * S + k] = acc[k];
+    }
+  }
+}
+
+__global__ void k_seg_fixup(u32 nthreads, SlotDesc sd, const u64* __restrict__ partial,
+                            const u32* __restrict__ partial_slot, u64* __restrict__ out_st) {
+  const int S = sd.nslots;
+  for (u32 t = blockIdx.x * blockDim.x + threadIdx.x; t < nthreads; t += gridDim.x * blockDim.x) {
+    u32 slot = partial_slot[t];
+    if (slot == 0xFFFFFFFFu) continue;
+    for (int k = 0; k < S; ++k)
+      atomic_combine(out_st + (size_t)slot * S + k, sd.op[k], sd.type[k], partial[(size_t)t * S + k]);
+  }
+}
+
+void collapse(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, u32 limit, const SlotDesc& sd,
+              int64_t row0, const u64* st_in, u64* out_lo, u64* out_hi, u64* out_st, CollapseTmp& tmp,
+              cudaStream_t st) {
+  if (m == 0) {
+    cudaMemsetAsync(tmp.total, 0, sizeof(u32), st);
+    return;
+  }
+  int g = grid_for(m, 256);
+  if (KW == 2) k_head_flags<2><<<g, 256, 0, st>>>(lo, hi, val, m, limit, tmp.flags);
+  else k_head_flags<1><<<g, 256, 0, st>>>(lo, hi, val, m, limit, tmp.flags);
+  scan_exclusive_u32(tmp.flags, m, tmp.scan_tmp, tmp.total, st);
+  u32 nthreads = (m + CL_ITEMS - 1) / CL_ITEMS;
+  int blocks = (nthreads + 127) / 128;
+  if (KW == 2)
+    k_seg_reduce<2><<<blocks, 128, 0, st>>>(lo, hi, val, m, limit, sd, row0, st_in, tmp.flags, out_lo, out_hi,
+                                             out_st, tmp.partial, tmp.partial_slot);
+  else
+    k_seg_reduce<1><<<blocks, 128, 0, st>>>(lo, hi, val, m, limit, sd, row0, st_in, tmp.flags, out_lo, out_hi,
+                                             out_st, tmp.partial, tmp.partial_slot);
+  if (sd.nslots) k_seg_fixup<<<grid_for(nthreads, 256), 256, 0, st>>>(nthreads, sd, tmp.partial, tmp.partial_slot, out_st);
+}
+
+// ============================================================= merge ====
+template <int KW>
+__global__ void k_rank(const u64* __restrict__ x_lo, const u64* __restrict__ x_hi, u32 nx,
+                       const u64* __restrict__ y_lo, const u64* __restrict__ y_hi, u32 ny, u32* __restrict__ rank,
+                       u32* __restrict__ match) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < nx; i += gridDim.x * blockDim.x) {
+    u64 l = x_lo[i], h = KW == 2 ? x_hi[i] : 0;
+    u32 p = lower_bound_key<KW>(y_lo, y_hi, ny, h, l);
+    rank[i] = p;
+    match[i] = (p < ny && key_eq<KW>(KW == 2 ? y_hi[p] : 0, y_lo[p], h, l)) ? 1u : 0u;
+  }
+}
+
+struct OpsArr { int op[ISA_MAX_SLOTS]; int type[ISA_MAX_SLOTS]; };
+
+template <int KW>
+__global__ void k_merge_write_a(const u64* __restrict__ a_lo, const u64* __restrict__ a_hi,
+                                const u64* __restrict__ a_st, u32 na, const u64* __restrict__ b_st,
+                                const u32* __restrict__ rank, const u32* __restrict__ mpre,
+                                const u32* __restrict__ match, int S, OpsArr ops, u64* __restrict__ c_lo,
+                                u64* __restrict__ c_hi, u64* __restrict__ c_st) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
+    u32 j = rank[i];
+    u32 o = i + j - mpre[i];
+    c_lo[o] = a_lo[i];
+    if (KW == 2) c_hi[o] = a_hi[i];
+    bool mt = match[i] != 0;
+    for (int k = 0; k < S; ++k) {
+      u64 s = a_st[(size_t)i * S + k];
+      if (mt) s = combine_slot(ops.op[k], ops.type[k], s, b_st[(size_t)j * S + k]);
+      c_st[(size_t)o * S + k] = s;
+    }
+  }
+}
+
+template <int KW>
+__global__ void k_merge_write_b(const u64* __restrict__ b_lo, const u64* __restrict__ b_hi,
+                                const u64* __restrict__ b_st, u32 nb, const u32* __restrict__ rank,
+                                const u32* __restrict__ mpre, const u32* __restrict__ match, int S,
+                                u64* __restrict__ c_lo, u64* __restrict__ c_hi, u64* __restrict__ c_st) {
+  for (u32 j = blockIdx.x * blockDim.x + threadIdx.x; j < nb; j += gridDim.x * blockDim.x) {
+    if (match[j]) continue;
+    u32 o = j + rank[j] - mpre[j];
+    c_lo[o] = b_lo[j];
+    if (KW == 2) c_hi[o] = b_hi[j];
+    for (int k = 0; k < S; ++k) c_st[(size_t)o * S + k] = b_st[(size_t)j * S + k];
+  }
+}
+
+__global__ void k_copy_u32(const u32* __restrict__ s, u32* __restrict__ d, u32 n) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) d[i] = s[i];
+}
+
+void merge_combine(int KW, int S, const int* ops, const int* types, const u64* a_lo, const u64* a_hi,
+                   const u64* a_st, u32 na, const u64* b_lo, const u64* b_hi, const u64* b_st, u32 nb,
+                   u64* c_lo, u64* c_hi, u64* c_st, MergeTmp& tmp, cudaStream_t st) {
+  OpsArr oa;
+  for (int k = 0; k < ISA_MAX_SLOTS; ++k) { oa.op[k] = k < S ? ops[k] : 0; oa.type[k] = k < S ? types[k] : 0; }
+  // ranks + match flags; prefix of match flags is built in a copy (match kept)
+  if (na) {
+    int g = grid_for(na, 256);
+    if (KW == 2) k_rank<2><<<g, 256, 0, st>>>(a_lo, a_hi, na, b_lo, b_hi, nb, tmp.rank_a, tmp.match_a);
+    else k_rank<1><<<g, 256, 0, st>>>(a_lo, a_hi, na, b_lo, b_hi, nb, tmp.rank_a, tmp.match_a);
+  }
+  if (nb) {
+    int g = grid_for(nb, 256);
+    if (KW == 2) k_rank<2><<<g, 256, 0, st>>>(b_lo, b_hi, nb, a_lo, a_hi, na, tmp.rank_b, tmp.match_b);
+    else k_rank<1><<<g, 256, 0, st>>>(b_lo, b_hi, nb, a_lo, a_hi, na, tmp.rank_b, tmp.match_b);
+  }
+  // prefix counts live after the flags: match_x[n + 1 + i]
+  u32* pre_a = tmp.match_a + na + 1;
+  u32* pre_b = tmp.match_b + nb + 1;
+  if (na) {
+    k_copy_u32<<<grid_for(na, 256), 256, 0, st>>>(tmp.match_a, pre_a, na);
+    scan_exclusive_u32(pre_a, na, tmp.scan_tmp, tmp.total, st);
+    int g = grid_for(na, 256);
+    if (KW == 2) k_merge_write_a<2><<<g, 256, 0, st>>>(a_lo, a_hi, a_st, na, b_st, tmp.rank_a, pre_a, tmp.match_a, S, oa, c_lo, c_hi, c_st);
+    else k_merge_write_a<1><<<g, 256, 0, st>>>(a_lo, a_hi, a_st, na, b_st, tmp.rank_a, pre_a, tmp.match_a, S, oa, c_lo, c_hi, c_st);
+  } else {
+    cudaMemsetAsync(tmp.total, 0, sizeof(u32), st);
+  }
+  if (nb) {
+    k_copy_u32<<<grid_for(nb, 256), 256, 0, st>>>(tmp.match_b, pre_b, nb);
+    scan_exclusive_u32(pre_b, nb, tmp.scan_tmp, tmp.total + 1, st);
+    int g = grid_for(nb, 256);
+    if (KW == 2) k_merge_write_b<2><<<g, 256, 0, st>>>(b_lo, b_hi, b_st, nb, tmp.rank_b, pre_b, tmp.match_b, S, c_lo, c_hi, c_st);
+    else k_merge_write_b<1><<<g, 256, 0, st>>>(b_lo, b_hi, b_st, nb, tmp.rank_b, pre_b, tmp.match_b, S, c_lo, c_hi, c_st);
+  } else {
+    cudaMemsetAsync(tmp.total + 1, 0, sizeof(u32), st);
+  }
+}
+
+__global__ void k_fold_partials(int nt, SlotDesc sd, const u64* __restrict__ partials, u32 grid, u64* __restrict__ T_st) {
+  const int S = sd.nslots;
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nt * S) return;
+  int j = q / S, s = q % S;
+  u64 x = identity_slot(sd.op[s], sd.type[s]);
+  for (u32 c = 0; c < grid; ++c) x = combine_slot(sd.op[s], sd.type[s], x, partials[((size_t)c * nt + j) * S + s]);
+  T_st[(size_t)j * S + s] = combine_slot(sd.op[s], sd.type[s], T_st[(size_t)j * S + s], x);
+}
+
+void fold_partials(int nt, const SlotDesc& sd, const u64* partials, u32 grid, u64* T_st, cudaStream_t st) {
+  int n = nt * sd.nslots;
+  if (n) k_fold_partials<<<1, 128, 0, st>>>(nt, sd, partials, grid, T_st);
+}
+
+__global__ void k_compact_misses(const u32* __restrict__ miss_buf, const u32* __restrict__ miss_cnt,
+                                 const u32* __restrict__ miss_off, u32 rpc, u32* __restrict__ out) {
+  const u32 c = blockIdx.x;
+  const u32 cnt = miss_cnt[c], off = miss_off[c];
+  for (u32 i = threadIdx.x; i < cnt; i += blockDim.x) out[off + i] = miss_buf[(size_t)c * rpc + i];
+}
+
+void compact_misses(const u32* miss_buf, const u32* miss_cnt, const u32* miss_off, u32 grid, u32 rows_per_cta,
+                    u32* out, cudaStream_t st) {
+  k_compact_misses<<<grid, 256, 0, st>>>(miss_buf, miss_cnt, miss_off, rows_per_cta, out);
+}
+
+// ============================================================ runs ====
+template <int KW>
+__global__ void k_run_lower_bounds(const RunRef* __restrict__ runs, int nruns, const u64* __restrict__ b_lo,
+                                   const u64* __restrict__ b_hi, int nb, u32* __restrict__ out) {
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nruns * nb) return;
+  int r = q / nb, b = q % nb;
+  RunRef rr = runs[r];
+  u32 l = 0, h = rr.rows;
+  u64 khi = KW == 2 ? b_hi[b] : 0, klo = b_lo[b];
+  while (l < h) {
+    u32 m = (l + h) >> 1;
+    u64 mhi = KW == 2 ? rr.hi[m] : 0;
+    if (key_less<KW>(mhi, rr.lo[m], khi, klo)) l = m + 1; else h = m;
+  }
+  out[q] = l;
+}
+
+void run_lower_bounds(int KW, const RunRef* runs_dev, int nruns, const u64* b_lo, const u64* b_hi, int nb, u32* out,
+                      cudaStream_t st) {
+  int n = nruns * nb;
+  if (n == 0) return;
+  int g = (n + 127) / 128;
+  if (KW == 2) k_run_lower_bounds<2><<<g, 128, 0, st>>>(runs_dev, nruns, b_lo, b_hi, nb, out);
+  else k_run_lower_bounds<1><<<g, 128, 0, st>>>(runs_dev, nruns, b_lo, b_hi, nb, out);
+}
+
+// ========================================================== export ====
+__global__ void k_export_key(const u64* __restrict__ lo, const u64* __restrict__ hi, u32 n, int dtype, int shift,
+                             int width, void* out) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    u64 f = key_field(hi ? hi[i] : 0, lo[i], shift, width);
+    if (dtype_signed(dtype)) f ^= (1ull << (width - 1));
+    switch (width) {
+      case 8: ((unsigned char*)out)[i] = (unsigned char)f; break;
+      case 16: ((unsigned short*)out)[i] = (unsigned short)f; break;
+      case 32: ((unsigned int*)out)[i] = (unsigned int)f; break;
+      default: ((u64*)out)[i] = f; break;
+    }
+  }
+}
+
+void export_key_col(const u64* lo, const u64* hi, u32 n, int dtype, int shift, int width, void* out, cudaStream_t st) {
+  if (n) k_export_key<<<grid_for(n, 256), 256, 0, st>>>(lo, hi, n, dtype, shift, width, out);
+}
+
+__global__ void k_export_slot(const u64* __restrict__ stt, int S, int s, u32 n, u64* __restrict__ out) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = stt[(size_t)i * S + s];
+}
+
+void export_slot(const u64* stt, int S, int s, u32 n, u64* out, cudaStream_t st) {
+  if (n) k_export_slot<<<grid_for(n, 256), 256, 0, st>>>(stt, S, s, n, out);
+}
+
+// ======================================================= partition ====
+__global__ void k_sample_keys(KeyDesc kd, i64 n, i64 stride, u64* __restrict__ out_lo, u64* __restrict__ out_hi) {
+  i64 ns = (n + stride - 1) / stride;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < ns; i += (i64)gridDim.x * blockDim.x) {
+    u64 h, l;
+    load_key(kd, i * stride, h, l);
+    out_lo[i] = l;
+    out_hi[i] = h;
+  }
+}
+
+void sample_keys(const KeyDesc& kd, int64_t n, int64_t stride, u64* out_lo, u64* out_hi, cudaStream_t st) {
+  int64_t ns = (n + stride - 1) / stride;
+  if (ns > 0) k_sample_keys<<<grid_for(ns, 256), 256, 0, st>>>(kd, n, stride, out_lo, out_hi);
+}
+
+template <int KW>
+__global__ void k_partition_dest(KeyDesc kd, u32 n, const u64* __restrict__ s_lo, const u64* __restrict__ s_hi, int ns,
+                                 u64* __restrict__ dest, u32* __restrict__ val) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    u64 h, l;
+    load_key(kd, i, h, l);
+    // number of splitters <= key (upper bound)
+    int lo_i = 0, hi_i = ns;
+    while (lo_i < hi_i) {
+      int m = (lo_i + hi_i) >> 1;
+      u64 mh = KW == 2 ? s_hi[m] : 0;
+      if (!key_less<KW>(h, l, mh, s_lo[m])) lo_i = m + 1; else hi_i = m;
+    }
+    dest[i] = (u64)lo_i;
+    val[i] = i;
+  }
+}
+
+void partition_dest(int KW, const KeyDesc& kd, u32 n, const u64* s_lo, const u64* s_hi, int ns, u64* dest_lo, u32* val,
+                    cudaStream_t st) {
+  if (n == 0) return;
+  int g = grid_for(n, 256);
+  if (KW == 2) k_partition_dest<2><<<g, 256, 0, st>>>(kd, n, s_lo, s_hi, ns, dest_lo, val);
+  else k_partition_dest<1><<<g, 256, 0, st>>>(kd, n, s_lo, s_hi, ns, dest_lo, val);
+}
+
+template <typename T>
+__global__ void k_gather(const T* __restrict__ src, const u32* __restrict__ perm, u32 n, T* __restrict__ dst) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[perm[i]];
+}
+
+void gather_column(const void* src, int elem_bytes, const u32* perm, u32 n, void* dst, cudaStream_t st) {
+  if (n == 0) return;
+  int g = grid_for(n, 256);
+  switch (elem_bytes) {
+    case 1: k_gather<unsigned char><<<g, 256, 0, st>>>((const unsigned char*)src, perm, n, (unsigned char*)dst); break;
+    case 2: k_gather<unsigned short><<<g, 256, 0, st>>>((const unsigned short*)src, perm, n, (unsigned short*)dst); break;
+    case 4: k_gather<unsigned int><<<g, 256, 0, st>>>((const unsigned int*)src, perm, n, (unsigned int*)dst); break;
+    default: k_gather<u64><<<g, 256, 0, st>>>((const u64*)src, perm, n, (u64*)dst); break;
+  }
+}
+
+__global__ void k_count_dest(const u64* __restrict__ d, u32 n, int ndest, u32* __restrict__ counts) {
+  // counts[k] = upper_bound(d, k) for the sorted destination array
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= ndest) return;
+  u32 l = 0, h = n;
+  while (l < h) {
+    u32 m = (l + h) >> 1;
+    if (d[m] <= (u64)k) l = m + 1; else h = m;
+  }
+  counts[k] = l;
+}
+
+void count_dest(const u64* dest_sorted, u32 n, int ndest, u32* counts, cudaStream_t st) {
+  k_count_dest<<<1, 256, 0, st>>>(dest_sorted, n, ndest, counts);
+}
+
+}  // namespace isa

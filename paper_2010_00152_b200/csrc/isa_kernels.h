@@ -1,0 +1,109 @@
+// Host-side launch wrappers for the sm_100a kernels in isa_kernels.cu.
+#pragma once
+#include "isa_common.cuh"
+
+namespace isa {
+
+// ---- scan -----------------------------------------------------------------
+// Exclusive prefix sum of n u32 values (in place).  `tmp` must hold
+// scan_tmp_words(n) u32.  If total != nullptr the grand total is written there
+// (device pointer).
+size_t scan_tmp_words(u32 n);
+void scan_exclusive_u32(u32* data, u32 n, u32* tmp, u32* total, cudaStream_t st);
+
+// ---- radix sort -----------------------------------------------------------
+// Stable LSD radix sort of (key, u32 value) pairs over key bits
+// [bit_lo, bit_hi), 8-bit digits.  Buffers ping-pong between *_a and *_b; the
+// return value is 0 if the result is in the *_a buffers and 1 for *_b.
+struct SortBufs {
+  u64* lo[2];
+  u64* hi[2];
+  u32* val[2];
+  u32* tile_hist;   // 256 * ceil(n / 4096)
+  u32* scan_tmp;
+};
+size_t sort_hist_words(u32 n);
+int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStream_t st, int64_t* launches);
+
+// ---- key building -------------------------------------------------------
+// keys of rows row0 + (pos ? pos[i] : i), i < n  ->  lo/hi/val(=pos or i);
+// varying[0..1] |= key ^ key_of_first (lo, hi).
+void build_keys(int KW, const KeyDesc& kd, int64_t row0, const u32* pos, u32 n,
+                u64* lo, u64* hi, u32* val, u64* varying, cudaStream_t st);
+// varying |= key ^ key[0] for an existing SoA key array
+void keys_varying(int KW, const u64* lo, const u64* hi, u32 n, u64* varying, cudaStream_t st);
+void iota_u32(u32* v, u32 n, cudaStream_t st);
+
+// ---- flush analysis ------------------------------------------------------
+// For each head of the sorted chunk (key != previous key) whose key is absent
+// from the table (T_lo/T_hi, t rows): set bit val[i] in `bitmap`, count.
+void new_heads(int KW, const u64* lo, const u64* hi, const u32* val, u32 m,
+               const u64* T_lo, const u64* T_hi, u32 t, u32* bitmap, u32* n_new,
+               cudaStream_t st);
+// position of the k-th (1-based) set bit of bitmap (nbits bits) -> *out
+void select_kth_bit(const u32* bitmap, u32 nbits, u32 k, u32* word_tmp, u32* scan_tmp,
+                    u32* out, cudaStream_t st);
+
+// ---- collapse (segmented reduce of a sorted sequence) -------------------
+// Elements i < m with val[i] < limit are grouped by equal key; each group
+// becomes one output row (key + combined state).  States come from the raw
+// input rows (make_state of row row0 + val[i]) when st_in == nullptr, else
+// from st_in[val[i] * S ..] (already-built states).
+struct CollapseTmp {
+  u32* flags;      // m + 1
+  u32* scan_tmp;
+  u64* partial;    // ceil(m / 8) * S
+  u32* partial_slot;  // ceil(m / 8)
+  u32* total;      // 1 (device)
+};
+void collapse(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, u32 limit,
+              const SlotDesc& sd, int64_t row0, const u64* st_in,
+              u64* out_lo, u64* out_hi, u64* out_st, CollapseTmp& tmp, cudaStream_t st);
+
+// ---- merge two sorted unique tables, combining equal keys ----------------
+struct MergeTmp {
+  u32* rank_a; u32* match_a;   // |A| + 1
+  u32* rank_b; u32* match_b;   // |B| + 1
+  u32* scan_tmp;
+  u32* total;                  // 2 (device): matches in A, matches in B
+};
+void merge_combine(int KW, int S, const int* ops, const int* types,
+                   const u64* a_lo, const u64* a_hi, const u64* a_st, u32 na,
+                   const u64* b_lo, const u64* b_hi, const u64* b_st, u32 nb,
+                   u64* c_lo, u64* c_hi, u64* c_st, MergeTmp& tmp, cudaStream_t st);
+
+// ---- tiny-table absorb (the early-aggregation probe for |T| <= 8) -------
+struct TinyTable { u64 lo[8]; u64 hi[8]; };
+// Grid geometry helper: CTAs and rows per CTA for n rows.
+void absorb_geometry(u32 n, int num_sms, u32* grid, u32* rows_per_cta);
+bool absorb_supported(int nt, int nslots);
+void absorb_tiny(int KW, int nt, const KeyDesc& kd, const SlotDesc& sd, int64_t row0, u32 n,
+                 const TinyTable& tt, u32 grid, u32 rows_per_cta,
+                 u64* partials, u32* miss_buf, u32* miss_cnt, cudaStream_t st);
+// T_st[j*S + s] = combine(T_st, fold_c partials[c][j][s])
+void fold_partials(int nt, const SlotDesc& sd, const u64* partials, u32 grid, u64* T_st, cudaStream_t st);
+// compact per-CTA miss lists (miss_off = exclusive scan of miss_cnt)
+void compact_misses(const u32* miss_buf, const u32* miss_cnt, const u32* miss_off, u32 grid,
+                    u32 rows_per_cta, u32* out, cudaStream_t st);
+
+// ---- runs / wide merge helpers ------------------------------------------
+// out[r * nb + b] = lower_bound(run r, bound b); run keys may be mapped host memory
+struct RunRef { const u64* lo; const u64* hi; u32 rows; };
+void run_lower_bounds(int KW, const RunRef* runs_dev, int nruns, const u64* b_lo, const u64* b_hi,
+                      int nb, u32* out, cudaStream_t st);
+
+// ---- result export --------------------------------------------------------
+// key column c of rows [0, n) -> out (column dtype); slot s -> out (8 bytes)
+void export_key_col(const u64* lo, const u64* hi, u32 n, int dtype, int shift, int width,
+                    void* out, cudaStream_t st);
+void export_slot(const u64* states, int S, int s, u32 n, u64* out, cudaStream_t st);
+
+// ---- partition (multi-GPU range split) -----------------------------------
+void sample_keys(const KeyDesc& kd, int64_t n, int64_t stride, u64* out_lo, u64* out_hi, cudaStream_t st);
+// dest[i] = #splitters <= key(i) -> written as the low key word for a 1-pass radix sort
+void partition_dest(int KW, const KeyDesc& kd, u32 n, const u64* s_lo, const u64* s_hi, int ns,
+                    u64* dest_lo, u32* val, cudaStream_t st);
+void gather_column(const void* src, int elem_bytes, const u32* perm, u32 n, void* dst, cudaStream_t st);
+void count_dest(const u64* dest_sorted, u32 n, int ndest, u32* counts, cudaStream_t st);
+
+}  // namespace isa

@@ -1,0 +1,585 @@
+"""SortAggregate on B200: the reference operator's entry points over the CUDA path.
+
+Drop-in for ``insortagg.sortagg.SortAggregate`` in wide-merge mode
+(/root/reference/pkg/src/insortagg/sortagg.py:725-784):
+
+* ``SortAggConfig`` has the reference's fields, defaults and validation
+  (sortagg.py:53-86) plus three placement knobs (``run_tier``,
+  ``chunk_rows_max``, ``merge_window_rows``).
+* ``SortAggregate(schema, config, store, ledger).execute(rows)`` returns the
+  sorted, unfinalized ``Row`` list and fills ``ledger``, ``initial_plan``,
+  ``executed_steps`` and ``runs_after_generation`` like the reference.
+* ``SortAggregate.execute_columns(keys, values)`` is the columnar fast path:
+  key / value tensors in, sorted key columns + state-slot columns out.
+
+All grouping work runs in libinsortagg_b200.so (run generation with early
+aggregation, host-tier spill, wide merge); Python only converts layouts.
+The merge planner / output estimator below are host-side bookkeeping that
+reproduce the reference's ``initial_plan`` from the run sizes and fill
+cycles the device reports.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .core import (
+    AggregateKind,
+    InvalidInputError,
+    MetricsLedger,
+    ResourceError,
+    Row,
+)
+
+WIDE = "wide"
+TRADITIONAL = "traditional"
+SEPARATE = "separate"
+
+READ_SORT_WRITE = "read_sort_write"
+REPLACEMENT_SELECTION = "replacement_selection"
+
+ASCENDING = "ascending"
+
+
+@dataclass
+class SortAggConfig:
+    """Operator configuration (sortagg.py:53-86)."""
+
+    memory_budget: int
+    page_capacity: int
+    run_generation_mode: str = READ_SORT_WRITE
+    merge_mode: str = WIDE
+    ovc_enabled: bool = True
+    ovc_cache: bool = True
+    ovc_direction: str = ASCENDING
+    interpolation_search: bool = False
+    batch_size: int = 1
+    leaf_capacity: int = 64
+    eviction_chunk: int | None = None
+    output_size_hint: int | None = None
+    max_preliminary_merges: int | None = None
+    # B200 placement knobs (no reference counterpart)
+    run_tier: str = "host"          # where spilled runs live: "host" (pinned DRAM) | "hbm"
+    chunk_rows_max: int = 0         # 0 = library default
+    window_rows: int = 0            # host-input staging window, 0 = default
+    merge_window_rows: int = 0      # wide-merge key-range window capacity, 0 = default
+
+    def __post_init__(self):
+        if self.page_capacity < 1:
+            raise InvalidInputError("page capacity must be positive")
+        if self.memory_budget < 2 * self.page_capacity:
+            raise InvalidInputError("memory budget must cover two pages")
+        if self.max_fanin < 2:
+            raise InvalidInputError("fan-in must be at least 2")
+        if self.run_generation_mode not in (READ_SORT_WRITE, REPLACEMENT_SELECTION):
+            raise InvalidInputError(
+                f"unknown run generation mode {self.run_generation_mode!r}")
+        if self.merge_mode not in (WIDE, TRADITIONAL, SEPARATE):
+            raise InvalidInputError(f"unknown merge mode {self.merge_mode!r}")
+        if self.run_tier not in ("host", "hbm"):
+            raise InvalidInputError(f"unknown run tier {self.run_tier!r}")
+
+    @property
+    def max_fanin(self):
+        return self.memory_budget // self.page_capacity
+
+
+# ---------------------------------------------------------------------------
+# host-side planner bookkeeping (reproduces the reference's initial_plan)
+# ---------------------------------------------------------------------------
+
+class OutputEstimator:
+    """Distinct-key (output size) estimate from run generation
+    (sortagg.py:89-160): the larger of observed distinct counts, the largest
+    run, and the read-sort-write fill-cycle inversion C = O ln(O / (O - M)),
+    capped at the rows seen."""
+
+    def __init__(self, budget):
+        self.budget = budget
+        self.steady_probes = 0
+        self.steady_absorbs = 0
+        self.steady_resident_sum = 0
+        self.cycles = []
+        self.observed = 1
+        self.max_run_rows = 0
+
+    def note_steady_probe(self, resident, absorbed):
+        self.steady_probes += 1
+        self.steady_resident_sum += resident
+        self.steady_absorbs += 1 if absorbed else 0
+
+    def note_cycle(self, consumed):
+        if consumed > 0:
+            self.cycles.append(consumed)
+
+    def observe_distinct(self, count):
+        self.observed = max(self.observed, count)
+
+    def note_runs(self, run_rows):
+        for rows in run_rows:
+            self.max_run_rows = max(self.max_run_rows, rows)
+
+    def _invert_cycle(self, mean_cycle, rows_seen):
+        m = self.budget
+        if mean_cycle <= m * (1 + 1e-9):
+            return rows_seen
+
+        def cycle_len(o):
+            return o * math.log(o / (o - m))
+
+        lo, hi = m * (1 + 1e-12), 2.0 * m
+        while cycle_len(hi) > mean_cycle:
+            hi *= 2
+            if hi > 1e18:
+                return rows_seen
+        for _ in range(80):
+            mid = 0.5 * (lo + hi)
+            if cycle_len(mid) > mean_cycle:
+                lo = mid
+            else:
+                hi = mid
+        return 0.5 * (lo + hi)
+
+    def estimate(self, rows_seen):
+        options = [self.observed, self.max_run_rows, 1]
+        if self.steady_probes >= 100:
+            options.append(self.steady_resident_sum / self.steady_absorbs
+                           if self.steady_absorbs else rows_seen)
+        if self.cycles:
+            options.append(self._invert_cycle(sum(self.cycles) / len(self.cycles), rows_seen))
+        est = max(options)
+        if rows_seen:
+            est = min(est, rows_seen)
+        return max(1, int(est))
+
+
+@dataclass(frozen=True)
+class PlanStep:
+    kind: str  # "traditional" | "wide"
+    input_run_ids: tuple
+    expected_output_rows: int
+
+
+@dataclass(frozen=True)
+class MergePlan:
+    steps: tuple
+    levels: int
+
+    @property
+    def wide_steps(self):
+        return sum(1 for s in self.steps if s.kind == "wide")
+
+
+def wide_admissible(sizes, o_est, config):
+    """Admission test of the final wide merge (sortagg.py:479-499)."""
+    if len(sizes) == 1:
+        return True
+    ordered = sorted(sizes)
+    if sum(ordered[:config.max_fanin]) < o_est:
+        return False
+    index_budget = config.memory_budget - 2 * config.page_capacity
+    if index_budget < 1:
+        return False
+    median = ordered[len(ordered) // 2]
+    return o_est * config.page_capacity / max(1, median) <= index_budget
+
+
+def plan_merge(run_sizes, o_est, config):
+    """Merge plan for runs of the given sizes (sortagg.py:502-542): fan-in
+    limited traditional levels over the smallest runs until the wide step is
+    admissible (run ids are positions in ``run_sizes``)."""
+    if not run_sizes:
+        raise InvalidInputError("cannot plan a merge without runs")
+    o_est = max(1, int(o_est))
+    fan = config.max_fanin
+    pool = sorted((rows, rid) for rid, rows in enumerate(run_sizes))
+    steps, levels, synthetic = [], 0, 0
+    while True:
+        sizes = [rows for rows, _ in pool]
+        if wide_admissible(sizes, o_est, config):
+            steps.append(PlanStep("wide", tuple(r for _, r in pool), min(sum(sizes), o_est)))
+            break
+        if len(pool) <= fan:
+            steps.append(PlanStep("traditional", tuple(r for _, r in pool), min(sum(sizes), o_est)))
+            break
+        levels += 1
+        merged = []
+        for start in range(0, len(pool), fan):
+            group = pool[start:start + fan]
+            if len(group) == 1:
+                merged.append(group[0])
+                continue
+            total = sum(rows for rows, _ in group)
+            out_rows = min(total, o_est) if total >= o_est else total
+            synthetic += 1
+            steps.append(PlanStep("traditional", tuple(r for _, r in group), out_rows))
+            merged.append((out_rows, f"planned-{synthetic}"))
+        pool = sorted(merged)
+    return MergePlan(tuple(steps), levels)
+
+
+# ---------------------------------------------------------------------------
+# run stores: accepted for signature parity; run placement is internal
+# ---------------------------------------------------------------------------
+
+class MemoryStore:
+    """Accepted as the ``store`` argument (runstore.py:157-192).  The B200
+    operator places runs itself (pinned host DRAM or HBM, ``run_tier``)."""
+
+    def __init__(self, retain_rows=False):
+        self.retain_rows = retain_rows
+
+
+class FileStore:
+    """File-backed run store of the reference (runstore.py:195-236).  The
+    byte-level page format is not part of the GPU path; passing one to
+    SortAggregate raises InvalidInputError."""
+
+    def __init__(self, directory):
+        self.directory = directory
+
+
+# ---------------------------------------------------------------------------
+# dtype plumbing
+# ---------------------------------------------------------------------------
+
+def _torch():
+    import torch
+    return torch
+
+
+def _isa_dtype(t):
+    torch = _torch()
+    table = {
+        torch.uint8: _native.U8, torch.int8: _native.I8, torch.int16: _native.I16,
+        torch.int32: _native.I32, torch.int64: _native.I64, torch.float32: _native.F32,
+        torch.float64: _native.F64,
+    }
+    for name, code in (("uint16", _native.U16), ("uint32", _native.U32), ("uint64", _native.U64)):
+        if hasattr(torch, name):
+            table[getattr(torch, name)] = code
+    code = table.get(t.dtype)
+    if code is None:
+        raise InvalidInputError(f"unsupported column dtype {t.dtype}")
+    return code
+
+
+_OP_CODES = {"add": _native.OP_ADD, "min": _native.OP_MIN, "max": _native.OP_MAX}
+
+
+class ColumnarResult(tuple):
+    """(key_columns, state_columns): sorted unique keys, one tensor per key
+    column (input dtype) and one per state slot (int64 or float64)."""
+
+    __slots__ = ()
+
+    def __new__(cls, keys, states):
+        return super().__new__(cls, (keys, states))
+
+    @property
+    def keys(self):
+        return self[0]
+
+    @property
+    def states(self):
+        return self[1]
+
+    def __len__(self):  # number of tuple fields (keys, states)
+        return 2
+
+    @property
+    def n_groups(self):
+        return int(self[0][0].shape[0]) if self[0] else 0
+
+
+class SortAggregate:
+    """Sort-based grouping / duplicate removal / aggregation on one B200.
+
+    ``execute`` consumes an unsorted row stream and returns aggregated rows in
+    ascending key order (sortagg.py:744-784); ``execute_columns`` does the same
+    on column tensors.  Runs spill to pinned host memory (default) or HBM.
+    """
+
+    def __init__(self, schema, config, store=None, ledger=None, *, device=None):
+        if isinstance(store, FileStore):
+            raise InvalidInputError(
+                "FileStore is not supported by the B200 operator; runs are placed "
+                "in pinned host memory or HBM (SortAggConfig.run_tier)")
+        if config.merge_mode != WIDE:
+            raise InvalidInputError(
+                f"merge_mode {config.merge_mode!r} is not supported by the B200 operator "
+                "(wide-merge path only)")
+        if config.run_generation_mode != READ_SORT_WRITE:
+            raise InvalidInputError(
+                f"run_generation_mode {config.run_generation_mode!r} is not supported by the "
+                "B200 operator (read-sort-write only)")
+        if any(c.kind != "int64" for c in schema.key_columns):
+            raise InvalidInputError("utf8 key columns are not supported by the B200 operator")
+        self.schema = schema
+        self.config = config
+        self.store = store
+        self.ledger = ledger if ledger is not None else MetricsLedger()
+        self.initial_plan = None
+        self.executed_steps = []
+        self.runs_after_generation = 0
+        self.device_ledger = None
+        self.cycles = []
+        self.run_rows = []
+        self._device = device
+        self._handles = {}
+
+    # -- native handles ----------------------------------------------------
+    def _device_index(self):
+        torch = _torch()
+        if self._device is not None:
+            d = torch.device(self._device)
+            return d.index if d.index is not None else torch.cuda.current_device()
+        return torch.cuda.current_device()
+
+    def _handle(self, key_codes, val_codes, slots):
+        dev = self._device_index()
+        sig = (tuple(key_codes), tuple(val_codes), tuple(slots), dev)
+        h = self._handles.get(sig)
+        if h is not None:
+            return h
+        cfg = _native.IsaConfig()
+        cfg.memory_budget = self.config.memory_budget
+        cfg.page_capacity = self.config.page_capacity
+        cfg.run_tier = _native.TIER_HOST if self.config.run_tier == "host" else _native.TIER_HBM
+        cfg.device = dev
+        cfg.chunk_rows_max = self.config.chunk_rows_max
+        cfg.window_rows = self.config.window_rows
+        cfg.merge_window_rows = self.config.merge_window_rows
+        sch = _native.IsaSchema()
+        if len(key_codes) > _native.MAX_KEY_COLS:
+            raise InvalidInputError("too many key columns")
+        if len(slots) > _native.MAX_SLOTS:
+            raise InvalidInputError("too many aggregate state slots")
+        if len(val_codes) > _native.MAX_VAL_COLS:
+            raise InvalidInputError("too many value columns")
+        sch.n_key_cols = len(key_codes)
+        for i, c in enumerate(key_codes):
+            sch.key_dtypes[i] = c
+        sch.n_val_cols = len(val_codes)
+        for i, c in enumerate(val_codes):
+            sch.val_dtypes[i] = c
+        sch.n_slots = len(slots)
+        for s, (op, ty, src, col) in enumerate(slots):
+            sch.slot_op[s] = op
+            sch.slot_type[s] = ty
+            sch.slot_src[s] = src
+            sch.slot_col[s] = col
+        h = _native.Handle(cfg, sch)
+        self._handles[sig] = h
+        return h
+
+    def close(self):
+        for h in self._handles.values():
+            h.close()
+        self._handles.clear()
+
+    # -- slot layout -----------------------------------------------------------
+    def _slots_from_values(self, value_cols):
+        """Schema.make_state layout (core.py:162-182) over value columns:
+        returns (value tensors, slot specs)."""
+        torch = _torch()
+        vals, slots = [], []
+        for agg, col in zip(self.schema.aggregates, value_cols):
+            if agg.kind == AggregateKind.COUNT:
+                slots.append((_native.OP_ADD, _native.SLOT_I64, _native.SRC_ONE, 0))
+                continue
+            if col is None:
+                raise InvalidInputError(f"aggregate {agg.name!r} needs a value column")
+            is_float = col.dtype in (torch.float32, torch.float64, torch.float16, torch.bfloat16)
+            ty = _native.SLOT_F64 if is_float else _native.SLOT_I64
+            idx = len(vals)
+            vals.append(col)
+            op = {AggregateKind.SUM: _native.OP_ADD, AggregateKind.MIN: _native.OP_MIN,
+                  AggregateKind.MAX: _native.OP_MAX, AggregateKind.AVG: _native.OP_ADD}[agg.kind]
+            slots.append((op, ty, _native.SRC_COLUMN, idx))
+            if agg.kind == AggregateKind.AVG:
+                slots.append((_native.OP_ADD, _native.SLOT_I64, _native.SRC_ONE, 0))
+        return vals, slots
+
+    def _resolve_values(self, values):
+        aggs = self.schema.aggregates
+        if values is None:
+            values = {}
+        if isinstance(values, dict):
+            out = []
+            for agg in aggs:
+                if agg.kind == AggregateKind.COUNT:
+                    out.append(None)
+                    continue
+                name = agg.column if agg.column is not None else agg.name
+                if name not in values:
+                    raise InvalidInputError(f"missing value column {name!r} for aggregate {agg.name!r}")
+                out.append(values[name])
+            return out
+        values = list(values)
+        if len(values) != len(aggs):
+            raise InvalidInputError(f"expected {len(aggs)} value columns (one per aggregate), got {len(values)}")
+        return values
+
+    # -- columnar fast path ----------------------------------------------------
+    def execute_columns(self, keys, values=None, *, states=False, stream=None):
+        """Group ``keys`` (list of 1-D integer tensors, most significant
+        first) and aggregate ``values``.
+
+        ``values``: dict column-name -> tensor (``AggregateSpec.column``, else
+        the aggregate name) or a list parallel to ``schema.aggregates`` (None
+        for COUNT).  With ``states=True`` ``values`` is instead a list of
+        already-built state-slot columns (one per slot, Schema layout) that
+        are combined with ``merge_states``.
+
+        Inputs on a CUDA device stay there; CPU inputs (pinned for speed) are
+        streamed to the GPU in windows.  Returns ColumnarResult(keys, states)
+        on the input's device.
+        """
+        torch = _torch()
+        keys = list(keys)
+        if len(keys) != self.schema.arity:
+            raise InvalidInputError(f"expected {self.schema.arity} key columns, got {len(keys)}")
+        n = int(keys[0].shape[0])
+        for k in keys:
+            if k.dim() != 1 or int(k.shape[0]) != n:
+                raise InvalidInputError("key columns must be 1-D and of equal length")
+        if states:
+            vals = list(values or [])
+            if len(vals) != self.schema.state_slots:
+                raise InvalidInputError(f"expected {self.schema.state_slots} state columns, got {len(vals)}")
+            slots = []
+            for s, (op, col) in enumerate(zip(self.schema.slot_ops(), vals)):
+                ty = _native.SLOT_F64 if col.dtype.is_floating_point else _native.SLOT_I64
+                slots.append((_OP_CODES[op], ty, _native.SRC_COLUMN, s))
+        else:
+            vals, slots = self._slots_from_values(self._resolve_values(values))
+        for v in vals:
+            if v.dim() != 1 or int(v.shape[0]) != n:
+                raise InvalidInputError("value columns must be 1-D and match the key length")
+        on_host = keys[0].device.type == "cpu"
+        cols = keys + vals
+        for c in cols:
+            if (c.device.type == "cpu") != on_host:
+                raise InvalidInputError("all columns must live on the same device type")
+        if not on_host:
+            dev = keys[0].device
+            self._device = dev
+            for c in cols:
+                if c.device != dev:
+                    raise InvalidInputError("all columns must be on the same CUDA device")
+        if not torch.cuda.is_available():
+            raise ResourceError("the B200 operator needs a CUDA device (torch.cuda.is_available() is False)")
+        keys = [k.contiguous() for k in keys]
+        vals = [v.contiguous() for v in vals]
+        key_codes = [_isa_dtype(k) for k in keys]
+        for c in key_codes:
+            if c in (_native.F32, _native.F64):
+                raise InvalidInputError("key columns must be integer")
+        val_codes = [_isa_dtype(v) for v in vals]
+        h = self._handle(key_codes, val_codes, slots)
+        dev_index = self._device_index()
+        if stream is None:
+            stream = torch.cuda.current_stream(dev_index)
+        sptr = ctypes_stream(stream)
+        with torch.cuda.device(dev_index):
+            n_groups = h.execute(n, [k.data_ptr() for k in keys], [v.data_ptr() for v in vals], on_host, sptr)
+            out_dev = torch.device("cpu") if on_host else keys[0].device
+            pin = on_host
+            out_keys = [torch.empty(n_groups, dtype=k.dtype, device=out_dev, pin_memory=pin) for k in keys]
+            out_states = [torch.empty(n_groups, dtype=torch.float64 if ty == _native.SLOT_F64 else torch.int64,
+                                      device=out_dev, pin_memory=pin)
+                          for (_, ty, _, _) in slots]
+            if n_groups:
+                h.result_copy([t.data_ptr() for t in out_keys], [t.data_ptr() for t in out_states], on_host, sptr)
+        self._record(h, n, n_groups)
+        return ColumnarResult(out_keys, out_states)
+
+    def _record(self, h, n_rows, n_groups):
+        led = h.metrics()
+        self.device_ledger = led.as_dict()
+        for name in MetricsLedger.__slots__:
+            setattr(self.ledger, name, getattr(self.ledger, name) + getattr(led, name))
+        self.cycles = h.cycles()
+        self.run_rows = h.run_rows()
+        self.runs_after_generation = len(self.run_rows)
+        self.executed_steps = []
+        self.initial_plan = None
+        if self.run_rows:
+            est = OutputEstimator(self.config.memory_budget)
+            for c in self.cycles:
+                est.note_cycle(c)
+            est.note_runs(self.run_rows)
+            o_est = (self.config.output_size_hint if self.config.output_size_hint is not None
+                     else est.estimate(n_rows))
+            self.initial_plan = plan_merge(self.run_rows, o_est, self.config)
+            self.executed_steps.append({"kind": "wide", "fan_in": len(self.run_rows),
+                                        "rows_out": n_groups, "preliminary_merges": 0})
+
+    # -- row-object compatibility path ------------------------------------------
+    def execute(self, rows):
+        """Aggregate an iterable of ``Row`` (key tuple, state tuple) and
+        return the sorted list of aggregated ``Row`` (sortagg.py:744-747)."""
+        torch = _torch()
+        rows = list(rows)
+        self.executed_steps = []
+        self.initial_plan = None
+        self.runs_after_generation = 0
+        if not rows:
+            return []
+        arity = self.schema.arity
+        nslots = self.schema.state_slots
+        key_cols = []
+        for j in range(arity):
+            col = [r.key[j] for r in rows]
+            key_cols.append(_int_column(col, f"key column {j}"))
+        state_cols = []
+        for s in range(nslots):
+            col = [r.state[s] for r in rows]
+            if any(isinstance(v, float) for v in col):
+                state_cols.append(np.asarray(col, dtype=np.float64))
+            else:
+                arr = _int_column(col, f"state slot {s}")
+                if arr.dtype != np.int64:
+                    raise InvalidInputError(f"state slot {s} does not fit int64")
+                state_cols.append(arr)
+        dev = torch.device("cuda", self._device_index())
+        keys_t = [torch.from_numpy(c).to(dev) for c in key_cols]
+        states_t = [torch.from_numpy(c).to(dev) for c in state_cols]
+        res = self.execute_columns(keys_t, states_t, states=True)
+        out_keys = [k.cpu().numpy() for k in res.keys]
+        out_states = [s.cpu().numpy() for s in res.states]
+        n = res.n_groups
+        key_lists = [_py_list(k) for k in out_keys]
+        state_lists = [_py_list(s) for s in out_states]
+        out = []
+        for i in range(n):
+            out.append(Row(tuple(kl[i] for kl in key_lists), tuple(sl[i] for sl in state_lists)))
+        return out
+
+
+def _int_column(values, what):
+    try:
+        return np.asarray(values, dtype=np.int64)
+    except (OverflowError, TypeError, ValueError):
+        pass
+    try:
+        arr = np.asarray(values, dtype=np.uint64)
+    except (OverflowError, TypeError, ValueError) as exc:
+        raise InvalidInputError(f"{what}: values must be integers in [-2^63, 2^64)") from exc
+    return arr
+
+
+def _py_list(arr):
+    if arr.dtype == np.uint64 or arr.dtype.kind in "iu":
+        return [int(v) for v in arr.tolist()]
+    return arr.tolist()
+
+
+def ctypes_stream(stream):
+    """cudaStream_t of a torch.cuda.Stream as an int (0 = legacy default)."""
+    return int(stream.cuda_stream) if stream is not None else 0

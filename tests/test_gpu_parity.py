@@ -1,0 +1,186 @@
+"""Parity of the CUDA path with the reference (golden fixtures) and the oracles.
+
+Bar: keys, counts, integer sums/min/max and distinct sets bit-exact; float
+sums within rel 1e-9 (float64 inputs) / 1e-5 (float32 inputs), the tolerance
+BASELINE.json's north star states.  Run-generation ledgers (fill cycles, run
+sizes, spilled rows) must equal the reference's.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import Golden, assert_slots_equal, golden_names
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import paper_2010_00152_b200 as isa  # noqa: E402
+from paper_2010_00152_b200 import workloads  # noqa: E402
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _check(res, want_keys, want_slots, rel=1e-9):
+    got_keys = [k.cpu().numpy() for k in res.keys]
+    got_slots = [s.cpu().numpy() for s in res.states]
+    assert len(got_keys[0]) == len(want_keys[0]), f"groups {len(got_keys[0])} != {len(want_keys[0])}"
+    for j, (g, w) in enumerate(zip(got_keys, want_keys)):
+        assert g.dtype == w.dtype, f"key {j} dtype"
+        assert np.array_equal(g, w), f"key column {j} differs"
+    for s, (g, w) in enumerate(zip(got_slots, want_slots)):
+        assert_slots_equal(g, w, rel=rel, what=f"slot {s}")
+
+
+def _cfg(memory, page, **kw):
+    return isa.SortAggConfig(memory_budget=memory, page_capacity=page, ovc_enabled=False, **kw)
+
+
+@pytest.mark.parametrize("name", golden_names())
+@pytest.mark.parametrize("variant", ["device", "host_input", "hbm_runs", "small_chunks"])
+def test_golden_columns(name, variant):
+    g = Golden(name)
+    sch = g.schema()
+    kw = {}
+    if variant == "hbm_runs":
+        kw["run_tier"] = "hbm"
+    if variant == "small_chunks":
+        kw.update(chunk_rows_max=5000, merge_window_rows=3000, window_rows=7000)
+    op = isa.SortAggregate(sch, _cfg(g.memory, g.page, **kw))
+    n = len(g.keys[0])
+    if variant == "host_input":
+        keys = [torch.from_numpy(np.ascontiguousarray(k)).pin_memory() for k in g.keys]
+        vals = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in g.values.items()}
+    else:
+        keys = [_cuda(k) for k in g.keys]
+        vals = {k: _cuda(v) for k, v in g.values.items()}
+    if n == 0:
+        res = op.execute_columns(keys, vals)
+        assert res.n_groups == 0
+        return
+    res = op.execute_columns(keys, vals)
+    if variant == "host_input":
+        assert res.keys[0].device.type == "cpu"
+    _check(res, g.out_keys, g.out_slots)
+    # run-generation ledger equals the reference's (exact read-sort-write)
+    assert op.cycles == [c for c in g.z["cycles"].tolist() if c > 0]
+    assert op.run_rows == g.z["run_rows"].tolist()
+    assert op.runs_after_generation == int(g.z["runs_after_generation"])
+    if g.single_wide:
+        assert op.ledger.rows_spilled == int(g.z["ledger_rows_spilled"])
+        assert op.ledger.rows_read_back == int(g.z["ledger_rows_read_back"])
+        assert op.ledger.pages_written == int(g.z["ledger_pages_written"])
+        assert op.ledger.pages_read == int(g.z["ledger_pages_read"])
+        assert op.ledger.merge_steps == int(g.z["ledger_merge_steps"])
+        assert op.ledger.merge_levels == int(g.z["ledger_merge_levels"])
+        if op.initial_plan is not None:
+            assert [s.kind for s in op.initial_plan.steps] == g.z["plan_kinds"].tolist()
+    else:
+        assert op.ledger.rows_spilled == int(g.z["run_rows"].sum())
+        assert [s.kind for s in op.initial_plan.steps] == g.z["plan_kinds"].tolist()
+    op.ledger.check_invariants()
+
+
+@pytest.mark.parametrize("name", ["e2e_3000_450_64_8", "edge_one_key", "edge_composite_signed", "cfg4_scaled",
+                                  "edge_single", "e2e_spill_once"])
+def test_golden_rows(name):
+    """Row-object compatibility path: execute(rows) -> list[Row] equal to the reference's."""
+    g = Golden(name)
+    sch = g.schema()
+    n = len(g.keys[0])
+    inputs = []
+    for n_, kind, col in g.aggs:
+        inputs.append(g.values[col].tolist() if col else [None] * n)
+    key_lists = [k.tolist() for k in g.keys]
+    rows = [isa.Row(tuple(kl[i] for kl in key_lists), sch.make_state(tuple(v[i] for v in inputs)) if g.aggs else ())
+            for i in range(n)]
+    op = isa.SortAggregate(sch, _cfg(g.memory, g.page))
+    out = op.execute(iter(rows))
+    assert len(out) == g.n_groups
+    want_keys = list(zip(*[k.tolist() for k in g.out_keys]))
+    assert [r.key for r in out] == want_keys
+    for s, col in enumerate(g.out_slots):
+        got = [r.state[s] for r in out]
+        if col.dtype.kind == "f":
+            np.testing.assert_allclose(got, col, rtol=1e-9)
+        else:
+            assert got == col.tolist()
+    assert all(out[i - 1].key < out[i].key for i in range(1, len(out)))
+
+
+def test_empty_rows():
+    sch = isa.Schema([isa.ColumnSpec("k")], [isa.AggregateSpec("n", isa.AggregateKind.COUNT)])
+    op = isa.SortAggregate(sch, _cfg(64, 8))
+    assert op.execute(iter([])) == []
+    assert op.ledger.rows_spilled == 0
+
+
+def _oracle_case(w, memory, page=100, rel=1e-9, **kw):
+    sch = w.schema
+    n = w.rows
+    keys_np = [k.cpu().numpy() for k in w.keys]
+    vals_np = {k: v.cpu().numpy() for k, v in w.values.items()}
+    slots = oracle.make_states(sch, vals_np, n)
+    want_keys, want_slots = oracle.reference_aggregate(keys_np, slots, oracle.slot_ops(sch))
+    op = isa.SortAggregate(sch, _cfg(memory, page, **kw))
+    res = op.execute_columns([k.cuda() for k in w.keys], {k: v.cuda() for k, v in w.values.items()})
+    _check(res, want_keys, want_slots, rel=rel)
+    return op
+
+
+@pytest.mark.parametrize("cfg,rows,memory", [
+    (1, 1_000_000, 4096),
+    (1, 3_000_000, 2048),
+    (2, 4_000_000, 4096),
+    (2, 3_000_000, 4),        # O = 6 > M = 4: spills every few rows
+    (3, 2_000_000, 1 << 16),
+    (3, 2_000_000, 1 << 22),  # no spill
+    (4, 2_000_000, 1 << 16),
+    (5, 3_000_000, 1 << 18),
+])
+def test_random_vs_oracle(cfg, rows, memory):
+    kw = {"domain": 1 << 20} if cfg in (3, 5) else {}
+    w = workloads.make(cfg, rows=rows, device="cpu", **kw)
+    rel = 1e-5 if cfg == 3 else 1e-9
+    _oracle_case(w, memory, rel=rel)
+
+
+def test_ledger_matches_c_oracle_mid_scale():
+    w = workloads.config5(rows=2_000_000, device="cpu", domain=1 << 19)
+    sch = w.schema
+    keys_np = [k.numpy() for k in w.keys]
+    slots = oracle.make_states(sch, {"v": w.values["v"].numpy()}, w.rows)
+    _, _, led, cycles = oracle.rsw_sortagg(keys_np, slots, oracle.slot_ops(sch), 1 << 15, 100)
+    op = _oracle_case(w, 1 << 15)
+    assert op.cycles == [c for c in cycles if c > 0]
+    assert op.ledger.rows_spilled == led["rows_spilled"]
+    assert op.runs_after_generation == led["runs"]
+
+
+def test_small_chunks_and_windows_vs_oracle():
+    w = workloads.config3(rows=1_500_000, device="cpu", domain=1 << 18)
+    _oracle_case(w, 1 << 14, rel=1e-5, chunk_rows_max=20_000, merge_window_rows=50_000)
+
+
+def test_full_scale_config2_properties():
+    """configs[1] at full size (2^28 rows): exactly the 6 groups, counts sum
+    to the input size, float sums match torch's float64 sums (order-free
+    property, rel 1e-9)."""
+    w = workloads.config2(device="cuda")
+    op = isa.SortAggregate(w.schema, _cfg(w.memory_budget, 100))
+    res = op.execute_columns(w.keys, w.values)
+    assert res.n_groups == 6
+    k1, k2 = [k.cpu().numpy() for k in res.keys]
+    assert list(zip(k1.tolist(), k2.tolist())) == [(a, b) for a in range(3) for b in range(2)]
+    counts = res.states[0]
+    assert int(counts.sum()) == w.rows
+    gid = w.keys[0].to(torch.int64) * 2 + w.keys[1].to(torch.int64)
+    want_counts = torch.bincount(gid, minlength=6)
+    assert torch.equal(counts.cpu(), want_counts.cpu())
+    for i in range(4):
+        want = torch.zeros(6, dtype=torch.float64, device="cuda").index_add_(0, gid, w.values[f"f{i}"])
+        np.testing.assert_allclose(res.states[1 + i].cpu().numpy(), want.cpu().numpy(), rtol=1e-9)
+    assert op.ledger.rows_spilled == 0

@@ -1,0 +1,84 @@
+"""The oracles, pinned against outputs of the reference itself (CPU only).
+
+Both restatements (numpy reference_aggregate, C read-sort-write + wide merge)
+must reproduce every golden fixture produced by running
+/root/reference/pkg/src/insortagg (tools/make_golden.py): keys and integer
+states bit-exact, float sums within rel 1e-9; the C restatement must also
+reproduce the run-generation ledger (fill cycles, run sizes, spilled rows).
+"""
+
+import numpy as np
+
+import oracle
+from conftest import assert_slots_equal
+
+
+def _inputs(golden):
+    sch = golden.schema()
+    n = len(golden.keys[0])
+    slots = oracle.make_states(sch, golden.values, n)
+    return sch, slots, oracle.slot_ops(sch)
+
+
+def test_fixture_inputs_unchanged(golden):
+    assert golden.input_sha() == str(golden.z["input_sha256"])
+
+
+def test_numpy_oracle_matches_reference(golden):
+    sch, slots, ops = _inputs(golden)
+    keys, states = oracle.reference_aggregate(golden.keys, slots, ops)
+    assert len(keys[0]) == golden.n_groups
+    for j, (g, w) in enumerate(zip(keys, golden.out_keys)):
+        assert np.array_equal(g, w), f"key column {j}"
+    for s, (g, w) in enumerate(zip(states, golden.out_slots)):
+        assert_slots_equal(g, w, what=f"slot {s}")
+
+
+def test_c_oracle_matches_reference(golden):
+    sch, slots, ops = _inputs(golden)
+    keys, states, ledger, cycles = oracle.rsw_sortagg(golden.keys, slots, ops, golden.memory, golden.page)
+    assert ledger["n_groups"] == golden.n_groups
+    for j, (g, w) in enumerate(zip(keys, golden.out_keys)):
+        assert np.array_equal(g, w), f"key column {j}"
+    for s, (g, w) in enumerate(zip(states, golden.out_slots)):
+        assert_slots_equal(g, w, what=f"slot {s}")
+    # run generation ledger: identical fill cycles and runs
+    assert [c for c in cycles if c > 0] == golden.z["cycles"].tolist()
+    assert ledger["runs"] == int(golden.z["runs_after_generation"])
+    assert ledger["runs"] == len(golden.z["run_rows"])
+    if golden.single_wide:
+        assert ledger["rows_spilled"] == int(golden.z["ledger_rows_spilled"])
+        assert ledger["pages_written"] == int(golden.z["ledger_pages_written"])
+        assert ledger["rows_read_back"] == int(golden.z["ledger_rows_read_back"])
+    else:
+        # the reference adds traditional merge levels; run generation alone matches
+        assert ledger["rows_spilled"] == int(golden.z["run_rows"].sum())
+
+
+def test_c_oracle_multithread_same_output(golden):
+    sch, slots, ops = _inputs(golden)
+    if len(golden.keys[0]) == 0:
+        return
+    sp = oracle.range_splitters(golden.keys, 4)
+    keys, states, _, _ = oracle.rsw_sortagg(golden.keys, slots, ops, golden.memory, golden.page, nthreads=4,
+                                            splitters=sp)
+    for g, w in zip(keys, golden.out_keys):
+        assert np.array_equal(g, w)
+    for g, w in zip(states, golden.out_slots):
+        assert_slots_equal(g, w)
+
+
+def test_key_normalization_round_trip():
+    rng = np.random.default_rng(3)
+    cols = [rng.integers(-128, 127, 1000).astype(np.int8), rng.integers(0, 2**16, 1000).astype(np.uint16),
+            rng.integers(-(2**62), 2**62, 1000)]
+    hi, lo = oracle.normalize_keys(cols)
+    back = oracle.denormalize_keys(hi, lo, [c.dtype for c in cols])
+    for a, b in zip(cols, back):
+        assert np.array_equal(a, b)
+    # order of the normalized image == lexicographic tuple order
+    order_norm = np.lexsort((lo, hi))
+    order_tuple = np.lexsort(tuple(reversed(cols)))
+    keys_norm = list(zip(*(c[order_norm] for c in cols)))
+    keys_tuple = list(zip(*(c[order_tuple] for c in cols)))
+    assert keys_norm == keys_tuple
