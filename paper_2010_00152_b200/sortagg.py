@@ -536,7 +536,10 @@ class SortAggregate:
         key_cols = []
         for j in range(arity):
             col = [r.key[j] for r in rows]
-            key_cols.append(_int_column(col, f"key column {j}"))
+            key_cols.append(_narrow(_int_column(col, f"key column {j}")))
+        if sum(c.dtype.itemsize * 8 for c in key_cols) > 128:
+            raise InvalidInputError("composite key values need more than 128 bits; "
+                                    "the B200 operator supports keys up to 128 bits")
         state_cols = []
         for s in range(nslots):
             col = [r.state[s] for r in rows]
@@ -571,6 +574,22 @@ def _int_column(values, what):
         arr = np.asarray(values, dtype=np.uint64)
     except (OverflowError, TypeError, ValueError) as exc:
         raise InvalidInputError(f"{what}: values must be integers in [-2^63, 2^64)") from exc
+    return arr
+
+
+def _narrow(arr):
+    """Smallest integer dtype holding every value (order preserving): keeps
+    composite Row keys within the 128-bit normalized key."""
+    if arr.size == 0:
+        return arr
+    lo, hi = int(arr.min()), int(arr.max())
+    if lo >= 0:
+        for dt in (np.uint8, np.uint16, np.uint32, np.uint64):
+            if hi <= np.iinfo(dt).max:
+                return arr.astype(dt)
+    for dt in (np.int8, np.int16, np.int32, np.int64):
+        if np.iinfo(dt).min <= lo and hi <= np.iinfo(dt).max:
+            return arr.astype(dt)
     return arr
 
 

@@ -145,7 +145,7 @@ def test_random_vs_oracle(cfg, rows, memory):
     kw = {"domain": 1 << 20} if cfg in (3, 5) else {}
     w = workloads.make(cfg, rows=rows, device="cpu", **kw)
     rel = 1e-5 if cfg == 3 else 1e-9
-    _oracle_case(w, memory, rel=rel)
+    _oracle_case(w, memory, page=min(100, memory // 2), rel=rel)
 
 
 def test_ledger_matches_c_oracle_mid_scale():
