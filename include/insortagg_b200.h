@@ -22,6 +22,7 @@
  *   isa_cycles        OutputEstimator.note_cycle inputs sortagg.py:116-118, 345
  *   isa_run_rows      RunMeta.row_count per run        runstore.py:145-154
  *   isa_last_error    the EngineError message          core.py:15-40
+ *   isa_phase_stats / isa_launch_count   (new: device-time accounting)
  *   isa_sample_keys / isa_partition    (new: multi-GPU range partitioning;
  *                     no reference function)
  *
@@ -122,6 +123,27 @@ typedef struct isa_ledger {
   double ms_wide_merge;
 } isa_ledger;
 
+/* device-time breakdown of the last execute (CUDA events on the caller's stream) */
+enum isa_phase_id {
+  ISA_PH_ABSORB = 0,       /* tiny-table absorb kernel (rows probed, bytes read) */
+  ISA_PH_SORT = 1,         /* key build + LSD radix sort of a chunk */
+  ISA_PH_FLUSH = 2,        /* new-key bitmap + k-th select (flush point) */
+  ISA_PH_COLLAPSE = 3,     /* segmented reduce of a sorted chunk */
+  ISA_PH_TABLE_MERGE = 4,  /* merge_combine(T, U) */
+  ISA_PH_WM_SORT = 5,      /* wide merge: window radix sort */
+  ISA_PH_WM_COLLAPSE = 6,  /* wide merge: window collapse + append */
+  ISA_PH_RUN_GEN = 7,      /* run generation total */
+  ISA_PH_WIDE_MERGE = 8,   /* wide merge total */
+  ISA_PH_COUNT = 9
+};
+
+typedef struct isa_phase {
+  double ms;        /* summed device time */
+  int64_t calls;    /* timed intervals (for ISA_PH_ABSORB: kernel launches) */
+  int64_t rows;     /* rows processed */
+  int64_t bytes;    /* algorithmic bytes (input read + output written) */
+} isa_phase;
+
 typedef struct isa_handle isa_handle;
 
 /* library version string */
@@ -153,6 +175,10 @@ ISA_API int64_t isa_cycles(isa_handle* h, int64_t* out, int64_t cap);
 /* Row counts of the runs of the last execute. */
 ISA_API int64_t isa_run_rows(isa_handle* h, int64_t* out, int64_t cap);
 ISA_API const char* isa_last_error(isa_handle* h);
+/* Per-phase device times of the last execute; returns ISA_PH_COUNT. */
+ISA_API int isa_phase_stats(isa_handle* h, isa_phase* out, int cap);
+/* Kernels launched by this library so far in the process. */
+ISA_API int64_t isa_launch_count(void);
 
 /* --- multi-GPU range partitioning primitives -------------------------- */
 /* Normalized (order-preserving, 128-bit) keys of rows 0, stride, 2*stride, ...

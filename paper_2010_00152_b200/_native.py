@@ -47,8 +47,16 @@ _STATUS_ERRORS = {
 EXPORTED_SYMBOLS = (
     "isa_version", "isa_create", "isa_destroy", "isa_execute", "isa_result_copy",
     "isa_metrics", "isa_cycles", "isa_run_rows", "isa_last_error",
-    "isa_sample_keys", "isa_partition",
+    "isa_sample_keys", "isa_partition", "isa_phase_stats", "isa_launch_count",
 )
+
+PHASES = ("absorb", "sort", "flush", "collapse", "table_merge", "wm_sort", "wm_collapse",
+          "run_generation", "wide_merge")
+
+
+class IsaPhase(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_double), ("calls", ctypes.c_int64), ("rows", ctypes.c_int64),
+                ("bytes", ctypes.c_int64)]
 
 
 class IsaConfig(ctypes.Structure):
@@ -133,6 +141,10 @@ def load():
     lib.isa_run_rows.argtypes = [vp, i64p, ctypes.c_int64]
     lib.isa_last_error.restype = ctypes.c_char_p
     lib.isa_last_error.argtypes = [vp]
+    lib.isa_phase_stats.restype = ctypes.c_int
+    lib.isa_phase_stats.argtypes = [vp, ctypes.POINTER(IsaPhase), ctypes.c_int]
+    lib.isa_launch_count.restype = ctypes.c_int64
+    lib.isa_launch_count.argtypes = []
     lib.isa_sample_keys.restype = ctypes.c_int
     lib.isa_sample_keys.argtypes = [vp, ctypes.c_int64, pp, ctypes.c_int64, vp, vp, vp]
     lib.isa_partition.restype = ctypes.c_int
@@ -143,6 +155,11 @@ def load():
 
 def version():
     return load().isa_version().decode()
+
+
+def launch_count():
+    """Kernels launched by libinsortagg_b200 so far in this process."""
+    return int(load().isa_launch_count())
 
 
 def _ptr_array(ptrs):
@@ -200,6 +217,12 @@ class Handle:
         buf = (ctypes.c_int64 * max(1, n))()
         self._lib.isa_cycles(self._h, buf, n)
         return [buf[i] for i in range(n)]
+
+    def phase_stats(self):
+        arr = (IsaPhase * len(PHASES))()
+        self._lib.isa_phase_stats(self._h, arr, len(PHASES))
+        return {name: {"ms": arr[i].ms, "calls": arr[i].calls, "rows": arr[i].rows, "bytes": arr[i].bytes}
+                for i, name in enumerate(PHASES)}
 
     def run_rows(self):
         n = self._lib.isa_run_rows(self._h, None, 0)

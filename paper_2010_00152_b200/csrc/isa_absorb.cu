@@ -21,17 +21,75 @@ namespace isa {
 
 enum { CLS_ADD_I = 0, CLS_ADD_F = 1, CLS_MIN_I = 2, CLS_MAX_I = 3, CLS_MIN_F = 4, CLS_MAX_F = 5 };
 
-template <int NT, typename T, typename F>
-__device__ __forceinline__ void ab_reduce_rows(const u32 (&hit)[AB_ROWS], const u64 (&v)[AB_ROWS], T ident, F f,
-                                               T (&t)[NT]) {
+// Load one column for the AB_ROWS rows of this thread's batch: one dtype
+// switch per (batch, column), then an unrolled, coalesced load per row.
+template <typename T>
+__device__ __forceinline__ void ab_load_col(const void* p, i64 base, u32 lim, T (&out)[AB_ROWS]) {
+  const T* q = (const T*)p + base;
 #pragma unroll
-  for (int j = 0; j < NT; ++j) t[j] = ident;
+  for (int k = 0; k < AB_ROWS; ++k) out[k] = ((u32)(k * AB_THREADS) < lim) ? __ldg(q + k * AB_THREADS) : T(0);
+}
+
+// Key field (order-preserving unsigned image) of every row of the batch.
+__device__ __forceinline__ void ab_key_field(int dt, const void* p, i64 base, u32 lim, u64 (&f)[AB_ROWS]) {
+  switch (dt) {
+    case DT_U8: case DT_I8: {
+      unsigned char t[AB_ROWS]; ab_load_col(p, base, lim, t);
+      const u64 x = dt == DT_I8 ? 0x80ull : 0;
 #pragma unroll
-  for (int k = 0; k < AB_ROWS; ++k) {
-    const T x = *reinterpret_cast<const T*>(&v[k]);
+      for (int k = 0; k < AB_ROWS; ++k) f[k] = (u64)t[k] ^ x;
+    } break;
+    case DT_U16: case DT_I16: {
+      unsigned short t[AB_ROWS]; ab_load_col(p, base, lim, t);
+      const u64 x = dt == DT_I16 ? 0x8000ull : 0;
 #pragma unroll
-    for (int j = 0; j < NT; ++j)
-      if (hit[k] == (u32)j) t[j] = f(t[j], x);
+      for (int k = 0; k < AB_ROWS; ++k) f[k] = (u64)t[k] ^ x;
+    } break;
+    case DT_U32: case DT_I32: {
+      unsigned int t[AB_ROWS]; ab_load_col(p, base, lim, t);
+      const u64 x = dt == DT_I32 ? 0x80000000ull : 0;
+#pragma unroll
+      for (int k = 0; k < AB_ROWS; ++k) f[k] = (u64)t[k] ^ x;
+    } break;
+    default: {
+      unsigned long long t[AB_ROWS]; ab_load_col(p, base, lim, t);
+      const u64 x = dt == DT_I64 ? 0x8000000000000000ull : 0;
+#pragma unroll
+      for (int k = 0; k < AB_ROWS; ++k) f[k] = (u64)t[k] ^ x;
+    } break;
+  }
+}
+
+// make_state value of every row of the batch as 8-byte slot bits.
+__device__ __forceinline__ void ab_slot_values(int src, int ty, int dt, const void* p, i64 base, u32 lim,
+                                               u64 (&v)[AB_ROWS]) {
+  if (src == SRC_ONE) {
+    const u64 one = ty == ST_F64 ? 0x3FF0000000000000ull : 1ull;
+#pragma unroll
+    for (int k = 0; k < AB_ROWS; ++k) v[k] = one;
+    return;
+  }
+  switch (dt) {
+    case DT_F64: { unsigned long long t[AB_ROWS]; ab_load_col(p, base, lim, t);
+#pragma unroll
+      for (int k = 0; k < AB_ROWS; ++k) v[k] = t[k]; } break;
+    case DT_F32: { float t[AB_ROWS]; ab_load_col(p, base, lim, t);
+#pragma unroll
+      for (int k = 0; k < AB_ROWS; ++k) v[k] = d2u((double)t[k]); } break;
+    case DT_I64: case DT_U64: { unsigned long long t[AB_ROWS]; ab_load_col(p, base, lim, t);
+#pragma unroll
+      for (int k = 0; k < AB_ROWS; ++k) v[k] = ty == ST_F64 ? d2u(dt == DT_I64 ? (double)(long long)t[k] : (double)t[k]) : t[k]; } break;
+    case DT_I32: { int t[AB_ROWS]; ab_load_col(p, base, lim, t);
+#pragma unroll
+      for (int k = 0; k < AB_ROWS; ++k) v[k] = ty == ST_F64 ? d2u((double)t[k]) : (u64)(i64)t[k]; } break;
+    case DT_U32: { unsigned int t[AB_ROWS]; ab_load_col(p, base, lim, t);
+#pragma unroll
+      for (int k = 0; k < AB_ROWS; ++k) v[k] = ty == ST_F64 ? d2u((double)t[k]) : (u64)t[k]; } break;
+    default: {   // 8/16-bit integer columns: rare, per-row generic path
+#pragma unroll
+      for (int k = 0; k < AB_ROWS; ++k)
+        v[k] = ((u32)(k * AB_THREADS) < lim) ? load_slot_value(src, ty, dt, p, base + k * AB_THREADS) : 0;
+    } break;
   }
 }
 
@@ -40,86 +98,73 @@ __global__ void __launch_bounds__(AB_THREADS) k_absorb_tiny(KeyDesc kd, SlotDesc
                                                            TinyTable tt, u32 rows_per_cta,
                                                            u64* __restrict__ partials, u32* __restrict__ miss_buf,
                                                            u32* __restrict__ miss_cnt) {
-  extern __shared__ __align__(16) u64 sacc[];   // [S][NT][AB_THREADS]
+  // Per-thread accumulators sacc[s][j][tid]: the address of (slot s, table
+  // row j) for thread tid is ((s*NT + j) * AB_THREADS + tid) * 8 bytes, so a
+  // warp's 32 accesses hit 32 consecutive 8-byte words whatever rows its
+  // lanes matched: conflict-free, and the cost per row does not grow with NT.
+  extern __shared__ __align__(16) u64 sacc[];
   __shared__ u32 sw[8];
   const int S = sd.nslots;
   const int tid = threadIdx.x;
   const u32 c = blockIdx.x;
   const u32 r0 = c * rows_per_cta;
   const u32 r1 = min(r0 + rows_per_cta, n);
-  int cls[ISA_MAX_SLOTS];
-  for (int s = 0; s < S; ++s) {
-    const int op = sd.op[s], ty = sd.type[s];
-    cls[s] = op == OP_ADD ? (ty == ST_F64 ? CLS_ADD_F : CLS_ADD_I)
-                          : (op == OP_MIN ? (ty == ST_F64 ? CLS_MIN_F : CLS_MIN_I) : (ty == ST_F64 ? CLS_MAX_F : CLS_MAX_I));
-    for (int j = 0; j < NT; ++j) sacc[(s * NT + j) * AB_THREADS + tid] = identity_slot(op, ty);
-  }
+  for (int s = 0; s < S; ++s)
+    for (int j = 0; j < NT; ++j) sacc[(s * NT + j) * AB_THREADS + tid] = identity_slot(sd.op[s], sd.type[s]);
 
   u32 nmiss = 0;
   for (u32 base = r0; base < r1; base += AB_THREADS * AB_ROWS) {
-    u32 hit[AB_ROWS];   // table row, NT = miss, 0xFF = past the end
+    const u32 row_t = base + tid;                       // this thread's first row of the batch
+    const u32 lim = r1 > row_t ? r1 - row_t : 0;        // rows k*AB_THREADS < lim are valid
+    u64 kl[AB_ROWS], kh[AB_ROWS];
+#pragma unroll
+    for (int k = 0; k < AB_ROWS; ++k) { kl[k] = 0; kh[k] = 0; }
+    for (int col = 0; col < kd.ncols; ++col) {
+      u64 f[AB_ROWS];
+      ab_key_field(kd.dtype[col], kd.ptr[col], row0 + row_t, lim, f);
+      const int s = kd.shift[col], wdt = kd.width[col];
+#pragma unroll
+      for (int k = 0; k < AB_ROWS; ++k) {
+        if (s < 64) {
+          kl[k] |= f[k] << s;
+          if (KW == 2 && s > 0 && s + wdt > 64) kh[k] |= f[k] >> (64 - s);
+        } else if (KW == 2) {
+          kh[k] |= f[k] << (s - 64);
+        }
+      }
+    }
+    u32 hit[AB_ROWS];   // table row; NT = miss; 0xFF = past the end
     bool anymiss = false;
 #pragma unroll
     for (int k = 0; k < AB_ROWS; ++k) {
-      const u32 row = base + k * AB_THREADS + tid;
-      hit[k] = 0xFFu;
-      if (row < r1) {
-        u64 h, l;
-        load_key(kd, row0 + row, h, l);
-        u32 hk = NT;
+      u32 hk = NT;
 #pragma unroll
-        for (int j = 0; j < NT; ++j)
-          if (key_eq<KW>(h, l, tt.hi[j], tt.lo[j])) hk = j;
-        hit[k] = hk;
-        anymiss |= (hk == NT);
-      }
+      for (int j = 0; j < NT; ++j) hk = key_eq<KW>(kh[k], kl[k], tt.hi[j], tt.lo[j]) ? (u32)j : hk;
+      if ((u32)(k * AB_THREADS) >= lim) hk = 0xFFu;
+      anymiss |= (hk == (u32)NT);
+      hit[k] = hk;
     }
     for (int s = 0; s < S; ++s) {
-      const int src = sd.src[s], ty = sd.type[s], dt = sd.dtype[s];
-      const void* p = sd.ptr[s];
+      const int op = sd.op[s], ty = sd.type[s];
       u64 v[AB_ROWS];
-#pragma unroll
-      for (int k = 0; k < AB_ROWS; ++k)
-        v[k] = (hit[k] < (u32)NT) ? load_slot_value(src, ty, dt, p, row0 + base + k * AB_THREADS + tid) : 0;
+      ab_slot_values(sd.src[s], ty, sd.dtype[s], sd.ptr[s], row0 + row_t, lim, v);
       u64* acc = sacc + (size_t)s * NT * AB_THREADS + tid;
-      switch (cls[s]) {
-        case CLS_ADD_F: {
-          double t[NT];
-          ab_reduce_rows<NT>(hit, v, 0.0, [](double a, double b) { return a + b; }, t);
-#pragma unroll
-          for (int j = 0; j < NT; ++j) acc[j * AB_THREADS] = d2u(u2d(acc[j * AB_THREADS]) + t[j]);
-        } break;
-        case CLS_ADD_I: {
-          long long t[NT];
-          ab_reduce_rows<NT>(hit, v, 0ll, [](long long a, long long b) { return (long long)((u64)a + (u64)b); }, t);
-#pragma unroll
-          for (int j = 0; j < NT; ++j) acc[j * AB_THREADS] = acc[j * AB_THREADS] + (u64)t[j];
-        } break;
-        case CLS_MIN_I: {
-          long long t[NT];
-          ab_reduce_rows<NT>(hit, v, 0x7FFFFFFFFFFFFFFFll, [](long long a, long long b) { return a <= b ? a : b; }, t);
-#pragma unroll
-          for (int j = 0; j < NT; ++j) acc[j * AB_THREADS] = combine_slot(OP_MIN, ST_I64, acc[j * AB_THREADS], (u64)t[j]);
-        } break;
-        case CLS_MAX_I: {
-          long long t[NT];
-          ab_reduce_rows<NT>(hit, v, (long long)0x8000000000000000ull, [](long long a, long long b) { return a >= b ? a : b; }, t);
-#pragma unroll
-          for (int j = 0; j < NT; ++j) acc[j * AB_THREADS] = combine_slot(OP_MAX, ST_I64, acc[j * AB_THREADS], (u64)t[j]);
-        } break;
-        case CLS_MIN_F: {
-          double t[NT];
-          ab_reduce_rows<NT>(hit, v, __longlong_as_double(0x7FF0000000000000ll), [](double a, double b) { return a <= b ? a : b; }, t);
-#pragma unroll
-          for (int j = 0; j < NT; ++j) acc[j * AB_THREADS] = combine_slot(OP_MIN, ST_F64, acc[j * AB_THREADS], d2u(t[j]));
-        } break;
-        default: {
-          double t[NT];
-          ab_reduce_rows<NT>(hit, v, __longlong_as_double((long long)0xFFF0000000000000ull), [](double a, double b) { return a >= b ? a : b; }, t);
-#pragma unroll
-          for (int j = 0; j < NT; ++j) acc[j * AB_THREADS] = combine_slot(OP_MAX, ST_F64, acc[j * AB_THREADS], d2u(t[j]));
-        } break;
+      const int cls = op == OP_ADD ? (ty == ST_F64 ? CLS_ADD_F : CLS_ADD_I)
+                                   : (op == OP_MIN ? (ty == ST_F64 ? CLS_MIN_F : CLS_MIN_I)
+                                                   : (ty == ST_F64 ? CLS_MAX_F : CLS_MAX_I));
+#define AB_LOOP(STMT)                                                   \
+  _Pragma("unroll") for (int k = 0; k < AB_ROWS; ++k) {                 \
+    if (hit[k] < (u32)NT) { u64* a = acc + hit[k] * AB_THREADS; STMT; } \
+  }
+      switch (cls) {
+        case CLS_ADD_F: AB_LOOP(*a = d2u(u2d(*a) + u2d(v[k]))) break;
+        case CLS_ADD_I: AB_LOOP(*a = *a + v[k]) break;
+        case CLS_MIN_I: AB_LOOP(*a = combine_slot(OP_MIN, ST_I64, *a, v[k])) break;
+        case CLS_MAX_I: AB_LOOP(*a = combine_slot(OP_MAX, ST_I64, *a, v[k])) break;
+        case CLS_MIN_F: AB_LOOP(*a = combine_slot(OP_MIN, ST_F64, *a, v[k])) break;
+        default: AB_LOOP(*a = combine_slot(OP_MAX, ST_F64, *a, v[k])) break;
       }
+#undef AB_LOOP
     }
     // ordered miss compaction (row order = (k, tid) within this step)
     if (__syncthreads_or(anymiss)) {
@@ -170,7 +215,7 @@ static void absorb_launch(const KeyDesc& kd, const SlotDesc& sd, int64_t row0, u
                          AB_MAX_CELLS * AB_THREADS * 8);
     attr = true;
   }
-  k_absorb_tiny<KW, NT><<<grid, AB_THREADS, smem, st>>>(kd, sd, row0, n, tt, rpc, partials, miss_buf, miss_cnt);
+  klaunch(k_absorb_tiny<KW, NT>, grid, AB_THREADS, smem, st, kd, sd, row0, n, tt, rpc, partials, miss_buf, miss_cnt);
 }
 
 template <int KW>

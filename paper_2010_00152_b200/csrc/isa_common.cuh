@@ -12,8 +12,22 @@
 // combine op (ADD/MIN/MAX, core.py:184-208) and an accumulator type (int64,
 // exact like Python ints within 2^63; or float64 like Python floats).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
+
+namespace isa {
+// number of kernels this library has launched (process-wide)
+extern std::atomic<long long> g_launches;
+}
+
+// Every kernel launch of the library goes through klaunch so that the
+// operator can report exactly how many of its kernels ran.
+template <typename... KArgs, typename... Args>
+inline void klaunch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  k<<<grid, block, smem, st>>>(static_cast<KArgs>(args)...);
+  isa::g_launches.fetch_add(1, std::memory_order_relaxed);
+}
 
 typedef uint64_t u64;
 typedef int64_t i64;

@@ -183,6 +183,43 @@ struct Engine {
   // host input windows
   Window win[2];
   // accounting
+  struct PhaseRec { int ph; cudaEvent_t a, b; int64_t rows, bytes; };
+  std::vector<PhaseRec> recs;
+  std::vector<cudaEvent_t> ev_pool;
+  isa_phase phases[ISA_PH_COUNT];
+  int open_ph[ISA_PH_COUNT];
+  cudaEvent_t ev_get() {
+    if (!ev_pool.empty()) { cudaEvent_t e = ev_pool.back(); ev_pool.pop_back(); return e; }
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+  }
+  void ph_begin(int ph) {
+    PhaseRec r{ph, ev_get(), ev_get(), 0, 0};
+    CK(cudaEventRecord(r.a, st));
+    open_ph[ph] = (int)recs.size();
+    recs.push_back(r);
+  }
+  void ph_end(int ph, int64_t rows = 0, int64_t bytes = 0) {
+    PhaseRec& r = recs[open_ph[ph]];
+    r.rows = rows;
+    r.bytes = bytes;
+    CK(cudaEventRecord(r.b, st));
+  }
+  void ph_collect() {   // after the stream is synchronized
+    for (auto& r : recs) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, r.a, r.b));
+      phases[r.ph].ms += ms;
+      phases[r.ph].calls += 1;
+      phases[r.ph].rows += r.rows;
+      phases[r.ph].bytes += r.bytes;
+      ev_pool.push_back(r.a);
+      ev_pool.push_back(r.b);
+    }
+    recs.clear();
+  }
+  int64_t absorb_row_bytes = 0;   // algorithmic bytes read per absorbed row
   isa_ledger led;
   std::vector<int64_t> cycles;
   int64_t launches = 0;
@@ -214,6 +251,8 @@ struct Engine {
                       &runref_dev, &bounds_lo, &bounds_hi, &bounds_out, &out_tmp};
     for (auto* b : bufs) b->release();
     for (auto& w : win) { for (auto& b : w.keys) b.release(); for (auto& b : w.vals) b.release(); }
+    for (auto& r : recs) { ev_pool.push_back(r.a); ev_pool.push_back(r.b); }
+    for (auto e : ev_pool) cudaEventDestroy(e);
     T.release(); U.release(); Tn.release(); result.release();
     pinned.release();
     devpool.release();
@@ -286,6 +325,13 @@ struct Engine {
         sd0.dtype[s] = dt;
       }
     }
+    absorb_row_bytes = key_bits / 8;
+    bool used[ISA_MAX_VAL_COLS] = {false};
+    for (int s = 0; s < S; ++s)
+      if (sd0.src[s] == SRC_COL && !used[sch.slot_col[s]]) {
+        used[sch.slot_col[s]] = true;
+        absorb_row_bytes += dtype_bits(sd0.dtype[s]) / 8;
+      }
   }
 
   // ------------------------------------------------------------ helpers --
@@ -337,10 +383,12 @@ struct Engine {
   // i < m.  Returns the buffer index holding the sorted result.
   int sort_rows(const KeyDesc& kd, int64_t row0, const u32* pos, u32 m) {
     ensure_sort(m);
+    ph_begin(ISA_PH_SORT);
     CK(cudaMemsetAsync(dvary(), 0, 2 * sizeof(u64), st));
     build_keys(KW, kd, row0, pos, m, s_lo[0].as<u64>(), s_hi[0].as<u64>(), s_val[0].as<u32>(), dvary(), st);
-    launches += 1;
-    return sort_built(m);
+    int cur = sort_built(m);
+    ph_end(ISA_PH_SORT, m, 0);
+    return cur;
   }
   int sort_built(u32 m) {
     CK(cudaMemcpyAsync(h_scal, dvary(), 2 * sizeof(u64), cudaMemcpyDeviceToHost, st));
@@ -356,7 +404,7 @@ struct Engine {
     for (int i = 0; i < 2; ++i) { b.lo[i] = s_lo[i].as<u64>(); b.hi[i] = s_hi[i].as<u64>(); b.val[i] = s_val[i].as<u32>(); }
     b.tile_hist = tile_hist.as<u32>();
     b.scan_tmp = scan_tmp.as<u32>();
-    return radix_sort_pairs(KW, b, m, lb, hb + 1, st, &launches);
+    return radix_sort_pairs(KW, b, m, lb, hb + 1, st, nullptr);
   }
 
   // Flush analysis on a sorted chunk of `span` rows: number of keys absent
@@ -366,19 +414,25 @@ struct Engine {
     bitmap.ensure((size_t)nw * 4 + 4);
     word_tmp.ensure((size_t)nw * 4 + 4);
     scan_tmp.ensure((scan_tmp_words(nw + 1) + 64) * 4);
+    ph_begin(ISA_PH_FLUSH);
     CK(cudaMemsetAsync(bitmap.p, 0, (size_t)nw * 4, st));
     CK(cudaMemsetAsync(dscal32(0), 0, sizeof(u32), st));
     new_heads(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, T.plo(), T.phi(), T.n,
               bitmap.as<u32>(), dscal32(0), st);
-    launches += 1;
-    u32 n_new = read_u32(dscal32(0));
+    CK(cudaMemcpyAsync(h_scal, dscal32(0), sizeof(u32), cudaMemcpyDeviceToHost, st));
+    ph_end(ISA_PH_FLUSH, m, 0);
+    sync();
+    u32 n_new = h_scal[0];
     const int64_t M = cfg.memory_budget;
     last_new = n_new;
     if ((int64_t)T.n + n_new <= M) return span;
     u32 k = (u32)(M - (int64_t)T.n + 1);
+    ph_begin(ISA_PH_FLUSH);
     select_kth_bit(bitmap.as<u32>(), span, k, word_tmp.as<u32>(), scan_tmp.as<u32>(), dscal32(1), st);
-    launches += 5;
-    return read_u32(dscal32(1));
+    CK(cudaMemcpyAsync(h_scal, dscal32(1), sizeof(u32), cudaMemcpyDeviceToHost, st));
+    ph_end(ISA_PH_FLUSH, 0, 0);
+    sync();
+    return h_scal[0];
   }
   u32 last_new = 0;
   bool tn_busy = false;
@@ -394,10 +448,14 @@ struct Engine {
     ct.partial = cl_partial.as<u64>();
     ct.partial_slot = cl_pslot.as<u32>();
     ct.total = dscal32(2);
+    const int phc = st_in ? ISA_PH_WM_COLLAPSE : ISA_PH_COLLAPSE;
+    ph_begin(phc);
     collapse(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, limit, sd, row0, st_in,
              out.plo(), out.phi(), out.pst(), ct, st);
-    launches += 6;
-    out.n = read_u32(dscal32(2));
+    CK(cudaMemcpyAsync(h_scal, dscal32(2), sizeof(u32), cudaMemcpyDeviceToHost, st));
+    ph_end(phc, m, 0);
+    sync();
+    out.n = h_scal[0];
   }
 
   // Tn <- merge_combine(T, U); swap into T
@@ -415,10 +473,13 @@ struct Engine {
     mt.rank_b = mg_rank_b.as<u32>(); mt.match_b = mg_match_b.as<u32>();
     mt.scan_tmp = scan_tmp.as<u32>();
     mt.total = dscal32(4);
+    ph_begin(ISA_PH_TABLE_MERGE);
     merge_combine(KW, S, ops, types, T.plo(), T.phi(), T.pst(), T.n, U.plo(), U.phi(), U.pst(), U.n, Tn.plo(),
                   Tn.phi(), Tn.pst(), mt, st);
-    launches += 12;
-    u32 matches = read_u32(dscal32(4));
+    CK(cudaMemcpyAsync(h_scal, dscal32(4), sizeof(u32), cudaMemcpyDeviceToHost, st));
+    ph_end(ISA_PH_TABLE_MERGE, (int64_t)T.n + U.n, 0);
+    sync();
+    u32 matches = h_scal[0];
     Tn.n = T.n + U.n - matches;
     std::swap(T, Tn);
     Tn.n = 0;
@@ -516,28 +577,25 @@ struct Engine {
     ab_miss_cnt.ensure((size_t)(grid + 1) * 4);
     ab_miss_off.ensure((size_t)(grid + 1) * 4);
     scan_tmp.ensure((scan_tmp_words(grid + 1) + 64) * 4);
+    ph_begin(ISA_PH_ABSORB);
     absorb_tiny(KW, nt, kd, sd, row0, span, tiny, grid, rpc, ab_partials.as<u64>(), ab_miss_buf.as<u32>(),
                 ab_miss_cnt.as<u32>(), st);
-    launches += 1;
+    ph_end(ISA_PH_ABSORB, span, (int64_t)span * absorb_row_bytes);
     CK(cudaMemcpyAsync(ab_miss_off.p, ab_miss_cnt.p, (size_t)grid * 4, cudaMemcpyDeviceToDevice, st));
     scan_exclusive_u32(ab_miss_off.as<u32>(), grid, scan_tmp.as<u32>(), dscal32(3), st);
-    launches += 3;
     u32 nmiss = read_u32(dscal32(3));
     if (nmiss == 0) {
       fold_partials(nt, sd, ab_partials.as<u64>(), grid, T.pst(), st);
-      launches += 1;
       last_new = 0;
       return a + span;
     }
     miss_list.ensure((size_t)nmiss * 4 + 64);
     compact_misses(ab_miss_buf.as<u32>(), ab_miss_cnt.as<u32>(), ab_miss_off.as<u32>(), grid, rpc,
                    miss_list.as<u32>(), st);
-    launches += 1;
     int cur = sort_rows(kd, row0, miss_list.as<u32>(), nmiss);
     u32 f = flush_point(cur, nmiss, span);
     if (f >= span) {
       fold_partials(nt, sd, ab_partials.as<u64>(), grid, T.pst(), st);
-      launches += 1;
       collapse_chunk(cur, nmiss, span, sd, row0, nullptr, U, std::min<int64_t>(nmiss, cfg.memory_budget));
       merge_into_T();
       refresh_tiny();
@@ -551,10 +609,11 @@ struct Engine {
       ab_partials.ensure((size_t)g2 * nt * std::max(S, 1) * 8 + 64);
       ab_miss_buf.ensure((size_t)g2 * r2 * 4 + 64);
       ab_miss_cnt.ensure((size_t)(g2 + 1) * 4);
+      ph_begin(ISA_PH_ABSORB);
       absorb_tiny(KW, nt, kd, sd, row0, f, tiny, g2, r2, ab_partials.as<u64>(), ab_miss_buf.as<u32>(),
                   ab_miss_cnt.as<u32>(), st);
+      ph_end(ISA_PH_ABSORB, f, (int64_t)f * absorb_row_bytes);
       fold_partials(nt, sd, ab_partials.as<u64>(), g2, T.pst(), st);
-      launches += 2;
     }
     collapse_chunk(cur, nmiss, f, sd, row0, nullptr, U, std::min<int64_t>(nmiss, cfg.memory_budget));
     merge_into_T();
@@ -664,7 +723,6 @@ struct Engine {
       CK(cudaMemcpyAsync(bounds_hi.p, bhi.data(), 8 * nb, cudaMemcpyHostToDevice, st));
       run_lower_bounds(KW, runref_dev.as<RunRef>(), k, bounds_lo.as<u64>(), bounds_hi.as<u64>(), nb,
                        bounds_out.as<u32>(), st);
-      launches += 1;
       CK(cudaMemcpyAsync(lb.data(), bounds_out.p, 4 * (size_t)k * nb, cudaMemcpyDeviceToHost, st));
       sync();
     }
@@ -719,10 +777,11 @@ struct Engine {
       CK(cudaMemcpyAsync(s_lo[0].p, stg_lo[slot].p, (size_t)m * 8, cudaMemcpyDeviceToDevice, st));
       if (KW == 2) CK(cudaMemcpyAsync(s_hi[0].p, stg_hi[slot].p, (size_t)m * 8, cudaMemcpyDeviceToDevice, st));
       iota_u32(s_val[0].as<u32>(), m, st);
+      ph_begin(ISA_PH_WM_SORT);
       CK(cudaMemsetAsync(dvary(), 0, 2 * sizeof(u64), st));
       keys_varying(KW, s_lo[0].as<u64>(), s_hi[0].as<u64>(), m, dvary(), st);
-      launches += 2;
       int cur = sort_built(m);
+      ph_end(ISA_PH_WM_SORT, m, 0);
       collapse_chunk(cur, m, 0xFFFFFFFFu, sd0, 0, stg_st[slot].as<u64>(), U, m);
       CK(cudaEventRecord(stg_free[slot], st));
       // append U to the result
@@ -767,12 +826,17 @@ struct Engine {
     devpool.reset();
     T.n = U.n = Tn.n = result.n = 0;
     tn_busy = false;
-    launches = 0;
+    memset(phases, 0, sizeof(phases));
+    for (auto& r : recs) { ev_pool.push_back(r.a); ev_pool.push_back(r.b); }
+    recs.clear();
+    const long long launch0 = g_launches.load();
     if (n < 0) throw IsaError(ISA_ERR_INVALID_INPUT, "negative row count");
     led.rows_seen = n;
-    if (n == 0) return 0;
+    if (n == 0) { led.kernel_launches = 0; return 0; }
     T.reserve(std::min<int64_t>(cfg.memory_budget, n) + 1, KW, S);
     auto t0 = std::chrono::steady_clock::now();
+    cudaEvent_t rg0 = ev_get(), rg1 = ev_get(), wm1 = ev_get();
+    CK(cudaEventRecord(rg0, st));
 
     int64_t wrows = on_host ? (cfg.window_rows > 0 ? cfg.window_rows : ((int64_t)32 << 20)) : n;
     int64_t a = 0, cycle_start = 0, last_len = 0, last_cycle = 0;
@@ -836,6 +900,7 @@ struct Engine {
     // residue becomes the last run if anything spilled (sortagg.py:353-374)
     if (!runs.empty()) spill_T();
     led.runs_after_generation = (int64_t)runs.size();
+    CK(cudaEventRecord(rg1, st));
     sync();
     auto t1 = std::chrono::steady_clock::now();
     led.ms_run_generation = std::chrono::duration<double, std::milli>(t1 - t0).count();
@@ -844,11 +909,25 @@ struct Engine {
       T.n = 0;
     } else {
       wide_merge();
+      CK(cudaEventRecord(wm1, st));
       sync();
       led.ms_wide_merge = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, rg1, wm1));
+      phases[ISA_PH_WIDE_MERGE].ms += ms;
+      phases[ISA_PH_WIDE_MERGE].calls += 1;
     }
+    {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, rg0, rg1));
+      phases[ISA_PH_RUN_GEN].ms += ms;
+      phases[ISA_PH_RUN_GEN].calls += 1;
+      phases[ISA_PH_RUN_GEN].rows += n;
+    }
+    ev_pool.push_back(rg0); ev_pool.push_back(rg1); ev_pool.push_back(wm1);
+    ph_collect();
     led.n_groups = result.n;
-    led.kernel_launches = launches;
+    led.kernel_launches = g_launches.load() - launch0;
     CK(cudaGetLastError());
     return result.n;
   }
@@ -901,7 +980,7 @@ struct Engine {
     for (int i = 0; i < 2; ++i) { b.lo[i] = s_lo[i].as<u64>(); b.hi[i] = nullptr; b.val[i] = s_val[i].as<u32>(); }
     b.tile_hist = tile_hist.as<u32>();
     b.scan_tmp = scan_tmp.as<u32>();
-    int cur = radix_sort_pairs(1, b, m, 0, 8, st, &launches);
+    int cur = radix_sort_pairs(1, b, m, 0, 8, st, nullptr);
     const u32* perm = s_val[cur].as<u32>();
     for (int c = 0; c < sch.n_key_cols; ++c) gather_column(key_cols[c], (int)key_elem(c), perm, m, key_out[c], st);
     for (int j = 0; j < sch.n_val_cols; ++j) gather_column(val_cols[j], (int)val_elem(j), perm, m, val_out[j], st);
@@ -994,6 +1073,14 @@ int64_t isa_cycles(isa_handle* h, int64_t* out, int64_t cap) {
   for (int64_t i = 0; i < (int64_t)c.size() && i < cap; ++i) out[i] = c[i];
   return (int64_t)c.size();
 }
+
+int isa_phase_stats(isa_handle* h, isa_phase* out, int cap) {
+  if (!h) return -1;
+  for (int i = 0; i < ISA_PH_COUNT && i < cap; ++i) out[i] = h->eng->phases[i];
+  return ISA_PH_COUNT;
+}
+
+int64_t isa_launch_count(void) { return (int64_t)isa::g_launches.load(); }
 
 int64_t isa_run_rows(isa_handle* h, int64_t* out, int64_t cap) {
   if (!h) return -1;

@@ -10,6 +10,8 @@
 
 namespace isa {
 
+std::atomic<long long> g_launches{0};
+
 // ============================================================== scan ====
 #define SC_THREADS 256
 #define SC_ITEMS 16
@@ -91,9 +93,9 @@ void scan_exclusive_u32(u32* data, u32 n, u32* tmp, u32* total, cudaStream_t st)
     if (total) cudaMemsetAsync(total, 0, sizeof(u32), st);
     return;
   }
-  k_scan_reduce<<<nb, SC_THREADS, 0, st>>>(data, n, tmp);
-  k_scan_single<<<1, SC_THREADS, 0, st>>>(tmp, nb, total);
-  k_scan_apply<<<nb, SC_THREADS, 0, st>>>(data, n, tmp);
+  klaunch(k_scan_reduce, nb, SC_THREADS, 0, st, data, n, tmp);
+  klaunch(k_scan_single, 1, SC_THREADS, 0, st, tmp, nb, total);
+  klaunch(k_scan_apply, nb, SC_THREADS, 0, st, data, n, tmp);
 }
 
 // ======================================================== radix sort ====
@@ -252,14 +254,14 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
   for (int shift = bit_lo; shift < bit_hi; shift += 8) {
     int nxt = cur ^ 1;
     if (KW == 2) {
-      k_rs_hist<2><<<ntiles, RS_THREADS, 0, st>>>(b.lo[cur], b.hi[cur], n, shift, b.tile_hist, ntiles);
+      klaunch(k_rs_hist<2>, ntiles, RS_THREADS, 0, st, b.lo[cur], b.hi[cur], n, shift, b.tile_hist, ntiles);
       scan_exclusive_u32(b.tile_hist, 256 * ntiles, b.scan_tmp, nullptr, st);
-      k_rs_scatter<2><<<ntiles, RS_THREADS, smem, st>>>(b.lo[cur], b.hi[cur], b.val[cur], b.lo[nxt], b.hi[nxt],
+      klaunch(k_rs_scatter<2>, ntiles, RS_THREADS, smem, st, b.lo[cur], b.hi[cur], b.val[cur], b.lo[nxt], b.hi[nxt],
                                                          b.val[nxt], n, shift, b.tile_hist, ntiles);
     } else {
-      k_rs_hist<1><<<ntiles, RS_THREADS, 0, st>>>(b.lo[cur], nullptr, n, shift, b.tile_hist, ntiles);
+      klaunch(k_rs_hist<1>, ntiles, RS_THREADS, 0, st, b.lo[cur], nullptr, n, shift, b.tile_hist, ntiles);
       scan_exclusive_u32(b.tile_hist, 256 * ntiles, b.scan_tmp, nullptr, st);
-      k_rs_scatter<1><<<ntiles, RS_THREADS, smem, st>>>(b.lo[cur], nullptr, b.val[cur], b.lo[nxt], nullptr,
+      klaunch(k_rs_scatter<1>, ntiles, RS_THREADS, smem, st, b.lo[cur], nullptr, b.val[cur], b.lo[nxt], nullptr,
                                                          b.val[nxt], n, shift, b.tile_hist, ntiles);
     }
     if (launches) *launches += 5;
@@ -307,8 +309,8 @@ void build_keys(int KW, const KeyDesc& kd, int64_t row0, const u32* pos, u32 n, 
                 u64* varying, cudaStream_t st) {
   if (n == 0) return;
   int g = grid_for(n, 256);
-  if (KW == 2) k_build_keys<2><<<g, 256, 0, st>>>(kd, row0, pos, n, lo, hi, val, varying);
-  else k_build_keys<1><<<g, 256, 0, st>>>(kd, row0, pos, n, lo, hi, val, varying);
+  if (KW == 2) klaunch(k_build_keys<2>, g, 256, 0, st, kd, row0, pos, n, lo, hi, val, varying);
+  else klaunch(k_build_keys<1>, g, 256, 0, st, kd, row0, pos, n, lo, hi, val, varying);
 }
 
 template <int KW>
@@ -332,15 +334,15 @@ __global__ void k_keys_varying(const u64* __restrict__ lo, const u64* __restrict
 void keys_varying(int KW, const u64* lo, const u64* hi, u32 n, u64* varying, cudaStream_t st) {
   if (n == 0) return;
   int g = grid_for(n, 256);
-  if (KW == 2) k_keys_varying<2><<<g, 256, 0, st>>>(lo, hi, n, varying);
-  else k_keys_varying<1><<<g, 256, 0, st>>>(lo, hi, n, varying);
+  if (KW == 2) klaunch(k_keys_varying<2>, g, 256, 0, st, lo, hi, n, varying);
+  else klaunch(k_keys_varying<1>, g, 256, 0, st, lo, hi, n, varying);
 }
 
 __global__ void k_iota(u32* v, u32 n) {
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = i;
 }
 void iota_u32(u32* v, u32 n, cudaStream_t st) {
-  if (n) k_iota<<<grid_for(n, 256), 256, 0, st>>>(v, n);
+  if (n) klaunch(k_iota, grid_for(n, 256), 256, 0, st, v, n);
 }
 
 // ==================================================== flush analysis ====
@@ -372,8 +374,8 @@ void new_heads(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, cons
                u32 t, u32* bitmap, u32* n_new, cudaStream_t st) {
   if (m == 0) return;
   int g = grid_for(m, 256);
-  if (KW == 2) k_new_heads<2><<<g, 256, 0, st>>>(lo, hi, val, m, T_lo, T_hi, t, bitmap, n_new);
-  else k_new_heads<1><<<g, 256, 0, st>>>(lo, hi, val, m, T_lo, T_hi, t, bitmap, n_new);
+  if (KW == 2) klaunch(k_new_heads<2>, g, 256, 0, st, lo, hi, val, m, T_lo, T_hi, t, bitmap, n_new);
+  else klaunch(k_new_heads<1>, g, 256, 0, st, lo, hi, val, m, T_lo, T_hi, t, bitmap, n_new);
 }
 
 __global__ void k_popc_words(const u32* __restrict__ bm, u32 nw, u32* __restrict__ cnt) {
@@ -398,9 +400,9 @@ __global__ void k_find_kth(const u32* __restrict__ bm, const u32* __restrict__ p
 void select_kth_bit(const u32* bitmap, u32 nbits, u32 k, u32* word_tmp, u32* scan_tmp, u32* out, cudaStream_t st) {
   u32 nw = (nbits + 31) / 32;
   int g = grid_for(nw, 256);
-  k_popc_words<<<g, 256, 0, st>>>(bitmap, nw, word_tmp);
+  klaunch(k_popc_words, g, 256, 0, st, bitmap, nw, word_tmp);
   scan_exclusive_u32(word_tmp, nw, scan_tmp, nullptr, st);
-  k_find_kth<<<g, 256, 0, st>>>(bitmap, word_tmp, nw, k, out);
+  klaunch(k_find_kth, g, 256, 0, st, bitmap, word_tmp, nw, k, out);
 }
 
 // ========================================================== collapse ====
@@ -501,18 +503,18 @@ void collapse(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, u32 l
     return;
   }
   int g = grid_for(m, 256);
-  if (KW == 2) k_head_flags<2><<<g, 256, 0, st>>>(lo, hi, val, m, limit, tmp.flags);
-  else k_head_flags<1><<<g, 256, 0, st>>>(lo, hi, val, m, limit, tmp.flags);
+  if (KW == 2) klaunch(k_head_flags<2>, g, 256, 0, st, lo, hi, val, m, limit, tmp.flags);
+  else klaunch(k_head_flags<1>, g, 256, 0, st, lo, hi, val, m, limit, tmp.flags);
   scan_exclusive_u32(tmp.flags, m, tmp.scan_tmp, tmp.total, st);
   u32 nthreads = (m + CL_ITEMS - 1) / CL_ITEMS;
   int blocks = (nthreads + 127) / 128;
   if (KW == 2)
-    k_seg_reduce<2><<<blocks, 128, 0, st>>>(lo, hi, val, m, limit, sd, row0, st_in, tmp.flags, out_lo, out_hi,
+    klaunch(k_seg_reduce<2>, blocks, 128, 0, st, lo, hi, val, m, limit, sd, row0, st_in, tmp.flags, out_lo, out_hi,
                                              out_st, tmp.partial, tmp.partial_slot);
   else
-    k_seg_reduce<1><<<blocks, 128, 0, st>>>(lo, hi, val, m, limit, sd, row0, st_in, tmp.flags, out_lo, out_hi,
+    klaunch(k_seg_reduce<1>, blocks, 128, 0, st, lo, hi, val, m, limit, sd, row0, st_in, tmp.flags, out_lo, out_hi,
                                              out_st, tmp.partial, tmp.partial_slot);
-  if (sd.nslots) k_seg_fixup<<<grid_for(nthreads, 256), 256, 0, st>>>(nthreads, sd, tmp.partial, tmp.partial_slot, out_st);
+  if (sd.nslots) klaunch(k_seg_fixup, grid_for(nthreads, 256), 256, 0, st, nthreads, sd, tmp.partial, tmp.partial_slot, out_st);
 }
 
 // ============================================================= merge ====
@@ -576,32 +578,32 @@ void merge_combine(int KW, int S, const int* ops, const int* types, const u64* a
   // ranks + match flags; prefix of match flags is built in a copy (match kept)
   if (na) {
     int g = grid_for(na, 256);
-    if (KW == 2) k_rank<2><<<g, 256, 0, st>>>(a_lo, a_hi, na, b_lo, b_hi, nb, tmp.rank_a, tmp.match_a);
-    else k_rank<1><<<g, 256, 0, st>>>(a_lo, a_hi, na, b_lo, b_hi, nb, tmp.rank_a, tmp.match_a);
+    if (KW == 2) klaunch(k_rank<2>, g, 256, 0, st, a_lo, a_hi, na, b_lo, b_hi, nb, tmp.rank_a, tmp.match_a);
+    else klaunch(k_rank<1>, g, 256, 0, st, a_lo, a_hi, na, b_lo, b_hi, nb, tmp.rank_a, tmp.match_a);
   }
   if (nb) {
     int g = grid_for(nb, 256);
-    if (KW == 2) k_rank<2><<<g, 256, 0, st>>>(b_lo, b_hi, nb, a_lo, a_hi, na, tmp.rank_b, tmp.match_b);
-    else k_rank<1><<<g, 256, 0, st>>>(b_lo, b_hi, nb, a_lo, a_hi, na, tmp.rank_b, tmp.match_b);
+    if (KW == 2) klaunch(k_rank<2>, g, 256, 0, st, b_lo, b_hi, nb, a_lo, a_hi, na, tmp.rank_b, tmp.match_b);
+    else klaunch(k_rank<1>, g, 256, 0, st, b_lo, b_hi, nb, a_lo, a_hi, na, tmp.rank_b, tmp.match_b);
   }
   // prefix counts live after the flags: match_x[n + 1 + i]
   u32* pre_a = tmp.match_a + na + 1;
   u32* pre_b = tmp.match_b + nb + 1;
   if (na) {
-    k_copy_u32<<<grid_for(na, 256), 256, 0, st>>>(tmp.match_a, pre_a, na);
+    klaunch(k_copy_u32, grid_for(na, 256), 256, 0, st, tmp.match_a, pre_a, na);
     scan_exclusive_u32(pre_a, na, tmp.scan_tmp, tmp.total, st);
     int g = grid_for(na, 256);
-    if (KW == 2) k_merge_write_a<2><<<g, 256, 0, st>>>(a_lo, a_hi, a_st, na, b_st, tmp.rank_a, pre_a, tmp.match_a, S, oa, c_lo, c_hi, c_st);
-    else k_merge_write_a<1><<<g, 256, 0, st>>>(a_lo, a_hi, a_st, na, b_st, tmp.rank_a, pre_a, tmp.match_a, S, oa, c_lo, c_hi, c_st);
+    if (KW == 2) klaunch(k_merge_write_a<2>, g, 256, 0, st, a_lo, a_hi, a_st, na, b_st, tmp.rank_a, pre_a, tmp.match_a, S, oa, c_lo, c_hi, c_st);
+    else klaunch(k_merge_write_a<1>, g, 256, 0, st, a_lo, a_hi, a_st, na, b_st, tmp.rank_a, pre_a, tmp.match_a, S, oa, c_lo, c_hi, c_st);
   } else {
     cudaMemsetAsync(tmp.total, 0, sizeof(u32), st);
   }
   if (nb) {
-    k_copy_u32<<<grid_for(nb, 256), 256, 0, st>>>(tmp.match_b, pre_b, nb);
+    klaunch(k_copy_u32, grid_for(nb, 256), 256, 0, st, tmp.match_b, pre_b, nb);
     scan_exclusive_u32(pre_b, nb, tmp.scan_tmp, tmp.total + 1, st);
     int g = grid_for(nb, 256);
-    if (KW == 2) k_merge_write_b<2><<<g, 256, 0, st>>>(b_lo, b_hi, b_st, nb, tmp.rank_b, pre_b, tmp.match_b, S, c_lo, c_hi, c_st);
-    else k_merge_write_b<1><<<g, 256, 0, st>>>(b_lo, b_hi, b_st, nb, tmp.rank_b, pre_b, tmp.match_b, S, c_lo, c_hi, c_st);
+    if (KW == 2) klaunch(k_merge_write_b<2>, g, 256, 0, st, b_lo, b_hi, b_st, nb, tmp.rank_b, pre_b, tmp.match_b, S, c_lo, c_hi, c_st);
+    else klaunch(k_merge_write_b<1>, g, 256, 0, st, b_lo, b_hi, b_st, nb, tmp.rank_b, pre_b, tmp.match_b, S, c_lo, c_hi, c_st);
   } else {
     cudaMemsetAsync(tmp.total + 1, 0, sizeof(u32), st);
   }
@@ -619,7 +621,7 @@ __global__ void k_fold_partials(int nt, SlotDesc sd, const u64* __restrict__ par
 
 void fold_partials(int nt, const SlotDesc& sd, const u64* partials, u32 grid, u64* T_st, cudaStream_t st) {
   int n = nt * sd.nslots;
-  if (n) k_fold_partials<<<1, 128, 0, st>>>(nt, sd, partials, grid, T_st);
+  if (n) klaunch(k_fold_partials, 1, 128, 0, st, nt, sd, partials, grid, T_st);
 }
 
 __global__ void k_compact_misses(const u32* __restrict__ miss_buf, const u32* __restrict__ miss_cnt,
@@ -631,7 +633,7 @@ __global__ void k_compact_misses(const u32* __restrict__ miss_buf, const u32* __
 
 void compact_misses(const u32* miss_buf, const u32* miss_cnt, const u32* miss_off, u32 grid, u32 rows_per_cta,
                     u32* out, cudaStream_t st) {
-  k_compact_misses<<<grid, 256, 0, st>>>(miss_buf, miss_cnt, miss_off, rows_per_cta, out);
+  klaunch(k_compact_misses, grid, 256, 0, st, miss_buf, miss_cnt, miss_off, rows_per_cta, out);
 }
 
 // ============================================================ runs ====
@@ -657,8 +659,8 @@ void run_lower_bounds(int KW, const RunRef* runs_dev, int nruns, const u64* b_lo
   int n = nruns * nb;
   if (n == 0) return;
   int g = (n + 127) / 128;
-  if (KW == 2) k_run_lower_bounds<2><<<g, 128, 0, st>>>(runs_dev, nruns, b_lo, b_hi, nb, out);
-  else k_run_lower_bounds<1><<<g, 128, 0, st>>>(runs_dev, nruns, b_lo, b_hi, nb, out);
+  if (KW == 2) klaunch(k_run_lower_bounds<2>, g, 128, 0, st, runs_dev, nruns, b_lo, b_hi, nb, out);
+  else klaunch(k_run_lower_bounds<1>, g, 128, 0, st, runs_dev, nruns, b_lo, b_hi, nb, out);
 }
 
 // ========================================================== export ====
@@ -677,7 +679,7 @@ __global__ void k_export_key(const u64* __restrict__ lo, const u64* __restrict__
 }
 
 void export_key_col(const u64* lo, const u64* hi, u32 n, int dtype, int shift, int width, void* out, cudaStream_t st) {
-  if (n) k_export_key<<<grid_for(n, 256), 256, 0, st>>>(lo, hi, n, dtype, shift, width, out);
+  if (n) klaunch(k_export_key, grid_for(n, 256), 256, 0, st, lo, hi, n, dtype, shift, width, out);
 }
 
 __global__ void k_export_slot(const u64* __restrict__ stt, int S, int s, u32 n, u64* __restrict__ out) {
@@ -685,7 +687,7 @@ __global__ void k_export_slot(const u64* __restrict__ stt, int S, int s, u32 n, 
 }
 
 void export_slot(const u64* stt, int S, int s, u32 n, u64* out, cudaStream_t st) {
-  if (n) k_export_slot<<<grid_for(n, 256), 256, 0, st>>>(stt, S, s, n, out);
+  if (n) klaunch(k_export_slot, grid_for(n, 256), 256, 0, st, stt, S, s, n, out);
 }
 
 // ======================================================= partition ====
@@ -701,7 +703,7 @@ __global__ void k_sample_keys(KeyDesc kd, i64 n, i64 stride, u64* __restrict__ o
 
 void sample_keys(const KeyDesc& kd, int64_t n, int64_t stride, u64* out_lo, u64* out_hi, cudaStream_t st) {
   int64_t ns = (n + stride - 1) / stride;
-  if (ns > 0) k_sample_keys<<<grid_for(ns, 256), 256, 0, st>>>(kd, n, stride, out_lo, out_hi);
+  if (ns > 0) klaunch(k_sample_keys, grid_for(ns, 256), 256, 0, st, kd, n, stride, out_lo, out_hi);
 }
 
 template <int KW>
@@ -726,8 +728,8 @@ void partition_dest(int KW, const KeyDesc& kd, u32 n, const u64* s_lo, const u64
                     cudaStream_t st) {
   if (n == 0) return;
   int g = grid_for(n, 256);
-  if (KW == 2) k_partition_dest<2><<<g, 256, 0, st>>>(kd, n, s_lo, s_hi, ns, dest_lo, val);
-  else k_partition_dest<1><<<g, 256, 0, st>>>(kd, n, s_lo, s_hi, ns, dest_lo, val);
+  if (KW == 2) klaunch(k_partition_dest<2>, g, 256, 0, st, kd, n, s_lo, s_hi, ns, dest_lo, val);
+  else klaunch(k_partition_dest<1>, g, 256, 0, st, kd, n, s_lo, s_hi, ns, dest_lo, val);
 }
 
 template <typename T>
@@ -739,10 +741,10 @@ void gather_column(const void* src, int elem_bytes, const u32* perm, u32 n, void
   if (n == 0) return;
   int g = grid_for(n, 256);
   switch (elem_bytes) {
-    case 1: k_gather<unsigned char><<<g, 256, 0, st>>>((const unsigned char*)src, perm, n, (unsigned char*)dst); break;
-    case 2: k_gather<unsigned short><<<g, 256, 0, st>>>((const unsigned short*)src, perm, n, (unsigned short*)dst); break;
-    case 4: k_gather<unsigned int><<<g, 256, 0, st>>>((const unsigned int*)src, perm, n, (unsigned int*)dst); break;
-    default: k_gather<u64><<<g, 256, 0, st>>>((const u64*)src, perm, n, (u64*)dst); break;
+    case 1: klaunch(k_gather<unsigned char>, g, 256, 0, st, (const unsigned char*)src, perm, n, (unsigned char*)dst); break;
+    case 2: klaunch(k_gather<unsigned short>, g, 256, 0, st, (const unsigned short*)src, perm, n, (unsigned short*)dst); break;
+    case 4: klaunch(k_gather<unsigned int>, g, 256, 0, st, (const unsigned int*)src, perm, n, (unsigned int*)dst); break;
+    default: klaunch(k_gather<u64>, g, 256, 0, st, (const u64*)src, perm, n, (u64*)dst); break;
   }
 }
 
@@ -759,7 +761,7 @@ __global__ void k_count_dest(const u64* __restrict__ d, u32 n, int ndest, u32* _
 }
 
 void count_dest(const u64* dest_sorted, u32 n, int ndest, u32* counts, cudaStream_t st) {
-  k_count_dest<<<1, 256, 0, st>>>(dest_sorted, n, ndest, counts);
+  klaunch(k_count_dest, 1, 256, 0, st, dest_sorted, n, ndest, counts);
 }
 
 }  // namespace isa

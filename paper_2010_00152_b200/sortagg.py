@@ -327,6 +327,7 @@ class SortAggregate:
         self.executed_steps = []
         self.runs_after_generation = 0
         self.device_ledger = None
+        self.phase_stats = {}
         self.cycles = []
         self.run_rows = []
         self._device = device
@@ -506,6 +507,7 @@ class SortAggregate:
             setattr(self.ledger, name, getattr(self.ledger, name) + getattr(led, name))
         self.cycles = h.cycles()
         self.run_rows = h.run_rows()
+        self.phase_stats = h.phase_stats()
         self.runs_after_generation = len(self.run_rows)
         self.executed_steps = []
         self.initial_plan = None
