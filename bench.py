@@ -95,7 +95,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
         except Exception:
@@ -253,11 +253,18 @@ def main():
     for _ in range(args.warmup):
         res = step()
     barrier()
+    # clocks are sampled from a >= 1 s load ramp right before the timed region
+    # through its end (a short timed region alone holds too few samples)
+    clocks = ClockSampler(local)
+    clocks.start()
+    t_ramp = time.perf_counter()
+    while time.perf_counter() - t_ramp < 1.0:
+        res = step()
+        torch.cuda.synchronize(dev)
+    barrier()
     stream = torch.cuda.current_stream(dev)
     phase_tot = {}
     launches0 = _native.launch_count()
-    clocks = ClockSampler(local)
-    clocks.start()
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)

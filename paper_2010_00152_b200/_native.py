@@ -20,7 +20,7 @@ from .core import (
 )
 
 LIB_NAME = "libinsortagg_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("ISA_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 MAX_KEY_COLS = 8
 MAX_SLOTS = 16

@@ -1,6 +1,8 @@
 // Tiny-table absorb kernel (early aggregation against a register-resident index).
 #include "isa_kernels.h"
 
+#include <random>
+
 namespace isa {
 
 // ======================================================= tiny absorb ====
@@ -190,6 +192,31 @@ __global__ void __launch_bounds__(AB_THREADS) k_absorb_tiny(KeyDesc kd, SlotDesc
     if (lane == 0) partials[((size_t)c * NT + j) * S + s] = x;
   }
   if (tid == 0) miss_cnt[c] = nmiss;
+}
+
+// 32-bit fold of a normalized key; bucket = (fold * mult) >> 28 (16 buckets)
+static inline u32 tiny_fold(u64 hi, u64 lo) {
+  u64 x = lo ^ hi;
+  return (u32)x ^ (u32)(x >> 32) ^ (u32)(hi >> 17);
+}
+
+// Perfect hash of the resident keys (kept for the probe variants; the
+// measured-fastest kernel compares against every resident key).
+bool tiny_perfect_hash(int KW, TinyTable& tt, int nt) {
+  std::mt19937_64 rng(0x2010001500000000ull + nt);
+  for (int attempt = 0; attempt < 100000; ++attempt) {
+    u32 mult = (u32)rng() | 1u;
+    u64 map = ~0ull;
+    bool ok = true;
+    for (int j = 0; j < nt && ok; ++j) {
+      u32 b = (tiny_fold(KW == 2 ? tt.hi[j] : 0, tt.lo[j]) * mult) >> 28;
+      if (((map >> (4 * b)) & 0xF) != 0xF) ok = false;
+      map &= ~(0xFull << (4 * b));
+      map |= (u64)j << (4 * b);
+    }
+    if (ok) { tt.mult = mult; tt.map = map; return true; }
+  }
+  return false;
 }
 
 bool absorb_supported(int nt, int nslots) { return nt >= 1 && nt <= 8 && nt * nslots <= AB_MAX_CELLS; }

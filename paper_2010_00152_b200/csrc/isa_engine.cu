@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -487,6 +488,7 @@ struct Engine {
   }
 
   void refresh_tiny() {
+    tiny_ok = false;
     if (T.n == 0 || T.n > 8) return;
     memset(&tiny, 0, sizeof(tiny));
     CK(cudaMemcpyAsync(h_scal, T.plo(), T.n * 8, cudaMemcpyDeviceToHost, st));
@@ -496,7 +498,10 @@ struct Engine {
       tiny.lo[j] = ((u64*)h_scal)[j];
       tiny.hi[j] = KW == 2 ? ((u64*)h_scal)[8 + j] : 0;
     }
+    tiny_perfect_hash(KW, tiny, (int)T.n);
+    tiny_ok = true;
   }
+  bool tiny_ok = false;
 
   // T becomes a run (RunWriter of a read-sort-write flush, sortagg.py:344-350)
   void spill_T() {
@@ -555,7 +560,7 @@ struct Engine {
     const u32 span = (u32)(b - a);
     const int64_t row0 = a - base;   // column element of row a
     led.chunks++;
-    if (T.n > 0 && T.n <= 8 && absorb_supported((int)T.n, S)) return absorb_chunk(kd, sd, row0, a, span);
+    if (T.n > 0 && T.n <= 8 && tiny_ok && absorb_supported((int)T.n, S)) return absorb_chunk(kd, sd, row0, a, span);
     int cur = sort_rows(kd, row0, nullptr, span);
     u32 f = flush_point(cur, span, span);
     collapse_chunk(cur, span, f, sd, row0, nullptr, U, std::min<int64_t>(span, cfg.memory_budget));
@@ -626,10 +631,12 @@ struct Engine {
     const int64_t M = cfg.memory_budget;
     int64_t cmax = cfg.chunk_rows_max > 0 ? cfg.chunk_rows_max : ((int64_t)64 << 20);
     int64_t len;
-    if (T.n > 0 && T.n <= 8 && absorb_supported((int)T.n, S)) {
-      len = std::min<int64_t>(cmax, (int64_t)1 << 28);
+    if (T.n > 0 && T.n <= 8 && tiny_ok && absorb_supported((int)T.n, S)) {
+      // one streaming pass over everything staged: the absorb kernel has no
+      // per-chunk memory beyond a per-CTA miss list
+      return std::min<int64_t>(remaining, cfg.chunk_rows_max > 0 ? cfg.chunk_rows_max : ((int64_t)1 << 30));
     } else if (last_len == 0) {
-      len = std::max<int64_t>(M + M / 8, 65536);
+      len = std::max<int64_t>(M + M / 8, 4096);
     } else if (last_flushed) {
       len = last_cycle + last_cycle / 8 + 4096;
     } else if (last_new > 0) {

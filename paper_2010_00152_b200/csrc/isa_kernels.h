@@ -73,7 +73,11 @@ void merge_combine(int KW, int S, const int* ops, const int* types,
                    u64* c_lo, u64* c_hi, u64* c_st, MergeTmp& tmp, cudaStream_t st);
 
 // ---- tiny-table absorb (the early-aggregation probe for |T| <= 8) -------
-struct TinyTable { u64 lo[8]; u64 hi[8]; };
+// Resident table of nt <= 8 keys plus a perfect hash over them: bucket(key) =
+// (mix(key) * mult) >> 60 (16 buckets), map nibble b = table row or 0xF.
+struct TinyTable { u64 lo[8]; u64 hi[8]; u64 mult; u64 map; };
+// host helper: find mult/map making bucket() injective on the table's keys
+bool tiny_perfect_hash(int KW, TinyTable& tt, int nt);
 // Grid geometry helper: CTAs and rows per CTA for n rows.
 void absorb_geometry(u32 n, int num_sms, u32* grid, u32* rows_per_cta);
 bool absorb_supported(int nt, int nslots);
