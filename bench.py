@@ -295,8 +295,8 @@ def main():
     val_b = w.value_bytes
     out_b = (n_groups or 0) * (key_b + 8 * w.schema.state_slots)
     b_in = rows * (key_b + val_b)
-    led = op.ledger
-    spill_rows = led.rows_spilled / max(1, args.steps)
+    dled = op.device_ledger or {}
+    spill_rows = dled.get("rows_spilled", 0)   # last execute (every step is identical)
     spill_b = 2 * spill_rows * (key_b + 8 * w.schema.state_slots) if run_tier == "host" else 0
     t_star = (b_in + out_b) / (peak * 1e9) + spill_b / (link * 1e9)
     # dominant kernel: the phase with the most device time among kernel phases
@@ -347,7 +347,9 @@ def main():
                           "b_in": b_in, "b_out": out_b, "b_spill": spill_b, "link_gbs": link,
                           "hbm_gbs": peak},
         "phases_ms_per_step": {k: v["ms"] / max(1, args.steps) for k, v in phase_tot.items() if v["ms"]},
-        "ledger_per_step": {"rows_spilled": spill_rows, "runs": op.runs_after_generation},
+        "ledger_per_step": {"rows_spilled": spill_rows, "runs": op.runs_after_generation,
+                            "bytes_d2h": dled.get("bytes_d2h"), "bytes_h2d": dled.get("bytes_h2d"),
+                            "merge_windows": dled.get("merge_windows"), "chunks": dled.get("chunks")},
         "gpu_launches": launches,
         "clocks": clk,
     }

@@ -533,6 +533,8 @@ class SortAggregate:
         self.runs_after_generation = 0
         if not rows:
             return []
+        if not torch.cuda.is_available():
+            raise ResourceError("the B200 operator needs a CUDA device (torch.cuda.is_available() is False)")
         arity = self.schema.arity
         nslots = self.schema.state_slots
         key_cols = []

@@ -1,0 +1,80 @@
+"""Device primitives of the multi-GPU path (sampling, partition kernel) and the
+distributed entry point on a single-rank NCCL group (the only GPU count this
+environment grants; the 2-rank exchange logic is covered over gloo)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+import paper_2010_00152_b200 as isa  # noqa: E402
+from paper_2010_00152_b200 import parallel, workloads  # noqa: E402
+
+
+def _op(w):
+    return isa.SortAggregate(w.schema, isa.SortAggConfig(memory_budget=w.memory_budget, page_capacity=100))
+
+
+@pytest.mark.parametrize("c", [1, 3, 4, 5])
+def test_sample_keys_matches_normalization(c):
+    w = workloads.make(c, rows=100_000, device="cpu", **({"domain": 1 << 16} if c in (3, 5) else {}))
+    op = _op(w)
+    keys = [k.cuda() for k in w.keys]
+    hi, lo = parallel.native_sampler(op, keys, 1000)
+    stride = max(1, w.rows // 1000)
+    want_hi, want_lo = oracle.normalize_keys([k.numpy() for k in w.keys])
+    assert np.array_equal(lo.cpu().numpy().view(np.uint64), want_lo[::stride])
+    assert np.array_equal(hi.cpu().numpy().view(np.uint64), want_hi[::stride])
+
+
+@pytest.mark.parametrize("c,G", [(5, 4), (3, 8), (4, 2), (1, 3), (2, 8)])
+def test_partition_kernel_is_stable_range_split(c, G):
+    w = workloads.make(c, rows=200_000, device="cpu", **({"domain": 1 << 18} if c in (3, 5) else {}))
+    op = _op(w)
+    keys = [k.cuda() for k in w.keys]
+    names = sorted(w.values)
+    vals = [w.values[n].cuda() for n in names]
+    s_hi, s_lo = parallel.native_sampler(op, keys, 4096)
+    sp_hi, sp_lo = parallel.choose_splitters(s_hi, s_lo, G)
+    pk, pv, counts = parallel.native_partitioner(op, keys, vals, sp_hi, sp_lo)
+    assert sum(counts) == w.rows and len(counts) == G
+    hi, lo = oracle.normalize_keys([k.numpy() for k in w.keys])
+    shi, slo = sp_hi.cpu().numpy().view(np.uint64), sp_lo.cpu().numpy().view(np.uint64)
+    dest = np.zeros(w.rows, dtype=np.int64)
+    for i in range(len(slo)):
+        dest += (hi > shi[i]) | ((hi == shi[i]) & (lo >= slo[i]))
+    order = np.argsort(dest, kind="stable")
+    assert counts == np.bincount(dest, minlength=G).tolist()
+    for got, k in zip(pk, w.keys):
+        assert np.array_equal(got.cpu().numpy(), k.numpy()[order])
+    for got, n in zip(pv, names):
+        assert np.array_equal(got.cpu().numpy(), w.values[n].numpy()[order])
+
+
+@pytest.mark.parametrize("mode", ["partition", "preaggregate"])
+def test_distributed_execute_single_rank_nccl(mode):
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        w = workloads.make(5, rows=500_000, device="cpu", domain=1 << 17)
+        op = _op(w)
+        res = parallel.distributed_execute(op, [k.cuda() for k in w.keys], {n: v.cuda() for n, v in w.values.items()},
+                                           mode=mode)
+        slots = oracle.make_states(w.schema, {n: v.numpy() for n, v in w.values.items()}, w.rows)
+        want_k, want_s = oracle.reference_aggregate([k.numpy() for k in w.keys], slots, oracle.slot_ops(w.schema))
+        assert np.array_equal(res.keys[0].cpu().numpy(), want_k[0])
+        for g, e in zip(res.states, want_s):
+            assert np.array_equal(g.cpu().numpy(), e)
+    finally:
+        dist.destroy_process_group()
