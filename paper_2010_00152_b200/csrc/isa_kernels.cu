@@ -609,19 +609,21 @@ void merge_combine(int KW, int S, const int* ops, const int* types, const u64* a
   }
 }
 
+// one warp per (table row, slot) cell: strided combine over the CTAs' partials, then a warp reduction
 __global__ void k_fold_partials(int nt, SlotDesc sd, const u64* __restrict__ partials, u32 grid, u64* __restrict__ T_st) {
   const int S = sd.nslots;
-  int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= nt * S) return;
-  int j = q / S, s = q % S;
-  u64 x = identity_slot(sd.op[s], sd.type[s]);
-  for (u32 c = 0; c < grid; ++c) x = combine_slot(sd.op[s], sd.type[s], x, partials[((size_t)c * nt + j) * S + s]);
-  T_st[(size_t)j * S + s] = combine_slot(sd.op[s], sd.type[s], T_st[(size_t)j * S + s], x);
+  const int q = blockIdx.x;   // cell
+  const int j = q / S, s = q % S;
+  const int op = sd.op[s], ty = sd.type[s];
+  u64 x = identity_slot(op, ty);
+  for (u32 c = threadIdx.x; c < grid; c += 32) x = combine_slot(op, ty, x, partials[((size_t)c * nt + j) * S + s]);
+  for (int o = 16; o; o >>= 1) x = combine_slot(op, ty, x, __shfl_xor_sync(0xffffffffu, x, o));
+  if (threadIdx.x == 0) T_st[(size_t)j * S + s] = combine_slot(op, ty, T_st[(size_t)j * S + s], x);
 }
 
 void fold_partials(int nt, const SlotDesc& sd, const u64* partials, u32 grid, u64* T_st, cudaStream_t st) {
   int n = nt * sd.nslots;
-  if (n) klaunch(k_fold_partials, 1, 128, 0, st, nt, sd, partials, grid, T_st);
+  if (n) klaunch(k_fold_partials, n, 32, 0, st, nt, sd, partials, grid, T_st);
 }
 
 __global__ void k_compact_misses(const u32* __restrict__ miss_buf, const u32* __restrict__ miss_cnt,
