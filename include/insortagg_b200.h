@@ -121,6 +121,8 @@ typedef struct isa_ledger {
   int64_t kernel_launches;
   double ms_run_generation;
   double ms_wide_merge;
+  double ms_host_sync;      /* host time blocked in stream synchronizations */
+  double ms_spill_wait;     /* host-observed wait for table buffers still being spilled */
 } isa_ledger;
 
 /* device-time breakdown of the last execute (CUDA events on the caller's stream) */

@@ -94,6 +94,8 @@ class IsaLedger(ctypes.Structure):
         "bytes_d2h", "kernel_launches")] + [
         ("ms_run_generation", ctypes.c_double),
         ("ms_wide_merge", ctypes.c_double),
+        ("ms_host_sync", ctypes.c_double),
+        ("ms_spill_wait", ctypes.c_double),
     ]
 
     def as_dict(self):

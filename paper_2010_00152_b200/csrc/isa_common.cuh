@@ -58,6 +58,7 @@ struct SlotDesc {
   int type[ISA_MAX_SLOTS];
   int src[ISA_MAX_SLOTS];
   int dtype[ISA_MAX_SLOTS];      // dtype of the source column (SRC_COL)
+  int alias[ISA_MAX_SLOTS];      // earlier slot reading the same column as the same type, or -1
   const void* ptr[ISA_MAX_SLOTS];
 };
 

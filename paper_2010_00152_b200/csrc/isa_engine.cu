@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <deque>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -162,12 +163,43 @@ struct Engine {
   // workspace
   DevBuf s_lo[2], s_hi[2], s_val[2], tile_hist, scan_tmp;
   DevBuf scal;   // small device scalars (u64 varying[2], u32 counters)
-  u32* h_scal = nullptr;   // pinned mirror (64 words)
+  u32* h_scal = nullptr;   // pinned, mapped mirror (64 u64 words)
+  u32* d_scal_mapped = nullptr;
+  // device -> h_scal through a kernel (see read_words)
+  void to_host(const void* dsrc, size_t bytes, size_t host_word_off = 0) {
+    read_words(d_scal_mapped + host_word_off, (const u32*)dsrc, (u32)((bytes + 3) / 4), st);
+  }
   DevBuf bitmap, word_tmp;
   DevBuf cl_flags, cl_partial, cl_pslot;
   DevBuf mg_rank_a, mg_match_a, mg_rank_b, mg_match_b;
   DevBuf ab_partials, ab_miss_buf, ab_miss_cnt, ab_miss_off, miss_list;
-  Table T, U, Tn;   // resident table, chunk collapse, merge output
+  Table T, U;       // resident table, chunk collapse
+  // tables whose buffers are still being copied to the host tier (event =
+  // copy done) and free tables; a spill never blocks the compute stream
+  // unless three copies are still in flight
+  struct BusyTable { Table t; cudaEvent_t ev; };
+  std::deque<BusyTable> busy;
+  std::vector<Table> spare;
+  std::vector<cudaEvent_t> busy_ev_pool;
+  Table take_table() {
+    while (!busy.empty() && cudaEventQuery(busy.front().ev) == cudaSuccess) {
+      spare.push_back(busy.front().t);
+      busy_ev_pool.push_back(busy.front().ev);
+      busy.pop_front();
+    }
+    Table t;
+    if (!spare.empty()) {
+      t = spare.back();
+      spare.pop_back();
+    } else if (busy.size() >= 3) {
+      CK(cudaStreamWaitEvent(st, busy.front().ev, 0));
+      t = busy.front().t;
+      busy_ev_pool.push_back(busy.front().ev);
+      busy.pop_front();
+    }
+    t.n = 0;
+    return t;
+  }
   std::vector<cudaEvent_t> tbl_free;   // not used for now
   TinyTable tiny;   // host mirror of T keys when |T| <= 8
   // runs
@@ -238,7 +270,8 @@ struct Engine {
       CK(cudaEventCreateWithFlags(&stg_free[i], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&win[i].ready, cudaEventDisableTiming));
     }
-    CK(cudaHostAlloc((void**)&h_scal, 64 * sizeof(u64), cudaHostAllocDefault));
+    CK(cudaHostAlloc((void**)&h_scal, 64 * sizeof(u64), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer((void**)&d_scal_mapped, h_scal, 0));
     scal.ensure(64 * sizeof(u64));
     memset(&led, 0, sizeof(led));
   }
@@ -254,7 +287,10 @@ struct Engine {
     for (auto& w : win) { for (auto& b : w.keys) b.release(); for (auto& b : w.vals) b.release(); }
     for (auto& r : recs) { ev_pool.push_back(r.a); ev_pool.push_back(r.b); }
     for (auto e : ev_pool) cudaEventDestroy(e);
-    T.release(); U.release(); Tn.release(); result.release();
+    T.release(); U.release(); result.release();
+    for (auto& t : spare) t.release();
+    for (auto& b : busy) { b.t.release(); cudaEventDestroy(b.ev); }
+    for (auto e : busy_ev_pool) cudaEventDestroy(e);
     pinned.release();
     devpool.release();
     if (h_scal) cudaFreeHost(h_scal);
@@ -326,6 +362,15 @@ struct Engine {
         sd0.dtype[s] = dt;
       }
     }
+    for (int s = 0; s < S; ++s) {
+      sd0.alias[s] = -1;
+      if (sd0.src[s] != SRC_COL) continue;
+      for (int q = 0; q < s; ++q)
+        if (sd0.src[q] == SRC_COL && sch.slot_col[q] == sch.slot_col[s] && sd0.type[q] == sd0.type[s]) {
+          sd0.alias[s] = q;
+          break;
+        }
+    }
     absorb_row_bytes = key_bits / 8;
     bool used[ISA_MAX_VAL_COLS] = {false};
     for (int s = 0; s < S; ++s)
@@ -336,9 +381,13 @@ struct Engine {
   }
 
   // ------------------------------------------------------------ helpers --
-  void sync() { CK(cudaStreamSynchronize(st)); }
+  void sync() {
+    auto t0 = std::chrono::steady_clock::now();
+    CK(cudaStreamSynchronize(st));
+    led.ms_host_sync += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
   u32 read_u32(const u32* dptr) {
-    CK(cudaMemcpyAsync(h_scal, dptr, sizeof(u32), cudaMemcpyDeviceToHost, st));
+    to_host(dptr, sizeof(u32));
     sync();
     return h_scal[0];
   }
@@ -392,7 +441,7 @@ struct Engine {
     return cur;
   }
   int sort_built(u32 m) {
-    CK(cudaMemcpyAsync(h_scal, dvary(), 2 * sizeof(u64), cudaMemcpyDeviceToHost, st));
+    to_host(dvary(), 2 * sizeof(u64));
     sync();
     u64 vlo = ((u64*)h_scal)[0], vhi = ((u64*)h_scal)[1];
     int hb = -1, lb = 128;
@@ -420,7 +469,7 @@ struct Engine {
     CK(cudaMemsetAsync(dscal32(0), 0, sizeof(u32), st));
     new_heads(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, T.plo(), T.phi(), T.n,
               bitmap.as<u32>(), dscal32(0), st);
-    CK(cudaMemcpyAsync(h_scal, dscal32(0), sizeof(u32), cudaMemcpyDeviceToHost, st));
+    to_host(dscal32(0), sizeof(u32));
     ph_end(ISA_PH_FLUSH, m, 0);
     sync();
     u32 n_new = h_scal[0];
@@ -430,13 +479,13 @@ struct Engine {
     u32 k = (u32)(M - (int64_t)T.n + 1);
     ph_begin(ISA_PH_FLUSH);
     select_kth_bit(bitmap.as<u32>(), span, k, word_tmp.as<u32>(), scan_tmp.as<u32>(), dscal32(1), st);
-    CK(cudaMemcpyAsync(h_scal, dscal32(1), sizeof(u32), cudaMemcpyDeviceToHost, st));
+    to_host(dscal32(1), sizeof(u32));
     ph_end(ISA_PH_FLUSH, 0, 0);
     sync();
     return h_scal[0];
   }
   u32 last_new = 0;
-  bool tn_busy = false;
+  size_t tcap = 1;   // capacity of every run-generation table: min(M, n) + 1
 
   // U <- collapse(sorted chunk restricted to positions < limit)
   void collapse_chunk(int cur, u32 m, u32 limit, const SlotDesc& sd, int64_t row0, const u64* st_in, Table& out,
@@ -453,37 +502,34 @@ struct Engine {
     ph_begin(phc);
     collapse(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, limit, sd, row0, st_in,
              out.plo(), out.phi(), out.pst(), ct, st);
-    CK(cudaMemcpyAsync(h_scal, dscal32(2), sizeof(u32), cudaMemcpyDeviceToHost, st));
+    to_host(dscal32(2), sizeof(u32));
     ph_end(phc, m, 0);
     sync();
     out.n = h_scal[0];
   }
 
-  // Tn <- merge_combine(T, U); swap into T
+  // T <- merge_combine(T, U) (into a free table; the old T becomes spare)
   void merge_into_T() {
     if (U.n == 0) return;
     if (T.n == 0) { std::swap(T, U); U.n = 0; return; }
     ensure_merge(T.n, U.n);
-    if (tn_busy) {   // Tn's buffers are still being copied to the host tier
-      CK(cudaStreamWaitEvent(st, spill_done, 0));
-      tn_busy = false;
-    }
-    Tn.reserve((size_t)T.n + U.n, KW, S);
+    Table out = take_table();
+    out.reserve(tcap, KW, S);   // |T ∪ U| <= min(M, n) by the flush analysis
     MergeTmp mt;
     mt.rank_a = mg_rank_a.as<u32>(); mt.match_a = mg_match_a.as<u32>();
     mt.rank_b = mg_rank_b.as<u32>(); mt.match_b = mg_match_b.as<u32>();
     mt.scan_tmp = scan_tmp.as<u32>();
     mt.total = dscal32(4);
     ph_begin(ISA_PH_TABLE_MERGE);
-    merge_combine(KW, S, ops, types, T.plo(), T.phi(), T.pst(), T.n, U.plo(), U.phi(), U.pst(), U.n, Tn.plo(),
-                  Tn.phi(), Tn.pst(), mt, st);
-    CK(cudaMemcpyAsync(h_scal, dscal32(4), sizeof(u32), cudaMemcpyDeviceToHost, st));
+    merge_combine(KW, S, ops, types, T.plo(), T.phi(), T.pst(), T.n, U.plo(), U.phi(), U.pst(), U.n, out.plo(),
+                  out.phi(), out.pst(), mt, st);
+    to_host(dscal32(4), sizeof(u32));
     ph_end(ISA_PH_TABLE_MERGE, (int64_t)T.n + U.n, 0);
     sync();
     u32 matches = h_scal[0];
-    Tn.n = T.n + U.n - matches;
-    std::swap(T, Tn);
-    Tn.n = 0;
+    out.n = T.n + U.n - matches;
+    spare.push_back(T);
+    T = out;
     U.n = 0;
   }
 
@@ -491,8 +537,8 @@ struct Engine {
     tiny_ok = false;
     if (T.n == 0 || T.n > 8) return;
     memset(&tiny, 0, sizeof(tiny));
-    CK(cudaMemcpyAsync(h_scal, T.plo(), T.n * 8, cudaMemcpyDeviceToHost, st));
-    if (KW == 2) CK(cudaMemcpyAsync((u64*)h_scal + 8, T.phi(), T.n * 8, cudaMemcpyDeviceToHost, st));
+    to_host(T.plo(), (size_t)T.n * 8);
+    if (KW == 2) to_host(T.phi(), (size_t)T.n * 8, 16);
     sync();
     for (u32 j = 0; j < T.n; ++j) {
       tiny.lo[j] = ((u64*)h_scal)[j];
@@ -525,17 +571,19 @@ struct Engine {
       if (KW == 2) CK(cudaMemcpyAsync(khi, T.phi(), nb_key, cudaMemcpyDeviceToHost, d2h));
       if (S) CK(cudaMemcpyAsync(kst, T.pst(), nb_st, cudaMemcpyDeviceToHost, d2h));
       CK(cudaEventRecord(spill_done, d2h));
+      cudaEvent_t bev;
+      if (!busy_ev_pool.empty()) { bev = busy_ev_pool.back(); busy_ev_pool.pop_back(); }
+      else CK(cudaEventCreateWithFlags(&bev, cudaEventDisableTiming));
+      CK(cudaEventRecord(bev, d2h));
       u64 *dlo = nullptr, *dhi = nullptr, *dst = nullptr;
       CK(cudaHostGetDevicePointer((void**)&dlo, klo, 0));
       if (khi) CK(cudaHostGetDevicePointer((void**)&dhi, khi, 0));
       if (kst) CK(cudaHostGetDevicePointer((void**)&dst, kst, 0));
       r.lo = dlo; r.hi = dhi; r.st = dst;
       led.bytes_d2h += nb_key * KW + nb_st;
-      // the spilled table's buffers go to Tn (free) once the copy is done:
-      // the compute stream waits for the copy before reusing them
-      std::swap(T, Tn);
-      T.n = 0;
-      tn_busy = true;   // Tn holds the spilled buffers until spill_done
+      // the spilled buffers are reused only after their copy completed
+      busy.push_back({T, bev});
+      T = take_table();
     } else {
       r.host = false;
       char* klo = devpool.alloc(nb_key);
@@ -563,7 +611,7 @@ struct Engine {
     if (T.n > 0 && T.n <= 8 && tiny_ok && absorb_supported((int)T.n, S)) return absorb_chunk(kd, sd, row0, a, span);
     int cur = sort_rows(kd, row0, nullptr, span);
     u32 f = flush_point(cur, span, span);
-    collapse_chunk(cur, span, f, sd, row0, nullptr, U, std::min<int64_t>(span, cfg.memory_budget));
+    collapse_chunk(cur, span, f, sd, row0, nullptr, U, tcap);
     merge_into_T();
     if (f < span) {
       spill_T();
@@ -601,7 +649,7 @@ struct Engine {
     u32 f = flush_point(cur, nmiss, span);
     if (f >= span) {
       fold_partials(nt, sd, ab_partials.as<u64>(), grid, T.pst(), st);
-      collapse_chunk(cur, nmiss, span, sd, row0, nullptr, U, std::min<int64_t>(nmiss, cfg.memory_budget));
+      collapse_chunk(cur, nmiss, span, sd, row0, nullptr, U, tcap);
       merge_into_T();
       refresh_tiny();
       return a + span;
@@ -620,7 +668,7 @@ struct Engine {
       ph_end(ISA_PH_ABSORB, f, (int64_t)f * absorb_row_bytes);
       fold_partials(nt, sd, ab_partials.as<u64>(), g2, T.pst(), st);
     }
-    collapse_chunk(cur, nmiss, f, sd, row0, nullptr, U, std::min<int64_t>(nmiss, cfg.memory_budget));
+    collapse_chunk(cur, nmiss, f, sd, row0, nullptr, U, tcap);
     merge_into_T();
     spill_T();
     return a + f;
@@ -685,7 +733,6 @@ struct Engine {
     int64_t total = 0;
     for (auto& r : runs) total += r.rows;
     CK(cudaStreamWaitEvent(st, spill_done, 0));
-    tn_busy = false;
     int64_t W = cfg.merge_window_rows > 0 ? cfg.merge_window_rows : ((int64_t)48 << 20);
     W = std::max<int64_t>(W, (int64_t)k * 64);
     // ---- plan windows from sampled keys (every F-th row of each run)
@@ -831,8 +878,12 @@ struct Engine {
     runs.clear();
     pinned.reset();
     devpool.reset();
-    T.n = U.n = Tn.n = result.n = 0;
-    tn_busy = false;
+    T.n = U.n = result.n = 0;
+    for (auto& b : busy) {   // the previous execute synchronized: every copy is done
+      spare.push_back(b.t);
+      busy_ev_pool.push_back(b.ev);
+    }
+    busy.clear();
     memset(phases, 0, sizeof(phases));
     for (auto& r : recs) { ev_pool.push_back(r.a); ev_pool.push_back(r.b); }
     recs.clear();
@@ -840,7 +891,11 @@ struct Engine {
     if (n < 0) throw IsaError(ISA_ERR_INVALID_INPUT, "negative row count");
     led.rows_seen = n;
     if (n == 0) { led.kernel_launches = 0; return 0; }
-    T.reserve(std::min<int64_t>(cfg.memory_budget, n) + 1, KW, S);
+    // every run-generation table holds up to M groups: size them once so
+    // swapping tables never reallocates (cudaFree would synchronize)
+    tcap = (size_t)std::min<int64_t>(cfg.memory_budget, n) + 1;
+    T.reserve(tcap, KW, S);
+    U.reserve(tcap, KW, S);
     auto t0 = std::chrono::steady_clock::now();
     cudaEvent_t rg0 = ev_get(), rg1 = ev_get(), wm1 = ev_get();
     CK(cudaEventRecord(rg0, st));

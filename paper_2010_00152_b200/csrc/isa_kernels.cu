@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const u64* __restrict__ 
 }
 
 template <int KW>
-__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const u64* __restrict__ lo_in, const u64* __restrict__ hi_in,
+__global__ void __launch_bounds__(RS_THREADS, 2) k_rs_scatter(const u64* __restrict__ lo_in, const u64* __restrict__ hi_in,
                                                          const u32* __restrict__ v_in, u64* __restrict__ lo_out,
                                                          u64* __restrict__ hi_out, u32* __restrict__ v_out, u32 n,
                                                          int shift, const u32* __restrict__ tile_off, u32 ntiles) {
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const u64* __restrict
   __syncthreads();
 
   u64 lo[RS_ITEMS], hi[RS_ITEMS];
-  u32 v[RS_ITEMS], off[RS_ITEMS], dg[RS_ITEMS];
+  u32 v[RS_ITEMS], off[RS_ITEMS];
   const u32 lt = lanemask_lt();
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
@@ -185,7 +185,6 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const u64* __restrict
     }
     cnt = __shfl_sync(0xffffffffu, cnt, leader);
     off[it] = cnt + __popc(peers & lt);
-    dg[it] = d;
     __syncwarp();
   }
   __syncthreads();
@@ -209,7 +208,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const u64* __restrict
   for (int it = 0; it < RS_ITEMS; ++it) {
     u32 li = w * RS_WARP_ITEMS + it * 32 + lane;
     if (li < tile_n) {
-      u32 d = dg[it];
+      u32 d = digit_of(hi[it], lo[it], shift);
       u32 p = dstart[d] + wcnt[w * 256 + d] + off[it];
       s_lo[p] = lo[it];
       if (KW == 2) s_hi[p] = hi[it];
@@ -338,6 +337,16 @@ void keys_varying(int KW, const u64* lo, const u64* hi, u32 n, u64* varying, cud
   else klaunch(k_keys_varying<1>, g, 256, 0, st, lo, hi, n, varying);
 }
 
+// Small device -> host reads through mapped pinned memory: the copy engines
+// stay free for bulk spill/readback copies (a 4-byte cudaMemcpyAsync would
+// queue behind a 200 MB spill on the same engine).
+__global__ void k_read_words(u32* __restrict__ dst_mapped, const u32* __restrict__ src, u32 nwords) {
+  for (u32 i = threadIdx.x; i < nwords; i += blockDim.x) dst_mapped[i] = src[i];
+}
+void read_words(u32* dst_mapped, const u32* src, u32 nwords, cudaStream_t st) {
+  klaunch(k_read_words, 1, 64, 0, st, dst_mapped, src, nwords);
+}
+
 __global__ void k_iota(u32* v, u32 n) {
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = i;
 }
@@ -418,18 +427,31 @@ __global__ void k_head_flags(const u64* __restrict__ lo, const u64* __restrict__
   }
 }
 
+template <int MS>
 __device__ __forceinline__ void load_state_row(const SlotDesc& sd, i64 row0, const u64* __restrict__ st_in, u32 v,
-                                               u64* s) {
+                                               u64 (&s)[MS]) {
   const int S = sd.nslots;
   if (st_in) {
     const u64* p = st_in + (size_t)v * S;
-    for (int k = 0; k < S; ++k) s[k] = p[k];
+#pragma unroll
+    for (int k = 0; k < MS; ++k)
+      if (k < S) s[k] = p[k];
   } else {
-    for (int k = 0; k < S; ++k) s[k] = load_slot_value(sd.src[k], sd.type[k], sd.dtype[k], sd.ptr[k], row0 + v);
+#pragma unroll
+    for (int k = 0; k < MS; ++k) {
+      if (k < S) {
+        const int a = sd.alias[k];
+        u64 x = 0;
+#pragma unroll
+        for (int q = 0; q < k; ++q)
+          if (q == a) x = s[q];
+        s[k] = a >= 0 ? x : load_slot_value(sd.src[k], sd.type[k], sd.dtype[k], sd.ptr[k], row0 + v);
+      }
+    }
   }
 }
 
-template <int KW>
+template <int KW, int MS>
 __global__ void k_seg_reduce(const u64* __restrict__ lo, const u64* __restrict__ hi, const u32* __restrict__ val,
                              u32 m, u32 limit, SlotDesc sd, i64 row0, const u64* __restrict__ st_in,
                              const u32* __restrict__ hpos, u64* __restrict__ out_lo, u64* __restrict__ out_hi,
@@ -439,59 +461,88 @@ __global__ void k_seg_reduce(const u64* __restrict__ lo, const u64* __restrict__
   const u32 i0 = t * CL_ITEMS;
   if (i0 >= m) return;
   const u32 i1 = min(i0 + CL_ITEMS, m);
-  u64 acc[ISA_MAX_SLOTS];
-  u64 cur[ISA_MAX_SLOTS];
+  u64 acc[MS];
+  u64 cur[MS];
+#pragma unroll
+  for (int k = 0; k < MS; ++k) acc[k] = cur[k] = 0;
   bool have = false, lead = true;
   u32 slot = 0;
   u64 prev_lo = 0, prev_hi = 0;
   if (i0 > 0) { prev_lo = lo[i0 - 1]; prev_hi = KW == 2 ? hi[i0 - 1] : 0; }
   partial_slot[t] = 0xFFFFFFFFu;
+  auto flush = [&]() {
+    if (lead) {
+#pragma unroll
+      for (int k = 0; k < MS; ++k)
+        if (k < S) partial[(size_t)t * S + k] = acc[k];
+      partial_slot[t] = hpos[i0] - 1;
+    } else {
+#pragma unroll
+      for (int k = 0; k < MS; ++k)
+        if (k < S) out_st[(size_t)slot * S + k] = acc[k];
+    }
+  };
   for (u32 i = i0; i < i1; ++i) {
     u64 l = lo[i], h = KW == 2 ? hi[i] : 0;
     u32 v = val[i];
     bool head = (i == 0) || !key_eq<KW>(h, l, prev_hi, prev_lo);
     prev_lo = l; prev_hi = h;
     if (v >= limit) continue;
-    if (S) load_state_row(sd, row0, st_in, v, cur);
+    if (S) load_state_row<MS>(sd, row0, st_in, v, cur);
     if (head) {
-      if (have) {
-        if (lead) {
-          for (int k = 0; k < S; ++k) partial[(size_t)t * S + k] = acc[k];
-          partial_slot[t] = hpos[i0] - 1;
-        } else {
-          for (int k = 0; k < S; ++k) out_st[(size_t)slot * S + k] = acc[k];
-        }
-      }
+      if (have) flush();
       have = true; lead = false;
       slot = hpos[i];
       out_lo[slot] = l;
       if (KW == 2) out_hi[slot] = h;
-      for (int k = 0; k < S; ++k) acc[k] = cur[k];
+#pragma unroll
+      for (int k = 0; k < MS; ++k) acc[k] = cur[k];
     } else if (!have) {
       have = true;
-      for (int k = 0; k < S; ++k) acc[k] = cur[k];
+#pragma unroll
+      for (int k = 0; k < MS; ++k) acc[k] = cur[k];
     } else {
-      for (int k = 0; k < S; ++k) acc[k] = combine_slot(sd.op[k], sd.type[k], acc[k], cur[k]);
+#pragma unroll
+      for (int k = 0; k < MS; ++k)
+        if (k < S) acc[k] = combine_slot(sd.op[k], sd.type[k], acc[k], cur[k]);
     }
   }
-  if (have) {
-    if (lead) {
-      for (int k = 0; k < S; ++k) partial[(size_t)t * S + k] = acc[k];
-      partial_slot[t] = hpos[i0] - 1;
-    } else {
-      for (int k = 0; k < S; ++k) out_st[(size_t)slot * S + k] = acc[k];
-    }
-  }
+  if (have) flush();
 }
 
+// Carries of segments that span several threads: consecutive threads that
+// carry into the same output slot are first combined inside the warp (a
+// segmented shuffle reduction toward the first lane of each run), then one
+// atomic per (warp, slot) — heavy keys (Zipf) would otherwise serialize
+// hundreds of thousands of same-address atomics.
+template <int MS>
 __global__ void k_seg_fixup(u32 nthreads, SlotDesc sd, const u64* __restrict__ partial,
                             const u32* __restrict__ partial_slot, u64* __restrict__ out_st) {
   const int S = sd.nslots;
-  for (u32 t = blockIdx.x * blockDim.x + threadIdx.x; t < nthreads; t += gridDim.x * blockDim.x) {
-    u32 slot = partial_slot[t];
-    if (slot == 0xFFFFFFFFu) continue;
-    for (int k = 0; k < S; ++k)
-      atomic_combine(out_st + (size_t)slot * S + k, sd.op[k], sd.type[k], partial[(size_t)t * S + k]);
+  const int lane = threadIdx.x & 31;
+  for (u32 base = blockIdx.x * blockDim.x; base < nthreads; base += gridDim.x * blockDim.x) {
+    const u32 t = base + threadIdx.x;
+    u32 slot = t < nthreads ? partial_slot[t] : 0xFFFFFFFFu;
+    u64 x[MS];
+#pragma unroll
+    for (int k = 0; k < MS; ++k) x[k] = (k < S && slot != 0xFFFFFFFFu) ? partial[(size_t)t * S + k] : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const u32 ys = __shfl_down_sync(0xffffffffu, slot, off);
+      const bool take = lane + off < 32 && ys == slot && slot != 0xFFFFFFFFu;
+#pragma unroll
+      for (int k = 0; k < MS; ++k) {
+        const u64 y = __shfl_down_sync(0xffffffffu, x[k], off);
+        if (k < S && take) x[k] = combine_slot(sd.op[k], sd.type[k], x[k], y);
+      }
+    }
+    const u32 prev = __shfl_up_sync(0xffffffffu, slot, 1);
+    const bool head = (lane == 0 || prev != slot) && slot != 0xFFFFFFFFu;
+    if (head) {
+#pragma unroll
+      for (int k = 0; k < MS; ++k)
+        if (k < S) atomic_combine(out_st + (size_t)slot * S + k, sd.op[k], sd.type[k], x[k]);
+    }
   }
 }
 
@@ -508,13 +559,21 @@ void collapse(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, u32 l
   scan_exclusive_u32(tmp.flags, m, tmp.scan_tmp, tmp.total, st);
   u32 nthreads = (m + CL_ITEMS - 1) / CL_ITEMS;
   int blocks = (nthreads + 127) / 128;
-  if (KW == 2)
-    klaunch(k_seg_reduce<2>, blocks, 128, 0, st, lo, hi, val, m, limit, sd, row0, st_in, tmp.flags, out_lo, out_hi,
-                                             out_st, tmp.partial, tmp.partial_slot);
-  else
-    klaunch(k_seg_reduce<1>, blocks, 128, 0, st, lo, hi, val, m, limit, sd, row0, st_in, tmp.flags, out_lo, out_hi,
-                                             out_st, tmp.partial, tmp.partial_slot);
-  if (sd.nslots) klaunch(k_seg_fixup, grid_for(nthreads, 256), 256, 0, st, nthreads, sd, tmp.partial, tmp.partial_slot, out_st);
+  const int S = sd.nslots;
+#define SR_LAUNCH(K, M) klaunch(k_seg_reduce<K, M>, blocks, 128, 0, st, lo, hi, val, m, limit, sd, row0, st_in, \
+                                tmp.flags, out_lo, out_hi, out_st, tmp.partial, tmp.partial_slot)
+#define SR_KW(K) { if (S <= 1) SR_LAUNCH(K, 1); else if (S <= 2) SR_LAUNCH(K, 2); else if (S <= 4) SR_LAUNCH(K, 4); \
+                   else if (S <= 8) SR_LAUNCH(K, 8); else SR_LAUNCH(K, 16); }
+  if (KW == 2) SR_KW(2) else SR_KW(1)
+#undef SR_KW
+#undef SR_LAUNCH
+  if (S) {
+    const int g = grid_for(nthreads, 256);
+    if (S <= 2) klaunch(k_seg_fixup<2>, g, 256, 0, st, nthreads, sd, tmp.partial, tmp.partial_slot, out_st);
+    else if (S <= 4) klaunch(k_seg_fixup<4>, g, 256, 0, st, nthreads, sd, tmp.partial, tmp.partial_slot, out_st);
+    else if (S <= 8) klaunch(k_seg_fixup<8>, g, 256, 0, st, nthreads, sd, tmp.partial, tmp.partial_slot, out_st);
+    else klaunch(k_seg_fixup<16>, g, 256, 0, st, nthreads, sd, tmp.partial, tmp.partial_slot, out_st);
+  }
 }
 
 // ============================================================= merge ====
@@ -532,7 +591,7 @@ __global__ void k_rank(const u64* __restrict__ x_lo, const u64* __restrict__ x_h
 
 struct OpsArr { int op[ISA_MAX_SLOTS]; int type[ISA_MAX_SLOTS]; };
 
-template <int KW>
+template <int KW, int MS>
 __global__ void k_merge_write_a(const u64* __restrict__ a_lo, const u64* __restrict__ a_hi,
                                 const u64* __restrict__ a_st, u32 na, const u64* __restrict__ b_st,
                                 const u32* __restrict__ rank, const u32* __restrict__ mpre,
@@ -544,10 +603,13 @@ __global__ void k_merge_write_a(const u64* __restrict__ a_lo, const u64* __restr
     c_lo[o] = a_lo[i];
     if (KW == 2) c_hi[o] = a_hi[i];
     bool mt = match[i] != 0;
-    for (int k = 0; k < S; ++k) {
-      u64 s = a_st[(size_t)i * S + k];
-      if (mt) s = combine_slot(ops.op[k], ops.type[k], s, b_st[(size_t)j * S + k]);
-      c_st[(size_t)o * S + k] = s;
+#pragma unroll
+    for (int k = 0; k < MS; ++k) {
+      if (k < S) {
+        u64 s = a_st[(size_t)i * S + k];
+        if (mt) s = combine_slot(ops.op[k], ops.type[k], s, b_st[(size_t)j * S + k]);
+        c_st[(size_t)o * S + k] = s;
+      }
     }
   }
 }
@@ -593,8 +655,13 @@ void merge_combine(int KW, int S, const int* ops, const int* types, const u64* a
     klaunch(k_copy_u32, grid_for(na, 256), 256, 0, st, tmp.match_a, pre_a, na);
     scan_exclusive_u32(pre_a, na, tmp.scan_tmp, tmp.total, st);
     int g = grid_for(na, 256);
-    if (KW == 2) klaunch(k_merge_write_a<2>, g, 256, 0, st, a_lo, a_hi, a_st, na, b_st, tmp.rank_a, pre_a, tmp.match_a, S, oa, c_lo, c_hi, c_st);
-    else klaunch(k_merge_write_a<1>, g, 256, 0, st, a_lo, a_hi, a_st, na, b_st, tmp.rank_a, pre_a, tmp.match_a, S, oa, c_lo, c_hi, c_st);
+#define MW_LAUNCH(K, M) klaunch(k_merge_write_a<K, M>, g, 256, 0, st, a_lo, a_hi, a_st, na, b_st, tmp.rank_a, pre_a, \
+                                tmp.match_a, S, oa, c_lo, c_hi, c_st)
+#define MW_KW(K) { if (S <= 1) MW_LAUNCH(K, 1); else if (S <= 2) MW_LAUNCH(K, 2); else if (S <= 4) MW_LAUNCH(K, 4); \
+                   else if (S <= 8) MW_LAUNCH(K, 8); else MW_LAUNCH(K, 16); }
+    if (KW == 2) MW_KW(2) else MW_KW(1)
+#undef MW_KW
+#undef MW_LAUNCH
   } else {
     cudaMemsetAsync(tmp.total, 0, sizeof(u32), st);
   }

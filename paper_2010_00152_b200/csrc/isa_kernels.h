@@ -33,6 +33,8 @@ void build_keys(int KW, const KeyDesc& kd, int64_t row0, const u32* pos, u32 n,
 // varying |= key ^ key[0] for an existing SoA key array
 void keys_varying(int KW, const u64* lo, const u64* hi, u32 n, u64* varying, cudaStream_t st);
 void iota_u32(u32* v, u32 n, cudaStream_t st);
+// copy nwords u32 from device memory to mapped pinned host memory (kernel, not a copy engine)
+void read_words(u32* dst_mapped, const u32* src, u32 nwords, cudaStream_t st);
 
 // ---- flush analysis ------------------------------------------------------
 // For each head of the sorted chunk (key != previous key) whose key is absent
