@@ -454,6 +454,16 @@ struct Engine {
     for (int i = 0; i < 2; ++i) { b.lo[i] = s_lo[i].as<u64>(); b.hi[i] = s_hi[i].as<u64>(); b.val[i] = s_val[i].as<u32>(); }
     b.tile_hist = tile_hist.as<u32>();
     b.scan_tmp = scan_tmp.as<u32>();
+    if (KW == 2 && hb >= 64 && lb < 64) {
+      // 128-bit keys whose high word varies: sort on the high word, then
+      // finish runs of equal high words with a stable sort on the low word
+      // (half the radix passes when high words are nearly unique)
+      int cur = radix_sort_pairs(KW, b, m, std::max(lb, 64), hb + 1, st, nullptr);
+      CK(cudaMemsetAsync(dscal32(5), 0, sizeof(u32), st));
+      sort_small_segments(b.lo[cur], b.hi[cur], b.val[cur], m, 64, dscal32(5), st);
+      if (read_u32(dscal32(5)) == 0) return cur;
+      return radix_sort_pairs(KW, b, m, lb, hb + 1, st, nullptr, cur);
+    }
     return radix_sort_pairs(KW, b, m, lb, hb + 1, st, nullptr);
   }
 

@@ -237,8 +237,9 @@ static size_t rs_scatter_smem(int KW) {
 
 size_t sort_hist_words(u32 n) { return (size_t)256 * ((n + RS_TILE - 1) / RS_TILE); }
 
-int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStream_t st, int64_t* launches) {
-  int cur = 0;
+int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStream_t st, int64_t* launches,
+                     int start) {
+  int cur = start;
   if (n <= 1 || bit_hi <= bit_lo) return cur;
   static bool attr_set[3] = {false, false, false};
   if (!attr_set[KW]) {
@@ -269,6 +270,42 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
   return cur;
 }
 
+static int grid_for(u64 n, int threads, int cap = 148 * 16);
+
+// 128-bit keys sorted on the high word only: finish every run of equal
+// high words (usually exact duplicates or rare collisions) with a stable
+// insertion sort on the low word.  A run longer than maxlen sets *too_long
+// (the caller then completes the sort with full LSD passes).
+__global__ void k_sort_small_segments(u64* __restrict__ lo, const u64* __restrict__ hi, u32* __restrict__ val, u32 n,
+                                      u32 maxlen, u32* __restrict__ too_long) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const u64 h = hi[i];
+    if (i > 0 && hi[i - 1] == h) continue;   // not the first element of a run
+    u32 j = i + 1;
+    while (j < n && hi[j] == h) {
+      ++j;
+      if (j - i > maxlen) break;
+    }
+    if (j - i > maxlen) { *too_long = 1u; continue; }
+    for (u32 a = i + 1; a < j; ++a) {
+      const u64 kl = lo[a];
+      const u32 kv = val[a];
+      u32 p = a;
+      while (p > i && lo[p - 1] > kl) {
+        lo[p] = lo[p - 1];
+        val[p] = val[p - 1];
+        --p;
+      }
+      lo[p] = kl;
+      val[p] = kv;
+    }
+  }
+}
+
+void sort_small_segments(u64* lo, const u64* hi, u32* val, u32 n, u32 maxlen, u32* too_long, cudaStream_t st) {
+  if (n) klaunch(k_sort_small_segments, grid_for(n, 256), 256, 0, st, lo, hi, val, n, maxlen, too_long);
+}
+
 // ======================================================= key building ====
 template <int KW>
 __global__ void k_build_keys(KeyDesc kd, i64 row0, const u32* __restrict__ pos, u32 n, u64* __restrict__ lo,
@@ -297,7 +334,7 @@ __global__ void k_build_keys(KeyDesc kd, i64 row0, const u32* __restrict__ pos, 
   }
 }
 
-static int grid_for(u64 n, int threads, int cap = 148 * 16) {
+static int grid_for(u64 n, int threads, int cap) {
   u64 g = (n + threads - 1) / threads;
   if (g < 1) g = 1;
   if (g > (u64)cap) g = cap;

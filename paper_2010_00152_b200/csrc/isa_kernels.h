@@ -23,7 +23,11 @@ struct SortBufs {
   u32* scan_tmp;
 };
 size_t sort_hist_words(u32 n);
-int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStream_t st, int64_t* launches);
+int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStream_t st, int64_t* launches,
+                     int start = 0);
+// stable insertion sort by the low word of every run of equal high words
+// (length <= maxlen; longer runs set *too_long)
+void sort_small_segments(u64* lo, const u64* hi, u32* val, u32 n, u32 maxlen, u32* too_long, cudaStream_t st);
 
 // ---- key building -------------------------------------------------------
 // keys of rows row0 + (pos ? pos[i] : i), i < n  ->  lo/hi/val(=pos or i);

@@ -184,3 +184,22 @@ def test_full_scale_config2_properties():
         want = torch.zeros(6, dtype=torch.float64, device="cuda").index_add_(0, gid, w.values[f"f{i}"])
         np.testing.assert_allclose(res.states[1 + i].cpu().numpy(), want.cpu().numpy(), rtol=1e-9)
     assert op.ledger.rows_spilled == 0
+
+
+@pytest.mark.parametrize("hi_card", [2, 1000, 1 << 40])
+def test_128bit_keys_high_word_cardinality(hi_card):
+    """128-bit keys sort on the high word first and finish equal-high runs on
+    the low word; a low-cardinality high word exercises the full-LSD fallback."""
+    rng = np.random.default_rng(hi_card % 1000 + 7)
+    n = 600_000
+    k1 = rng.integers(0, hi_card, n, dtype=np.uint64)
+    k2 = rng.integers(0, 1 << 20, n, dtype=np.uint64)
+    v = rng.integers(-1000, 1000, n)
+    sch = isa.Schema([isa.ColumnSpec("a"), isa.ColumnSpec("b")],
+                     [isa.AggregateSpec("n", isa.AggregateKind.COUNT), isa.AggregateSpec("s", isa.AggregateKind.SUM, "v"),
+                      isa.AggregateSpec("m", isa.AggregateKind.MIN, "v")])
+    slots = oracle.make_states(sch, {"v": v}, n)
+    want_k, want_s = oracle.reference_aggregate([k1, k2], slots, oracle.slot_ops(sch))
+    op = isa.SortAggregate(sch, _cfg(1 << 14, 100))
+    res = op.execute_columns([_cuda(k1), _cuda(k2)], {"v": _cuda(v)})
+    _check(res, want_k, want_s)
