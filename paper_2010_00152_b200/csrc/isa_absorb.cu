@@ -20,42 +20,45 @@ namespace isa {
 // inside the chunk) costs nothing.
 #define AB_THREADS 256
 #define AB_ROWS 16
-#define AB_MAX_CELLS 48   // nt * S accumulators per thread (shared memory)
+#define AB_MAX_CELLS 54   // (nt + 1) * S accumulators per thread (shared memory)
 
 enum { CLS_ADD_I = 0, CLS_ADD_F = 1, CLS_MIN_I = 2, CLS_MAX_I = 3, CLS_MIN_F = 4, CLS_MAX_F = 5 };
 
 // Load one column for the AB_ROWS rows of this thread's batch: one dtype
 // switch per (batch, column), then an unrolled, coalesced load per row.
-template <typename T>
+// FULL: every row of the batch is valid (no per-row bounds predicate).
+template <bool FULL, typename T>
 __device__ __forceinline__ void ab_load_col(const void* p, i64 base, u32 lim, T (&out)[AB_ROWS]) {
   const T* q = (const T*)p + base;
 #pragma unroll
-  for (int k = 0; k < AB_ROWS; ++k) out[k] = ((u32)(k * AB_THREADS) < lim) ? __ldg(q + k * AB_THREADS) : T(0);
+  for (int k = 0; k < AB_ROWS; ++k)
+    out[k] = (FULL || (u32)(k * AB_THREADS) < lim) ? __ldg(q + k * AB_THREADS) : T(0);
 }
 
 // Key field (order-preserving unsigned image) of every row of the batch.
+template <bool FULL>
 __device__ __forceinline__ void ab_key_field(int dt, const void* p, i64 base, u32 lim, u64 (&f)[AB_ROWS]) {
   switch (dt) {
     case DT_U8: case DT_I8: {
-      unsigned char t[AB_ROWS]; ab_load_col(p, base, lim, t);
+      unsigned char t[AB_ROWS]; ab_load_col<FULL>(p, base, lim, t);
       const u64 x = dt == DT_I8 ? 0x80ull : 0;
 #pragma unroll
       for (int k = 0; k < AB_ROWS; ++k) f[k] = (u64)t[k] ^ x;
     } break;
     case DT_U16: case DT_I16: {
-      unsigned short t[AB_ROWS]; ab_load_col(p, base, lim, t);
+      unsigned short t[AB_ROWS]; ab_load_col<FULL>(p, base, lim, t);
       const u64 x = dt == DT_I16 ? 0x8000ull : 0;
 #pragma unroll
       for (int k = 0; k < AB_ROWS; ++k) f[k] = (u64)t[k] ^ x;
     } break;
     case DT_U32: case DT_I32: {
-      unsigned int t[AB_ROWS]; ab_load_col(p, base, lim, t);
+      unsigned int t[AB_ROWS]; ab_load_col<FULL>(p, base, lim, t);
       const u64 x = dt == DT_I32 ? 0x80000000ull : 0;
 #pragma unroll
       for (int k = 0; k < AB_ROWS; ++k) f[k] = (u64)t[k] ^ x;
     } break;
     default: {
-      unsigned long long t[AB_ROWS]; ab_load_col(p, base, lim, t);
+      unsigned long long t[AB_ROWS]; ab_load_col<FULL>(p, base, lim, t);
       const u64 x = dt == DT_I64 ? 0x8000000000000000ull : 0;
 #pragma unroll
       for (int k = 0; k < AB_ROWS; ++k) f[k] = (u64)t[k] ^ x;
@@ -64,36 +67,112 @@ __device__ __forceinline__ void ab_key_field(int dt, const void* p, i64 base, u3
 }
 
 // make_state value of every row of the batch as 8-byte slot bits.
-__device__ __forceinline__ void ab_slot_values(int src, int ty, int dt, const void* p, i64 base, u32 lim,
-                                               u64 (&v)[AB_ROWS]) {
-  if (src == SRC_ONE) {
-    const u64 one = ty == ST_F64 ? 0x3FF0000000000000ull : 1ull;
-#pragma unroll
-    for (int k = 0; k < AB_ROWS; ++k) v[k] = one;
-    return;
-  }
+template <bool FULL>
+__device__ __forceinline__ void ab_slot_values(int ty, int dt, const void* p, i64 base, u32 lim, u64 (&v)[AB_ROWS]) {
   switch (dt) {
-    case DT_F64: { unsigned long long t[AB_ROWS]; ab_load_col(p, base, lim, t);
+    case DT_F64: { unsigned long long t[AB_ROWS]; ab_load_col<FULL>(p, base, lim, t);
 #pragma unroll
       for (int k = 0; k < AB_ROWS; ++k) v[k] = t[k]; } break;
-    case DT_F32: { float t[AB_ROWS]; ab_load_col(p, base, lim, t);
+    case DT_F32: { float t[AB_ROWS]; ab_load_col<FULL>(p, base, lim, t);
 #pragma unroll
       for (int k = 0; k < AB_ROWS; ++k) v[k] = d2u((double)t[k]); } break;
-    case DT_I64: case DT_U64: { unsigned long long t[AB_ROWS]; ab_load_col(p, base, lim, t);
+    case DT_I64: case DT_U64: { unsigned long long t[AB_ROWS]; ab_load_col<FULL>(p, base, lim, t);
 #pragma unroll
       for (int k = 0; k < AB_ROWS; ++k) v[k] = ty == ST_F64 ? d2u(dt == DT_I64 ? (double)(long long)t[k] : (double)t[k]) : t[k]; } break;
-    case DT_I32: { int t[AB_ROWS]; ab_load_col(p, base, lim, t);
+    case DT_I32: { int t[AB_ROWS]; ab_load_col<FULL>(p, base, lim, t);
 #pragma unroll
       for (int k = 0; k < AB_ROWS; ++k) v[k] = ty == ST_F64 ? d2u((double)t[k]) : (u64)(i64)t[k]; } break;
-    case DT_U32: { unsigned int t[AB_ROWS]; ab_load_col(p, base, lim, t);
+    case DT_U32: { unsigned int t[AB_ROWS]; ab_load_col<FULL>(p, base, lim, t);
 #pragma unroll
       for (int k = 0; k < AB_ROWS; ++k) v[k] = ty == ST_F64 ? d2u((double)t[k]) : (u64)t[k]; } break;
-    default: {   // 8/16-bit integer columns: rare, per-row generic path
+    default: {   // 8/16-bit integer value columns: rare, per-row generic path
 #pragma unroll
       for (int k = 0; k < AB_ROWS; ++k)
-        v[k] = ((u32)(k * AB_THREADS) < lim) ? load_slot_value(src, ty, dt, p, base + k * AB_THREADS) : 0;
+        v[k] = (FULL || (u32)(k * AB_THREADS) < lim) ? load_slot_value(SRC_COL, ty, dt, p, base + k * AB_THREADS) : 0;
     } break;
   }
+}
+
+// One batch (AB_ROWS rows per thread, row k*AB_THREADS + tid).  KW = 0:
+// keys of <= 32 bits compared as u32; 1/2: one/two 64-bit words.
+template <int KW, int NT, bool FULL>
+__device__ __forceinline__ u32 ab_batch(const KeyDesc& kd, const SlotDesc& sd, const TinyTable& tt, i64 row_abs,
+                                        u32 lim, u64* __restrict__ sacc_t, u32* __restrict__ missbits_out) {
+  u64 kl[AB_ROWS], kh[AB_ROWS];
+#pragma unroll
+  for (int k = 0; k < AB_ROWS; ++k) { kl[k] = 0; kh[k] = 0; }
+  for (int col = 0; col < kd.ncols; ++col) {
+    u64 f[AB_ROWS];
+    ab_key_field<FULL>(kd.dtype[col], kd.ptr[col], row_abs, lim, f);
+    const int s = kd.shift[col], wdt = kd.width[col];
+#pragma unroll
+    for (int k = 0; k < AB_ROWS; ++k) {
+      if (KW == 0) {
+        kl[k] = (u32)kl[k] | ((u32)f[k] << s);
+      } else if (s < 64) {
+        kl[k] |= f[k] << s;
+        if (KW == 2 && s > 0 && s + wdt > 64) kh[k] |= f[k] >> (64 - s);
+      } else if (KW == 2) {
+        kh[k] |= f[k] << (s - 64);
+      }
+    }
+  }
+  // probe: table row, or NT (the trash cell) for misses and rows past the end
+  u32 hoff[AB_ROWS];
+  u32 missbits = 0;
+  u64 pc = 0;   // per-table-row 8-bit hit counters (COUNT slots)
+#pragma unroll
+  for (int k = 0; k < AB_ROWS; ++k) {
+    u32 hk = NT;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      bool eq;
+      if (KW == 0) eq = (u32)kl[k] == (u32)tt.lo[j];
+      else eq = key_eq<KW == 2 ? 2 : 1>(kh[k], kl[k], tt.hi[j], tt.lo[j]);
+      hk = eq ? (u32)j : hk;
+    }
+    const bool valid = FULL || (u32)(k * AB_THREADS) < lim;
+    if (!valid) hk = NT;
+    if (valid && hk == (u32)NT) missbits |= 1u << k;
+    if (hk < (u32)NT) pc += 1ull << (8 * hk);
+    hoff[k] = hk * (AB_THREADS * 8);
+  }
+  const int S = sd.nslots;
+  for (int s = 0; s < S; ++s) {
+    const int op = sd.op[s], ty = sd.type[s];
+    char* acc = (char*)(sacc_t + (size_t)s * (NT + 1) * AB_THREADS);
+    if (sd.src[s] == SRC_ONE) {
+      if (op == OP_ADD && ty == ST_I64) {   // COUNT / AVG count: from the packed counters
+#pragma unroll
+        for (int j = 0; j < NT; ++j) ((u64*)acc)[j * AB_THREADS] += (pc >> (8 * j)) & 0xFFull;
+      } else {
+        const u64 one = ty == ST_F64 ? 0x3FF0000000000000ull : 1ull;
+#pragma unroll
+        for (int k = 0; k < AB_ROWS; ++k) { u64* a = (u64*)(acc + hoff[k]); *a = combine_slot(op, ty, *a, one); }
+      }
+      continue;
+    }
+    u64 v[AB_ROWS];
+    ab_slot_values<FULL>(ty, sd.dtype[s], sd.ptr[s], row_abs, lim, v);
+#define AB_LOOP(STMT)                                   \
+  _Pragma("unroll") for (int k = 0; k < AB_ROWS; ++k) { \
+    u64* a = (u64*)(acc + hoff[k]);                     \
+    STMT;                                               \
+  }
+    if (op == OP_ADD) {
+      if (ty == ST_F64) AB_LOOP(*a = d2u(u2d(*a) + u2d(v[k])))
+      else AB_LOOP(*a = *a + v[k])
+    } else if (ty == ST_F64) {
+      if (op == OP_MIN) AB_LOOP(*a = combine_slot(OP_MIN, ST_F64, *a, v[k]))
+      else AB_LOOP(*a = combine_slot(OP_MAX, ST_F64, *a, v[k]))
+    } else {
+      if (op == OP_MIN) AB_LOOP(*a = combine_slot(OP_MIN, ST_I64, *a, v[k]))
+      else AB_LOOP(*a = combine_slot(OP_MAX, ST_I64, *a, v[k]))
+    }
+#undef AB_LOOP
+  }
+  *missbits_out = missbits;
+  return missbits;
 }
 
 template <int KW, int NT>
@@ -101,10 +180,11 @@ __global__ void __launch_bounds__(AB_THREADS) k_absorb_tiny(KeyDesc kd, SlotDesc
                                                            TinyTable tt, u32 rows_per_cta,
                                                            u64* __restrict__ partials, u32* __restrict__ miss_buf,
                                                            u32* __restrict__ miss_cnt) {
-  // Per-thread accumulators sacc[s][j][tid]: the address of (slot s, table
-  // row j) for thread tid is ((s*NT + j) * AB_THREADS + tid) * 8 bytes, so a
-  // warp's 32 accesses hit 32 consecutive 8-byte words whatever rows its
-  // lanes matched: conflict-free, and the cost per row does not grow with NT.
+  // Per-thread accumulators sacc[s][j][tid], j = NT is a trash cell for
+  // misses: the address of (slot s, table row j) for thread tid is
+  // ((s*(NT+1) + j) * AB_THREADS + tid) * 8 bytes, so a warp's 32 accesses
+  // hit 32 consecutive 8-byte words whatever rows its lanes matched
+  // (conflict-free, branch-free), and the cost per row does not grow with NT.
   extern __shared__ __align__(16) u64 sacc[];
   __shared__ u32 sw[8];
   const int S = sd.nslots;
@@ -113,66 +193,21 @@ __global__ void __launch_bounds__(AB_THREADS) k_absorb_tiny(KeyDesc kd, SlotDesc
   const u32 r0 = c * rows_per_cta;
   const u32 r1 = min(r0 + rows_per_cta, n);
   for (int s = 0; s < S; ++s)
-    for (int j = 0; j < NT; ++j) sacc[(s * NT + j) * AB_THREADS + tid] = identity_slot(sd.op[s], sd.type[s]);
+    for (int j = 0; j <= NT; ++j) sacc[(s * (NT + 1) + j) * AB_THREADS + tid] = identity_slot(sd.op[s], sd.type[s]);
 
   u32 nmiss = 0;
   for (u32 base = r0; base < r1; base += AB_THREADS * AB_ROWS) {
     const u32 row_t = base + tid;                       // this thread's first row of the batch
     const u32 lim = r1 > row_t ? r1 - row_t : 0;        // rows k*AB_THREADS < lim are valid
-    u64 kl[AB_ROWS], kh[AB_ROWS];
-#pragma unroll
-    for (int k = 0; k < AB_ROWS; ++k) { kl[k] = 0; kh[k] = 0; }
-    for (int col = 0; col < kd.ncols; ++col) {
-      u64 f[AB_ROWS];
-      ab_key_field(kd.dtype[col], kd.ptr[col], row0 + row_t, lim, f);
-      const int s = kd.shift[col], wdt = kd.width[col];
-#pragma unroll
-      for (int k = 0; k < AB_ROWS; ++k) {
-        if (s < 64) {
-          kl[k] |= f[k] << s;
-          if (KW == 2 && s > 0 && s + wdt > 64) kh[k] |= f[k] >> (64 - s);
-        } else if (KW == 2) {
-          kh[k] |= f[k] << (s - 64);
-        }
-      }
-    }
-    u32 hit[AB_ROWS];   // table row; NT = miss; 0xFF = past the end
-    bool anymiss = false;
-#pragma unroll
-    for (int k = 0; k < AB_ROWS; ++k) {
-      u32 hk = NT;
-#pragma unroll
-      for (int j = 0; j < NT; ++j) hk = key_eq<KW>(kh[k], kl[k], tt.hi[j], tt.lo[j]) ? (u32)j : hk;
-      if ((u32)(k * AB_THREADS) >= lim) hk = 0xFFu;
-      anymiss |= (hk == (u32)NT);
-      hit[k] = hk;
-    }
-    for (int s = 0; s < S; ++s) {
-      const int op = sd.op[s], ty = sd.type[s];
-      u64 v[AB_ROWS];
-      ab_slot_values(sd.src[s], ty, sd.dtype[s], sd.ptr[s], row0 + row_t, lim, v);
-      u64* acc = sacc + (size_t)s * NT * AB_THREADS + tid;
-      const int cls = op == OP_ADD ? (ty == ST_F64 ? CLS_ADD_F : CLS_ADD_I)
-                                   : (op == OP_MIN ? (ty == ST_F64 ? CLS_MIN_F : CLS_MIN_I)
-                                                   : (ty == ST_F64 ? CLS_MAX_F : CLS_MAX_I));
-#define AB_LOOP(STMT)                                                   \
-  _Pragma("unroll") for (int k = 0; k < AB_ROWS; ++k) {                 \
-    if (hit[k] < (u32)NT) { u64* a = acc + hit[k] * AB_THREADS; STMT; } \
-  }
-      switch (cls) {
-        case CLS_ADD_F: AB_LOOP(*a = d2u(u2d(*a) + u2d(v[k]))) break;
-        case CLS_ADD_I: AB_LOOP(*a = *a + v[k]) break;
-        case CLS_MIN_I: AB_LOOP(*a = combine_slot(OP_MIN, ST_I64, *a, v[k])) break;
-        case CLS_MAX_I: AB_LOOP(*a = combine_slot(OP_MAX, ST_I64, *a, v[k])) break;
-        case CLS_MIN_F: AB_LOOP(*a = combine_slot(OP_MIN, ST_F64, *a, v[k])) break;
-        default: AB_LOOP(*a = combine_slot(OP_MAX, ST_F64, *a, v[k])) break;
-      }
-#undef AB_LOOP
-    }
+    u32 missbits;
+    if (base + AB_THREADS * AB_ROWS <= r1)
+      ab_batch<KW, NT, true>(kd, sd, tt, row0 + row_t, lim, sacc + tid, &missbits);
+    else
+      ab_batch<KW, NT, false>(kd, sd, tt, row0 + row_t, lim, sacc + tid, &missbits);
     // ordered miss compaction (row order = (k, tid) within this step)
-    if (__syncthreads_or(anymiss)) {
+    if (__syncthreads_or(missbits != 0)) {
       for (int k = 0; k < AB_ROWS; ++k) {
-        u32 f = (hit[k] == (u32)NT) ? 1u : 0u;
+        u32 f = (missbits >> k) & 1u;
         u32 tot;
         u32 pre = block_excl_scan256(f, sw, &tot);
         if (f) miss_buf[(size_t)c * rows_per_cta + nmiss + pre] = base + k * AB_THREADS + tid;
@@ -186,7 +221,7 @@ __global__ void __launch_bounds__(AB_THREADS) k_absorb_tiny(KeyDesc kd, SlotDesc
   for (int q = w; q < S * NT; q += AB_THREADS / 32) {
     const int s = q / NT, j = q % NT;
     const int op = sd.op[s], ty = sd.type[s];
-    const u64* row = sacc + (size_t)q * AB_THREADS;
+    const u64* row = sacc + (size_t)(s * (NT + 1) + j) * AB_THREADS;
     u64 x = row[lane];
     for (int i = lane + 32; i < AB_THREADS; i += 32) x = combine_slot(op, ty, x, row[i]);
     for (int o = 16; o; o >>= 1) x = combine_slot(op, ty, x, __shfl_xor_sync(0xffffffffu, x, o));
@@ -220,7 +255,7 @@ bool tiny_perfect_hash(int KW, TinyTable& tt, int nt) {
   return false;
 }
 
-bool absorb_supported(int nt, int nslots) { return nt >= 1 && nt <= 8 && nt * nslots <= AB_MAX_CELLS; }
+bool absorb_supported(int nt, int nslots) { return nt >= 1 && nt <= 8 && (nt + 1) * nslots <= AB_MAX_CELLS; }
 
 void absorb_geometry(u32 n, int num_sms, u32* grid, u32* rows_per_cta) {
   const u32 step = AB_THREADS * AB_ROWS;
@@ -237,7 +272,7 @@ template <int KW, int NT>
 static void absorb_launch(const KeyDesc& kd, const SlotDesc& sd, int64_t row0, u32 n, const TinyTable& tt, u32 grid,
                           u32 rpc, u64* partials, u32* miss_buf, u32* miss_cnt, cudaStream_t st) {
   static bool attr = false;
-  const size_t smem = (size_t)sd.nslots * NT * AB_THREADS * 8;
+  const size_t smem = (size_t)sd.nslots * (NT + 1) * AB_THREADS * 8;
   if (!attr) {
     cudaFuncSetAttribute(k_absorb_tiny<KW, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          AB_MAX_CELLS * AB_THREADS * 8);
@@ -259,6 +294,10 @@ static void absorb_dispatch(int nt, const KeyDesc& kd, const SlotDesc& sd, int64
 
 void absorb_tiny(int KW, int nt, const KeyDesc& kd, const SlotDesc& sd, int64_t row0, u32 n, const TinyTable& tt,
                  u32 grid, u32 rows_per_cta, u64* partials, u32* miss_buf, u32* miss_cnt, cudaStream_t st) {
+  if (KW == 1 && kd.total_bits <= 32) {   // narrow keys: 32-bit compares
+    absorb_dispatch<0>(nt, kd, sd, row0, n, tt, grid, rows_per_cta, partials, miss_buf, miss_cnt, st);
+    return;
+  }
   if (KW == 2) absorb_dispatch<2>(nt, kd, sd, row0, n, tt, grid, rows_per_cta, partials, miss_buf, miss_cnt, st);
   else absorb_dispatch<1>(nt, kd, sd, row0, n, tt, grid, rows_per_cta, partials, miss_buf, miss_cnt, st);
 }
