@@ -83,6 +83,8 @@ typedef struct isa_config {
   int64_t chunk_rows_max;    /* 0 = auto: largest run-generation chunk */
   int64_t window_rows;       /* 0 = auto: host-input staging window (rows) */
   int64_t merge_window_rows; /* 0 = auto: wide-merge key-range window capacity (rows) */
+  int32_t preaggregate;      /* tile-local pre-aggregation before the chunk sort: 0 auto, 1 always, 2 never */
+  int32_t reserved;
 } isa_config;
 
 typedef struct isa_schema {

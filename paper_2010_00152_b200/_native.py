@@ -68,6 +68,8 @@ class IsaConfig(ctypes.Structure):
         ("chunk_rows_max", ctypes.c_int64),
         ("window_rows", ctypes.c_int64),
         ("merge_window_rows", ctypes.c_int64),
+        ("preaggregate", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 

@@ -395,7 +395,7 @@ void iota_u32(u32* v, u32 n, cudaStream_t st) {
 template <int KW>
 __global__ void k_new_heads(const u64* __restrict__ lo, const u64* __restrict__ hi, const u32* __restrict__ val,
                             u32 m, const u64* __restrict__ T_lo, const u64* __restrict__ T_hi, u32 t,
-                            u32* __restrict__ bitmap, u32* __restrict__ n_new) {
+                            u32* __restrict__ bitmap, u32* __restrict__ n_new, const u32* __restrict__ firstpos) {
   u32 cnt = 0;
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
     u64 l = lo[i], h = KW == 2 ? hi[i] : 0;
@@ -407,7 +407,7 @@ __global__ void k_new_heads(const u64* __restrict__ lo, const u64* __restrict__ 
       in_t = p < t && key_eq<KW>(KW == 2 ? T_hi[p] : 0, T_lo[p], h, l);
     }
     if (!in_t) {
-      u32 pos = val[i];
+      u32 pos = firstpos ? firstpos[val[i]] : val[i];
       atomicOr(&bitmap[pos >> 5], 1u << (pos & 31));
       ++cnt;
     }
@@ -417,11 +417,11 @@ __global__ void k_new_heads(const u64* __restrict__ lo, const u64* __restrict__ 
 }
 
 void new_heads(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, const u64* T_lo, const u64* T_hi,
-               u32 t, u32* bitmap, u32* n_new, cudaStream_t st) {
+               u32 t, u32* bitmap, u32* n_new, cudaStream_t st, const u32* firstpos) {
   if (m == 0) return;
   int g = grid_for(m, 256);
-  if (KW == 2) klaunch(k_new_heads<2>, g, 256, 0, st, lo, hi, val, m, T_lo, T_hi, t, bitmap, n_new);
-  else klaunch(k_new_heads<1>, g, 256, 0, st, lo, hi, val, m, T_lo, T_hi, t, bitmap, n_new);
+  if (KW == 2) klaunch(k_new_heads<2>, g, 256, 0, st, lo, hi, val, m, T_lo, T_hi, t, bitmap, n_new, firstpos);
+  else klaunch(k_new_heads<1>, g, 256, 0, st, lo, hi, val, m, T_lo, T_hi, t, bitmap, n_new, firstpos);
 }
 
 __global__ void k_popc_words(const u32* __restrict__ bm, u32 nw, u32* __restrict__ cnt) {

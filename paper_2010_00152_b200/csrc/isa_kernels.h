@@ -40,12 +40,22 @@ void iota_u32(u32* v, u32 n, cudaStream_t st);
 // copy nwords u32 from device memory to mapped pinned host memory (kernel, not a copy engine)
 void read_words(u32* dst_mapped, const u32* src, u32 nwords, cudaStream_t st);
 
+// ---- K1 tile-local pre-aggregation (isa_tile.cu) --------------------------
+u32 tile_rows();
+// groups of every tile of rows [row0, row0 + n): slotted layout t * tile_rows() + g
+void tile_collapse(int KW, const KeyDesc& kd, const SlotDesc& sd, int64_t row0, u32 n, u64* g_lo, u64* g_hi,
+                   u32* g_first, u64* g_st, u32* g_count, cudaStream_t st);
+// compact slotted groups into sort buffers (value = slotted index); varying |= key ^ key(group 0)
+void compact_groups(int KW, const u64* g_lo, const u64* g_hi, const u32* g_count, const u32* g_off, u32 tiles,
+                    u64* lo, u64* hi, u32* val, u64* varying, cudaStream_t st);
+
 // ---- flush analysis ------------------------------------------------------
 // For each head of the sorted chunk (key != previous key) whose key is absent
 // from the table (T_lo/T_hi, t rows): set bit val[i] in `bitmap`, count.
+// firstpos != nullptr: val[i] indexes firstpos[] (tile groups) for the row position
 void new_heads(int KW, const u64* lo, const u64* hi, const u32* val, u32 m,
                const u64* T_lo, const u64* T_hi, u32 t, u32* bitmap, u32* n_new,
-               cudaStream_t st);
+               cudaStream_t st, const u32* firstpos = nullptr);
 // position of the k-th (1-based) set bit of bitmap (nbits bits) -> *out
 void select_kth_bit(const u32* bitmap, u32 nbits, u32 k, u32* word_tmp, u32* scan_tmp,
                     u32* out, cudaStream_t st);

@@ -67,6 +67,7 @@ class SortAggConfig:
     chunk_rows_max: int = 0         # 0 = library default
     window_rows: int = 0            # host-input staging window, 0 = default
     merge_window_rows: int = 0      # wide-merge key-range window capacity, 0 = default
+    preaggregate: str = "auto"      # tile-local pre-aggregation before chunk sorts: auto | always | never
 
     def __post_init__(self):
         if self.page_capacity < 1:
@@ -82,6 +83,8 @@ class SortAggConfig:
             raise InvalidInputError(f"unknown merge mode {self.merge_mode!r}")
         if self.run_tier not in ("host", "hbm"):
             raise InvalidInputError(f"unknown run tier {self.run_tier!r}")
+        if self.preaggregate not in ("auto", "always", "never"):
+            raise InvalidInputError(f"unknown preaggregate mode {self.preaggregate!r}")
 
     @property
     def max_fanin(self):
@@ -355,6 +358,7 @@ class SortAggregate:
         cfg.chunk_rows_max = self.config.chunk_rows_max
         cfg.window_rows = self.config.window_rows
         cfg.merge_window_rows = self.config.merge_window_rows
+        cfg.preaggregate = {"auto": 0, "always": 1, "never": 2}[self.config.preaggregate]
         sch = _native.IsaSchema()
         if len(key_codes) > _native.MAX_KEY_COLS:
             raise InvalidInputError("too many key columns")

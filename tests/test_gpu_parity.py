@@ -40,7 +40,7 @@ def _cfg(memory, page, **kw):
 
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("variant", ["device", "host_input", "hbm_runs", "small_chunks"])
+@pytest.mark.parametrize("variant", ["device", "host_input", "hbm_runs", "small_chunks", "k1_always", "k1_never"])
 def test_golden_columns(name, variant):
     g = Golden(name)
     sch = g.schema()
@@ -49,6 +49,10 @@ def test_golden_columns(name, variant):
         kw["run_tier"] = "hbm"
     if variant == "small_chunks":
         kw.update(chunk_rows_max=5000, merge_window_rows=3000, window_rows=7000)
+    if variant == "k1_always":
+        kw.update(preaggregate="always", chunk_rows_max=70000)
+    if variant == "k1_never":
+        kw.update(preaggregate="never")
     op = isa.SortAggregate(sch, _cfg(g.memory, g.page, **kw))
     n = len(g.keys[0])
     if variant == "host_input":
@@ -141,28 +145,45 @@ def _oracle_case(w, memory, page=100, rel=1e-9, **kw):
     (4, 2_000_000, 1 << 16),
     (5, 3_000_000, 1 << 18),
 ])
-def test_random_vs_oracle(cfg, rows, memory):
+@pytest.mark.parametrize("pre", ["auto", "always", "never"])
+def test_random_vs_oracle(cfg, rows, memory, pre):
     kw = {"domain": 1 << 20} if cfg in (3, 5) else {}
     w = workloads.make(cfg, rows=rows, device="cpu", **kw)
     rel = 1e-5 if cfg == 3 else 1e-9
-    _oracle_case(w, memory, page=min(100, memory // 2), rel=rel)
+    _oracle_case(w, memory, page=min(100, memory // 2), rel=rel, preaggregate=pre)
 
 
-def test_ledger_matches_c_oracle_mid_scale():
+@pytest.mark.parametrize("pre", ["always", "never"])
+def test_ledger_matches_c_oracle_mid_scale(pre):
     w = workloads.config5(rows=2_000_000, device="cpu", domain=1 << 19)
     sch = w.schema
     keys_np = [k.numpy() for k in w.keys]
     slots = oracle.make_states(sch, {"v": w.values["v"].numpy()}, w.rows)
     _, _, led, cycles = oracle.rsw_sortagg(keys_np, slots, oracle.slot_ops(sch), 1 << 15, 100)
-    op = _oracle_case(w, 1 << 15)
+    op = _oracle_case(w, 1 << 15, preaggregate=pre)
     assert op.cycles == [c for c in cycles if c > 0]
     assert op.ledger.rows_spilled == led["rows_spilled"]
     assert op.runs_after_generation == led["runs"]
 
 
-def test_small_chunks_and_windows_vs_oracle():
+@pytest.mark.parametrize("pre", ["always", "never"])
+def test_small_chunks_and_windows_vs_oracle(pre):
     w = workloads.config3(rows=1_500_000, device="cpu", domain=1 << 18)
-    _oracle_case(w, 1 << 14, rel=1e-5, chunk_rows_max=20_000, merge_window_rows=50_000)
+    _oracle_case(w, 1 << 14, rel=1e-5, chunk_rows_max=100_000, merge_window_rows=50_000, preaggregate=pre)
+
+
+@pytest.mark.parametrize("memory", [1 << 12, 1 << 14])
+def test_zipf_ledger_with_tile_preaggregation(memory):
+    """Skewed keys with the tile pre-aggregation forced on: flush rows fall
+    inside tiles; run sizes and fill cycles must still equal the C oracle's."""
+    w = workloads.config3(rows=1_000_000, device="cpu", domain=1 << 16)
+    keys_np = [k.numpy() for k in w.keys]
+    vals_np = {k: v.numpy() for k, v in w.values.items()}
+    slots = oracle.make_states(w.schema, vals_np, w.rows)
+    _, _, led, cycles = oracle.rsw_sortagg(keys_np, slots, oracle.slot_ops(w.schema), memory, 100)
+    op = _oracle_case(w, memory, rel=1e-5, preaggregate="always", chunk_rows_max=150_000)
+    assert op.cycles == [c for c in cycles if c > 0]
+    assert op.run_rows and op.ledger.rows_spilled == led["rows_spilled"]
 
 
 def test_full_scale_config2_properties():

@@ -7,7 +7,9 @@ from paper_2010_00152_b200 import workloads
 c = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 w = workloads.make(c, device="cuda")
 tier = sys.argv[2] if len(sys.argv) > 2 else "host"
-op = isa.SortAggregate(w.schema, isa.SortAggConfig(memory_budget=w.memory_budget, page_capacity=100, run_tier=tier))
+pre = sys.argv[4] if len(sys.argv) > 4 else "auto"
+op = isa.SortAggregate(w.schema, isa.SortAggConfig(memory_budget=w.memory_budget, page_capacity=100, run_tier=tier,
+                                                  preaggregate=pre))
 for i in range(int(sys.argv[3]) if len(sys.argv) > 3 else 3):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     op.execute_columns(w.keys, w.values)
