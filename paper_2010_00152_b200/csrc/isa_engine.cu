@@ -631,7 +631,10 @@ struct Engine {
     const int64_t row0 = a - base;   // column element of row a
     led.chunks++;
     if (T.n > 0 && T.n <= 8 && tiny_ok && absorb_supported((int)T.n, S)) return absorb_chunk(kd, sd, row0, a, span);
-    if (k1_mode != 0 && span >= 64 * tile_rows()) return k1_chunk(kd, sd, row0, a, span);
+    // tiny chunks are not worth the extra pass in auto mode; "always" keeps
+    // it down to 4 tiles (also what the parity tests exercise)
+    const u32 k1_min = (cfg.preaggregate == 1 ? 4 : 64) * tile_rows();
+    if (k1_mode != 0 && span >= k1_min) return k1_chunk(kd, sd, row0, a, span);
     int cur = sort_rows(kd, row0, nullptr, span);
     u32 f = flush_point(cur, span, span);
     collapse_chunk(cur, span, f, sd, row0, nullptr, U, tcap);

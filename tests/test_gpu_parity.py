@@ -50,7 +50,7 @@ def test_golden_columns(name, variant):
     if variant == "small_chunks":
         kw.update(chunk_rows_max=5000, merge_window_rows=3000, window_rows=7000)
     if variant == "k1_always":
-        kw.update(preaggregate="always", chunk_rows_max=70000)
+        kw.update(preaggregate="always", chunk_rows_max=20000)
     if variant == "k1_never":
         kw.update(preaggregate="never")
     op = isa.SortAggregate(sch, _cfg(g.memory, g.page, **kw))
@@ -169,7 +169,7 @@ def test_ledger_matches_c_oracle_mid_scale(pre):
 @pytest.mark.parametrize("pre", ["always", "never"])
 def test_small_chunks_and_windows_vs_oracle(pre):
     w = workloads.config3(rows=1_500_000, device="cpu", domain=1 << 18)
-    _oracle_case(w, 1 << 14, rel=1e-5, chunk_rows_max=100_000, merge_window_rows=50_000, preaggregate=pre)
+    _oracle_case(w, 1 << 14, rel=1e-5, chunk_rows_max=20_000, merge_window_rows=50_000, preaggregate=pre)
 
 
 @pytest.mark.parametrize("memory", [1 << 12, 1 << 14])
@@ -181,7 +181,7 @@ def test_zipf_ledger_with_tile_preaggregation(memory):
     vals_np = {k: v.numpy() for k, v in w.values.items()}
     slots = oracle.make_states(w.schema, vals_np, w.rows)
     _, _, led, cycles = oracle.rsw_sortagg(keys_np, slots, oracle.slot_ops(w.schema), memory, 100)
-    op = _oracle_case(w, memory, rel=1e-5, preaggregate="always", chunk_rows_max=150_000)
+    op = _oracle_case(w, memory, rel=1e-5, preaggregate="always", chunk_rows_max=50_000)
     assert op.cycles == [c for c in cycles if c > 0]
     assert op.run_rows and op.ledger.rows_spilled == led["rows_spilled"]
 
