@@ -2,6 +2,7 @@
 #include "isa_kernels.h"
 
 #include <cstring>
+#include <algorithm>
 #include <random>
 
 namespace isa {
@@ -95,9 +96,14 @@ __device__ __forceinline__ void ab_slot_values(int ty, int dt, const void* p, i6
 
 // One batch (AB_ROWS rows per thread, row k*AB_THREADS + tid).  KW = 0:
 // keys of <= 32 bits compared as u32; 1/2: one/two 64-bit words.
+__device__ __forceinline__ bool ab_is_count(const SlotDesc& sd, int s) {
+  return sd.src[s] == SRC_ONE && sd.op[s] == OP_ADD && sd.type[s] == ST_I64;
+}
+
 template <int KW, int NT, bool FULL>
 __device__ __forceinline__ u32 ab_batch(const KeyDesc& kd, const SlotDesc& sd, const TinyTable& tt, i64 row_abs,
-                                        u32 lim, u64* __restrict__ sacc_t, u32* __restrict__ missbits_out) {
+                                        u32 lim, u64* __restrict__ sacc_t, u32* __restrict__ missbits_out,
+                                        u32 (&cnt)[NT]) {
   u64 kl[AB_ROWS], kh[AB_ROWS];
 #pragma unroll
   for (int k = 0; k < AB_ROWS; ++k) { kl[k] = 0; kh[k] = 0; }
@@ -138,14 +144,15 @@ __device__ __forceinline__ u32 ab_batch(const KeyDesc& kd, const SlotDesc& sd, c
     hoff[k] = hk * (AB_THREADS * 8);
   }
   const int S = sd.nslots;
+#pragma unroll
+  for (int j = 0; j < NT; ++j) cnt[j] += (u32)(pc >> (8 * j)) & 0xFFu;   // COUNT slots: registers
+  int cell = 0;
   for (int s = 0; s < S; ++s) {
     const int op = sd.op[s], ty = sd.type[s];
-    char* acc = (char*)(sacc_t + (size_t)s * (NT + 1) * AB_THREADS);
+    if (ab_is_count(sd, s)) continue;
+    char* acc = (char*)(sacc_t + (size_t)(cell++) * (NT + 1) * AB_THREADS);
     if (sd.src[s] == SRC_ONE) {
-      if (op == OP_ADD && ty == ST_I64) {   // COUNT / AVG count: from the packed counters
-#pragma unroll
-        for (int j = 0; j < NT; ++j) ((u64*)acc)[j * AB_THREADS] += (pc >> (8 * j)) & 0xFFull;
-      } else {
+      {
         const u64 one = ty == ST_F64 ? 0x3FF0000000000000ull : 1ull;
 #pragma unroll
         for (int k = 0; k < AB_ROWS; ++k) { u64* a = (u64*)(acc + hoff[k]); *a = combine_slot(op, ty, *a, one); }
@@ -176,7 +183,7 @@ __device__ __forceinline__ u32 ab_batch(const KeyDesc& kd, const SlotDesc& sd, c
 }
 
 template <int KW, int NT>
-__global__ void __launch_bounds__(AB_THREADS) k_absorb_tiny(KeyDesc kd, SlotDesc sd, i64 row0, u32 n,
+__global__ void __launch_bounds__(AB_THREADS, 3) k_absorb_tiny(KeyDesc kd, SlotDesc sd, i64 row0, u32 n,
                                                            TinyTable tt, u32 rows_per_cta,
                                                            u64* __restrict__ partials, u32* __restrict__ miss_buf,
                                                            u32* __restrict__ miss_cnt) {
@@ -187,13 +194,23 @@ __global__ void __launch_bounds__(AB_THREADS) k_absorb_tiny(KeyDesc kd, SlotDesc
   // (conflict-free, branch-free), and the cost per row does not grow with NT.
   extern __shared__ __align__(16) u64 sacc[];
   __shared__ u32 sw[8];
+  __shared__ u32 scnt[AB_THREADS / 32][NT];
   const int S = sd.nslots;
   const int tid = threadIdx.x;
   const u32 c = blockIdx.x;
   const u32 r0 = c * rows_per_cta;
   const u32 r1 = min(r0 + rows_per_cta, n);
-  for (int s = 0; s < S; ++s)
-    for (int j = 0; j <= NT; ++j) sacc[(s * (NT + 1) + j) * AB_THREADS + tid] = identity_slot(sd.op[s], sd.type[s]);
+  {
+    int cell = 0;
+    for (int s = 0; s < S; ++s) {
+      if (ab_is_count(sd, s)) continue;
+      for (int j = 0; j <= NT; ++j) sacc[(cell * (NT + 1) + j) * AB_THREADS + tid] = identity_slot(sd.op[s], sd.type[s]);
+      ++cell;
+    }
+  }
+  u32 cnt[NT];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) cnt[j] = 0;
 
   u32 nmiss = 0;
   for (u32 base = r0; base < r1; base += AB_THREADS * AB_ROWS) {
@@ -201,9 +218,9 @@ __global__ void __launch_bounds__(AB_THREADS) k_absorb_tiny(KeyDesc kd, SlotDesc
     const u32 lim = r1 > row_t ? r1 - row_t : 0;        // rows k*AB_THREADS < lim are valid
     u32 missbits;
     if (base + AB_THREADS * AB_ROWS <= r1)
-      ab_batch<KW, NT, true>(kd, sd, tt, row0 + row_t, lim, sacc + tid, &missbits);
+      ab_batch<KW, NT, true>(kd, sd, tt, row0 + row_t, lim, sacc + tid, &missbits, cnt);
     else
-      ab_batch<KW, NT, false>(kd, sd, tt, row0 + row_t, lim, sacc + tid, &missbits);
+      ab_batch<KW, NT, false>(kd, sd, tt, row0 + row_t, lim, sacc + tid, &missbits, cnt);
     // ordered miss compaction (row order = (k, tid) within this step)
     if (__syncthreads_or(missbits != 0)) {
       for (int k = 0; k < AB_ROWS; ++k) {
@@ -216,12 +233,30 @@ __global__ void __launch_bounds__(AB_THREADS) k_absorb_tiny(KeyDesc kd, SlotDesc
     }
   }
   __syncthreads();
-  // block reduction of the per-thread accumulators: one warp per cell
+  // COUNT totals: warp sums, then across warps
   const int lane = tid & 31, w = tid >> 5;
-  for (int q = w; q < S * NT; q += AB_THREADS / 32) {
-    const int s = q / NT, j = q % NT;
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    u32 x = cnt[j];
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) scnt[w][j] = x;
+  }
+  __syncthreads();
+  if (tid < NT) {
+    u64 x = 0;
+    for (int ww = 0; ww < AB_THREADS / 32; ++ww) x += scnt[ww][tid];
+    for (int s = 0; s < S; ++s)
+      if (ab_is_count(sd, s)) partials[((size_t)c * NT + tid) * S + s] = x;
+  }
+  // block reduction of the per-thread accumulators: one warp per (cell slot, row)
+  int ncell = 0;
+  for (int s = 0; s < S; ++s) ncell += ab_is_count(sd, s) ? 0 : 1;
+  for (int q = w; q < ncell * NT; q += AB_THREADS / 32) {
+    const int ci = q / NT, j = q % NT;
+    int s = 0;
+    for (int cc = -1;; ++s) { if (!ab_is_count(sd, s)) ++cc; if (cc == ci) break; }
     const int op = sd.op[s], ty = sd.type[s];
-    const u64* row = sacc + (size_t)(s * (NT + 1) + j) * AB_THREADS;
+    const u64* row = sacc + (size_t)(ci * (NT + 1) + j) * AB_THREADS;
     u64 x = row[lane];
     for (int i = lane + 32; i < AB_THREADS; i += 32) x = combine_slot(op, ty, x, row[i]);
     for (int o = 16; o; o >>= 1) x = combine_slot(op, ty, x, __shfl_xor_sync(0xffffffffu, x, o));
@@ -272,7 +307,9 @@ template <int KW, int NT>
 static void absorb_launch(const KeyDesc& kd, const SlotDesc& sd, int64_t row0, u32 n, const TinyTable& tt, u32 grid,
                           u32 rpc, u64* partials, u32* miss_buf, u32* miss_cnt, cudaStream_t st) {
   static bool attr = false;
-  const size_t smem = (size_t)sd.nslots * (NT + 1) * AB_THREADS * 8;
+  int ncell = 0;
+  for (int s = 0; s < sd.nslots; ++s) ncell += (sd.src[s] == SRC_ONE && sd.op[s] == OP_ADD && sd.type[s] == ST_I64) ? 0 : 1;
+  const size_t smem = (size_t)std::max(ncell, 1) * (NT + 1) * AB_THREADS * 8;
   if (!attr) {
     cudaFuncSetAttribute(k_absorb_tiny<KW, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          AB_MAX_CELLS * AB_THREADS * 8);
