@@ -443,9 +443,16 @@ struct Engine {
     return cur;
   }
   int sort_built(u32 m) {
-    to_host(dvary(), 2 * sizeof(u64));
-    sync();
-    u64 vlo = ((u64*)h_scal)[0], vhi = ((u64*)h_scal)[1];
+    u64 vlo, vhi;
+    if (key_bits <= 16) {   // at most two 8-bit passes: sort every bit, no host round trip
+      vlo = key_bits == 64 ? ~0ull : ((1ull << key_bits) - 1);
+      vhi = 0;
+    } else {
+      to_host(dvary(), 2 * sizeof(u64));
+      sync();
+      vlo = ((u64*)h_scal)[0];
+      vhi = ((u64*)h_scal)[1];
+    }
     int hb = -1, lb = 128;
     if (vhi) { hb = 127 - __builtin_clzll(vhi); }
     else if (vlo) { hb = 63 - __builtin_clzll(vlo); }
@@ -1090,34 +1097,45 @@ struct Engine {
     return result.n;
   }
 
+  // Device outputs: one fused export kernel on the caller's stream, no host
+  // synchronization (stream order makes the columns ready for the caller).
+  // Host outputs: export into a device staging area, then one D2H copy per
+  // column and a single synchronization.
   void result_copy(void* const* key_out, void* const* slot_out, bool out_on_host, cudaStream_t stream) {
     CK(cudaSetDevice(dev));
     st = stream;
     const u32 n = result.n;
     if (n == 0) return;
+    ExportDesc ed;
+    memset(&ed, 0, sizeof(ed));
+    ed.ncols = kd0.ncols;
+    ed.nslots = S;
+    size_t off = 0;
+    std::vector<size_t> koff(kd0.ncols), soff(S);
     for (int c = 0; c < kd0.ncols; ++c) {
-      void* dst = key_out[c];
-      size_t eb = (size_t)n * key_elem(c);
-      if (!dst) continue;
-      if (out_on_host) { out_tmp.ensure(eb); dst = out_tmp.p; }
-      export_key_col(result.plo(), KW == 2 ? result.phi() : nullptr, n, kd0.dtype[c], kd0.shift[c], kd0.width[c],
-                     dst, st);
-      if (out_on_host) {
-        CK(cudaMemcpyAsync(key_out[c], out_tmp.p, eb, cudaMemcpyDeviceToHost, st));
-        sync();
-      }
+      ed.shift[c] = kd0.shift[c];
+      ed.width[c] = kd0.width[c];
+      ed.is_signed[c] = dtype_signed(kd0.dtype[c]) ? 1 : 0;
+      koff[c] = off;
+      if (key_out[c]) off += (((size_t)n * key_elem(c)) + 255) & ~(size_t)255;
     }
     for (int s = 0; s < S; ++s) {
-      void* dst = slot_out[s];
-      size_t eb = (size_t)n * 8;
-      if (!dst) continue;
-      if (out_on_host) { out_tmp.ensure(eb); dst = out_tmp.p; }
-      export_slot(result.pst(), S, s, n, (u64*)dst, st);
-      if (out_on_host) {
-        CK(cudaMemcpyAsync(slot_out[s], out_tmp.p, eb, cudaMemcpyDeviceToHost, st));
-        sync();
-      }
+      soff[s] = off;
+      if (slot_out[s]) off += (((size_t)n * 8) + 255) & ~(size_t)255;
     }
+    if (out_on_host) out_tmp.ensure(off + 256);
+    for (int c = 0; c < kd0.ncols; ++c)
+      ed.key_dst[c] = !key_out[c] ? nullptr : (out_on_host ? (void*)(out_tmp.as<char>() + koff[c]) : key_out[c]);
+    for (int s = 0; s < S; ++s)
+      ed.slot_dst[s] = !slot_out[s] ? nullptr : (out_on_host ? (void*)(out_tmp.as<char>() + soff[s]) : slot_out[s]);
+    export_all(result.plo(), KW == 2 ? result.phi() : nullptr, result.pst(), n, ed, st);
+    if (!out_on_host) return;
+    for (int c = 0; c < kd0.ncols; ++c)
+      if (key_out[c])
+        CK(cudaMemcpyAsync(key_out[c], out_tmp.as<char>() + koff[c], (size_t)n * key_elem(c), cudaMemcpyDeviceToHost, st));
+    for (int s = 0; s < S; ++s)
+      if (slot_out[s])
+        CK(cudaMemcpyAsync(slot_out[s], out_tmp.as<char>() + soff[s], (size_t)n * 8, cudaMemcpyDeviceToHost, st));
     sync();
   }
 

@@ -788,6 +788,32 @@ void export_key_col(const u64* lo, const u64* hi, u32 n, int dtype, int shift, i
   if (n) klaunch(k_export_key, grid_for(n, 256), 256, 0, st, lo, hi, n, dtype, shift, width, out);
 }
 
+// every key column and every state slot of rows [0, n) in one pass
+__global__ void k_export_all(const u64* __restrict__ lo, const u64* __restrict__ hi, const u64* __restrict__ stt,
+                             u32 n, ExportDesc ed) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const u64 l = lo[i], h = hi ? hi[i] : 0;
+    for (int c = 0; c < ed.ncols; ++c) {
+      if (!ed.key_dst[c]) continue;
+      const int w = ed.width[c];
+      u64 f = key_field(h, l, ed.shift[c], w);
+      if (ed.is_signed[c]) f ^= (1ull << (w - 1));
+      switch (w) {
+        case 8: ((unsigned char*)ed.key_dst[c])[i] = (unsigned char)f; break;
+        case 16: ((unsigned short*)ed.key_dst[c])[i] = (unsigned short)f; break;
+        case 32: ((unsigned int*)ed.key_dst[c])[i] = (unsigned int)f; break;
+        default: ((u64*)ed.key_dst[c])[i] = f; break;
+      }
+    }
+    for (int s = 0; s < ed.nslots; ++s)
+      if (ed.slot_dst[s]) ((u64*)ed.slot_dst[s])[i] = stt[(size_t)i * ed.nslots + s];
+  }
+}
+
+void export_all(const u64* lo, const u64* hi, const u64* stt, u32 n, const ExportDesc& ed, cudaStream_t st) {
+  if (n) klaunch(k_export_all, grid_for(n, 256), 256, 0, st, lo, hi, stt, n, ed);
+}
+
 __global__ void k_export_slot(const u64* __restrict__ stt, int S, int s, u32 n, u64* __restrict__ out) {
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = stt[(size_t)i * S + s];
 }

@@ -132,6 +132,14 @@ void run_lower_bounds(int KW, const RunRef* runs_dev, int nruns, const u64* b_lo
 void export_key_col(const u64* lo, const u64* hi, u32 n, int dtype, int shift, int width,
                     void* out, cudaStream_t st);
 void export_slot(const u64* states, int S, int s, u32 n, u64* out, cudaStream_t st);
+struct ExportDesc {
+  int ncols, nslots;
+  int shift[ISA_MAX_KEY_COLS], width[ISA_MAX_KEY_COLS], is_signed[ISA_MAX_KEY_COLS];
+  void* key_dst[ISA_MAX_KEY_COLS];
+  void* slot_dst[ISA_MAX_SLOTS];
+};
+// all key columns + all slots in one kernel (null destinations are skipped)
+void export_all(const u64* lo, const u64* hi, const u64* states, u32 n, const ExportDesc& ed, cudaStream_t st);
 
 // ---- partition (multi-GPU range split) -----------------------------------
 void sample_keys(const KeyDesc& kd, int64_t n, int64_t stride, u64* out_lo, u64* out_hi, cudaStream_t st);
