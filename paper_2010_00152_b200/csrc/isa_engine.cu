@@ -136,6 +136,8 @@ struct Table {
 struct Run {
   u64* lo = nullptr;   // host-mapped or device pointer usable by kernels
   u64* hi = nullptr;
+  const u64* host_lo = nullptr;   // host view of host-tier runs
+  const u64* host_hi = nullptr;
   u64* st = nullptr;
   u32 rows = 0;
   bool host = true;
@@ -609,6 +611,8 @@ struct Engine {
       if (khi) CK(cudaHostGetDevicePointer((void**)&dhi, khi, 0));
       if (kst) CK(cudaHostGetDevicePointer((void**)&dst, kst, 0));
       r.lo = dlo; r.hi = dhi; r.st = dst;
+      r.host_lo = (const u64*)klo;
+      r.host_hi = (const u64*)khi;
       led.bytes_d2h += nb_key * KW + nb_st;
       // the spilled buffers are reused only after their copy completed
       busy.push_back({T, bev});
@@ -839,16 +843,29 @@ struct Engine {
     // ---- plan windows from sampled keys (every F-th row of each run)
     int64_t F = std::max<int64_t>(1, W / (8 * (int64_t)k));
     std::vector<std::pair<u64, u64>> samples;   // (hi, lo)
-    std::vector<u64> tmp_lo, tmp_hi;
-    for (auto& r : runs) {
-      int64_t ns = (r.rows + F - 1) / F;
-      if (ns == 0) continue;
-      tmp_lo.resize(ns);
-      tmp_hi.assign(ns, 0);
-      CK(cudaMemcpy2DAsync(tmp_lo.data(), 8, r.lo, F * 8, 8, ns, cudaMemcpyDefault, st));
-      if (KW == 2) CK(cudaMemcpy2DAsync(tmp_hi.data(), 8, r.hi, F * 8, 8, ns, cudaMemcpyDefault, st));
+    int64_t total_s = 0;
+    for (auto& r : runs) total_s += (r.rows + F - 1) / F;
+    std::vector<u64> tmp_lo(std::max<int64_t>(total_s, 1)), tmp_hi(std::max<int64_t>(total_s, 1), 0);
+    CK(cudaEventSynchronize(spill_done));   // the host reads host-tier runs directly
+    {
+      int64_t o = 0;
+      for (auto& r : runs) {   // every strided sample copy first, one synchronization after
+        int64_t ns = (r.rows + F - 1) / F;
+        if (ns == 0) continue;
+        if (r.host) {
+          for (int64_t i = 0; i < ns; ++i) {
+            tmp_lo[o + i] = r.host_lo[i * F];
+            if (KW == 2) tmp_hi[o + i] = r.host_hi[i * F];
+          }
+        } else {
+          CK(cudaMemcpy2DAsync(tmp_lo.data() + o, 8, r.lo, F * 8, 8, ns, cudaMemcpyDeviceToHost, st));
+          if (KW == 2) CK(cudaMemcpy2DAsync(tmp_hi.data() + o, 8, r.hi, F * 8, 8, ns, cudaMemcpyDeviceToHost, st));
+        }
+        o += ns;
+      }
       sync();
-      for (int64_t i = 0; i < ns; ++i) samples.push_back({tmp_hi[i], tmp_lo[i]});
+      samples.reserve(total_s);
+      for (int64_t i = 0; i < total_s; ++i) samples.push_back({tmp_hi[i], tmp_lo[i]});
     }
     std::sort(samples.begin(), samples.end());
     std::vector<std::pair<u64, u64>> bounds;
