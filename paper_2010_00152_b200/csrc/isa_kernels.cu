@@ -31,7 +31,8 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_reduce(const u32* __restric
   if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(SC_THREADS) k_scan_single(u32* __restrict__ bsum, u32 nb, u32* __restrict__ total) {
+__global__ void __launch_bounds__(SC_THREADS) k_scan_single(u32* __restrict__ bsum, u32 nb, u32* __restrict__ total,
+                                                           bool write_total_slot) {
   __shared__ u32 sw[8];
   u32 carry = 0;
   for (u32 base = 0; base < nb; base += SC_TILE) {
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_single(u32* __restrict__ bs
     carry += tot;
   }
   if (threadIdx.x == 0) {
-    bsum[nb] = carry;
+    if (write_total_slot) bsum[nb] = carry;
     if (total) *total = carry;
   }
 }
@@ -93,8 +94,12 @@ void scan_exclusive_u32(u32* data, u32 n, u32* tmp, u32* total, cudaStream_t st)
     if (total) cudaMemsetAsync(total, 0, sizeof(u32), st);
     return;
   }
+  if (n <= 16 * SC_TILE) {   // small: one CTA scans in place (1 launch instead of 3)
+    klaunch(k_scan_single, 1, SC_THREADS, 0, st, data, n, total, false);
+    return;
+  }
   klaunch(k_scan_reduce, nb, SC_THREADS, 0, st, data, n, tmp);
-  klaunch(k_scan_single, 1, SC_THREADS, 0, st, tmp, nb, total);
+  klaunch(k_scan_single, 1, SC_THREADS, 0, st, tmp, nb, total, true);
   klaunch(k_scan_apply, nb, SC_THREADS, 0, st, data, n, tmp);
 }
 
@@ -201,7 +206,7 @@ __global__ void __launch_bounds__(RS_THREADS, 2) k_rs_scatter(const u64* __restr
     u32 tot;
     u32 ds = block_excl_scan256(run, sw, &tot);
     dstart[d] = ds;
-    gbase[d] = tile_off[(size_t)d * ntiles + tile] - ds;
+    gbase[d] = tile_off ? tile_off[(size_t)d * ntiles + tile] - ds : 0u;   // one tile: in-tile offsets are global
   }
   __syncthreads();
 #pragma unroll
@@ -253,6 +258,16 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
   const size_t smem = rs_scatter_smem(KW);
   for (int shift = bit_lo; shift < bit_hi; shift += 8) {
     int nxt = cur ^ 1;
+    if (ntiles == 1) {   // the scatter's in-tile digit scan is the global offset
+      if (KW == 2)
+        klaunch(k_rs_scatter<2>, 1, RS_THREADS, smem, st, b.lo[cur], b.hi[cur], b.val[cur], b.lo[nxt], b.hi[nxt],
+                b.val[nxt], n, shift, (const u32*)nullptr, 1u);
+      else
+        klaunch(k_rs_scatter<1>, 1, RS_THREADS, smem, st, b.lo[cur], (const u64*)nullptr, b.val[cur], b.lo[nxt],
+                (u64*)nullptr, b.val[nxt], n, shift, (const u32*)nullptr, 1u);
+      cur = nxt;
+      continue;
+    }
     if (KW == 2) {
       klaunch(k_rs_hist<2>, ntiles, RS_THREADS, 0, st, b.lo[cur], b.hi[cur], n, shift, b.tile_hist, ntiles);
       scan_exclusive_u32(b.tile_hist, 256 * ntiles, b.scan_tmp, nullptr, st);
