@@ -21,6 +21,7 @@
  *                     runs_after_generation / executed_steps sortagg.py:740-742
  *   isa_cycles        OutputEstimator.note_cycle inputs sortagg.py:116-118, 345
  *   isa_run_rows      RunMeta.row_count per run        runstore.py:145-154
+ *   isa_steps         SortAggregate.executed_steps     sortagg.py:777-780, 831-834, 847-848
  *   isa_last_error    the EngineError message          core.py:15-40
  *   isa_phase_stats / isa_launch_count   (new: device-time accounting)
  *   isa_sample_keys / isa_partition    (new: multi-GPU range partitioning;
@@ -84,8 +85,26 @@ typedef struct isa_config {
   int64_t window_rows;       /* 0 = auto: host-input staging window (rows) */
   int64_t merge_window_rows; /* 0 = auto: wide-merge key-range window capacity (rows) */
   int32_t preaggregate;      /* tile-local pre-aggregation before the chunk sort: 0 auto, 1 always, 2 never */
-  int32_t reserved;
+  int32_t merge_mode;        /* isa_merge_mode (SortAggConfig.merge_mode) */
+  int64_t output_size_hint;  /* SortAggConfig.output_size_hint; <= 0 = none */
 } isa_config;
+
+/* SortAggConfig.merge_mode (sortagg.py:45-47): wide = in-sort early
+ * aggregation + one wide merge; traditional / separate = priority-queue run
+ * generation without early aggregation + fan-in-limited merge levels
+ * (sortagg.py:379-455, 788-849) */
+enum isa_merge_mode { ISA_MERGE_WIDE = 0, ISA_MERGE_TRADITIONAL = 1, ISA_MERGE_SEPARATE = 2 };
+
+/* one executed merge step (SortAggregate.executed_steps, sortagg.py:777-780, 831-834, 847-848) */
+enum isa_step_kind { ISA_STEP_WIDE = 0, ISA_STEP_TRADITIONAL = 1, ISA_STEP_FINAL = 2 };
+typedef struct isa_step {
+  int32_t kind;
+  int32_t collapsed;
+  int64_t fan_in;
+  int64_t rows_in;
+  int64_t rows_out;
+  int64_t level;
+} isa_step;
 
 typedef struct isa_schema {
   int32_t n_key_cols;                       /* 1..8, most significant first */
@@ -176,6 +195,8 @@ ISA_API int isa_result_copy(isa_handle* h, void* const* key_out, void* const* sl
 ISA_API int isa_metrics(isa_handle* h, isa_ledger* out);
 /* Read-sort-write fill-cycle lengths of the last execute (rows per cycle). */
 ISA_API int64_t isa_cycles(isa_handle* h, int64_t* out, int64_t cap);
+/* Merge steps of the last execute, in execution order; returns their number. */
+ISA_API int64_t isa_steps(isa_handle* h, isa_step* out, int64_t cap);
 /* Row counts of the runs of the last execute. */
 ISA_API int64_t isa_run_rows(isa_handle* h, int64_t* out, int64_t cap);
 ISA_API const char* isa_last_error(isa_handle* h);

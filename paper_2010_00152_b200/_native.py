@@ -47,7 +47,7 @@ _STATUS_ERRORS = {
 EXPORTED_SYMBOLS = (
     "isa_version", "isa_create", "isa_destroy", "isa_execute", "isa_result_copy",
     "isa_metrics", "isa_cycles", "isa_run_rows", "isa_last_error",
-    "isa_sample_keys", "isa_partition", "isa_phase_stats", "isa_launch_count",
+    "isa_sample_keys", "isa_partition", "isa_phase_stats", "isa_launch_count", "isa_steps",
 )
 
 PHASES = ("absorb", "sort", "flush", "collapse", "table_merge", "wm_sort", "wm_collapse",
@@ -69,8 +69,18 @@ class IsaConfig(ctypes.Structure):
         ("window_rows", ctypes.c_int64),
         ("merge_window_rows", ctypes.c_int64),
         ("preaggregate", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("merge_mode", ctypes.c_int32),
+        ("output_size_hint", ctypes.c_int64),
     ]
+
+
+class IsaStep(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("collapsed", ctypes.c_int32), ("fan_in", ctypes.c_int64),
+                ("rows_in", ctypes.c_int64), ("rows_out", ctypes.c_int64), ("level", ctypes.c_int64)]
+
+
+MERGE_WIDE, MERGE_TRADITIONAL, MERGE_SEPARATE = 0, 1, 2
+STEP_WIDE, STEP_TRADITIONAL, STEP_FINAL = 0, 1, 2
 
 
 class IsaSchema(ctypes.Structure):
@@ -145,6 +155,8 @@ def load():
     lib.isa_run_rows.argtypes = [vp, i64p, ctypes.c_int64]
     lib.isa_last_error.restype = ctypes.c_char_p
     lib.isa_last_error.argtypes = [vp]
+    lib.isa_steps.restype = ctypes.c_int64
+    lib.isa_steps.argtypes = [vp, ctypes.POINTER(IsaStep), ctypes.c_int64]
     lib.isa_phase_stats.restype = ctypes.c_int
     lib.isa_phase_stats.argtypes = [vp, ctypes.POINTER(IsaPhase), ctypes.c_int]
     lib.isa_launch_count.restype = ctypes.c_int64
@@ -227,6 +239,12 @@ class Handle:
         self._lib.isa_phase_stats(self._h, arr, len(PHASES))
         return {name: {"ms": arr[i].ms, "calls": arr[i].calls, "rows": arr[i].rows, "bytes": arr[i].bytes}
                 for i, name in enumerate(PHASES)}
+
+    def steps(self):
+        cnt = self._lib.isa_steps(self._h, None, 0)
+        arr = (IsaStep * max(1, cnt))()
+        self._lib.isa_steps(self._h, arr, cnt)
+        return [arr[i] for i in range(cnt)]
 
     def run_rows(self):
         n = self._lib.isa_run_rows(self._h, None, 0)

@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <chrono>
 #include <deque>
+#include <functional>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -141,6 +142,7 @@ struct Run {
   u64* st = nullptr;
   u32 rows = 0;
   bool host = true;
+  int level = 0;
 };
 
 struct Window {      // staged host input
@@ -317,6 +319,7 @@ struct Engine {
     if (cfg.memory_budget > (int64_t)1 << 30)
       throw IsaError(ISA_ERR_INVALID_INPUT, "memory budget above 2^30 groups is not supported");
     if (cfg.preaggregate < 0 || cfg.preaggregate > 2) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown preaggregate mode");
+    if (cfg.merge_mode < ISA_MERGE_WIDE || cfg.merge_mode > ISA_MERGE_SEPARATE) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown merge mode");
     if (cfg.run_tier != ISA_TIER_HOST && cfg.run_tier != ISA_TIER_HBM)
       throw IsaError(ISA_ERR_INVALID_INPUT, "unknown run tier");
     if (sch.n_key_cols < 1) throw IsaError(ISA_ERR_INVALID_INPUT, "schema needs at least one key column");
@@ -580,32 +583,16 @@ struct Engine {
   }
   bool tiny_ok = false;
 
-  // T becomes a run (RunWriter of a read-sort-write flush, sortagg.py:344-350)
-  void spill_T() {
-    if (T.n == 0) return;
+  // allocate run storage (pinned host pool or device pool) for `rows` rows
+  Run alloc_run(u32 rows) {
     Run r;
-    r.rows = T.n;
-    size_t nb_key = (size_t)T.n * 8, nb_st = (size_t)T.n * 8 * S;
+    r.rows = rows;
+    const size_t nb_key = std::max<size_t>((size_t)rows * 8, 8), nb_st = std::max<size_t>((size_t)rows * 8 * S, 8);
     if (cfg.run_tier == ISA_TIER_HOST) {
       r.host = true;
       char* klo = pinned.alloc(nb_key);
       char* khi = KW == 2 ? pinned.alloc(nb_key) : nullptr;
       char* kst = S ? pinned.alloc(nb_st) : nullptr;
-      // copy on the d2h stream after the table is complete; the table's
-      // buffers are recycled only after the copy finished (event below)
-      cudaEvent_t ev;
-      CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-      CK(cudaEventRecord(ev, st));
-      CK(cudaStreamWaitEvent(d2h, ev, 0));
-      cudaEventDestroy(ev);
-      CK(cudaMemcpyAsync(klo, T.plo(), nb_key, cudaMemcpyDeviceToHost, d2h));
-      if (KW == 2) CK(cudaMemcpyAsync(khi, T.phi(), nb_key, cudaMemcpyDeviceToHost, d2h));
-      if (S) CK(cudaMemcpyAsync(kst, T.pst(), nb_st, cudaMemcpyDeviceToHost, d2h));
-      CK(cudaEventRecord(spill_done, d2h));
-      cudaEvent_t bev;
-      if (!busy_ev_pool.empty()) { bev = busy_ev_pool.back(); busy_ev_pool.pop_back(); }
-      else CK(cudaEventCreateWithFlags(&bev, cudaEventDisableTiming));
-      CK(cudaEventRecord(bev, d2h));
       u64 *dlo = nullptr, *dhi = nullptr, *dst = nullptr;
       CK(cudaHostGetDevicePointer((void**)&dlo, klo, 0));
       if (khi) CK(cudaHostGetDevicePointer((void**)&dhi, khi, 0));
@@ -613,24 +600,55 @@ struct Engine {
       r.lo = dlo; r.hi = dhi; r.st = dst;
       r.host_lo = (const u64*)klo;
       r.host_hi = (const u64*)khi;
-      led.bytes_d2h += nb_key * KW + nb_st;
-      // the spilled buffers are reused only after their copy completed
+    } else {
+      r.host = false;
+      r.lo = (u64*)devpool.alloc(nb_key);
+      r.hi = KW == 2 ? (u64*)devpool.alloc(nb_key) : nullptr;
+      r.st = S ? (u64*)devpool.alloc(nb_st) : nullptr;
+    }
+    return r;
+  }
+
+  // copy `n` table rows into run storage at row offset `off` (on stream s)
+  void copy_into_run(Run& r, Table& t, u32 n, size_t off, cudaStream_t s) {
+    const size_t nb_key = (size_t)n * 8, nb_st = (size_t)n * 8 * S;
+    CK(cudaMemcpyAsync(r.lo + off, t.plo(), nb_key, cudaMemcpyDefault, s));
+    if (KW == 2) CK(cudaMemcpyAsync(r.hi + off, t.phi(), nb_key, cudaMemcpyDefault, s));
+    if (S) CK(cudaMemcpyAsync(r.st + off * S, t.pst(), nb_st, cudaMemcpyDefault, s));
+    if (r.host) led.bytes_d2h += nb_key * KW + nb_st;
+  }
+
+  void account_written(const Run& r) {
+    led.rows_spilled += r.rows;
+    led.pages_written += (r.rows + cfg.page_capacity - 1) / cfg.page_capacity;
+  }
+
+  // T becomes a run (RunWriter of a read-sort-write flush, sortagg.py:344-350)
+  void spill_T() {
+    if (T.n == 0) return;
+    Run r = alloc_run(T.n);
+    if (cfg.run_tier == ISA_TIER_HOST) {
+      // copy on the d2h stream after the table is complete; the table's
+      // buffers are recycled only after the copy finished (busy list)
+      cudaEvent_t ev;
+      CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      CK(cudaEventRecord(ev, st));
+      CK(cudaStreamWaitEvent(d2h, ev, 0));
+      cudaEventDestroy(ev);
+      copy_into_run(r, T, T.n, 0, d2h);
+      CK(cudaEventRecord(spill_done, d2h));
+      cudaEvent_t bev;
+      if (!busy_ev_pool.empty()) { bev = busy_ev_pool.back(); busy_ev_pool.pop_back(); }
+      else CK(cudaEventCreateWithFlags(&bev, cudaEventDisableTiming));
+      CK(cudaEventRecord(bev, d2h));
       busy.push_back({T, bev});
       T = take_table();
     } else {
-      r.host = false;
-      char* klo = devpool.alloc(nb_key);
-      char* khi = KW == 2 ? devpool.alloc(nb_key) : nullptr;
-      char* kst = S ? devpool.alloc(nb_st) : nullptr;
-      CK(cudaMemcpyAsync(klo, T.plo(), nb_key, cudaMemcpyDeviceToDevice, st));
-      if (KW == 2) CK(cudaMemcpyAsync(khi, T.phi(), nb_key, cudaMemcpyDeviceToDevice, st));
-      if (S) CK(cudaMemcpyAsync(kst, T.pst(), nb_st, cudaMemcpyDeviceToDevice, st));
-      r.lo = (u64*)klo; r.hi = (u64*)khi; r.st = (u64*)kst;
+      copy_into_run(r, T, T.n, 0, st);
       T.n = 0;
     }
     runs.push_back(r);
-    led.rows_spilled += r.rows;
-    led.pages_written += (r.rows + cfg.page_capacity - 1) / cfg.page_capacity;
+    account_written(r);
   }
 
   // ------------------------------------------------------------ chunks --
@@ -833,7 +851,12 @@ struct Engine {
   }
 
   // -------------------------------------------------------- wide merge --
-  void wide_merge() {
+  // Merge `rs` window by window (key-range windows planned from sampled
+  // keys, slices staged double-buffered, each window radix-sorted); every
+  // window's sorted output -- collapsed into unique groups, or with
+  // duplicates kept -- is handed to emit(table, distinct keys).
+  void merge_runs(std::vector<Run>& rs, bool collapse, const std::function<void(Table&, u32)>& emit) {
+    auto& runs = rs;
     const int k = (int)runs.size();
     int64_t total = 0;
     for (auto& r : runs) total += r.rows;
@@ -914,8 +937,6 @@ struct Engine {
       if (S) stg_st[i].ensure(wmax * 8 * S + 8);
       CK(cudaEventRecord(stg_free[i], st));
     }
-    result.n = 0;
-    result.reserve(std::max<int64_t>(1, std::min<int64_t>(total, W)), KW, S);
     auto stage = [&](int w, int slot) -> int64_t {
       CK(cudaStreamWaitEvent(h2d, stg_free[slot], 0));
       int64_t off = 0;
@@ -954,20 +975,161 @@ struct Engine {
       keys_varying(KW, s_lo[0].as<u64>(), s_hi[0].as<u64>(), m, dvary(), st);
       int cur = sort_built(m);
       ph_end(ISA_PH_WM_SORT, m, 0);
-      collapse_chunk(cur, m, 0xFFFFFFFFu, sd0, 0, stg_st[slot].as<u64>(), U, m);
+      u32 distinct;
+      if (collapse) {
+        collapse_chunk(cur, m, 0xFFFFFFFFu, sd0, 0, stg_st[slot].as<u64>(), U, m);
+        distinct = U.n;
+      } else {
+        U.reserve(m, KW, S);
+        CK(cudaMemsetAsync(dscal32(7), 0, sizeof(u32), st));
+        materialize(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, sd0, 0,
+                    stg_st[slot].as<u64>(), U.plo(), U.phi(), U.pst(), dscal32(7), st);
+        U.n = m;
+        distinct = read_u32(dscal32(7));
+      }
       CK(cudaEventRecord(stg_free[slot], st));
-      // append U to the result
-      size_t need = (size_t)result.n + U.n;
-      if (need > result.lo.bytes / 8) grow_result(need);
-      CK(cudaMemcpyAsync(result.plo() + result.n, U.plo(), (size_t)U.n * 8, cudaMemcpyDeviceToDevice, st));
-      if (KW == 2) CK(cudaMemcpyAsync(result.phi() + result.n, U.phi(), (size_t)U.n * 8, cudaMemcpyDeviceToDevice, st));
-      if (S) CK(cudaMemcpyAsync(result.pst() + (size_t)result.n * S, U.pst(), (size_t)U.n * 8 * S, cudaMemcpyDeviceToDevice, st));
-      result.n += U.n;
+      emit(U, distinct);
     }
     U.n = 0;
+  }
+
+  // Final wide merge of all runs into the result (sortagg.py:588-674)
+  void wide_merge() {
+    int64_t total = 0;
+    for (auto& r : runs) total += r.rows;
+    const int64_t W = cfg.merge_window_rows > 0 ? cfg.merge_window_rows : ((int64_t)48 << 20);
+    result.n = 0;
+    result.reserve(std::max<int64_t>(1, std::min<int64_t>(total, W)), KW, S);
+    merge_runs(runs, true, [&](Table& w, u32) { append_result(w); });
     led.pages_read = led.pages_written;
     led.merge_steps += 1;
     led.merge_levels += 1;
+    steps.push_back({ISA_STEP_WIDE, 1, (int64_t)runs.size(), total, (int64_t)result.n, 0});
+  }
+
+  void append_result(Table& w) {
+    size_t need = (size_t)result.n + w.n;
+    if (need > result.lo.bytes / 8) grow_result(need);
+    CK(cudaMemcpyAsync(result.plo() + result.n, w.plo(), (size_t)w.n * 8, cudaMemcpyDeviceToDevice, st));
+    if (KW == 2) CK(cudaMemcpyAsync(result.phi() + result.n, w.phi(), (size_t)w.n * 8, cudaMemcpyDeviceToDevice, st));
+    if (S) CK(cudaMemcpyAsync(result.pst() + (size_t)result.n * S, w.pst(), (size_t)w.n * 8 * S, cudaMemcpyDeviceToDevice, st));
+    result.n += w.n;
+  }
+
+  // ------------------------------------------- traditional / separate --
+  std::vector<isa_step> steps;
+  int64_t pq_observed = 1, pq_max_run = 0;
+
+  // OutputEstimator.estimate without fill cycles (sortagg.py:146-160)
+  int64_t pq_estimate(int64_t rows_seen) {
+    if (cfg.output_size_hint > 0) return cfg.output_size_hint;
+    int64_t est = std::max<int64_t>({pq_observed, pq_max_run, (int64_t)1});
+    if (rows_seen) est = std::min(est, rows_seen);
+    return std::max<int64_t>(1, est);
+  }
+
+  // merge_mode traditional / separate (sortagg.py:788-849): priority-queue
+  // run generation, read-sort-write (every M rows -> one sorted run,
+  // duplicates kept, sortagg.py:379-455), fan-in-limited merge levels over
+  // the smallest runs that collapse only when their input covers the output
+  // estimate (never in separate mode), then a final collapsing merge.
+  int64_t execute_pq(int64_t n, const void* const* key_cols, const void* const* val_cols, bool on_host) {
+    const int64_t M = cfg.memory_budget;
+    const int64_t F = cfg.memory_budget / cfg.page_capacity;
+    const bool collapse_allowed = cfg.merge_mode != ISA_MERGE_SEPARATE;
+    pq_observed = 1;
+    pq_max_run = 0;
+    int64_t wrows = on_host ? std::max<int64_t>(cfg.window_rows > 0 ? cfg.window_rows : ((int64_t)32 << 20), M) : n;
+    if (on_host) wrows = (wrows / M) * M;   // windows hold whole blocks
+    Window& w = win[0];
+    for (int64_t ws = 0; ws < n; ws += wrows) {
+      const int64_t we = std::min(n, ws + wrows);
+      const void* kb[ISA_MAX_KEY_COLS];
+      const void* vb[ISA_MAX_VAL_COLS];
+      int64_t base = 0;
+      if (on_host) {
+        sync();   // the previous window is fully consumed
+        stage_window(w, key_cols, val_cols, ws, we);
+        CK(cudaStreamWaitEvent(st, w.ready, 0));
+        for (int c = 0; c < sch.n_key_cols; ++c) kb[c] = w.keys[c].p;
+        for (int j = 0; j < sch.n_val_cols; ++j) vb[j] = w.vals[j].p;
+        base = ws;
+      } else {
+        for (int c = 0; c < sch.n_key_cols; ++c) kb[c] = key_cols[c];
+        for (int j = 0; j < sch.n_val_cols; ++j) vb[j] = val_cols[j];
+      }
+      KeyDesc kd = kd_at(kb);
+      SlotDesc sd = sd_at(vb);
+      for (int64_t a = ws; a < we; a += M) {
+        const u32 m = (u32)std::min<int64_t>(M, we - a);
+        const int cur = sort_rows(kd, a - base, nullptr, m);
+        if (n <= M) {   // everything fits: sort + collapse in memory, no runs (sortagg.py:398-404, 793-795)
+          collapse_chunk(cur, m, 0xFFFFFFFFu, sd, a - base, nullptr, result, m);
+          return result.n;
+        }
+        U.reserve(m, KW, S);
+        materialize(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, sd, a - base, nullptr,
+                    U.plo(), U.phi(), U.pst(), nullptr, st);
+        U.n = m;
+        Run r = alloc_run(m);
+        copy_into_run(r, U, m, 0, st);
+        runs.push_back(r);
+        account_written(r);
+        pq_max_run = std::max<int64_t>(pq_max_run, m);
+        led.chunks++;
+      }
+    }
+    U.n = 0;
+    led.runs_after_generation = (int64_t)runs.size();
+    sync();
+    // traditional merge levels over the smallest runs (sortagg.py:813-837)
+    std::vector<Run> pool = runs;
+    while ((int64_t)pool.size() > F) {
+      const int64_t o_est = pq_estimate(n);
+      std::stable_sort(pool.begin(), pool.end(), [](const Run& x, const Run& y) { return x.rows < y.rows; });
+      int level = 0;
+      for (auto& r : pool) level = std::max(level, r.level);
+      ++level;
+      std::vector<Run> nxt;
+      for (size_t g = 0; g < pool.size(); g += (size_t)F) {
+        std::vector<Run> group(pool.begin() + g, pool.begin() + std::min(pool.size(), g + (size_t)F));
+        if (group.size() == 1) { nxt.push_back(group[0]); continue; }
+        int64_t total = 0;
+        for (auto& r : group) total += r.rows;
+        const bool collapse = collapse_allowed && total >= o_est;
+        Run out = alloc_run((u32)total);
+        out.level = level;
+        size_t off = 0;
+        int64_t observed = 0;
+        merge_runs(group, collapse, [&](Table& t, u32 distinct) {
+          copy_into_run(out, t, t.n, off, st);
+          off += t.n;
+          observed += distinct;
+          sync();   // the window table is reused by the next window
+        });
+        out.rows = (u32)off;
+        for (auto& r : group) led.pages_read += (r.rows + cfg.page_capacity - 1) / cfg.page_capacity;
+        account_written(out);
+        led.merge_steps += 1;
+        pq_observed = std::max(pq_observed, observed);
+        steps.push_back({ISA_STEP_TRADITIONAL, collapse ? 1 : 0, (int64_t)group.size(), total, (int64_t)out.rows, level});
+        nxt.push_back(out);
+      }
+      led.merge_levels += 1;
+      pool = nxt;
+    }
+    // final merge with collapse into the output (sortagg.py:839-849)
+    int64_t total = 0;
+    for (auto& r : pool) total += r.rows;
+    const int64_t W = cfg.merge_window_rows > 0 ? cfg.merge_window_rows : ((int64_t)48 << 20);
+    result.n = 0;
+    result.reserve(std::max<int64_t>(1, std::min<int64_t>(total, W)), KW, S);
+    merge_runs(pool, true, [&](Table& t, u32) { append_result(t); });
+    for (auto& r : pool) led.pages_read += (r.rows + cfg.page_capacity - 1) / cfg.page_capacity;
+    led.merge_steps += 1;
+    led.merge_levels += 1;
+    steps.push_back({ISA_STEP_FINAL, 1, (int64_t)pool.size(), total, (int64_t)result.n, 0});
+    return result.n;
   }
 
   void grow_result(size_t need) {
@@ -1007,8 +1169,19 @@ struct Engine {
     recs.clear();
     const long long launch0 = g_launches.load();
     if (n < 0) throw IsaError(ISA_ERR_INVALID_INPUT, "negative row count");
+    steps.clear();
     led.rows_seen = n;
     if (n == 0) { led.kernel_launches = 0; return 0; }
+    if (cfg.merge_mode != ISA_MERGE_WIDE) {
+      auto t0p = std::chrono::steady_clock::now();
+      int64_t g = execute_pq(n, key_cols, val_cols, on_host);
+      sync();
+      ph_collect();
+      led.ms_run_generation = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0p).count();
+      led.n_groups = g;
+      led.kernel_launches = g_launches.load() - launch0;
+      return g;
+    }
     // every run-generation table holds up to M groups: size them once so
     // swapping tables never reallocates (cudaFree would synchronize)
     tcap = (size_t)std::min<int64_t>(cfg.memory_budget, n) + 1;
@@ -1265,6 +1438,13 @@ int64_t isa_cycles(isa_handle* h, int64_t* out, int64_t cap) {
   auto& c = h->eng->cycles;
   for (int64_t i = 0; i < (int64_t)c.size() && i < cap; ++i) out[i] = c[i];
   return (int64_t)c.size();
+}
+
+int64_t isa_steps(isa_handle* h, isa_step* out, int64_t cap) {
+  if (!h) return -1;
+  auto& s = h->eng->steps;
+  for (int64_t i = 0; i < (int64_t)s.size() && i < cap; ++i) out[i] = s[i];
+  return (int64_t)s.size();
 }
 
 int isa_phase_stats(isa_handle* h, isa_phase* out, int cap) {

@@ -628,6 +628,51 @@ void collapse(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, u32 l
   }
 }
 
+// Materialize a sorted sequence as run rows (duplicates kept): keys from the
+// sorted buffers, states gathered by value index from already-built states
+// (st_in) or built from the raw input rows (make_state).
+template <int KW, int MS>
+__global__ void k_materialize(const u64* __restrict__ lo, const u64* __restrict__ hi, const u32* __restrict__ val,
+                              u32 m, SlotDesc sd, i64 row0, const u64* __restrict__ st_in, u64* __restrict__ out_lo,
+                              u64* __restrict__ out_hi, u64* __restrict__ out_st) {
+  const int S = sd.nslots;
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    out_lo[i] = lo[i];
+    if (KW == 2) out_hi[i] = hi[i];
+    if (S) {
+      u64 s[MS];
+      load_state_row<MS>(sd, row0, st_in, val[i], s);
+#pragma unroll
+      for (int q = 0; q < MS; ++q)
+        if (q < S) out_st[(size_t)i * S + q] = s[q];
+    }
+  }
+}
+
+template <int KW>
+__global__ void k_count_heads(const u64* __restrict__ lo, const u64* __restrict__ hi, u32 m, u32* __restrict__ out) {
+  u32 c = 0;
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    c += (i == 0 || !key_eq<KW>(KW == 2 ? hi[i] : 0, lo[i], KW == 2 ? hi[i - 1] : 0, lo[i - 1])) ? 1u : 0u;
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+void materialize(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, const SlotDesc& sd, int64_t row0,
+                 const u64* st_in, u64* out_lo, u64* out_hi, u64* out_st, u32* heads, cudaStream_t st) {
+  if (m == 0) return;
+  const int g = grid_for(m, 256), S = sd.nslots;
+#define MT(K, M) klaunch(k_materialize<K, M>, g, 256, 0, st, lo, hi, val, m, sd, row0, st_in, out_lo, out_hi, out_st)
+#define MT_KW(K) { if (S <= 1) MT(K, 1); else if (S <= 2) MT(K, 2); else if (S <= 4) MT(K, 4); else if (S <= 8) MT(K, 8); else MT(K, 16); }
+  if (KW == 2) MT_KW(2) else MT_KW(1)
+#undef MT_KW
+#undef MT
+  if (heads) {
+    if (KW == 2) klaunch(k_count_heads<2>, g, 256, 0, st, lo, hi, m, heads);
+    else klaunch(k_count_heads<1>, g, 256, 0, st, lo, (const u64*)nullptr, m, heads);
+  }
+}
+
 // ============================================================= merge ====
 template <int KW>
 __global__ void k_rank(const u64* __restrict__ x_lo, const u64* __restrict__ x_hi, u32 nx,

@@ -76,6 +76,12 @@ void collapse(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, u32 l
               const SlotDesc& sd, int64_t row0, const u64* st_in,
               u64* out_lo, u64* out_hi, u64* out_st, CollapseTmp& tmp, cudaStream_t st);
 
+// ---- materialize a sorted sequence as run rows (duplicates kept) ---------
+// states from st_in[val * S] or, when st_in == nullptr, make_state of row row0 + val;
+// heads != nullptr: += number of distinct keys (device counter)
+void materialize(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, const SlotDesc& sd, int64_t row0,
+                 const u64* st_in, u64* out_lo, u64* out_hi, u64* out_st, u32* heads, cudaStream_t st);
+
 // ---- merge two sorted unique tables, combining equal keys ----------------
 struct MergeTmp {
   u32* rank_a; u32* match_a;   // |A| + 1

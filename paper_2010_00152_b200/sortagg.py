@@ -305,6 +305,9 @@ class SortAggregate:
     ``execute`` consumes an unsorted row stream and returns aggregated rows in
     ascending key order (sortagg.py:744-784); ``execute_columns`` does the same
     on column tensors.  Runs spill to pinned host memory (default) or HBM.
+    ``merge_mode`` wide (the paper's in-sort aggregation + wide merge),
+    traditional or separate (priority-queue run generation + fan-in merge
+    levels, sortagg.py:788-849); read-sort-write run generation.
     """
 
     def __init__(self, schema, config, store=None, ledger=None, *, device=None):
@@ -312,10 +315,6 @@ class SortAggregate:
             raise InvalidInputError(
                 "FileStore is not supported by the B200 operator; runs are placed "
                 "in pinned host memory or HBM (SortAggConfig.run_tier)")
-        if config.merge_mode != WIDE:
-            raise InvalidInputError(
-                f"merge_mode {config.merge_mode!r} is not supported by the B200 operator "
-                "(wide-merge path only)")
         if config.run_generation_mode != READ_SORT_WRITE:
             raise InvalidInputError(
                 f"run_generation_mode {config.run_generation_mode!r} is not supported by the "
@@ -359,6 +358,9 @@ class SortAggregate:
         cfg.window_rows = self.config.window_rows
         cfg.merge_window_rows = self.config.merge_window_rows
         cfg.preaggregate = {"auto": 0, "always": 1, "never": 2}[self.config.preaggregate]
+        cfg.merge_mode = {WIDE: _native.MERGE_WIDE, TRADITIONAL: _native.MERGE_TRADITIONAL,
+                          SEPARATE: _native.MERGE_SEPARATE}[self.config.merge_mode]
+        cfg.output_size_hint = self.config.output_size_hint if self.config.output_size_hint is not None else 0
         sch = _native.IsaSchema()
         if len(key_codes) > _native.MAX_KEY_COLS:
             raise InvalidInputError("too many key columns")
@@ -522,9 +524,18 @@ class SortAggregate:
             est.note_runs(self.run_rows)
             o_est = (self.config.output_size_hint if self.config.output_size_hint is not None
                      else est.estimate(n_rows))
-            self.initial_plan = plan_merge(self.run_rows, o_est, self.config)
-            self.executed_steps.append({"kind": "wide", "fan_in": len(self.run_rows),
-                                        "rows_out": n_groups, "preliminary_merges": 0})
+            if self.config.merge_mode in (WIDE, TRADITIONAL):   # sortagg.py:764, 804-805
+                self.initial_plan = plan_merge(self.run_rows, o_est, self.config)
+        for stp in h.steps():
+            if stp.kind == _native.STEP_WIDE:
+                self.executed_steps.append({"kind": "wide", "fan_in": stp.fan_in, "rows_out": stp.rows_out,
+                                            "preliminary_merges": 0})
+            elif stp.kind == _native.STEP_TRADITIONAL:
+                self.executed_steps.append({"kind": "traditional", "fan_in": stp.fan_in, "rows_in": stp.rows_in,
+                                            "rows_out": stp.rows_out, "collapsed": bool(stp.collapsed),
+                                            "level": stp.level})
+            else:
+                self.executed_steps.append({"kind": "final", "fan_in": stp.fan_in, "rows_out": stp.rows_out})
 
     # -- row-object compatibility path ------------------------------------------
     def execute(self, rows):

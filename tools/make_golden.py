@@ -40,7 +40,7 @@ def _kind(name):
     return getattr(core.AggregateKind, name.upper())
 
 
-def run_reference(key_cols, aggs, values, memory, page=100, hint=None):
+def run_reference(key_cols, aggs, values, memory, page=100, hint=None, mode="wide"):
     """key_cols: list of numpy integer arrays; aggs: [(name, kind, column)];
     values: dict column -> numpy array.  Returns dict of outputs."""
     core, sortagg, runstore = _ref()
@@ -62,14 +62,18 @@ def run_reference(key_cols, aggs, values, memory, page=100, hint=None):
         inputs = tuple(vlists[c][i] if c is not None else None for _, _, c in aggs)
         rows.append(core.Row(key, schema.make_state(inputs) if aggs else ()))
     cfg = sortagg.SortAggConfig(memory_budget=memory, page_capacity=page, ovc_enabled=False,
-                                output_size_hint=hint)
+                                output_size_hint=hint, merge_mode=mode)
     # run generation alone for cycles / run sizes (same deterministic input)
     store = runstore.MemoryStore()
     led0 = core.MetricsLedger()
-    runs, _index, est, _seen = sortagg.index_run_generation(iter(rows), schema, cfg, store,
-                                                            runstore.RowCodec(schema), led0)
+    if mode == "wide":
+        runs, _index, est, _seen = sortagg.index_run_generation(iter(rows), schema, cfg, store,
+                                                                runstore.RowCodec(schema), led0)
+        cycles = list(est.cycles)
+    else:
+        runs, _mem, _seen = sortagg.pq_run_generation(iter(rows), schema, cfg, store, runstore.RowCodec(schema), led0)
+        cycles = []
     run_rows = [m.row_count for m in runs]
-    cycles = list(est.cycles)
     op = sortagg.SortAggregate(schema, cfg, runstore.MemoryStore())
     t0 = time.time()
     out = op.execute(iter(rows))
@@ -88,6 +92,10 @@ def run_reference(key_cols, aggs, values, memory, page=100, hint=None):
         "plan_kinds": np.asarray([s.kind for s in op.initial_plan.steps] if op.initial_plan else [], dtype="U16"),
         "plan_levels": np.int64(op.initial_plan.levels if op.initial_plan else -1),
         "executed_kinds": np.asarray([s["kind"] for s in op.executed_steps], dtype="U16"),
+        "executed_fan_in": np.asarray([s["fan_in"] for s in op.executed_steps], dtype=np.int64),
+        "executed_rows_out": np.asarray([s["rows_out"] for s in op.executed_steps], dtype=np.int64),
+        "executed_collapsed": np.asarray([int(s.get("collapsed", True)) for s in op.executed_steps], dtype=np.int64),
+        "merge_mode": np.asarray(mode, dtype="U16"),
         "ref_seconds": np.float64(secs),
     }
     for j, (c, b) in enumerate(zip(key_cols, bias)):
@@ -103,8 +111,8 @@ def run_reference(key_cols, aggs, values, memory, page=100, hint=None):
     return res
 
 
-def save(name, spec, key_cols, aggs, values, memory, page=100, store_inputs=True, extra=None, hint=None):
-    res = run_reference(key_cols, aggs, values, memory, page, hint)
+def save(name, spec, key_cols, aggs, values, memory, page=100, store_inputs=True, extra=None, hint=None, mode="wide"):
+    res = run_reference(key_cols, aggs, values, memory, page, hint, mode)
     payload = dict(res)
     payload["memory_budget"] = np.int64(memory)
     payload["page_capacity"] = np.int64(page)
@@ -221,6 +229,16 @@ def main():
         kk = uniform_planted(rng, n, o)
         save(f"e2e_{n}_{o}_{m}_{p}", f"test_sortagg shape {(n, o, m, p)}", [kk.astype(np.int64)],
              [("n", "count", None)], {}, m, p)
+    # traditional / separate merge modes (sortagg.py:379-455, 545-574, 788-849): pq run generation + fan-in levels
+    for mode in ("traditional", "separate"):
+        for (n, o, m, p) in [(3000, 450, 64, 8), (800, 800, 64, 8), (1000, 3, 64, 8), (64, 20, 64, 8)]:
+            kk = uniform_planted(rng, n, o)
+            save(f"{mode}_{n}_{o}_{m}_{p}", f"{mode} mode, test_sortagg shape {(n, o, m, p)}",
+                 [kk.astype(np.int64)], [("n", "count", None)], {}, m, p, mode=mode)
+        kk = uniform_planted(rng, 20_000, 1_500)
+        save(f"{mode}_levels", f"{mode} mode, 20000 rows / 1500 keys, M=256, P=16 (several merge levels)",
+             [kk.astype(np.int64)], [("n", "count", None), ("s", "sum", "v"), ("mn", "min", "v")],
+             {"v": rng.integers(-1000, 1000, 20_000)}, 256, 16, mode=mode)
     # wide merge of many runs of a large budget (test_sortagg.py:326-338 shape)
     kk = uniform_planted(rng, 30_000, 2_500)
     save("e2e_spill_once", "30000 rows / 2500 keys, M=1000, P=10", [kk.astype(np.int64)],
