@@ -1,9 +1,7 @@
 // Tiny-table absorb kernel (early aggregation against a register-resident index).
 #include "isa_kernels.h"
 
-#include <cstring>
 #include <algorithm>
-#include <random>
 
 namespace isa {
 
@@ -279,31 +277,6 @@ __global__ void __launch_bounds__(AB_THREADS, 3) k_absorb_tiny(KeyDesc kd, SlotD
   if (tid == 0) miss_cnt[c] = nmiss;
 }
 
-// 32-bit fold of a normalized key; bucket = (fold * mult) >> 28 (16 buckets)
-static inline u32 tiny_fold(u64 hi, u64 lo) {
-  u64 x = lo ^ hi;
-  return (u32)x ^ (u32)(x >> 32) ^ (u32)(hi >> 17);
-}
-
-// Perfect hash of the resident keys (kept for the probe variants; the
-// measured-fastest kernel compares against every resident key).
-bool tiny_perfect_hash(int KW, TinyTable& tt, int nt) {
-  std::mt19937_64 rng(0x2010001500000000ull + nt);
-  for (int attempt = 0; attempt < 100000; ++attempt) {
-    u32 mult = (u32)rng() | 1u;
-    u64 map = ~0ull;
-    bool ok = true;
-    for (int j = 0; j < nt && ok; ++j) {
-      u32 b = (tiny_fold(KW == 2 ? tt.hi[j] : 0, tt.lo[j]) * mult) >> 28;
-      if (((map >> (4 * b)) & 0xF) != 0xF) ok = false;
-      map &= ~(0xFull << (4 * b));
-      map |= (u64)j << (4 * b);
-    }
-    if (ok) { tt.mult = mult; tt.map = map; return true; }
-  }
-  return false;
-}
-
 bool absorb_supported(int nt, int nslots) { return nt >= 1 && nt <= 8 && (nt + 1) * nslots <= AB_MAX_CELLS; }
 
 void absorb_geometry(u32 n, int num_sms, u32* grid, u32* rows_per_cta) {
@@ -351,292 +324,6 @@ void absorb_tiny(int KW, int nt, const KeyDesc& kd, const SlotDesc& sd, int64_t 
   }
   if (KW == 2) absorb_dispatch<2>(nt, kd, sd, row0, n, tt, grid, rows_per_cta, partials, miss_buf, miss_cnt, st);
   else absorb_dispatch<1>(nt, kd, sd, row0, n, tt, grid, rows_per_cta, partials, miss_buf, miss_cnt, st);
-}
-
-}  // namespace isa
-
-namespace isa {
-
-// ------------------------------------------------------------------------
-// Prefetching absorb kernel (used when the slots read <= 4 distinct value
-// columns).  Same contract as k_absorb_tiny, but every key column and every
-// distinct value column of the batch (AP_R rows per thread, one row per
-// lane) is loaded before any of it is used: one DRAM round trip per batch
-// instead of one per slot, i.e. (key cols + value cols) x AP_R independent
-// loads in flight per thread.  The resident-table size is a runtime value.
-// ------------------------------------------------------------------------
-#define AP_THREADS 256
-#define AP_R 8
-#define AP_STEP (AP_THREADS * AP_R)
-
-// Loaders with the dtype switch hoisted out of the row loop (rows k*AP_THREADS + tid).
-template <typename T>
-__device__ __forceinline__ void ap_load(const void* p, i64 b, u32 lim, u32 tid, T (&out)[AP_R]) {
-  const T* q = (const T*)p + b;
-#pragma unroll
-  for (int k = 0; k < AP_R; ++k) out[k] = ((u32)(k * AP_THREADS) + tid < lim) ? __ldg(q + k * AP_THREADS) : T(0);
-}
-
-__device__ __forceinline__ void ap_key_field(int dt, const void* p, i64 b, u32 lim, u32 tid, u64 (&f)[AP_R]) {
-  switch (dt) {
-    case DT_U8: case DT_I8: {
-      unsigned char t[AP_R]; ap_load(p, b, lim, tid, t);
-      const u64 x = dt == DT_I8 ? 0x80ull : 0;
-#pragma unroll
-      for (int k = 0; k < AP_R; ++k) f[k] = (u64)t[k] ^ x;
-    } break;
-    case DT_U16: case DT_I16: {
-      unsigned short t[AP_R]; ap_load(p, b, lim, tid, t);
-      const u64 x = dt == DT_I16 ? 0x8000ull : 0;
-#pragma unroll
-      for (int k = 0; k < AP_R; ++k) f[k] = (u64)t[k] ^ x;
-    } break;
-    case DT_U32: case DT_I32: {
-      unsigned int t[AP_R]; ap_load(p, b, lim, tid, t);
-      const u64 x = dt == DT_I32 ? 0x80000000ull : 0;
-#pragma unroll
-      for (int k = 0; k < AP_R; ++k) f[k] = (u64)t[k] ^ x;
-    } break;
-    default: {
-      unsigned long long t[AP_R]; ap_load(p, b, lim, tid, t);
-      const u64 x = dt == DT_I64 ? 0x8000000000000000ull : 0;
-#pragma unroll
-      for (int k = 0; k < AP_R; ++k) f[k] = (u64)t[k] ^ x;
-    } break;
-  }
-}
-
-// canonical value bits: float columns -> float64 bits, integer columns -> int64 bits
-__device__ __forceinline__ void ap_col_values(int dt, const void* p, i64 b, u32 lim, u32 tid, u64 (&v)[AP_R]) {
-  switch (dt) {
-    case DT_F64: case DT_I64: case DT_U64: {
-      unsigned long long t[AP_R]; ap_load(p, b, lim, tid, t);
-#pragma unroll
-      for (int k = 0; k < AP_R; ++k) v[k] = t[k];
-    } break;
-    case DT_F32: {
-      float t[AP_R]; ap_load(p, b, lim, tid, t);
-#pragma unroll
-      for (int k = 0; k < AP_R; ++k) v[k] = d2u((double)t[k]);
-    } break;
-    case DT_I32: {
-      int t[AP_R]; ap_load(p, b, lim, tid, t);
-#pragma unroll
-      for (int k = 0; k < AP_R; ++k) v[k] = (u64)(i64)t[k];
-    } break;
-    case DT_U32: {
-      unsigned int t[AP_R]; ap_load(p, b, lim, tid, t);
-#pragma unroll
-      for (int k = 0; k < AP_R; ++k) v[k] = (u64)t[k];
-    } break;
-    case DT_I16: {
-      short t[AP_R]; ap_load(p, b, lim, tid, t);
-#pragma unroll
-      for (int k = 0; k < AP_R; ++k) v[k] = (u64)(i64)t[k];
-    } break;
-    case DT_U16: {
-      unsigned short t[AP_R]; ap_load(p, b, lim, tid, t);
-#pragma unroll
-      for (int k = 0; k < AP_R; ++k) v[k] = (u64)t[k];
-    } break;
-    case DT_I8: {
-      signed char t[AP_R]; ap_load(p, b, lim, tid, t);
-#pragma unroll
-      for (int k = 0; k < AP_R; ++k) v[k] = (u64)(i64)t[k];
-    } break;
-    default: {
-      unsigned char t[AP_R]; ap_load(p, b, lim, tid, t);
-#pragma unroll
-      for (int k = 0; k < AP_R; ++k) v[k] = (u64)t[k];
-    } break;
-  }
-}
-
-template <int KW, int NC>
-__global__ void __launch_bounds__(AP_THREADS, 2) k_absorb_pf(KeyDesc kd, SlotDesc sd, ColSet cs, i64 row0, u32 n,
-                                                            TinyTable tt, int nt, u32 rows_per_cta,
-                                                            u64* __restrict__ partials, u32* __restrict__ miss_buf,
-                                                            u32* __restrict__ miss_cnt) {
-  extern __shared__ __align__(16) u64 sacc[];   // [S][nt][AP_THREADS]
-  __shared__ u32 sw[8];
-  const int S = sd.nslots;
-  const int tid = threadIdx.x;
-  const u32 c = blockIdx.x;
-  const u32 r0 = c * rows_per_cta;
-  const u32 r1 = min(r0 + rows_per_cta, n);
-  for (int s = 0; s < S; ++s)
-    for (int j = 0; j < nt; ++j) sacc[(s * nt + j) * AP_THREADS + tid] = identity_slot(sd.op[s], sd.type[s]);
-
-  u32 nmiss = 0;
-  for (u32 base = r0; base < r1; base += AP_STEP) {
-    const u32 lim = r1 - base;
-    // ---- issue every load of the batch
-    u64 kl[AP_R], kh[AP_R];
-#pragma unroll
-    for (int k = 0; k < AP_R; ++k) { kl[k] = 0; kh[k] = 0; }
-    for (int col = 0; col < kd.ncols; ++col) {
-      const int sh = kd.shift[col], wd = kd.width[col];
-      u64 f[AP_R];
-      ap_key_field(kd.dtype[col], kd.ptr[col], row0 + base + tid, lim, tid, f);
-#pragma unroll
-      for (int k = 0; k < AP_R; ++k) {
-        if (sh < 64) {
-          kl[k] |= f[k] << sh;
-          if (KW == 2 && sh > 0 && sh + wd > 64) kh[k] |= f[k] >> (64 - sh);
-        } else if (KW == 2) {
-          kh[k] |= f[k] << (sh - 64);
-        }
-      }
-    }
-    u64 cv[NC][AP_R];   // canonical column values: int columns -> int64 bits, float columns -> float64 bits
-#pragma unroll
-    for (int cc = 0; cc < NC; ++cc) {
-      if (cc < cs.n) {
-        ap_col_values(cs.dtype[cc], cs.ptr[cc], row0 + base + tid, lim, tid, cv[cc]);
-      } else {
-#pragma unroll
-        for (int k = 0; k < AP_R; ++k) cv[cc][k] = 0;
-      }
-    }
-    // ---- probe
-    u32 hoff[AP_R];
-    u32 missbits = 0;
-    u64 pc = 0;
-#pragma unroll
-    for (int k = 0; k < AP_R; ++k) {
-      u32 hk = 8;
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j < nt && key_eq<KW>(kh[k], kl[k], tt.hi[j], tt.lo[j])) hk = j;
-      const bool valid = (u32)(k * AP_THREADS + tid) < lim;
-      if (valid && hk == 8) missbits |= 1u << k;
-      if (!valid) hk = 8;
-      pc += hk < 8 ? (1ull << (8 * hk)) : 0ull;
-      hoff[k] = hk;
-    }
-    // ---- COUNT-like slots from the packed counters
-    for (u32 m = cs.count_slots; m; m &= m - 1) {
-      const int s = __ffs(m) - 1;
-      u64* acc = sacc + (size_t)s * nt * AP_THREADS + tid;
-      for (int j = 0; j < nt; ++j) acc[j * AP_THREADS] += (pc >> (8 * j)) & 0xFFull;
-    }
-    // ---- value slots, column by column (static register indexing)
-#pragma unroll
-    for (int cc = 0; cc < NC; ++cc) {
-      if (cc >= cs.n) continue;
-      for (u32 m = cs.slots[cc]; m; m &= m - 1) {
-        const int s = __ffs(m) - 1;
-        const int op = sd.op[s], ty = sd.type[s];
-        const bool i2f = ty == ST_F64 && !dtype_float(cs.dtype[cc]);
-        u64* acc = sacc + (size_t)s * nt * AP_THREADS + tid;
-#define AP_LOOP(STMT)                                                                 \
-  _Pragma("unroll") for (int k = 0; k < AP_R; ++k) {                                  \
-    if (hoff[k] < 8) { u64* a = acc + hoff[k] * AP_THREADS; const u64 x = cv[cc][k]; STMT; } \
-  }
-        if (i2f) {
-          AP_LOOP(*a = combine_slot(op, ST_F64, *a, d2u((double)(i64)x)))
-        } else if (op == OP_ADD && ty == ST_F64) {
-          AP_LOOP(*a = d2u(u2d(*a) + u2d(x)))
-        } else if (op == OP_ADD) {
-          AP_LOOP(*a = *a + x)
-        } else {
-          AP_LOOP(*a = combine_slot(op, ty, *a, x))
-        }
-#undef AP_LOOP
-      }
-    }
-    // ---- other constant slots (ADD of 1.0 as float64, MIN/MAX of 1)
-    for (u32 m = cs.const_slots; m; m &= m - 1) {
-      const int s = __ffs(m) - 1;
-      const u64 one = sd.type[s] == ST_F64 ? 0x3FF0000000000000ull : 1ull;
-      u64* acc = sacc + (size_t)s * nt * AP_THREADS + tid;
-#pragma unroll
-      for (int k = 0; k < AP_R; ++k)
-        if (hoff[k] < 8) { u64* a = acc + hoff[k] * AP_THREADS; *a = combine_slot(sd.op[s], sd.type[s], *a, one); }
-    }
-    // ---- ordered miss compaction (batch-row order)
-    if (__syncthreads_or(missbits != 0)) {
-      for (int k = 0; k < AP_R; ++k) {
-        const u32 f = (missbits >> k) & 1u;
-        u32 tot;
-        u32 pre = block_excl_scan256(f, sw, &tot);
-        if (f) miss_buf[(size_t)c * rows_per_cta + nmiss + pre] = base + k * AP_THREADS + tid;
-        nmiss += tot;
-      }
-    }
-  }
-  __syncthreads();
-  const int lane = tid & 31, w = tid >> 5;
-  for (int q = w; q < S * nt; q += AP_THREADS / 32) {
-    const int s = q / nt, j = q % nt;
-    const int op = sd.op[s], ty = sd.type[s];
-    const u64* row = sacc + (size_t)q * AP_THREADS;
-    u64 x = row[lane];
-    for (int i = lane + 32; i < AP_THREADS; i += 32) x = combine_slot(op, ty, x, row[i]);
-    for (int o = 16; o; o >>= 1) x = combine_slot(op, ty, x, __shfl_xor_sync(0xffffffffu, x, o));
-    if (lane == 0) partials[((size_t)c * nt + j) * S + s] = x;
-  }
-  if (tid == 0) miss_cnt[c] = nmiss;
-}
-
-bool absorb_pf_columns(const SlotDesc& sd, ColSet* cs) {
-  memset(cs, 0, sizeof(*cs));
-  for (int s = 0; s < sd.nslots; ++s) {
-    if (sd.src[s] == SRC_ONE) {
-      if (sd.op[s] == OP_ADD && sd.type[s] == ST_I64) cs->count_slots |= 1u << s;
-      else cs->const_slots |= 1u << s;
-      continue;
-    }
-    int c = -1;
-    for (int q = 0; q < cs->n; ++q)
-      if (cs->ptr[q] == sd.ptr[s] && cs->dtype[q] == sd.dtype[s]) c = q;
-    if (c < 0) {
-      if (cs->n == 4) return false;
-      c = cs->n++;
-      cs->ptr[c] = sd.ptr[s];
-      cs->dtype[c] = sd.dtype[s];
-    }
-    // a float column feeding an integer slot is rejected by validation; the
-    // canonical value type follows the column
-    cs->slots[c] |= 1u << s;
-  }
-  return true;
-}
-
-void absorb_geometry_pf(u32 n, int num_sms, u32* grid, u32* rows_per_cta) {
-  u32 max_grid = (u32)num_sms * 2;
-  u32 rpc = (n + max_grid - 1) / max_grid;
-  rpc = ((rpc + AP_STEP - 1) / AP_STEP) * AP_STEP;
-  if (rpc == 0) rpc = AP_STEP;
-  *rows_per_cta = rpc;
-  *grid = (n + rpc - 1) / rpc;
-  if (*grid == 0) *grid = 1;
-}
-
-template <int KW, int NC>
-static void absorb_pf_launch(const KeyDesc& kd, const SlotDesc& sd, const ColSet& cs, int64_t row0, u32 n,
-                             const TinyTable& tt, int nt, u32 grid, u32 rpc, u64* partials, u32* miss_buf,
-                             u32* miss_cnt, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_absorb_pf<KW, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * AP_THREADS * 8);
-    attr = true;
-  }
-  const size_t smem = (size_t)sd.nslots * nt * AP_THREADS * 8;
-  klaunch(k_absorb_pf<KW, NC>, grid, AP_THREADS, smem, st, kd, sd, cs, row0, n, tt, nt, rpc, partials, miss_buf,
-          miss_cnt);
-}
-
-void absorb_pf(int KW, int nt, const KeyDesc& kd, const SlotDesc& sd, const ColSet& cs, int64_t row0, u32 n,
-               const TinyTable& tt, u32 grid, u32 rows_per_cta, u64* partials, u32* miss_buf, u32* miss_cnt,
-               cudaStream_t st) {
-#define APL(K, C) absorb_pf_launch<K, C>(kd, sd, cs, row0, n, tt, nt, grid, rows_per_cta, partials, miss_buf, miss_cnt, st)
-  if (KW == 2) {
-    if (cs.n <= 1) APL(2, 1); else if (cs.n <= 2) APL(2, 2); else APL(2, 4);
-  } else {
-    if (cs.n <= 1) APL(1, 1); else if (cs.n <= 2) APL(1, 2); else APL(1, 4);
-  }
-#undef APL
 }
 
 }  // namespace isa

@@ -204,7 +204,6 @@ struct Engine {
     t.n = 0;
     return t;
   }
-  std::vector<cudaEvent_t> tbl_free;   // not used for now
   TinyTable tiny;   // host mirror of T keys when |T| <= 8
   // runs
   PinnedPool pinned;
@@ -259,7 +258,6 @@ struct Engine {
   int64_t absorb_row_bytes = 0;   // algorithmic bytes read per absorbed row
   isa_ledger led;
   std::vector<int64_t> cycles;
-  int64_t launches = 0;
 
   Engine(const isa_config& c, const isa_schema& s) : cfg(c), sch(s) {
     validate();
@@ -578,7 +576,6 @@ struct Engine {
       tiny.lo[j] = ((u64*)h_scal)[j];
       tiny.hi[j] = KW == 2 ? ((u64*)h_scal)[8 + j] : 0;
     }
-    tiny_perfect_hash(KW, tiny, (int)T.n);
     tiny_ok = true;
   }
   bool tiny_ok = false;
@@ -735,25 +732,15 @@ struct Engine {
   // one absorb pass over rows [row0, row0 + n) of the chunk -> per-CTA partials + miss lists
   void absorb_pass(const KeyDesc& kd, const SlotDesc& sd, int64_t row0, u32 n, u32* grid_out, u32* rpc_out) {
     const int nt = (int)T.n;
-    // measured on B200 (configs[1]): v2 2.01 ms vs prefetching variant 2.74 ms
-    // (124 registers -> 16 warps/SM); the variant stays selectable
-    static const bool want_pf = getenv("ISA_ABSORB_PF") != nullptr;
-    ColSet cs;
-    const bool pf = want_pf && absorb_pf_columns(sd, &cs);
     u32 grid, rpc;
-    if (pf) absorb_geometry_pf(n, num_sms, &grid, &rpc);
-    else absorb_geometry(n, num_sms, &grid, &rpc);
+    absorb_geometry(n, num_sms, &grid, &rpc);
     ab_partials.ensure((size_t)grid * nt * std::max(S, 1) * 8 + 64);
     ab_miss_buf.ensure((size_t)grid * rpc * 4 + 64);
     ab_miss_cnt.ensure((size_t)(grid + 1) * 4);
     ab_miss_off.ensure((size_t)(grid + 1) * 4);
     ph_begin(ISA_PH_ABSORB);
-    if (pf)
-      absorb_pf(KW, nt, kd, sd, cs, row0, n, tiny, grid, rpc, ab_partials.as<u64>(), ab_miss_buf.as<u32>(),
+    absorb_tiny(KW, nt, kd, sd, row0, n, tiny, grid, rpc, ab_partials.as<u64>(), ab_miss_buf.as<u32>(),
                 ab_miss_cnt.as<u32>(), st);
-    else
-      absorb_tiny(KW, nt, kd, sd, row0, n, tiny, grid, rpc, ab_partials.as<u64>(), ab_miss_buf.as<u32>(),
-                  ab_miss_cnt.as<u32>(), st);
     ph_end(ISA_PH_ABSORB, n, (int64_t)n * absorb_row_bytes);
     *grid_out = grid;
     *rpc_out = rpc;

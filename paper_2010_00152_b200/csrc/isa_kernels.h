@@ -95,32 +95,14 @@ void merge_combine(int KW, int S, const int* ops, const int* types,
                    u64* c_lo, u64* c_hi, u64* c_st, MergeTmp& tmp, cudaStream_t st);
 
 // ---- tiny-table absorb (the early-aggregation probe for |T| <= 8) -------
-// Resident table of nt <= 8 keys plus a perfect hash over them: bucket(key) =
-// (mix(key) * mult) >> 60 (16 buckets), map nibble b = table row or 0xF.
-struct TinyTable { u64 lo[8]; u64 hi[8]; u64 mult; u64 map; };
-// host helper: find mult/map making bucket() injective on the table's keys
-bool tiny_perfect_hash(int KW, TinyTable& tt, int nt);
+// Resident table of nt <= 8 keys (kernel parameters)
+struct TinyTable { u64 lo[8]; u64 hi[8]; };
 // Grid geometry helper: CTAs and rows per CTA for n rows.
 void absorb_geometry(u32 n, int num_sms, u32* grid, u32* rows_per_cta);
 bool absorb_supported(int nt, int nslots);
 void absorb_tiny(int KW, int nt, const KeyDesc& kd, const SlotDesc& sd, int64_t row0, u32 n,
                  const TinyTable& tt, u32 grid, u32 rows_per_cta,
                  u64* partials, u32* miss_buf, u32* miss_cnt, cudaStream_t st);
-// Prefetching variant: <= 4 distinct value columns, all loads of a batch
-// issued before use.  ColSet maps distinct value columns to the slots they feed.
-struct ColSet {
-  int n;                 // distinct value columns
-  int dtype[4];
-  const void* ptr[4];
-  u32 slots[4];          // bitmask of slots fed by column c
-  u32 count_slots;       // SRC_ONE + ADD + int64 (COUNT, AVG count)
-  u32 const_slots;       // other SRC_ONE slots
-};
-bool absorb_pf_columns(const SlotDesc& sd, ColSet* cs);
-void absorb_geometry_pf(u32 n, int num_sms, u32* grid, u32* rows_per_cta);
-void absorb_pf(int KW, int nt, const KeyDesc& kd, const SlotDesc& sd, const ColSet& cs, int64_t row0, u32 n,
-               const TinyTable& tt, u32 grid, u32 rows_per_cta, u64* partials, u32* miss_buf, u32* miss_cnt,
-               cudaStream_t st);
 // T_st[j*S + s] = combine(T_st, fold_c partials[c][j][s])
 void fold_partials(int nt, const SlotDesc& sd, const u64* partials, u32 grid, u64* T_st, cudaStream_t st);
 // compact per-CTA miss lists (miss_off = exclusive scan of miss_cnt)
