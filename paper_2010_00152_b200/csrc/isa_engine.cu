@@ -785,6 +785,7 @@ struct Engine {
   }
 
   // next chunk length (rows) for the sort path
+  static constexpr int64_t kProbeRows = 4096;  // = one radix-sort tile (RS_TILE)
   int64_t chunk_len(int64_t remaining, int64_t last_len, bool last_flushed, int64_t last_cycle) {
     const int64_t M = cfg.memory_budget;
     int64_t cmax = cfg.chunk_rows_max > 0 ? cfg.chunk_rows_max : ((int64_t)64 << 20);
@@ -794,14 +795,17 @@ struct Engine {
       // per-chunk memory beyond a per-CTA miss list
       return std::min<int64_t>(remaining, cfg.chunk_rows_max > 0 ? cfg.chunk_rows_max : ((int64_t)1 << 30));
     } else if (last_len == 0) {
-      len = std::max<int64_t>(M + M / 8, 4096);
+      // probe chunk: one sort tile (no histogram/scan passes); it measures
+      // the new-group rate for the next chunk and, when the input has only
+      // a handful of groups, hands the rest to the absorb kernel
+      len = kProbeRows;
     } else if (last_flushed) {
       len = last_cycle + last_cycle / 8 + 4096;
     } else if (last_new > 0) {
       double rate = (double)last_new / (double)last_len;
       double need = (double)(M - (int64_t)T.n + 1) / rate;
       len = (int64_t)(need * 1.125) + 4096;
-      len = std::min(len, last_len * 4);
+      if (last_len > kProbeRows) len = std::min(len, last_len * 4);
     } else {
       len = last_len * 4;
     }

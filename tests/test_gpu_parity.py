@@ -239,3 +239,56 @@ def test_128bit_keys_high_word_cardinality(hi_card):
     op = isa.SortAggregate(sch, _cfg(1 << 14, 100))
     res = op.execute_columns([_cuda(k1), _cuda(k2)], {"v": _cuda(v)})
     _check(res, want_k, want_s)
+
+
+def _few_groups_case(nt, key_kind, n, extra, seed, wide=False):
+    """n rows over nt base groups, plus `extra` new groups first seen in the
+    second half (absorb misses); keys of the given kind, mixed value types."""
+    rng = np.random.default_rng(seed)
+    base = rng.choice(1 << 12, nt, replace=False)
+    ids = base[rng.integers(0, nt, n)]
+    if extra:
+        pos = np.sort(rng.choice(np.arange(n // 2, n), extra, replace=False))
+        ids[pos] = (1 << 12) + np.arange(extra) * 7 + 1
+        ids[pos[-1]:][rng.random(n - pos[-1]) < 0.01] = ids[pos[-1]]   # the last new key recurs
+    if key_kind == "i8":
+        keys = [(ids % 251 - 125).astype(np.int8)] if not extra else [(ids % 16381 - 8190).astype(np.int16)]
+    elif key_kind == "i32x2":
+        keys = [(ids // 64).astype(np.int32) - 5, (ids % 64).astype(np.int32)]
+    elif key_kind == "u64x2":   # 128-bit normalized keys
+        keys = [(ids.astype(np.uint64) * np.uint64(0x9E3779B97F4A7C15)), (ids % 3).astype(np.uint64)]
+    else:
+        keys = [ids.astype(np.int64) * -3]
+    vals = {"v": rng.uniform(-1e3, 1e3, n), "w": rng.integers(-(1 << 30), 1 << 30, n).astype(np.int32),
+            "x": rng.integers(-(1 << 40), 1 << 40, n), "y": rng.standard_normal(n).astype(np.float32)}
+    cols = [isa.ColumnSpec(f"k{i}") for i in range(len(keys))]
+    aggs = [isa.AggregateSpec("n", isa.AggregateKind.COUNT), isa.AggregateSpec("s", isa.AggregateKind.SUM, "v"),
+            isa.AggregateSpec("lo", isa.AggregateKind.MIN, "w"), isa.AggregateSpec("hi", isa.AggregateKind.MAX, "x"),
+            isa.AggregateSpec("a", isa.AggregateKind.AVG, "y")]
+    if wide:   # more state slots than the bulk kernel keeps in registers
+        aggs += [isa.AggregateSpec("vlo", isa.AggregateKind.MIN, "v"), isa.AggregateSpec("yhi", isa.AggregateKind.MAX, "y")]
+    return isa.Schema(cols, aggs), keys, vals
+
+
+@pytest.mark.parametrize("nt", [1, 3, 6, 8])
+@pytest.mark.parametrize("key_kind", ["i8", "i32x2", "u64x2", "i64"])
+@pytest.mark.parametrize("extra,memory,wide", [(0, 4096, False), (40, 4096, False), (40, None, False),
+                                               (40, 4096, True)])
+def test_tiny_table_absorb_vs_oracle(nt, key_kind, extra, memory, wide):
+    """The |T| <= 8 absorb kernel: ragged
+    row counts, late new groups (absorb misses), flushes inside an absorb
+    chunk (memory = nt + 3), every value dtype; ledger equals the C oracle's."""
+    n = 1_000_003 + 517 * nt
+    sch, keys, vals = _few_groups_case(nt, key_kind, n, extra, seed=nt * 31 + len(key_kind), wide=wide)
+    M = memory if memory is not None else nt + 3
+    slots = oracle.make_states(sch, vals, n)
+    want_k, want_s = oracle.reference_aggregate(keys, slots, oracle.slot_ops(sch))
+    _, _, led, cycles = oracle.rsw_sortagg(keys, slots, oracle.slot_ops(sch), M, 2)
+    for on_host in (False, True):
+        op = isa.SortAggregate(sch, _cfg(M, 2))
+        kk = [torch.from_numpy(k).pin_memory() if on_host else _cuda(k) for k in keys]
+        vv = {c: (torch.from_numpy(v).pin_memory() if on_host else _cuda(v)) for c, v in vals.items()}
+        res = op.execute_columns(kk, vv)
+        _check(res, want_k, want_s, rel=1e-5)
+        assert op.cycles == [c for c in cycles if c > 0]
+        assert op.ledger.rows_spilled == led["rows_spilled"]
