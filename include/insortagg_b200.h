@@ -157,7 +157,8 @@ enum isa_phase_id {
   ISA_PH_WM_COLLAPSE = 6,  /* wide merge: window collapse + append */
   ISA_PH_RUN_GEN = 7,      /* run generation total */
   ISA_PH_WIDE_MERGE = 8,   /* wide merge total */
-  ISA_PH_COUNT = 9
+  ISA_PH_PROBE = 9,        /* first-chunk tiny-table discovery (<= 8 groups) */
+  ISA_PH_COUNT = 10
 };
 
 typedef struct isa_phase {

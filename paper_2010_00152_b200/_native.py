@@ -51,7 +51,7 @@ EXPORTED_SYMBOLS = (
 )
 
 PHASES = ("absorb", "sort", "flush", "collapse", "table_merge", "wm_sort", "wm_collapse",
-          "run_generation", "wide_merge")
+          "run_generation", "wide_merge", "probe")
 
 
 class IsaPhase(ctypes.Structure):
@@ -178,6 +178,11 @@ def launch_count():
     return int(load().isa_launch_count())
 
 
+def phases_dict(arr):
+    return {name: {"ms": arr[i].ms, "calls": arr[i].calls, "rows": arr[i].rows, "bytes": arr[i].bytes}
+            for i, name in enumerate(PHASES)}
+
+
 def _ptr_array(ptrs):
     arr = (ctypes.c_void_p * max(1, len(ptrs)))()
     for i, p in enumerate(ptrs):
@@ -234,11 +239,13 @@ class Handle:
         self._lib.isa_cycles(self._h, buf, n)
         return [buf[i] for i in range(n)]
 
-    def phase_stats(self):
+    def phase_raw(self):
         arr = (IsaPhase * len(PHASES))()
         self._lib.isa_phase_stats(self._h, arr, len(PHASES))
-        return {name: {"ms": arr[i].ms, "calls": arr[i].calls, "rows": arr[i].rows, "bytes": arr[i].bytes}
-                for i, name in enumerate(PHASES)}
+        return arr
+
+    def phase_stats(self):
+        return phases_dict(self.phase_raw())
 
     def steps(self):
         cnt = self._lib.isa_steps(self._h, None, 0)

@@ -326,4 +326,118 @@ void absorb_tiny(int KW, int nt, const KeyDesc& kd, const SlotDesc& sd, int64_t 
   else absorb_dispatch<1>(nt, kd, sd, row0, n, tt, grid, rows_per_cta, partials, miss_buf, miss_cnt, st);
 }
 
+// ============================================================= probe ====
+// First chunk of an execute (T empty, <= PR_THREADS * PR_RPT rows): find the
+// distinct keys in first-occurrence order, one block-wide round per key
+// (OrderedIndex.insert_or_aggregate inserting into an empty index,
+// memindex.py:197-236).  If there are at most max_nt of them the chunk needs
+// no flush (max_nt <= M), so the kernel writes the sorted table T (keys +
+// combined states) and publishes the keys to mapped host memory for the
+// absorb kernel's parameters; otherwise it only reports failure and the
+// host runs the general sort path on the chunk.  out (mapped, u64 words):
+// [0] = nt or ~0 on failure, [8 + j] = lo, [16 + j] = hi of sorted row j.
+#define PR_THREADS 1024
+#define PR_RPT 4
+template <int KW>
+__global__ void __launch_bounds__(PR_THREADS) k_probe_tiny(KeyDesc kd, SlotDesc sd, i64 row0, u32 n, u32 max_nt,
+                                                         u64* __restrict__ T_lo, u64* __restrict__ T_hi,
+                                                         u64* __restrict__ T_st, u64* out) {
+  __shared__ u64 tlo[8], thi[8];
+  __shared__ u32 s_min, s_rank[8];
+  __shared__ u64 red[PR_THREADS / 32][8];
+  const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const u32 NONE = 0xFFFFFFFFu;
+  u64 klo[PR_RPT], khi[PR_RPT];
+  u32 hk[PR_RPT];
+#pragma unroll
+  for (int k = 0; k < PR_RPT; ++k) {
+    const u32 q = k * PR_THREADS + tid;
+    klo[k] = khi[k] = 0;
+    hk[k] = NONE;
+    if (q < n) load_key(kd, row0 + q, khi[k], klo[k]);
+  }
+  u32 nt = 0;
+  bool ok = true;
+  for (;;) {
+    if (tid == 0) s_min = NONE;
+    __syncthreads();
+    u32 mine = NONE;
+#pragma unroll
+    for (int k = PR_RPT - 1; k >= 0; --k) {
+      const u32 q = k * PR_THREADS + tid;
+      if (q < n && hk[k] == NONE) mine = q;
+    }
+    mine = __reduce_min_sync(0xffffffffu, mine);
+    if (lane == 0 && mine != NONE) atomicMin(&s_min, mine);
+    __syncthreads();
+    const u32 m = s_min;
+    if (m == NONE) break;
+    if (nt == max_nt) { ok = false; break; }
+    if (tid == m % PR_THREADS) {
+      const int km = (int)(m / PR_THREADS);
+#pragma unroll
+      for (int k = 0; k < PR_RPT; ++k)
+        if (k == km) { tlo[nt] = klo[k]; thi[nt] = khi[k]; }
+    }
+    __syncthreads();
+    const u64 nlo = tlo[nt], nhi = thi[nt];
+#pragma unroll
+    for (int k = 0; k < PR_RPT; ++k)
+      if (hk[k] == NONE && key_eq<KW>(khi[k], klo[k], nhi, nlo)) hk[k] = nt;
+    ++nt;
+  }
+  if (!ok) {
+    if (tid == 0) *(volatile u64*)out = ~0ull;
+    return;
+  }
+  if (tid < nt) {   // rank of table row tid among the nt keys = its sorted position
+    u32 r = 0;
+    for (u32 j = 0; j < nt; ++j) r += key_less<KW>(thi[j], tlo[j], thi[tid], tlo[tid]) ? 1u : 0u;
+    s_rank[tid] = r;
+  }
+  // combined states: per thread over its rows, warp shuffle, then across warps
+  const int S = sd.nslots;
+  for (int s = 0; s < S; ++s) {
+    const int op = sd.op[s], ty = sd.type[s];
+    u64 v[PR_RPT];
+#pragma unroll
+    for (int k = 0; k < PR_RPT; ++k) {
+      const u32 q = k * PR_THREADS + tid;
+      v[k] = q < n ? load_slot_value(sd.src[s], ty, sd.dtype[s], sd.ptr[s], row0 + q) : 0;
+    }
+    const u64 id = identity_slot(op, ty);
+    for (u32 j = 0; j < nt; ++j) {
+      u64 x = id;
+#pragma unroll
+      for (int k = 0; k < PR_RPT; ++k)
+        if (hk[k] == j) x = combine_slot(op, ty, x, v[k]);
+      for (int o = 16; o; o >>= 1) x = combine_slot(op, ty, x, __shfl_xor_sync(0xffffffffu, x, o));
+      if (lane == 0) red[w][j] = x;
+    }
+    __syncthreads();
+    if (tid < nt) {
+      u64 x = red[0][tid];
+      for (int ww = 1; ww < PR_THREADS / 32; ++ww) x = combine_slot(op, ty, x, red[ww][tid]);
+      T_st[(size_t)s_rank[tid] * S + s] = x;
+    }
+    __syncthreads();
+  }
+  if (tid < nt) {
+    const u32 r = s_rank[tid];
+    T_lo[r] = tlo[tid];
+    if (KW == 2) T_hi[r] = thi[tid];
+    ((volatile u64*)out)[8 + r] = tlo[tid];
+    ((volatile u64*)out)[16 + r] = thi[tid];
+  }
+  if (tid == 0) *(volatile u64*)out = nt;
+}
+
+u32 probe_rows() { return PR_THREADS * PR_RPT; }
+
+void probe_tiny(int KW, const KeyDesc& kd, const SlotDesc& sd, int64_t row0, u32 n, u32 max_nt, u64* T_lo,
+                u64* T_hi, u64* T_st, u64* out_mapped, cudaStream_t st) {
+  if (KW == 2) klaunch(k_probe_tiny<2>, 1, PR_THREADS, 0, st, kd, sd, (i64)row0, n, max_nt, T_lo, T_hi, T_st, out_mapped);
+  else klaunch(k_probe_tiny<1>, 1, PR_THREADS, 0, st, kd, sd, (i64)row0, n, max_nt, T_lo, T_hi, T_st, out_mapped);
+}
+
 }  // namespace isa

@@ -656,6 +656,7 @@ struct Engine {
     const u32 span = (u32)(b - a);
     const int64_t row0 = a - base;   // column element of row a
     led.chunks++;
+    if (T.n == 0 && span <= probe_rows() && probe_chunk(kd, sd, row0, span)) return b;
     if (T.n > 0 && T.n <= 8 && tiny_ok && absorb_supported((int)T.n, S)) return absorb_chunk(kd, sd, row0, a, span);
     // tiny chunks are not worth the extra pass in auto mode; "always" keeps
     // it down to 4 tiles (also what the parity tests exercise)
@@ -671,6 +672,31 @@ struct Engine {
     }
     refresh_tiny();
     return b;
+  }
+
+  // First chunk into an empty T: one single-CTA kernel finds the chunk's
+  // groups when there are few of them (<= 8 and <= M: no flush possible),
+  // writes T and hands the keys to the absorb kernel; false = use the sort path.
+  bool probe_chunk(const KeyDesc& kd, const SlotDesc& sd, int64_t row0, u32 span) {
+    u32 max_nt = 0;
+    for (int t = 8; t >= 1; --t)
+      if (t <= cfg.memory_budget && absorb_supported(t, S)) { max_nt = (u32)t; break; }
+    if (max_nt == 0) return false;
+    ph_begin(ISA_PH_PROBE);
+    probe_tiny(KW, kd, sd, row0, span, max_nt, T.plo(), T.phi(), T.pst(), (u64*)d_scal_mapped, st);
+    ph_end(ISA_PH_PROBE, span, 0);
+    sync();
+    const volatile u64* hw = (const volatile u64*)h_scal;
+    if (hw[0] == ~0ull) return false;
+    T.n = (u32)hw[0];
+    last_new = T.n;
+    memset(&tiny, 0, sizeof(tiny));
+    for (u32 j = 0; j < T.n; ++j) {
+      tiny.lo[j] = hw[8 + j];
+      tiny.hi[j] = KW == 2 ? hw[16 + j] : 0;
+    }
+    tiny_ok = true;
+    return true;
   }
 
   // Sort path with tile-local pre-aggregation (K1): sort the tiles' groups

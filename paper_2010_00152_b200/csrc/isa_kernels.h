@@ -103,6 +103,11 @@ bool absorb_supported(int nt, int nslots);
 void absorb_tiny(int KW, int nt, const KeyDesc& kd, const SlotDesc& sd, int64_t row0, u32 n,
                  const TinyTable& tt, u32 grid, u32 rows_per_cta,
                  u64* partials, u32* miss_buf, u32* miss_cnt, cudaStream_t st);
+// First-chunk discovery of <= max_nt groups into an empty T (k_probe_tiny);
+// out_mapped[0] = nt, or ~0 when the chunk has more groups (T untouched).
+u32 probe_rows();
+void probe_tiny(int KW, const KeyDesc& kd, const SlotDesc& sd, int64_t row0, u32 n, u32 max_nt, u64* T_lo,
+                u64* T_hi, u64* T_st, u64* out_mapped, cudaStream_t st);
 // T_st[j*S + s] = combine(T_st, fold_c partials[c][j][s])
 void fold_partials(int nt, const SlotDesc& sd, const u64* partials, u32 grid, u64* T_st, cudaStream_t st);
 // compact per-CTA miss lists (miss_off = exclusive scan of miss_cnt)

@@ -299,6 +299,17 @@ class ColumnarResult(tuple):
         return int(self[0][0].shape[0]) if self[0] else 0
 
 
+def _lazy(name, doc):
+    def get(self):
+        if name not in self._info:
+            self._materialize()
+        return self._info[name]
+
+    def put(self, value):
+        self._info[name] = value
+    return property(get, put, doc=doc)
+
+
 class SortAggregate:
     """Sort-based grouping / duplicate removal / aggregation on one B200.
 
@@ -309,6 +320,14 @@ class SortAggregate:
     traditional or separate (priority-queue run generation + fan-in merge
     levels, sortagg.py:788-849); read-sort-write run generation.
     """
+
+    cycles = _lazy("cycles", "fill-cycle lengths of the last execute (rows consumed per flush)")
+    run_rows = _lazy("run_rows", "rows of every run written by the last execute")
+    phase_stats = _lazy("phase_stats", "per-phase device times of the last execute")
+    runs_after_generation = _lazy("runs_after_generation", "SortAggregate.runs_after_generation")
+    executed_steps = _lazy("executed_steps", "SortAggregate.executed_steps")
+    initial_plan = _lazy("initial_plan", "SortAggregate.initial_plan")
+    device_ledger = _lazy("device_ledger", "native isa_ledger of the last execute (dict)")
 
     def __init__(self, schema, config, store=None, ledger=None, *, device=None):
         if isinstance(store, FileStore):
@@ -325,13 +344,9 @@ class SortAggregate:
         self.config = config
         self.store = store
         self.ledger = ledger if ledger is not None else MetricsLedger()
-        self.initial_plan = None
-        self.executed_steps = []
-        self.runs_after_generation = 0
-        self.device_ledger = None
-        self.phase_stats = {}
-        self.cycles = []
-        self.run_rows = []
+        self._last = None
+        self._info = {}
+        self._materialize()
         self._device = device
         self._handles = {}
 
@@ -493,49 +508,73 @@ class SortAggregate:
         if stream is None:
             stream = torch.cuda.current_stream(dev_index)
         sptr = ctypes_stream(stream)
-        with torch.cuda.device(dev_index):
-            n_groups = h.execute(n, [k.data_ptr() for k in keys], [v.data_ptr() for v in vals], on_host, sptr)
-            out_dev = torch.device("cpu") if on_host else keys[0].device
-            pin = on_host
-            out_keys = [torch.empty(n_groups, dtype=k.dtype, device=out_dev, pin_memory=pin) for k in keys]
-            out_states = [torch.empty(n_groups, dtype=torch.float64 if ty == _native.SLOT_F64 else torch.int64,
-                                      device=out_dev, pin_memory=pin)
-                          for (_, ty, _, _) in slots]
-            if n_groups:
-                h.result_copy([t.data_ptr() for t in out_keys], [t.data_ptr() for t in out_states], on_host, sptr)
+        # the native side selects the device itself; outputs name it explicitly
+        n_groups = h.execute(n, [k.data_ptr() for k in keys], [v.data_ptr() for v in vals], on_host, sptr)
+        out_dev = torch.device("cpu") if on_host else keys[0].device
+        pin = on_host
+        out_keys = [torch.empty(n_groups, dtype=k.dtype, device=out_dev, pin_memory=pin) for k in keys]
+        out_states = [torch.empty(n_groups, dtype=torch.float64 if ty == _native.SLOT_F64 else torch.int64,
+                                  device=out_dev, pin_memory=pin)
+                      for (_, ty, _, _) in slots]
+        if n_groups:
+            h.result_copy([t.data_ptr() for t in out_keys], [t.data_ptr() for t in out_states], on_host, sptr)
         self._record(h, n, n_groups)
         return ColumnarResult(out_keys, out_states)
 
     def _record(self, h, n_rows, n_groups):
+        """Fold the device ledger into ``ledger`` now; the per-execute details
+        (cycles, run sizes, phases, plan, steps) are read from the handle on
+        first access, keeping the per-call host overhead off the GPU's path."""
         led = h.metrics()
-        self.device_ledger = led.as_dict()
         for name in MetricsLedger.__slots__:
             setattr(self.ledger, name, getattr(self.ledger, name) + getattr(led, name))
-        self.cycles = h.cycles()
-        self.run_rows = h.run_rows()
-        self.phase_stats = h.phase_stats()
-        self.runs_after_generation = len(self.run_rows)
-        self.executed_steps = []
-        self.initial_plan = None
-        if self.run_rows:
-            est = OutputEstimator(self.config.memory_budget)
-            for c in self.cycles:
-                est.note_cycle(c)
-            est.note_runs(self.run_rows)
-            o_est = (self.config.output_size_hint if self.config.output_size_hint is not None
-                     else est.estimate(n_rows))
-            if self.config.merge_mode in (WIDE, TRADITIONAL):   # sortagg.py:764, 804-805
-                self.initial_plan = plan_merge(self.run_rows, o_est, self.config)
-        for stp in h.steps():
-            if stp.kind == _native.STEP_WIDE:
-                self.executed_steps.append({"kind": "wide", "fan_in": stp.fan_in, "rows_out": stp.rows_out,
-                                            "preliminary_merges": 0})
-            elif stp.kind == _native.STEP_TRADITIONAL:
-                self.executed_steps.append({"kind": "traditional", "fan_in": stp.fan_in, "rows_in": stp.rows_in,
-                                            "rows_out": stp.rows_out, "collapsed": bool(stp.collapsed),
-                                            "level": stp.level})
-            else:
-                self.executed_steps.append({"kind": "final", "fan_in": stp.fan_in, "rows_out": stp.rows_out})
+        self._last = (h, n_rows, led)
+        self._info = {}
+
+    def phase_snapshot(self):
+        """Raw per-phase device times of the last execute (cheap; turn into
+        a dict with ``_native.phases_dict``)."""
+        return self._last[0].phase_raw() if self._last is not None else None
+
+    def _materialize(self):
+        info = self._info
+        if self._last is None:
+            defaults = {"device_ledger": None, "cycles": [], "run_rows": [], "phase_stats": {},
+                        "runs_after_generation": 0, "executed_steps": [], "initial_plan": None}
+            for k, v in defaults.items():
+                info.setdefault(k, v)
+            return
+        h, n_rows, led = self._last
+        info.setdefault("device_ledger", led.as_dict())
+        cycles = info.setdefault("cycles", h.cycles())
+        run_rows = info.setdefault("run_rows", h.run_rows())
+        info.setdefault("phase_stats", h.phase_stats())
+        info.setdefault("runs_after_generation", len(run_rows))
+        if "initial_plan" not in info:
+            plan = None
+            if run_rows:
+                est = OutputEstimator(self.config.memory_budget)
+                for c in cycles:
+                    est.note_cycle(c)
+                est.note_runs(run_rows)
+                o_est = (self.config.output_size_hint if self.config.output_size_hint is not None
+                         else est.estimate(n_rows))
+                if self.config.merge_mode in (WIDE, TRADITIONAL):   # sortagg.py:764, 804-805
+                    plan = plan_merge(run_rows, o_est, self.config)
+            info["initial_plan"] = plan
+        if "executed_steps" not in info:
+            steps = []
+            for stp in h.steps():
+                if stp.kind == _native.STEP_WIDE:
+                    steps.append({"kind": "wide", "fan_in": stp.fan_in, "rows_out": stp.rows_out,
+                                  "preliminary_merges": 0})
+                elif stp.kind == _native.STEP_TRADITIONAL:
+                    steps.append({"kind": "traditional", "fan_in": stp.fan_in, "rows_in": stp.rows_in,
+                                  "rows_out": stp.rows_out, "collapsed": bool(stp.collapsed),
+                                  "level": stp.level})
+                else:
+                    steps.append({"kind": "final", "fan_in": stp.fan_in, "rows_out": stp.rows_out})
+            info["executed_steps"] = steps
 
     # -- row-object compatibility path ------------------------------------------
     def execute(self, rows):
