@@ -330,11 +330,13 @@ void absorb_tiny(int KW, int nt, const KeyDesc& kd, const SlotDesc& sd, int64_t 
 // First chunk of an execute (T empty, <= PR_THREADS * PR_RPT rows): find the
 // distinct keys in first-occurrence order, one block-wide round per key
 // (OrderedIndex.insert_or_aggregate inserting into an empty index,
-// memindex.py:197-236).  If there are at most max_nt of them the chunk needs
-// no flush (max_nt <= M), so the kernel writes the sorted table T (keys +
-// combined states) and publishes the keys to mapped host memory for the
-// absorb kernel's parameters; otherwise it only reports failure and the
-// host runs the general sort path on the chunk.  out (mapped, u64 words):
+// memindex.py:197-236).  If there are at most max_nt of them no flush can
+// happen before the chunk ends (max_nt <= M), and a table holding exactly
+// these keys from the start is equivalent (every row of the chunk hits it):
+// the kernel writes the sorted keys into T with identity states and
+// publishes them to mapped host memory for the absorb kernel, which then
+// aggregates the chunk's rows with the rest.  Otherwise it only reports
+// failure and the host runs the general sort path on the chunk.  out (mapped, u64 words):
 // [0] = nt or ~0 on failure, [8 + j] = lo, [16 + j] = hi of sorted row j.
 #define PR_THREADS 1024
 #define PR_RPT 4
@@ -343,8 +345,7 @@ __global__ void __launch_bounds__(PR_THREADS) k_probe_tiny(KeyDesc kd, SlotDesc 
                                                          u64* __restrict__ T_lo, u64* __restrict__ T_hi,
                                                          u64* __restrict__ T_st, u64* out) {
   __shared__ u64 tlo[8], thi[8];
-  __shared__ u32 s_min, s_rank[8];
-  __shared__ u64 red[PR_THREADS / 32][8];
+  __shared__ u32 s_min;
   const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const u32 NONE = 0xFFFFFFFFu;
   u64 klo[PR_RPT], khi[PR_RPT];
@@ -390,45 +391,18 @@ __global__ void __launch_bounds__(PR_THREADS) k_probe_tiny(KeyDesc kd, SlotDesc 
     if (tid == 0) *(volatile u64*)out = ~0ull;
     return;
   }
-  if (tid < nt) {   // rank of table row tid among the nt keys = its sorted position
+  // table row tid -> its sorted position; states start at the identity (the
+  // absorb pass that follows covers these rows too)
+  if (tid < nt) {
     u32 r = 0;
     for (u32 j = 0; j < nt; ++j) r += key_less<KW>(thi[j], tlo[j], thi[tid], tlo[tid]) ? 1u : 0u;
-    s_rank[tid] = r;
-  }
-  // combined states: per thread over its rows, warp shuffle, then across warps
-  const int S = sd.nslots;
-  for (int s = 0; s < S; ++s) {
-    const int op = sd.op[s], ty = sd.type[s];
-    u64 v[PR_RPT];
-#pragma unroll
-    for (int k = 0; k < PR_RPT; ++k) {
-      const u32 q = k * PR_THREADS + tid;
-      v[k] = q < n ? load_slot_value(sd.src[s], ty, sd.dtype[s], sd.ptr[s], row0 + q) : 0;
-    }
-    const u64 id = identity_slot(op, ty);
-    for (u32 j = 0; j < nt; ++j) {
-      u64 x = id;
-#pragma unroll
-      for (int k = 0; k < PR_RPT; ++k)
-        if (hk[k] == j) x = combine_slot(op, ty, x, v[k]);
-      for (int o = 16; o; o >>= 1) x = combine_slot(op, ty, x, __shfl_xor_sync(0xffffffffu, x, o));
-      if (lane == 0) red[w][j] = x;
-    }
-    __syncthreads();
-    if (tid < nt) {
-      u64 x = red[0][tid];
-      for (int ww = 1; ww < PR_THREADS / 32; ++ww) x = combine_slot(op, ty, x, red[ww][tid]);
-      T_st[(size_t)s_rank[tid] * S + s] = x;
-    }
-    __syncthreads();
-  }
-  if (tid < nt) {
-    const u32 r = s_rank[tid];
     T_lo[r] = tlo[tid];
     if (KW == 2) T_hi[r] = thi[tid];
     ((volatile u64*)out)[8 + r] = tlo[tid];
     ((volatile u64*)out)[16 + r] = thi[tid];
   }
+  const int S = sd.nslots;
+  if (tid < nt * S) T_st[tid] = identity_slot(sd.op[tid % S], sd.type[tid % S]);
   if (tid == 0) *(volatile u64*)out = nt;
 }
 

@@ -416,9 +416,10 @@ struct Engine {
       if (KW == 2) s_hi[i].ensure(n * 8);
       s_val[i].ensure(n * 4);
     }
-    tile_hist.ensure(sort_hist_words((u32)n) * 4 + 64);
-    size_t sc = std::max<size_t>(scan_tmp_words((u32)(sort_hist_words((u32)n) + 1)), scan_tmp_words((u32)n + 1));
-    scan_tmp.ensure((sc + 64) * 4);
+    const size_t had = tile_hist.bytes;
+    tile_hist.ensure(sort_aux_bytes((u32)n) + 64);
+    if (tile_hist.bytes != had) CK(cudaMemsetAsync(tile_hist.p, 0, tile_hist.bytes, st));   // look-back epochs start at 0
+    scan_tmp.ensure((scan_tmp_words((u32)n + 1) + 64) * 4);
   }
   void ensure_collapse(size_t m) {
     cl_flags.ensure((m + 1) * 4);
@@ -464,8 +465,7 @@ struct Engine {
     if (hb < 0) return 0;   // all keys equal: already sorted (stable)
     SortBufs b;
     for (int i = 0; i < 2; ++i) { b.lo[i] = s_lo[i].as<u64>(); b.hi[i] = s_hi[i].as<u64>(); b.val[i] = s_val[i].as<u32>(); }
-    b.tile_hist = tile_hist.as<u32>();
-    b.scan_tmp = scan_tmp.as<u32>();
+    b.aux = tile_hist.p;
     if (KW == 2 && hb >= 64 && lb < 64) {
       // 128-bit keys whose high word varies: sort on the high word, then
       // finish runs of equal high words with a stable sort on the low word
@@ -656,7 +656,6 @@ struct Engine {
     const u32 span = (u32)(b - a);
     const int64_t row0 = a - base;   // column element of row a
     led.chunks++;
-    if (T.n == 0 && span <= probe_rows() && probe_chunk(kd, sd, row0, span)) return b;
     if (T.n > 0 && T.n <= 8 && tiny_ok && absorb_supported((int)T.n, S)) return absorb_chunk(kd, sd, row0, a, span);
     // tiny chunks are not worth the extra pass in auto mode; "always" keeps
     // it down to 4 tiles (also what the parity tests exercise)
@@ -1256,6 +1255,12 @@ struct Engine {
       }
       KeyDesc kd = kd_at(kb);
       SlotDesc sd = sd_at(vb);
+      if (a == 0 && T.n == 0) {
+        // probe: when the first rows hold only a few groups, T starts with
+        // exactly those keys (identity states) and the absorb kernel takes
+        // every row from here on, the probed ones included
+        probe_chunk(kd, sd, a - base, (u32)std::min<int64_t>(probe_rows(), std::min(n, wend) - a));
+      }
       int64_t len = chunk_len(std::min(n, wend) - a, last_len, last_flushed, last_cycle);
       int64_t b = a + len;
       int64_t nxt = process_chunk(kd, sd, base, a, b);
@@ -1361,8 +1366,7 @@ struct Engine {
     partition_dest(KW, kd, m, sp_lo, sp_hi, ns, s_lo_buf(0), s_val[0].as<u32>(), st);
     SortBufs b;
     for (int i = 0; i < 2; ++i) { b.lo[i] = s_lo[i].as<u64>(); b.hi[i] = nullptr; b.val[i] = s_val[i].as<u32>(); }
-    b.tile_hist = tile_hist.as<u32>();
-    b.scan_tmp = scan_tmp.as<u32>();
+    b.aux = tile_hist.p;
     int cur = radix_sort_pairs(1, b, m, 0, 8, st, nullptr);
     const u32* perm = s_val[cur].as<u32>();
     for (int c = 0; c < sch.n_key_cols; ++c) gather_column(key_cols[c], (int)key_elem(c), perm, m, key_out[c], st);

@@ -7,6 +7,8 @@
 #include "isa_kernels.h"
 #include <cstdio>
 #include <algorithm>
+#include <atomic>
+#include <stdexcept>
 
 namespace isa {
 
@@ -118,37 +120,31 @@ __device__ __forceinline__ u32 digit_of(u64 hi, u64 lo, int shift) {
   return (u32)(v & 0xFFu);
 }
 
-template <int KW>
-__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const u64* __restrict__ klo, const u64* __restrict__ khi,
-                                                      u32 n, int shift, u32* __restrict__ tile_hist, u32 ntiles) {
-  __shared__ u32 h[RS_WARPS * 256];
-  for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) h[i] = 0;
-  __syncthreads();
-  const u32 tile = blockIdx.x, base = tile * RS_TILE;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll 4
-  for (int it = 0; it < RS_ITEMS; ++it) {
-    u32 i = base + it * RS_THREADS + threadIdx.x;
-    bool valid = i < n;
-    u32 d = 256 + lane;
-    if (valid) d = digit_of(KW == 2 ? khi[i] : 0, klo[i], shift);
-    u32 peers = __match_any_sync(0xffffffffu, d);
-    if (valid && lane == __ffs(peers) - 1) atomicAdd(&h[w * 256 + d], (u32)__popc(peers));
-  }
-  __syncthreads();
-  for (int d = threadIdx.x; d < 256; d += RS_THREADS) {
-    u32 s = 0;
-#pragma unroll
-    for (int ww = 0; ww < RS_WARPS; ++ww) s += h[ww * 256 + d];
-    tile_hist[(size_t)d * ntiles + tile] = s;
-  }
+#define RS_LB 4   // look-back window (predecessor status words per round trip)
+__device__ __forceinline__ u64 ld_relaxed_gpu(const u64* p) {
+  u64 v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(u64* p, u64 v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// One LSD pass over 8 bits.  Single tile (status == nullptr): the in-tile
+// digit scan is the global offset.  Otherwise onesweep: tiles are taken in
+// order from a counter, every tile publishes its per-digit count and looks
+// back over its predecessors (decoupled look-back) for the exclusive prefix;
+// the digit's global start comes from the all-pass histogram (ghist).
+// Status word per (tile, digit): count | flag << 32 (1 aggregate, 2
+// inclusive prefix) | epoch << 34; words of other passes carry another epoch
+// and read as "not published yet", so the array is never cleared.
 template <int KW>
-__global__ void __launch_bounds__(RS_THREADS, 2) k_rs_scatter(const u64* __restrict__ lo_in, const u64* __restrict__ hi_in,
+__global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : 3) k_rs_scatter(const u64* __restrict__ lo_in, const u64* __restrict__ hi_in,
                                                          const u32* __restrict__ v_in, u64* __restrict__ lo_out,
                                                          u64* __restrict__ hi_out, u32* __restrict__ v_out, u32 n,
-                                                         int shift, const u32* __restrict__ tile_off, u32 ntiles) {
+                                                         int shift, u64* __restrict__ status,
+                                                         const u32* __restrict__ ghist, u32* __restrict__ tile_ctr,
+                                                         u32 epoch) {
   extern __shared__ __align__(16) unsigned char smem[];
   u32* wcnt = (u32*)smem;               // [RS_WARPS][256]
   u32* dstart = wcnt + RS_WARPS * 256;  // [256]
@@ -159,7 +155,9 @@ __global__ void __launch_bounds__(RS_THREADS, 2) k_rs_scatter(const u64* __restr
   u32* s_v = (u32*)(s_lo + KW * RS_TILE);
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const u32 tile = blockIdx.x, base = tile * RS_TILE;
+  if (status && tid == 0) sw[0] = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const u32 tile = status ? sw[0] : blockIdx.x, base = tile * RS_TILE;
   const u32 tile_n = min((u32)RS_TILE, n - base);
   for (int i = tid; i < RS_WARPS * 256; i += RS_THREADS) wcnt[i] = 0;
   __syncthreads();
@@ -206,7 +204,36 @@ __global__ void __launch_bounds__(RS_THREADS, 2) k_rs_scatter(const u64* __restr
     u32 tot;
     u32 ds = block_excl_scan256(run, sw, &tot);
     dstart[d] = ds;
-    gbase[d] = tile_off ? tile_off[(size_t)d * ntiles + tile] - ds : 0u;   // one tile: in-tile offsets are global
+    if (!status) {
+      gbase[d] = 0u;   // one tile: in-tile offsets are global
+    } else {
+      const u32 gs = block_excl_scan256(ghist[d], sw, &tot);   // global start of digit d
+      const u64 E = (u64)epoch << 34;
+      u32 excl = 0;
+      if (tile == 0) {
+        st_relaxed_gpu(status + d, E | (2ull << 32) | run);
+      } else {
+        st_relaxed_gpu(status + (size_t)tile * 256 + d, E | (1ull << 32) | run);
+        // look back RS_LB predecessors per round trip
+        int j = (int)tile - 1;
+        bool done = false;
+        while (!done) {
+          u64 x[RS_LB];
+#pragma unroll
+          for (int i = 0; i < RS_LB; ++i)
+            x[i] = j - i >= 0 ? ld_relaxed_gpu(status + (size_t)(j - i) * 256 + d) : (E | (2ull << 32));
+#pragma unroll
+          for (int i = 0; i < RS_LB; ++i) {
+            if ((x[i] >> 34) != (u64)epoch) break;   // not published yet: reload from tile j
+            excl += (u32)x[i];
+            --j;
+            if (((x[i] >> 32) & 3u) == 2u) { done = true; break; }
+          }
+        }
+        st_relaxed_gpu(status + (size_t)tile * 256 + d, E | (2ull << 32) | (excl + run));
+      }
+      gbase[d] = gs + excl - ds;
+    }
   }
   __syncthreads();
 #pragma unroll
@@ -236,11 +263,34 @@ __global__ void __launch_bounds__(RS_THREADS, 2) k_rs_scatter(const u64* __restr
   }
 }
 
+// Histograms of every pass's digit in one read of the keys (onesweep
+// upsweep): ghist[p][d] += count of digit d at bits [bit_lo + 8p, +8).
+#define RS_MAX_PASS 16
+template <int KW>
+__global__ void __launch_bounds__(256) k_rs_hist_all(const u64* __restrict__ klo, const u64* __restrict__ khi, u32 n,
+                                                     int bit_lo, int npass, u32* __restrict__ ghist) {
+  __shared__ u32 h[RS_MAX_PASS * 256];
+  for (int i = threadIdx.x; i < npass * 256; i += 256) h[i] = 0;
+  __syncthreads();
+  for (u32 i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+    const u64 lo = klo[i], hi = KW == 2 ? khi[i] : 0;
+    for (int p = 0; p < npass; ++p) atomicAdd(&h[p * 256 + digit_of(hi, lo, bit_lo + 8 * p)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < npass * 256; i += 256)
+    if (h[i]) atomicAdd(&ghist[i], h[i]);
+}
+
 static size_t rs_scatter_smem(int KW) {
   return (RS_WARPS * 256 + 256 + 256 + 8) * sizeof(u32) + (size_t)RS_TILE * (8 * KW + 4);
 }
 
-size_t sort_hist_words(u32 n) { return (size_t)256 * ((n + RS_TILE - 1) / RS_TILE); }
+// aux layout: [ghist: RS_MAX_PASS * 256 u32][tile counters: RS_MAX_PASS u32][pad][status: 256 * ntiles u64].
+// The status words sit at a fixed offset and are only ever written as
+// status words (or zero), so no stale counter can alias a live epoch.
+#define RS_AUX_HDR 16640
+size_t sort_aux_bytes(u32 n) { return RS_AUX_HDR + (size_t)256 * ((n + RS_TILE - 1) / RS_TILE) * 8; }
+static std::atomic<u32> g_rs_epoch{0};
 
 int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStream_t st, int64_t* launches,
                      int start) {
@@ -256,30 +306,32 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
   }
   const u32 ntiles = (n + RS_TILE - 1) / RS_TILE;
   const size_t smem = rs_scatter_smem(KW);
-  for (int shift = bit_lo; shift < bit_hi; shift += 8) {
-    int nxt = cur ^ 1;
-    if (ntiles == 1) {   // the scatter's in-tile digit scan is the global offset
-      if (KW == 2)
-        klaunch(k_rs_scatter<2>, 1, RS_THREADS, smem, st, b.lo[cur], b.hi[cur], b.val[cur], b.lo[nxt], b.hi[nxt],
-                b.val[nxt], n, shift, (const u32*)nullptr, 1u);
-      else
-        klaunch(k_rs_scatter<1>, 1, RS_THREADS, smem, st, b.lo[cur], (const u64*)nullptr, b.val[cur], b.lo[nxt],
-                (u64*)nullptr, b.val[nxt], n, shift, (const u32*)nullptr, 1u);
-      cur = nxt;
-      continue;
-    }
-    if (KW == 2) {
-      klaunch(k_rs_hist<2>, ntiles, RS_THREADS, 0, st, b.lo[cur], b.hi[cur], n, shift, b.tile_hist, ntiles);
-      scan_exclusive_u32(b.tile_hist, 256 * ntiles, b.scan_tmp, nullptr, st);
+  const int npass = (bit_hi - bit_lo + 7) / 8;
+  u32* ghist = (u32*)b.aux;
+  u32* tctr = ghist + RS_MAX_PASS * 256;
+  u64* status = (u64*)((char*)b.aux + RS_AUX_HDR);
+  if (ntiles > 1) {
+    if (npass > RS_MAX_PASS) throw std::runtime_error("radix sort: too many passes");
+    cudaMemsetAsync(ghist, 0, (RS_MAX_PASS * 256 + RS_MAX_PASS) * 4, st);
+    const u32 g = std::min<u32>(ntiles, 148u * 8u);
+    if (KW == 2) klaunch(k_rs_hist_all<2>, g, 256, 0, st, b.lo[cur], b.hi[cur], n, bit_lo, npass, ghist);
+    else klaunch(k_rs_hist_all<1>, g, 256, 0, st, b.lo[cur], (const u64*)nullptr, n, bit_lo, npass, ghist);
+  }
+  for (int p = 0; p < npass; ++p) {
+    const int shift = bit_lo + 8 * p;
+    const int nxt = cur ^ 1;
+    const bool one = ntiles == 1;
+    u64* stt = one ? nullptr : status;
+    const u32* gh = one ? nullptr : ghist + p * 256;
+    u32* tc = one ? nullptr : tctr + p;
+    const u32 ep = one ? 0u : ((g_rs_epoch.fetch_add(1) % 0x3FFFFFFEu) + 1u);
+    if (KW == 2)
       klaunch(k_rs_scatter<2>, ntiles, RS_THREADS, smem, st, b.lo[cur], b.hi[cur], b.val[cur], b.lo[nxt], b.hi[nxt],
-                                                         b.val[nxt], n, shift, b.tile_hist, ntiles);
-    } else {
-      klaunch(k_rs_hist<1>, ntiles, RS_THREADS, 0, st, b.lo[cur], nullptr, n, shift, b.tile_hist, ntiles);
-      scan_exclusive_u32(b.tile_hist, 256 * ntiles, b.scan_tmp, nullptr, st);
-      klaunch(k_rs_scatter<1>, ntiles, RS_THREADS, smem, st, b.lo[cur], nullptr, b.val[cur], b.lo[nxt], nullptr,
-                                                         b.val[nxt], n, shift, b.tile_hist, ntiles);
-    }
-    if (launches) *launches += 5;
+              b.val[nxt], n, shift, stt, gh, tc, ep);
+    else
+      klaunch(k_rs_scatter<1>, ntiles, RS_THREADS, smem, st, b.lo[cur], (const u64*)nullptr, b.val[cur], b.lo[nxt],
+              (u64*)nullptr, b.val[nxt], n, shift, stt, gh, tc, ep);
+    if (launches) *launches += 1;
     cur = nxt;
   }
   return cur;

@@ -19,10 +19,9 @@ struct SortBufs {
   u64* lo[2];
   u64* hi[2];
   u32* val[2];
-  u32* tile_hist;   // 256 * ceil(n / 4096)
-  u32* scan_tmp;
+  void* aux;        // sort_aux_bytes(n): look-back status, histograms, tile counters (zeroed when allocated)
 };
-size_t sort_hist_words(u32 n);
+size_t sort_aux_bytes(u32 n);
 int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStream_t st, int64_t* launches,
                      int start = 0);
 // stable insertion sort by the low word of every run of equal high words
