@@ -87,6 +87,8 @@ typedef struct isa_config {
   int32_t preaggregate;      /* tile-local pre-aggregation before the chunk sort: 0 auto, 1 always, 2 never */
   int32_t merge_mode;        /* isa_merge_mode (SortAggConfig.merge_mode) */
   int64_t output_size_hint;  /* SortAggConfig.output_size_hint; <= 0 = none */
+  int32_t run_codec;         /* host-tier runs across PCIe: 0 auto (bit-packed on the GPU when >= 32K rows), 1 raw, 2 packed */
+  int32_t reserved0;
 } isa_config;
 
 /* SortAggConfig.merge_mode (sortagg.py:45-47): wide = in-sort early

@@ -71,6 +71,8 @@ class IsaConfig(ctypes.Structure):
         ("preaggregate", ctypes.c_int32),
         ("merge_mode", ctypes.c_int32),
         ("output_size_hint", ctypes.c_int64),
+        ("run_codec", ctypes.c_int32),
+        ("reserved0", ctypes.c_int32),
     ]
 
 

@@ -1,0 +1,217 @@
+// Run codec: frame-of-reference bit packing of spilled runs.
+//
+// A host-tier run crosses PCIe twice (spill, then wide-merge read-back); at
+// ~55 GB/s per direction against ~6.5 TB/s of HBM that link is the bound of
+// every spilling configuration.  Runs are sorted and their state columns are
+// narrow in practice (counts, bounded sums, keys spread over a block of
+// consecutive sorted values), so each run is packed on the GPU before the
+// D2H copy and unpacked on the GPU after the H2D copy: HBM-speed integer
+// work traded for link bytes.  Lossless for every bit pattern.
+//
+// Block of PK_ROWS consecutive run rows; columns = key words (lo, then hi
+// for 128-bit keys), then the S state slots.  Every column value is mapped
+// to an order-preserving u64 (keys: as is; int64 slots: x ^ 2^63; f64 slots:
+// the IEEE sortable transform), then coded as (value - block minimum) in
+// `width` bits, width = bits of (max - min).  Random access (a row's value
+// from its block header and two payload words) keeps binary search over
+// packed runs possible in place (the wide merge's exact slice bounds).
+//
+// Block layout (8-byte words): ncol headers {base, width | word_off << 8},
+// then every column's payload words (word_off counted from the payload).
+#include "isa_kernels.h"
+
+namespace isa {
+
+#define PK_THREADS 256
+
+__host__ __device__ __forceinline__ int pk_ncol(int kw, int S) { return kw + S; }
+
+__device__ __forceinline__ u64 pk_fwd(u64 bits, int is_f64, int is_key) {
+  if (is_key) return bits;
+  if (is_f64) return (bits >> 63) ? ~bits : (bits ^ 0x8000000000000000ull);
+  return bits ^ 0x8000000000000000ull;
+}
+__device__ __forceinline__ u64 pk_inv(u64 v, int is_f64, int is_key) {
+  if (is_key) return v;
+  if (is_f64) return (v >> 63) ? (v ^ 0x8000000000000000ull) : ~v;
+  return v ^ 0x8000000000000000ull;
+}
+
+__device__ __forceinline__ u64 pk_get(const PackSrc& p, int c, u32 row) {
+  if (c < p.kw) return c == 0 ? p.lo[row] : p.hi[row];
+  const int s = c - p.kw;
+  return pk_fwd(p.st[(size_t)row * p.S + s], (p.fmask >> s) & 1u, 0);
+}
+
+__device__ __forceinline__ u64 pk_extract(const u64* w, u32 i, u32 width) {
+  if (width == 0) return 0;
+  const u64 bit = (u64)i * width;
+  const u32 q = (u32)(bit >> 6), r = (u32)(bit & 63);
+  u64 x = w[q] >> r;
+  if (r + width > 64) x |= w[q + 1] << (64 - r);
+  return width == 64 ? x : (x & ((1ull << width) - 1));
+}
+
+__device__ __forceinline__ u64 block_reduce_min_max(u64 v, bool is_max, u64* sw) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int o = 16; o; o >>= 1) {
+    const u64 t = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? (t > v ? t : v) : (t < v ? t : v);
+  }
+  __syncthreads();
+  if (lane == 0) sw[w] = v;
+  __syncthreads();
+  u64 r = sw[0];
+  for (int i = 1; i < PK_THREADS / 32; ++i) r = is_max ? (sw[i] > r ? sw[i] : r) : (sw[i] < r ? sw[i] : r);
+  return r;
+}
+
+// per (block, column): base, width, payload word offset; per block: bytes
+__global__ void __launch_bounds__(PK_THREADS) k_pack_sizes(PackSrc p, u64* __restrict__ hdr, u32* __restrict__ blk_bytes) {
+  __shared__ u64 sw[PK_THREADS / 32];
+  const u32 b = blockIdx.x, r0 = b * PK_ROWS;
+  const u32 rows = min((u32)PK_ROWS, p.n - r0);
+  const int ncol = pk_ncol(p.kw, p.S);
+  u64 word_off = 0;
+  for (int c = 0; c < ncol; ++c) {
+    u64 mn = ~0ull, mx = 0;
+    for (u32 i = threadIdx.x; i < rows; i += PK_THREADS) {
+      const u64 v = pk_get(p, c, r0 + i);
+      mn = v < mn ? v : mn;
+      mx = v > mx ? v : mx;
+    }
+    mn = block_reduce_min_max(mn, false, sw);
+    mx = block_reduce_min_max(mx, true, sw);
+    const u32 width = mx == mn ? 0u : (u32)(64 - __clzll((long long)(mx - mn)));
+    if (threadIdx.x == 0) {
+      hdr[((size_t)b * ncol + c) * 2] = mn;
+      hdr[((size_t)b * ncol + c) * 2 + 1] = (u64)width | (word_off << 8);
+    }
+    word_off += ((u64)rows * width + 63) / 64;
+  }
+  if (threadIdx.x == 0) blk_bytes[b] = (u32)((ncol * 2 + word_off) * 8);
+}
+
+// write every block at its offset: headers, then each column's packed words
+__global__ void __launch_bounds__(PK_THREADS) k_pack_write(PackSrc p, const u64* __restrict__ hdr,
+                                                           const u32* __restrict__ blk_off, char* __restrict__ out) {
+  __shared__ u64 vals[PK_ROWS];
+  const u32 b = blockIdx.x, r0 = b * PK_ROWS;
+  const u32 rows = min((u32)PK_ROWS, p.n - r0);
+  const int ncol = pk_ncol(p.kw, p.S);
+  u64* blk = (u64*)(out + blk_off[b]);
+  for (int i = threadIdx.x; i < ncol * 2; i += PK_THREADS) blk[i] = hdr[(size_t)b * ncol * 2 + i];
+  u64* payload = blk + ncol * 2;
+  for (int c = 0; c < ncol; ++c) {
+    const u64 base = hdr[((size_t)b * ncol + c) * 2];
+    const u64 meta = hdr[((size_t)b * ncol + c) * 2 + 1];
+    const u32 width = (u32)(meta & 0xFF);
+    if (width == 0) continue;
+    __syncthreads();
+    for (u32 i = threadIdx.x; i < rows; i += PK_THREADS) vals[i] = pk_get(p, c, r0 + i) - base;
+    __syncthreads();
+    u64* wout = payload + (meta >> 8);
+    const u32 nwords = (u32)(((u64)rows * width + 63) / 64);
+    for (u32 q = threadIdx.x; q < nwords; q += PK_THREADS) {
+      const u64 lo_bit = (u64)q * 64;
+      const u32 i0 = (u32)(lo_bit / width);
+      const u32 i1 = min(rows - 1, (u32)((lo_bit + 63) / width));
+      u64 word = 0;
+      for (u32 i = i0; i <= i1; ++i) {
+        const long long pos = (long long)((u64)i * width) - (long long)lo_bit;   // bit of value i in this word
+        const u64 v = vals[i];
+        word |= pos >= 0 ? (v << pos) : (v >> (-pos));
+      }
+      wout[q] = word;
+    }
+  }
+}
+
+u32 pack_blocks(u32 n) { return (n + PK_ROWS - 1) / PK_ROWS; }
+
+void pack_sizes(const PackSrc& p, u64* hdr, u32* blk_bytes, cudaStream_t st) {
+  const u32 nb = pack_blocks(p.n);
+  if (nb) klaunch(k_pack_sizes, nb, PK_THREADS, 0, st, p, hdr, blk_bytes);
+}
+
+void pack_write(const PackSrc& p, const u64* hdr, const u32* blk_off, char* out, cudaStream_t st) {
+  const u32 nb = pack_blocks(p.n);
+  if (nb) klaunch(k_pack_write, nb, PK_THREADS, 0, st, p, hdr, blk_off, out);
+}
+
+// one CTA per descriptor: rows [e0, e1) of a packed block -> dst rows
+__global__ void __launch_bounds__(PK_THREADS) k_unpack(const UnpackBlk* __restrict__ d, const char* __restrict__ src,
+                                                       int kw, int S, u32 fmask, u64* __restrict__ lo,
+                                                       u64* __restrict__ hi, u64* __restrict__ st) {
+  const UnpackBlk u = d[blockIdx.x];
+  const u64* blk = (const u64*)(src + u.src_off);
+  const int ncol = pk_ncol(kw, S);
+  const u64* payload = blk + ncol * 2;
+  for (int c = 0; c < ncol; ++c) {
+    const u64 base = blk[c * 2], meta = blk[c * 2 + 1];
+    const u32 width = (u32)(meta & 0xFF);
+    const u64* w = payload + (meta >> 8);
+    for (u32 i = u.e0 + threadIdx.x; i < u.e1; i += PK_THREADS) {
+      const u64 v = base + pk_extract(w, i, width);
+      const u32 o = u.dst + (i - u.e0);
+      if (c < kw) {
+        if (c == 0) lo[o] = v;
+        else hi[o] = v;
+      } else {
+        const int s = c - kw;
+        st[(size_t)o * S + s] = pk_inv(v, (fmask >> s) & 1u, 0);
+      }
+    }
+  }
+}
+
+void unpack_blocks(const UnpackBlk* d, u32 nd, const char* src, int kw, int S, u32 fmask, u64* lo, u64* hi, u64* st,
+                   cudaStream_t stream) {
+  if (nd) klaunch(k_unpack, nd, PK_THREADS, 0, stream, d, src, kw, S, fmask, lo, hi, st);
+}
+
+// key of `row` of a packed run, read in place (mapped host memory)
+template <int KW>
+__device__ __forceinline__ void pk_key_at(const RunRef& r, u32 row, u64& khi, u64& klo) {
+  const u32 b = row / PK_ROWS, i = row % PK_ROWS;
+  const u64* blk = (const u64*)(r.pk + r.blk_off[b]);
+  const int ncol = pk_ncol(KW, r.S);
+  const u64* payload = blk + ncol * 2;
+  klo = blk[0] + pk_extract(payload + (blk[1] >> 8), i, (u32)(blk[1] & 0xFF));
+  khi = 0;
+  if (KW == 2) khi = blk[2] + pk_extract(payload + (blk[3] >> 8), i, (u32)(blk[3] & 0xFF));
+}
+
+template <int KW>
+__global__ void k_run_lower_bounds(const RunRef* __restrict__ runs, int nruns, const u64* __restrict__ b_lo,
+                                   const u64* __restrict__ b_hi, int nb, u32* __restrict__ out) {
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nruns * nb) return;
+  int r = q / nb, b = q % nb;
+  const RunRef rr = runs[r];
+  u32 l = 0, h = rr.rows;
+  const u64 khi = KW == 2 ? b_hi[b] : 0, klo = b_lo[b];
+  while (l < h) {
+    const u32 m = (l + h) >> 1;
+    u64 mhi = 0, mlo;
+    if (rr.pk) {
+      pk_key_at<KW>(rr, m, mhi, mlo);
+    } else {
+      mlo = rr.lo[m];
+      if (KW == 2) mhi = rr.hi[m];
+    }
+    if (key_less<KW>(mhi, mlo, khi, klo)) l = m + 1; else h = m;
+  }
+  out[q] = l;
+}
+
+void run_lower_bounds(int KW, const RunRef* runs_dev, int nruns, const u64* b_lo, const u64* b_hi, int nb, u32* out,
+                      cudaStream_t st) {
+  int n = nruns * nb;
+  if (n == 0) return;
+  int g = (n + 127) / 128;
+  if (KW == 2) klaunch(k_run_lower_bounds<2>, g, 128, 0, st, runs_dev, nruns, b_lo, b_hi, nb, out);
+  else klaunch(k_run_lower_bounds<1>, g, 128, 0, st, runs_dev, nruns, b_lo, b_hi, nb, out);
+}
+
+}  // namespace isa

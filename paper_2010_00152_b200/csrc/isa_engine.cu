@@ -122,6 +122,7 @@ struct DevicePool {
 // sorted unique group table (keys SoA, states AoS) in device memory
 struct Table {
   DevBuf lo, hi, st;
+  DevBuf pk;   // packed image of the table while it is being spilled
   u32 n = 0;
   u64* plo() { return lo.as<u64>(); }
   u64* phi() { return hi.as<u64>(); }
@@ -131,7 +132,7 @@ struct Table {
     if (KW == 2) hi.ensure(cap * 8);
     if (S) st.ensure(cap * 8 * S);
   }
-  void release() { lo.release(); hi.release(); st.release(); n = 0; }
+  void release() { lo.release(); hi.release(); st.release(); pk.release(); n = 0; }
 };
 
 struct Run {
@@ -143,6 +144,12 @@ struct Run {
   u32 rows = 0;
   bool host = true;
   int level = 0;
+  // packed host run (isa_codec.cu): blocks of PK_ROWS rows
+  const char* pk_host = nullptr;   // host view
+  const char* pk_dev = nullptr;    // mapped device view (slice search)
+  const u32* off_host = nullptr;   // block byte offsets (nblk + 1)
+  const u32* off_dev = nullptr;
+  u32 nblk = 0;
 };
 
 struct Window {      // staged host input
@@ -214,6 +221,13 @@ struct Engine {
   DevBuf stg_lo[2], stg_hi[2], stg_st[2];
   cudaEvent_t stg_ready[2] = {nullptr, nullptr}, stg_free[2] = {nullptr, nullptr};
   DevBuf runref_dev, bounds_lo, bounds_hi, bounds_out;
+  DevBuf pk_hdr, pk_sz;                     // codec: block headers, block byte sizes -> offsets
+  DevBuf stg_pk[2], stg_desc[2];            // wide merge: packed bytes and unpack descriptors per slot
+  std::vector<UnpackBlk> desc_host[2];
+  UnpackBlk* desc_pinned[2] = {nullptr, nullptr};
+  size_t desc_cap[2] = {0, 0};
+  cudaEvent_t desc_done[2] = {nullptr, nullptr};
+  u32 fmask = 0;                            // f64 state slots (codec transform)
   Table result;
   DevBuf out_tmp;
   // host input windows
@@ -270,6 +284,8 @@ struct Engine {
     for (int i = 0; i < 2; ++i) {
       CK(cudaEventCreateWithFlags(&stg_ready[i], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&stg_free[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&desc_done[i], cudaEventDisableTiming));
+      CK(cudaEventRecord(desc_done[i], 0));
       CK(cudaEventCreateWithFlags(&win[i].ready, cudaEventDisableTiming));
     }
     CK(cudaHostAlloc((void**)&h_scal, 64 * sizeof(u64), cudaHostAllocMapped));
@@ -284,7 +300,12 @@ struct Engine {
                       &scal, &bitmap, &word_tmp, &cl_flags, &cl_partial, &cl_pslot, &mg_rank_a, &mg_match_a,
                       &mg_rank_b, &mg_match_b, &ab_partials, &ab_miss_buf, &ab_miss_cnt, &ab_miss_off,
                       &miss_list, &stg_lo[0], &stg_lo[1], &stg_hi[0], &stg_hi[1], &stg_st[0], &stg_st[1],
-                      &runref_dev, &bounds_lo, &bounds_hi, &bounds_out, &out_tmp};
+                      &runref_dev, &bounds_lo, &bounds_hi, &bounds_out, &out_tmp, &pk_hdr, &pk_sz,
+                      &stg_pk[0], &stg_pk[1], &stg_desc[0], &stg_desc[1]};
+    for (int i = 0; i < 2; ++i) {
+      if (desc_pinned[i]) cudaFreeHost(desc_pinned[i]);
+      if (desc_done[i]) cudaEventDestroy(desc_done[i]);
+    }
     for (auto* b : bufs) b->release();
     for (auto& w : win) { for (auto& b : w.keys) b.release(); for (auto& b : w.vals) b.release(); }
     for (auto& r : recs) { ev_pool.push_back(r.a); ev_pool.push_back(r.b); }
@@ -318,6 +339,7 @@ struct Engine {
       throw IsaError(ISA_ERR_INVALID_INPUT, "memory budget above 2^30 groups is not supported");
     if (cfg.preaggregate < 0 || cfg.preaggregate > 2) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown preaggregate mode");
     if (cfg.merge_mode < ISA_MERGE_WIDE || cfg.merge_mode > ISA_MERGE_SEPARATE) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown merge mode");
+    if (cfg.run_codec < 0 || cfg.run_codec > 2) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown run codec");
     if (cfg.run_tier != ISA_TIER_HOST && cfg.run_tier != ISA_TIER_HBM)
       throw IsaError(ISA_ERR_INVALID_INPUT, "unknown run tier");
     if (sch.n_key_cols < 1) throw IsaError(ISA_ERR_INVALID_INPUT, "schema needs at least one key column");
@@ -357,6 +379,7 @@ struct Engine {
       if (src != ISA_SRC_ONE && src != ISA_SRC_COLUMN) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown slot source");
       sd0.op[s] = ops[s] = op;
       sd0.type[s] = types[s] = ty;
+      if (ty == ISA_SLOT_F64) fmask |= 1u << s;
       sd0.src[s] = src;
       if (src == ISA_SRC_COLUMN) {
         int col = sch.slot_col[s];
@@ -620,9 +643,69 @@ struct Engine {
     led.pages_written += (r.rows + cfg.page_capacity - 1) / cfg.page_capacity;
   }
 
+  // small runs are not worth the extra synchronization (their link time is tiny)
+  bool pack_runs(u32 rows) const {
+    if (cfg.run_tier != ISA_TIER_HOST || cfg.merge_mode != ISA_MERGE_WIDE) return false;
+    return cfg.run_codec == 2 || (cfg.run_codec == 0 && rows >= kPackMinRows);
+  }
+  static constexpr u32 kPackMinRows = 1u << 15;
+
+  // T packed on the GPU (isa_codec.cu), then the packed bytes cross PCIe.
+  // One host synchronization learns the packed size.
+  Run spill_packed(Table& t) {
+    PackSrc ps{t.plo(), t.phi(), t.pst(), t.n, KW, S, fmask};
+    const u32 nblk = pack_blocks(t.n);
+    const int ncol = KW + S;
+    pk_hdr.ensure((size_t)nblk * ncol * 16 + 16);
+    pk_sz.ensure((size_t)(nblk + 1) * 4 + 16);
+    scan_tmp.ensure((scan_tmp_words(nblk + 1) + 64) * 4);
+    pack_sizes(ps, pk_hdr.as<u64>(), pk_sz.as<u32>(), st);
+    scan_exclusive_u32(pk_sz.as<u32>(), nblk, scan_tmp.as<u32>(), pk_sz.as<u32>() + nblk, st);
+    const u32 bytes = read_u32(pk_sz.as<u32>() + nblk);   // offsets[nblk] = total
+    // packed blocks, then the block offsets: both owned by the table until
+    // its D2H copies are done (pk_sz is reused by the next spill)
+    const size_t off_at = ((size_t)bytes + 15) & ~(size_t)15;
+    t.pk.ensure(off_at + (size_t)(nblk + 1) * 4 + 16);
+    pack_write(ps, pk_hdr.as<u64>(), pk_sz.as<u32>(), t.pk.as<char>(), st);
+    CK(cudaMemcpyAsync(t.pk.as<char>() + off_at, pk_sz.p, (size_t)(nblk + 1) * 4, cudaMemcpyDeviceToDevice, st));
+    Run r;
+    r.rows = t.n;
+    r.host = true;
+    r.nblk = nblk;
+    char* hb = pinned.alloc((size_t)bytes + 16);
+    u32* hoff = (u32*)pinned.alloc((size_t)(nblk + 1) * 4 + 16);
+    const char* db = nullptr;
+    const u32* doff = nullptr;
+    CK(cudaHostGetDevicePointer((void**)&db, hb, 0));
+    CK(cudaHostGetDevicePointer((void**)&doff, hoff, 0));
+    r.pk_host = hb; r.pk_dev = db; r.off_host = hoff; r.off_dev = doff;
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, st));
+    CK(cudaStreamWaitEvent(d2h, ev, 0));
+    cudaEventDestroy(ev);
+    CK(cudaMemcpyAsync(hb, t.pk.p, bytes, cudaMemcpyDeviceToHost, d2h));
+    CK(cudaMemcpyAsync(hoff, t.pk.as<char>() + off_at, (size_t)(nblk + 1) * 4, cudaMemcpyDeviceToHost, d2h));
+    led.bytes_d2h += bytes + (size_t)(nblk + 1) * 4;
+    return r;
+  }
+
   // T becomes a run (RunWriter of a read-sort-write flush, sortagg.py:344-350)
   void spill_T() {
     if (T.n == 0) return;
+    if (pack_runs(T.n)) {
+      Run r = spill_packed(T);
+      CK(cudaEventRecord(spill_done, d2h));
+      cudaEvent_t bev;
+      if (!busy_ev_pool.empty()) { bev = busy_ev_pool.back(); busy_ev_pool.pop_back(); }
+      else CK(cudaEventCreateWithFlags(&bev, cudaEventDisableTiming));
+      CK(cudaEventRecord(bev, d2h));
+      busy.push_back({T, bev});
+      T = take_table();
+      runs.push_back(r);
+      account_written(r);
+      return;
+    }
     Run r = alloc_run(T.n);
     if (cfg.run_tier == ISA_TIER_HOST) {
       // copy on the d2h stream after the table is complete; the table's
@@ -891,7 +974,18 @@ struct Engine {
       for (auto& r : runs) {   // every strided sample copy first, one synchronization after
         int64_t ns = (r.rows + F - 1) / F;
         if (ns == 0) continue;
-        if (r.host) {
+        if (r.pk_host) {
+          // block minima of the key words: (hi of the block's first row,
+          // lowest lo of the block) <= the first key -- split points only
+          // need to be keys in range, slice bounds are searched exactly
+          const int ncol = KW + S;
+          for (int64_t i = 0; i < ns; ++i) {
+            const u64* blk = (const u64*)(r.pk_host + r.off_host[(i * F) / PK_ROWS]);
+            tmp_lo[o + i] = blk[0];
+            if (KW == 2) tmp_hi[o + i] = blk[2];
+            (void)ncol;
+          }
+        } else if (r.host) {
           for (int64_t i = 0; i < ns; ++i) {
             tmp_lo[o + i] = r.host_lo[i * F];
             if (KW == 2) tmp_hi[o + i] = r.host_hi[i * F];
@@ -922,7 +1016,7 @@ struct Engine {
     std::vector<u32> lb((size_t)k * std::max(nb, 1));
     if (nb > 0) {
       std::vector<RunRef> refs(k);
-      for (int i = 0; i < k; ++i) refs[i] = {runs[i].lo, runs[i].hi, runs[i].rows};
+      for (int i = 0; i < k; ++i) refs[i] = {runs[i].lo, runs[i].hi, runs[i].rows, S, runs[i].pk_dev, runs[i].off_dev};
       runref_dev.ensure(sizeof(RunRef) * k);
       bounds_lo.ensure(8 * nb);
       bounds_hi.ensure(8 * nb);
@@ -953,20 +1047,76 @@ struct Engine {
       if (S) stg_st[i].ensure(wmax * 8 * S + 8);
       CK(cudaEventRecord(stg_free[i], st));
     }
+    bool any_packed = false;
+    for (auto& r : runs) any_packed |= r.pk_host != nullptr;
+    if (any_packed) {
+      // packed bytes per window: at most the covering blocks of every slice
+      size_t pmax = 0;
+      for (int w = 0; w < nwin; ++w) {
+        size_t b = 0;
+        for (int r = 0; r < k; ++r) {
+          if (!runs[r].pk_host) continue;
+          u32 s0, s1;
+          slice(r, w, s0, s1);
+          if (s1 > s0) b += runs[r].off_host[(s1 - 1) / PK_ROWS + 1] - runs[r].off_host[s0 / PK_ROWS];
+        }
+        pmax = std::max(pmax, b);
+      }
+      for (int i = 0; i < 2; ++i) stg_pk[i].ensure(pmax + 16);
+    }
     auto stage = [&](int w, int slot) -> int64_t {
       CK(cudaStreamWaitEvent(h2d, stg_free[slot], 0));
       int64_t off = 0;
+      size_t poff = 0;
+      auto& desc = desc_host[slot];
+      desc.clear();
       for (int r = 0; r < k; ++r) {
         u32 s0, s1;
         slice(r, w, s0, s1);
         size_t cnt = s1 - s0;
         if (!cnt) continue;
+        if (runs[r].pk_host) {
+          // covering blocks' bytes, then one unpack descriptor per block
+          const u32 b0 = s0 / PK_ROWS, b1 = (s1 - 1) / PK_ROWS;
+          const u32 o0 = runs[r].off_host[b0], o1 = runs[r].off_host[b1 + 1];
+          CK(cudaMemcpyAsync(stg_pk[slot].as<char>() + poff, runs[r].pk_host + o0, o1 - o0, cudaMemcpyHostToDevice, h2d));
+          led.bytes_h2d += o1 - o0;
+          for (u32 b = b0; b <= b1; ++b) {
+            const u32 r0 = b * PK_ROWS;
+            UnpackBlk d;
+            d.src_off = poff + (runs[r].off_host[b] - o0);
+            d.e0 = std::max(s0, r0) - r0;
+            d.e1 = std::min<u32>(s1, std::min<u32>(r0 + PK_ROWS, runs[r].rows)) - r0;
+            d.dst = (u32)(off + (r0 + d.e0 - s0));
+            d.pad = 0;
+            desc.push_back(d);
+          }
+          poff += o1 - o0;
+          off += cnt;
+          continue;
+        }
         cudaMemcpyKind kind = runs[r].host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
         CK(cudaMemcpyAsync(stg_lo[slot].as<u64>() + off, runs[r].lo + s0, cnt * 8, cudaMemcpyDefault, h2d));
         if (KW == 2) CK(cudaMemcpyAsync(stg_hi[slot].as<u64>() + off, runs[r].hi + s0, cnt * 8, cudaMemcpyDefault, h2d));
         if (S) CK(cudaMemcpyAsync(stg_st[slot].as<u64>() + off * S, runs[r].st + (size_t)s0 * S, cnt * 8 * S, cudaMemcpyDefault, h2d));
         if (kind == cudaMemcpyHostToDevice) led.bytes_h2d += cnt * 8 * (KW + S);
         off += cnt;
+      }
+      if (!desc.empty()) {
+        // descriptors through a pinned buffer (its previous copy must be done)
+        CK(cudaEventSynchronize(desc_done[slot]));
+        if (desc_cap[slot] < desc.size()) {
+          if (desc_pinned[slot]) CK(cudaFreeHost(desc_pinned[slot]));
+          desc_cap[slot] = desc.size() + desc.size() / 2 + 64;
+          CK(cudaHostAlloc((void**)&desc_pinned[slot], desc_cap[slot] * sizeof(UnpackBlk), cudaHostAllocDefault));
+        }
+        memcpy(desc_pinned[slot], desc.data(), desc.size() * sizeof(UnpackBlk));
+        stg_desc[slot].ensure(desc.size() * sizeof(UnpackBlk) + 16);
+        CK(cudaMemcpyAsync(stg_desc[slot].p, desc_pinned[slot], desc.size() * sizeof(UnpackBlk),
+                           cudaMemcpyHostToDevice, h2d));
+        CK(cudaEventRecord(desc_done[slot], h2d));
+        unpack_blocks(stg_desc[slot].as<UnpackBlk>(), (u32)desc.size(), stg_pk[slot].as<char>(), KW, S, fmask,
+                      stg_lo[slot].as<u64>(), stg_hi[slot].as<u64>(), stg_st[slot].as<u64>(), h2d);
       }
       CK(cudaEventRecord(stg_ready[slot], h2d));
       return off;

@@ -854,33 +854,6 @@ void compact_misses(const u32* miss_buf, const u32* miss_cnt, const u32* miss_of
   klaunch(k_compact_misses, grid, 256, 0, st, miss_buf, miss_cnt, miss_off, rows_per_cta, out);
 }
 
-// ============================================================ runs ====
-template <int KW>
-__global__ void k_run_lower_bounds(const RunRef* __restrict__ runs, int nruns, const u64* __restrict__ b_lo,
-                                   const u64* __restrict__ b_hi, int nb, u32* __restrict__ out) {
-  int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= nruns * nb) return;
-  int r = q / nb, b = q % nb;
-  RunRef rr = runs[r];
-  u32 l = 0, h = rr.rows;
-  u64 khi = KW == 2 ? b_hi[b] : 0, klo = b_lo[b];
-  while (l < h) {
-    u32 m = (l + h) >> 1;
-    u64 mhi = KW == 2 ? rr.hi[m] : 0;
-    if (key_less<KW>(mhi, rr.lo[m], khi, klo)) l = m + 1; else h = m;
-  }
-  out[q] = l;
-}
-
-void run_lower_bounds(int KW, const RunRef* runs_dev, int nruns, const u64* b_lo, const u64* b_hi, int nb, u32* out,
-                      cudaStream_t st) {
-  int n = nruns * nb;
-  if (n == 0) return;
-  int g = (n + 127) / 128;
-  if (KW == 2) klaunch(k_run_lower_bounds<2>, g, 128, 0, st, runs_dev, nruns, b_lo, b_hi, nb, out);
-  else klaunch(k_run_lower_bounds<1>, g, 128, 0, st, runs_dev, nruns, b_lo, b_hi, nb, out);
-}
-
 // ========================================================== export ====
 __global__ void k_export_key(const u64* __restrict__ lo, const u64* __restrict__ hi, u32 n, int dtype, int shift,
                              int width, void* out) {

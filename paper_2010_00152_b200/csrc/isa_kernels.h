@@ -115,7 +115,20 @@ void compact_misses(const u32* miss_buf, const u32* miss_cnt, const u32* miss_of
 
 // ---- runs / wide merge helpers ------------------------------------------
 // out[r * nb + b] = lower_bound(run r, bound b); run keys may be mapped host memory
-struct RunRef { const u64* lo; const u64* hi; u32 rows; };
+// A run for the wide merge's slice search: raw key words (lo/hi), or a
+// packed run (pk != nullptr: blocks at pk + blk_off[b], S state slots).
+struct RunRef { const u64* lo; const u64* hi; u32 rows; int S; const char* pk; const u32* blk_off; };
+
+// ---- run codec (isa_codec.cu) -------------------------------------------
+#define PK_ROWS 1024
+struct PackSrc { const u64* lo; const u64* hi; const u64* st; u32 n; int kw; int S; u32 fmask; };
+struct UnpackBlk { u64 src_off; u32 e0, e1, dst, pad; };
+u32 pack_blocks(u32 n);
+// per-block headers (ncol x 2 u64) and byte sizes
+void pack_sizes(const PackSrc& p, u64* hdr, u32* blk_bytes, cudaStream_t st);
+void pack_write(const PackSrc& p, const u64* hdr, const u32* blk_off, char* out, cudaStream_t st);
+void unpack_blocks(const UnpackBlk* d, u32 nd, const char* src, int kw, int S, u32 fmask, u64* lo, u64* hi, u64* st,
+                   cudaStream_t stream);
 void run_lower_bounds(int KW, const RunRef* runs_dev, int nruns, const u64* b_lo, const u64* b_hi,
                       int nb, u32* out, cudaStream_t st);
 

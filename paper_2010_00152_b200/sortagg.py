@@ -68,6 +68,7 @@ class SortAggConfig:
     window_rows: int = 0            # host-input staging window, 0 = default
     merge_window_rows: int = 0      # wide-merge key-range window capacity, 0 = default
     preaggregate: str = "auto"      # tile-local pre-aggregation before chunk sorts: auto | always | never
+    run_codec: str = "auto"         # host-tier runs cross PCIe bit-packed: auto (runs >= 32K rows) | packed | raw
 
     def __post_init__(self):
         if self.page_capacity < 1:
@@ -85,6 +86,8 @@ class SortAggConfig:
             raise InvalidInputError(f"unknown run tier {self.run_tier!r}")
         if self.preaggregate not in ("auto", "always", "never"):
             raise InvalidInputError(f"unknown preaggregate mode {self.preaggregate!r}")
+        if self.run_codec not in ("auto", "packed", "raw"):
+            raise InvalidInputError(f"unknown run codec {self.run_codec!r}")
 
     @property
     def max_fanin(self):
@@ -376,6 +379,7 @@ class SortAggregate:
         cfg.merge_mode = {WIDE: _native.MERGE_WIDE, TRADITIONAL: _native.MERGE_TRADITIONAL,
                           SEPARATE: _native.MERGE_SEPARATE}[self.config.merge_mode]
         cfg.output_size_hint = self.config.output_size_hint if self.config.output_size_hint is not None else 0
+        cfg.run_codec = {"auto": 0, "raw": 1, "packed": 2}[self.config.run_codec]
         sch = _native.IsaSchema()
         if len(key_codes) > _native.MAX_KEY_COLS:
             raise InvalidInputError("too many key columns")
