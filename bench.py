@@ -18,7 +18,10 @@ Contract (one JSON line on rank 0):
   launch duration (CUDA events inside the library), against the measured HBM
   copy bandwidth in MEASURED_PEAKS.json.  step_roofline = the minimum-traffic
   step time (B_in + B_out) / BW_HBM (+ spill bytes / link BW when runs go to
-  the host tier) over the measured step time.
+  the host tier) over the measured step time; spill bytes are the
+  algorithmic ones (spilled rows x row bytes, written and read back).  Runs
+  cross PCIe bit-packed, so b_link_moved / frac_moved restate the bound with
+  the bytes that actually moved.
 * cpu_baseline = the oracle port (oracle/rsw_oracle.c: read-sort-write run
   generation + wide merge, key-range partitioned over all host threads) on a
   bounded sample of the same workload, rank 0 at N = 1.
@@ -304,6 +307,10 @@ def main():
     spill_rows = dled.get("rows_spilled", 0)   # last execute (every step is identical)
     spill_b = 2 * spill_rows * (key_b + 8 * w.schema.state_slots) if run_tier == "host" else 0
     t_star = (b_in + out_b) / (peak * 1e9) + spill_b / (link * 1e9)
+    # the same bound with the link bytes actually moved (host-tier runs cross
+    # PCIe bit-packed by the run codec, so this can be well below spill_b)
+    link_b = (dled.get("bytes_d2h", 0) + dled.get("bytes_h2d", 0)) if run_tier == "host" else 0
+    t_moved = (b_in + out_b) / (peak * 1e9) + link_b / (link * 1e9)
     # dominant kernel: the phase with the most device time among kernel phases
     kernel_phases = ["absorb", "sort", "collapse", "table_merge", "wm_sort", "wm_collapse", "flush"]
     dom = max(kernel_phases, key=lambda k: phase_tot.get(k, {}).get("ms", 0.0))
@@ -350,7 +357,8 @@ def main():
                      "launches_per_step": dp["calls"] / max(1, args.steps), "peak_source": peak_src},
         "step_roofline": {"t_star_ms": t_star * 1e3, "frac": (t_star * 1e3) / ms_step if ms_step else None,
                           "b_in": b_in, "b_out": out_b, "b_spill": spill_b, "link_gbs": link,
-                          "hbm_gbs": peak},
+                          "hbm_gbs": peak, "b_link_moved": link_b, "t_moved_ms": t_moved * 1e3,
+                          "frac_moved": (t_moved * 1e3) / ms_step if ms_step else None},
         "phases_ms_per_step": {k: v["ms"] / max(1, args.steps) for k, v in phase_tot.items() if v["ms"]},
         "ledger_per_step": {"rows_spilled": spill_rows, "runs": op.runs_after_generation,
                             "bytes_d2h": dled.get("bytes_d2h"), "bytes_h2d": dled.get("bytes_h2d"),

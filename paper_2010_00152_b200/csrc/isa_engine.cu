@@ -471,7 +471,9 @@ struct Engine {
   }
   int sort_built(u32 m) {
     u64 vlo, vhi;
-    if (key_bits <= 16) {   // at most two 8-bit passes: sort every bit, no host round trip
+    if (key_bits <= 16 || (key_bits <= 32 && m <= (1u << 20))) {
+      // at most two 8-bit passes, or a small chunk of <= 32-bit keys: sort
+      // every key bit instead of a host round trip for the varying bits
       vlo = key_bits == 64 ? ~0ull : ((1ull << key_bits) - 1);
       vhi = 0;
     } else {
@@ -514,14 +516,25 @@ struct Engine {
     CK(cudaMemsetAsync(dscal32(0), 0, sizeof(u32), st));
     new_heads(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, T.plo(), T.phi(), T.n,
               bitmap.as<u32>(), dscal32(0), st, firstpos);
+    const int64_t M = cfg.memory_budget;
+    u32 k = (u32)(M - (int64_t)T.n + 1);   // >= 1: |T| <= M
+    if (span <= (1u << 20)) {
+      // small chunks: select the k-th new head speculatively and read both
+      // numbers with one synchronization (the select is cheap here)
+      select_kth_bit(bitmap.as<u32>(), span, k, word_tmp.as<u32>(), scan_tmp.as<u32>(), dscal32(1), st);
+      to_host(dscal32(0), 2 * sizeof(u32));
+      ph_end(ISA_PH_FLUSH, m, 0);
+      sync();
+      const u32 n_new = h_scal[0], f = h_scal[1];
+      last_new = n_new;
+      return (int64_t)T.n + n_new <= M ? span : f;
+    }
     to_host(dscal32(0), sizeof(u32));
     ph_end(ISA_PH_FLUSH, m, 0);
     sync();
     u32 n_new = h_scal[0];
-    const int64_t M = cfg.memory_budget;
     last_new = n_new;
     if ((int64_t)T.n + n_new <= M) return span;
-    u32 k = (u32)(M - (int64_t)T.n + 1);
     ph_begin(ISA_PH_FLUSH);
     select_kth_bit(bitmap.as<u32>(), span, k, word_tmp.as<u32>(), scan_tmp.as<u32>(), dscal32(1), st);
     to_host(dscal32(1), sizeof(u32));
