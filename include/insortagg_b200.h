@@ -74,7 +74,9 @@ enum isa_slot_type { ISA_SLOT_I64 = 0, ISA_SLOT_F64 = 1 };
 enum isa_slot_src { ISA_SRC_ONE = 0, ISA_SRC_COLUMN = 1 };
 
 /* where spilled runs live */
-enum isa_run_tier { ISA_TIER_HOST = 0, ISA_TIER_HBM = 1 };
+/* where runs live: pinned host DRAM, HBM, or files in the reference's page
+ * format (FileStore tier, runstore.py:195-236; needs isa_set_spill_dir) */
+enum isa_run_tier { ISA_TIER_HOST = 0, ISA_TIER_HBM = 1, ISA_TIER_FILE = 2 };
 
 typedef struct isa_config {
   int64_t memory_budget;     /* M: group-table budget in rows  (SortAggConfig.memory_budget) */
@@ -188,6 +190,13 @@ ISA_API void isa_destroy(isa_handle* h);
 ISA_API int isa_execute(isa_handle* h, int64_t n_rows, const void* const* key_cols,
                 const void* const* val_cols, int32_t input_on_host,
                 void* stream, int64_t* n_groups_out);
+
+/* FileStore tier (runstore.py:195-236): runs are written to
+ * `dir`/run_NNNNNN.bin, byte-identical to the reference's RunWriter pages
+ * (runstore.py:120-129, 239-301: int64 key columns and int64 states only),
+ * numbered from first_run_id on, and read back from there by the wide merge
+ * (page crc32 verified: ISA_ERR_CORRUPTION on mismatch). */
+ISA_API int isa_set_spill_dir(isa_handle* h, const char* dir, int64_t first_run_id);
 
 /* Copy the last result out: key_out[i] receives column i in its input dtype,
  * slot_out[s] receives slot s as int64 or float64 (per slot_type).  Buffers

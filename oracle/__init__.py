@@ -244,3 +244,35 @@ def range_splitters(key_cols, parts, sample=65536, seed=0):
     picks = [int(len(order) * (t + 1) / parts) for t in range(parts - 1)]
     picks = [min(p, len(order) - 1) for p in picks]
     return shi[picks], slo[picks]
+
+
+def parse_run_pages(data, arity, slots):
+    """Restatement of parse_page over a whole run file (runstore.py:120-142):
+    12-byte header (row_count, byte_length, crc32 of the body), high key,
+    rows of int64 (key columns, then state slots).  Returns (keys
+    [arity x rows], states [slots x rows], page row counts); raises
+    ValueError on a length or checksum mismatch."""
+    import struct
+    import zlib
+    keys, states, counts = [[] for _ in range(arity)], [[] for _ in range(slots)], []
+    off, width = 0, arity + slots
+    while off < len(data):
+        rows, length, crc = struct.unpack_from("<III", data, off)
+        body = data[off + 12: off + 12 + length]
+        if len(body) != length or (zlib.crc32(body) & 0xFFFFFFFF) != crc:
+            raise ValueError(f"page at {off}: bad length or checksum")
+        vals = np.frombuffer(body, dtype="<i8")
+        if len(vals) != arity + rows * width:
+            raise ValueError(f"page at {off}: row count does not match the body")
+        hk = vals[:arity]
+        rv = vals[arity:].reshape(rows, width)
+        if rows and not np.array_equal(hk, rv[-1, :arity]):
+            raise ValueError(f"page at {off}: high key is not the last row's key")
+        for j in range(arity):
+            keys[j].append(rv[:, j])
+        for s_ in range(slots):
+            states[s_].append(rv[:, arity + s_])
+        counts.append(rows)
+        off += 12 + length
+    cat = lambda parts: np.concatenate(parts) if parts else np.zeros(0, dtype=np.int64)
+    return [cat(k) for k in keys], [cat(s_) for s_ in states], counts

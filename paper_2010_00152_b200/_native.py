@@ -32,7 +32,7 @@ DTYPE_BITS = {U8: 8, I8: 8, U16: 16, I16: 16, U32: 32, I32: 32, U64: 64, I64: 64
 OP_ADD, OP_MIN, OP_MAX = 0, 1, 2
 SLOT_I64, SLOT_F64 = 0, 1
 SRC_ONE, SRC_COLUMN = 0, 1
-TIER_HOST, TIER_HBM = 0, 1
+TIER_HOST, TIER_HBM, TIER_FILE = 0, 1, 2
 
 _STATUS_ERRORS = {
     1: InvalidInputError,
@@ -48,6 +48,7 @@ EXPORTED_SYMBOLS = (
     "isa_version", "isa_create", "isa_destroy", "isa_execute", "isa_result_copy",
     "isa_metrics", "isa_cycles", "isa_run_rows", "isa_last_error",
     "isa_sample_keys", "isa_partition", "isa_phase_stats", "isa_launch_count", "isa_steps",
+    "isa_set_spill_dir",
 )
 
 PHASES = ("absorb", "sort", "flush", "collapse", "table_merge", "wm_sort", "wm_collapse",
@@ -149,6 +150,8 @@ def load():
     lib.isa_execute.argtypes = [vp, ctypes.c_int64, pp, pp, ctypes.c_int32, vp, i64p]
     lib.isa_result_copy.restype = ctypes.c_int
     lib.isa_result_copy.argtypes = [vp, pp, pp, ctypes.c_int32, vp]
+    lib.isa_set_spill_dir.restype = ctypes.c_int
+    lib.isa_set_spill_dir.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64]
     lib.isa_metrics.restype = ctypes.c_int
     lib.isa_metrics.argtypes = [vp, ctypes.POINTER(IsaLedger)]
     lib.isa_cycles.restype = ctypes.c_int64
@@ -225,6 +228,9 @@ class Handle:
         self._check(self._lib.isa_execute(self._h, n_rows, _ptr_array(key_ptrs), _ptr_array(val_ptrs),
                                           1 if on_host else 0, stream, ctypes.byref(out)))
         return out.value
+
+    def set_spill_dir(self, directory, first_run_id):
+        self._check(self._lib.isa_set_spill_dir(self._h, os.fsencode(directory), int(first_run_id)))
 
     def result_copy(self, key_ptrs, slot_ptrs, on_host, stream):
         self._check(self._lib.isa_result_copy(self._h, _ptr_array(key_ptrs), _ptr_array(slot_ptrs),

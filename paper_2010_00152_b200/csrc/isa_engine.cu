@@ -30,6 +30,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <fcntl.h>
+#include <unistd.h>
 #include <deque>
 #include <functional>
 #include <cstdlib>
@@ -150,6 +152,10 @@ struct Run {
   const u32* off_host = nullptr;   // block byte offsets (nblk + 1)
   const u32* off_dev = nullptr;
   u32 nblk = 0;
+  // FileStore-tier run: reference page format in `path`
+  std::string path;
+  u32 npages = 0;
+  std::vector<u64> hk_lo, hk_hi;   // normalized high key of every page
 };
 
 struct Window {      // staged host input
@@ -228,6 +234,19 @@ struct Engine {
   size_t desc_cap[2] = {0, 0};
   cudaEvent_t desc_done[2] = {nullptr, nullptr};
   u32 fmask = 0;                            // f64 state slots (codec transform)
+  // FileStore tier
+  PageSpec ps0;
+  std::string spill_dir;
+  int64_t next_run_id = 0;
+  char* file_pin = nullptr;                 // pinned staging of a run's pages (spill)
+  size_t file_pin_cap = 0;
+  char* fstage[2] = {nullptr, nullptr};     // pinned staging of a window's pages (merge)
+  size_t fstage_cap[2] = {0, 0};
+  cudaEvent_t fstage_done[2] = {nullptr, nullptr};
+  std::vector<PageRef> pref_host[2];
+  PageRef* pref_pinned[2] = {nullptr, nullptr};
+  size_t pref_cap[2] = {0, 0};
+  DevBuf stg_pref[2];
   Table result;
   DevBuf out_tmp;
   // host input windows
@@ -286,6 +305,8 @@ struct Engine {
       CK(cudaEventCreateWithFlags(&stg_free[i], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&desc_done[i], cudaEventDisableTiming));
       CK(cudaEventRecord(desc_done[i], 0));
+      CK(cudaEventCreateWithFlags(&fstage_done[i], cudaEventDisableTiming));
+      CK(cudaEventRecord(fstage_done[i], 0));
       CK(cudaEventCreateWithFlags(&win[i].ready, cudaEventDisableTiming));
     }
     CK(cudaHostAlloc((void**)&h_scal, 64 * sizeof(u64), cudaHostAllocMapped));
@@ -305,7 +326,12 @@ struct Engine {
     for (int i = 0; i < 2; ++i) {
       if (desc_pinned[i]) cudaFreeHost(desc_pinned[i]);
       if (desc_done[i]) cudaEventDestroy(desc_done[i]);
+      if (fstage[i]) cudaFreeHost(fstage[i]);
+      if (pref_pinned[i]) cudaFreeHost(pref_pinned[i]);
+      if (fstage_done[i]) cudaEventDestroy(fstage_done[i]);
+      stg_pref[i].release();
     }
+    if (file_pin) cudaFreeHost(file_pin);
     for (auto* b : bufs) b->release();
     for (auto& w : win) { for (auto& b : w.keys) b.release(); for (auto& b : w.vals) b.release(); }
     for (auto& r : recs) { ev_pool.push_back(r.a); ev_pool.push_back(r.b); }
@@ -340,8 +366,10 @@ struct Engine {
     if (cfg.preaggregate < 0 || cfg.preaggregate > 2) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown preaggregate mode");
     if (cfg.merge_mode < ISA_MERGE_WIDE || cfg.merge_mode > ISA_MERGE_SEPARATE) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown merge mode");
     if (cfg.run_codec < 0 || cfg.run_codec > 2) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown run codec");
-    if (cfg.run_tier != ISA_TIER_HOST && cfg.run_tier != ISA_TIER_HBM)
+    if (cfg.run_tier != ISA_TIER_HOST && cfg.run_tier != ISA_TIER_HBM && cfg.run_tier != ISA_TIER_FILE)
       throw IsaError(ISA_ERR_INVALID_INPUT, "unknown run tier");
+    if (cfg.run_tier == ISA_TIER_FILE && cfg.merge_mode != ISA_MERGE_WIDE)
+      throw IsaError(ISA_ERR_INVALID_INPUT, "the FileStore tier supports merge_mode wide");
     if (sch.n_key_cols < 1) throw IsaError(ISA_ERR_INVALID_INPUT, "schema needs at least one key column");
     if (sch.n_key_cols > ISA_MAX_KEY_COLS) throw IsaError(ISA_ERR_INVALID_INPUT, "too many key columns");
     if (sch.n_slots < 0 || sch.n_slots > ISA_MAX_SLOTS) throw IsaError(ISA_ERR_INVALID_INPUT, "too many state slots");
@@ -370,6 +398,17 @@ struct Engine {
       if (sch.val_dtypes[j] < ISA_U8 || sch.val_dtypes[j] > ISA_F64)
         throw IsaError(ISA_ERR_INVALID_INPUT, "unknown value column dtype");
     S = sch.n_slots;
+    memset(&ps0, 0, sizeof(ps0));
+    ps0.kw = KW;
+    ps0.arity = sch.n_key_cols;
+    ps0.S = S;
+    ps0.P = (int)std::min<int64_t>(cfg.page_capacity, 1 << 30);
+    ps0.body_full = (u32)(8 * ps0.arity + (int64_t)ps0.P * 8 * (ps0.arity + S));
+    for (int c = 0; c < sch.n_key_cols; ++c) {
+      ps0.shift[c] = kd0.shift[c];
+      ps0.width[c] = kd0.width[c];
+      ps0.sgn[c] = dtype_signed(kd0.dtype[c]) ? 1 : 0;
+    }
     memset(&sd0, 0, sizeof(sd0));
     sd0.nslots = S;
     for (int s = 0; s < S; ++s) {
@@ -380,6 +419,9 @@ struct Engine {
       sd0.op[s] = ops[s] = op;
       sd0.type[s] = types[s] = ty;
       if (ty == ISA_SLOT_F64) fmask |= 1u << s;
+      if (ty == ISA_SLOT_F64 && cfg.run_tier == ISA_TIER_FILE)
+        throw IsaError(ISA_ERR_INVALID_INPUT,
+                       "FileStore pages hold int64 state slots only (runstore.py:96, 101); use a host or hbm run tier");
       sd0.src[s] = src;
       if (src == ISA_SRC_COLUMN) {
         int col = sch.slot_col[s];
@@ -703,9 +745,131 @@ struct Engine {
     return r;
   }
 
+  static void grow_pinned(char*& p, size_t& cap, size_t need) {
+    if (need <= cap) return;
+    if (p) CK(cudaFreeHost(p));
+    cap = std::max(need, cap + cap / 2);
+    CK(cudaHostAlloc((void**)&p, cap, cudaHostAllocDefault));
+  }
+
+  // FileStore tier: T encoded as reference pages on the GPU, copied out and
+  // written to run_NNNNNN.bin (RunWriter + FileStore.append_page,
+  // runstore.py:205-220, 239-301).  Synchronous: the file is complete when
+  // this returns.
+  Run spill_file(Table& t) {
+    if (spill_dir.empty()) throw IsaError(ISA_ERR_INVALID_INPUT, "FileStore tier without a spill directory");
+    const u32 n = t.n;
+    const u32 bytes = page_run_bytes(ps0, n);
+    const u32 npages = (n + ps0.P - 1) / ps0.P;
+    t.pk.ensure((size_t)bytes + 16);
+    CK(cudaMemsetAsync(dscal32(6), 0, sizeof(u32), st));
+    page_encode(ps0, t.plo(), t.phi(), t.pst(), n, t.pk.as<char>(), dscal32(6), st);
+    grow_pinned(file_pin, file_pin_cap, bytes);
+    CK(cudaMemcpyAsync(file_pin, t.pk.p, bytes, cudaMemcpyDeviceToHost, st));
+    Run r;
+    r.rows = n;
+    r.host = true;
+    r.npages = npages;
+    r.hk_lo.resize(npages);
+    if (KW == 2) r.hk_hi.resize(npages);
+    // page high keys: rows P-1, 2P-1, ... and the last row
+    if (npages > 1) {
+      CK(cudaMemcpy2DAsync(r.hk_lo.data(), 8, t.plo() + (ps0.P - 1), (size_t)ps0.P * 8, 8, npages - 1,
+                           cudaMemcpyDeviceToHost, st));
+      if (KW == 2)
+        CK(cudaMemcpy2DAsync(r.hk_hi.data(), 8, t.phi() + (ps0.P - 1), (size_t)ps0.P * 8, 8, npages - 1,
+                             cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaMemcpyAsync(r.hk_lo.data() + npages - 1, t.plo() + n - 1, 8, cudaMemcpyDeviceToHost, st));
+    if (KW == 2) CK(cudaMemcpyAsync(r.hk_hi.data() + npages - 1, t.phi() + n - 1, 8, cudaMemcpyDeviceToHost, st));
+    to_host(dscal32(6), sizeof(u32));
+    sync();
+    if (h_scal[0])
+      throw IsaError(ISA_ERR_INVALID_INPUT, "a uint64 key value >= 2^63 cannot be written as an int64 page column");
+    char name[32];
+    snprintf(name, sizeof(name), "run_%06lld.bin", (long long)next_run_id++);
+    r.path = spill_dir + "/" + name;
+    int fd = ::open(r.path.c_str(), O_CREAT | O_WRONLY | O_TRUNC, 0644);
+    if (fd < 0) throw IsaError(ISA_ERR_RESOURCE, "cannot create " + r.path);
+    size_t done = 0;
+    while (done < bytes) {
+      ssize_t w = ::write(fd, file_pin + done, bytes - done);
+      if (w <= 0) { ::close(fd); throw IsaError(ISA_ERR_RESOURCE, "short write to " + r.path); }
+      done += (size_t)w;
+    }
+    ::close(fd);
+    led.bytes_d2h += bytes;
+    t.n = 0;
+    return r;
+  }
+
+  // int64 page column value -> normalized key bits of column c (host)
+  u64 page_field(int c, i64 v) const {
+    const int w = ps0.width[c];
+    u64 f = (u64)v;
+    if (ps0.sgn[c]) f ^= 1ull << (w - 1);
+    if (w < 64) f &= (1ull << w) - 1;
+    return f;
+  }
+  static void pread_all(const std::string& path, char* dst, size_t bytes, size_t off) {
+    int fd = ::open(path.c_str(), O_RDONLY);
+    if (fd < 0) throw IsaError(ISA_ERR_RESOURCE, "cannot open " + path);
+    size_t done = 0;
+    while (done < bytes) {
+      ssize_t r = ::pread(fd, dst + done, bytes - done, (off_t)(off + done));
+      if (r <= 0) { ::close(fd); throw IsaError(ISA_ERR_CORRUPTION, "truncated run file " + path); }
+      done += (size_t)r;
+    }
+    ::close(fd);
+  }
+  size_t page_off(u32 p) const { return (size_t)p * (12 + ps0.body_full); }
+  u32 page_rows(const Run& r, u32 p) const { return std::min<u32>((u32)ps0.P, r.rows - p * (u32)ps0.P); }
+  size_t page_len(const Run& r, u32 p) const {
+    return 12 + 8 * (size_t)ps0.arity + (size_t)page_rows(r, p) * 8 * (ps0.arity + S);
+  }
+  // first row of file run r whose key >= (bhi, blo): page high keys, then
+  // the keys of one page read back (host; the slice search of the merge)
+  u32 file_lower_bound(const Run& r, u64 bhi, u64 blo) {
+    u32 l = 0, h = r.npages;
+    auto less_b = [&](u64 khi, u64 klo) { return KW == 2 ? (khi < bhi || (khi == bhi && klo < blo)) : klo < blo; };
+    while (l < h) {
+      u32 m = (l + h) / 2;
+      if (less_b(KW == 2 ? r.hk_hi[m] : 0, r.hk_lo[m])) l = m + 1; else h = m;
+    }
+    if (l == r.npages) return r.rows;
+    std::vector<char> pg(page_len(r, l));
+    pread_all(r.path, pg.data(), pg.size(), page_off(l));
+    const u32 rows = page_rows(r, l);
+    const char* body = pg.data() + 12;
+    for (u32 i = 0; i < rows; ++i) {
+      const char* row = body + 8 * ps0.arity + (size_t)i * 8 * (ps0.arity + S);
+      u64 klo = 0, khi = 0;
+      for (int c = 0; c < ps0.arity; ++c) {
+        i64 v;
+        memcpy(&v, row + 8 * c, 8);
+        const u64 f = page_field(c, v);
+        const int s = ps0.shift[c], w = ps0.width[c];
+        if (s < 64) {
+          klo |= f << s;
+          if (s > 0 && s + w > 64) khi |= f >> (64 - s);
+        } else {
+          khi |= f << (s - 64);
+        }
+      }
+      if (!less_b(khi, klo)) return l * (u32)ps0.P + i;
+    }
+    return l * (u32)ps0.P + rows;
+  }
+
   // T becomes a run (RunWriter of a read-sort-write flush, sortagg.py:344-350)
   void spill_T() {
     if (T.n == 0) return;
+    if (cfg.run_tier == ISA_TIER_FILE) {
+      Run r = spill_file(T);
+      runs.push_back(r);
+      account_written(r);
+      return;
+    }
     if (pack_runs(T.n)) {
       Run r = spill_packed(T);
       CK(cudaEventRecord(spill_done, d2h));
@@ -987,7 +1151,14 @@ struct Engine {
       for (auto& r : runs) {   // every strided sample copy first, one synchronization after
         int64_t ns = (r.rows + F - 1) / F;
         if (ns == 0) continue;
-        if (r.pk_host) {
+        if (!r.path.empty()) {
+          // high key of the page holding the sampled row (>= its key)
+          for (int64_t i = 0; i < ns; ++i) {
+            const u32 pg = (u32)((i * F) / ps0.P);
+            tmp_lo[o + i] = r.hk_lo[pg];
+            if (KW == 2) tmp_hi[o + i] = r.hk_hi[pg];
+          }
+        } else if (r.pk_host) {
           // block minima of the key words: (hi of the block's first row,
           // lowest lo of the block) <= the first key -- split points only
           // need to be keys in range, slice bounds are searched exactly
@@ -1029,7 +1200,9 @@ struct Engine {
     std::vector<u32> lb((size_t)k * std::max(nb, 1));
     if (nb > 0) {
       std::vector<RunRef> refs(k);
-      for (int i = 0; i < k; ++i) refs[i] = {runs[i].lo, runs[i].hi, runs[i].rows, S, runs[i].pk_dev, runs[i].off_dev};
+      for (int i = 0; i < k; ++i)
+        refs[i] = runs[i].path.empty() ? RunRef{runs[i].lo, runs[i].hi, runs[i].rows, S, runs[i].pk_dev, runs[i].off_dev}
+                                       : RunRef{nullptr, nullptr, 0u, S, nullptr, nullptr};
       runref_dev.ensure(sizeof(RunRef) * k);
       bounds_lo.ensure(8 * nb);
       bounds_hi.ensure(8 * nb);
@@ -1043,6 +1216,9 @@ struct Engine {
                        bounds_out.as<u32>(), st);
       CK(cudaMemcpyAsync(lb.data(), bounds_out.p, 4 * (size_t)k * nb, cudaMemcpyDeviceToHost, st));
       sync();
+      for (int i = 0; i < k; ++i)   // FileStore runs: searched on the host (page high keys + one page)
+        if (!runs[i].path.empty())
+          for (int b = 0; b < nb; ++b) lb[(size_t)i * nb + b] = file_lower_bound(runs[i], bhi[b], blo[b]);
     }
     auto slice = [&](int r, int w, u32& s0, u32& s1) {
       s0 = (w == 0) ? 0 : lb[(size_t)r * nb + (w - 1)];
@@ -1054,6 +1230,7 @@ struct Engine {
       for (int r = 0; r < k; ++r) { u32 s0, s1; slice(r, w, s0, s1); rows += s1 - s0; }
       wmax = std::max(wmax, rows);
     }
+    CK(cudaMemsetAsync(dscal32(12), 0, sizeof(u32), st));   // page checksum failures (FileStore runs)
     for (int i = 0; i < 2; ++i) {
       stg_lo[i].ensure(wmax * 8 + 8);
       if (KW == 2) stg_hi[i].ensure(wmax * 8 + 8);
@@ -1061,21 +1238,32 @@ struct Engine {
       CK(cudaEventRecord(stg_free[i], st));
     }
     bool any_packed = false;
-    for (auto& r : runs) any_packed |= r.pk_host != nullptr;
+    for (auto& r : runs) any_packed |= r.pk_host != nullptr || !r.path.empty();
     if (any_packed) {
-      // packed bytes per window: at most the covering blocks of every slice
+      // packed bytes per window: at most the covering blocks (or pages) of every slice
       size_t pmax = 0;
       for (int w = 0; w < nwin; ++w) {
         size_t b = 0;
         for (int r = 0; r < k; ++r) {
-          if (!runs[r].pk_host) continue;
           u32 s0, s1;
           slice(r, w, s0, s1);
-          if (s1 > s0) b += runs[r].off_host[(s1 - 1) / PK_ROWS + 1] - runs[r].off_host[s0 / PK_ROWS];
+          if (s1 <= s0) continue;
+          if (runs[r].pk_host) {
+            b += runs[r].off_host[(s1 - 1) / PK_ROWS + 1] - runs[r].off_host[s0 / PK_ROWS];
+          } else if (!runs[r].path.empty()) {
+            const u32 p0 = s0 / ps0.P, p1 = (s1 - 1) / ps0.P;
+            b += page_off(p1) + page_len(runs[r], p1) - page_off(p0) + 16;
+          }
         }
         pmax = std::max(pmax, b);
       }
-      for (int i = 0; i < 2; ++i) stg_pk[i].ensure(pmax + 16);
+      for (int i = 0; i < 2; ++i) {
+        stg_pk[i].ensure(pmax + 16);
+        if (cfg.run_tier == ISA_TIER_FILE && fstage_cap[i] < pmax + 16) {
+          CK(cudaEventSynchronize(fstage_done[i]));   // no copy out of it is pending
+          grow_pinned(fstage[i], fstage_cap[i], pmax + 16);
+        }
+      }
     }
     auto stage = [&](int w, int slot) -> int64_t {
       CK(cudaStreamWaitEvent(h2d, stg_free[slot], 0));
@@ -1083,11 +1271,37 @@ struct Engine {
       size_t poff = 0;
       auto& desc = desc_host[slot];
       desc.clear();
+      auto& prefs = pref_host[slot];
+      prefs.clear();
+      size_t fbytes = 0;
       for (int r = 0; r < k; ++r) {
         u32 s0, s1;
         slice(r, w, s0, s1);
         size_t cnt = s1 - s0;
         if (!cnt) continue;
+        if (!runs[r].path.empty()) {
+          // FileStore run: read the covering pages back from its file
+          // (read_page / parse_page, runstore.py:132-142, 315-333)
+          const u32 p0 = s0 / ps0.P, p1 = (s1 - 1) / ps0.P;
+          const size_t o0 = page_off(p0), len = page_off(p1) + page_len(runs[r], p1) - o0;
+          if (fbytes == 0) CK(cudaEventSynchronize(fstage_done[slot]));   // its previous H2D is done
+          if (fbytes + len > fstage_cap[slot]) throw IsaError(ISA_ERR_CONTRACT, "page staging overflow");
+          pread_all(runs[r].path, fstage[slot] + fbytes, len, o0);
+          for (u32 pg = p0; pg <= p1; ++pg) {
+            const u32 r0 = pg * (u32)ps0.P;
+            PageRef pr;
+            pr.src_off = fbytes + (page_off(pg) - o0);
+            pr.rows = page_rows(runs[r], pg);
+            pr.e0 = std::max(s0, r0) - r0;
+            pr.e1 = std::min<u32>(s1, r0 + pr.rows) - r0;
+            pr.dst = (u32)(off + (r0 + pr.e0 - s0));
+            prefs.push_back(pr);
+          }
+          fbytes += (len + 15) & ~(size_t)15;
+          led.bytes_h2d += len;
+          off += cnt;
+          continue;
+        }
         if (runs[r].pk_host) {
           // covering blocks' bytes, then one unpack descriptor per block
           const u32 b0 = s0 / PK_ROWS, b1 = (s1 - 1) / PK_ROWS;
@@ -1114,6 +1328,21 @@ struct Engine {
         if (S) CK(cudaMemcpyAsync(stg_st[slot].as<u64>() + off * S, runs[r].st + (size_t)s0 * S, cnt * 8 * S, cudaMemcpyDefault, h2d));
         if (kind == cudaMemcpyHostToDevice) led.bytes_h2d += cnt * 8 * (KW + S);
         off += cnt;
+      }
+      if (!prefs.empty()) {
+        CK(cudaMemcpyAsync(stg_pk[slot].p, fstage[slot], fbytes, cudaMemcpyHostToDevice, h2d));
+        if (pref_cap[slot] < prefs.size()) {
+          if (pref_pinned[slot]) CK(cudaFreeHost(pref_pinned[slot]));
+          pref_cap[slot] = prefs.size() + prefs.size() / 2 + 64;
+          CK(cudaHostAlloc((void**)&pref_pinned[slot], pref_cap[slot] * sizeof(PageRef), cudaHostAllocDefault));
+        }
+        memcpy(pref_pinned[slot], prefs.data(), prefs.size() * sizeof(PageRef));
+        stg_pref[slot].ensure(prefs.size() * sizeof(PageRef) + 16);
+        CK(cudaMemcpyAsync(stg_pref[slot].p, pref_pinned[slot], prefs.size() * sizeof(PageRef),
+                           cudaMemcpyHostToDevice, h2d));
+        CK(cudaEventRecord(fstage_done[slot], h2d));
+        page_decode(ps0, stg_pref[slot].as<PageRef>(), (u32)prefs.size(), stg_pk[slot].as<char>(),
+                    stg_lo[slot].as<u64>(), stg_hi[slot].as<u64>(), stg_st[slot].as<u64>(), dscal32(12), h2d);
       }
       if (!desc.empty()) {
         // descriptors through a pinned buffer (its previous copy must be done)
@@ -1180,6 +1409,8 @@ struct Engine {
     result.n = 0;
     result.reserve(std::max<int64_t>(1, std::min<int64_t>(total, W)), KW, S);
     merge_runs(runs, true, [&](Table& w, u32) { append_result(w); });
+    if (cfg.run_tier == ISA_TIER_FILE && read_u32(dscal32(12)))
+      throw IsaError(ISA_ERR_CORRUPTION, "page checksum mismatch");   // parse_page, runstore.py:132-142
     led.pages_read = led.pages_written;
     led.merge_steps += 1;
     led.merge_levels += 1;
@@ -1599,6 +1830,13 @@ int isa_execute(isa_handle* h, int64_t n_rows, const void* const* key_cols, cons
   } catch (const std::exception& e) {
     return fail(h, e);
   }
+}
+
+int isa_set_spill_dir(isa_handle* h, const char* dir, int64_t first_run_id) {
+  if (!h || !dir) return ISA_ERR_CONTRACT;
+  h->eng->spill_dir = dir;
+  h->eng->next_run_id = first_run_id;
+  return ISA_OK;
 }
 
 int isa_result_copy(isa_handle* h, void* const* key_out, void* const* slot_out, int32_t out_on_host, void* stream) {

@@ -129,6 +129,19 @@ void pack_sizes(const PackSrc& p, u64* hdr, u32* blk_bytes, cudaStream_t st);
 void pack_write(const PackSrc& p, const u64* hdr, const u32* blk_off, char* out, cudaStream_t st);
 void unpack_blocks(const UnpackBlk* d, u32 nd, const char* src, int kw, int S, u32 fmask, u64* lo, u64* hi, u64* st,
                    cudaStream_t stream);
+
+// ---- reference page format (isa_pages.cu, runstore.py:1-20, 120-142) ----
+struct PageSpec {
+  int kw, arity, S, P;
+  u32 body_full;   // 8 * arity + P * 8 * (arity + S)
+  int shift[ISA_MAX_KEY_COLS], width[ISA_MAX_KEY_COLS], sgn[ISA_MAX_KEY_COLS];
+};
+struct PageRef { u64 src_off; u32 rows, e0, e1, dst; };
+u32 page_run_bytes(const PageSpec& ps, u32 n);
+void page_encode(const PageSpec& ps, const u64* lo, const u64* hi, const u64* st, u32 n, char* out, u32* bad,
+                 cudaStream_t stream);
+void page_decode(const PageSpec& ps, const PageRef* refs, u32 nrefs, const char* src, u64* lo, u64* hi, u64* st,
+                 u32* bad, cudaStream_t stream);
 void run_lower_bounds(int KW, const RunRef* runs_dev, int nruns, const u64* b_lo, const u64* b_hi,
                       int nb, u32* out, cudaStream_t st);
 

@@ -21,6 +21,8 @@ cycles the device reports.
 
 from __future__ import annotations
 
+import os
+
 import math
 from dataclasses import dataclass
 
@@ -241,12 +243,70 @@ class MemoryStore:
 
 
 class FileStore:
-    """File-backed run store of the reference (runstore.py:195-236).  The
-    byte-level page format is not part of the GPU path; passing one to
-    SortAggregate raises InvalidInputError."""
+    """Temporary storage backed by one file per run in a directory
+    (runstore.py:195-236), same file names and page index.  With a FileStore
+    the B200 operator writes its runs there in the reference's page format
+    (byte-identical to RunWriter's pages: the reference's ``read_page`` reads
+    them) and its wide merge reads them back from the files."""
 
     def __init__(self, directory):
         self.directory = directory
+        os.makedirs(directory, exist_ok=True)
+        self._offsets = {}
+        self._handles = {}
+        self._next = 0
+
+    def _path(self, run_id):
+        return os.path.join(self.directory, f"run_{run_id:06d}.bin")
+
+    def new_run(self):
+        rid = self._next
+        self._next += 1
+        self._offsets[rid] = []
+        self._handles[rid] = open(self._path(rid), "wb")
+        return rid
+
+    def append_page(self, run_id, page, rows=None):
+        fh = self._handles[run_id]
+        self._offsets[run_id].append((fh.tell(), len(page)))
+        fh.write(page)
+
+    def finalize_run(self, run_id):
+        fh = self._handles.pop(run_id, None)
+        if fh is not None:
+            fh.close()
+
+    def page_bytes(self, run_id, index):
+        off, length = self._offsets[run_id][index]
+        with open(self._path(run_id), "rb") as fh:
+            fh.seek(off)
+            return fh.read(length)
+
+    def retained(self, run_id, index):
+        return None
+
+    def close(self):
+        for rid in list(self._handles):
+            self.finalize_run(rid)
+
+    def _adopt(self, run_rows, arity, slots, page_capacity):
+        """Register runs the native writer produced (ids _next, _next+1, ...)
+        with their page index (page sizes follow from the row counts)."""
+        ids = []
+        for rows in run_rows:
+            rid = self._next
+            self._next += 1
+            off, pages = 0, []
+            left = rows
+            while left > 0:
+                r = min(page_capacity, left)
+                length = 12 + 8 * arity + r * 8 * (arity + slots)
+                pages.append((off, length))
+                off += length
+                left -= r
+            self._offsets[rid] = pages
+            ids.append(rid)
+        return ids
 
 
 # ---------------------------------------------------------------------------
@@ -334,9 +394,8 @@ class SortAggregate:
 
     def __init__(self, schema, config, store=None, ledger=None, *, device=None):
         if isinstance(store, FileStore):
-            raise InvalidInputError(
-                "FileStore is not supported by the B200 operator; runs are placed "
-                "in pinned host memory or HBM (SortAggConfig.run_tier)")
+            if config.merge_mode != WIDE:
+                raise InvalidInputError("the FileStore run tier supports merge_mode 'wide'")
         if config.run_generation_mode != READ_SORT_WRITE:
             raise InvalidInputError(
                 f"run_generation_mode {config.run_generation_mode!r} is not supported by the "
@@ -370,7 +429,10 @@ class SortAggregate:
         cfg = _native.IsaConfig()
         cfg.memory_budget = self.config.memory_budget
         cfg.page_capacity = self.config.page_capacity
-        cfg.run_tier = _native.TIER_HOST if self.config.run_tier == "host" else _native.TIER_HBM
+        if isinstance(self.store, FileStore):
+            cfg.run_tier = _native.TIER_FILE
+        else:
+            cfg.run_tier = _native.TIER_HOST if self.config.run_tier == "host" else _native.TIER_HBM
         cfg.device = dev
         cfg.chunk_rows_max = self.config.chunk_rows_max
         cfg.window_rows = self.config.window_rows
@@ -512,8 +574,13 @@ class SortAggregate:
         if stream is None:
             stream = torch.cuda.current_stream(dev_index)
         sptr = ctypes_stream(stream)
+        file_store = isinstance(self.store, FileStore)
+        if file_store:
+            h.set_spill_dir(self.store.directory, self.store._next)
         # the native side selects the device itself; outputs name it explicitly
         n_groups = h.execute(n, [k.data_ptr() for k in keys], [v.data_ptr() for v in vals], on_host, sptr)
+        if file_store:
+            self.run_ids = self.store._adopt(h.run_rows(), len(keys), len(slots), self.config.page_capacity)
         out_dev = torch.device("cpu") if on_host else keys[0].device
         pin = on_host
         out_keys = [torch.empty(n_groups, dtype=k.dtype, device=out_dev, pin_memory=pin) for k in keys]

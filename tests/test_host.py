@@ -6,6 +6,8 @@ import math
 import random
 
 import numpy as np
+import os
+
 import pytest
 import torch
 
@@ -127,7 +129,8 @@ def test_operator_rejects_out_of_scope_modes():
     with pytest.raises(isa.InvalidInputError, match="run_generation_mode"):
         isa.SortAggregate(sch, cfg(64, 8, run_generation_mode=isa.REPLACEMENT_SELECTION))
     with pytest.raises(isa.InvalidInputError, match="FileStore"):
-        isa.SortAggregate(sch, cfg(64, 8), isa.FileStore("/tmp/x"))
+        isa.SortAggregate(sch, cfg(64, 8, merge_mode="traditional"), isa.FileStore("/tmp/isa_fs_x"))
+    isa.SortAggregate(sch, cfg(64, 8), isa.FileStore("/tmp/isa_fs_x"))   # wide: accepted
     with pytest.raises(isa.InvalidInputError, match="utf8"):
         isa.SortAggregate(isa.Schema([isa.ColumnSpec("s", kind=isa.UTF8)]), cfg(64, 8))
 
@@ -184,3 +187,19 @@ def test_splitmix_matches_numpy():
         z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
         z = z ^ (z >> np.uint64(31))
     assert np.array_equal(got, z)
+
+
+def test_filestore_mirror_page_index(tmp_path):
+    """FileStore mirrors the reference (runstore.py:195-236); runs adopted
+    from the native writer get the page index RunWriter would have made."""
+    fs = isa.FileStore(str(tmp_path))
+    rid = fs.new_run()
+    fs.append_page(rid, b"abc")
+    fs.append_page(rid, b"defg")
+    fs.finalize_run(rid)
+    assert fs.page_bytes(rid, 1) == b"defg" and fs.retained(rid, 0) is None
+    ids = fs._adopt([10, 3], arity=2, slots=1, page_capacity=4)
+    assert ids == [1, 2]
+    assert fs._offsets[1] == [(0, 124), (124, 124), (248, 12 + 16 + 2 * 24)]
+    assert fs._offsets[2] == [(0, 12 + 16 + 3 * 24)]
+    assert os.path.basename(fs._path(2)) == "run_000002.bin"

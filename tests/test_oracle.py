@@ -7,7 +7,10 @@ states bit-exact, float sums within rel 1e-9; the C restatement must also
 reproduce the run-generation ledger (fill cycles, run sizes, spilled rows).
 """
 
+import os
+
 import numpy as np
+import pytest
 
 import oracle
 from conftest import assert_slots_equal
@@ -84,3 +87,37 @@ def test_key_normalization_round_trip():
     keys_norm = list(zip(*(c[order_norm] for c in cols)))
     keys_tuple = list(zip(*(c[order_tuple] for c in cols)))
     assert keys_norm == keys_tuple
+
+
+@pytest.mark.parametrize("name", ["pages_3000_450_64_8", "pages_composite_avg", "pages_distinct"])
+def test_page_parser_on_reference_run_files(name):
+    """The oracle's page parser reads the reference's own FileStore run files:
+    every page checks out, every run is strictly ascending and sized by the
+    page capacity, and the runs' union aggregates to the reference output."""
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", f"{name}.npz"))
+    arity = sum(1 for k in z.files if k.startswith("in_k"))
+    slots = sum(1 for k in z.files if k.startswith("out_s"))
+    P = int(z["page_capacity"])
+    blob = z["run_bytes"].tobytes()
+    off = 0
+    all_k, all_s = [[] for _ in range(arity)], [[] for _ in range(slots)]
+    for length in z["run_lengths"]:
+        keys, states, counts = oracle.parse_run_pages(blob[off: off + int(length)], arity, slots)
+        off += int(length)
+        assert all(c == P for c in counts[:-1]) and 0 < counts[-1] <= P
+        order = np.lexsort(tuple(reversed(keys)))
+        assert np.array_equal(order, np.arange(len(order)))
+        for j in range(arity):
+            all_k[j].append(keys[j])
+        for s_ in range(slots):
+            all_s[s_].append(states[s_])
+    assert off == len(blob)
+    ops = [a.split(":")[1] for a in z["aggs"]]
+    slot_ops = []
+    for op_ in ops:
+        slot_ops += {"count": ["add"], "sum": ["add"], "min": ["min"], "max": ["max"], "avg": ["add", "add"]}[op_]
+    want_k, want_s = oracle.reference_aggregate([np.concatenate(k) for k in all_k],
+                                                [np.concatenate(s_) for s_ in all_s], slot_ops)
+    # run rows are a subset of the groups (the final residue is the last run): every run key is an output key
+    out_keys = set(zip(*[z[f"out_k{j}"].astype(np.int64).tolist() for j in range(arity)]))
+    assert set(zip(*[k.tolist() for k in want_k])) <= out_keys

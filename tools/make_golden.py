@@ -11,7 +11,8 @@ page_capacity=100 unless stated, default read-sort-write + wide merge.
 Keys >= 2^63 cannot be spilled by the reference codec (runstore.py:50, 59):
 uint64 columns are fed as x - 2^63 (order preserving) and mapped back.
 
-Usage: python tools/make_golden.py   (writes tests/golden/)
+Usage: python tools/make_golden.py [pages]   (writes tests/golden/; `pages`
+only regenerates the FileStore page fixtures)
 """
 
 from __future__ import annotations
@@ -140,6 +141,76 @@ def save(name, spec, key_cols, aggs, values, memory, page=100, store_inputs=True
           f"-> {os.path.getsize(path) / 1024:.0f} KiB")
 
 
+def save_pages(name, spec, key_cols, aggs, values, memory, page):
+    """Run the reference with a FileStore and keep every run file's bytes
+    (runstore.py page format) next to the inputs and the output rows."""
+    import tempfile
+    core, sortagg, runstore = _ref()
+    k = len(key_cols)
+    schema = core.Schema([core.ColumnSpec(f"k{i}") for i in range(k)],
+                         [core.AggregateSpec(n, _kind(kd), c) for n, kd, c in aggs])
+    cols = [np.asarray(c).astype(np.int64).tolist() for c in key_cols]
+    vlists = {nm: np.asarray(v).tolist() for nm, v in values.items()}
+    rows = []
+    for i in range(len(key_cols[0])):
+        inputs = tuple(vlists[c][i] if c is not None else None for _, _, c in aggs)
+        rows.append(core.Row(tuple(col[i] for col in cols), schema.make_state(inputs)))
+    cfg = sortagg.SortAggConfig(memory_budget=memory, page_capacity=page, ovc_enabled=False)
+    with tempfile.TemporaryDirectory() as d:
+        store = runstore.FileStore(d)
+        op = sortagg.SortAggregate(schema, cfg, store)
+        out = op.execute(iter(rows))
+        store.close()
+        # run generation's runs come first (ids 0..R-1); traditional levels the
+        # reference plans before its wide step write further runs, which the
+        # B200 path never needs (one wide merge)
+        files = sorted(f for f in os.listdir(d) if f.startswith("run_"))[: op.runs_after_generation]
+        blobs = [open(os.path.join(d, f), "rb").read() for f in files]
+    payload = {
+        "spec": np.asarray(spec, dtype="U256"),
+        "memory_budget": np.int64(memory), "page_capacity": np.int64(page),
+        "aggs": np.asarray([f"{n}:{kd}:{c or ''}" for n, kd, c in aggs], dtype="U64"),
+        "run_files": np.asarray(files, dtype="U32"),
+        "run_bytes": np.frombuffer(b"".join(blobs), dtype=np.uint8),
+        "run_lengths": np.asarray([len(b) for b in blobs], dtype=np.int64),
+        "runs_after_generation": np.int64(op.runs_after_generation),
+        "executed_kinds": np.asarray([s_["kind"] for s_ in op.executed_steps], dtype="U16"),
+    }
+    for j, c in enumerate(key_cols):
+        payload[f"in_k{j}"] = np.asarray(c)
+        payload[f"out_k{j}"] = np.asarray([r.key[j] for r in out], dtype=np.int64).astype(np.asarray(c).dtype)
+    for nm, v in values.items():
+        payload[f"in_v_{nm}"] = np.asarray(v)
+    for s_ in range(schema.state_slots):
+        payload[f"out_s{s_}"] = np.asarray([r.state[s_] for r in out], dtype=np.int64)
+    path = os.path.join(OUT, f"{name}.npz")
+    np.savez_compressed(path, **payload)
+    print(f"{name}: {len(files)} run files, {sum(len(b) for b in blobs)} bytes -> {os.path.getsize(path) / 1024:.0f} KiB")
+
+
+def pages_main():
+    rng = np.random.default_rng(2010001552)
+    n, o = 3000, 450
+    kk = uniform_planted(rng, n, o) * 7 - 1000
+    v = rng.integers(-10**6, 10**6, n)
+    save_pages("pages_3000_450_64_8", "reference FileStore runs: 3000 rows / 450 int64 keys, M=64, P=8",
+               [kk.astype(np.int64)], [("n", "count", None), ("s", "sum", "v"), ("lo", "min", "v"),
+                                       ("hi", "max", "v")], {"v": v}, 64, 8)
+    n, o = 5000, 900
+    ids = uniform_planted(rng, n, o)
+    c0 = (ids % 7 - 3).astype(np.int8)
+    c1 = ((ids // 7) * 37 - 2000).astype(np.int16)
+    c2 = (ids * 2654435761 % (1 << 32)).astype(np.uint32)
+    w = rng.integers(0, 1000, n)
+    save_pages("pages_composite_avg", "reference FileStore runs: (int8, int16, uint32) keys, count + avg, M=100, P=16",
+               [c0, c1, c2], [("n", "count", None), ("a", "avg", "w")], {"w": w}, 100, 16)
+    kd = rng.integers(0, 1 << 40, 4000)
+    kd = np.concatenate([kd, kd[:2000]])
+    rng.shuffle(kd)
+    save_pages("pages_distinct", "reference FileStore runs: DISTINCT over int64, M=500, P=100",
+               [kd.astype(np.int64)], [], {}, 500, 100)
+
+
 def uniform_planted(rng, n, distinct):
     ids = np.concatenate([np.arange(distinct), rng.integers(0, distinct, n - distinct)])
     rng.shuffle(ids)
@@ -246,4 +317,9 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["pages"]:
+        os.makedirs(OUT, exist_ok=True)
+        pages_main()
+    else:
+        main()
+        pages_main()
