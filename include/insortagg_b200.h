@@ -191,6 +191,23 @@ ISA_API int isa_execute(isa_handle* h, int64_t n_rows, const void* const* key_co
                 const void* const* val_cols, int32_t input_on_host,
                 void* stream, int64_t* n_groups_out);
 
+/* Downstream consumers of sorted output (the paper's interesting orderings,
+ * PAPER.md:850-853).
+ * bench.in_stream_aggregate (bench.py:199-212): aggregate rows already
+ * sorted on the key (every run of equal consecutive keys becomes one group;
+ * no sort, no memory budget).  Same inputs as isa_execute; the result is
+ * read with isa_result_copy. */
+ISA_API int isa_in_stream_aggregate(isa_handle* h, int64_t n_rows, const void* const* key_cols,
+                                    const void* const* val_cols, int32_t input_on_host, void* stream,
+                                    int64_t* n_groups_out);
+/* bench.merge_intersect (bench.py:536-550): the keys present in both
+ * strictly ascending key-column inputs (e.g. two SortAggregate outputs),
+ * written to out_keys (device memory, or host memory with on_host = 1);
+ * *n_out = their count (out_keys need room for min(n_a, n_b) keys). */
+ISA_API int isa_merge_intersect(isa_handle* h, int64_t n_a, const void* const* a_keys, int64_t n_b,
+                                const void* const* b_keys, void* const* out_keys, int32_t on_host,
+                                void* stream, int64_t* n_out);
+
 /* FileStore tier (runstore.py:195-236): runs are written to
  * `dir`/run_NNNNNN.bin, byte-identical to the reference's RunWriter pages
  * (runstore.py:120-129, 239-301: int64 key columns and int64 states only),

@@ -48,7 +48,7 @@ EXPORTED_SYMBOLS = (
     "isa_version", "isa_create", "isa_destroy", "isa_execute", "isa_result_copy",
     "isa_metrics", "isa_cycles", "isa_run_rows", "isa_last_error",
     "isa_sample_keys", "isa_partition", "isa_phase_stats", "isa_launch_count", "isa_steps",
-    "isa_set_spill_dir",
+    "isa_set_spill_dir", "isa_in_stream_aggregate", "isa_merge_intersect",
 )
 
 PHASES = ("absorb", "sort", "flush", "collapse", "table_merge", "wm_sort", "wm_collapse",
@@ -150,6 +150,10 @@ def load():
     lib.isa_execute.argtypes = [vp, ctypes.c_int64, pp, pp, ctypes.c_int32, vp, i64p]
     lib.isa_result_copy.restype = ctypes.c_int
     lib.isa_result_copy.argtypes = [vp, pp, pp, ctypes.c_int32, vp]
+    lib.isa_in_stream_aggregate.restype = ctypes.c_int
+    lib.isa_in_stream_aggregate.argtypes = [vp, ctypes.c_int64, pp, pp, ctypes.c_int32, vp, i64p]
+    lib.isa_merge_intersect.restype = ctypes.c_int
+    lib.isa_merge_intersect.argtypes = [vp, ctypes.c_int64, pp, ctypes.c_int64, pp, pp, ctypes.c_int32, vp, i64p]
     lib.isa_set_spill_dir.restype = ctypes.c_int
     lib.isa_set_spill_dir.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64]
     lib.isa_metrics.restype = ctypes.c_int
@@ -227,6 +231,19 @@ class Handle:
         out = ctypes.c_int64(0)
         self._check(self._lib.isa_execute(self._h, n_rows, _ptr_array(key_ptrs), _ptr_array(val_ptrs),
                                           1 if on_host else 0, stream, ctypes.byref(out)))
+        return out.value
+
+    def in_stream(self, n_rows, key_ptrs, val_ptrs, on_host, stream):
+        out = ctypes.c_int64(0)
+        self._check(self._lib.isa_in_stream_aggregate(self._h, n_rows, _ptr_array(key_ptrs), _ptr_array(val_ptrs),
+                                                      1 if on_host else 0, stream, ctypes.byref(out)))
+        return out.value
+
+    def merge_intersect(self, n_a, a_ptrs, n_b, b_ptrs, out_ptrs, on_host, stream):
+        out = ctypes.c_int64(0)
+        self._check(self._lib.isa_merge_intersect(self._h, n_a, _ptr_array(a_ptrs), n_b, _ptr_array(b_ptrs),
+                                                  _ptr_array(out_ptrs), 1 if on_host else 0, stream,
+                                                  ctypes.byref(out)))
         return out.value
 
     def set_spill_dir(self, directory, first_run_id):

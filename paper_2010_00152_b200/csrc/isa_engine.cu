@@ -1745,6 +1745,102 @@ struct Engine {
     sync();
   }
 
+  // ------------------------------------------------ downstream consumers --
+  // Device copies of host columns (pinned or pageable) for the one-shot entry points.
+  void to_device_cols(int64_t n, const void* const* key_cols, const void* const* val_cols, int nval,
+                      std::vector<const void*>& kb, std::vector<const void*>& vb) {
+    Window& w = win[0];
+    CK(cudaStreamSynchronize(h2d));
+    w.staged = false;
+    stage_window(w, key_cols, val_cols, 0, n);
+    CK(cudaStreamWaitEvent(st, w.ready, 0));
+    kb.assign(sch.n_key_cols, nullptr);
+    vb.assign(std::max(nval, 1), nullptr);
+    for (int c = 0; c < sch.n_key_cols; ++c) kb[c] = w.keys[c].p;
+    for (int j = 0; j < nval; ++j) vb[j] = w.vals[j].p;
+    w.staged = false;
+  }
+
+  // bench.in_stream_aggregate (bench.py:199-212): rows already sorted on the
+  // key -> one group per run of equal consecutive keys (no sort, no budget);
+  // the result is read with isa_result_copy.
+  int64_t in_stream(int64_t n, const void* const* key_cols, const void* const* val_cols, bool on_host,
+                    cudaStream_t stream) {
+    CK(cudaSetDevice(dev));
+    st = stream;
+    memset(&led, 0, sizeof(led));
+    memset(phases, 0, sizeof(phases));
+    runs.clear();
+    cycles.clear();
+    steps.clear();
+    result.n = 0;
+    if (n < 0) throw IsaError(ISA_ERR_INVALID_INPUT, "negative row count");
+    if (n > 0x7FFFFFFFll) throw IsaError(ISA_ERR_INVALID_INPUT, "in-stream aggregation of more than 2^31 rows");
+    led.rows_seen = n;
+    if (n == 0) return 0;
+    const u32 m = (u32)n;
+    std::vector<const void*> kb, vb;
+    if (on_host) to_device_cols(n, key_cols, val_cols, sch.n_val_cols, kb, vb);
+    const KeyDesc kd = kd_at(on_host ? kb.data() : key_cols);
+    const SlotDesc sd = sd_at(on_host ? vb.data() : val_cols);
+    ensure_sort(m);
+    CK(cudaMemsetAsync(dvary(), 0, 2 * sizeof(u64), st));
+    build_keys(KW, kd, 0, nullptr, m, s_lo[0].as<u64>(), s_hi[0].as<u64>(), s_val[0].as<u32>(), dvary(), st);
+    collapse_chunk(0, m, 0xFFFFFFFFu, sd, 0, nullptr, result, (size_t)m + 1);
+    led.n_groups = result.n;
+    ph_collect();
+    return result.n;
+  }
+
+  // bench.merge_intersect (bench.py:536-550): keys present in both inputs,
+  // each strictly ascending (SortAggregate outputs); binary-search ranks of
+  // a in b, then a compaction.  Output keys in the input dtypes.
+  int64_t merge_intersect(int64_t na, const void* const* a_keys, int64_t nb, const void* const* b_keys,
+                          void* const* out_keys, bool on_host, cudaStream_t stream) {
+    CK(cudaSetDevice(dev));
+    st = stream;
+    if (na < 0 || nb < 0) throw IsaError(ISA_ERR_INVALID_INPUT, "negative row count");
+    if (na > 0x7FFFFFFFll || nb > 0x7FFFFFFFll) throw IsaError(ISA_ERR_INVALID_INPUT, "inputs of more than 2^31 keys");
+    if (na == 0 || nb == 0) return 0;
+    const u32 ma = (u32)na, mb = (u32)nb;
+    ensure_sort(std::max(ma, mb));
+    ensure_merge(ma, mb);
+    std::vector<const void*> kb, vb;
+    if (on_host) to_device_cols(nb, b_keys, nullptr, 0, kb, vb);
+    build_keys(KW, kd_at(on_host ? kb.data() : b_keys), 0, nullptr, mb, s_lo[1].as<u64>(), s_hi[1].as<u64>(),
+               s_val[1].as<u32>(), dvary(), st);
+    if (on_host) {
+      // the window's buffers are reused for a: b's keys are already normalized
+      CK(cudaStreamSynchronize(st));
+      to_device_cols(na, a_keys, nullptr, 0, kb, vb);
+    }
+    build_keys(KW, kd_at(on_host ? kb.data() : a_keys), 0, nullptr, ma, s_lo[0].as<u64>(), s_hi[0].as<u64>(),
+               s_val[0].as<u32>(), dvary(), st);
+    rank_match(KW, s_lo[0].as<u64>(), s_hi[0].as<u64>(), ma, s_lo[1].as<u64>(), s_hi[1].as<u64>(), mb,
+               mg_rank_a.as<u32>(), mg_match_a.as<u32>(), st);
+    u32* pre = mg_match_a.as<u32>() + ma + 1;
+    CK(cudaMemcpyAsync(pre, mg_match_a.p, (size_t)ma * 4, cudaMemcpyDeviceToDevice, st));
+    scan_exclusive_u32(pre, ma, scan_tmp.as<u32>(), dscal32(8), st);
+    const u32 k = read_u32(dscal32(8));
+    U.reserve(std::max<u32>(k, 1), KW, S);
+    compact_keys(KW, s_lo[0].as<u64>(), s_hi[0].as<u64>(), mg_match_a.as<u32>(), pre, ma, U.plo(), U.phi(), st);
+    for (int c = 0; c < kd0.ncols; ++c) {
+      if (!out_keys[c] || !k) continue;
+      if (on_host) {
+        out_tmp.ensure((size_t)k * 8 + 256);
+        export_key_col(U.plo(), KW == 2 ? U.phi() : nullptr, k, kd0.dtype[c], kd0.shift[c], kd0.width[c],
+                       out_tmp.p, st);
+        CK(cudaMemcpyAsync(out_keys[c], out_tmp.p, (size_t)k * key_elem(c), cudaMemcpyDeviceToHost, st));
+        sync();
+      } else {
+        export_key_col(U.plo(), KW == 2 ? U.phi() : nullptr, k, kd0.dtype[c], kd0.shift[c], kd0.width[c],
+                       out_keys[c], st);
+      }
+    }
+    U.n = 0;
+    return k;
+  }
+
   // --------------------------------------------------------- partition --
   void partition(int64_t n, const void* const* key_cols, const void* const* val_cols, const u64* sp_lo,
                  const u64* sp_hi, int ns, void* const* key_out, void* const* val_out, int64_t* counts,
@@ -1826,6 +1922,31 @@ int isa_execute(isa_handle* h, int64_t n_rows, const void* const* key_cols, cons
   try {
     int64_t g = h->eng->execute(n_rows, key_cols, val_cols, input_on_host != 0, (cudaStream_t)stream);
     if (n_groups_out) *n_groups_out = g;
+    return ISA_OK;
+  } catch (const std::exception& e) {
+    return fail(h, e);
+  }
+}
+
+int isa_in_stream_aggregate(isa_handle* h, int64_t n_rows, const void* const* key_cols, const void* const* val_cols,
+                            int32_t input_on_host, void* stream, int64_t* n_groups_out) {
+  if (!h) return ISA_ERR_CONTRACT;
+  try {
+    int64_t g = h->eng->in_stream(n_rows, key_cols, val_cols, input_on_host != 0, (cudaStream_t)stream);
+    if (n_groups_out) *n_groups_out = g;
+    return ISA_OK;
+  } catch (const std::exception& e) {
+    return fail(h, e);
+  }
+}
+
+int isa_merge_intersect(isa_handle* h, int64_t n_a, const void* const* a_keys, int64_t n_b,
+                        const void* const* b_keys, void* const* out_keys, int32_t on_host, void* stream,
+                        int64_t* n_out) {
+  if (!h) return ISA_ERR_CONTRACT;
+  try {
+    int64_t k = h->eng->merge_intersect(n_a, a_keys, n_b, b_keys, out_keys, on_host != 0, (cudaStream_t)stream);
+    if (n_out) *n_out = k;
     return ISA_OK;
   } catch (const std::exception& e) {
     return fail(h, e);

@@ -781,6 +781,33 @@ __global__ void k_copy_u32(const u32* __restrict__ s, u32* __restrict__ d, u32 n
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) d[i] = s[i];
 }
 
+void rank_match(int KW, const u64* x_lo, const u64* x_hi, u32 nx, const u64* y_lo, const u64* y_hi, u32 ny,
+                u32* rank, u32* match, cudaStream_t st) {
+  if (!nx) return;
+  const int g = grid_for(nx, 256);
+  if (KW == 2) klaunch(k_rank<2>, g, 256, 0, st, x_lo, x_hi, nx, y_lo, y_hi, ny, rank, match);
+  else klaunch(k_rank<1>, g, 256, 0, st, x_lo, x_hi, nx, y_lo, y_hi, ny, rank, match);
+}
+
+template <int KW>
+__global__ void k_compact_keys(const u64* __restrict__ lo, const u64* __restrict__ hi, const u32* __restrict__ flag,
+                               const u32* __restrict__ pre, u32 n, u64* __restrict__ out_lo,
+                               u64* __restrict__ out_hi) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (!flag[i]) continue;
+    out_lo[pre[i]] = lo[i];
+    if (KW == 2) out_hi[pre[i]] = hi[i];
+  }
+}
+
+void compact_keys(int KW, const u64* lo, const u64* hi, const u32* flag, const u32* pre, u32 n, u64* out_lo,
+                  u64* out_hi, cudaStream_t st) {
+  if (!n) return;
+  const int g = grid_for(n, 256);
+  if (KW == 2) klaunch(k_compact_keys<2>, g, 256, 0, st, lo, hi, flag, pre, n, out_lo, out_hi);
+  else klaunch(k_compact_keys<1>, g, 256, 0, st, lo, hi, flag, pre, n, out_lo, out_hi);
+}
+
 void merge_combine(int KW, int S, const int* ops, const int* types, const u64* a_lo, const u64* a_hi,
                    const u64* a_st, u32 na, const u64* b_lo, const u64* b_hi, const u64* b_st, u32 nb,
                    u64* c_lo, u64* c_hi, u64* c_st, MergeTmp& tmp, cudaStream_t st) {

@@ -93,6 +93,13 @@ void merge_combine(int KW, int S, const int* ops, const int* types,
                    const u64* b_lo, const u64* b_hi, const u64* b_st, u32 nb,
                    u64* c_lo, u64* c_hi, u64* c_st, MergeTmp& tmp, cudaStream_t st);
 
+// rank[i] = lower_bound of x[i] in y, match[i] = (y[rank[i]] == x[i])
+void rank_match(int KW, const u64* x_lo, const u64* x_hi, u32 nx, const u64* y_lo, const u64* y_hi, u32 ny,
+                u32* rank, u32* match, cudaStream_t st);
+// out[pre[i]] = key[i] where flag[i]
+void compact_keys(int KW, const u64* lo, const u64* hi, const u32* flag, const u32* pre, u32 n, u64* out_lo,
+                  u64* out_hi, cudaStream_t st);
+
 // ---- tiny-table absorb (the early-aggregation probe for |T| <= 8) -------
 // Resident table of nt <= 8 keys (kernel parameters)
 struct TinyTable { u64 lo[8]; u64 hi[8]; };

@@ -528,6 +528,26 @@ class SortAggregate:
         streamed to the GPU in windows.  Returns ColumnarResult(keys, states)
         on the input's device.
         """
+        h, n, keys, vals, slots, on_host, sptr = self._prepare(keys, values, states, stream)
+        file_store = isinstance(self.store, FileStore)
+        if file_store:
+            h.set_spill_dir(self.store.directory, self.store._next)
+        # the native side selects the device itself; outputs name it explicitly
+        n_groups = h.execute(n, [k.data_ptr() for k in keys], [v.data_ptr() for v in vals], on_host, sptr)
+        if file_store:
+            self.run_ids = self.store._adopt(h.run_rows(), len(keys), len(slots), self.config.page_capacity)
+        return self._collect(h, n, n_groups, keys, slots, on_host, sptr)
+
+    def in_stream_columns(self, keys, values=None, *, states=False, stream=None):
+        """``in_stream_aggregate`` (bench.py:199-212) over columns already
+        sorted on the key: every run of equal consecutive keys becomes one
+        group (no sort, no memory budget, nothing spilled).  Same arguments
+        and result as ``execute_columns``."""
+        h, n, keys, vals, slots, on_host, sptr = self._prepare(keys, values, states, stream)
+        n_groups = h.in_stream(n, [k.data_ptr() for k in keys], [v.data_ptr() for v in vals], on_host, sptr)
+        return self._collect(h, n, n_groups, keys, slots, on_host, sptr)
+
+    def _prepare(self, keys, values, states, stream):
         torch = _torch()
         keys = list(keys)
         if len(keys) != self.schema.arity:
@@ -570,17 +590,12 @@ class SortAggregate:
                 raise InvalidInputError("key columns must be integer")
         val_codes = [_isa_dtype(v) for v in vals]
         h = self._handle(key_codes, val_codes, slots)
-        dev_index = self._device_index()
         if stream is None:
-            stream = torch.cuda.current_stream(dev_index)
-        sptr = ctypes_stream(stream)
-        file_store = isinstance(self.store, FileStore)
-        if file_store:
-            h.set_spill_dir(self.store.directory, self.store._next)
-        # the native side selects the device itself; outputs name it explicitly
-        n_groups = h.execute(n, [k.data_ptr() for k in keys], [v.data_ptr() for v in vals], on_host, sptr)
-        if file_store:
-            self.run_ids = self.store._adopt(h.run_rows(), len(keys), len(slots), self.config.page_capacity)
+            stream = torch.cuda.current_stream(self._device_index())
+        return h, n, keys, vals, slots, on_host, ctypes_stream(stream)
+
+    def _collect(self, h, n, n_groups, keys, slots, on_host, sptr):
+        torch = _torch()
         out_dev = torch.device("cpu") if on_host else keys[0].device
         pin = on_host
         out_keys = [torch.empty(n_groups, dtype=k.dtype, device=out_dev, pin_memory=pin) for k in keys]
@@ -591,6 +606,37 @@ class SortAggregate:
             h.result_copy([t.data_ptr() for t in out_keys], [t.data_ptr() for t in out_states], on_host, sptr)
         self._record(h, n, n_groups)
         return ColumnarResult(out_keys, out_states)
+
+    def intersect_columns(self, keys_a, keys_b, *, stream=None):
+        """``merge_intersect`` (bench.py:536-550) of two strictly ascending
+        key-column sets (e.g. two ``execute_columns`` outputs' keys): the keys
+        present in both, ascending, as key columns."""
+        torch = _torch()
+        keys_a, keys_b = list(keys_a), list(keys_b)
+        if len(keys_a) != self.schema.arity or len(keys_b) != self.schema.arity:
+            raise InvalidInputError(f"expected {self.schema.arity} key columns per input")
+        for ka, kb in zip(keys_a, keys_b):
+            if ka.dtype != kb.dtype:
+                raise InvalidInputError("both inputs need the same key dtypes")
+        on_host = keys_a[0].device.type == "cpu"
+        if any((k.device.type == "cpu") != on_host for k in keys_a + keys_b):
+            raise InvalidInputError("all columns must live on the same device type")
+        if not torch.cuda.is_available():
+            raise ResourceError("the B200 operator needs a CUDA device (torch.cuda.is_available() is False)")
+        if not on_host:
+            self._device = keys_a[0].device
+        keys_a = [k.contiguous() for k in keys_a]
+        keys_b = [k.contiguous() for k in keys_b]
+        na, nb = int(keys_a[0].shape[0]), int(keys_b[0].shape[0])
+        h = self._handle([_isa_dtype(k) for k in keys_a], [], ())
+        if stream is None:
+            stream = torch.cuda.current_stream(self._device_index())
+        sptr = ctypes_stream(stream)
+        out_dev = torch.device("cpu") if on_host else keys_a[0].device
+        out = [torch.empty(min(na, nb), dtype=k.dtype, device=out_dev, pin_memory=on_host) for k in keys_a]
+        k = h.merge_intersect(na, [t.data_ptr() for t in keys_a], nb, [t.data_ptr() for t in keys_b],
+                              [t.data_ptr() for t in out], on_host, sptr)
+        return [t[:k] for t in out]
 
     def _record(self, h, n_rows, n_groups):
         """Fold the device ledger into ``ledger`` now; the per-execute details
@@ -651,13 +697,19 @@ class SortAggregate:
     def execute(self, rows):
         """Aggregate an iterable of ``Row`` (key tuple, state tuple) and
         return the sorted list of aggregated ``Row`` (sortagg.py:744-747)."""
-        torch = _torch()
         rows = list(rows)
         self.executed_steps = []
         self.initial_plan = None
         self.runs_after_generation = 0
         if not rows:
             return []
+        keys_t, states_t = self._row_columns(rows)
+        return self._rows_from(self.execute_columns(keys_t, states_t, states=True))
+
+    def _row_columns(self, rows):
+        """Row objects -> key columns (narrowest order-preserving dtypes) and
+        state-slot columns, on this operator's CUDA device."""
+        torch = _torch()
         if not torch.cuda.is_available():
             raise ResourceError("the B200 operator needs a CUDA device (torch.cuda.is_available() is False)")
         arity = self.schema.arity
@@ -680,18 +732,15 @@ class SortAggregate:
                     raise InvalidInputError(f"state slot {s} does not fit int64")
                 state_cols.append(arr)
         dev = torch.device("cuda", self._device_index())
-        keys_t = [torch.from_numpy(c).to(dev) for c in key_cols]
-        states_t = [torch.from_numpy(c).to(dev) for c in state_cols]
-        res = self.execute_columns(keys_t, states_t, states=True)
+        return ([torch.from_numpy(c).to(dev) for c in key_cols], [torch.from_numpy(c).to(dev) for c in state_cols])
+
+    @staticmethod
+    def _rows_from(res):
         out_keys = [k.cpu().numpy() for k in res.keys]
         out_states = [s.cpu().numpy() for s in res.states]
-        n = res.n_groups
         key_lists = [_py_list(k) for k in out_keys]
         state_lists = [_py_list(s) for s in out_states]
-        out = []
-        for i in range(n):
-            out.append(Row(tuple(kl[i] for kl in key_lists), tuple(sl[i] for sl in state_lists)))
-        return out
+        return [Row(tuple(kl[i] for kl in key_lists), tuple(sl[i] for sl in state_lists)) for i in range(res.n_groups)]
 
 
 def _int_column(values, what):

