@@ -328,9 +328,9 @@ void absorb_tiny(int KW, int nt, const KeyDesc& kd, const SlotDesc& sd, int64_t 
 
 // ============================================================= probe ====
 // First chunk of an execute (T empty, <= PR_THREADS * PR_RPT rows): find the
-// distinct keys in first-occurrence order, one block-wide round per key
-// (OrderedIndex.insert_or_aggregate inserting into an empty index,
-// memindex.py:197-236).  If there are at most max_nt of them no flush can
+// distinct keys (OrderedIndex.insert_or_aggregate inserting into an empty
+// index, memindex.py:197-236): every warp dedupes its rows with
+// warp-synchronous rounds, then warp 0 dedupes the per-warp lists.  If there are at most max_nt of them no flush can
 // happen before the chunk ends (max_nt <= M), and a table holding exactly
 // these keys from the start is equivalent (every row of the chunk hits it):
 // the kernel writes the sorted keys into T with identity states and
@@ -340,70 +340,94 @@ void absorb_tiny(int KW, int nt, const KeyDesc& kd, const SlotDesc& sd, int64_t 
 // [0] = nt or ~0 on failure, [8 + j] = lo, [16 + j] = hi of sorted row j.
 #define PR_THREADS 1024
 #define PR_RPT 4
+// Distinct keys of `nrow` candidates held by the 32 lanes (row bits in
+// `pending`, keys selectable by index): warp-synchronous rounds, each picks
+// the first pending candidate, broadcasts its key and clears every equal
+// one.  Appends to (tlo, thi)[*cnt ..]; returns false past `cap` keys.
+template <int KW, int R>
+__device__ __forceinline__ bool warp_distinct(const u64 (&klo)[R], const u64 (&khi)[R], u32 pending, u32 cap,
+                                              u64* tlo, u64* thi, u32* cnt) {
+  const u32 full = 0xffffffffu;
+  const u32 lane = threadIdx.x & 31;
+  for (;;) {
+    const u32 ball = __ballot_sync(full, pending != 0);
+    if (!ball) return true;
+    if (*cnt == cap) return false;
+    const int src = __ffs(ball) - 1;
+    const int kk = __ffs(__shfl_sync(full, pending, src)) - 1;
+    u64 blo = 0, bhi = 0;
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if (k == kk) { blo = klo[k]; bhi = khi[k]; }
+    blo = __shfl_sync(full, blo, src);
+    bhi = __shfl_sync(full, bhi, src);
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if (((pending >> k) & 1u) && key_eq<KW>(khi[k], klo[k], bhi, blo)) pending &= ~(1u << k);
+    if (lane == 0) { tlo[*cnt] = blo; thi[*cnt] = bhi; }
+    __syncwarp();
+    ++*cnt;
+  }
+}
+
 template <int KW>
 __global__ void __launch_bounds__(PR_THREADS) k_probe_tiny(KeyDesc kd, SlotDesc sd, i64 row0, u32 n, u32 max_nt,
                                                          u64* __restrict__ T_lo, u64* __restrict__ T_hi,
                                                          u64* __restrict__ T_st, u64* out) {
+  constexpr int NW = PR_THREADS / 32;
+  __shared__ u64 wlo[NW][8], whi[NW][8];
+  __shared__ u32 wn[NW];
   __shared__ u64 tlo[8], thi[8];
-  __shared__ u32 s_min;
   const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const u32 NONE = 0xFFFFFFFFu;
   u64 klo[PR_RPT], khi[PR_RPT];
-  u32 hk[PR_RPT];
+  u32 pending = 0;
 #pragma unroll
   for (int k = 0; k < PR_RPT; ++k) {
     const u32 q = k * PR_THREADS + tid;
     klo[k] = khi[k] = 0;
-    hk[k] = NONE;
-    if (q < n) load_key(kd, row0 + q, khi[k], klo[k]);
+    if (q < n) {
+      load_key(kd, row0 + q, khi[k], klo[k]);
+      pending |= 1u << k;
+    }
   }
+  // 1. every warp: the distinct keys of its rows (at most max_nt)
+  u32 cnt = 0;
+  const bool fits = warp_distinct<KW, PR_RPT>(klo, khi, pending, max_nt, wlo[w], whi[w], &cnt);
+  if (lane == 0) wn[w] = fits ? cnt : 0xFFFFFFFFu;
+  __syncthreads();
+  if (w != 0) return;
+  // 2. warp 0: the distinct keys over every warp's list
+  const u32 mine = wn[lane < NW ? lane : 0];
+  const bool over = __any_sync(0xffffffffu, lane < NW && mine == 0xFFFFFFFFu);
   u32 nt = 0;
-  bool ok = true;
-  for (;;) {
-    if (tid == 0) s_min = NONE;
-    __syncthreads();
-    u32 mine = NONE;
+  bool ok = !over;
+  if (ok) {
+    u64 clo[8], chi[8];
+    u32 cp = 0;
 #pragma unroll
-    for (int k = PR_RPT - 1; k >= 0; --k) {
-      const u32 q = k * PR_THREADS + tid;
-      if (q < n && hk[k] == NONE) mine = q;
+    for (int j = 0; j < 8; ++j) {
+      clo[j] = chi[j] = 0;
+      if (lane < NW && (u32)j < mine) { clo[j] = wlo[lane][j]; chi[j] = whi[lane][j]; cp |= 1u << j; }
     }
-    mine = __reduce_min_sync(0xffffffffu, mine);
-    if (lane == 0 && mine != NONE) atomicMin(&s_min, mine);
-    __syncthreads();
-    const u32 m = s_min;
-    if (m == NONE) break;
-    if (nt == max_nt) { ok = false; break; }
-    if (tid == m % PR_THREADS) {
-      const int km = (int)(m / PR_THREADS);
-#pragma unroll
-      for (int k = 0; k < PR_RPT; ++k)
-        if (k == km) { tlo[nt] = klo[k]; thi[nt] = khi[k]; }
-    }
-    __syncthreads();
-    const u64 nlo = tlo[nt], nhi = thi[nt];
-#pragma unroll
-    for (int k = 0; k < PR_RPT; ++k)
-      if (hk[k] == NONE && key_eq<KW>(khi[k], klo[k], nhi, nlo)) hk[k] = nt;
-    ++nt;
+    ok = warp_distinct<KW, 8>(clo, chi, cp, max_nt, tlo, thi, &nt);
   }
   if (!ok) {
-    if (tid == 0) *(volatile u64*)out = ~0ull;
+    if (lane == 0) *(volatile u64*)out = ~0ull;
     return;
   }
-  // table row tid -> its sorted position; states start at the identity (the
+  // table row -> its sorted position; states start at the identity (the
   // absorb pass that follows covers these rows too)
-  if (tid < nt) {
+  if (lane < nt) {
     u32 r = 0;
-    for (u32 j = 0; j < nt; ++j) r += key_less<KW>(thi[j], tlo[j], thi[tid], tlo[tid]) ? 1u : 0u;
-    T_lo[r] = tlo[tid];
-    if (KW == 2) T_hi[r] = thi[tid];
-    ((volatile u64*)out)[8 + r] = tlo[tid];
-    ((volatile u64*)out)[16 + r] = thi[tid];
+    for (u32 j = 0; j < nt; ++j) r += key_less<KW>(thi[j], tlo[j], thi[lane], tlo[lane]) ? 1u : 0u;
+    T_lo[r] = tlo[lane];
+    if (KW == 2) T_hi[r] = thi[lane];
+    ((volatile u64*)out)[8 + r] = tlo[lane];
+    ((volatile u64*)out)[16 + r] = thi[lane];
   }
   const int S = sd.nslots;
-  if (tid < nt * S) T_st[tid] = identity_slot(sd.op[tid % S], sd.type[tid % S]);
-  if (tid == 0) *(volatile u64*)out = nt;
+  for (int i = lane; i < (int)nt * S; i += 32) T_st[i] = identity_slot(sd.op[i % S], sd.type[i % S]);
+  if (lane == 0) *(volatile u64*)out = nt;
 }
 
 u32 probe_rows() { return PR_THREADS * PR_RPT; }

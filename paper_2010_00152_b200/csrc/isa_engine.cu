@@ -234,6 +234,7 @@ struct Engine {
   size_t desc_cap[2] = {0, 0};
   cudaEvent_t desc_done[2] = {nullptr, nullptr};
   u32 fmask = 0;                            // f64 state slots (codec transform)
+  DevBuf t_backup;                          // T's states before a speculative absorb fold
   // FileStore tier
   PageSpec ps0;
   std::string spill_dir;
@@ -322,7 +323,7 @@ struct Engine {
                       &mg_rank_b, &mg_match_b, &ab_partials, &ab_miss_buf, &ab_miss_cnt, &ab_miss_off,
                       &miss_list, &stg_lo[0], &stg_lo[1], &stg_hi[0], &stg_hi[1], &stg_st[0], &stg_st[1],
                       &runref_dev, &bounds_lo, &bounds_hi, &bounds_out, &out_tmp, &pk_hdr, &pk_sz,
-                      &stg_pk[0], &stg_pk[1], &stg_desc[0], &stg_desc[1]};
+                      &stg_pk[0], &stg_pk[1], &stg_desc[0], &stg_desc[1], &t_backup};
     for (int i = 0; i < 2; ++i) {
       if (desc_pinned[i]) cudaFreeHost(desc_pinned[i]);
       if (desc_done[i]) cudaEventDestroy(desc_done[i]);
@@ -1038,12 +1039,20 @@ struct Engine {
     scan_tmp.ensure((scan_tmp_words(grid + 1) + 64) * 4);
     CK(cudaMemcpyAsync(ab_miss_off.p, ab_miss_cnt.p, (size_t)grid * 4, cudaMemcpyDeviceToDevice, st));
     scan_exclusive_u32(ab_miss_off.as<u32>(), grid, scan_tmp.as<u32>(), dscal32(3), st);
+    // fold speculatively (the common case: no misses) before the one host
+    // round trip; T's states are kept to undo it when the chunk has misses
+    const size_t tst_bytes = (size_t)nt * S * 8;
+    if (S) {
+      t_backup.ensure(tst_bytes + 8);
+      CK(cudaMemcpyAsync(t_backup.p, T.pst(), tst_bytes, cudaMemcpyDeviceToDevice, st));
+    }
+    fold_partials(nt, sd, ab_partials.as<u64>(), grid, T.pst(), st);
     u32 nmiss = read_u32(dscal32(3));
     if (nmiss == 0) {
-      fold_partials(nt, sd, ab_partials.as<u64>(), grid, T.pst(), st);
       last_new = 0;
       return a + span;
     }
+    if (S) CK(cudaMemcpyAsync(T.pst(), t_backup.p, tst_bytes, cudaMemcpyDeviceToDevice, st));
     miss_list.ensure((size_t)nmiss * 4 + 64);
     compact_misses(ab_miss_buf.as<u32>(), ab_miss_cnt.as<u32>(), ab_miss_off.as<u32>(), grid, rpc,
                    miss_list.as<u32>(), st);
