@@ -29,6 +29,7 @@
 #include "../../include/insortagg_b200.h"
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <fcntl.h>
 #include <unistd.h>
@@ -1094,7 +1095,17 @@ struct Engine {
       // a handful of groups, hands the rest to the absorb kernel
       len = kProbeRows;
     } else if (last_flushed) {
-      len = last_cycle + last_cycle / 8 + 4096;
+      // the next flush ~ one fill cycle away; the margin follows how much
+      // consecutive cycles have varied (rows past the flush are sorted for
+      // nothing; a chunk that ends short costs an extra table merge)
+      double dev = 0.03;
+      if (cycles.size() >= 2) {
+        dev = 0;
+        for (size_t i = 1; i < cycles.size(); ++i)
+          dev = std::max(dev, std::fabs((double)cycles[i] / (double)std::max<int64_t>(cycles[i - 1], 1) - 1.0));
+      }
+      const double slack = std::min(0.125, 0.01 + 4.0 * dev);
+      len = last_cycle + (int64_t)((double)last_cycle * slack) + 4096;
     } else if (last_new > 0) {
       double rate = (double)last_new / (double)last_len;
       double need = (double)(M - (int64_t)T.n + 1) / rate;
