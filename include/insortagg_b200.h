@@ -208,6 +208,28 @@ ISA_API int isa_merge_intersect(isa_handle* h, int64_t n_a, const void* const* a
                                 const void* const* b_keys, void* const* out_keys, int32_t on_host,
                                 void* stream, int64_t* n_out);
 
+/* Fused range exchange for multi-GPU execution: the
+ * partition kernel's gather stores every row straight into the destination
+ * rank's receive columns over NVLink / NVSwitch (peer pointers from CUDA IPC),
+ * instead of a local partition followed by an NCCL all-to-all.
+ * isa_partition_counts: destinations by splitters (as isa_partition) and the
+ * per-destination row counts (kept: the permutation stays in the handle).
+ * isa_scatter_to_peers: peer_cols[d * (n_key_cols + n_val_cols) + c] =
+ * destination d's receive column c (keys then values); this rank's rows for d
+ * land at row peer_offsets[d] of it.  Returns after the stores completed. */
+ISA_API int isa_partition_counts(isa_handle* h, int64_t n_rows, const void* const* key_cols,
+                                 const uint64_t* split_lo, const uint64_t* split_hi, int32_t n_split,
+                                 int64_t* counts, void* stream);
+ISA_API int isa_scatter_to_peers(isa_handle* h, int64_t n_rows, const void* const* key_cols,
+                                 const void* const* val_cols, void* const* peer_cols,
+                                 const int64_t* peer_offsets, void* stream);
+/* CUDA IPC plumbing for the receive columns: 72-byte handles (allocation
+ * handle + the pointer's offset inside the allocation); open returns the
+ * mapped allocation base (for isa_ipc_close) and the pointer. */
+ISA_API int isa_ipc_handle(void* dev_ptr, void* handle_out);
+ISA_API int isa_ipc_open(const void* handle, void** base_out, void** dev_ptr_out);
+ISA_API int isa_ipc_close(void* base);
+
 /* FileStore tier (runstore.py:195-236): runs are written to
  * `dir`/run_NNNNNN.bin, byte-identical to the reference's RunWriter pages
  * (runstore.py:120-129, 239-301: int64 key columns and int64 states only),

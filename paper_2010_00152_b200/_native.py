@@ -48,7 +48,8 @@ EXPORTED_SYMBOLS = (
     "isa_version", "isa_create", "isa_destroy", "isa_execute", "isa_result_copy",
     "isa_metrics", "isa_cycles", "isa_run_rows", "isa_last_error",
     "isa_sample_keys", "isa_partition", "isa_phase_stats", "isa_launch_count", "isa_steps",
-    "isa_set_spill_dir", "isa_in_stream_aggregate", "isa_merge_intersect",
+    "isa_set_spill_dir", "isa_in_stream_aggregate", "isa_merge_intersect", "isa_partition_counts",
+    "isa_scatter_to_peers", "isa_ipc_handle", "isa_ipc_open", "isa_ipc_close",
 )
 
 PHASES = ("absorb", "sort", "flush", "collapse", "table_merge", "wm_sort", "wm_collapse",
@@ -154,6 +155,16 @@ def load():
     lib.isa_in_stream_aggregate.argtypes = [vp, ctypes.c_int64, pp, pp, ctypes.c_int32, vp, i64p]
     lib.isa_merge_intersect.restype = ctypes.c_int
     lib.isa_merge_intersect.argtypes = [vp, ctypes.c_int64, pp, ctypes.c_int64, pp, pp, ctypes.c_int32, vp, i64p]
+    lib.isa_partition_counts.restype = ctypes.c_int
+    lib.isa_partition_counts.argtypes = [vp, ctypes.c_int64, pp, vp, vp, ctypes.c_int32, i64p, vp]
+    lib.isa_scatter_to_peers.restype = ctypes.c_int
+    lib.isa_scatter_to_peers.argtypes = [vp, ctypes.c_int64, pp, pp, pp, i64p, vp]
+    lib.isa_ipc_handle.restype = ctypes.c_int
+    lib.isa_ipc_handle.argtypes = [vp, vp]
+    lib.isa_ipc_open.restype = ctypes.c_int
+    lib.isa_ipc_open.argtypes = [vp, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p)]
+    lib.isa_ipc_close.restype = ctypes.c_int
+    lib.isa_ipc_close.argtypes = [vp]
     lib.isa_set_spill_dir.restype = ctypes.c_int
     lib.isa_set_spill_dir.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64]
     lib.isa_metrics.restype = ctypes.c_int
@@ -246,6 +257,17 @@ class Handle:
                                                   ctypes.byref(out)))
         return out.value
 
+    def partition_counts(self, n_rows, key_ptrs, split_lo, split_hi, n_split, stream):
+        counts = (ctypes.c_int64 * (n_split + 1))()
+        self._check(self._lib.isa_partition_counts(self._h, n_rows, _ptr_array(key_ptrs), split_lo, split_hi,
+                                                   n_split, counts, stream))
+        return [counts[i] for i in range(n_split + 1)]
+
+    def scatter_to_peers(self, n_rows, key_ptrs, val_ptrs, peer_ptrs, peer_offsets, stream):
+        offs = (ctypes.c_int64 * max(1, len(peer_offsets)))(*peer_offsets)
+        self._check(self._lib.isa_scatter_to_peers(self._h, n_rows, _ptr_array(key_ptrs), _ptr_array(val_ptrs),
+                                                   _ptr_array(peer_ptrs), offs, stream))
+
     def set_spill_dir(self, directory, first_run_id):
         self._check(self._lib.isa_set_spill_dir(self._h, os.fsencode(directory), int(first_run_id)))
 
@@ -294,3 +316,23 @@ class Handle:
                                             split_lo, split_hi, n_split, _ptr_array(key_out),
                                             _ptr_array(val_out), counts, stream))
         return [counts[i] for i in range(n_split + 1)]
+
+
+def ipc_handle(ptr):
+    """72-byte CUDA IPC handle of a device pointer (allocation handle + offset)."""
+    buf = ctypes.create_string_buffer(72)
+    if load().isa_ipc_handle(ctypes.c_void_p(ptr), buf) != 0:
+        raise ResourceError("cudaIpcGetMemHandle failed")
+    return bytes(buf.raw)
+
+
+def ipc_open(handle):
+    """Map a peer's pointer: returns (allocation base for ipc_close, pointer)."""
+    base, ptr = ctypes.c_void_p(0), ctypes.c_void_p(0)
+    if load().isa_ipc_open(ctypes.create_string_buffer(handle, 72), ctypes.byref(base), ctypes.byref(ptr)) != 0:
+        raise ResourceError("cudaIpcOpenMemHandle failed")
+    return base.value, ptr.value
+
+
+def ipc_close(base):
+    load().isa_ipc_close(ctypes.c_void_p(base))

@@ -1861,6 +1861,66 @@ struct Engine {
     return k;
   }
 
+  // ------------------------------------------- fused range exchange --
+  // Phase 1: destinations + the destination-sorted permutation (kept in the
+  // handle) and per-destination counts.  Phase 2: one kernel gathers every
+  // column in that order and stores it into the destination ranks' receive
+  // columns (peer pointers), so the data crosses NVLink inside the kernel.
+  int pc_cur = 0;
+  u32 pc_m = 0;
+  int pc_ndest = 0;
+  DevBuf pc_tab, pc_off, pc_seg;
+  void partition_counts(int64_t n, const void* const* key_cols, const u64* sp_lo, const u64* sp_hi, int ns,
+                        int64_t* counts, cudaStream_t stream) {
+    CK(cudaSetDevice(dev));
+    st = stream;
+    if (ns < 0 || ns > 255) throw IsaError(ISA_ERR_INVALID_INPUT, "at most 255 splitters");
+    if (n > 0x7FFFFFFFll) throw IsaError(ISA_ERR_INVALID_INPUT, "partition of more than 2^31 rows per call");
+    const u32 m = (u32)n;
+    pc_m = m;
+    pc_ndest = ns + 1;
+    if (m == 0) { for (int d = 0; d <= ns; ++d) counts[d] = 0; return; }
+    ensure_sort(m);
+    KeyDesc kd = kd_at(key_cols);
+    partition_dest(KW, kd, m, sp_lo, sp_hi, ns, s_lo_buf(0), s_val[0].as<u32>(), st);
+    SortBufs b;
+    for (int i = 0; i < 2; ++i) { b.lo[i] = s_lo[i].as<u64>(); b.hi[i] = nullptr; b.val[i] = s_val[i].as<u32>(); }
+    b.aux = tile_hist.p;
+    pc_cur = radix_sort_pairs(1, b, m, 0, 8, st, nullptr);
+    word_tmp.ensure(4 * 256);
+    count_dest(s_lo[pc_cur].as<u64>(), m, ns + 1, word_tmp.as<u32>(), st);
+    std::vector<u32> ub(ns + 1);
+    CK(cudaMemcpyAsync(ub.data(), word_tmp.p, 4 * (ns + 1), cudaMemcpyDeviceToHost, st));
+    sync();
+    u32 prev = 0;
+    std::vector<u32> seg(ns + 1);
+    for (int d = 0; d <= ns; ++d) { counts[d] = ub[d] - prev; seg[d] = prev; prev = ub[d]; }
+    pc_seg.ensure(4 * 256);
+    CK(cudaMemcpyAsync(pc_seg.p, seg.data(), 4 * (ns + 1), cudaMemcpyHostToDevice, st));
+    sync();
+  }
+  void scatter_to_peers(int64_t n, const void* const* key_cols, const void* const* val_cols,
+                        void* const* peer_cols, const int64_t* peer_off, cudaStream_t stream) {
+    CK(cudaSetDevice(dev));
+    st = stream;
+    if ((u32)n != pc_m) throw IsaError(ISA_ERR_CONTRACT, "scatter_to_peers without a matching partition_counts");
+    if (n == 0) return;
+    PeerScatter ps;
+    memset(&ps, 0, sizeof(ps));
+    for (int c = 0; c < sch.n_key_cols; ++c) { ps.src[ps.ncols] = key_cols[c]; ps.elem[ps.ncols++] = (int)key_elem(c); }
+    for (int j = 0; j < sch.n_val_cols; ++j) { ps.src[ps.ncols] = val_cols[j]; ps.elem[ps.ncols++] = (int)val_elem(j); }
+    const size_t ntab = (size_t)pc_ndest * ps.ncols;
+    pc_tab.ensure(ntab * sizeof(void*) + 16);
+    pc_off.ensure((size_t)pc_ndest * 8 + 16);
+    std::vector<u64> offs(pc_ndest);
+    for (int d = 0; d < pc_ndest; ++d) offs[d] = (u64)peer_off[d];
+    CK(cudaMemcpyAsync(pc_tab.p, peer_cols, ntab * sizeof(void*), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(pc_off.p, offs.data(), (size_t)pc_ndest * 8, cudaMemcpyHostToDevice, st));
+    scatter_peers(ps, s_val[pc_cur].as<u32>(), s_lo[pc_cur].as<u64>(), (u32)n, (void* const*)pc_tab.p,
+                  pc_off.as<u64>(), pc_seg.as<u32>(), st);
+    sync();   // the host buffers above, and the peers may read once every rank returned
+  }
+
   // --------------------------------------------------------- partition --
   void partition(int64_t n, const void* const* key_cols, const void* const* val_cols, const u64* sp_lo,
                  const u64* sp_hi, int ns, void* const* key_out, void* const* val_out, int64_t* counts,
@@ -1971,6 +2031,77 @@ int isa_merge_intersect(isa_handle* h, int64_t n_a, const void* const* a_keys, i
   } catch (const std::exception& e) {
     return fail(h, e);
   }
+}
+
+int isa_partition_counts(isa_handle* h, int64_t n_rows, const void* const* key_cols, const uint64_t* split_lo,
+                         const uint64_t* split_hi, int32_t n_split, int64_t* counts, void* stream) {
+  if (!h || !counts) return ISA_ERR_CONTRACT;
+  try {
+    h->eng->partition_counts(n_rows, key_cols, (const u64*)split_lo, (const u64*)split_hi, n_split, counts,
+                             (cudaStream_t)stream);
+    return ISA_OK;
+  } catch (const std::exception& e) {
+    return fail(h, e);
+  }
+}
+
+int isa_scatter_to_peers(isa_handle* h, int64_t n_rows, const void* const* key_cols, const void* const* val_cols,
+                         void* const* peer_cols, const int64_t* peer_offsets, void* stream) {
+  if (!h || !peer_cols || !peer_offsets) return ISA_ERR_CONTRACT;
+  try {
+    h->eng->scatter_to_peers(n_rows, key_cols, val_cols, peer_cols, peer_offsets, (cudaStream_t)stream);
+    return ISA_OK;
+  } catch (const std::exception& e) {
+    return fail(h, e);
+  }
+}
+
+// An IPC handle names a whole allocation (a caching allocator hands out
+// pointers inside larger segments): the 72-byte handle carries the
+// allocation's handle plus the pointer's offset inside it (base from the
+// driver's cuMemGetAddressRange, reached through the runtime's entry-point
+// query so the library does not link libcuda).
+typedef int (*GetAddressRangeFn)(unsigned long long*, size_t*, unsigned long long);
+static GetAddressRangeFn address_range_fn() {
+  static GetAddressRangeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (GetAddressRangeFn)p;
+  }
+  return fn;
+}
+
+int isa_ipc_handle(void* dev_ptr, void* handle_out /* 72 bytes */) {
+  if (!dev_ptr || !handle_out) return ISA_ERR_CONTRACT;
+  GetAddressRangeFn fn = address_range_fn();
+  if (!fn) return ISA_ERR_CUDA;
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (fn(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) != 0) return ISA_ERR_CUDA;
+  cudaIpcMemHandle_t hnd;
+  if (cudaIpcGetMemHandle(&hnd, (void*)(uintptr_t)base) != cudaSuccess) return ISA_ERR_CUDA;
+  const uint64_t off = (uint64_t)((uintptr_t)dev_ptr - (uintptr_t)base);
+  memcpy(handle_out, &hnd, sizeof(hnd));
+  memcpy((char*)handle_out + 64, &off, 8);
+  return ISA_OK;
+}
+
+int isa_ipc_open(const void* handle, void** base_out, void** dev_ptr_out) {
+  if (!handle || !base_out || !dev_ptr_out) return ISA_ERR_CONTRACT;
+  cudaIpcMemHandle_t hnd;
+  uint64_t off = 0;
+  memcpy(&hnd, handle, sizeof(hnd));
+  memcpy(&off, (const char*)handle + 64, 8);
+  if (cudaIpcOpenMemHandle(base_out, hnd, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return ISA_ERR_CUDA;
+  *dev_ptr_out = (char*)*base_out + off;
+  return ISA_OK;
+}
+
+int isa_ipc_close(void* base) {
+  return cudaIpcCloseMemHandle(base) == cudaSuccess ? ISA_OK : ISA_ERR_CUDA;
 }
 
 int isa_set_spill_dir(isa_handle* h, const char* dir, int64_t first_run_id) {

@@ -992,6 +992,35 @@ void gather_column(const void* src, int elem_bytes, const u32* perm, u32 n, void
   }
 }
 
+// Fused exchange: row i of the destination-sorted order (perm[i] = source
+// row, dest[i] = destination rank) is gathered from the local columns and
+// stored straight into the destination rank's receive columns (peer memory
+// over NVLink / NVSwitch), at peer_off[d] + (i - seg_start[d]).
+__global__ void k_scatter_peers(const PeerScatter ps, const u32* __restrict__ perm, const u64* __restrict__ dest,
+                                u32 n, void* const* __restrict__ peer_cols, const u64* __restrict__ peer_off,
+                                const u32* __restrict__ seg_start) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const u32 d = (u32)dest[i];
+    const u32 r = perm[i];
+    const u64 o = peer_off[d] + (i - seg_start[d]);
+    for (int c = 0; c < ps.ncols; ++c) {
+      char* dst = (char*)peer_cols[(size_t)d * ps.ncols + c];
+      const char* src = (const char*)ps.src[c];
+      switch (ps.elem[c]) {
+        case 1: ((unsigned char*)dst)[o] = ((const unsigned char*)src)[r]; break;
+        case 2: ((unsigned short*)dst)[o] = ((const unsigned short*)src)[r]; break;
+        case 4: ((unsigned int*)dst)[o] = ((const unsigned int*)src)[r]; break;
+        default: ((u64*)dst)[o] = ((const u64*)src)[r]; break;
+      }
+    }
+  }
+}
+
+void scatter_peers(const PeerScatter& ps, const u32* perm, const u64* dest, u32 n, void* const* peer_cols,
+                   const u64* peer_off, const u32* seg_start, cudaStream_t st) {
+  if (n) klaunch(k_scatter_peers, grid_for(n, 256), 256, 0, st, ps, perm, dest, n, peer_cols, peer_off, seg_start);
+}
+
 __global__ void k_count_dest(const u64* __restrict__ d, u32 n, int ndest, u32* __restrict__ counts) {
   // counts[k] = upper_bound(d, k) for the sorted destination array
   int k = blockIdx.x * blockDim.x + threadIdx.x;

@@ -173,5 +173,8 @@ void partition_dest(int KW, const KeyDesc& kd, u32 n, const u64* s_lo, const u64
                     u64* dest_lo, u32* val, cudaStream_t st);
 void gather_column(const void* src, int elem_bytes, const u32* perm, u32 n, void* dst, cudaStream_t st);
 void count_dest(const u64* dest_sorted, u32 n, int ndest, u32* counts, cudaStream_t st);
+struct PeerScatter { int ncols; const void* src[ISA_MAX_KEY_COLS + ISA_MAX_VAL_COLS]; int elem[ISA_MAX_KEY_COLS + ISA_MAX_VAL_COLS]; };
+void scatter_peers(const PeerScatter& ps, const u32* perm, const u64* dest, u32 n, void* const* peer_cols,
+                   const u64* peer_off, const u32* seg_start, cudaStream_t st);
 
 }  // namespace isa

@@ -12,7 +12,14 @@ partitioning for parallel computation).  Steps:
 3. stable partition of the local rows by destination (isa_partition: one
    8-bit radix pass on the destination + column gathers),
 4. exchange counts, then every column, with all_to_all_single over NCCL
-   (NVLink / NVSwitch) — variable-count all-to-all,
+   (NVLink / NVSwitch) — variable-count all-to-all; or, with
+   ``exchange="p2p"`` (env ISA_EXCHANGE), the fused form: one kernel per rank
+   gathers its rows in destination order and stores them straight into the
+   destination ranks' receive columns through CUDA-IPC peer pointers
+   (isa_partition_counts + isa_scatter_to_peers), so the transfer happens
+   inside the partition kernel.  NCCL stays the default until the fused
+   path has run on a multi-GPU box (the single-GPU test drives the same
+   kernel with simulated peers),
 5. run the local SortAggregate on the received rows.
 
 ``mode="preaggregate"`` runs the local operator first and exchanges the
@@ -26,6 +33,8 @@ can drive it over gloo with the oracle standing in for the CUDA kernels.
 """
 
 from __future__ import annotations
+
+import os
 
 import torch
 import torch.distributed as dist
@@ -98,6 +107,61 @@ def exchange_columns(columns, send_counts, group=None):
     return out, recv_counts
 
 
+def p2p_offsets(count_matrix, me):
+    """Row offset of rank ``me``'s block inside every destination's receive
+    columns: blocks are laid out in source-rank order, so destination d
+    receives rank r's rows at sum(count_matrix[q][d] for q < r)."""
+    world = len(count_matrix)
+    return [sum(count_matrix[q][d] for q in range(me)) for d in range(world)]
+
+
+def exchange_p2p(op, keys, cols, split_hi, split_lo, group=None):
+    """Fused range exchange over NVLink / NVSwitch peer memory: every rank
+    allocates its receive columns, the CUDA IPC handles are all-gathered,
+    and one kernel per rank gathers its rows in destination order and stores
+    them straight into the destinations' receive columns
+    (isa_partition_counts + isa_scatter_to_peers).  Returns (received key
+    columns, received value columns)."""
+    from .sortagg import ctypes_stream
+    from . import _native
+    world = _group_size(group)
+    me = dist.get_rank(group)
+    dev = keys[0].device
+    n = int(keys[0].shape[0])
+    h = _key_handle(op, keys, cols)
+    st = torch.cuda.current_stream(dev)
+    counts = h.partition_counts(n, [k.data_ptr() for k in keys], split_lo.contiguous().data_ptr(),
+                                split_hi.contiguous().data_ptr(), world - 1, ctypes_stream(st))
+    mine = torch.tensor(counts, dtype=torch.int64, device=dev)
+    allc = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(allc, mine, group=group)
+    matrix = [[int(x) for x in c.tolist()] for c in allc]
+    recv_n = sum(matrix[q][me] for q in range(world))
+    recv = [torch.empty(max(recv_n, 1), dtype=t.dtype, device=dev) for t in list(keys) + list(cols)]
+    handles = [_native.ipc_handle(t.data_ptr()) for t in recv]
+    every = [None] * world
+    dist.all_gather_object(every, handles, group=group)
+    opened, table = [], []
+    try:
+        for d in range(world):
+            for c, hd in enumerate(every[d]):
+                if d == me:
+                    table.append(recv[c].data_ptr())
+                else:
+                    base, p = _native.ipc_open(hd)
+                    opened.append(base)
+                    table.append(p)
+        dist.barrier(group=group)   # every receive column exists before anyone stores into it
+        h.scatter_to_peers(n, [k.data_ptr() for k in keys], [c.data_ptr() for c in cols], table,
+                           p2p_offsets(matrix, me), ctypes_stream(st))
+        dist.barrier(group=group)   # every rank's stores are done before anyone reads
+    finally:
+        for base in opened:
+            _native.ipc_close(base)
+    recv = [t[:recv_n] for t in recv]
+    return recv[: len(keys)], recv[len(keys):]
+
+
 def native_sampler(op, keys, per_rank):
     """Normalized keys of ~per_rank evenly spaced local rows (CUDA kernel)."""
     from .sortagg import ctypes_stream
@@ -139,7 +203,7 @@ def native_partitioner(op, keys, values, split_hi, split_lo):
 
 
 def distributed_execute(op, keys, values=None, *, mode="partition", group=None, samples_per_rank=1 << 16,
-                        sampler=None, partitioner=None, local_execute=None, merge_execute=None):
+                        sampler=None, partitioner=None, local_execute=None, merge_execute=None, exchange=None):
     """Range-partitioned SortAggregate over every rank of ``group``.
 
     Returns this rank's slice of the globally sorted result (a
@@ -169,9 +233,16 @@ def distributed_execute(op, keys, values=None, *, mode="partition", group=None, 
     s_hi, s_lo = sampler(keys)
     all_hi, all_lo = gather_samples(s_hi, s_lo, group)
     split_hi, split_lo = choose_splitters(all_hi, all_lo, world)
-    pk, pc, counts = partitioner(keys, cols, split_hi, split_lo)
-    recv, _ = exchange_columns(pk + pc, counts, group)
-    rk, rc = recv[: len(pk)], recv[len(pk):]
+    exchange = exchange or os.environ.get("ISA_EXCHANGE", "nccl")
+    if exchange == "p2p":
+        # fused: the partition kernel stores into the peers' receive columns
+        rk, rc = exchange_p2p(op, keys, cols, split_hi, split_lo, group)
+    elif exchange == "nccl":
+        pk, pc, counts = partitioner(keys, cols, split_hi, split_lo)
+        recv, _ = exchange_columns(pk + pc, counts, group)
+        rk, rc = recv[: len(pk)], recv[len(pk):]
+    else:
+        raise InvalidInputError(f"unknown exchange {exchange!r}")
     if mode == "preaggregate":
         return merge_execute(rk, rc)
     return local_execute(rk, dict(zip(names, rc)) if names is not None else rc)

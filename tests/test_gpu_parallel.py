@@ -78,3 +78,53 @@ def test_distributed_execute_single_rank_nccl(mode):
             assert np.array_equal(g.cpu().numpy(), e)
     finally:
         dist.destroy_process_group()
+
+
+def test_fused_scatter_to_simulated_peers():
+    """isa_partition_counts + isa_scatter_to_peers with three receive
+    buffers on this GPU standing in for peers: as rank 1 of 3, every
+    destination's block holds exactly the rows isa_partition assigns it, in
+    the same (stable) order, at the offset after rank 0's block."""
+    from paper_2010_00152_b200 import parallel, workloads
+    from paper_2010_00152_b200.sortagg import ctypes_stream
+    w = workloads.config5(rows=500_000, device="cuda", domain=1 << 24)
+    op = isa.SortAggregate(w.schema, isa.SortAggConfig(memory_budget=1 << 16, page_capacity=100))
+    keys, vals = list(w.keys), [w.values["v"]]
+    sh, sl = parallel.native_sampler(op, keys, 4096)
+    split_hi, split_lo = parallel.choose_splitters(sh, sl, 3)
+    pk, pv, counts = parallel.native_partitioner(op, keys, vals, split_hi, split_lo)
+    h = parallel._key_handle(op, keys, vals)
+    st = torch.cuda.current_stream()
+    got = h.partition_counts(w.rows, [k.data_ptr() for k in keys], split_lo.contiguous().data_ptr(),
+                             split_hi.contiguous().data_ptr(), 2, ctypes_stream(st))
+    assert got == counts
+    rank0 = [7, 11, 13]   # rows rank 0 sends to each destination
+    matrix = [rank0, counts, [0, 0, 0]]
+    offs = parallel.p2p_offsets(matrix, 1)
+    recv = [[torch.full((rank0[d] + counts[d] + 5,), -1, dtype=t.dtype, device="cuda") for t in keys + vals]
+            for d in range(3)]
+    table = [t.data_ptr() for d in range(3) for t in recv[d]]
+    h.scatter_to_peers(w.rows, [k.data_ptr() for k in keys], [v.data_ptr() for v in vals], table, offs,
+                       ctypes_stream(st))
+    torch.cuda.synchronize()
+    start = 0
+    for d in range(3):
+        for c, src in enumerate(pk + pv):
+            block = recv[d][c][offs[d]: offs[d] + counts[d]]
+            assert torch.equal(block, src[start: start + counts[d]])
+            assert bool((recv[d][c][: offs[d]] == -1).all()) and bool((recv[d][c][offs[d] + counts[d]:] == -1).all())
+        start += counts[d]
+    assert sum(counts) == w.rows
+
+
+def test_ipc_handle_carries_the_offset_in_its_allocation():
+    """Receive columns come from torch's caching allocator (pointers inside
+    larger segments): the IPC handle names the segment, plus the offset."""
+    import struct
+    from paper_2010_00152_b200 import _native
+    buf = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    a, b = buf[4096:], buf[65536:]
+    ha, hb = _native.ipc_handle(a.data_ptr()), _native.ipc_handle(b.data_ptr())
+    assert len(ha) == 72 and ha[:64] == hb[:64]
+    off_a, off_b = struct.unpack("<Q", ha[64:])[0], struct.unpack("<Q", hb[64:])[0]
+    assert off_b - off_a == 65536 - 4096

@@ -133,3 +133,12 @@ def test_choose_splitters_unsigned_order():
     got = sl.numpy().view(np.uint64).tolist()
     assert got == sorted(got)
     assert got[0] <= 2**63 <= got[1] or got == [7, 2**63 + 3] or got[0] >= 5
+
+
+def test_p2p_offsets_layout():
+    """Receive blocks are laid out in source-rank order."""
+    from paper_2010_00152_b200.parallel import p2p_offsets
+    m = [[3, 1, 0], [2, 2, 5], [0, 4, 1]]   # m[src][dst]
+    assert p2p_offsets(m, 0) == [0, 0, 0]
+    assert p2p_offsets(m, 1) == [3, 1, 0]
+    assert p2p_offsets(m, 2) == [5, 3, 5]
