@@ -318,17 +318,23 @@ def _torch():
     return torch
 
 
+_DTYPE_CODES = None
+
+
 def _isa_dtype(t):
-    torch = _torch()
-    table = {
-        torch.uint8: _native.U8, torch.int8: _native.I8, torch.int16: _native.I16,
-        torch.int32: _native.I32, torch.int64: _native.I64, torch.float32: _native.F32,
-        torch.float64: _native.F64,
-    }
-    for name, code in (("uint16", _native.U16), ("uint32", _native.U32), ("uint64", _native.U64)):
-        if hasattr(torch, name):
-            table[getattr(torch, name)] = code
-    code = table.get(t.dtype)
+    global _DTYPE_CODES
+    if _DTYPE_CODES is None:
+        torch = _torch()
+        table = {
+            torch.uint8: _native.U8, torch.int8: _native.I8, torch.int16: _native.I16,
+            torch.int32: _native.I32, torch.int64: _native.I64, torch.float32: _native.F32,
+            torch.float64: _native.F64,
+        }
+        for name, code in (("uint16", _native.U16), ("uint32", _native.U32), ("uint64", _native.U64)):
+            if hasattr(torch, name):
+                table[getattr(torch, name)] = code
+        _DTYPE_CODES = table
+    code = _DTYPE_CODES.get(t.dtype)
     if code is None:
         raise InvalidInputError(f"unsupported column dtype {t.dtype}")
     return code
@@ -416,6 +422,9 @@ class SortAggregate:
     def _device_index(self):
         torch = _torch()
         if self._device is not None:
+            idx = getattr(self._device, "index", None)
+            if idx is not None:
+                return idx
             d = torch.device(self._device)
             return d.index if d.index is not None else torch.cuda.current_device()
         return torch.cuda.current_device()
