@@ -20,6 +20,8 @@
 // then every column's payload words (word_off counted from the payload).
 #include "isa_kernels.h"
 
+#include <atomic>
+
 namespace isa {
 
 #define PK_THREADS 256
@@ -125,6 +127,157 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack_write(PackSrc p, const u64*
       wout[q] = word;
     }
   }
+}
+
+// Single-pass packing: every CTA takes the next block (atomic ticket),
+// stages its rows of every column in shared memory with coalesced reads
+// (state slots are AoS: one flat read of the block's records), reduces all
+// columns' min/max at once, learns its byte offset by decoupled look-back
+// over the previous blocks' sizes, and writes header + payload.  Replaces
+// sizes -> scan -> write (three passes, two reads of the run) when the
+// columns fit the shared-memory stage.
+#define PKF_MAXC 8
+__device__ __forceinline__ u64 pkf_ld(const u64* p) {
+  u64 v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void pkf_st(u64* p, u64 v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(PK_THREADS) k_pack_fused(PackSrc p, u64* __restrict__ status, u32 epoch,
+                                                           u32* __restrict__ ticket, u32* __restrict__ blk_off,
+                                                           char* __restrict__ out) {
+  extern __shared__ __align__(16) u64 stage[];   // [ncol][PK_ROWS]
+  __shared__ u64 s_mn[PK_THREADS / 32][PKF_MAXC], s_mx[PK_THREADS / 32][PKF_MAXC];
+  __shared__ u64 s_base[PKF_MAXC];
+  __shared__ u32 s_width[PKF_MAXC], s_woff[PKF_MAXC], s_b, s_off;
+  const int ncol = pk_ncol(p.kw, p.S);
+  const u32 nblk = (p.n + PK_ROWS - 1) / PK_ROWS;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) s_b = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const u32 b = s_b, r0 = b * PK_ROWS;
+  const u32 rows = min((u32)PK_ROWS, p.n - r0);
+  // 1. stage (transformed values)
+  for (u32 i = tid; i < rows; i += PK_THREADS) {
+    stage[i] = p.lo[r0 + i];
+    if (p.kw == 2) stage[PK_ROWS + i] = p.hi[r0 + i];
+  }
+  if (p.S) {
+    const u64* src = p.st + (size_t)r0 * p.S;
+    for (u32 j = tid; j < rows * (u32)p.S; j += PK_THREADS) {
+      const u32 i = j / p.S, s_ = j % p.S;
+      stage[(size_t)(p.kw + s_) * PK_ROWS + i] = pk_fwd(src[j], (p.fmask >> s_) & 1u, 0);
+    }
+  }
+  __syncthreads();
+  // 2. min / max of every column
+  u64 mn[PKF_MAXC], mx[PKF_MAXC];
+#pragma unroll
+  for (int c = 0; c < PKF_MAXC; ++c) { mn[c] = ~0ull; mx[c] = 0; }
+  for (u32 i = tid; i < rows; i += PK_THREADS) {
+#pragma unroll
+    for (int c = 0; c < PKF_MAXC; ++c) {
+      if (c < ncol) {
+        const u64 v = stage[(size_t)c * PK_ROWS + i];
+        mn[c] = v < mn[c] ? v : mn[c];
+        mx[c] = v > mx[c] ? v : mx[c];
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < PKF_MAXC; ++c) {
+    for (int o = 16; o; o >>= 1) {
+      const u64 a = __shfl_xor_sync(0xffffffffu, mn[c], o), z = __shfl_xor_sync(0xffffffffu, mx[c], o);
+      mn[c] = a < mn[c] ? a : mn[c];
+      mx[c] = z > mx[c] ? z : mx[c];
+    }
+    if (lane == 0) { s_mn[w][c] = mn[c]; s_mx[w][c] = mx[c]; }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    u64 woff = 0;
+    for (int c = 0; c < ncol; ++c) {
+      u64 a = s_mn[0][c], z = s_mx[0][c];
+      for (int ww = 1; ww < PK_THREADS / 32; ++ww) {
+        a = s_mn[ww][c] < a ? s_mn[ww][c] : a;
+        z = s_mx[ww][c] > z ? s_mx[ww][c] : z;
+      }
+      const u32 width = z == a ? 0u : (u32)(64 - __clzll((long long)(z - a)));
+      s_base[c] = a;
+      s_width[c] = width;
+      s_woff[c] = (u32)woff;
+      woff += ((u64)rows * width + 63) / 64;
+    }
+    const u32 bytes = (u32)((ncol * 2 + woff) * 8);
+    // 3. decoupled look-back over the previous blocks' byte counts
+    const u64 E = (u64)epoch << 34;
+    u32 excl = 0;
+    if (b == 0) {
+      pkf_st(status, E | (2ull << 32) | bytes);
+    } else {
+      pkf_st(status + b, E | (1ull << 32) | bytes);
+      for (int j = (int)b - 1;;) {
+        const u64 x = pkf_ld(status + j);
+        if ((x >> 34) != (u64)epoch) continue;
+        excl += (u32)x;
+        if (((x >> 32) & 3u) == 2u) break;
+        --j;
+      }
+      pkf_st(status + b, E | (2ull << 32) | (excl + bytes));
+    }
+    s_off = excl;
+    blk_off[b] = excl;
+    if (b == nblk - 1) blk_off[nblk] = excl + bytes;
+  }
+  __syncthreads();
+  // 4. header + payload at the block's offset
+  u64* blk = (u64*)(out + s_off);
+  if (tid < ncol) {
+    blk[tid * 2] = s_base[tid];
+    blk[tid * 2 + 1] = (u64)s_width[tid] | ((u64)s_woff[tid] << 8);
+  }
+  u64* payload = blk + ncol * 2;
+  for (int c = 0; c < ncol; ++c) {
+    const u32 width = s_width[c];
+    if (width == 0) continue;
+    const u64 base = s_base[c];
+    const u64* vals = stage + (size_t)c * PK_ROWS;
+    u64* wout = payload + s_woff[c];
+    const u32 nwords = (u32)(((u64)rows * width + 63) / 64);
+    for (u32 q = tid; q < nwords; q += PK_THREADS) {
+      const u64 lo_bit = (u64)q * 64;
+      const u32 i0 = (u32)(lo_bit / width);
+      const u32 i1 = min(rows - 1, (u32)((lo_bit + 63) / width));
+      u64 word = 0;
+      for (u32 i = i0; i <= i1; ++i) {
+        const long long pos = (long long)((u64)i * width) - (long long)lo_bit;
+        const u64 v = vals[i] - base;
+        word |= pos >= 0 ? (v << pos) : (v >> (-pos));
+      }
+      wout[q] = word;
+    }
+  }
+}
+
+bool pack_fused_ok(const PackSrc& p) { return pk_ncol(p.kw, p.S) <= PKF_MAXC; }
+
+static std::atomic<u32> g_pk_epoch{0};
+
+void pack_fused(const PackSrc& p, u64* status, u32* ticket, u32* blk_off, char* out, cudaStream_t st) {
+  const u32 nb = pack_blocks(p.n);
+  if (!nb) return;
+  const size_t smem = (size_t)pk_ncol(p.kw, p.S) * PK_ROWS * 8;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_pack_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, PKF_MAXC * PK_ROWS * 8);
+    attr = true;
+  }
+  const u32 ep = (g_pk_epoch.fetch_add(1) % 0x3FFFFFFEu) + 1u;
+  cudaMemsetAsync(ticket, 0, sizeof(u32), st);
+  klaunch(k_pack_fused, nb, PK_THREADS, smem, st, p, status, ep, ticket, blk_off, out);
 }
 
 u32 pack_blocks(u32 n) { return (n + PK_ROWS - 1) / PK_ROWS; }

@@ -228,7 +228,7 @@ struct Engine {
   DevBuf stg_lo[2], stg_hi[2], stg_st[2];
   cudaEvent_t stg_ready[2] = {nullptr, nullptr}, stg_free[2] = {nullptr, nullptr};
   DevBuf runref_dev, bounds_lo, bounds_hi, bounds_out;
-  DevBuf pk_hdr, pk_sz;                     // codec: block headers, block byte sizes -> offsets
+  DevBuf pk_hdr, pk_sz, pk_status;          // codec: block headers, byte sizes -> offsets, look-back words
   DevBuf stg_pk[2], stg_desc[2];            // wide merge: packed bytes and unpack descriptors per slot
   std::vector<UnpackBlk> desc_host[2];
   UnpackBlk* desc_pinned[2] = {nullptr, nullptr};
@@ -324,7 +324,7 @@ struct Engine {
                       &mg_rank_b, &mg_match_b, &ab_partials, &ab_miss_buf, &ab_miss_cnt, &ab_miss_off,
                       &miss_list, &stg_lo[0], &stg_lo[1], &stg_hi[0], &stg_hi[1], &stg_st[0], &stg_st[1],
                       &runref_dev, &bounds_lo, &bounds_hi, &bounds_out, &out_tmp, &pk_hdr, &pk_sz,
-                      &stg_pk[0], &stg_pk[1], &stg_desc[0], &stg_desc[1], &t_backup};
+                      &stg_pk[0], &stg_pk[1], &stg_desc[0], &stg_desc[1], &t_backup, &pk_status};
     for (int i = 0; i < 2; ++i) {
       if (desc_pinned[i]) cudaFreeHost(desc_pinned[i]);
       if (desc_done[i]) cudaEventDestroy(desc_done[i]);
@@ -713,17 +713,31 @@ struct Engine {
     PackSrc ps{t.plo(), t.phi(), t.pst(), t.n, KW, S, fmask};
     const u32 nblk = pack_blocks(t.n);
     const int ncol = KW + S;
-    pk_hdr.ensure((size_t)nblk * ncol * 16 + 16);
-    pk_sz.ensure((size_t)(nblk + 1) * 4 + 16);
-    scan_tmp.ensure((scan_tmp_words(nblk + 1) + 64) * 4);
-    pack_sizes(ps, pk_hdr.as<u64>(), pk_sz.as<u32>(), st);
-    scan_exclusive_u32(pk_sz.as<u32>(), nblk, scan_tmp.as<u32>(), pk_sz.as<u32>() + nblk, st);
-    const u32 bytes = read_u32(pk_sz.as<u32>() + nblk);   // offsets[nblk] = total
+    pk_sz.ensure((size_t)(nblk + 2) * 4 + 16);
+    u32 bytes = 0;
+    size_t off_at = 0;
+    if (pack_fused_ok(ps)) {
+      // one pass; the output is bounded by the raw size
+      const size_t bound = (size_t)nblk * ncol * 16 + (size_t)t.n * ncol * 8 + 64;
+      t.pk.ensure(bound + (size_t)(nblk + 1) * 4 + 32);
+      const size_t had = pk_status.bytes;
+      pk_status.ensure((size_t)nblk * 8 + 16);
+      if (pk_status.bytes != had) CK(cudaMemsetAsync(pk_status.p, 0, pk_status.bytes, st));   // epochs start at 0
+      pack_fused(ps, pk_status.as<u64>(), pk_sz.as<u32>() + nblk + 1, pk_sz.as<u32>(), t.pk.as<char>(), st);
+      bytes = read_u32(pk_sz.as<u32>() + nblk);   // offsets[nblk] = total
+      off_at = ((size_t)bytes + 15) & ~(size_t)15;
+    } else {
+      pk_hdr.ensure((size_t)nblk * ncol * 16 + 16);
+      scan_tmp.ensure((scan_tmp_words(nblk + 1) + 64) * 4);
+      pack_sizes(ps, pk_hdr.as<u64>(), pk_sz.as<u32>(), st);
+      scan_exclusive_u32(pk_sz.as<u32>(), nblk, scan_tmp.as<u32>(), pk_sz.as<u32>() + nblk, st);
+      bytes = read_u32(pk_sz.as<u32>() + nblk);   // offsets[nblk] = total
+      off_at = ((size_t)bytes + 15) & ~(size_t)15;
+      t.pk.ensure(off_at + (size_t)(nblk + 1) * 4 + 16);
+      pack_write(ps, pk_hdr.as<u64>(), pk_sz.as<u32>(), t.pk.as<char>(), st);
+    }
     // packed blocks, then the block offsets: both owned by the table until
     // its D2H copies are done (pk_sz is reused by the next spill)
-    const size_t off_at = ((size_t)bytes + 15) & ~(size_t)15;
-    t.pk.ensure(off_at + (size_t)(nblk + 1) * 4 + 16);
-    pack_write(ps, pk_hdr.as<u64>(), pk_sz.as<u32>(), t.pk.as<char>(), st);
     CK(cudaMemcpyAsync(t.pk.as<char>() + off_at, pk_sz.p, (size_t)(nblk + 1) * 4, cudaMemcpyDeviceToDevice, st));
     Run r;
     r.rows = t.n;

@@ -134,6 +134,11 @@ u32 pack_blocks(u32 n);
 // per-block headers (ncol x 2 u64) and byte sizes
 void pack_sizes(const PackSrc& p, u64* hdr, u32* blk_bytes, cudaStream_t st);
 void pack_write(const PackSrc& p, const u64* hdr, const u32* blk_off, char* out, cudaStream_t st);
+// single pass (staged columns + look-back offsets) when <= 8 columns:
+// blk_off[nblk + 1] receives the offsets and the total; status = nblk look-back
+// words that were zero when allocated (pass epochs keep them valid after)
+bool pack_fused_ok(const PackSrc& p);
+void pack_fused(const PackSrc& p, u64* status, u32* ticket, u32* blk_off, char* out, cudaStream_t st);
 void unpack_blocks(const UnpackBlk* d, u32 nd, const char* src, int kw, int S, u32 fmask, u64* lo, u64* hi, u64* st,
                    cudaStream_t stream);
 
