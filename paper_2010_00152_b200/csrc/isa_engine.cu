@@ -182,6 +182,13 @@ struct Engine {
   DevBuf s_lo[2], s_hi[2], s_val[2], tile_hist, scan_tmp;
   DevBuf scal;   // small device scalars (u64 varying[2], u32 counters)
   u32* h_scal = nullptr;   // pinned, mapped mirror (64 u64 words)
+  u32* h_hist = nullptr;   // pinned, mapped: radix histograms for the ranking choice
+  // per-execute cache of the onesweep ranking choice, per sort context
+  // (0: run-generation chunks, 1: wide-merge windows / other)
+  struct RankHint { signed char h[16]; int bit_lo = -1, npass = 0; };
+  RankHint rank_hint[2];
+  int sort_ctx = 1;
+  u32* d_hist_mapped = nullptr;
   u32* d_scal_mapped = nullptr;
   // device -> h_scal through a kernel (see read_words)
   void to_host(const void* dsrc, size_t bytes, size_t host_word_off = 0) {
@@ -312,6 +319,8 @@ struct Engine {
       CK(cudaEventCreateWithFlags(&win[i].ready, cudaEventDisableTiming));
     }
     CK(cudaHostAlloc((void**)&h_scal, 64 * sizeof(u64), cudaHostAllocMapped));
+    CK(cudaHostAlloc((void**)&h_hist, 16 * 256 * sizeof(u32), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer((void**)&d_hist_mapped, h_hist, 0));
     CK(cudaHostGetDevicePointer((void**)&d_scal_mapped, h_scal, 0));
     scal.ensure(64 * sizeof(u64));
     memset(&led, 0, sizeof(led));
@@ -346,6 +355,7 @@ struct Engine {
     pinned.release();
     devpool.release();
     if (h_scal) cudaFreeHost(h_scal);
+    if (h_hist) cudaFreeHost(h_hist);
     if (h2d) cudaStreamDestroy(h2d);
     if (d2h) cudaStreamDestroy(d2h);
     if (spill_done) cudaEventDestroy(spill_done);
@@ -509,7 +519,9 @@ struct Engine {
     ph_begin(ISA_PH_SORT);
     CK(cudaMemsetAsync(dvary(), 0, 2 * sizeof(u64), st));
     build_keys(KW, kd, row0, pos, m, s_lo[0].as<u64>(), s_hi[0].as<u64>(), s_val[0].as<u32>(), dvary(), st);
+    sort_ctx = 0;
     int cur = sort_built(m);
+    sort_ctx = 1;
     ph_end(ISA_PH_SORT, m, 0);
     return cur;
   }
@@ -535,6 +547,16 @@ struct Engine {
     SortBufs b;
     for (int i = 0; i < 2; ++i) { b.lo[i] = s_lo[i].as<u64>(); b.hi[i] = s_hi[i].as<u64>(); b.val[i] = s_val[i].as<u32>(); }
     b.aux = tile_hist.p;
+    b.map_dev = d_hist_mapped;
+    b.map_host = h_hist;
+    RankHint& rh = rank_hint[sort_ctx];
+    b.hint = rh.h;
+    b.hint_bit_lo = rh.bit_lo;
+    b.hint_npass = rh.npass;
+    struct HintBack {   // copy the (possibly updated) choice back on every return path
+      RankHint& rh; SortBufs& b;
+      ~HintBack() { rh.bit_lo = b.hint_bit_lo; rh.npass = b.hint_npass; }
+    } hint_back{rh, b};
     if (KW == 2 && hb >= 64 && lb < 64) {
       // 128-bit keys whose high word varies: sort on the high word, then
       // finish runs of equal high words with a stable sort on the low word
@@ -1614,6 +1636,7 @@ struct Engine {
     const long long launch0 = g_launches.load();
     if (n < 0) throw IsaError(ISA_ERR_INVALID_INPUT, "negative row count");
     steps.clear();
+    for (auto& rh : rank_hint) { memset(rh.h, 0xFF, sizeof(rh.h)); rh.bit_lo = -1; rh.npass = 0; }
     led.rows_seen = n;
     if (n == 0) { led.kernel_launches = 0; return 0; }
     if (cfg.merge_mode != ISA_MERGE_WIDE) {

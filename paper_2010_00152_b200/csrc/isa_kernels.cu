@@ -7,8 +7,10 @@
 #include "isa_kernels.h"
 #include <cstdio>
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <stdexcept>
+#include <vector>
 
 namespace isa {
 
@@ -138,7 +140,7 @@ __device__ __forceinline__ void st_relaxed_gpu(u64* p, u64 v) {
 // Status word per (tile, digit): count | flag << 32 (1 aggregate, 2
 // inclusive prefix) | epoch << 34; words of other passes carry another epoch
 // and read as "not published yet", so the array is never cleared.
-template <int KW>
+template <int KW, bool BALLOT>
 __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : 3) k_rs_scatter(const u64* __restrict__ lo_in, const u64* __restrict__ hi_in,
                                                          const u32* __restrict__ v_in, u64* __restrict__ lo_out,
                                                          u64* __restrict__ hi_out, u32* __restrict__ v_out, u32 n,
@@ -179,7 +181,21 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : 3) k_rs_scatter(cons
     u32 li = w * RS_WARP_ITEMS + it * 32 + lane;
     bool valid = li < tile_n;
     u32 d = valid ? digit_of(hi[it], lo[it], shift) : 256 + lane;
-    u32 peers = __match_any_sync(0xffffffffu, d);
+    // lanes holding the same digit: MATCH.ANY, or (BALLOT: chosen by the
+    // host for large passes whose digits are not skewed) eight independent
+    // ballots -- data-independent cost, measured faster on uniform digits
+    u32 peers;
+    if (!BALLOT) {
+      peers = __match_any_sync(0xffffffffu, d);
+    } else {
+      peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const u32 bits = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? bits : ~bits;
+      }
+      if (!valid) peers = 1u << lane;
+    }
     int leader = __ffs(peers) - 1;
     u32 cnt = 0;
     if (valid && lane == leader) {
@@ -298,10 +314,13 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
   if (n <= 1 || bit_hi <= bit_lo) return cur;
   static bool attr_set[3] = {false, false, false};
   if (!attr_set[KW]) {
-    if (KW == 2)
-      cudaFuncSetAttribute(k_rs_scatter<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_scatter_smem(2));
-    else
-      cudaFuncSetAttribute(k_rs_scatter<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_scatter_smem(1));
+    if (KW == 2) {
+      cudaFuncSetAttribute(k_rs_scatter<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_scatter_smem(2));
+      cudaFuncSetAttribute(k_rs_scatter<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_scatter_smem(2));
+    } else {
+      cudaFuncSetAttribute(k_rs_scatter<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_scatter_smem(1));
+      cudaFuncSetAttribute(k_rs_scatter<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_scatter_smem(1));
+    }
     attr_set[KW] = true;
   }
   const u32 ntiles = (n + RS_TILE - 1) / RS_TILE;
@@ -317,6 +336,38 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
     if (KW == 2) klaunch(k_rs_hist_all<2>, g, 256, 0, st, b.lo[cur], b.hi[cur], n, bit_lo, npass, ghist);
     else klaunch(k_rs_hist_all<1>, g, 256, 0, st, b.lo[cur], (const u64*)nullptr, n, bit_lo, npass, ghist);
   }
+  // ranking per pass: ballots for large passes without heavy digits (one
+  // small read-back of the histograms; MATCH.ANY otherwise)
+  bool ballot[RS_MAX_PASS] = {};
+  static int mode = -2;
+  if (mode == -2) {
+    const char* e = getenv("ISA_RANK");
+    mode = !e ? -1 : (e[0] == 'm' ? 0 : (e[0] == 'b' ? 1 : -1));
+  }
+  if (mode >= 0) {
+    for (int p = 0; p < npass; ++p) ballot[p] = mode == 1 && ntiles > 1;
+  }
+  const bool hinted = mode >= 0 || (b.hint && b.hint[0] >= 0 && b.hint_bit_lo == bit_lo && b.hint_npass == npass);
+  if (hinted) {
+    if (mode < 0)
+      for (int p = 0; p < npass; ++p) ballot[p] = b.hint[p] != 0;
+  } else if (ntiles >= 64 && b.map_dev) {
+    // through mapped host memory by a kernel: a copy-engine read would queue
+    // behind the spill copies on the D2H engine
+    read_words(b.map_dev, ghist, (u32)npass * 256, st);
+    cudaStreamSynchronize(st);
+    const volatile u32* hh = b.map_host;
+    for (int p = 0; p < npass; ++p) {
+      u32 mx = 0;
+      for (int d = 0; d < 256; ++d) mx = std::max(mx, (u32)hh[(size_t)p * 256 + d]);
+      ballot[p] = (u64)mx * 32 <= (u64)n;   // no digit holds more than 1/32 of the keys
+    }
+    if (b.hint) {   // later sorts of the same kind reuse the choice (no read-back)
+      for (int p = 0; p < npass; ++p) b.hint[p] = ballot[p] ? 1 : 0;
+      b.hint_bit_lo = bit_lo;
+      b.hint_npass = npass;
+    }
+  }
   for (int p = 0; p < npass; ++p) {
     const int shift = bit_lo + 8 * p;
     const int nxt = cur ^ 1;
@@ -325,12 +376,17 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
     const u32* gh = one ? nullptr : ghist + p * 256;
     u32* tc = one ? nullptr : tctr + p;
     const u32 ep = one ? 0u : ((g_rs_epoch.fetch_add(1) % 0x3FFFFFFEu) + 1u);
-    if (KW == 2)
-      klaunch(k_rs_scatter<2>, ntiles, RS_THREADS, smem, st, b.lo[cur], b.hi[cur], b.val[cur], b.lo[nxt], b.hi[nxt],
-              b.val[nxt], n, shift, stt, gh, tc, ep);
-    else
-      klaunch(k_rs_scatter<1>, ntiles, RS_THREADS, smem, st, b.lo[cur], (const u64*)nullptr, b.val[cur], b.lo[nxt],
-              (u64*)nullptr, b.val[nxt], n, shift, stt, gh, tc, ep);
+#define RS_GO(K, BL, HI_IN, HI_OUT)                                                                          \
+  klaunch(k_rs_scatter<K, BL>, ntiles, RS_THREADS, smem, st, b.lo[cur], HI_IN, b.val[cur], b.lo[nxt], HI_OUT, \
+          b.val[nxt], n, shift, stt, gh, tc, ep)
+    if (KW == 2) {
+      if (ballot[p]) RS_GO(2, true, b.hi[cur], b.hi[nxt]);
+      else RS_GO(2, false, b.hi[cur], b.hi[nxt]);
+    } else {
+      if (ballot[p]) RS_GO(1, true, (const u64*)nullptr, (u64*)nullptr);
+      else RS_GO(1, false, (const u64*)nullptr, (u64*)nullptr);
+    }
+#undef RS_GO
     if (launches) *launches += 1;
     cur = nxt;
   }

@@ -20,6 +20,10 @@ struct SortBufs {
   u64* hi[2];
   u32* val[2];
   void* aux;        // sort_aux_bytes(n): look-back status, histograms, tile counters (zeroed when allocated)
+  u32* map_dev = nullptr;          // mapped pinned host words (>= 16 * 256), device view
+  const u32* map_host = nullptr;   // ... and host view (per-pass histograms for the ranking choice)
+  signed char* hint = nullptr;     // [16] cached ranking choice per pass (hint[0] < 0: none yet)
+  int hint_bit_lo = -1, hint_npass = 0;
 };
 size_t sort_aux_bytes(u32 n);
 int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStream_t st, int64_t* launches,
