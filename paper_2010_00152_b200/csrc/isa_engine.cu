@@ -616,8 +616,9 @@ struct Engine {
   size_t tcap = 1;   // capacity of every run-generation table: min(M, n) + 1
 
   // U <- collapse(sorted chunk restricted to positions < limit)
+  // known_n >= 0: the caller knows the group count (no host round trip)
   void collapse_chunk(int cur, u32 m, u32 limit, const SlotDesc& sd, int64_t row0, const u64* st_in, Table& out,
-                      size_t out_cap, bool merge_phase = true) {
+                      size_t out_cap, bool merge_phase = true, int64_t known_n = -1) {
     ensure_collapse(m);
     out.reserve(out_cap, KW, S);
     CollapseTmp ct;
@@ -630,6 +631,11 @@ struct Engine {
     ph_begin(phc);
     collapse(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, limit, sd, row0, st_in,
              out.plo(), out.phi(), out.pst(), ct, st);
+    if (known_n >= 0) {
+      ph_end(phc, m, 0);
+      out.n = (u32)known_n;
+      return;
+    }
     to_host(dscal32(2), sizeof(u32));
     ph_end(phc, m, 0);
     sync();
@@ -960,8 +966,12 @@ struct Engine {
     const u32 k1_min = (cfg.preaggregate == 1 ? 4 : 64) * tile_rows();
     if (k1_mode != 0 && span >= k1_min) return k1_chunk(kd, sd, row0, a, span);
     int cur = sort_rows(kd, row0, nullptr, span);
+    const bool t_empty = T.n == 0;
     u32 f = flush_point(cur, span, span);
-    collapse_chunk(cur, span, f, sd, row0, nullptr, U, tcap);
+    // with T empty every group of the chunk before f is new: M of them on a
+    // flush, else the new-key count the flush analysis already returned
+    const int64_t known = t_empty ? (f < span ? cfg.memory_budget : (int64_t)last_new) : -1;
+    collapse_chunk(cur, span, f, sd, row0, nullptr, U, tcap, true, known);
     merge_into_T();
     if (f < span) {
       spill_T();
