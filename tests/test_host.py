@@ -203,3 +203,24 @@ def test_filestore_mirror_page_index(tmp_path):
     assert fs._offsets[1] == [(0, 124), (124, 124), (248, 12 + 16 + 2 * 24)]
     assert fs._offsets[2] == [(0, 12 + 16 + 3 * 24)]
     assert os.path.basename(fs._path(2)) == "run_000002.bin"
+
+
+def test_config_knobs_validated():
+    for kw, msg in (({"run_codec": "zstd"}, "run codec"), ({"run_tier": "nvme"}, "run tier"),
+                    ({"preaggregate": "maybe"}, "preaggregate")):
+        with pytest.raises(isa.InvalidInputError, match=msg):
+            cfg(64, 8, **kw)
+    assert cfg(64, 8).run_codec == "auto"
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_downstream_needs_the_gpu():
+    from paper_2010_00152_b200 import downstream
+    sch = isa.Schema([isa.ColumnSpec("k")], [isa.AggregateSpec("n", isa.AggregateKind.COUNT)])
+    rows = [isa.Row((1,), (1,)), isa.Row((2,), (1,))]
+    with pytest.raises(isa.ResourceError):
+        list(downstream.in_stream_aggregate(rows, sch))
+    with pytest.raises(isa.ResourceError):
+        downstream.merge_intersect(rows, rows)
+    assert list(downstream.in_stream_aggregate([], sch)) == []
+    assert downstream.merge_intersect([], rows) == []
