@@ -573,6 +573,17 @@ struct Engine {
   // Flush analysis on a sorted chunk of `span` rows: number of keys absent
   // from T; if |T| + new > M returns the chunk-relative flush row, else span.
   u32 flush_point(int cur, u32 m, u32 span, const u32* firstpos = nullptr) {
+    if (!firstpos && flush_small_ok(span)) {
+      const u32 k = (u32)(cfg.memory_budget - (int64_t)T.n + 1);   // >= 1: |T| <= M
+      ph_begin(ISA_PH_FLUSH);
+      flush_small(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, T.plo(), T.phi(), T.n, span,
+                  k, d_scal_mapped, st);
+      ph_end(ISA_PH_FLUSH, m, 0);
+      sync();
+      const u32 n_new = ((volatile u32*)h_scal)[0], f = ((volatile u32*)h_scal)[1];
+      last_new = n_new;
+      return (int64_t)T.n + n_new <= cfg.memory_budget ? span : f;
+    }
     u32 nw = (span + 31) / 32;
     bitmap.ensure((size_t)nw * 4 + 4);
     word_tmp.ensure((size_t)nw * 4 + 4);

@@ -539,6 +539,89 @@ __global__ void k_new_heads(const u64* __restrict__ lo, const u64* __restrict__ 
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(n_new, cnt);
 }
 
+// Small chunks (span <= FS_MAX_BITS): the whole flush analysis in one CTA --
+// new heads into a shared-memory bitmap, their count, and the k-th set bit
+// (the flush row) -- written straight to mapped host memory: out[0] = new
+// keys, out[1] = flush row (span when fewer than k).
+#define FS_THREADS 1024
+#define FS_MAX_BITS 32768
+template <int KW>
+__global__ void __launch_bounds__(FS_THREADS) k_flush_small(const u64* __restrict__ lo, const u64* __restrict__ hi,
+                                                          const u32* __restrict__ val, u32 m,
+                                                          const u64* __restrict__ T_lo, const u64* __restrict__ T_hi,
+                                                          u32 t, u32 span, u32 k, u32* out) {
+  __shared__ u32 bm[FS_MAX_BITS / 32];
+  __shared__ u32 sw[FS_THREADS / 32];
+  const u32 nw = (span + 31) / 32;
+  for (u32 i = threadIdx.x; i < nw; i += FS_THREADS) bm[i] = 0;
+  __syncthreads();
+  for (u32 i = threadIdx.x; i < m; i += FS_THREADS) {
+    const u64 l = lo[i], h = KW == 2 ? hi[i] : 0;
+    if (i > 0 && key_eq<KW>(h, l, KW == 2 ? hi[i - 1] : 0, lo[i - 1])) continue;
+    bool in_t = false;
+    if (t) {
+      const u32 p = lower_bound_key<KW>(T_lo, T_hi, t, h, l);
+      in_t = p < t && key_eq<KW>(KW == 2 ? T_hi[p] : 0, T_lo[p], h, l);
+    }
+    if (!in_t) {
+      const u32 pos = val[i];
+      atomicOr(&bm[pos >> 5], 1u << (pos & 31));
+    }
+  }
+  __syncthreads();
+  // words per thread: contiguous ranges so the prefix follows bit order
+  const u32 per = (nw + FS_THREADS - 1) / FS_THREADS;
+  const u32 w0 = threadIdx.x * per, w1 = min(nw, w0 + per);
+  u32 c = 0;
+  for (u32 w = w0; w < w1; ++w) c += __popc(bm[w]);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  u32 x = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sw[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    u32 v = sw[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    sw[lane] = v;
+  }
+  __syncthreads();
+  const u32 total = sw[FS_THREADS / 32 - 1];
+  u32 pre = (wid ? sw[wid - 1] : 0) + x - c;   // exclusive prefix of this thread's words
+  if (threadIdx.x == 0) {
+    ((volatile u32*)out)[0] = total;
+    if (total < k) ((volatile u32*)out)[1] = span;
+  }
+  if (k >= 1 && pre < k && pre + c >= k) {
+    for (u32 w = w0; w < w1; ++w) {
+      const u32 word = bm[w], pc = __popc(word);
+      if (pre + pc >= k) {
+        u32 need = k - pre, bits = word;
+        for (;;) {
+          const int b = __ffs(bits) - 1;
+          if (--need == 0) { ((volatile u32*)out)[1] = w * 32 + b; break; }
+          bits &= bits - 1;
+        }
+        break;
+      }
+      pre += pc;
+    }
+  }
+}
+
+bool flush_small_ok(u32 span) { return span <= FS_MAX_BITS; }
+
+void flush_small(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, const u64* T_lo, const u64* T_hi, u32 t,
+                 u32 span, u32 k, u32* out_mapped, cudaStream_t st) {
+  if (KW == 2) klaunch(k_flush_small<2>, 1, FS_THREADS, 0, st, lo, hi, val, m, T_lo, T_hi, t, span, k, out_mapped);
+  else klaunch(k_flush_small<1>, 1, FS_THREADS, 0, st, lo, hi, val, m, T_lo, T_hi, t, span, k, out_mapped);
+}
+
 void new_heads(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, const u64* T_lo, const u64* T_hi,
                u32 t, u32* bitmap, u32* n_new, cudaStream_t st, const u32* firstpos) {
   if (m == 0) return;

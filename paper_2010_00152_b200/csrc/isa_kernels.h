@@ -60,6 +60,11 @@ void new_heads(int KW, const u64* lo, const u64* hi, const u32* val, u32 m,
                const u64* T_lo, const u64* T_hi, u32 t, u32* bitmap, u32* n_new,
                cudaStream_t st, const u32* firstpos = nullptr);
 // position of the k-th (1-based) set bit of bitmap (nbits bits) -> *out
+// whole flush analysis of a small chunk in one CTA: out_mapped[0] = new
+// keys, [1] = row of the k-th new key's first occurrence (span if fewer)
+bool flush_small_ok(u32 span);
+void flush_small(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, const u64* T_lo, const u64* T_hi, u32 t,
+                 u32 span, u32 k, u32* out_mapped, cudaStream_t st);
 void select_kth_bit(const u32* bitmap, u32 nbits, u32 k, u32* word_tmp, u32* scan_tmp,
                     u32* out, cudaStream_t st);
 
