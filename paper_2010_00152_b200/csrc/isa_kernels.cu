@@ -659,6 +659,7 @@ void select_kth_bit(const u32* bitmap, u32 nbits, u32 k, u32* word_tmp, u32* sca
 
 // ========================================================== collapse ====
 #define CL_ITEMS 8
+u32 collapse_threads(u32 m) { return (m + CL_ITEMS - 1) / CL_ITEMS; }
 
 template <int KW>
 __global__ void k_head_flags(const u64* __restrict__ lo, const u64* __restrict__ hi, const u32* __restrict__ val,
