@@ -500,8 +500,8 @@ struct Engine {
   }
   void ensure_collapse(size_t m) {
     cl_flags.ensure((m + 1) * 4);
-    cl_pslot.ensure(((size_t)collapse_threads((u32)m) + 1) * 4);
-    if (S) cl_partial.ensure(((size_t)collapse_threads((u32)m) + 1) * 8 * S);
+    cl_pslot.ensure(((size_t)collapse_threads((u32)m, S) + 1) * 4);
+    if (S) cl_partial.ensure(((size_t)collapse_threads((u32)m, S) + 1) * 8 * S);
     scan_tmp.ensure((scan_tmp_words((u32)m + 1) + 64) * 4);
   }
   void ensure_merge(size_t na, size_t nb) {

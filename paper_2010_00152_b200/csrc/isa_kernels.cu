@@ -658,8 +658,15 @@ void select_kth_bit(const u32* bitmap, u32 nbits, u32 k, u32* word_tmp, u32* sca
 }
 
 // ========================================================== collapse ====
-#define CL_ITEMS 8
-u32 collapse_threads(u32 m) { return (m + CL_ITEMS - 1) / CL_ITEMS; }
+// Consecutive sorted items per segmented-reduce thread: 4 for states of
+// <= 2 slots (measured: config 5's collapse 51 -> 35 ms; more threads keep
+// more random gathers in flight), 8 for wider states (config 3's 5 slots:
+// 4 was 7% slower).
+__host__ __device__ constexpr int cl_items(int MS) { return MS <= 2 ? 4 : 8; }
+u32 collapse_threads(u32 m, int S) {
+  const u32 c = (u32)cl_items(S <= 1 ? 1 : (S <= 2 ? 2 : 4));
+  return (m + c - 1) / c;
+}
 
 template <int KW>
 __global__ void k_head_flags(const u64* __restrict__ lo, const u64* __restrict__ hi, const u32* __restrict__ val,
@@ -702,9 +709,10 @@ __global__ void k_seg_reduce(const u64* __restrict__ lo, const u64* __restrict__
                              u64* __restrict__ out_st, u64* __restrict__ partial, u32* __restrict__ partial_slot) {
   const int S = sd.nslots;
   const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
-  const u32 i0 = t * CL_ITEMS;
+  constexpr u32 CLI = (u32)cl_items(MS);
+  const u32 i0 = t * CLI;
   if (i0 >= m) return;
-  const u32 i1 = min(i0 + CL_ITEMS, m);
+  const u32 i1 = min(i0 + CLI, m);
   u64 acc[MS];
   u64 cur[MS];
 #pragma unroll
@@ -801,7 +809,7 @@ void collapse(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, u32 l
   if (KW == 2) klaunch(k_head_flags<2>, g, 256, 0, st, lo, hi, val, m, limit, tmp.flags);
   else klaunch(k_head_flags<1>, g, 256, 0, st, lo, hi, val, m, limit, tmp.flags);
   scan_exclusive_u32(tmp.flags, m, tmp.scan_tmp, tmp.total, st);
-  u32 nthreads = (m + CL_ITEMS - 1) / CL_ITEMS;
+  u32 nthreads = collapse_threads(m, sd.nslots);
   int blocks = (nthreads + 127) / 128;
   const int S = sd.nslots;
 #define SR_LAUNCH(K, M) klaunch(k_seg_reduce<K, M>, blocks, 128, 0, st, lo, hi, val, m, limit, sd, row0, st_in, \

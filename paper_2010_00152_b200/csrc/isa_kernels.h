@@ -81,7 +81,7 @@ struct CollapseTmp {
   u32* total;      // 1 (device)
 };
 // segmented-reduce threads for m items (per-thread partial-state buffers)
-u32 collapse_threads(u32 m);
+u32 collapse_threads(u32 m, int S);
 void collapse(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, u32 limit,
               const SlotDesc& sd, int64_t row0, const u64* st_in,
               u64* out_lo, u64* out_hi, u64* out_st, CollapseTmp& tmp, cudaStream_t st);
