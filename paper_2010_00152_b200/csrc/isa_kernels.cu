@@ -664,7 +664,7 @@ void select_kth_bit(const u32* bitmap, u32 nbits, u32 k, u32* word_tmp, u32* sca
 // 4 was 7% slower).
 __host__ __device__ constexpr int cl_items(int MS) { return MS <= 2 ? 4 : 8; }
 u32 collapse_threads(u32 m, int S) {
-  const u32 c = (u32)cl_items(S <= 1 ? 1 : (S <= 2 ? 2 : 4));
+  const u32 c = (u32)cl_items(S <= 1 ? 1 : (S <= 2 ? 2 : (S <= 4 ? 4 : (S <= 5 ? 5 : 8))));
   return (m + c - 1) / c;
 }
 
@@ -815,7 +815,7 @@ void collapse(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, u32 l
 #define SR_LAUNCH(K, M) klaunch(k_seg_reduce<K, M>, blocks, 128, 0, st, lo, hi, val, m, limit, sd, row0, st_in, \
                                 tmp.flags, out_lo, out_hi, out_st, tmp.partial, tmp.partial_slot)
 #define SR_KW(K) { if (S <= 1) SR_LAUNCH(K, 1); else if (S <= 2) SR_LAUNCH(K, 2); else if (S <= 4) SR_LAUNCH(K, 4); \
-                   else if (S <= 8) SR_LAUNCH(K, 8); else SR_LAUNCH(K, 16); }
+                   else if (S <= 5) SR_LAUNCH(K, 5); else if (S <= 8) SR_LAUNCH(K, 8); else SR_LAUNCH(K, 16); }
   if (KW == 2) SR_KW(2) else SR_KW(1)
 #undef SR_KW
 #undef SR_LAUNCH
