@@ -60,6 +60,7 @@ struct SlotDesc {
   int dtype[ISA_MAX_SLOTS];      // dtype of the source column (SRC_COL)
   int alias[ISA_MAX_SLOTS];      // earlier slot reading the same column as the same type, or -1
   const void* ptr[ISA_MAX_SLOTS];
+  int stride[ISA_MAX_SLOTS];     // bytes between rows of ptr (0: the dtype's size; >0: packed row records)
 };
 
 __host__ __device__ __forceinline__ int dtype_bits(int dt) {

@@ -333,7 +333,7 @@ struct Engine {
                       &mg_rank_b, &mg_match_b, &ab_partials, &ab_miss_buf, &ab_miss_cnt, &ab_miss_off,
                       &miss_list, &stg_lo[0], &stg_lo[1], &stg_hi[0], &stg_hi[1], &stg_st[0], &stg_st[1],
                       &runref_dev, &bounds_lo, &bounds_hi, &bounds_out, &out_tmp, &pk_hdr, &pk_sz,
-                      &stg_pk[0], &stg_pk[1], &stg_desc[0], &stg_desc[1], &t_backup, &pk_status};
+                      &stg_pk[0], &stg_pk[1], &stg_desc[0], &stg_desc[1], &t_backup, &pk_status, &rec_buf};
     for (int i = 0; i < 2; ++i) {
       if (desc_pinned[i]) cudaFreeHost(desc_pinned[i]);
       if (desc_done[i]) cudaEventDestroy(desc_done[i]);
@@ -982,7 +982,15 @@ struct Engine {
     // with T empty every group of the chunk before f is new: M of them on a
     // flush, else the new-key count the flush analysis already returned
     const int64_t known = t_empty ? (f < span ? cfg.memory_budget : (int64_t)last_new) : -1;
-    collapse_chunk(cur, span, f, sd, row0, nullptr, U, tcap, true, known);
+    SlotDesc sdc = sd;
+    int64_t r0c = row0;
+    if (f >= (1u << 20) && pack_records(sd, sdc, f)) {
+      // >= 2 value columns: one record per row, so the collapse's random
+      // gather touches one sector per row instead of one per column
+      row_pack(rpk, row0, f, rec_buf.as<char>(), st);
+      r0c = 0;
+    }
+    collapse_chunk(cur, span, f, sdc, r0c, nullptr, U, tcap, true, known);
     merge_into_T();
     if (f < span) {
       spill_T();
@@ -1201,6 +1209,43 @@ struct Engine {
     }
     CK(cudaEventRecord(w.ready, h2d));
     w.staged = true;
+  }
+
+  // Row-record layout for the collapse of a large sort-path chunk: true
+  // (and sdc pointing into rec_buf) when the slots read >= 2 distinct
+  // value columns that fit a 16-byte record.
+  RowPack rpk;
+  DevBuf rec_buf;
+  bool pack_records(const SlotDesc& sd, SlotDesc& sdc, u32 rows) {
+    memset(&rpk, 0, sizeof(rpk));
+    int off = 0;
+    int col_of[ISA_MAX_SLOTS];
+    for (int s = 0; s < S; ++s) {
+      col_of[s] = -1;
+      if (sd.src[s] != SRC_COL || sd.alias[s] >= 0) continue;
+      int found = -1;
+      for (int c = 0; c < rpk.nc; ++c)
+        if (rpk.src[c] == sd.ptr[s]) found = c;
+      if (found < 0) {
+        const int el = dtype_bits(sd.dtype[s]) / 8;
+        off = (off + el - 1) / el * el;
+        rpk.src[rpk.nc] = sd.ptr[s];
+        rpk.elem[rpk.nc] = el;
+        rpk.off[rpk.nc] = off;
+        off += el;
+        found = rpk.nc++;
+      }
+      col_of[s] = found;
+    }
+    if (rpk.nc < 2 || off > 16) return false;
+    rpk.R = off <= 8 ? 8 : 16;
+    rec_buf.ensure((size_t)rows * rpk.R + 64);
+    for (int s = 0; s < S; ++s) {
+      if (col_of[s] < 0) continue;
+      sdc.ptr[s] = rec_buf.as<char>() + rpk.off[col_of[s]];
+      sdc.stride[s] = rpk.R;
+    }
+    return true;
   }
 
   // -------------------------------------------------------- wide merge --

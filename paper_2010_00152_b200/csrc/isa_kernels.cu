@@ -657,6 +657,29 @@ void select_kth_bit(const u32* bitmap, u32 nbits, u32 k, u32* word_tmp, u32* sca
   klaunch(k_find_kth, g, 256, 0, st, bitmap, word_tmp, nw, k, out);
 }
 
+// ====================================================== row records ====
+// The chunk's value columns interleaved into one record per row (rows <
+// n): the segmented reduce then gathers one record (one sector) per row
+// instead of one sector per column.
+__global__ void k_row_pack(RowPack rp, i64 row0, u32 n, char* __restrict__ out) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    char* rec = out + (size_t)i * rp.R;
+    for (int c = 0; c < rp.nc; ++c) {
+      const char* src = (const char*)rp.src[c];
+      switch (rp.elem[c]) {
+        case 1: *(unsigned char*)(rec + rp.off[c]) = ((const unsigned char*)src)[row0 + i]; break;
+        case 2: *(unsigned short*)(rec + rp.off[c]) = ((const unsigned short*)src)[row0 + i]; break;
+        case 4: *(unsigned int*)(rec + rp.off[c]) = ((const unsigned int*)src)[row0 + i]; break;
+        default: *(u64*)(rec + rp.off[c]) = ((const u64*)src)[row0 + i]; break;
+      }
+    }
+  }
+}
+
+void row_pack(const RowPack& rp, int64_t row0, u32 n, char* out, cudaStream_t st) {
+  if (n) klaunch(k_row_pack, grid_for(n, 256), 256, 0, st, rp, (i64)row0, n, out);
+}
+
 // ========================================================== collapse ====
 // Consecutive sorted items per segmented-reduce thread: 4 for states of
 // <= 2 slots (measured: config 5's collapse 51 -> 35 ms; more threads keep
@@ -696,7 +719,10 @@ __device__ __forceinline__ void load_state_row(const SlotDesc& sd, i64 row0, con
 #pragma unroll
         for (int q = 0; q < k; ++q)
           if (q == a) x = s[q];
-        s[k] = a >= 0 ? x : load_slot_value(sd.src[k], sd.type[k], sd.dtype[k], sd.ptr[k], row0 + v);
+        s[k] = a >= 0 ? x
+                      : (sd.stride[k] ? load_slot_value(sd.src[k], sd.type[k], sd.dtype[k],
+                                                        (const char*)sd.ptr[k] + (size_t)(row0 + v) * sd.stride[k], 0)
+                                      : load_slot_value(sd.src[k], sd.type[k], sd.dtype[k], sd.ptr[k], row0 + v));
       }
     }
   }

@@ -80,6 +80,9 @@ struct CollapseTmp {
   u32* partial_slot;  // ceil(m / 8)
   u32* total;      // 1 (device)
 };
+// value columns of rows [row0, row0 + n) interleaved into R-byte records
+struct RowPack { int nc; const void* src[ISA_MAX_SLOTS]; int elem[ISA_MAX_SLOTS]; int off[ISA_MAX_SLOTS]; int R; };
+void row_pack(const RowPack& rp, int64_t row0, u32 n, char* out, cudaStream_t st);
 // segmented-reduce threads for m items (per-thread partial-state buffers)
 u32 collapse_threads(u32 m, int S);
 void collapse(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, u32 limit,
