@@ -432,3 +432,20 @@ def test_sort_intersect_plan_vs_reference():
     out_h = op.intersect_columns([t.cpu() for t in a], [t.cpu() for t in b])
     assert np.array_equal(out_h[0].numpy(), z["out_keys"])
     assert downstream.merge_intersect([], ra[:3]) == []
+
+
+@pytest.mark.parametrize("cfg,domain", [(5, 1 << 22)])
+def test_large_chunk_flush_rows_vs_c_oracle(cfg, domain):
+    """Fill cycles of more than 2^20 rows (large-chunk flush analysis: global
+    new-head bitmap + k-th select): cycles and run sizes equal the C
+    restatement's exactly."""
+    w = workloads.make(cfg, rows=8_000_000, device="cpu", domain=domain)
+    keys_np = [k.numpy() for k in w.keys]
+    vals_np = {k: v.numpy() for k, v in w.values.items()}
+    slots = oracle.make_states(w.schema, vals_np, w.rows)
+    M = 1 << 20
+    _, _, led, cycles = oracle.rsw_sortagg(keys_np, slots, oracle.slot_ops(w.schema), M, 100)
+    op = _oracle_case(w, M, rel=1e-5 if cfg == 3 else 1e-9, preaggregate="never")
+    assert op.cycles == [c for c in cycles if c > 0]
+    assert max(op.cycles) > (1 << 20)
+    assert op.ledger.rows_spilled == led["rows_spilled"] and op.runs_after_generation == led["runs"]
