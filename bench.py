@@ -387,11 +387,15 @@ def main():
         e2e_step()
         barrier()
         k2 = args.e2e_steps or args.steps
-        t0 = time.perf_counter()
+        # device clock (CUDA events on the launching stream) around the
+        # synchronous public-API calls; max over ranks below
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         for _ in range(k2):
             outs = e2e_step()
+        e1.record(stream)
         barrier()
-        secs = (time.perf_counter() - t0) / k2
+        secs = e0.elapsed_time(e1) / 1e3 / k2
         if world > 1:
             t = torch.tensor([secs], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
