@@ -1791,8 +1791,24 @@ struct Engine {
       if (last_len == 0) last_len = 1;
       a = nxt;
     }
-    // residue becomes the last run if anything spilled (sortagg.py:353-374)
-    if (!runs.empty()) spill_T();
+    // residue becomes the last run if anything spilled (sortagg.py:353-374);
+    // with host-tier runs it stays where it is (HBM): the wide merge reads it
+    // next, so a PCIe round trip would buy nothing (the ledger counts it as
+    // written like every run)
+    if (!runs.empty()) {
+      if (cfg.run_tier == ISA_TIER_HOST && T.n > 0) {
+        Run r;
+        r.rows = T.n;
+        r.host = false;
+        r.lo = T.plo();
+        r.hi = KW == 2 ? T.phi() : nullptr;
+        r.st = S ? T.pst() : nullptr;
+        runs.push_back(r);
+        account_written(r);
+      } else {
+        spill_T();
+      }
+    }
     led.runs_after_generation = (int64_t)runs.size();
     CK(cudaEventRecord(rg1, st));
     sync();
