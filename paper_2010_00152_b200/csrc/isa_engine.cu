@@ -549,6 +549,7 @@ struct Engine {
     b.aux = tile_hist.p;
     b.map_dev = d_hist_mapped;
     b.map_host = h_hist;
+    b.pack_ok = true;   // bits outside [lb, hb] do not vary (see above)
     RankHint& rh = rank_hint[sort_ctx];
     b.hint = rh.h;
     b.hint_bit_lo = rh.bit_lo;

@@ -140,13 +140,22 @@ __device__ __forceinline__ void st_relaxed_gpu(u64* p, u64 v) {
 // Status word per (tile, digit): count | flag << 32 (1 aggregate, 2
 // inclusive prefix) | epoch << 34; words of other passes carry another epoch
 // and read as "not published yet", so the array is never cleared.
-template <int KW, bool BALLOT>
-__global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : 3) k_rs_scatter(const u64* __restrict__ lo_in, const u64* __restrict__ hi_in,
+//
+// Packed mode (PK > 0, KW == 1 only; the caller guarantees that key bits
+// outside [pk_lo, pk_lo + 32) are the same in every key): a pass moves one
+// 8-byte word per row, (key bits [pk_lo, +32) << 32) | row id, instead of
+// 8 + 4 bytes.  PK 1 packs on the way in (and records the constant key bits
+// in *pk_const), PK 2 moves packed words, PK 3 unpacks on the way out to
+// the usual (key, row id) columns.  `shift` is then the digit's position
+// in the packed word.
+template <int KW, bool BALLOT, int PK = 0>
+__global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 2 ? 4 : 3)) k_rs_scatter(const u64* __restrict__ lo_in, const u64* __restrict__ hi_in,
                                                          const u32* __restrict__ v_in, u64* __restrict__ lo_out,
                                                          u64* __restrict__ hi_out, u32* __restrict__ v_out, u32 n,
                                                          int shift, u64* __restrict__ status,
                                                          const u32* __restrict__ ghist, u32* __restrict__ tile_ctr,
-                                                         u32 epoch) {
+                                                         u32 epoch, int pk_lo, u64* __restrict__ pk_const) {
+  static_assert(PK == 0 || KW == 1, "packed passes carry one key word");
   extern __shared__ __align__(16) unsigned char smem[];
   u32* wcnt = (u32*)smem;               // [RS_WARPS][256]
   u32* dstart = wcnt + RS_WARPS * 256;  // [256]
@@ -174,7 +183,11 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : 3) k_rs_scatter(cons
     u32 gi = base + li;
     lo[it] = valid ? lo_in[gi] : 0;
     hi[it] = (KW == 2 && valid) ? hi_in[gi] : 0;
-    v[it] = valid ? v_in[gi] : 0;
+    v[it] = (PK <= 1 && valid) ? v_in[gi] : 0;
+    if (PK == 1) {
+      if (gi == 0 && valid) *pk_const = lo[it] & ~(0xFFFFFFFFull << pk_lo);
+      lo[it] = (((lo[it] >> pk_lo) & 0xFFFFFFFFull) << 32) | v[it];
+    }
   }
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
@@ -260,9 +273,10 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : 3) k_rs_scatter(cons
       u32 p = dstart[d] + wcnt[w * 256 + d] + off[it];
       s_lo[p] = lo[it];
       if (KW == 2) s_hi[p] = hi[it];
-      s_v[p] = v[it];
+      if (!PK) s_v[p] = v[it];
     }
   }
+  const u64 kc = PK == 3 ? *pk_const : 0;
   __syncthreads();
 #pragma unroll 4
   for (int it = 0; it < RS_ITEMS; ++it) {
@@ -272,9 +286,14 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : 3) k_rs_scatter(cons
       u64 h = KW == 2 ? s_hi[p] : 0;
       u32 d = digit_of(h, l, shift);
       u32 dst = gbase[d] + p;
-      lo_out[dst] = l;
-      if (KW == 2) hi_out[dst] = h;
-      v_out[dst] = s_v[p];
+      if (PK == 3) {
+        lo_out[dst] = kc | ((l >> 32) << pk_lo);
+        v_out[dst] = (u32)l;
+      } else {
+        lo_out[dst] = l;
+        if (KW == 2) hi_out[dst] = h;
+        if (!PK) v_out[dst] = s_v[p];
+      }
     }
   }
 }
@@ -297,8 +316,8 @@ __global__ void __launch_bounds__(256) k_rs_hist_all(const u64* __restrict__ klo
     if (h[i]) atomicAdd(&ghist[i], h[i]);
 }
 
-static size_t rs_scatter_smem(int KW) {
-  return (RS_WARPS * 256 + 256 + 256 + 8) * sizeof(u32) + (size_t)RS_TILE * (8 * KW + 4);
+static size_t rs_scatter_smem(int KW, bool packed = false) {
+  return (RS_WARPS * 256 + 256 + 256 + 8) * sizeof(u32) + (size_t)RS_TILE * (packed ? 8 : 8 * KW + 4);
 }
 
 // aux layout: [ghist: RS_MAX_PASS * 256 u32][tile counters: RS_MAX_PASS u32][pad][status: 256 * ntiles u64].
@@ -314,6 +333,15 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
   if (n <= 1 || bit_hi <= bit_lo) return cur;
   static bool attr_set[3] = {false, false, false};
   if (!attr_set[KW]) {
+    if (KW == 1) {
+      const int ps = (int)rs_scatter_smem(1, true);
+      cudaFuncSetAttribute(k_rs_scatter<1, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ps);
+      cudaFuncSetAttribute(k_rs_scatter<1, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ps);
+      cudaFuncSetAttribute(k_rs_scatter<1, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ps);
+      cudaFuncSetAttribute(k_rs_scatter<1, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ps);
+      cudaFuncSetAttribute(k_rs_scatter<1, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ps);
+      cudaFuncSetAttribute(k_rs_scatter<1, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ps);
+    }
     if (KW == 2) {
       cudaFuncSetAttribute(k_rs_scatter<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_scatter_smem(2));
       cudaFuncSetAttribute(k_rs_scatter<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_scatter_smem(2));
@@ -329,6 +357,12 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
   u32* ghist = (u32*)b.aux;
   u32* tctr = ghist + RS_MAX_PASS * 256;
   u64* status = (u64*)((char*)b.aux + RS_AUX_HDR);
+  u64* pk_const = (u64*)((char*)b.aux + RS_AUX_HDR - 64);   // header pad, after the tile counters
+  // packed passes: one 8-byte word per row when the varying key bits fit 32
+  static int pk_env = -1;
+  if (pk_env < 0) { const char* e = getenv("ISA_PACKED"); pk_env = e && e[0] == '0' ? 0 : 1; }
+  const bool packed = pk_env && KW == 1 && b.pack_ok && ntiles > 1 && npass >= 2 && bit_hi - bit_lo <= 32;
+  const size_t psmem = rs_scatter_smem(1, true);
   if (ntiles > 1) {
     if (npass > RS_MAX_PASS) throw std::runtime_error("radix sort: too many passes");
     cudaMemsetAsync(ghist, 0, (RS_MAX_PASS * 256 + RS_MAX_PASS) * 4, st);
@@ -378,8 +412,23 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
     const u32 ep = one ? 0u : ((g_rs_epoch.fetch_add(1) % 0x3FFFFFFEu) + 1u);
 #define RS_GO(K, BL, HI_IN, HI_OUT)                                                                          \
   klaunch(k_rs_scatter<K, BL>, ntiles, RS_THREADS, smem, st, b.lo[cur], HI_IN, b.val[cur], b.lo[nxt], HI_OUT, \
-          b.val[nxt], n, shift, stt, gh, tc, ep)
-    if (KW == 2) {
+          b.val[nxt], n, shift, stt, gh, tc, ep, 0, (u64*)nullptr)
+#define RS_PK(PK)                                                                                            \
+  do {                                                                                                       \
+    if (ballot[p])                                                                                           \
+      klaunch(k_rs_scatter<1, true, PK>, ntiles, RS_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,      \
+              b.val[cur], b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - bit_lo, stt, gh, tc, ep, bit_lo, \
+              pk_const);                                                                                     \
+    else                                                                                                     \
+      klaunch(k_rs_scatter<1, false, PK>, ntiles, RS_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,     \
+              b.val[cur], b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - bit_lo, stt, gh, tc, ep, bit_lo, \
+              pk_const);                                                                                     \
+  } while (0)
+    if (packed) {
+      if (p == 0) RS_PK(1);
+      else if (p == npass - 1) RS_PK(3);
+      else RS_PK(2);
+    } else if (KW == 2) {
       if (ballot[p]) RS_GO(2, true, b.hi[cur], b.hi[nxt]);
       else RS_GO(2, false, b.hi[cur], b.hi[nxt]);
     } else {
@@ -387,6 +436,7 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
       else RS_GO(1, false, (const u64*)nullptr, (u64*)nullptr);
     }
 #undef RS_GO
+#undef RS_PK
     if (launches) *launches += 1;
     cur = nxt;
   }

@@ -24,6 +24,7 @@ struct SortBufs {
   const u32* map_host = nullptr;   // ... and host view (per-pass histograms for the ranking choice)
   signed char* hint = nullptr;     // [16] cached ranking choice per pass (hint[0] < 0: none yet)
   int hint_bit_lo = -1, hint_npass = 0;
+  bool pack_ok = false;   // key bits outside [bit_lo, bit_hi) are equal in every key (packed passes allowed)
 };
 size_t sort_aux_bytes(u32 n);
 int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStream_t st, int64_t* launches,
