@@ -4,6 +4,7 @@
 // reduce, merge): no tensor cores.  Design rules followed: coalesced global
 // access, shared-memory staging of tiles, warp-synchronous ranking with
 // match.any, grids sized from the SM count for streaming kernels.
+#include <type_traits>
 #include "isa_kernels.h"
 #include <cstdio>
 #include <algorithm>
@@ -122,6 +123,13 @@ __device__ __forceinline__ u32 digit_of(u64 hi, u64 lo, int shift) {
   return (u32)(v & 0xFFu);
 }
 
+// one key word: no cross-word digit (the hot loops of k_rs_scatter)
+template <int KW>
+__device__ __forceinline__ u32 digit_kw(u64 hi, u64 lo, int shift) {
+  if (KW == 1) return (u32)(lo >> shift) & 0xFFu;
+  return digit_of(hi, lo, shift);
+}
+
 #define RS_LB 4   // look-back window (predecessor status words per round trip)
 __device__ __forceinline__ u64 ld_relaxed_gpu(const u64* p) {
   u64 v;
@@ -154,7 +162,8 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 2 ? 4 : 3)) k
                                                          u64* __restrict__ hi_out, u32* __restrict__ v_out, u32 n,
                                                          int shift, u64* __restrict__ status,
                                                          const u32* __restrict__ ghist, u32* __restrict__ tile_ctr,
-                                                         u32 epoch, int pk_lo, u64* __restrict__ pk_const) {
+                                                         u32 epoch, int pk_lo, u64* __restrict__ pk_const,
+                                                         int lb_sleep) {
   static_assert(PK == 0 || KW == 1, "packed passes carry one key word");
   extern __shared__ __align__(16) unsigned char smem[];
   u32* wcnt = (u32*)smem;               // [RS_WARPS][256]
@@ -176,10 +185,13 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 2 ? 4 : 3)) k
   u64 lo[RS_ITEMS], hi[RS_ITEMS];
   u32 v[RS_ITEMS], off[RS_ITEMS];
   const u32 lt = lanemask_lt();
+  // load + rank; full tiles (all but the last) drop every bounds test
+  auto load_rank = [&](auto full_tag) {
+  constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
     u32 li = w * RS_WARP_ITEMS + it * 32 + lane;
-    bool valid = li < tile_n;
+    const bool valid = FULL || li < tile_n;
     u32 gi = base + li;
     lo[it] = valid ? lo_in[gi] : 0;
     hi[it] = (KW == 2 && valid) ? hi_in[gi] : 0;
@@ -192,8 +204,8 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 2 ? 4 : 3)) k
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
     u32 li = w * RS_WARP_ITEMS + it * 32 + lane;
-    bool valid = li < tile_n;
-    u32 d = valid ? digit_of(hi[it], lo[it], shift) : 256 + lane;
+    const bool valid = FULL || li < tile_n;
+    u32 d = valid ? digit_kw<KW>(hi[it], lo[it], shift) : 256 + lane;
     // lanes holding the same digit: MATCH.ANY, or (BALLOT: chosen by the
     // host for large passes whose digits are not skewed) eight independent
     // ballots -- data-independent cost, measured faster on uniform digits
@@ -201,13 +213,14 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 2 ? 4 : 3)) k
     if (!BALLOT) {
       peers = __match_any_sync(0xffffffffu, d);
     } else {
-      peers = __ballot_sync(0xffffffffu, valid);
+      peers = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
 #pragma unroll
       for (int b = 0; b < 8; ++b) {
-        const u32 bits = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-        peers &= ((d >> b) & 1u) ? bits : ~bits;
+        const u32 bit = (d >> b) & 1u;
+        const u32 bits = __ballot_sync(0xffffffffu, bit);
+        peers &= ~(bits ^ (0u - bit));   // lanes whose bit b equals mine (one LOP3)
       }
-      if (!valid) peers = 1u << lane;
+      if (!FULL && !valid) peers = 1u << lane;
     }
     int leader = __ffs(peers) - 1;
     u32 cnt = 0;
@@ -216,52 +229,33 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 2 ? 4 : 3)) k
       wcnt[w * 256 + d] = cnt + __popc(peers);
     }
     cnt = __shfl_sync(0xffffffffu, cnt, leader);
-    off[it] = cnt + __popc(peers & lt);
+    off[it] = (cnt + __popc(peers & lt)) | (d << 16);   // digit kept for the staging loop
     __syncwarp();
   }
+  };
+  if (tile_n == RS_TILE) load_rank(std::true_type{});
+  else load_rank(std::false_type{});
   __syncthreads();
+  // per-digit exclusive prefix over warps, then over digits; the tile's
+  // aggregate is published now, but the look-back for its exclusive prefix
+  // waits until the rows are staged, so predecessors have had that long to
+  // publish (fewer spinning reloads)
+  const int dg = tid;  // RS_THREADS == 256: thread = digit
+  u32 run = 0, ds, gs = 0;
   {
-    // per-digit exclusive prefix over warps, then over digits
-    const int d = tid;  // RS_THREADS == 256
-    u32 run = 0;
 #pragma unroll
     for (int ww = 0; ww < RS_WARPS; ++ww) {
-      u32 c = wcnt[ww * 256 + d];
-      wcnt[ww * 256 + d] = run;
+      u32 c = wcnt[ww * 256 + dg];
+      wcnt[ww * 256 + dg] = run;
       run += c;
     }
     u32 tot;
-    u32 ds = block_excl_scan256(run, sw, &tot);
-    dstart[d] = ds;
-    if (!status) {
-      gbase[d] = 0u;   // one tile: in-tile offsets are global
-    } else {
-      const u32 gs = block_excl_scan256(ghist[d], sw, &tot);   // global start of digit d
+    ds = block_excl_scan256(run, sw, &tot);
+    dstart[dg] = ds;
+    if (status) {
+      gs = block_excl_scan256(ghist[dg], sw, &tot);   // global start of digit dg
       const u64 E = (u64)epoch << 34;
-      u32 excl = 0;
-      if (tile == 0) {
-        st_relaxed_gpu(status + d, E | (2ull << 32) | run);
-      } else {
-        st_relaxed_gpu(status + (size_t)tile * 256 + d, E | (1ull << 32) | run);
-        // look back RS_LB predecessors per round trip
-        int j = (int)tile - 1;
-        bool done = false;
-        while (!done) {
-          u64 x[RS_LB];
-#pragma unroll
-          for (int i = 0; i < RS_LB; ++i)
-            x[i] = j - i >= 0 ? ld_relaxed_gpu(status + (size_t)(j - i) * 256 + d) : (E | (2ull << 32));
-#pragma unroll
-          for (int i = 0; i < RS_LB; ++i) {
-            if ((x[i] >> 34) != (u64)epoch) break;   // not published yet: reload from tile j
-            excl += (u32)x[i];
-            --j;
-            if (((x[i] >> 32) & 3u) == 2u) { done = true; break; }
-          }
-        }
-        st_relaxed_gpu(status + (size_t)tile * 256 + d, E | (2ull << 32) | (excl + run));
-      }
-      gbase[d] = gs + excl - ds;
+      st_relaxed_gpu(status + (size_t)tile * 256 + dg, E | ((tile == 0 ? 2ull : 1ull) << 32) | run);
     }
   }
   __syncthreads();
@@ -269,12 +263,41 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 2 ? 4 : 3)) k
   for (int it = 0; it < RS_ITEMS; ++it) {
     u32 li = w * RS_WARP_ITEMS + it * 32 + lane;
     if (li < tile_n) {
-      u32 d = digit_of(hi[it], lo[it], shift);
-      u32 p = dstart[d] + wcnt[w * 256 + d] + off[it];
+      const u32 d = off[it] >> 16;
+      u32 p = dstart[d] + wcnt[w * 256 + d] + (off[it] & 0xFFFFu);
       s_lo[p] = lo[it];
       if (KW == 2) s_hi[p] = hi[it];
       if (!PK) s_v[p] = v[it];
     }
+  }
+  if (!status) {
+    gbase[dg] = 0u;   // one tile: in-tile offsets are global
+  } else {
+    const u64 E = (u64)epoch << 34;
+    u32 excl = 0;
+    if (tile != 0) {
+      // look back RS_LB predecessors per round trip
+      int j = (int)tile - 1;
+      bool done = false;
+      while (!done) {
+        u64 x[RS_LB];
+#pragma unroll
+        for (int i = 0; i < RS_LB; ++i)
+          x[i] = j - i >= 0 ? ld_relaxed_gpu(status + (size_t)(j - i) * 256 + dg) : (E | (2ull << 32));
+#pragma unroll
+        for (int i = 0; i < RS_LB; ++i) {
+          if ((x[i] >> 34) != (u64)epoch) {   // not published yet: reload from tile j
+            if (lb_sleep) __nanosleep(lb_sleep);
+            break;
+          }
+          excl += (u32)x[i];
+          --j;
+          if (((x[i] >> 32) & 3u) == 2u) { done = true; break; }
+        }
+      }
+      st_relaxed_gpu(status + (size_t)tile * 256 + dg, E | (2ull << 32) | (excl + run));
+    }
+    gbase[dg] = gs + excl - ds;
   }
   const u64 kc = PK == 3 ? *pk_const : 0;
   __syncthreads();
@@ -284,7 +307,7 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 2 ? 4 : 3)) k
     if (p < tile_n) {
       u64 l = s_lo[p];
       u64 h = KW == 2 ? s_hi[p] : 0;
-      u32 d = digit_of(h, l, shift);
+      u32 d = digit_kw<KW>(h, l, shift);
       u32 dst = gbase[d] + p;
       if (PK == 3) {
         lo_out[dst] = kc | ((l >> 32) << pk_lo);
@@ -363,6 +386,8 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
   if (pk_env < 0) { const char* e = getenv("ISA_PACKED"); pk_env = e && e[0] == '0' ? 0 : 1; }
   const bool packed = pk_env && KW == 1 && b.pack_ok && ntiles > 1 && npass >= 2 && bit_hi - bit_lo <= 32;
   const size_t psmem = rs_scatter_smem(1, true);
+  static int lb_sleep = -1;   // look-back back-off (ns) while a predecessor has not published
+  if (lb_sleep < 0) { const char* e = getenv("ISA_LB_SLEEP"); lb_sleep = e ? atoi(e) : 0; }
   if (ntiles > 1) {
     if (npass > RS_MAX_PASS) throw std::runtime_error("radix sort: too many passes");
     cudaMemsetAsync(ghist, 0, (RS_MAX_PASS * 256 + RS_MAX_PASS) * 4, st);
@@ -412,17 +437,17 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
     const u32 ep = one ? 0u : ((g_rs_epoch.fetch_add(1) % 0x3FFFFFFEu) + 1u);
 #define RS_GO(K, BL, HI_IN, HI_OUT)                                                                          \
   klaunch(k_rs_scatter<K, BL>, ntiles, RS_THREADS, smem, st, b.lo[cur], HI_IN, b.val[cur], b.lo[nxt], HI_OUT, \
-          b.val[nxt], n, shift, stt, gh, tc, ep, 0, (u64*)nullptr)
+          b.val[nxt], n, shift, stt, gh, tc, ep, 0, (u64*)nullptr, lb_sleep)
 #define RS_PK(PK)                                                                                            \
   do {                                                                                                       \
     if (ballot[p])                                                                                           \
       klaunch(k_rs_scatter<1, true, PK>, ntiles, RS_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,      \
               b.val[cur], b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - bit_lo, stt, gh, tc, ep, bit_lo, \
-              pk_const);                                                                                     \
+              pk_const, lb_sleep);                                                                                     \
     else                                                                                                     \
       klaunch(k_rs_scatter<1, false, PK>, ntiles, RS_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,     \
               b.val[cur], b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - bit_lo, stt, gh, tc, ep, bit_lo, \
-              pk_const);                                                                                     \
+              pk_const, lb_sleep);                                                                                     \
   } while (0)
     if (packed) {
       if (p == 0) RS_PK(1);

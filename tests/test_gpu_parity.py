@@ -449,3 +449,18 @@ def test_large_chunk_flush_rows_vs_c_oracle(cfg, domain):
     assert op.cycles == [c for c in cycles if c > 0]
     assert max(op.cycles) > (1 << 20)
     assert op.ledger.rows_spilled == led["rows_spilled"] and op.runs_after_generation == led["runs"]
+
+
+@pytest.mark.parametrize("shift,bits,base", [(5, 27, -(1 << 50)), (7, 32, 3 << 45), (0, 20, -7)])
+def test_packed_radix_passes_vs_oracle(shift, bits, base):
+    """Keys whose varying bits span <= 32 take the packed radix passes
+    (one 8-byte word per row, isa_kernels.cu k_rs_scatter PK 1/2/3): the
+    constant key bits outside the span (negative / high offsets) must come
+    back unchanged, and chunks span many sort tiles."""
+    w = workloads.config5(rows=3_000_000, device="cpu", domain=1 << 22)
+    g = torch.Generator().manual_seed(2010 + shift)
+    x = torch.randint(0, 1 << bits, (w.rows,), generator=g, dtype=torch.int64)
+    if bits == 32:
+        x[:2] = torch.tensor([0, (1 << 32) - 1])   # both span ends present
+    w.keys[0] = base + (x << shift)
+    _oracle_case(w, 1 << 18)
