@@ -130,7 +130,9 @@ __device__ __forceinline__ u32 digit_kw(u64 hi, u64 lo, int shift) {
   return digit_of(hi, lo, shift);
 }
 
+#ifndef RS_LB
 #define RS_LB 4   // look-back window (predecessor status words per round trip)
+#endif
 __device__ __forceinline__ u64 ld_relaxed_gpu(const u64* p) {
   u64 v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
