@@ -130,6 +130,10 @@ __device__ __forceinline__ u32 digit_kw(u64 hi, u64 lo, int shift) {
   return digit_of(hi, lo, shift);
 }
 
+#ifndef RS_WUNROLL
+#define RS_WUNROLL 16   // write-out loop unroll (shared-memory loads in flight per thread; 4: -1 to -3% sort)
+#endif
+static constexpr int kRsWriteUnroll = RS_WUNROLL;
 #ifndef RS_LB
 #define RS_LB 4   // look-back window (predecessor status words per round trip)
 #endif
@@ -303,7 +307,7 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 2 ? 4 : 3)) k
   }
   const u64 kc = PK == 3 ? *pk_const : 0;
   __syncthreads();
-#pragma unroll 4
+#pragma unroll kRsWriteUnroll
   for (int it = 0; it < RS_ITEMS; ++it) {
     u32 p = it * RS_THREADS + tid;
     if (p < tile_n) {
