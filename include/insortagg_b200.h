@@ -76,7 +76,9 @@ enum isa_slot_src { ISA_SRC_ONE = 0, ISA_SRC_COLUMN = 1 };
 /* where spilled runs live */
 /* where runs live: pinned host DRAM, HBM, or files in the reference's page
  * format (FileStore tier, runstore.py:195-236; needs isa_set_spill_dir) */
-enum isa_run_tier { ISA_TIER_HOST = 0, ISA_TIER_HBM = 1, ISA_TIER_FILE = 2 };
+/* ISA_TIER_AUTO: runs stay in HBM (bit-packed when >= 32K rows) while they
+ * fit hbm_run_budget, the rest go to pinned host DRAM */
+enum isa_run_tier { ISA_TIER_HOST = 0, ISA_TIER_HBM = 1, ISA_TIER_FILE = 2, ISA_TIER_AUTO = 3 };
 
 typedef struct isa_config {
   int64_t memory_budget;     /* M: group-table budget in rows  (SortAggConfig.memory_budget) */
@@ -91,6 +93,7 @@ typedef struct isa_config {
   int64_t output_size_hint;  /* SortAggConfig.output_size_hint; <= 0 = none */
   int32_t run_codec;         /* host-tier runs across PCIe: 0 auto (bit-packed on the GPU when >= 32K rows), 1 raw, 2 packed */
   int32_t reserved0;
+  int64_t hbm_run_budget;    /* ISA_TIER_AUTO: bytes of HBM runs may use; 0 = 40% of the free HBM at execute start */
 } isa_config;
 
 /* SortAggConfig.merge_mode (sortagg.py:45-47): wide = in-sort early
@@ -255,6 +258,31 @@ ISA_API const char* isa_last_error(isa_handle* h);
 ISA_API int isa_phase_stats(isa_handle* h, isa_phase* out, int cap);
 /* Kernels launched by this library so far in the process. */
 ISA_API int64_t isa_launch_count(void);
+
+/* Per-kernel-family device timing (new: the bench's kernel-true roofline).
+ * When on, the library records CUDA events around the launches of its main
+ * kernels on their streams (this host thread only).  isa_kernel_stats, called
+ * after the caller synchronized, returns per family the summed device ms,
+ * launches and algorithmic bytes since the previous call, and resets them. */
+enum isa_kernel_family {
+  ISA_KF_SCATTER = 0,   /* onesweep radix scatter pass */
+  ISA_KF_HIST = 1,      /* all-pass radix histogram */
+  ISA_KF_COLLAPSE = 2,  /* segmented reduce of a sorted chunk / window */
+  ISA_KF_PACK = 3,      /* run codec: pack */
+  ISA_KF_UNPACK = 4,    /* run codec: unpack */
+  ISA_KF_ABSORB = 5,    /* tiny-table absorb */
+  ISA_KF_MERGE = 6,     /* wide merge: tile merge */
+  ISA_KF_FLUSH = 7,     /* flush analysis */
+  ISA_KF_EXPORT = 8,    /* result export */
+  ISA_KF_COUNT = 9
+};
+typedef struct isa_kstat {
+  double ms;
+  int64_t launches;
+  int64_t bytes;
+} isa_kstat;
+ISA_API void isa_set_kernel_timing(int32_t on);
+ISA_API int isa_kernel_stats(isa_kstat* out, int cap);
 
 /* --- multi-GPU range partitioning primitives -------------------------- */
 /* Normalized (order-preserving, 128-bit) keys of rows 0, stride, 2*stride, ...

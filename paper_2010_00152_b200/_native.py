@@ -32,7 +32,7 @@ DTYPE_BITS = {U8: 8, I8: 8, U16: 16, I16: 16, U32: 32, I32: 32, U64: 64, I64: 64
 OP_ADD, OP_MIN, OP_MAX = 0, 1, 2
 SLOT_I64, SLOT_F64 = 0, 1
 SRC_ONE, SRC_COLUMN = 0, 1
-TIER_HOST, TIER_HBM, TIER_FILE = 0, 1, 2
+TIER_HOST, TIER_HBM, TIER_FILE, TIER_AUTO = 0, 1, 2, 3
 
 _STATUS_ERRORS = {
     1: InvalidInputError,
@@ -50,7 +50,11 @@ EXPORTED_SYMBOLS = (
     "isa_sample_keys", "isa_partition", "isa_phase_stats", "isa_launch_count", "isa_steps",
     "isa_set_spill_dir", "isa_in_stream_aggregate", "isa_merge_intersect", "isa_partition_counts",
     "isa_scatter_to_peers", "isa_ipc_handle", "isa_ipc_open", "isa_ipc_close",
+    "isa_set_kernel_timing", "isa_kernel_stats",
 )
+
+# isa_kernel_family (kernel-true roofline families)
+KERNEL_FAMILIES = ("scatter", "hist", "collapse", "pack", "unpack", "absorb", "merge", "flush", "export")
 
 PHASES = ("absorb", "sort", "flush", "collapse", "table_merge", "wm_sort", "wm_collapse",
           "run_generation", "wide_merge", "probe")
@@ -59,6 +63,10 @@ PHASES = ("absorb", "sort", "flush", "collapse", "table_merge", "wm_sort", "wm_c
 class IsaPhase(ctypes.Structure):
     _fields_ = [("ms", ctypes.c_double), ("calls", ctypes.c_int64), ("rows", ctypes.c_int64),
                 ("bytes", ctypes.c_int64)]
+
+
+class IsaKstat(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_double), ("launches", ctypes.c_int64), ("bytes", ctypes.c_int64)]
 
 
 class IsaConfig(ctypes.Structure):
@@ -75,6 +83,7 @@ class IsaConfig(ctypes.Structure):
         ("output_size_hint", ctypes.c_int64),
         ("run_codec", ctypes.c_int32),
         ("reserved0", ctypes.c_int32),
+        ("hbm_run_budget", ctypes.c_int64),
     ]
 
 
@@ -181,6 +190,10 @@ def load():
     lib.isa_phase_stats.argtypes = [vp, ctypes.POINTER(IsaPhase), ctypes.c_int]
     lib.isa_launch_count.restype = ctypes.c_int64
     lib.isa_launch_count.argtypes = []
+    lib.isa_set_kernel_timing.restype = None
+    lib.isa_set_kernel_timing.argtypes = [ctypes.c_int32]
+    lib.isa_kernel_stats.restype = ctypes.c_int
+    lib.isa_kernel_stats.argtypes = [ctypes.POINTER(IsaKstat), ctypes.c_int]
     lib.isa_sample_keys.restype = ctypes.c_int
     lib.isa_sample_keys.argtypes = [vp, ctypes.c_int64, pp, ctypes.c_int64, vp, vp, vp]
     lib.isa_partition.restype = ctypes.c_int
@@ -196,6 +209,20 @@ def version():
 def launch_count():
     """Kernels launched by libinsortagg_b200 so far in this process."""
     return int(load().isa_launch_count())
+
+
+def set_kernel_timing(on):
+    """CUDA-event timing of the library's main kernels (this host thread)."""
+    load().isa_set_kernel_timing(1 if on else 0)
+
+
+def kernel_stats():
+    """Per kernel family {ms, launches, bytes} since the last call (call after
+    synchronizing the device)."""
+    arr = (IsaKstat * len(KERNEL_FAMILIES))()
+    load().isa_kernel_stats(arr, len(KERNEL_FAMILIES))
+    return {name: {"ms": arr[i].ms, "launches": arr[i].launches, "bytes": arr[i].bytes}
+            for i, name in enumerate(KERNEL_FAMILIES)}
 
 
 def phases_dict(arr):

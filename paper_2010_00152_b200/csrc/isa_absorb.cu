@@ -293,15 +293,13 @@ void absorb_geometry(u32 n, int num_sms, u32* grid, u32* rows_per_cta) {
 template <int KW, int NT>
 static void absorb_launch(const KeyDesc& kd, const SlotDesc& sd, int64_t row0, u32 n, const TinyTable& tt, u32 grid,
                           u32 rpc, u64* partials, u32* miss_buf, u32* miss_cnt, cudaStream_t st) {
-  static bool attr = false;
+  static std::atomic<unsigned long long> attr{0};
   int ncell = 0;
   for (int s = 0; s < sd.nslots; ++s) ncell += (sd.src[s] == SRC_ONE && sd.op[s] == OP_ADD && sd.type[s] == ST_I64) ? 0 : 1;
   const size_t smem = (size_t)std::max(ncell, 1) * NT * AB_THREADS * 8;
-  if (!attr) {
+  if (first_on_device(attr))
     cudaFuncSetAttribute(k_absorb_tiny<KW, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          AB_MAX_CELLS * AB_THREADS * 8);
-    attr = true;
-  }
   klaunch(k_absorb_tiny<KW, NT>, grid, AB_THREADS, smem, st, kd, sd, row0, n, tt, rpc, partials, miss_buf, miss_cnt);
 }
 

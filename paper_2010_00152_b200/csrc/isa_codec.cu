@@ -20,6 +20,7 @@
 // then every column's payload words (word_off counted from the payload).
 #include "isa_kernels.h"
 
+#include <algorithm>
 #include <atomic>
 
 namespace isa {
@@ -270,11 +271,9 @@ void pack_fused(const PackSrc& p, u64* status, u32* ticket, u32* blk_off, char* 
   const u32 nb = pack_blocks(p.n);
   if (!nb) return;
   const size_t smem = (size_t)pk_ncol(p.kw, p.S) * PK_ROWS * 8;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr))
     cudaFuncSetAttribute(k_pack_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, PKF_MAXC * PK_ROWS * 8);
-    attr = true;
-  }
   const u32 ep = (g_pk_epoch.fetch_add(1) % 0x3FFFFFFEu) + 1u;
   cudaMemsetAsync(ticket, 0, sizeof(u32), st);
   klaunch(k_pack_fused, nb, PK_THREADS, smem, st, p, status, ep, ticket, blk_off, out);
@@ -297,7 +296,8 @@ __global__ void __launch_bounds__(PK_THREADS) k_unpack(const UnpackBlk* __restri
                                                        int kw, int S, u32 fmask, u64* __restrict__ lo,
                                                        u64* __restrict__ hi, u64* __restrict__ st) {
   const UnpackBlk u = d[blockIdx.x];
-  const u64* blk = (const u64*)(src + u.src_off);
+  const u64* blk = (const u64*)(uintptr_t)u.src_off;   // absolute (staged copy or HBM-resident run)
+  (void)src;
   const int ncol = pk_ncol(kw, S);
   const u64* payload = blk + ncol * 2;
   for (int c = 0; c < ncol; ++c) {
@@ -356,6 +356,39 @@ __global__ void k_run_lower_bounds(const RunRef* __restrict__ runs, int nruns, c
     if (key_less<KW>(mhi, mlo, khi, klo)) l = m + 1; else h = m;
   }
   out[q] = l;
+}
+
+// keys of rows 0, F, 2F, ... of every run (sample q of run r at soff[r] + i;
+// runs without samples have soff[r] == soff[r + 1])
+template <int KW>
+__global__ void k_run_samples(const RunRef* __restrict__ runs, int nruns, const int64_t* __restrict__ soff, int64_t F,
+                              int64_t total, u64* __restrict__ out_lo, u64* __restrict__ out_hi) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    int l = 0, h = nruns;   // largest l with soff[l] <= q: a run that has samples
+    while (h - l > 1) {
+      const int m = (l + h) >> 1;
+      if (soff[m] <= q) l = m; else h = m;
+    }
+    const RunRef rr = runs[l];
+    const u32 row = (u32)((q - soff[l]) * F);
+    u64 khi = 0, klo;
+    if (rr.pk) {
+      pk_key_at<KW>(rr, row, khi, klo);
+    } else {
+      klo = rr.lo[row];
+      if (KW == 2) khi = rr.hi[row];
+    }
+    out_lo[q] = klo;
+    if (KW == 2) out_hi[q] = khi;
+  }
+}
+
+void run_samples(int KW, const RunRef* runs_dev, int nruns, const int64_t* soff_dev, int64_t F, int64_t total,
+                 u64* out_lo, u64* out_hi, cudaStream_t st) {
+  if (total <= 0) return;
+  const int g = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  if (KW == 2) klaunch(k_run_samples<2>, g, 256, 0, st, runs_dev, nruns, soff_dev, F, total, out_lo, out_hi);
+  else klaunch(k_run_samples<1>, g, 256, 0, st, runs_dev, nruns, soff_dev, F, total, out_lo, out_hi);
 }
 
 void run_lower_bounds(int KW, const RunRef* runs_dev, int nruns, const u64* b_lo, const u64* b_hi, int nb, u32* out,

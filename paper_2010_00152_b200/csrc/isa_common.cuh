@@ -19,6 +19,29 @@
 namespace isa {
 // number of kernels this library has launched (process-wide)
 extern std::atomic<long long> g_launches;
+
+// Per-kernel-family device timing (CUDA events around the launches of the
+// library's main kernels, on their stream), on when kt_enabled(): the
+// bench's kernel-true roofline.  alg_bytes = the algorithmic bytes the
+// launch moves (inputs read once + outputs written once).
+enum KFam { KF_SCATTER = 0, KF_HIST, KF_COLLAPSE, KF_PACK, KF_UNPACK, KF_ABSORB, KF_MERGE, KF_FLUSH, KF_EXPORT,
+            KF_COUNT };
+bool kt_enabled();
+void kt_set(bool on);
+void kt_begin(int fam, cudaStream_t st);
+void kt_end(int fam, int64_t alg_bytes, cudaStream_t st);
+void kt_add_bytes(int fam, int64_t alg_bytes);   // to the family's last record (bytes known after the launch)
+// after the stream(s) synchronized: per family summed ms, launches, bytes
+void kt_collect(double* ms, int64_t* launches, int64_t* bytes);
+
+// Kernel attributes (e.g. the dynamic shared-memory limit) are per device:
+// true the first time a call site reaches this for the current device.
+inline bool first_on_device(std::atomic<unsigned long long>& seen) {
+  int d = 0;
+  cudaGetDevice(&d);
+  const unsigned long long bit = 1ull << (d & 63);
+  return !(seen.fetch_or(bit) & bit);
+}
 }
 
 // Every kernel launch of the library goes through klaunch so that the

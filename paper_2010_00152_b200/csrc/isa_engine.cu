@@ -298,6 +298,7 @@ struct Engine {
     recs.clear();
   }
   int64_t absorb_row_bytes = 0;   // algorithmic bytes read per absorbed row
+  int64_t value_row_bytes = 0;    // distinct value-column bytes per input row
   isa_ledger led;
   std::vector<int64_t> cycles;
 
@@ -378,8 +379,10 @@ struct Engine {
     if (cfg.preaggregate < 0 || cfg.preaggregate > 2) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown preaggregate mode");
     if (cfg.merge_mode < ISA_MERGE_WIDE || cfg.merge_mode > ISA_MERGE_SEPARATE) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown merge mode");
     if (cfg.run_codec < 0 || cfg.run_codec > 2) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown run codec");
-    if (cfg.run_tier != ISA_TIER_HOST && cfg.run_tier != ISA_TIER_HBM && cfg.run_tier != ISA_TIER_FILE)
+    if (cfg.run_tier != ISA_TIER_HOST && cfg.run_tier != ISA_TIER_HBM && cfg.run_tier != ISA_TIER_FILE &&
+        cfg.run_tier != ISA_TIER_AUTO)
       throw IsaError(ISA_ERR_INVALID_INPUT, "unknown run tier");
+    if (cfg.hbm_run_budget < 0) throw IsaError(ISA_ERR_INVALID_INPUT, "hbm_run_budget must be >= 0");
     if (cfg.run_tier == ISA_TIER_FILE && cfg.merge_mode != ISA_MERGE_WIDE)
       throw IsaError(ISA_ERR_INVALID_INPUT, "the FileStore tier supports merge_mode wide");
     if (sch.n_key_cols < 1) throw IsaError(ISA_ERR_INVALID_INPUT, "schema needs at least one key column");
@@ -453,6 +456,17 @@ struct Engine {
           break;
         }
     }
+    // 32-bit byte counts: packed run images (block offsets are u32) and
+    // FileStore page images (page_run_bytes) of a run of up to M groups
+    {
+      const int64_t M = cfg.memory_budget, ncol = KW + S;
+      const int64_t pack_bound = M * 8 * ncol + ((M + 1023) / 1024 + 1) * (ncol * 16 + 8) + 4096;
+      pack_u32_ok = pack_bound < (int64_t)0xF0000000ll;
+      const int64_t pages = (M + cfg.page_capacity - 1) / cfg.page_capacity;
+      const int64_t page_bound = pages * (12 + 8 * (int64_t)sch.n_key_cols) + M * 8 * (sch.n_key_cols + S);
+      if (cfg.run_tier == ISA_TIER_FILE && page_bound >= (int64_t)0xF0000000ll)
+        throw IsaError(ISA_ERR_INVALID_INPUT, "a run of memory_budget groups exceeds 4 GiB of pages; lower memory_budget");
+    }
     absorb_row_bytes = key_bits / 8;
     bool used[ISA_MAX_VAL_COLS] = {false};
     for (int s = 0; s < S; ++s)
@@ -460,6 +474,7 @@ struct Engine {
         used[sch.slot_col[s]] = true;
         absorb_row_bytes += dtype_bits(sd0.dtype[s]) / 8;
       }
+    value_row_bytes = absorb_row_bytes - key_bits / 8;
   }
 
   // ------------------------------------------------------------ helpers --
@@ -641,17 +656,24 @@ struct Engine {
     ct.total = dscal32(2);
     const int phc = (st_in && merge_phase) ? ISA_PH_WM_COLLAPSE : ISA_PH_COLLAPSE;
     ph_begin(phc);
+    kt_begin(KF_COLLAPSE, st);
     collapse(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, limit, sd, row0, st_in,
              out.plo(), out.phi(), out.pst(), ct, st);
+    // algorithmic bytes: every sorted (key, row id) read once, the rows'
+    // values (or staged states) read once, the groups written once
+    kt_end(KF_COLLAPSE, (int64_t)m * (8 * KW + 4 + (st_in ? 8 * S : value_row_bytes)), st);
+    const int64_t out_row = 8 * KW + 8 * S;
     if (known_n >= 0) {
       ph_end(phc, m, 0);
       out.n = (u32)known_n;
+      kt_add_bytes(KF_COLLAPSE, known_n * out_row);
       return;
     }
     to_host(dscal32(2), sizeof(u32));
     ph_end(phc, m, 0);
     sync();
     out.n = h_scal[0];
+    kt_add_bytes(KF_COLLAPSE, (int64_t)out.n * out_row);
   }
 
   // out <- merge_combine(A, B); A's buffers become spare, B is emptied
@@ -701,11 +723,20 @@ struct Engine {
   bool tiny_ok = false;
 
   // allocate run storage (pinned host pool or device pool) for `rows` rows
+  // run placement of the auto tier: HBM while the runs fit hbm_left bytes
+  int64_t hbm_left = 0;
+  bool run_to_device(size_t bytes) {
+    if (cfg.run_tier == ISA_TIER_HBM) return true;
+    if (cfg.run_tier != ISA_TIER_AUTO) return false;
+    if ((int64_t)bytes > hbm_left) return false;
+    hbm_left -= (int64_t)bytes;
+    return true;
+  }
   Run alloc_run(u32 rows) {
     Run r;
     r.rows = rows;
     const size_t nb_key = std::max<size_t>((size_t)rows * 8, 8), nb_st = std::max<size_t>((size_t)rows * 8 * S, 8);
-    if (cfg.run_tier == ISA_TIER_HOST) {
+    if (!run_to_device(nb_key * KW + (S ? nb_st : 0))) {
       r.host = true;
       char* klo = pinned.alloc(nb_key);
       char* khi = KW == 2 ? pinned.alloc(nb_key) : nullptr;
@@ -741,8 +772,11 @@ struct Engine {
   }
 
   // small runs are not worth the extra synchronization (their link time is tiny)
+  bool pack_u32_ok = true;   // packed images of the largest run fit 32-bit offsets
   bool pack_runs(u32 rows) const {
-    if (cfg.run_tier != ISA_TIER_HOST || cfg.merge_mode != ISA_MERGE_WIDE) return false;
+    if ((cfg.run_tier != ISA_TIER_HOST && cfg.run_tier != ISA_TIER_AUTO) || cfg.merge_mode != ISA_MERGE_WIDE ||
+        !pack_u32_ok)
+      return false;
     return cfg.run_codec == 2 || (cfg.run_codec == 0 && rows >= kPackMinRows);
   }
   static constexpr u32 kPackMinRows = 1u << 15;
@@ -756,6 +790,7 @@ struct Engine {
     pk_sz.ensure((size_t)(nblk + 2) * 4 + 16);
     u32 bytes = 0;
     size_t off_at = 0;
+    kt_begin(KF_PACK, st);
     if (pack_fused_ok(ps)) {
       // one pass; the output is bounded by the raw size
       const size_t bound = (size_t)nblk * ncol * 16 + (size_t)t.n * ncol * 8 + 64;
@@ -764,6 +799,7 @@ struct Engine {
       pk_status.ensure((size_t)nblk * 8 + 16);
       if (pk_status.bytes != had) CK(cudaMemsetAsync(pk_status.p, 0, pk_status.bytes, st));   // epochs start at 0
       pack_fused(ps, pk_status.as<u64>(), pk_sz.as<u32>() + nblk + 1, pk_sz.as<u32>(), t.pk.as<char>(), st);
+      kt_end(KF_PACK, (int64_t)t.n * 8 * ncol, st);
       bytes = read_u32(pk_sz.as<u32>() + nblk);   // offsets[nblk] = total
       off_at = ((size_t)bytes + 15) & ~(size_t)15;
     } else {
@@ -775,14 +811,30 @@ struct Engine {
       off_at = ((size_t)bytes + 15) & ~(size_t)15;
       t.pk.ensure(off_at + (size_t)(nblk + 1) * 4 + 16);
       pack_write(ps, pk_hdr.as<u64>(), pk_sz.as<u32>(), t.pk.as<char>(), st);
+      kt_end(KF_PACK, (int64_t)t.n * 8 * ncol * 2, st);
     }
+    kt_add_bytes(KF_PACK, bytes);
     // packed blocks, then the block offsets: both owned by the table until
     // its D2H copies are done (pk_sz is reused by the next spill)
     CK(cudaMemcpyAsync(t.pk.as<char>() + off_at, pk_sz.p, (size_t)(nblk + 1) * 4, cudaMemcpyDeviceToDevice, st));
     Run r;
     r.rows = t.n;
-    r.host = true;
     r.nblk = nblk;
+    if (run_to_device((size_t)bytes + (size_t)(nblk + 1) * 4 + 512)) {
+      // auto tier: the packed image stays in HBM (one D2D copy on the
+      // compute stream; the table is free again right after it)
+      r.host = false;
+      char* db = devpool.alloc((size_t)bytes + 16);
+      u32* doff = (u32*)devpool.alloc((size_t)(nblk + 1) * 4 + 16);
+      u32* hoff = (u32*)pinned.alloc((size_t)(nblk + 1) * 4 + 16);
+      CK(cudaMemcpyAsync(db, t.pk.p, bytes, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(doff, t.pk.as<char>() + off_at, (size_t)(nblk + 1) * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(hoff, t.pk.as<char>() + off_at, (size_t)(nblk + 1) * 4, cudaMemcpyDeviceToHost, st));
+      r.pk_dev = db; r.off_dev = doff; r.off_host = hoff;
+      dev_packed = true;
+      return r;
+    }
+    r.host = true;
     char* hb = pinned.alloc((size_t)bytes + 16);
     u32* hoff = (u32*)pinned.alloc((size_t)(nblk + 1) * 4 + 16);
     const char* db = nullptr;
@@ -918,6 +970,7 @@ struct Engine {
   }
 
   // T becomes a run (RunWriter of a read-sort-write flush, sortagg.py:344-350)
+  bool dev_packed = false;   // a packed run of this execute went to HBM (spill_T: no busy table)
   void spill_T() {
     if (T.n == 0) return;
     if (cfg.run_tier == ISA_TIER_FILE) {
@@ -928,6 +981,12 @@ struct Engine {
     }
     if (pack_runs(T.n)) {
       Run r = spill_packed(T);
+      if (!r.host) {   // stream-ordered D2D copy: T's buffers are reusable right away
+        T.n = 0;
+        runs.push_back(r);
+        account_written(r);
+        return;
+      }
       CK(cudaEventRecord(spill_done, d2h));
       cudaEvent_t bev;
       if (!busy_ev_pool.empty()) { bev = busy_ev_pool.back(); busy_ev_pool.pop_back(); }
@@ -940,7 +999,7 @@ struct Engine {
       return;
     }
     Run r = alloc_run(T.n);
-    if (cfg.run_tier == ISA_TIER_HOST) {
+    if (r.host) {
       // copy on the d2h stream after the table is complete; the table's
       // buffers are recycled only after the copy finished (busy list)
       cudaEvent_t ev;
@@ -1092,8 +1151,10 @@ struct Engine {
     ab_miss_cnt.ensure((size_t)(grid + 1) * 4);
     ab_miss_off.ensure((size_t)(grid + 1) * 4);
     ph_begin(ISA_PH_ABSORB);
+    kt_begin(KF_ABSORB, st);
     absorb_tiny(KW, nt, kd, sd, row0, n, tiny, grid, rpc, ab_partials.as<u64>(), ab_miss_buf.as<u32>(),
                 ab_miss_cnt.as<u32>(), st);
+    kt_end(KF_ABSORB, (int64_t)n * absorb_row_bytes, st);
     ph_end(ISA_PH_ABSORB, n, (int64_t)n * absorb_row_bytes);
     *grid_out = grid;
     *rpc_out = rpc;
@@ -1270,36 +1331,39 @@ struct Engine {
     std::vector<u64> tmp_lo(std::max<int64_t>(total_s, 1)), tmp_hi(std::max<int64_t>(total_s, 1), 0);
     CK(cudaEventSynchronize(spill_done));   // the host reads host-tier runs directly
     {
-      int64_t o = 0;
-      for (auto& r : runs) {   // every strided sample copy first, one synchronization after
-        int64_t ns = (r.rows + F - 1) / F;
-        if (ns == 0) continue;
-        if (!r.path.empty()) {
-          // high key of the page holding the sampled row (>= its key)
-          for (int64_t i = 0; i < ns; ++i) {
-            const u32 pg = (u32)((i * F) / ps0.P);
-            tmp_lo[o + i] = r.hk_lo[pg];
-            if (KW == 2) tmp_hi[o + i] = r.hk_hi[pg];
-          }
-        } else if (r.pk_host) {
-          // block minima of the key words: (hi of the block's first row,
-          // lowest lo of the block) <= the first key -- split points only
-          // need to be keys in range, slice bounds are searched exactly
-          const int ncol = KW + S;
-          for (int64_t i = 0; i < ns; ++i) {
-            const u64* blk = (const u64*)(r.pk_host + r.off_host[(i * F) / PK_ROWS]);
-            tmp_lo[o + i] = blk[0];
-            if (KW == 2) tmp_hi[o + i] = blk[2];
-            (void)ncol;
-          }
-        } else if (r.host) {
-          for (int64_t i = 0; i < ns; ++i) {
-            tmp_lo[o + i] = r.host_lo[i * F];
-            if (KW == 2) tmp_hi[o + i] = r.host_hi[i * F];
-          }
-        } else {
-          CK(cudaMemcpy2DAsync(tmp_lo.data() + o, 8, r.lo, F * 8, 8, ns, cudaMemcpyDeviceToHost, st));
-          if (KW == 2) CK(cudaMemcpy2DAsync(tmp_hi.data() + o, 8, r.hi, F * 8, 8, ns, cudaMemcpyDeviceToHost, st));
+      // FileStore runs: the high key of the page holding each sampled row
+      // (>= its key; split points only need to be keys in range, slice
+      // bounds are searched exactly); every other run: the sampled rows'
+      // keys, read by one kernel (HBM, mapped host memory, packed blocks)
+      std::vector<int64_t> soff(k + 1, 0);
+      std::vector<RunRef> refs(k);
+      for (int i = 0; i < k; ++i) {
+        const Run& r = runs[i];
+        const int64_t ns = r.path.empty() ? (r.rows + F - 1) / F : 0;
+        soff[i + 1] = soff[i] + ns;
+        refs[i] = RunRef{r.lo, r.hi, r.rows, S, r.pk_dev, r.off_dev};
+      }
+      const int64_t dev_s = soff[k];
+      if (dev_s > 0) {
+        runref_dev.ensure(sizeof(RunRef) * k);
+        bounds_out.ensure(8 * (size_t)(k + 1));
+        bounds_lo.ensure(8 * (size_t)dev_s);
+        bounds_hi.ensure(8 * (size_t)dev_s);
+        CK(cudaMemcpyAsync(runref_dev.p, refs.data(), sizeof(RunRef) * k, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(bounds_out.p, soff.data(), 8 * (size_t)(k + 1), cudaMemcpyHostToDevice, st));
+        run_samples(KW, runref_dev.as<RunRef>(), k, (const int64_t*)bounds_out.p, F, dev_s, bounds_lo.as<u64>(),
+                    bounds_hi.as<u64>(), st);
+        CK(cudaMemcpyAsync(tmp_lo.data(), bounds_lo.p, 8 * (size_t)dev_s, cudaMemcpyDeviceToHost, st));
+        if (KW == 2) CK(cudaMemcpyAsync(tmp_hi.data(), bounds_hi.p, 8 * (size_t)dev_s, cudaMemcpyDeviceToHost, st));
+      }
+      int64_t o = dev_s;
+      for (auto& r : runs) {
+        if (r.path.empty()) continue;
+        const int64_t ns = (r.rows + F - 1) / F;
+        for (int64_t i = 0; i < ns; ++i) {
+          const u32 pg = (u32)((i * F) / ps0.P);
+          tmp_lo[o + i] = r.hk_lo[pg];
+          if (KW == 2) tmp_hi[o + i] = r.hk_hi[pg];
         }
         o += ns;
       }
@@ -1394,6 +1458,7 @@ struct Engine {
       size_t poff = 0;
       auto& desc = desc_host[slot];
       desc.clear();
+      int64_t unpack_bytes = 0;   // packed bytes read + rows written
       auto& prefs = pref_host[slot];
       prefs.clear();
       size_t fbytes = 0;
@@ -1425,23 +1490,29 @@ struct Engine {
           off += cnt;
           continue;
         }
-        if (runs[r].pk_host) {
-          // covering blocks' bytes, then one unpack descriptor per block
+        if (runs[r].pk_host || runs[r].pk_dev) {
+          // covering blocks' bytes (host runs: copied into the staging
+          // area; HBM runs: read in place), one unpack descriptor per block
           const u32 b0 = s0 / PK_ROWS, b1 = (s1 - 1) / PK_ROWS;
           const u32 o0 = runs[r].off_host[b0], o1 = runs[r].off_host[b1 + 1];
-          CK(cudaMemcpyAsync(stg_pk[slot].as<char>() + poff, runs[r].pk_host + o0, o1 - o0, cudaMemcpyHostToDevice, h2d));
-          led.bytes_h2d += o1 - o0;
+          const bool on_host = runs[r].pk_host != nullptr;
+          if (on_host) {
+            CK(cudaMemcpyAsync(stg_pk[slot].as<char>() + poff, runs[r].pk_host + o0, o1 - o0, cudaMemcpyHostToDevice, h2d));
+            led.bytes_h2d += o1 - o0;
+          }
+          const u64 src0 = on_host ? (u64)(uintptr_t)(stg_pk[slot].as<char>() + poff) : (u64)(uintptr_t)(runs[r].pk_dev + o0);
           for (u32 b = b0; b <= b1; ++b) {
             const u32 r0 = b * PK_ROWS;
             UnpackBlk d;
-            d.src_off = poff + (runs[r].off_host[b] - o0);
+            d.src_off = src0 + (runs[r].off_host[b] - o0);
             d.e0 = std::max(s0, r0) - r0;
             d.e1 = std::min<u32>(s1, std::min<u32>(r0 + PK_ROWS, runs[r].rows)) - r0;
             d.dst = (u32)(off + (r0 + d.e0 - s0));
             d.pad = 0;
             desc.push_back(d);
           }
-          poff += o1 - o0;
+          if (on_host) poff += o1 - o0;
+          unpack_bytes += (int64_t)(o1 - o0) + (int64_t)cnt * 8 * (KW + S);
           off += cnt;
           continue;
         }
@@ -1480,8 +1551,10 @@ struct Engine {
         CK(cudaMemcpyAsync(stg_desc[slot].p, desc_pinned[slot], desc.size() * sizeof(UnpackBlk),
                            cudaMemcpyHostToDevice, h2d));
         CK(cudaEventRecord(desc_done[slot], h2d));
+        kt_begin(KF_UNPACK, h2d);
         unpack_blocks(stg_desc[slot].as<UnpackBlk>(), (u32)desc.size(), stg_pk[slot].as<char>(), KW, S, fmask,
                       stg_lo[slot].as<u64>(), stg_hi[slot].as<u64>(), stg_st[slot].as<u64>(), h2d);
+        kt_end(KF_UNPACK, unpack_bytes, h2d);
       }
       CK(cudaEventRecord(stg_ready[slot], h2d));
       return off;
@@ -1542,6 +1615,7 @@ struct Engine {
 
   void append_result(Table& w) {
     size_t need = (size_t)result.n + w.n;
+    if (need > 0xFFFFFFFFull) throw IsaError(ISA_ERR_INVALID_INPUT, "more than 2^32-1 output groups are not supported");
     if (need > result.lo.bytes / 8) grow_result(need);
     CK(cudaMemcpyAsync(result.plo() + result.n, w.plo(), (size_t)w.n * 8, cudaMemcpyDeviceToDevice, st));
     if (KW == 2) CK(cudaMemcpyAsync(result.phi() + result.n, w.phi(), (size_t)w.n * 8, cudaMemcpyDeviceToDevice, st));
@@ -1629,6 +1703,8 @@ struct Engine {
         if (group.size() == 1) { nxt.push_back(group[0]); continue; }
         int64_t total = 0;
         for (auto& r : group) total += r.rows;
+        if (total > (int64_t)0xFFFFFFFFll)
+          throw IsaError(ISA_ERR_INVALID_INPUT, "a traditional merge step of more than 2^32-1 rows is not supported");
         const bool collapse = collapse_allowed && total >= o_est;
         Run out = alloc_run((u32)total);
         out.level = level;
@@ -1706,6 +1782,13 @@ struct Engine {
     for (auto& rh : rank_hint) { memset(rh.h, 0xFF, sizeof(rh.h)); rh.bit_lo = -1; rh.npass = 0; }
     led.rows_seen = n;
     if (n == 0) { led.kernel_launches = 0; return 0; }
+    dev_packed = false;
+    hbm_left = 0;
+    if (cfg.run_tier == ISA_TIER_AUTO) {
+      size_t fr = 0, tot = 0;
+      CK(cudaMemGetInfo(&fr, &tot));
+      hbm_left = cfg.hbm_run_budget > 0 ? cfg.hbm_run_budget : (int64_t)(0.4 * (double)fr);
+    }
     if (cfg.merge_mode != ISA_MERGE_WIDE) {
       auto t0p = std::chrono::steady_clock::now();
       int64_t g = execute_pq(n, key_cols, val_cols, on_host);
@@ -1797,7 +1880,7 @@ struct Engine {
     // next, so a PCIe round trip would buy nothing (the ledger counts it as
     // written like every run)
     if (!runs.empty()) {
-      if (cfg.run_tier == ISA_TIER_HOST && T.n > 0) {
+      if ((cfg.run_tier == ISA_TIER_HOST || cfg.run_tier == ISA_TIER_AUTO) && T.n > 0) {
         Run r;
         r.rows = T.n;
         r.host = false;
@@ -1874,7 +1957,9 @@ struct Engine {
       ed.key_dst[c] = !key_out[c] ? nullptr : (out_on_host ? (void*)(out_tmp.as<char>() + koff[c]) : key_out[c]);
     for (int s = 0; s < S; ++s)
       ed.slot_dst[s] = !slot_out[s] ? nullptr : (out_on_host ? (void*)(out_tmp.as<char>() + soff[s]) : slot_out[s]);
+    kt_begin(KF_EXPORT, st);
     export_all(result.plo(), KW == 2 ? result.phi() : nullptr, result.pst(), n, ed, st);
+    kt_end(KF_EXPORT, (int64_t)n * 2 * (8 * KW + 8 * S), st);
     if (!out_on_host) return;
     for (int c = 0; c < kd0.ncols; ++c)
       if (key_out[c])
@@ -2268,6 +2353,16 @@ int isa_phase_stats(isa_handle* h, isa_phase* out, int cap) {
 }
 
 int64_t isa_launch_count(void) { return (int64_t)isa::g_launches.load(); }
+
+void isa_set_kernel_timing(int32_t on) { isa::kt_set(on != 0); }
+
+int isa_kernel_stats(isa_kstat* out, int cap) {
+  double ms[isa::KF_COUNT];
+  int64_t la[isa::KF_COUNT], by[isa::KF_COUNT];
+  isa::kt_collect(ms, la, by);
+  for (int f = 0; f < isa::KF_COUNT && f < cap; ++f) out[f] = isa_kstat{ms[f], la[f], by[f]};
+  return isa::KF_COUNT;
+}
 
 int64_t isa_run_rows(isa_handle* h, int64_t* out, int64_t cap) {
   if (!h) return -1;

@@ -17,6 +17,68 @@ namespace isa {
 
 std::atomic<long long> g_launches{0};
 
+// ------------------------------------------------------- kernel timer ---
+namespace {
+struct KtRec { int fam; cudaEvent_t a, b; int64_t bytes; };
+struct KTimer {
+  bool on = false;
+  std::vector<KtRec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t open[KF_COUNT] = {};
+  double ms[KF_COUNT] = {};
+  int64_t launches[KF_COUNT] = {}, bytes[KF_COUNT] = {};
+  cudaEvent_t get() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+thread_local KTimer g_kt;
+}  // namespace
+
+bool kt_enabled() { return g_kt.on; }
+void kt_set(bool on) { g_kt.on = on; }
+void kt_begin(int fam, cudaStream_t st) {
+  if (!g_kt.on) return;
+  cudaEvent_t e = g_kt.get();
+  cudaEventRecord(e, st);
+  g_kt.open[fam] = e;
+}
+void kt_end(int fam, int64_t alg_bytes, cudaStream_t st) {
+  if (!g_kt.on || !g_kt.open[fam]) return;
+  cudaEvent_t e = g_kt.get();
+  cudaEventRecord(e, st);
+  g_kt.recs.push_back({fam, g_kt.open[fam], e, alg_bytes});
+  g_kt.open[fam] = nullptr;
+}
+void kt_add_bytes(int fam, int64_t alg_bytes) {
+  if (!g_kt.on) return;
+  for (size_t i = g_kt.recs.size(); i-- > 0;)
+    if (g_kt.recs[i].fam == fam) { g_kt.recs[i].bytes += alg_bytes; return; }
+}
+void kt_collect(double* ms, int64_t* launches, int64_t* bytes) {
+  for (auto& r : g_kt.recs) {
+    float t = 0;
+    if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) {
+      g_kt.ms[r.fam] += t;
+      g_kt.launches[r.fam] += 1;
+      g_kt.bytes[r.fam] += r.bytes;
+    }
+    g_kt.pool.push_back(r.a);
+    g_kt.pool.push_back(r.b);
+  }
+  g_kt.recs.clear();
+  for (int f = 0; f < KF_COUNT; ++f) {
+    if (ms) ms[f] = g_kt.ms[f];
+    if (launches) launches[f] = g_kt.launches[f];
+    if (bytes) bytes[f] = g_kt.bytes[f];
+    g_kt.ms[f] = 0;
+    g_kt.launches[f] = 0;
+    g_kt.bytes[f] = 0;
+  }
+}
+
 // ============================================================== scan ====
 #define SC_THREADS 256
 #define SC_ITEMS 16
@@ -360,8 +422,8 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
                      int start) {
   int cur = start;
   if (n <= 1 || bit_hi <= bit_lo) return cur;
-  static bool attr_set[3] = {false, false, false};
-  if (!attr_set[KW]) {
+  static std::atomic<unsigned long long> attr_set[3];
+  if (first_on_device(attr_set[KW])) {
     if (KW == 1) {
       const int ps = (int)rs_scatter_smem(1, true);
       cudaFuncSetAttribute(k_rs_scatter<1, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ps);
@@ -378,7 +440,6 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
       cudaFuncSetAttribute(k_rs_scatter<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_scatter_smem(1));
       cudaFuncSetAttribute(k_rs_scatter<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_scatter_smem(1));
     }
-    attr_set[KW] = true;
   }
   const u32 ntiles = (n + RS_TILE - 1) / RS_TILE;
   const size_t smem = rs_scatter_smem(KW);
@@ -398,8 +459,10 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
     if (npass > RS_MAX_PASS) throw std::runtime_error("radix sort: too many passes");
     cudaMemsetAsync(ghist, 0, (RS_MAX_PASS * 256 + RS_MAX_PASS) * 4, st);
     const u32 g = std::min<u32>(ntiles, 148u * 8u);
+    kt_begin(KF_HIST, st);
     if (KW == 2) klaunch(k_rs_hist_all<2>, g, 256, 0, st, b.lo[cur], b.hi[cur], n, bit_lo, npass, ghist);
     else klaunch(k_rs_hist_all<1>, g, 256, 0, st, b.lo[cur], (const u64*)nullptr, n, bit_lo, npass, ghist);
+    kt_end(KF_HIST, (int64_t)n * 8 * KW, st);
   }
   // ranking per pass: ballots for large passes without heavy digits (one
   // small read-back of the histograms; MATCH.ANY otherwise)
@@ -455,6 +518,10 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
               b.val[cur], b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - bit_lo, stt, gh, tc, ep, bit_lo, \
               pk_const, lb_sleep);                                                                                     \
   } while (0)
+    // algorithmic bytes of the pass: every row's key words + row id read and written once
+    // (packed passes: 8-byte words in the middle, 12 -> 8 / 8 -> 12 at the ends)
+    const int64_t pass_bytes = (int64_t)n * (packed ? (p == 0 || p == npass - 1 ? 20 : 16) : 2 * (8 * KW + 4));
+    kt_begin(KF_SCATTER, st);
     if (packed) {
       if (p == 0) RS_PK(1);
       else if (p == npass - 1) RS_PK(3);
@@ -466,6 +533,7 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
       if (ballot[p]) RS_GO(1, true, (const u64*)nullptr, (u64*)nullptr);
       else RS_GO(1, false, (const u64*)nullptr, (u64*)nullptr);
     }
+    kt_end(KF_SCATTER, pass_bytes, st);
 #undef RS_GO
 #undef RS_PK
     if (launches) *launches += 1;

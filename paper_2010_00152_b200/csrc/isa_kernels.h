@@ -144,7 +144,7 @@ struct RunRef { const u64* lo; const u64* hi; u32 rows; int S; const char* pk; c
 // ---- run codec (isa_codec.cu) -------------------------------------------
 #define PK_ROWS 1024
 struct PackSrc { const u64* lo; const u64* hi; const u64* st; u32 n; int kw; int S; u32 fmask; };
-struct UnpackBlk { u64 src_off; u32 e0, e1, dst, pad; };
+struct UnpackBlk { u64 src_off; u32 e0, e1, dst, pad; };   // src_off: absolute device address of the block
 u32 pack_blocks(u32 n);
 // per-block headers (ncol x 2 u64) and byte sizes
 void pack_sizes(const PackSrc& p, u64* hdr, u32* blk_bytes, cudaStream_t st);
@@ -169,6 +169,9 @@ void page_encode(const PageSpec& ps, const u64* lo, const u64* hi, const u64* st
                  cudaStream_t stream);
 void page_decode(const PageSpec& ps, const PageRef* refs, u32 nrefs, const char* src, u64* lo, u64* hi, u64* st,
                  u32* bad, cudaStream_t stream);
+// keys of rows 0, F, 2F, ... of every run into out (run r's samples from soff_dev[r])
+void run_samples(int KW, const RunRef* runs_dev, int nruns, const int64_t* soff_dev, int64_t F, int64_t total,
+                 u64* out_lo, u64* out_hi, cudaStream_t st);
 void run_lower_bounds(int KW, const RunRef* runs_dev, int nruns, const u64* b_lo, const u64* b_hi,
                       int nb, u32* out, cudaStream_t st);
 

@@ -156,11 +156,9 @@ static size_t tc_smem(int KW, int S) {
 template <int KW, int MS>
 static void tc_launch(const KeyDesc& kd, const SlotDesc& sd, int64_t row0, u32 n, u64* g_lo, u64* g_hi, u32* g_first,
                       u64* g_st, u32* g_count, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr))
     cudaFuncSetAttribute(k_tile_collapse<KW, MS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem(2, 16));
-    attr = true;
-  }
   const u32 tiles = (n + TC_TILE - 1) / TC_TILE;
   klaunch(k_tile_collapse<KW, MS>, tiles, TC_THREADS, tc_smem(KW, sd.nslots), st, kd, sd, row0, n, g_lo, g_hi, g_first,
           g_st, g_count);

@@ -65,7 +65,8 @@ class SortAggConfig:
     output_size_hint: int | None = None
     max_preliminary_merges: int | None = None
     # B200 placement knobs (no reference counterpart)
-    run_tier: str = "host"          # where spilled runs live: "host" (pinned DRAM) | "hbm"
+    run_tier: str = "auto"          # where spilled runs live: "auto" (HBM while they fit, then pinned DRAM) | "host" | "hbm"
+    hbm_run_budget: int = 0         # run_tier "auto": HBM bytes for runs, 0 = 40% of the free HBM
     chunk_rows_max: int = 0         # 0 = library default
     window_rows: int = 0            # host-input staging window, 0 = default
     merge_window_rows: int = 0      # wide-merge key-range window capacity, 0 = default
@@ -84,7 +85,7 @@ class SortAggConfig:
                 f"unknown run generation mode {self.run_generation_mode!r}")
         if self.merge_mode not in (WIDE, TRADITIONAL, SEPARATE):
             raise InvalidInputError(f"unknown merge mode {self.merge_mode!r}")
-        if self.run_tier not in ("host", "hbm"):
+        if self.run_tier not in ("auto", "host", "hbm"):
             raise InvalidInputError(f"unknown run tier {self.run_tier!r}")
         if self.preaggregate not in ("auto", "always", "never"):
             raise InvalidInputError(f"unknown preaggregate mode {self.preaggregate!r}")
@@ -441,7 +442,9 @@ class SortAggregate:
         if isinstance(self.store, FileStore):
             cfg.run_tier = _native.TIER_FILE
         else:
-            cfg.run_tier = _native.TIER_HOST if self.config.run_tier == "host" else _native.TIER_HBM
+            cfg.run_tier = {"host": _native.TIER_HOST, "hbm": _native.TIER_HBM,
+                            "auto": _native.TIER_AUTO}[self.config.run_tier]
+        cfg.hbm_run_budget = self.config.hbm_run_budget
         cfg.device = dev
         cfg.chunk_rows_max = self.config.chunk_rows_max
         cfg.window_rows = self.config.window_rows
@@ -707,10 +710,11 @@ class SortAggregate:
         """Aggregate an iterable of ``Row`` (key tuple, state tuple) and
         return the sorted list of aggregated ``Row`` (sortagg.py:744-747)."""
         rows = list(rows)
-        self.executed_steps = []
-        self.initial_plan = None
-        self.runs_after_generation = 0
         if not rows:
+            # nothing of a previous execute may leak into this one's details
+            self._last = None
+            self._info = {}
+            self._materialize()
             return []
         keys_t, states_t = self._row_columns(rows)
         return self._rows_from(self.execute_columns(keys_t, states_t, states=True))

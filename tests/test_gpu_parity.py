@@ -40,16 +40,18 @@ def _cfg(memory, page, **kw):
 
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("variant", ["device", "host_input", "hbm_runs", "packed_runs", "small_chunks", "k1_always",
-                                     "k1_never"])
+@pytest.mark.parametrize("variant", ["device", "host_input", "hbm_runs", "packed_runs", "host_runs", "small_chunks",
+                                     "k1_always", "k1_never"])
 def test_golden_columns(name, variant):
     g = Golden(name)
     sch = g.schema()
     kw = {}
     if variant == "hbm_runs":
         kw["run_tier"] = "hbm"
-    if variant == "packed_runs":
+    if variant == "packed_runs":   # auto tier: bit-packed runs kept in HBM
         kw["run_codec"] = "packed"
+    if variant == "host_runs":     # pinned host tier, bit-packed across PCIe
+        kw.update(run_tier="host", run_codec="packed")
     if variant == "small_chunks":
         kw.update(chunk_rows_max=5000, merge_window_rows=3000, window_rows=7000, run_codec="packed")
     if variant == "k1_always":
@@ -57,7 +59,7 @@ def test_golden_columns(name, variant):
     if variant == "k1_never":
         kw.update(preaggregate="never")
     mode = str(g.z["merge_mode"]) if "merge_mode" in g.z else "wide"
-    if mode != "wide" and variant in ("k1_always", "k1_never", "small_chunks", "packed_runs"):
+    if mode != "wide" and variant in ("k1_always", "k1_never", "small_chunks", "packed_runs", "host_runs"):
         pytest.skip("pre-aggregation / chunking knobs apply to the wide path only")
     op = isa.SortAggregate(sch, _cfg(g.memory, g.page, merge_mode=mode, **kw))
     n = len(g.keys[0])
@@ -305,8 +307,8 @@ def test_packed_runs_vs_raw(cfg, rows, memory):
     kw = {"domain": 1 << 22} if cfg in (3, 5) else {}
     w = workloads.make(cfg, rows=rows, device="cpu", **kw)
     rel = 1e-5 if cfg == 3 else 1e-9
-    packed = _oracle_case(w, memory, rel=rel, run_codec="packed")
-    raw = _oracle_case(w, memory, rel=rel, run_codec="raw")
+    packed = _oracle_case(w, memory, rel=rel, run_codec="packed", run_tier="host")
+    raw = _oracle_case(w, memory, rel=rel, run_codec="raw", run_tier="host")
     assert packed.run_rows == raw.run_rows and packed.ledger.rows_spilled == raw.ledger.rows_spilled
     assert packed.ledger.rows_read_back == raw.ledger.rows_read_back
     assert 0 < packed.device_ledger["bytes_d2h"] < raw.device_ledger["bytes_d2h"]

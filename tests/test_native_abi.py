@@ -64,3 +64,39 @@ def test_null_handle_contract():
     lib = _native.load()
     assert lib.isa_execute(None, 0, None, None, 0, None, None) == 3   # ISA_ERR_CONTRACT
     assert lib.isa_launch_count() >= 0
+
+
+def test_create_rejects_32bit_overflowing_page_images():
+    """A FileStore run of memory_budget groups whose page image would pass
+    4 GiB is rejected up front (page offsets and sizes are 32-bit)."""
+    cfg = _native.IsaConfig()
+    cfg.memory_budget, cfg.page_capacity = 1 << 30, 100
+    cfg.run_tier = _native.TIER_FILE
+    sch = _native.IsaSchema()
+    sch.n_key_cols = 1
+    sch.key_dtypes[0] = _native.I64
+    sch.n_val_cols = 1
+    sch.val_dtypes[0] = _native.I64
+    sch.n_slots = 2
+    for s in range(2):
+        sch.slot_op[s] = _native.OP_ADD
+        sch.slot_type[s] = _native.SLOT_I64
+        sch.slot_src[s] = _native.SRC_COLUMN
+        sch.slot_col[s] = 0
+    lib = _native.load()
+    assert not lib.isa_create(ctypes.byref(cfg), ctypes.byref(sch))
+    assert b"4 GiB" in lib.isa_last_error(None)
+    cfg.run_tier = _native.TIER_AUTO
+    cfg.hbm_run_budget = -1
+    assert not lib.isa_create(ctypes.byref(cfg), ctypes.byref(sch))
+    assert b"hbm_run_budget" in lib.isa_last_error(None)
+
+
+def test_kernel_timing_toggle_without_a_device():
+    """Kernel-family timing is host bookkeeping: toggling and reading it
+    needs no GPU (nothing recorded -> zeros)."""
+    _native.set_kernel_timing(True)
+    st = _native.kernel_stats()
+    _native.set_kernel_timing(False)
+    assert set(st) == set(_native.KERNEL_FAMILIES)
+    assert all(v["launches"] == 0 for v in st.values())
