@@ -106,6 +106,11 @@ struct DevicePool {
   struct Block { char* p; size_t bytes; size_t used; };
   std::vector<Block> blocks;
   void reset() { for (auto& b : blocks) b.used = 0; }
+  size_t capacity() const {
+    size_t c = 0;
+    for (auto& b : blocks) c += b.bytes;
+    return c;
+  }
   char* alloc(size_t bytes) {
     bytes = (bytes + 255) & ~(size_t)255;
     for (auto& b : blocks)
@@ -139,6 +144,7 @@ struct Table {
 };
 
 struct Run {
+  u32* dir = nullptr;  // bucket directory (isa_merge.cu), device memory, nb + 1 entries
   u64* lo = nullptr;   // host-mapped or device pointer usable by kernels
   u64* hi = nullptr;
   const u64* host_lo = nullptr;   // host view of host-tier runs
@@ -231,6 +237,82 @@ struct Engine {
   DevicePool devpool;
   std::vector<Run> runs;
   cudaEvent_t spill_done = nullptr;
+  // tile merge (isa_merge.cu): bucketing of this execute, run directories
+  Bucketing bk{};
+  bool bk_ready = false;
+  DevicePool dirpool;
+  DevBuf tm_D, tm_P, tm_base, tm_status, tm_dirptrs, tm_scal;
+  i64* tm_base_pin = nullptr;
+  size_t tm_base_cap = 0;
+  size_t tm_status_bytes = 0;
+  int64_t in_n = 0;                 // rows of the current execute's input
+  bool in_on_host = false;
+  const void* in_keys[ISA_MAX_KEY_COLS] = {};
+  static bool tile_merge_env() {
+    static int v = -1;
+    if (v < 0) { const char* e = getenv("ISA_TILE_MERGE"); v = (e && e[0] == '0') ? 0 : 1; }
+    return v == 1;
+  }
+  bool dirs_wanted() const {
+    return tile_merge_env() && cfg.merge_mode == ISA_MERGE_WIDE && cfg.run_tier != ISA_TIER_FILE;
+  }
+  // Bucketing for the run directories, chosen at the first spill: the key
+  // range of the first run (a sorted table: first and last key), widened by
+  // the sampled range of the whole input when it is on the device; nb
+  // buckets of ~ a quarter tile each.
+  void ensure_bucketing() {
+    if (bk_ready) return;
+    to_host(T.plo(), 8, 0);
+    to_host(T.plo() + (T.n - 1), 8, 2);
+    if (KW == 2) { to_host(T.phi(), 8, 4); to_host(T.phi() + (T.n - 1), 8, 6); }
+    sync();
+    const u64* hw = (const u64*)h_scal;
+    u64 mnl = hw[0], mxl = hw[1], mnh = KW == 2 ? hw[2] : 0, mxh = KW == 2 ? hw[3] : 0;
+    auto less = [](u64 ah, u64 al, u64 bh, u64 bl) { return ah < bh || (ah == bh && al < bl); };
+    if (!in_on_host && in_n > 0) {
+      const int64_t want = 1 << 16;
+      const int64_t stride = std::max<int64_t>(1, in_n / want);
+      const int64_t ns = (in_n + stride - 1) / stride;
+      tm_scal.ensure((size_t)ns * 16 + 64);
+      u64* dlo = tm_scal.as<u64>();
+      u64* dhi = dlo + ns;
+      isa::sample_keys(kd_at(in_keys), in_n, stride, dlo, dhi, st);
+      std::vector<u64> hl(ns), hh(ns, 0);
+      CK(cudaMemcpyAsync(hl.data(), dlo, 8 * ns, cudaMemcpyDeviceToHost, st));
+      if (KW == 2) CK(cudaMemcpyAsync(hh.data(), dhi, 8 * ns, cudaMemcpyDeviceToHost, st));
+      sync();
+      for (int64_t i = 0; i < ns; ++i) {
+        if (less(hh[i], hl[i], mnh, mnl)) { mnh = hh[i]; mnl = hl[i]; }
+        if (less(mxh, mxl, hh[i], hl[i])) { mxh = hh[i]; mxl = hl[i]; }
+      }
+    }
+    // range and a 1/16 margin on both sides (saturating)
+    unsigned __int128 mn = ((unsigned __int128)mnh << 64) | mnl, mx = ((unsigned __int128)mxh << 64) | mxl;
+    const unsigned __int128 top = KW == 2 ? ~(unsigned __int128)0 : (unsigned __int128)(~0ull);
+    const unsigned __int128 span = mx - mn, pad = span / 16;
+    mn = mn > pad ? mn - pad : 0;
+    mx = top - mx > pad ? mx + pad : top;
+    const unsigned __int128 range = mx - mn;
+    int rbits = 0;
+    for (unsigned __int128 x = range; x; x >>= 1) ++rbits;
+    const int64_t kest = std::max<int64_t>(2, in_n / std::max<int64_t>(1, cfg.memory_budget) + 2);
+    const u32 cap = std::max<u32>(256, tile_merge_cap(KW, S, (int)std::min<int64_t>(kest, 4096)));
+    int lnb = 8;
+    while (lnb < 22 && ((int64_t)1 << lnb) * (int64_t)cap < 4 * in_n) ++lnb;
+    bk.g_lo = (u64)mn;
+    bk.g_hi = (u64)(mn >> 64);
+    bk.nb = 1u << lnb;
+    bk.shift = std::max(0, rbits - lnb);
+    bk_ready = true;
+  }
+  // directory of the sorted table T (about to become a run)
+  u32* make_dir() {
+    if (!dirs_wanted() || T.n == 0) return nullptr;
+    ensure_bucketing();
+    u32* d = (u32*)dirpool.alloc((size_t)(bk.nb + 1) * 4);
+    dir_build(KW, T.plo(), T.phi(), T.n, bk, d, st);
+    return d;
+  }
   // wide merge
   DevBuf stg_lo[2], stg_hi[2], stg_st[2];
   cudaEvent_t stg_ready[2] = {nullptr, nullptr}, stg_free[2] = {nullptr, nullptr};
@@ -334,7 +416,8 @@ struct Engine {
                       &mg_rank_b, &mg_match_b, &ab_partials, &ab_miss_buf, &ab_miss_cnt, &ab_miss_off,
                       &miss_list, &stg_lo[0], &stg_lo[1], &stg_hi[0], &stg_hi[1], &stg_st[0], &stg_st[1],
                       &runref_dev, &bounds_lo, &bounds_hi, &bounds_out, &out_tmp, &pk_hdr, &pk_sz,
-                      &stg_pk[0], &stg_pk[1], &stg_desc[0], &stg_desc[1], &t_backup, &pk_status, &rec_buf};
+                      &stg_pk[0], &stg_pk[1], &stg_desc[0], &stg_desc[1], &t_backup, &pk_status, &rec_buf,
+                      &tm_D, &tm_P, &tm_base, &tm_status, &tm_dirptrs, &tm_scal};
     for (int i = 0; i < 2; ++i) {
       if (desc_pinned[i]) cudaFreeHost(desc_pinned[i]);
       if (desc_done[i]) cudaEventDestroy(desc_done[i]);
@@ -355,6 +438,8 @@ struct Engine {
     for (auto e : busy_ev_pool) cudaEventDestroy(e);
     pinned.release();
     devpool.release();
+    dirpool.release();
+    if (tm_base_pin) cudaFreeHost(tm_base_pin);
     if (h_scal) cudaFreeHost(h_scal);
     if (h_hist) cudaFreeHost(h_hist);
     if (h2d) cudaStreamDestroy(h2d);
@@ -979,8 +1064,10 @@ struct Engine {
       account_written(r);
       return;
     }
+    u32* dir = make_dir();
     if (pack_runs(T.n)) {
       Run r = spill_packed(T);
+      r.dir = dir;
       if (!r.host) {   // stream-ordered D2D copy: T's buffers are reusable right away
         T.n = 0;
         runs.push_back(r);
@@ -999,6 +1086,7 @@ struct Engine {
       return;
     }
     Run r = alloc_run(T.n);
+    r.dir = dir;
     if (r.host) {
       // copy on the d2h stream after the table is complete; the table's
       // buffers are recycled only after the copy finished (busy list)
@@ -1315,7 +1403,155 @@ struct Engine {
   // keys, slices staged double-buffered, each window radix-sorted); every
   // window's sorted output -- collapsed into unique groups, or with
   // duplicates kept -- is handed to emit(table, distinct keys).
-  void merge_runs(std::vector<Run>& rs, bool collapse, const std::function<void(Table&, u32)>& emit) {
+  // Windows from run directories (tile merge): window w = buckets
+  // [wb[w], wb[w + 1]); lb[r * nbound + i] = first row of run r at bucket
+  // wb[i + 1]; P at the window boundaries.
+  struct TilePlan {
+    int nbound = 0;
+    std::vector<u32> wb;
+    std::vector<u64> pw;
+    std::vector<u32> lb;
+    u32 cap = 0;
+  };
+  // Output size estimate for the result's first allocation: the largest
+  // run and the OutputEstimator's read-sort-write inversion of the mean fill
+  // cycle, C = O ln(O / (O - M)) (sortagg.py:129-144), capped at the rows.
+  int64_t estimate_groups(int64_t total_rows) {
+    int64_t est = 1;
+    for (auto& r : runs) est = std::max<int64_t>(est, r.rows);
+    if (!cycles.empty()) {
+      double mean = 0;
+      for (auto c : cycles) mean += (double)c;
+      mean /= (double)cycles.size();
+      const double M = (double)cfg.memory_budget;
+      if (mean <= M * (1 + 1e-9)) return total_rows;
+      auto clen = [&](double o) { return o * std::log(o / (o - M)); };
+      double lo = M * (1 + 1e-12), hi = 2 * M;
+      while (clen(hi) > mean && hi < 1e18) hi *= 2;
+      for (int i = 0; i < 80; ++i) {
+        const double mid = 0.5 * (lo + hi);
+        if (clen(mid) > mean) lo = mid; else hi = mid;
+      }
+      est = std::max<int64_t>(est, (int64_t)(0.5 * (lo + hi)));
+    }
+    return std::min(est, total_rows);
+  }
+
+  // Run directories -> D (transposed), P (rows below each bucket), windows
+  // of <= W rows on a coarse grid of bucket boundaries, and the per-run
+  // slice bounds at the window boundaries.  False: use the sampled-window
+  // path (a run without a directory, too many runs for a tile).
+  bool build_tile_plan(TilePlan& tp) {
+    const int k = (int)runs.size();
+    if (!dirs_wanted() || !bk_ready || k < 1) return false;
+    for (auto& r : runs)
+      if (!r.dir) return false;
+    const u32 cap = tile_merge_cap(KW, S, k);
+    if (cap < 512) return false;
+    const u32 nb1 = bk.nb + 1;
+    std::vector<u32*> ptrs(k);
+    for (int r = 0; r < k; ++r) ptrs[r] = runs[r].dir;
+    tm_dirptrs.ensure(sizeof(u32*) * k + 16);
+    CK(cudaMemcpyAsync(tm_dirptrs.p, ptrs.data(), sizeof(u32*) * k, cudaMemcpyHostToDevice, st));
+    tm_D.ensure((size_t)nb1 * k * 4 + 64);
+    tm_P.ensure((size_t)nb1 * 8 + 64);
+    dir_transpose((u32* const*)tm_dirptrs.p, k, nb1, tm_D.as<u32>(), st);
+    dir_rowsum(tm_D.as<u32>(), k, nb1, tm_P.as<u64>(), st);
+    const u32 C = std::min<u32>(1024, bk.nb);   // nb is a power of two >= 256
+    const u32 nc = bk.nb / C + 1;                // coarse points 0, C, 2C, ..., nb
+    std::vector<u64> pc(nc);
+    CK(cudaMemcpy2DAsync(pc.data(), 8, tm_P.p, (size_t)C * 8, 8, nc, cudaMemcpyDeviceToHost, st));
+    sync();
+    int64_t W = cfg.merge_window_rows > 0 ? cfg.merge_window_rows : ((int64_t)48 << 20);
+    tp.wb.assign(1, 0u);
+    tp.pw.assign(1, pc[0]);
+    for (u32 c = 1; c < nc; ++c) {
+      // cut before coarse step c when it would take the window past W rows
+      if ((int64_t)(pc[c] - tp.pw.back()) > W && tp.wb.back() != (c - 1) * C) {
+        tp.wb.push_back((c - 1) * C);
+        tp.pw.push_back(pc[c - 1]);
+      }
+    }
+    tp.wb.push_back(bk.nb);
+    tp.pw.push_back(pc[nc - 1]);
+    tp.nbound = (int)tp.wb.size() - 2;
+    std::vector<u32> rowsb((size_t)std::max(tp.nbound, 1) * k);
+    for (int i = 0; i < tp.nbound; ++i)
+      CK(cudaMemcpyAsync(rowsb.data() + (size_t)i * k, tm_D.as<u32>() + (size_t)tp.wb[i + 1] * k, (size_t)k * 4,
+                         cudaMemcpyDeviceToHost, st));
+    sync();
+    tp.lb.assign((size_t)k * std::max(tp.nbound, 1), 0u);
+    for (int i = 0; i < tp.nbound; ++i)
+      for (int r = 0; r < k; ++r) tp.lb[(size_t)r * tp.nbound + i] = rowsb[(size_t)i * k + r];
+    tp.cap = cap;
+    return true;
+  }
+
+  // One staged window through the tile merge, groups appended to the
+  // result in place.  False: a tile overflowed its capacity (skewed
+  // buckets); the caller merges the window with the radix-sort path.
+  bool tile_window(TilePlan& tp, int w, u32 m, int slot, const std::vector<int64_t>& soff) {
+    const int k = (int)runs.size();
+    if (tm_base_cap < (size_t)k) {
+      if (tm_base_pin) CK(cudaFreeHost(tm_base_pin));
+      tm_base_cap = (size_t)k + 64;
+      CK(cudaHostAlloc((void**)&tm_base_pin, tm_base_cap * 8, cudaHostAllocDefault));
+    }
+    for (int r = 0; r < k; ++r) {
+      const i64 s0 = w == 0 ? 0 : (i64)tp.lb[(size_t)r * tp.nbound + (w - 1)];
+      tm_base_pin[r] = (i64)soff[r] - s0;
+    }
+    tm_base.ensure((size_t)k * 8 + 16);
+    CK(cudaMemcpyAsync(tm_base.p, tm_base_pin, (size_t)k * 8, cudaMemcpyHostToDevice, st));
+    const u32 target = tp.cap / 2;
+    const u64 rows = tp.pw[w + 1] - tp.pw[w];
+    const u32 ntiles = (u32)((rows + target - 1) / target);
+    if ((size_t)result.n + m > result.lo.bytes / 8) grow_result((size_t)result.n + m);
+    const size_t need = (size_t)ntiles * 8 + 64;
+    if (tm_status_bytes < need) {
+      tm_status.ensure(need);
+      tm_status_bytes = tm_status.bytes;
+      CK(cudaMemsetAsync(tm_status.p, 0, tm_status.bytes, st));   // epoch 0: never a live status word
+    }
+    TileMergeArgs a;
+    memset(&a, 0, sizeof(a));
+    a.P = tm_P.as<u64>();
+    a.D = tm_D.as<u32>();
+    a.base = (const i64*)tm_base.p;
+    a.k = k;
+    a.b_lo = tp.wb[w];
+    a.b_hi = tp.wb[w + 1];
+    a.target = target;
+    a.ntiles = ntiles;
+    a.cap = tp.cap;
+    a.s_lo = stg_lo[slot].as<u64>();
+    a.s_hi = KW == 2 ? stg_hi[slot].as<u64>() : nullptr;
+    a.s_st = S ? stg_st[slot].as<u64>() : nullptr;
+    a.sd = sd0;
+    a.out_lo = result.plo() + result.n;
+    a.out_hi = KW == 2 ? result.phi() + result.n : nullptr;
+    a.out_st = S ? result.pst() + (size_t)result.n * S : nullptr;
+    a.status = tm_status.as<u64>();
+    a.ticket = dscal32(19);
+    a.total = dscal32(20);
+    a.overflow = dscal32(21);
+    CK(cudaMemsetAsync(dscal32(20), 0, 2 * sizeof(u32), st));
+    ph_begin(ISA_PH_WM_COLLAPSE);
+    kt_begin(KF_MERGE, st);
+    tile_merge(KW, a, st);
+    kt_end(KF_MERGE, (int64_t)m * (8 * KW + 8 * S), st);
+    to_host(dscal32(20), 2 * sizeof(u32));
+    ph_end(ISA_PH_WM_COLLAPSE, m, 0);
+    sync();
+    const u32 groups = h_scal[0], over = h_scal[1];
+    if (over) return false;
+    kt_add_bytes(KF_MERGE, (int64_t)groups * (8 * KW + 8 * S));
+    result.n += groups;
+    return true;
+  }
+
+  void merge_runs(std::vector<Run>& rs, bool collapse, const std::function<void(Table&, u32)>& emit,
+                  TilePlan* tp = nullptr) {
     auto& runs = rs;
     const int k = (int)runs.size();
     int64_t total = 0;
@@ -1323,90 +1559,97 @@ struct Engine {
     CK(cudaStreamWaitEvent(st, spill_done, 0));
     int64_t W = cfg.merge_window_rows > 0 ? cfg.merge_window_rows : ((int64_t)48 << 20);
     W = std::max<int64_t>(W, (int64_t)k * 64);
-    // ---- plan windows from sampled keys (every F-th row of each run)
-    int64_t F = std::max<int64_t>(1, W / (8 * (int64_t)k));
-    std::vector<std::pair<u64, u64>> samples;   // (hi, lo)
-    int64_t total_s = 0;
-    for (auto& r : runs) total_s += (r.rows + F - 1) / F;
-    std::vector<u64> tmp_lo(std::max<int64_t>(total_s, 1)), tmp_hi(std::max<int64_t>(total_s, 1), 0);
     CK(cudaEventSynchronize(spill_done));   // the host reads host-tier runs directly
-    {
-      // FileStore runs: the high key of the page holding each sampled row
-      // (>= its key; split points only need to be keys in range, slice
-      // bounds are searched exactly); every other run: the sampled rows'
-      // keys, read by one kernel (HBM, mapped host memory, packed blocks)
-      std::vector<int64_t> soff(k + 1, 0);
-      std::vector<RunRef> refs(k);
-      for (int i = 0; i < k; ++i) {
-        const Run& r = runs[i];
-        const int64_t ns = r.path.empty() ? (r.rows + F - 1) / F : 0;
-        soff[i + 1] = soff[i] + ns;
-        refs[i] = RunRef{r.lo, r.hi, r.rows, S, r.pk_dev, r.off_dev};
-      }
-      const int64_t dev_s = soff[k];
-      if (dev_s > 0) {
-        runref_dev.ensure(sizeof(RunRef) * k);
-        bounds_out.ensure(8 * (size_t)(k + 1));
-        bounds_lo.ensure(8 * (size_t)dev_s);
-        bounds_hi.ensure(8 * (size_t)dev_s);
-        CK(cudaMemcpyAsync(runref_dev.p, refs.data(), sizeof(RunRef) * k, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(bounds_out.p, soff.data(), 8 * (size_t)(k + 1), cudaMemcpyHostToDevice, st));
-        run_samples(KW, runref_dev.as<RunRef>(), k, (const int64_t*)bounds_out.p, F, dev_s, bounds_lo.as<u64>(),
-                    bounds_hi.as<u64>(), st);
-        CK(cudaMemcpyAsync(tmp_lo.data(), bounds_lo.p, 8 * (size_t)dev_s, cudaMemcpyDeviceToHost, st));
-        if (KW == 2) CK(cudaMemcpyAsync(tmp_hi.data(), bounds_hi.p, 8 * (size_t)dev_s, cudaMemcpyDeviceToHost, st));
-      }
-      int64_t o = dev_s;
-      for (auto& r : runs) {
-        if (r.path.empty()) continue;
-        const int64_t ns = (r.rows + F - 1) / F;
-        for (int64_t i = 0; i < ns; ++i) {
-          const u32 pg = (u32)((i * F) / ps0.P);
-          tmp_lo[o + i] = r.hk_lo[pg];
-          if (KW == 2) tmp_hi[o + i] = r.hk_hi[pg];
+    int nb = 0;
+    std::vector<u32> lb;
+    if (tp) {
+      nb = tp->nbound;
+      lb = tp->lb;
+    } else {
+      // ---- plan windows from sampled keys (every F-th row of each run)
+      int64_t F = std::max<int64_t>(1, W / (8 * (int64_t)k));
+      std::vector<std::pair<u64, u64>> samples;   // (hi, lo)
+      int64_t total_s = 0;
+      for (auto& r : runs) total_s += (r.rows + F - 1) / F;
+      std::vector<u64> tmp_lo(std::max<int64_t>(total_s, 1)), tmp_hi(std::max<int64_t>(total_s, 1), 0);
+      {
+        // FileStore runs: the high key of the page holding each sampled row
+        // (>= its key; split points only need to be keys in range, slice
+        // bounds are searched exactly); every other run: the sampled rows'
+        // keys, read by one kernel (HBM, mapped host memory, packed blocks)
+        std::vector<int64_t> soff(k + 1, 0);
+        std::vector<RunRef> refs(k);
+        for (int i = 0; i < k; ++i) {
+          const Run& r = runs[i];
+          const int64_t ns = r.path.empty() ? (r.rows + F - 1) / F : 0;
+          soff[i + 1] = soff[i] + ns;
+          refs[i] = RunRef{r.lo, r.hi, r.rows, S, r.pk_dev, r.off_dev};
         }
-        o += ns;
+        const int64_t dev_s = soff[k];
+        if (dev_s > 0) {
+          runref_dev.ensure(sizeof(RunRef) * k);
+          bounds_out.ensure(8 * (size_t)(k + 1));
+          bounds_lo.ensure(8 * (size_t)dev_s);
+          bounds_hi.ensure(8 * (size_t)dev_s);
+          CK(cudaMemcpyAsync(runref_dev.p, refs.data(), sizeof(RunRef) * k, cudaMemcpyHostToDevice, st));
+          CK(cudaMemcpyAsync(bounds_out.p, soff.data(), 8 * (size_t)(k + 1), cudaMemcpyHostToDevice, st));
+          run_samples(KW, runref_dev.as<RunRef>(), k, (const int64_t*)bounds_out.p, F, dev_s, bounds_lo.as<u64>(),
+                      bounds_hi.as<u64>(), st);
+          CK(cudaMemcpyAsync(tmp_lo.data(), bounds_lo.p, 8 * (size_t)dev_s, cudaMemcpyDeviceToHost, st));
+          if (KW == 2) CK(cudaMemcpyAsync(tmp_hi.data(), bounds_hi.p, 8 * (size_t)dev_s, cudaMemcpyDeviceToHost, st));
+        }
+        int64_t o = dev_s;
+        for (auto& r : runs) {
+          if (r.path.empty()) continue;
+          const int64_t ns = (r.rows + F - 1) / F;
+          for (int64_t i = 0; i < ns; ++i) {
+            const u32 pg = (u32)((i * F) / ps0.P);
+            tmp_lo[o + i] = r.hk_lo[pg];
+            if (KW == 2) tmp_hi[o + i] = r.hk_hi[pg];
+          }
+          o += ns;
+        }
+        sync();
+        samples.reserve(total_s);
+        for (int64_t i = 0; i < total_s; ++i) samples.push_back({tmp_hi[i], tmp_lo[i]});
       }
-      sync();
-      samples.reserve(total_s);
-      for (int64_t i = 0; i < total_s; ++i) samples.push_back({tmp_hi[i], tmp_lo[i]});
-    }
-    std::sort(samples.begin(), samples.end());
-    std::vector<std::pair<u64, u64>> bounds;
-    int64_t acc = (int64_t)k * F;
-    for (auto& s : samples) {
-      if (acc + F > W && (bounds.empty() || bounds.back() != s)) {
-        bounds.push_back(s);
-        acc = (int64_t)k * F;
+      std::sort(samples.begin(), samples.end());
+      std::vector<std::pair<u64, u64>> bounds;
+      int64_t acc = (int64_t)k * F;
+      for (auto& s : samples) {
+        if (acc + F > W && (bounds.empty() || bounds.back() != s)) {
+          bounds.push_back(s);
+          acc = (int64_t)k * F;
+        }
+        acc += F;
       }
-      acc += F;
+      nb = (int)bounds.size();
+      // ---- exact slice boundaries: lower_bound of every bound in every run
+      lb.assign((size_t)k * std::max(nb, 1), 0u);
+      if (nb > 0) {
+        std::vector<RunRef> refs(k);
+        for (int i = 0; i < k; ++i)
+          refs[i] = runs[i].path.empty() ? RunRef{runs[i].lo, runs[i].hi, runs[i].rows, S, runs[i].pk_dev, runs[i].off_dev}
+                                         : RunRef{nullptr, nullptr, 0u, S, nullptr, nullptr};
+        runref_dev.ensure(sizeof(RunRef) * k);
+        bounds_lo.ensure(8 * nb);
+        bounds_hi.ensure(8 * nb);
+        bounds_out.ensure(4 * (size_t)k * nb);
+        std::vector<u64> blo(nb), bhi(nb);
+        for (int i = 0; i < nb; ++i) { bhi[i] = bounds[i].first; blo[i] = bounds[i].second; }
+        CK(cudaMemcpyAsync(runref_dev.p, refs.data(), sizeof(RunRef) * k, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(bounds_lo.p, blo.data(), 8 * nb, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(bounds_hi.p, bhi.data(), 8 * nb, cudaMemcpyHostToDevice, st));
+        run_lower_bounds(KW, runref_dev.as<RunRef>(), k, bounds_lo.as<u64>(), bounds_hi.as<u64>(), nb,
+                         bounds_out.as<u32>(), st);
+        CK(cudaMemcpyAsync(lb.data(), bounds_out.p, 4 * (size_t)k * nb, cudaMemcpyDeviceToHost, st));
+        sync();
+        for (int i = 0; i < k; ++i)   // FileStore runs: searched on the host (page high keys + one page)
+          if (!runs[i].path.empty())
+            for (int b = 0; b < nb; ++b) lb[(size_t)i * nb + b] = file_lower_bound(runs[i], bhi[b], blo[b]);
+      }
     }
-    const int nb = (int)bounds.size();
     const int nwin = nb + 1;
-    // ---- exact slice boundaries: lower_bound of every bound in every run
-    std::vector<u32> lb((size_t)k * std::max(nb, 1));
-    if (nb > 0) {
-      std::vector<RunRef> refs(k);
-      for (int i = 0; i < k; ++i)
-        refs[i] = runs[i].path.empty() ? RunRef{runs[i].lo, runs[i].hi, runs[i].rows, S, runs[i].pk_dev, runs[i].off_dev}
-                                       : RunRef{nullptr, nullptr, 0u, S, nullptr, nullptr};
-      runref_dev.ensure(sizeof(RunRef) * k);
-      bounds_lo.ensure(8 * nb);
-      bounds_hi.ensure(8 * nb);
-      bounds_out.ensure(4 * (size_t)k * nb);
-      std::vector<u64> blo(nb), bhi(nb);
-      for (int i = 0; i < nb; ++i) { bhi[i] = bounds[i].first; blo[i] = bounds[i].second; }
-      CK(cudaMemcpyAsync(runref_dev.p, refs.data(), sizeof(RunRef) * k, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(bounds_lo.p, blo.data(), 8 * nb, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(bounds_hi.p, bhi.data(), 8 * nb, cudaMemcpyHostToDevice, st));
-      run_lower_bounds(KW, runref_dev.as<RunRef>(), k, bounds_lo.as<u64>(), bounds_hi.as<u64>(), nb,
-                       bounds_out.as<u32>(), st);
-      CK(cudaMemcpyAsync(lb.data(), bounds_out.p, 4 * (size_t)k * nb, cudaMemcpyDeviceToHost, st));
-      sync();
-      for (int i = 0; i < k; ++i)   // FileStore runs: searched on the host (page high keys + one page)
-        if (!runs[i].path.empty())
-          for (int b = 0; b < nb; ++b) lb[(size_t)i * nb + b] = file_lower_bound(runs[i], bhi[b], blo[b]);
-    }
     auto slice = [&](int r, int w, u32& s0, u32& s1) {
       s0 = (w == 0) ? 0 : lb[(size_t)r * nb + (w - 1)];
       s1 = (w == nwin - 1) ? runs[r].rows : lb[(size_t)r * nb + w];
@@ -1452,6 +1695,9 @@ struct Engine {
         }
       }
     }
+    std::vector<int64_t> soffs[2];   // staged row of each run's slice, per staging slot
+    soffs[0].assign(k, 0);
+    soffs[1].assign(k, 0);
     auto stage = [&](int w, int slot) -> int64_t {
       CK(cudaStreamWaitEvent(h2d, stg_free[slot], 0));
       int64_t off = 0;
@@ -1466,6 +1712,7 @@ struct Engine {
         u32 s0, s1;
         slice(r, w, s0, s1);
         size_t cnt = s1 - s0;
+        soffs[slot][r] = off;
         if (!cnt) continue;
         if (!runs[r].path.empty()) {
           // FileStore run: read the covering pages back from its file
@@ -1569,6 +1816,10 @@ struct Engine {
       led.rows_read_back += m;
       led.merge_windows++;
       if (m == 0) { CK(cudaEventRecord(stg_free[slot], st)); continue; }
+      if (tp && collapse && tile_window(*tp, w, m, slot, soffs[slot])) {
+        CK(cudaEventRecord(stg_free[slot], st));
+        continue;
+      }
       // sort the window's rows by key: keys copied into sort buffers, value = staged row index
       ensure_sort(m);
       CK(cudaMemcpyAsync(s_lo[0].p, stg_lo[slot].p, (size_t)m * 8, cudaMemcpyDeviceToDevice, st));
@@ -1603,8 +1854,15 @@ struct Engine {
     for (auto& r : runs) total += r.rows;
     const int64_t W = cfg.merge_window_rows > 0 ? cfg.merge_window_rows : ((int64_t)48 << 20);
     result.n = 0;
-    result.reserve(std::max<int64_t>(1, std::min<int64_t>(total, W)), KW, S);
-    merge_runs(runs, true, [&](Table& w, u32) { append_result(w); });
+    TilePlan tp;
+    const bool tiles = build_tile_plan(tp);
+    if (tiles) {   // room for the estimated output (grown by a quarter if short)
+      const int64_t est = estimate_groups(total);
+      result.reserve(std::max<int64_t>(1, std::min<int64_t>(total, est + est / 16 + W)), KW, S);
+    } else {
+      result.reserve(std::max<int64_t>(1, std::min<int64_t>(total, W)), KW, S);
+    }
+    merge_runs(runs, true, [&](Table& w, u32) { append_result(w); }, tiles ? &tp : nullptr);
     if (cfg.run_tier == ISA_TIER_FILE && read_u32(dscal32(12)))
       throw IsaError(ISA_ERR_CORRUPTION, "page checksum mismatch");   // parse_page, runstore.py:132-142
     led.pages_read = led.pages_written;
@@ -1742,7 +2000,8 @@ struct Engine {
   }
 
   void grow_result(size_t need) {
-    size_t cap = std::max(need, result.lo.bytes / 8 * 2);
+    const size_t have = result.lo.bytes / 8;
+    size_t cap = std::max(need, have + have / 4);
     Table nt;
     nt.reserve(cap, KW, S);
     if (result.n) {
@@ -1784,10 +2043,18 @@ struct Engine {
     if (n == 0) { led.kernel_launches = 0; return 0; }
     dev_packed = false;
     hbm_left = 0;
+    bk_ready = false;
+    dirpool.reset();
+    in_n = n;
+    in_on_host = on_host;
+    for (int c = 0; c < sch.n_key_cols; ++c) in_keys[c] = key_cols[c];
     if (cfg.run_tier == ISA_TIER_AUTO) {
       size_t fr = 0, tot = 0;
       CK(cudaMemGetInfo(&fr, &tot));
-      hbm_left = cfg.hbm_run_budget > 0 ? cfg.hbm_run_budget : (int64_t)(0.4 * (double)fr);
+      // half of what is free, counting this handle's own run pool (kept
+      // from the previous execute, reused before anything new is allocated)
+      hbm_left = cfg.hbm_run_budget > 0 ? cfg.hbm_run_budget
+                                        : (int64_t)(0.5 * ((double)fr + (double)devpool.capacity()));
     }
     if (cfg.merge_mode != ISA_MERGE_WIDE) {
       auto t0p = std::chrono::steady_clock::now();
@@ -1882,6 +2149,7 @@ struct Engine {
     if (!runs.empty()) {
       if ((cfg.run_tier == ISA_TIER_HOST || cfg.run_tier == ISA_TIER_AUTO) && T.n > 0) {
         Run r;
+        r.dir = make_dir();
         r.rows = T.n;
         r.host = false;
         r.lo = T.plo();
@@ -2204,6 +2472,7 @@ void isa_destroy(isa_handle* h) {
 int isa_execute(isa_handle* h, int64_t n_rows, const void* const* key_cols, const void* const* val_cols,
                 int32_t input_on_host, void* stream, int64_t* n_groups_out) {
   if (!h) return ISA_ERR_CONTRACT;
+  (void)cudaGetLastError();   // a failed call before this one must not fail this one
   try {
     int64_t g = h->eng->execute(n_rows, key_cols, val_cols, input_on_host != 0, (cudaStream_t)stream);
     if (n_groups_out) *n_groups_out = g;
@@ -2382,6 +2651,7 @@ int isa_sample_keys(isa_handle* h, int64_t n_rows, const void* const* key_cols, 
   try {
     if (stride < 1) throw IsaError(ISA_ERR_INVALID_INPUT, "stride must be positive");
     CK(cudaSetDevice(h->eng->dev));
+    (void)cudaGetLastError();
     KeyDesc kd = h->eng->kd_at(key_cols);
     isa::sample_keys(kd, n_rows, stride, out_lo, out_hi, (cudaStream_t)stream);
     CK(cudaGetLastError());

@@ -175,6 +175,36 @@ void run_samples(int KW, const RunRef* runs_dev, int nruns, const int64_t* soff_
 void run_lower_bounds(int KW, const RunRef* runs_dev, int nruns, const u64* b_lo, const u64* b_hi,
                       int nb, u32* out, cudaStream_t st);
 
+// ---- wide merge by key-range tiles (isa_merge.cu) ---------------------------
+// Monotone bucket function of the normalized key, fixed per execute:
+// bucket = clamp((key - g) >> shift, 0, nb - 1) (keys below g -> 0).
+struct Bucketing { u64 g_lo, g_hi; int shift; u32 nb; };
+// dir[b], b in [0, nb]: first row of the sorted run (lo/hi, n rows) whose bucket is >= b
+void dir_build(int KW, const u64* lo, const u64* hi, u32 n, const Bucketing& bk, u32* dir, cudaStream_t st);
+// D[b * k + r] = dirs[r][b] (dirs_dev: device array of k device pointers)
+void dir_transpose(u32* const* dirs_dev, int k, u32 nb1, u32* D, cudaStream_t st);
+// P[b] = sum_r D[b * k + r]
+void dir_rowsum(const u32* D, int k, u32 nb1, u64* P, cudaStream_t st);
+struct TileMergeArgs {
+  const u64* P;            // [nb + 1] rows below bucket b (all runs)
+  const u32* D;            // [nb + 1][k] first row of run r at bucket >= b
+  const i64* base;         // [k] staged row of run r's row 0 (staged position = base[r] + D[b][r])
+  int k;
+  u32 b_lo, b_hi;          // the window's buckets [b_lo, b_hi)
+  u32 target;              // rows per tile (planned from P)
+  u32 ntiles;
+  u32 cap;                 // rows a tile may hold (tile_merge_cap)
+  const u64* s_lo; const u64* s_hi; const u64* s_st;   // staged window rows
+  SlotDesc sd;             // nslots, op, type
+  u64* out_lo; u64* out_hi; u64* out_st;                // first output group
+  u64* status; u32 epoch; u32* ticket;                  // look-back words (ntiles, epoch-tagged), tile counter
+  u32* total;              // groups written by the window
+  u32* overflow;           // set when a tile holds more than cap rows (the window must be redone)
+};
+// tile capacity in rows for KW key words, S slots and k runs (0: not possible)
+u32 tile_merge_cap(int KW, int S, int k);
+void tile_merge(int KW, TileMergeArgs& a, cudaStream_t st);
+
 // ---- result export --------------------------------------------------------
 // key column c of rows [0, n) -> out (column dtype); slot s -> out (8 bytes)
 void export_key_col(const u64* lo, const u64* hi, u32 n, int dtype, int shift, int width,

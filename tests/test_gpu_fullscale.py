@@ -15,6 +15,18 @@ import paper_2010_00152_b200 as isa  # noqa: E402
 from paper_2010_00152_b200 import workloads  # noqa: E402
 
 
+@pytest.fixture(autouse=True)
+def _free_device_memory():
+    """Full-scale tests hold tens of GB: hand torch's cached blocks back to
+    the driver so the library's own allocations fit."""
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+    yield
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
 def _cfg(w, **kw):
     return isa.SortAggConfig(memory_budget=w.memory_budget, page_capacity=100, **kw)
 

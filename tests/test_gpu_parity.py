@@ -466,3 +466,58 @@ def test_packed_radix_passes_vs_oracle(shift, bits, base):
         x[:2] = torch.tensor([0, (1 << 32) - 1])   # both span ends present
     w.keys[0] = base + (x << shift)
     _oracle_case(w, 1 << 18)
+
+
+def _int_workload(key, val, memory):
+    sch = workloads._int_schema([("n", isa.AggregateKind.COUNT, None), ("s", isa.AggregateKind.SUM, "v"),
+                                 ("lo", isa.AggregateKind.MIN, "v"), ("hi", isa.AggregateKind.MAX, "v")], 1)
+    return workloads.Workload(5, int(key.numel()), sch, [key], {"v": val}, memory)
+
+
+@pytest.mark.parametrize("on_host", [False, True])
+def test_tile_merge_skewed_buckets_fall_back(on_host):
+    """Keys packed into a tiny range next to a few keys spread over int64:
+    the linear bucket function puts most rows into one bucket, the tiles of
+    those windows overflow, and the windows are merged by the radix-sort
+    path instead -- same result as the oracle."""
+    g = torch.Generator().manual_seed(7)
+    n = 600_000
+    dense = torch.randint(0, 3000, (n,), generator=g, dtype=torch.int64)
+    wide = torch.randint(-(1 << 62), 1 << 62, (n // 100,), generator=g, dtype=torch.int64)
+    key = torch.cat([dense, wide])[torch.randperm(n + n // 100, generator=g)]
+    val = torch.randint(-1000, 1000, (key.numel(),), generator=g, dtype=torch.int64)
+    w = _int_workload(key, val, 1 << 10)
+    keys_np = [key.numpy()]
+    slots = oracle.make_states(w.schema, {"v": val.numpy()}, w.rows)
+    want_k, want_s = oracle.reference_aggregate(keys_np, slots, oracle.slot_ops(w.schema))
+    op = isa.SortAggregate(w.schema, _cfg(1 << 10, 100))
+    kk = [key.pin_memory()] if on_host else [key.cuda()]
+    vv = {"v": val.pin_memory() if on_host else val.cuda()}
+    _check(op.execute_columns(kk, vv), want_k, want_s)
+    assert op.runs_after_generation > 1
+
+
+@pytest.mark.parametrize("on_host", [False, True])
+def test_tile_merge_sorted_input(on_host):
+    """Ascending input: every run covers its own key range.  Host input
+    fixes the buckets from the first run only (later keys clamp into the
+    last bucket), device input from a sample of the whole input."""
+    n = 400_000
+    key = torch.arange(n, dtype=torch.int64) * 7 // 3
+    val = torch.arange(n, dtype=torch.int64) % 1000
+    w = _int_workload(key, val, 1 << 12)
+    slots = oracle.make_states(w.schema, {"v": val.numpy()}, n)
+    want_k, want_s = oracle.reference_aggregate([key.numpy()], slots, oracle.slot_ops(w.schema))
+    op = isa.SortAggregate(w.schema, _cfg(1 << 12, 100))
+    kk = [key.pin_memory()] if on_host else [key.cuda()]
+    vv = {"v": val.pin_memory() if on_host else val.cuda()}
+    _check(op.execute_columns(kk, vv), want_k, want_s)
+
+
+@pytest.mark.parametrize("memory", [512, 4096])
+def test_tile_merge_many_runs(memory):
+    """Hundreds to thousands of runs in one wide merge: tiles hold a few
+    rows of every run."""
+    w = workloads.config5(rows=1_000_000, device="cpu", domain=1 << 20)
+    op = _oracle_case(w, memory, page=min(100, memory // 2))
+    assert op.runs_after_generation > 200
