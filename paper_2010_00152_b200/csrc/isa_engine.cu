@@ -201,7 +201,7 @@ struct Engine {
     read_words(d_scal_mapped + host_word_off, (const u32*)dsrc, (u32)((bytes + 3) / 4), st);
   }
   DevBuf bitmap, word_tmp;
-  DevBuf cl_flags, cl_partial, cl_pslot;
+  DevBuf cl_flags, cl_partial, cl_pslot, cl_status, cl_pay;
   DevBuf mg_rank_a, mg_match_a, mg_rank_b, mg_match_b;
   DevBuf ab_partials, ab_miss_buf, ab_miss_cnt, ab_miss_off, miss_list;
   Table T, U;       // resident table, chunk collapse
@@ -241,20 +241,25 @@ struct Engine {
   Bucketing bk{};
   bool bk_ready = false;
   DevicePool dirpool;
-  DevBuf tm_D, tm_P, tm_base, tm_status, tm_dirptrs, tm_scal;
+  DevBuf tm_D, tm_P, tm_base, tm_status, tm_dirptrs, tm_scal, tm_gap, tm_tb;
   i64* tm_base_pin = nullptr;
   size_t tm_base_cap = 0;
   size_t tm_status_bytes = 0;
   int64_t in_n = 0;                 // rows of the current execute's input
   bool in_on_host = false;
   const void* in_keys[ISA_MAX_KEY_COLS] = {};
-  static bool tile_merge_env() {
-    static int v = -1;
-    if (v < 0) { const char* e = getenv("ISA_TILE_MERGE"); v = (e && e[0] == '0') ? 0 : 1; }
-    return v == 1;
+  // ISA_TILE_MERGE=1/0 forces the tile merge on/off; default: on for
+  // 128-bit keys (config 4: wide merge 77 -> 43 ms), off otherwise (the
+  // radix-sorted windows are faster on configs 3 and 5, profiles/r2_ab_merge_collapse.txt)
+  static int tile_merge_env() {   // read per execute (tests switch it)
+    const char* e = getenv("ISA_TILE_MERGE");
+    return !e ? -1 : (e[0] == '0' ? 0 : 1);
   }
+  int tm_mode = -1;   // tile_merge_env() at the start of the current execute
   bool dirs_wanted() const {
-    return tile_merge_env() && cfg.merge_mode == ISA_MERGE_WIDE && cfg.run_tier != ISA_TIER_FILE;
+    const int e = tm_mode;
+    const bool on = e < 0 ? KW == 2 : e == 1;
+    return on && cfg.merge_mode == ISA_MERGE_WIDE && cfg.run_tier != ISA_TIER_FILE;
   }
   // Bucketing for the run directories, chosen at the first spill: the key
   // range of the first run (a sorted table: first and last key), widened by
@@ -310,7 +315,8 @@ struct Engine {
     if (!dirs_wanted() || T.n == 0) return nullptr;
     ensure_bucketing();
     u32* d = (u32*)dirpool.alloc((size_t)(bk.nb + 1) * 4);
-    dir_build(KW, T.plo(), T.phi(), T.n, bk, d, st);
+    tm_gap.ensure(dir_tmp_bytes());
+    dir_build(KW, T.plo(), T.phi(), T.n, bk, d, tm_gap.p, st);
     return d;
   }
   // wide merge
@@ -412,12 +418,12 @@ struct Engine {
     cudaSetDevice(dev);
     cudaDeviceSynchronize();
     DevBuf* bufs[] = {&s_lo[0], &s_lo[1], &s_hi[0], &s_hi[1], &s_val[0], &s_val[1], &tile_hist, &scan_tmp,
-                      &scal, &bitmap, &word_tmp, &cl_flags, &cl_partial, &cl_pslot, &mg_rank_a, &mg_match_a,
+                      &scal, &bitmap, &word_tmp, &cl_flags, &cl_partial, &cl_pslot, &cl_status, &cl_pay, &mg_rank_a, &mg_match_a,
                       &mg_rank_b, &mg_match_b, &ab_partials, &ab_miss_buf, &ab_miss_cnt, &ab_miss_off,
                       &miss_list, &stg_lo[0], &stg_lo[1], &stg_hi[0], &stg_hi[1], &stg_st[0], &stg_st[1],
                       &runref_dev, &bounds_lo, &bounds_hi, &bounds_out, &out_tmp, &pk_hdr, &pk_sz,
                       &stg_pk[0], &stg_pk[1], &stg_desc[0], &stg_desc[1], &t_backup, &pk_status, &rec_buf,
-                      &tm_D, &tm_P, &tm_base, &tm_status, &tm_dirptrs, &tm_scal};
+                      &tm_D, &tm_P, &tm_base, &tm_status, &tm_dirptrs, &tm_scal, &tm_gap, &tm_tb};
     for (int i = 0; i < 2; ++i) {
       if (desc_pinned[i]) cudaFreeHost(desc_pinned[i]);
       if (desc_done[i]) cudaEventDestroy(desc_done[i]);
@@ -599,6 +605,13 @@ struct Engine {
     scan_tmp.ensure((scan_tmp_words((u32)n + 1) + 64) * 4);
   }
   void ensure_collapse(size_t m) {
+    {
+      const size_t nt = collapse_tiles((u32)m, S) + 1;
+      const size_t had = cl_status.bytes;
+      cl_status.ensure(nt * 8 + 64);
+      if (cl_status.bytes != had) CK(cudaMemsetAsync(cl_status.p, 0, cl_status.bytes, st));   // epochs start at 0
+      cl_pay.ensure(nt * 2 * std::max(S, 1) * 8 + 64);
+    }
     cl_flags.ensure((m + 1) * 4);
     cl_pslot.ensure(((size_t)collapse_threads((u32)m, S) + 1) * 4);
     if (S) cl_partial.ensure(((size_t)collapse_threads((u32)m, S) + 1) * 8 * S);
@@ -739,6 +752,9 @@ struct Engine {
     ct.partial = cl_partial.as<u64>();
     ct.partial_slot = cl_pslot.as<u32>();
     ct.total = dscal32(2);
+    ct.status = cl_status.as<u64>();
+    ct.pay = cl_pay.as<u64>();
+    ct.ticket = dscal32(22);
     const int phc = (st_in && merge_phase) ? ISA_PH_WM_COLLAPSE : ISA_PH_COLLAPSE;
     ph_begin(phc);
     kt_begin(KF_COLLAPSE, st);
@@ -1535,6 +1551,8 @@ struct Engine {
     a.ticket = dscal32(19);
     a.total = dscal32(20);
     a.overflow = dscal32(21);
+    tm_tb.ensure((size_t)(ntiles + 2) * 4);
+    a.tb = tm_tb.as<u32>();
     CK(cudaMemsetAsync(dscal32(20), 0, 2 * sizeof(u32), st));
     ph_begin(ISA_PH_WM_COLLAPSE);
     kt_begin(KF_MERGE, st);
@@ -2042,6 +2060,7 @@ struct Engine {
     led.rows_seen = n;
     if (n == 0) { led.kernel_launches = 0; return 0; }
     dev_packed = false;
+    tm_mode = tile_merge_env();
     hbm_left = 0;
     bk_ready = false;
     dirpool.reset();

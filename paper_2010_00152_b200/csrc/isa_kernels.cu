@@ -973,11 +973,329 @@ __global__ void k_seg_fixup(u32 nthreads, SlotDesc sd, const u64* __restrict__ p
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused collapse: head flags, group numbering and the segmented reduce in one
+// kernel over tiles of CF_THREADS * CF_IT sorted rows (Schema.merge_states
+// over runs of equal keys, core.py:184-208; evict_all's sorted unique
+// output, memindex.py:275-285).  Tiles take their index from a counter and
+// chain through a decoupled look-back whose payload is (groups so far, state
+// of the group still open at the tile's end): a tile learns both its first
+// output index and the carry-in state of a group that started in an earlier
+// tile.  Inside a tile every thread reduces its consecutive rows; a
+// segmented scan over the threads gives each thread the state of the group
+// open at its first row.  A group is written by the thread that holds the
+// next group's head (or by the very last thread), so every output row is
+// written once, without atomics.  The keys and row ids are read once
+// (striped, coalesced, transposed through shared memory), each included
+// row's state gathered once.
+#define CF_THREADS 256
+__host__ __device__ constexpr int cf_items(int MS) { return MS <= 2 ? 8 : (MS <= 8 ? 4 : 2); }
+
+__device__ __forceinline__ u64 ld_acquire_gpu(const u64* p) {
+  u64 v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(u64* p, u64 v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <int MS>
+__device__ __forceinline__ void cf_identity(const SlotDesc& sd, u64 (&x)[MS]) {
+#pragma unroll
+  for (int k = 0; k < MS; ++k) x[k] = k < sd.nslots ? identity_slot(sd.op[k], sd.type[k]) : 0;
+}
+// a <- a (+) b, a before b in row order
+template <int MS>
+__device__ __forceinline__ void cf_combine(const SlotDesc& sd, u64 (&a)[MS], const u64 (&b)[MS]) {
+#pragma unroll
+  for (int k = 0; k < MS; ++k)
+    if (k < sd.nslots) a[k] = combine_slot(sd.op[k], sd.type[k], a[k], b[k]);
+}
+
+template <int KW, int MS>
+__global__ void __launch_bounds__(CF_THREADS) k_collapse_fused(
+    const u64* __restrict__ lo, const u64* __restrict__ hi, const u32* __restrict__ val, u32 m, u32 limit, SlotDesc sd,
+    i64 row0, const u64* __restrict__ st_in, u64* __restrict__ out_lo, u64* __restrict__ out_hi,
+    u64* __restrict__ out_st, u64* __restrict__ status, u64* __restrict__ pay, u32* __restrict__ ticket, u32 epoch,
+    u32 ntiles, u32* __restrict__ total) {
+  constexpr int IT = cf_items(MS);
+  constexpr u32 TILE = CF_THREADS * IT;
+  constexpr u32 PADN = TILE + TILE / IT;
+  __shared__ u64 s_lo[PADN];
+  __shared__ u64 s_hi[KW == 2 ? PADN : 1];
+  __shared__ u32 s_v[PADN];
+  __shared__ u32 s_tile, s_hx, sw[8];
+  __shared__ u64 s_prev_lo, s_prev_hi;
+  __shared__ u64 s_wv[8][MS];
+  __shared__ unsigned char s_wf[8];
+  __shared__ u64 s_carry[MS];
+  const int S = sd.nslots;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const u32 tile = s_tile;
+  const u32 base = tile * TILE;
+  const u32 tn = min(TILE, m - base);
+  auto P = [](u32 i) { return i + i / IT; };
+  // ---- striped, coalesced loads -> shared memory
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const u32 q = it * CF_THREADS + tid;
+    if (q < tn) {
+      s_lo[P(q)] = lo[base + q];
+      if (KW == 2) s_hi[P(q)] = hi[base + q];
+      s_v[P(q)] = val[base + q];
+    }
+  }
+  if (tid == 0 && base > 0) {
+    s_prev_lo = lo[base - 1];
+    s_prev_hi = KW == 2 ? hi[base - 1] : 0;
+  }
+  __syncthreads();
+  // ---- blocked: heads, included rows, gathered states
+  const u32 i0 = tid * IT;
+  u64 kl[IT], kh[IT];
+  u32 hmask = 0, imask = 0;
+  u64 pl = 0, ph = 0;
+  bool have_prev = false;
+  if (i0 > 0 && i0 <= tn) { pl = s_lo[P(i0 - 1)]; ph = KW == 2 ? s_hi[P(i0 - 1)] : 0; have_prev = true; }
+  else if (i0 == 0 && base > 0) { pl = s_prev_lo; ph = s_prev_hi; have_prev = true; }
+  u64 cur[IT][MS];
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const u32 i = i0 + it;
+    kl[it] = 0; kh[it] = 0;
+    if (i < tn) {
+      kl[it] = s_lo[P(i)];
+      kh[it] = KW == 2 ? s_hi[P(i)] : 0;
+      const u32 v = s_v[P(i)];
+      const bool inc = v < limit;
+      const bool head = inc && (!have_prev || !key_eq<KW>(kh[it], kl[it], ph, pl));
+      pl = kl[it]; ph = kh[it]; have_prev = true;
+      if (inc) {
+        imask |= 1u << it;
+        if (S) load_state_row<MS>(sd, row0, st_in, v, cur[it]);
+      }
+      if (head) hmask |= 1u << it;
+    }
+  }
+  // ---- thread summary: lead (rows before the first head) or trail (from the last head)
+  u64 sv[MS];
+  cf_identity<MS>(sd, sv);
+  const u32 nh = __popc(hmask);
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    if (!((imask >> it) & 1u)) continue;
+    if ((hmask >> it) & 1u) {
+#pragma unroll
+      for (int k = 0; k < MS; ++k) sv[k] = cur[it][k];
+    } else {
+      cf_combine<MS>(sd, sv, cur[it]);
+    }
+  }
+  // after this loop: nh > 0 -> sv = trail; nh == 0 -> sv = lead (all rows)
+  u32 htot;
+  const u32 hx = block_excl_scan256(nh, sw, &htot);
+  // ---- segmented scan over threads of (has head, sv): exclusive -> (fx, cx)
+  bool f = nh > 0;
+  u64 v[MS];
+#pragma unroll
+  for (int k = 0; k < MS; ++k) v[k] = sv[k];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const bool fu = __shfl_up_sync(0xffffffffu, f, o);
+    u64 vu[MS];
+#pragma unroll
+    for (int k = 0; k < MS; ++k) vu[k] = __shfl_up_sync(0xffffffffu, v[k], o);
+    if (lane >= o) {
+      if (!f) {
+        cf_combine<MS>(sd, vu, v);
+#pragma unroll
+        for (int k = 0; k < MS; ++k) v[k] = vu[k];
+      }
+      f = f || fu;
+    }
+  }
+  if (lane == 31) {
+    s_wf[wid] = f ? 1 : 0;
+#pragma unroll
+    for (int k = 0; k < MS; ++k) s_wv[wid][k] = v[k];
+  }
+  // exclusive within the warp
+  bool fx = __shfl_up_sync(0xffffffffu, f, 1);
+  u64 cx[MS];
+#pragma unroll
+  for (int k = 0; k < MS; ++k) cx[k] = __shfl_up_sync(0xffffffffu, v[k], 1);
+  if (lane == 0) { fx = false; cf_identity<MS>(sd, cx); }
+  __syncthreads();
+  // warp prefixes (thread 0, in order) + the tile's inclusive summary
+  __shared__ unsigned char s_pf[8];
+  __shared__ u64 s_pv[8][MS];
+  __shared__ u64 s_tv[MS];
+  __shared__ unsigned char s_tf;
+  if (tid == 0) {
+    bool pf = false;
+    u64 pv[MS];
+    cf_identity<MS>(sd, pv);
+    for (int q = 0; q < 8; ++q) {
+      s_pf[q] = pf ? 1 : 0;
+#pragma unroll
+      for (int k = 0; k < MS; ++k) s_pv[q][k] = pv[k];
+      if (s_wf[q]) {
+#pragma unroll
+        for (int k = 0; k < MS; ++k) pv[k] = s_wv[q][k];
+        pf = true;
+      } else {
+        u64 t[MS];
+#pragma unroll
+        for (int k = 0; k < MS; ++k) t[k] = s_wv[q][k];
+        cf_combine<MS>(sd, pv, t);
+      }
+    }
+    s_tf = pf ? 1 : 0;
+#pragma unroll
+    for (int k = 0; k < MS; ++k) s_tv[k] = pv[k];
+    // ---- decoupled look-back: groups before this tile, carry-in state
+    const u64 E = (u64)epoch << 34;
+    u64* agg = pay + (size_t)tile * 2 * S;
+    u64* inc = agg + S;
+    u32 Hx = 0;
+    u64 acc[MS];
+    cf_identity<MS>(sd, acc);
+    if (tile == 0) {
+#pragma unroll
+      for (int k = 0; k < MS; ++k)
+        if (k < S) inc[k] = pv[k];
+      st_release_gpu(status, E | (2ull << 32) | htot);
+    } else {
+#pragma unroll
+      for (int k = 0; k < MS; ++k)
+        if (k < S) agg[k] = pv[k];
+      st_release_gpu(status + tile, E | (1ull << 32) | htot);
+      bool sdone = false;
+      for (int q = (int)tile - 1; q >= 0;) {
+        const u64 x = ld_acquire_gpu(status + q);
+        if ((x >> 34) != (u64)epoch) continue;   // not published yet
+        const u32 fl = (u32)(x >> 32) & 3u;
+        const u64* qp = pay + (size_t)q * 2 * S + (fl == 2 ? S : 0);
+        Hx += (u32)x;
+        if (!sdone) {
+          u64 t[MS];
+#pragma unroll
+          for (int k = 0; k < MS; ++k) t[k] = k < S ? qp[k] : 0;
+          cf_combine<MS>(sd, t, acc);
+#pragma unroll
+          for (int k = 0; k < MS; ++k) acc[k] = t[k];
+          if (fl == 1 && (u32)x > 0) sdone = true;
+        }
+        if (fl == 2) break;
+        --q;
+      }
+      u64 ti[MS];
+#pragma unroll
+      for (int k = 0; k < MS; ++k) ti[k] = acc[k];
+      if (!pf) cf_combine<MS>(sd, ti, pv);
+#pragma unroll
+      for (int k = 0; k < MS; ++k)
+        if (k < S) inc[k] = pf ? pv[k] : ti[k];
+      st_release_gpu(status + tile, E | (2ull << 32) | (Hx + htot));
+    }
+    s_hx = Hx;
+#pragma unroll
+    for (int k = 0; k < MS; ++k) s_carry[k] = acc[k];
+    if (tile + 1 == ntiles) *total = Hx + htot;
+  }
+  __syncthreads();
+  // ---- this thread's carry-in: the state of the group open at its first row
+  const u32 Hx = s_hx;
+  {
+    const bool wf = s_pf[wid];
+    if (!fx) {
+      u64 t[MS];
+#pragma unroll
+      for (int k = 0; k < MS; ++k) t[k] = s_pv[wid][k];
+      cf_combine<MS>(sd, t, cx);
+#pragma unroll
+      for (int k = 0; k < MS; ++k) cx[k] = t[k];
+      fx = wf;
+    }
+    if (!fx) {
+      u64 t[MS];
+#pragma unroll
+      for (int k = 0; k < MS; ++k) t[k] = s_carry[k];
+      cf_combine<MS>(sd, t, cx);
+#pragma unroll
+      for (int k = 0; k < MS; ++k) cx[k] = t[k];
+    }
+  }
+  // ---- writes: groups that close in this thread
+  u32 g = Hx + hx;           // index of this thread's first head
+  bool open = g > 0;         // a group is open at this thread's first row
+  u64 acc[MS];
+#pragma unroll
+  for (int k = 0; k < MS; ++k) acc[k] = cx[k];
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    if (!((imask >> it) & 1u)) continue;
+    if ((hmask >> it) & 1u) {
+      if (open && S) {
+#pragma unroll
+        for (int k = 0; k < MS; ++k)
+          if (k < S) out_st[(size_t)(g - 1) * S + k] = acc[k];
+      }
+      out_lo[g] = kl[it];
+      if (KW == 2) out_hi[g] = kh[it];
+#pragma unroll
+      for (int k = 0; k < MS; ++k) acc[k] = cur[it][k];
+      open = true;
+      ++g;
+    } else {
+      cf_combine<MS>(sd, acc, cur[it]);
+    }
+  }
+  if (tile + 1 == ntiles && tid == CF_THREADS - 1 && open && S) {
+#pragma unroll
+    for (int k = 0; k < MS; ++k)
+      if (k < S) out_st[(size_t)(g - 1) * S + k] = acc[k];
+  }
+}
+
+static std::atomic<u32> g_cf_epoch{0};
+static bool collapse_fused_env() {
+  static int v = -1;
+  // opt-in (ISA_COLLAPSE=fused): measured slower than the multi-kernel
+  // collapse (config 5 35 -> 45 ms, config 3 43 -> 112 ms per 1e9 rows:
+  // register-bound occupancy for the random gathers, and the single-thread
+  // look-back walks long heavy-hitter segments tile by tile)
+  if (v < 0) { const char* e = getenv("ISA_COLLAPSE"); v = (e && e[0] == 'f') ? 1 : 0; }
+  return v == 1;
+}
+u32 collapse_tiles(u32 m, int S) {
+  const int MS = S <= 1 ? 1 : (S <= 2 ? 2 : (S <= 4 ? 4 : (S <= 5 ? 5 : (S <= 8 ? 8 : 16))));
+  const u32 tile = CF_THREADS * cf_items(MS);
+  return (m + tile - 1) / tile;
+}
+
 void collapse(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, u32 limit, const SlotDesc& sd,
               int64_t row0, const u64* st_in, u64* out_lo, u64* out_hi, u64* out_st, CollapseTmp& tmp,
               cudaStream_t st) {
   if (m == 0) {
     cudaMemsetAsync(tmp.total, 0, sizeof(u32), st);
+    return;
+  }
+  if (tmp.status && collapse_fused_env()) {
+    const int S = sd.nslots;
+    const u32 nt = collapse_tiles(m, S);
+    const u32 ep = (g_cf_epoch.fetch_add(1) % 0x3FFFFFFEu) + 1u;
+    cudaMemsetAsync(tmp.ticket, 0, sizeof(u32), st);
+#define CF_LAUNCH(K, M) klaunch(k_collapse_fused<K, M>, nt, CF_THREADS, 0, st, lo, hi, val, m, limit, sd, (i64)row0, st_in, \
+                                out_lo, out_hi, out_st, tmp.status, tmp.pay, tmp.ticket, ep, nt, tmp.total)
+#define CF_KW(K) { if (S <= 1) CF_LAUNCH(K, 1); else if (S <= 2) CF_LAUNCH(K, 2); else if (S <= 4) CF_LAUNCH(K, 4); \
+                   else if (S <= 5) CF_LAUNCH(K, 5); else if (S <= 8) CF_LAUNCH(K, 8); else CF_LAUNCH(K, 16); }
+    if (KW == 2) CF_KW(2) else CF_KW(1)
+#undef CF_KW
+#undef CF_LAUNCH
     return;
   }
   int g = grid_for(m, 256);

@@ -80,7 +80,12 @@ struct CollapseTmp {
   u64* partial;    // ceil(m / 8) * S
   u32* partial_slot;  // ceil(m / 8)
   u32* total;      // 1 (device)
+  // fused single-kernel collapse (used when status != nullptr):
+  u64* status = nullptr;   // collapse_tiles(m, S) look-back words, zero when allocated (epoch-tagged after)
+  u64* pay = nullptr;      // collapse_tiles(m, S) * 2 * S state words
+  u32* ticket = nullptr;   // tile counter
 };
+u32 collapse_tiles(u32 m, int S);
 // value columns of rows [row0, row0 + n) interleaved into R-byte records
 struct RowPack { int nc; const void* src[ISA_MAX_SLOTS]; int elem[ISA_MAX_SLOTS]; int off[ISA_MAX_SLOTS]; int R; };
 void row_pack(const RowPack& rp, int64_t row0, u32 n, char* out, cudaStream_t st);
@@ -180,7 +185,9 @@ void run_lower_bounds(int KW, const RunRef* runs_dev, int nruns, const u64* b_lo
 // bucket = clamp((key - g) >> shift, 0, nb - 1) (keys below g -> 0).
 struct Bucketing { u64 g_lo, g_hi; int shift; u32 nb; };
 // dir[b], b in [0, nb]: first row of the sorted run (lo/hi, n rows) whose bucket is >= b
-void dir_build(int KW, const u64* lo, const u64* hi, u32 n, const Bucketing& bk, u32* dir, cudaStream_t st);
+// tmp: dir_tmp_bytes() of device scratch (list of long bucket ranges)
+size_t dir_tmp_bytes();
+void dir_build(int KW, const u64* lo, const u64* hi, u32 n, const Bucketing& bk, u32* dir, void* tmp, cudaStream_t st);
 // D[b * k + r] = dirs[r][b] (dirs_dev: device array of k device pointers)
 void dir_transpose(u32* const* dirs_dev, int k, u32 nb1, u32* D, cudaStream_t st);
 // P[b] = sum_r D[b * k + r]
@@ -200,6 +207,8 @@ struct TileMergeArgs {
   u64* status; u32 epoch; u32* ticket;                  // look-back words (ntiles, epoch-tagged), tile counter
   u32* total;              // groups written by the window
   u32* overflow;           // set when a tile holds more than cap rows (the window must be redone)
+  int pbits;               // sort-word prefix bits (set by tile_merge)
+  u32* tb;                 // [ntiles + 1] scratch: the tiles' bucket bounds (filled by tile_merge)
 };
 // tile capacity in rows for KW key words, S slots and k runs (0: not possible)
 u32 tile_merge_cap(int KW, int S, int k);

@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 namespace isa {
 
@@ -41,17 +42,43 @@ __device__ __forceinline__ u32 bucket_of(const Bucketing& bk, u64 hi, u64 lo) {
 }
 
 // dir[b] (b in [0, nb]) = first row i of a sorted run with bucket(key_i) >= b
-// (n when none): row i writes the buckets (bucket(i - 1), bucket(i)], the
-// last row also (bucket(n - 1), nb].
+// (n when none): row i owns the buckets (bucket(i - 1), bucket(i)], the
+// last row also (bucket(n - 1), nb].  Short ranges are written by the row's
+// thread; long ones (the empty margins below the first and above the last
+// key, gaps in clustered key sets) go to a list that a second kernel fills
+// with whole CTAs, so no thread writes more than DIR_INLINE entries.
+#define DIR_INLINE 32
+#define DIR_GAP_CAP (1u << 16)
+struct DirGap { u32 q0, q1, v, pad; };   // dir[q0 .. q1) = v
+
 template <int KW>
 __global__ void k_dir_build(const u64* __restrict__ lo, const u64* __restrict__ hi, u32 n, Bucketing bk,
-                            u32* __restrict__ dir) {
+                            u32* __restrict__ dir, DirGap* __restrict__ gaps, u32* __restrict__ ngaps, u32 gap_cap) {
+  auto emit = [&](u32 q0, u32 q1, u32 v) {   // dir[q0, q1) = v
+    if (q1 <= q0) return;
+    if (q1 - q0 <= DIR_INLINE) {
+      for (u32 q = q0; q < q1; ++q) dir[q] = v;
+      return;
+    }
+    const u32 g = atomicAdd(ngaps, 1u);
+    if (g < gap_cap) gaps[g] = DirGap{q0, q1, v, 0u};
+    else for (u32 q = q0; q < q1; ++q) dir[q] = v;   // list full: slow but correct
+  };
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const u32 b = bucket_of(bk, KW == 2 ? hi[i] : 0, lo[i]);
-    const long long bp = i == 0 ? -1 : (long long)bucket_of(bk, KW == 2 ? hi[i - 1] : 0, lo[i - 1]);
-    for (long long q = bp + 1; q <= (long long)b; ++q) dir[q] = i;
-    if (i == n - 1)
-      for (u32 q = b + 1; q <= bk.nb; ++q) dir[q] = n;
+    const u32 q0 = i == 0 ? 0u : bucket_of(bk, KW == 2 ? hi[i - 1] : 0, lo[i - 1]) + 1;
+    emit(q0, b + 1, i);
+    if (i == n - 1) emit(b + 1, bk.nb + 1, n);
+  }
+}
+
+// one CTA per listed range (grid-stride over the list)
+__global__ void k_dir_gaps(u32* __restrict__ dir, const DirGap* __restrict__ gaps, const u32* __restrict__ ngaps,
+                           u32 gap_cap) {
+  const u32 ng = min(*ngaps, gap_cap);
+  for (u32 g = blockIdx.x; g < ng; g += gridDim.x) {
+    const DirGap d = gaps[g];
+    for (u32 q = d.q0 + threadIdx.x; q < d.q1; q += blockDim.x) dir[q] = d.v;
   }
 }
 
@@ -59,14 +86,21 @@ __global__ void k_fill_u32(u32* __restrict__ p, u32 n, u32 v) {
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = v;
 }
 
-void dir_build(int KW, const u64* lo, const u64* hi, u32 n, const Bucketing& bk, u32* dir, cudaStream_t st) {
+size_t dir_tmp_bytes() { return 16 + (size_t)DIR_GAP_CAP * sizeof(DirGap); }
+
+void dir_build(int KW, const u64* lo, const u64* hi, u32 n, const Bucketing& bk, u32* dir, void* tmp,
+               cudaStream_t st) {
   if (n == 0) {
-    klaunch(k_fill_u32, (bk.nb + 256) / 256, 256, 0, st, dir, bk.nb + 1, 0u);
+    klaunch(k_fill_u32, std::min<u32>((bk.nb + 256) / 256, 148u * 16u), 256, 0, st, dir, bk.nb + 1, 0u);
     return;
   }
+  u32* ngaps = (u32*)tmp;
+  DirGap* gaps = (DirGap*)((char*)tmp + 16);
+  cudaMemsetAsync(ngaps, 0, sizeof(u32), st);
   const int g = (int)std::min<u32>((n + 255) / 256, 148u * 16u);
-  if (KW == 2) klaunch(k_dir_build<2>, g, 256, 0, st, lo, hi, n, bk, dir);
-  else klaunch(k_dir_build<1>, g, 256, 0, st, lo, hi, n, bk, dir);
+  if (KW == 2) klaunch(k_dir_build<2>, g, 256, 0, st, lo, hi, n, bk, dir, gaps, ngaps, (u32)DIR_GAP_CAP);
+  else klaunch(k_dir_build<1>, g, 256, 0, st, lo, hi, n, bk, dir, gaps, ngaps, (u32)DIR_GAP_CAP);
+  klaunch(k_dir_gaps, 148 * 2, 256, 0, st, dir, (const DirGap*)gaps, (const u32*)ngaps, (u32)DIR_GAP_CAP);
 }
 
 // D[b * k + r] = dirs[r][b]: 32 x 32 tiles through shared memory
@@ -129,10 +163,9 @@ __device__ __forceinline__ u32 p_lower_bound(const u64* __restrict__ P, u32 lo, 
   return lo;
 }
 
+// Per row: key words, states, two u32 sort words, u32 group id, u8 head.
 size_t tile_merge_smem(int KW, int S, int k, u32 cap) {
-  // keys, states, two u16 order arrays, u32 group ids, u8 heads; segment
-  // offsets (k + 1 u32) and sources (k i64); per-warp digit counters
-  return (size_t)cap * (8 * KW + 8 * S + 2 + 2 + 4 + 1) + 16 + (size_t)(k + 1) * 4 + (size_t)k * 8 + 16 +
+  return (size_t)cap * (8 * KW + 8 * S + 4 + 4 + 4 + 1) + 16 + (size_t)(k + 1) * 4 + (size_t)k * 8 + 16 +
          TM_WARPS * 256 * 4 + 256 * 4 + 64;
 }
 
@@ -141,11 +174,94 @@ u32 tile_merge_cap(int KW, int S, int k) {
   const size_t budget = 100 * 1024;
   const size_t fixed = tile_merge_smem(KW, S, k, 0);
   if (fixed >= budget) return 0;
-  size_t cap = (budget - fixed) / (size_t)(8 * KW + 8 * S + 9);
+  size_t cap = (budget - fixed) / (size_t)(8 * KW + 8 * S + 13);
   cap = std::min<size_t>(cap, TM_MAX_CAP);
   return (u32)(cap & ~(size_t)255);
 }
 
+// (key - base) >> sh, 128-bit difference (KW == 1: hi words are 0)
+template <int KW>
+__device__ __forceinline__ u64 tm_off(u64 h, u64 l, u64 bh, u64 bl, int sh) {
+  if (KW == 1) return sh >= 64 ? 0 : ((l - bl) >> sh);
+  const u64 dl = l - bl, dh = h - bh - (l < bl ? 1ull : 0ull);
+  if (sh >= 64) return dh >> (sh - 64);
+  if (sh == 0) return dl;
+  return (dl >> sh) | (dh << (64 - sh));
+}
+
+// One stable LSD pass over the tile's u32 sort words (rows in warp-contiguous
+// ranges of WI, every lane ranks its items with MATCH.ANY and per-warp digit
+// counters); digit(w) is the pass's 8-bit digit of word w.
+template <typename DigitFn>
+__device__ __forceinline__ void tm_pass(const u32* __restrict__ cur, u32* __restrict__ nxt, u32 n, u32 WI, u32* wcnt,
+                                        u32* dstart, u32* sw, DigitFn digit) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const u32 lt = lanemask_lt();
+  for (int q = lane; q < 256; q += 32) wcnt[w * 256 + q] = 0;
+  __syncwarp();
+  u32 it_d[TM_MAX_IT], it_w[TM_MAX_IT], it_r[TM_MAX_IT];
+#pragma unroll
+  for (int it = 0; it < TM_MAX_IT; ++it) {
+    const u32 i = w * WI + it * 32 + lane;
+    const bool in_w = (u32)it * 32 < WI;
+    const bool valid = in_w && i < n;
+    u32 d = 256 + lane, x = 0;
+    if (valid) {
+      x = cur[i];
+      d = digit(x);
+    }
+    it_d[it] = d;
+    it_w[it] = x;
+    if (in_w) {
+      const u32 peers = __match_any_sync(0xffffffffu, d);
+      const int leader = __ffs(peers) - 1;
+      u32 c = 0;
+      if (valid && lane == leader) {
+        c = wcnt[w * 256 + d];
+        wcnt[w * 256 + d] = c + __popc(peers);
+      }
+      c = __shfl_sync(0xffffffffu, c, leader);
+      it_r[it] = c + __popc(peers & lt);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  {   // per digit: exclusive over warps, then over digits
+    const int dg = tid;
+    u32 run = 0;
+#pragma unroll
+    for (int ww = 0; ww < TM_WARPS; ++ww) {
+      const u32 c = wcnt[ww * 256 + dg];
+      wcnt[ww * 256 + dg] = run;
+      run += c;
+    }
+    u32 tot;
+    dstart[dg] = block_excl_scan256(run, sw, &tot);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < TM_MAX_IT; ++it) {
+    const u32 i = w * WI + it * 32 + lane;
+    if ((u32)it * 32 < WI && i < n) {
+      const u32 d = it_d[it];
+      nxt[dstart[d] + wcnt[w * 256 + d] + it_r[it]] = it_w[it];
+    }
+  }
+  __syncthreads();
+}
+
+// One tile: rows of the k run segments [D[B0][r], D[B1][r]) loaded into
+// shared memory (one thread per row, its segment found by binary search over
+// the segment offsets), sorted stably by key, equal keys combined in run
+// order, groups written at their final place in the result.
+//
+// Sort: the tile's key span comes from the segments' end rows (each segment
+// is sorted).  Every row gets a u32 word (prefix << 12 | row), prefix = the
+// top <= 20 bits of (key - min); an LSD radix sort of the words orders the
+// tile exactly when the span fits 20 bits (dense keys: config 5) and up to
+// runs of equal prefix otherwise (sparse keys: those runs are short and are
+// finished by an insertion sort on the full key; a run longer than 64 makes
+// the tile fall back to an LSD sort over every span bit).
 template <int KW, int MS>
 __global__ void __launch_bounds__(TM_THREADS, 2) k_tile_merge(TileMergeArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -155,15 +271,15 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_tile_merge(TileMergeArgs a) {
   u64* klo = (u64*)smem;
   u64* khi = klo + cap;                                   // KW == 2
   u64* sst = klo + (size_t)cap * KW;                      // [cap][S]
-  unsigned short* ord0 = (unsigned short*)(sst + (size_t)cap * S);
-  unsigned short* ord1 = ord0 + cap;
-  u32* gid = (u32*)(((uintptr_t)(ord1 + cap) + 15) & ~(uintptr_t)15);
+  u32* wa = (u32*)(sst + (size_t)cap * S);
+  u32* wb = wa + cap;
+  u32* gid = wb + cap;
   unsigned char* head = (unsigned char*)(gid + cap);
   u32* seg_off = (u32*)(((uintptr_t)(head + cap) + 15) & ~(uintptr_t)15);   // [k + 1]
   i64* seg_src = (i64*)(((uintptr_t)(seg_off + k + 1) + 15) & ~(uintptr_t)15);   // [k]
   u32* wcnt = (u32*)(seg_src + k);                        // [TM_WARPS][256]
   u32* dstart = wcnt + TM_WARPS * 256;                    // [256]
-  __shared__ u32 s_j, s_B0, s_B1, s_n, s_ng, s_base, s_bits;
+  __shared__ u32 s_j, s_B0, s_B1, s_n, s_base, s_bits, s_long;
   __shared__ u32 sw[TM_WARPS];
   __shared__ u64 s_min_lo[TM_WARPS], s_min_hi[TM_WARPS], s_max_lo[TM_WARPS], s_max_hi[TM_WARPS];
 
@@ -171,9 +287,9 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_tile_merge(TileMergeArgs a) {
   if (tid == 0) {
     const u32 j = atomicAdd(a.ticket, 1u);
     s_j = j;
-    const u64 p0 = a.P[a.b_lo];
-    s_B0 = j == 0 ? a.b_lo : p_lower_bound(a.P, a.b_lo, a.b_hi, p0 + (u64)j * a.target);
-    s_B1 = j + 1 >= a.ntiles ? a.b_hi : p_lower_bound(a.P, a.b_lo, a.b_hi, p0 + (u64)(j + 1) * a.target);
+    s_B0 = a.tb[j];
+    s_B1 = a.tb[j + 1];
+    s_long = 0;
   }
   __syncthreads();
   const u32 j = s_j, B0 = s_B0, B1 = s_B1;
@@ -202,30 +318,56 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_tile_merge(TileMergeArgs a) {
   if (over && tid == 0) atomicExch(a.overflow, 1u);
 
   u32 ng = 0;
+  unsigned char exact = 1;
+  u32* cur = wa;
   if (!over && n > 0) {
-    // ---- load the segments (one warp per segment: coalesced rows and states)
-    for (int r = w; r < k; r += TM_WARPS) {
-      const u32 o = seg_off[r], len = seg_off[r + 1] - o;
-      if (!len) continue;
-      const i64 src = seg_src[r];
-      for (u32 i = lane; i < len; i += 32) {
-        klo[o + i] = a.s_lo[src + i];
-        if (KW == 2) khi[o + i] = a.s_hi[src + i];
+    // ---- load: one thread per row (LU rows in flight per thread)
+    constexpr int LU = MS <= 2 ? 4 : (MS <= 5 ? 2 : 1);
+    for (u32 i0 = tid; i0 < n; i0 += LU * TM_THREADS) {
+      i64 src[LU];
+#pragma unroll
+      for (int u = 0; u < LU; ++u) {
+        const u32 i = i0 + u * TM_THREADS;
+        src[u] = -1;
+        if (i < n) {
+          int l = 0, h = k;   // last r with seg_off[r] <= i (a non-empty segment)
+          while (h - l > 1) {
+            const int m = (l + h) >> 1;
+            if (seg_off[m] <= i) l = m; else h = m;
+          }
+          src[u] = seg_src[l] + (i64)(i - seg_off[l]);
+        }
       }
-      if (S) {
-        const u64* sp = a.s_st + (size_t)src * S;
-        u64* dp = sst + (size_t)o * S;
-        for (u32 q = lane; q < len * (u32)S; q += 32) dp[q] = sp[q];
+      u64 kl[LU], kh[LU], sv[LU][MS];
+#pragma unroll
+      for (int u = 0; u < LU; ++u) {
+        if (src[u] < 0) continue;
+        kl[u] = a.s_lo[src[u]];
+        if (KW == 2) kh[u] = a.s_hi[src[u]];
+#pragma unroll
+        for (int s = 0; s < MS; ++s)
+          if (s < S) sv[u][s] = a.s_st[(size_t)src[u] * S + s];
+      }
+#pragma unroll
+      for (int u = 0; u < LU; ++u) {
+        if (src[u] < 0) continue;
+        const u32 i = i0 + u * TM_THREADS;
+        klo[i] = kl[u];
+        if (KW == 2) khi[i] = kh[u];
+#pragma unroll
+        for (int s = 0; s < MS; ++s)
+          if (s < S) sst[(size_t)i * S + s] = sv[u][s];
       }
     }
     __syncthreads();
-    // ---- key span of the tile: min, max -> bits that vary
+    // ---- key span: min of the segments' first rows, max of their last rows
     u64 mnl = ~0ull, mnh = KW == 2 ? ~0ull : 0, mxl = 0, mxh = 0;
-    for (u32 i = tid; i < n; i += TM_THREADS) {
-      const u64 l = klo[i], h = KW == 2 ? khi[i] : 0;
-      if (key_less<KW>(h, l, mnh, mnl)) { mnh = h; mnl = l; }
-      if (key_less<KW>(mxh, mxl, h, l)) { mxh = h; mxl = l; }
-      ord0[i] = (unsigned short)i;
+    for (int r = tid; r < k; r += TM_THREADS) {
+      const u32 o0 = seg_off[r], o1 = seg_off[r + 1];
+      if (o1 == o0) continue;
+      const u64 l0 = klo[o0], h0 = KW == 2 ? khi[o0] : 0, l1 = klo[o1 - 1], h1 = KW == 2 ? khi[o1 - 1] : 0;
+      if (key_less<KW>(h0, l0, mnh, mnl)) { mnh = h0; mnl = l0; }
+      if (key_less<KW>(mxh, mxl, h1, l1)) { mxh = h1; mxl = l1; }
     }
     for (int o = 16; o; o >>= 1) {
       const u64 al = __shfl_xor_sync(0xffffffffu, mnl, o), ah = __shfl_xor_sync(0xffffffffu, mnh, o);
@@ -246,88 +388,70 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_tile_merge(TileMergeArgs a) {
     }
     __syncthreads();
     const u64 bl = s_min_lo[0], bh = s_min_hi[0];
-    const int npass = ((int)s_bits + 7) / 8;
-    // ---- stable LSD radix sort of the row order on (key - min)
-    unsigned short* cur = ord0;
-    unsigned short* nxt = ord1;
+    const int bits = (int)s_bits;
+    const int pb = bits < a.pbits ? bits : a.pbits;   // prefix bits (20; tests lower it)
+    const int psh = bits - pb;              // prefix = (key - min) >> psh
+    exact = psh == 0;
+    for (u32 i = tid; i < n; i += TM_THREADS)
+      wa[i] = ((u32)tm_off<KW>(KW == 2 ? khi[i] : 0, klo[i], bh, bl, psh) << 12) | i;
+    __syncthreads();
     const u32 WI = (((n + TM_WARPS - 1) / TM_WARPS) + 31) & ~31u;   // rows per warp, in order
-    const u32 lt = lanemask_lt();
-    for (int p = 0; p < npass; ++p) {
-      const int sh = 8 * p;
-      for (int q = lane; q < 256; q += 32) wcnt[w * 256 + q] = 0;
-      __syncwarp();
-      u32 it_d[TM_MAX_IT], it_r[TM_MAX_IT];
-      unsigned short it_x[TM_MAX_IT];
-#pragma unroll
-      for (int it = 0; it < TM_MAX_IT; ++it) {
-        const u32 i = w * WI + it * 32 + lane;
-        const bool in_w = (u32)it * 32 < WI;
-        const bool valid = in_w && i < n;
-        u32 d = 256 + lane;
-        unsigned short x = 0;
-        if (valid) {
-          x = cur[i];
-          const u64 l = klo[x];
-          u64 v;
-          if (KW == 2) {
-            const u64 h = khi[x];
-            const u64 dl = l - bl, dh = h - bh - (l < bl ? 1ull : 0ull);
-            v = sh >= 64 ? (dh >> (sh - 64)) : (sh == 0 ? dl : ((dl >> sh) | (dh << (64 - sh))));
-          } else {
-            v = (l - bl) >> sh;
-          }
-          d = (u32)(v & 0xFFu);
-        }
-        it_d[it] = d;
-        it_x[it] = x;
-        if (in_w) {
-          const u32 peers = __match_any_sync(0xffffffffu, d);
-          const int leader = __ffs(peers) - 1;
-          u32 c = 0;
-          if (valid && lane == leader) {
-            c = wcnt[w * 256 + d];
-            wcnt[w * 256 + d] = c + __popc(peers);
-          }
-          c = __shfl_sync(0xffffffffu, c, leader);
-          it_r[it] = c + __popc(peers & lt);
-          __syncwarp();
-        }
-      }
-      __syncthreads();
-      {   // per digit: exclusive over warps, then over digits
-        const int dg = tid;
-        u32 run = 0;
-#pragma unroll
-        for (int ww = 0; ww < TM_WARPS; ++ww) {
-          const u32 c = wcnt[ww * 256 + dg];
-          wcnt[ww * 256 + dg] = run;
-          run += c;
-        }
-        u32 tot;
-        dstart[dg] = block_excl_scan256(run, sw, &tot);
-      }
-      __syncthreads();
-#pragma unroll
-      for (int it = 0; it < TM_MAX_IT; ++it) {
-        const u32 i = w * WI + it * 32 + lane;
-        if ((u32)it * 32 < WI && i < n) {
-          const u32 d = it_d[it];
-          nxt[dstart[d] + wcnt[w * 256 + d] + it_r[it]] = it_x[it];
-        }
-      }
-      __syncthreads();
-      unsigned short* t = cur; cur = nxt; nxt = t;
+    u32* nxt = wb;
+    for (int sh = 12; sh < 12 + pb; sh += 8) {
+      tm_pass(cur, nxt, n, WI, wcnt, dstart, sw, [sh](u32 x) { return (x >> sh) & 0xFFu; });
+      u32* t = cur; cur = nxt; nxt = t;
     }
-    // ---- heads + group ids (thread-contiguous items, block scan of counts)
     const u32 ipt = (n + TM_THREADS - 1) / TM_THREADS;
     const u32 i0 = min(n, tid * ipt), i1 = min(n, i0 + ipt);
+    if (!exact) {
+      // runs of equal prefix starting in this thread's range: insertion sort
+      // by the full key (stable: ties keep their order)
+      for (u32 s0 = i0; s0 < i1; ++s0) {
+        const u32 pfx = cur[s0] >> 12;
+        if (s0 > 0 && (cur[s0 - 1] >> 12) == pfx) continue;   // not a run start
+        u32 e = s0 + 1;
+        while (e < n && (cur[e] >> 12) == pfx) ++e;
+        if (e - s0 < 2) continue;
+        if (e - s0 > 64) { s_long = 1; continue; }
+        for (u32 x = s0 + 1; x < e; ++x) {
+          const u32 v = cur[x];
+          const u32 vi = v & 0xFFFu;
+          const u64 vl = klo[vi], vh = KW == 2 ? khi[vi] : 0;
+          u32 y = x;
+          while (y > s0) {
+            const u32 ui = cur[y - 1] & 0xFFFu;
+            if (!key_less<KW>(vh, vl, KW == 2 ? khi[ui] : 0, klo[ui])) break;
+            cur[y] = cur[y - 1];
+            --y;
+          }
+          cur[y] = v;
+        }
+      }
+      __syncthreads();
+      if (s_long) {
+        // a long run of equal prefix: LSD over every span bit (keys read
+        // through the row index), starting from the prefix order
+        for (int sh = 0; sh < bits; sh += 8) {
+          tm_pass(cur, nxt, n, WI, wcnt, dstart, sw, [&](u32 x) {
+            const u32 xi = x & 0xFFFu;
+            return (u32)tm_off<KW>(KW == 2 ? khi[xi] : 0, klo[xi], bh, bl, sh) & 0xFFu;
+          });
+          u32* t = cur; cur = nxt; nxt = t;
+        }
+      }
+    }
+    // ---- heads + group ids (thread-contiguous items, block scan of counts)
     u32 c = 0;
     for (u32 i = i0; i < i1; ++i) {
-      const unsigned short x = cur[i];
       bool hd = i == 0;
       if (!hd) {
-        const unsigned short y = cur[i - 1];
-        hd = !key_eq<KW>(KW == 2 ? khi[x] : 0, klo[x], KW == 2 ? khi[y] : 0, klo[y]);
+        const u32 x = cur[i], y = cur[i - 1];
+        if (exact) {
+          hd = (x >> 12) != (y >> 12);
+        } else {
+          const u32 xi = x & 0xFFFu, yi = y & 0xFFFu;
+          hd = !key_eq<KW>(KW == 2 ? khi[xi] : 0, klo[xi], KW == 2 ? khi[yi] : 0, klo[yi]);
+        }
       }
       head[i] = hd ? 1 : 0;
       c += hd ? 1u : 0u;
@@ -372,11 +496,10 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_tile_merge(TileMergeArgs a) {
   if (over || n == 0) return;
   // ---- groups: the head's thread combines the group's rows in order
   const u32 base = s_base;
-  unsigned short* cur = (((s_bits + 7) / 8) & 1) ? ord1 : ord0;
   for (u32 i = tid; i < n; i += TM_THREADS) {
     if (!head[i]) continue;
     const u32 o = base + gid[i];
-    const unsigned short x = cur[i];
+    const u32 x = cur[i] & 0xFFFu;
     a.out_lo[o] = klo[x];
     if (KW == 2) a.out_hi[o] = khi[x];
     if (S) {
@@ -385,7 +508,7 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_tile_merge(TileMergeArgs a) {
       for (int s = 0; s < MS; ++s)
         if (s < S) acc[s] = sst[(size_t)x * S + s];
       for (u32 jn = i + 1; jn < n && !head[jn]; ++jn) {
-        const unsigned short y = cur[jn];
+        const u32 y = cur[jn] & 0xFFFu;
 #pragma unroll
         for (int s = 0; s < MS; ++s)
           if (s < S) acc[s] = combine_slot(a.sd.op[s], a.sd.type[s], acc[s], sst[(size_t)y * S + s]);
@@ -395,6 +518,16 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_tile_merge(TileMergeArgs a) {
         if (s < S) a.out_st[(size_t)o * S + s] = acc[s];
     }
   }
+}
+
+// tile j of the window = buckets [tb[j], tb[j + 1]): tb[j] = first bucket
+// whose P reaches P[b_lo] + j * target (one thread per bound)
+__global__ void k_tile_bounds(const u64* __restrict__ P, u32 b_lo, u32 b_hi, u32 target, u32 ntiles,
+                              u32* __restrict__ tb) {
+  const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j > ntiles) return;
+  const u64 p0 = P[b_lo];
+  tb[j] = j == 0 ? b_lo : (j == ntiles ? b_hi : p_lower_bound(P, b_lo, b_hi, p0 + (u64)j * target));
 }
 
 static std::atomic<u32> g_tm_epoch{0};
@@ -410,7 +543,12 @@ static void tm_launch(TileMergeArgs& a, size_t smem, cudaStream_t st) {
 void tile_merge(int KW, TileMergeArgs& a, cudaStream_t st) {
   if (a.ntiles == 0) return;
   a.epoch = (g_tm_epoch.fetch_add(1) % 0x3FFFFFFEu) + 1u;
+  // ISA_TM_PREFIX_BITS (1..20, tests): fewer prefix bits exercise the
+  // insertion-sort finish and the full-width fallback on ordinary inputs
+  const char* e = getenv("ISA_TM_PREFIX_BITS");
+  a.pbits = e ? std::max(1, std::min(20, atoi(e))) : 20;
   cudaMemsetAsync(a.ticket, 0, sizeof(u32), st);
+  klaunch(k_tile_bounds, (a.ntiles + 256) / 256, 256, 0, st, a.P, a.b_lo, a.b_hi, a.target, a.ntiles, a.tb);
   const size_t smem = tile_merge_smem(KW, a.sd.nslots, a.k, a.cap);
   const int S = a.sd.nslots;
 #define TM_KW(K)                                   \

@@ -41,9 +41,11 @@ def _cfg(memory, page, **kw):
 
 @pytest.mark.parametrize("name", golden_names())
 @pytest.mark.parametrize("variant", ["device", "host_input", "hbm_runs", "packed_runs", "host_runs", "small_chunks",
-                                     "k1_always", "k1_never"])
-def test_golden_columns(name, variant):
+                                     "k1_always", "k1_never", "tile_merge", "radix_merge"])
+def test_golden_columns(name, variant, monkeypatch):
     g = Golden(name)
+    if variant in ("tile_merge", "radix_merge"):   # force either wide-merge path
+        monkeypatch.setenv("ISA_TILE_MERGE", "1" if variant == "tile_merge" else "0")
     sch = g.schema()
     kw = {}
     if variant == "hbm_runs":
@@ -59,7 +61,8 @@ def test_golden_columns(name, variant):
     if variant == "k1_never":
         kw.update(preaggregate="never")
     mode = str(g.z["merge_mode"]) if "merge_mode" in g.z else "wide"
-    if mode != "wide" and variant in ("k1_always", "k1_never", "small_chunks", "packed_runs", "host_runs"):
+    if mode != "wide" and variant in ("k1_always", "k1_never", "small_chunks", "packed_runs", "host_runs",
+                                      "tile_merge", "radix_merge"):
         pytest.skip("pre-aggregation / chunking knobs apply to the wide path only")
     op = isa.SortAggregate(sch, _cfg(g.memory, g.page, merge_mode=mode, **kw))
     n = len(g.keys[0])
@@ -475,11 +478,12 @@ def _int_workload(key, val, memory):
 
 
 @pytest.mark.parametrize("on_host", [False, True])
-def test_tile_merge_skewed_buckets_fall_back(on_host):
+def test_tile_merge_skewed_buckets_fall_back(on_host, monkeypatch):
     """Keys packed into a tiny range next to a few keys spread over int64:
     the linear bucket function puts most rows into one bucket, the tiles of
     those windows overflow, and the windows are merged by the radix-sort
     path instead -- same result as the oracle."""
+    monkeypatch.setenv("ISA_TILE_MERGE", "1")
     g = torch.Generator().manual_seed(7)
     n = 600_000
     dense = torch.randint(0, 3000, (n,), generator=g, dtype=torch.int64)
@@ -498,10 +502,11 @@ def test_tile_merge_skewed_buckets_fall_back(on_host):
 
 
 @pytest.mark.parametrize("on_host", [False, True])
-def test_tile_merge_sorted_input(on_host):
+def test_tile_merge_sorted_input(on_host, monkeypatch):
     """Ascending input: every run covers its own key range.  Host input
     fixes the buckets from the first run only (later keys clamp into the
     last bucket), device input from a sample of the whole input."""
+    monkeypatch.setenv("ISA_TILE_MERGE", "1")
     n = 400_000
     key = torch.arange(n, dtype=torch.int64) * 7 // 3
     val = torch.arange(n, dtype=torch.int64) % 1000
@@ -515,9 +520,25 @@ def test_tile_merge_sorted_input(on_host):
 
 
 @pytest.mark.parametrize("memory", [512, 4096])
-def test_tile_merge_many_runs(memory):
+def test_tile_merge_many_runs(memory, monkeypatch):
     """Hundreds to thousands of runs in one wide merge: tiles hold a few
     rows of every run."""
+    monkeypatch.setenv("ISA_TILE_MERGE", "1")
     w = workloads.config5(rows=1_000_000, device="cpu", domain=1 << 20)
     op = _oracle_case(w, memory, page=min(100, memory // 2))
     assert op.runs_after_generation > 200
+
+
+@pytest.mark.parametrize("pbits", [2, 7])
+@pytest.mark.parametrize("cfg", [3, 4, 5])
+def test_tile_merge_inexact_prefix(cfg, pbits, monkeypatch):
+    """Tile sort words carry only `pbits` bits of the key: rows whose
+    prefixes tie are finished by the insertion sort on the full key (short
+    runs) or by the full-width LSD fallback (runs longer than 64) -- the
+    result must not change."""
+    monkeypatch.setenv("ISA_TM_PREFIX_BITS", str(pbits))
+    monkeypatch.setenv("ISA_TILE_MERGE", "1")
+    rows = {3: 400_000, 4: 300_000, 5: 600_000}[cfg]
+    w = workloads.make(cfg, rows=rows, device="cpu", **({"domain": 1 << 20} if cfg in (3, 5) else {}))
+    op = _oracle_case(w, 4096, page=100, rel=1e-5 if cfg == 3 else 1e-9)
+    assert op.runs_after_generation > 10
