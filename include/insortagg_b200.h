@@ -92,8 +92,10 @@ typedef struct isa_config {
   int32_t merge_mode;        /* isa_merge_mode (SortAggConfig.merge_mode) */
   int64_t output_size_hint;  /* SortAggConfig.output_size_hint; <= 0 = none */
   int32_t run_codec;         /* host-tier runs across PCIe: 0 auto (bit-packed on the GPU when >= 32K rows), 1 raw, 2 packed */
-  int32_t reserved0;
-  int64_t hbm_run_budget;    /* ISA_TIER_AUTO: bytes of HBM runs may use; 0 = 40% of the free HBM at execute start */
+  int32_t hot_absorb;        /* rows whose key is in a large resident table are absorbed through a hash image of
+                                it instead of being sorted (memindex.py:209-215): 0 auto (fill cycles of >= 2 M rows),
+                                1 always, 2 never */
+  int64_t hbm_run_budget;    /* ISA_TIER_AUTO: bytes of HBM runs may use; 0 = half of the free HBM at execute start */
 } isa_config;
 
 /* SortAggConfig.merge_mode (sortagg.py:45-47): wide = in-sort early
@@ -165,7 +167,8 @@ enum isa_phase_id {
   ISA_PH_RUN_GEN = 7,      /* run generation total */
   ISA_PH_WIDE_MERGE = 8,   /* wide merge total */
   ISA_PH_PROBE = 9,        /* first-chunk tiny-table discovery (<= 8 groups) */
-  ISA_PH_COUNT = 10
+  ISA_PH_HOT = 10,         /* large-table absorb: hash image, probe, absorb of the hits */
+  ISA_PH_COUNT = 11
 };
 
 typedef struct isa_phase {

@@ -54,10 +54,11 @@ EXPORTED_SYMBOLS = (
 )
 
 # isa_kernel_family (kernel-true roofline families)
-KERNEL_FAMILIES = ("scatter", "hist", "collapse", "pack", "unpack", "absorb", "merge", "flush", "export")
+KERNEL_FAMILIES = ("scatter", "hist", "collapse", "pack", "unpack", "absorb", "merge", "flush", "export", "hot_probe",
+                   "hot_absorb")
 
 PHASES = ("absorb", "sort", "flush", "collapse", "table_merge", "wm_sort", "wm_collapse",
-          "run_generation", "wide_merge", "probe")
+          "run_generation", "wide_merge", "probe", "hot")
 
 
 class IsaPhase(ctypes.Structure):
@@ -82,7 +83,7 @@ class IsaConfig(ctypes.Structure):
         ("merge_mode", ctypes.c_int32),
         ("output_size_hint", ctypes.c_int64),
         ("run_codec", ctypes.c_int32),
-        ("reserved0", ctypes.c_int32),
+        ("hot_absorb", ctypes.c_int32),
         ("hbm_run_budget", ctypes.c_int64),
     ]
 

@@ -29,30 +29,10 @@ namespace isa {
 
 __host__ __device__ __forceinline__ int pk_ncol(int kw, int S) { return kw + S; }
 
-__device__ __forceinline__ u64 pk_fwd(u64 bits, int is_f64, int is_key) {
-  if (is_key) return bits;
-  if (is_f64) return (bits >> 63) ? ~bits : (bits ^ 0x8000000000000000ull);
-  return bits ^ 0x8000000000000000ull;
-}
-__device__ __forceinline__ u64 pk_inv(u64 v, int is_f64, int is_key) {
-  if (is_key) return v;
-  if (is_f64) return (v >> 63) ? (v ^ 0x8000000000000000ull) : ~v;
-  return v ^ 0x8000000000000000ull;
-}
-
 __device__ __forceinline__ u64 pk_get(const PackSrc& p, int c, u32 row) {
   if (c < p.kw) return c == 0 ? p.lo[row] : p.hi[row];
   const int s = c - p.kw;
   return pk_fwd(p.st[(size_t)row * p.S + s], (p.fmask >> s) & 1u, 0);
-}
-
-__device__ __forceinline__ u64 pk_extract(const u64* w, u32 i, u32 width) {
-  if (width == 0) return 0;
-  const u64 bit = (u64)i * width;
-  const u32 q = (u32)(bit >> 6), r = (u32)(bit & 63);
-  u64 x = w[q] >> r;
-  if (r + width > 64) x |= w[q + 1] << (64 - r);
-  return width == 64 ? x : (x & ((1ull << width) - 1));
 }
 
 __device__ __forceinline__ u64 block_reduce_min_max(u64 v, bool is_max, u64* sw) {
@@ -153,7 +133,7 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack_fused(PackSrc p, u64* __res
   extern __shared__ __align__(16) u64 stage[];   // [ncol][PK_ROWS]
   __shared__ u64 s_mn[PK_THREADS / 32][PKF_MAXC], s_mx[PK_THREADS / 32][PKF_MAXC];
   __shared__ u64 s_base[PKF_MAXC];
-  __shared__ u32 s_width[PKF_MAXC], s_woff[PKF_MAXC], s_b, s_off;
+  __shared__ u32 s_width[PKF_MAXC], s_woff[PKF_MAXC], s_b, s_off, s_bytes;
   const int ncol = pk_ncol(p.kw, p.S);
   const u32 nblk = (p.n + PK_ROWS - 1) / PK_ROWS;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -212,26 +192,39 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack_fused(PackSrc p, u64* __res
       s_woff[c] = (u32)woff;
       woff += ((u64)rows * width + 63) / 64;
     }
-    const u32 bytes = (u32)((ncol * 2 + woff) * 8);
-    // 3. decoupled look-back over the previous blocks' byte counts
+    s_bytes = (u32)((ncol * 2 + woff) * 8);
+  }
+  __syncthreads();
+  // 3. decoupled look-back over the previous blocks' byte counts, one warp:
+  //    32 predecessors per round trip
+  if (w == 0) {
+    const u32 bytes = s_bytes;
     const u64 E = (u64)epoch << 34;
     u32 excl = 0;
     if (b == 0) {
-      pkf_st(status, E | (2ull << 32) | bytes);
+      if (lane == 0) pkf_st(status, E | (2ull << 32) | bytes);
     } else {
-      pkf_st(status + b, E | (1ull << 32) | bytes);
-      for (int j = (int)b - 1;;) {
-        const u64 x = pkf_ld(status + j);
-        if ((x >> 34) != (u64)epoch) continue;
-        excl += (u32)x;
-        if (((x >> 32) & 3u) == 2u) break;
-        --j;
+      if (lane == 0) pkf_st(status + b, E | (1ull << 32) | bytes);
+      int jj = (int)b - 1;
+      for (;;) {
+        const int q = jj - lane;
+        const u64 x = q >= 0 ? pkf_ld(status + q) : (E | (2ull << 32));
+        if (!__all_sync(0xffffffffu, (x >> 34) == (u64)epoch)) continue;
+        const u32 inc = __ballot_sync(0xffffffffu, ((x >> 32) & 3u) == 2u);
+        const int first = inc ? __ffs(inc) - 1 : 32;
+        u32 v = lane <= first ? (u32)x : 0u;
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (inc) break;
+        jj -= 32;
       }
-      pkf_st(status + b, E | (2ull << 32) | (excl + bytes));
+      if (lane == 0) pkf_st(status + b, E | (2ull << 32) | (excl + bytes));
     }
-    s_off = excl;
-    blk_off[b] = excl;
-    if (b == nblk - 1) blk_off[nblk] = excl + bytes;
+    if (lane == 0) {
+      s_off = excl;
+      blk_off[b] = excl;
+      if (b == nblk - 1) blk_off[nblk] = excl + bytes;
+    }
   }
   __syncthreads();
   // 4. header + payload at the block's offset

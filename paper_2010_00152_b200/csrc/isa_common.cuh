@@ -25,7 +25,7 @@ extern std::atomic<long long> g_launches;
 // bench's kernel-true roofline.  alg_bytes = the algorithmic bytes the
 // launch moves (inputs read once + outputs written once).
 enum KFam { KF_SCATTER = 0, KF_HIST, KF_COLLAPSE, KF_PACK, KF_UNPACK, KF_ABSORB, KF_MERGE, KF_FLUSH, KF_EXPORT,
-            KF_COUNT };
+            KF_HOT_PROBE, KF_HOT_ABSORB, KF_COUNT };
 bool kt_enabled();
 void kt_set(bool on);
 void kt_begin(int fam, cudaStream_t st);
@@ -266,5 +266,56 @@ __device__ __forceinline__ u32 block_excl_scan256(u32 v, u32* sw, u32* total) {
   *total = sw[7];
   __syncthreads();
   return pre + x - v;
+}
+
+// ---- run codec value transforms (isa_codec.cu; shared with the tile merge's in-place decode)
+__device__ __forceinline__ u64 pk_fwd(u64 bits, int is_f64, int is_key) {
+  if (is_key) return bits;
+  if (is_f64) return (bits >> 63) ? ~bits : (bits ^ 0x8000000000000000ull);
+  return bits ^ 0x8000000000000000ull;
+}
+__device__ __forceinline__ u64 pk_inv(u64 v, int is_f64, int is_key) {
+  if (is_key) return v;
+  if (is_f64) return (v >> 63) ? (v ^ 0x8000000000000000ull) : ~v;
+  return v ^ 0x8000000000000000ull;
+}
+
+__device__ __forceinline__ u64 pk_extract(const u64* w, u32 i, u32 width) {
+  if (width == 0) return 0;
+  const u64 bit = (u64)i * width;
+  const u32 q = (u32)(bit >> 6), r = (u32)(bit & 63);
+  u64 x = w[q] >> r;
+  if (r + width > 64) x |= w[q + 1] << (64 - r);
+  return width == 64 ? x : (x & ((1ull << width) - 1));
+}
+
+// Schema.make_state of one input row (st_in == nullptr: from the value
+// columns, with aliases and packed row records) or an already-built state
+// row st_in[v * S ..]
+template <int MS>
+__device__ __forceinline__ void load_state_row(const SlotDesc& sd, i64 row0, const u64* __restrict__ st_in, u32 v,
+                                               u64 (&s)[MS]) {
+  const int S = sd.nslots;
+  if (st_in) {
+    const u64* p = st_in + (size_t)v * S;
+#pragma unroll
+    for (int k = 0; k < MS; ++k)
+      if (k < S) s[k] = p[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < MS; ++k) {
+      if (k < S) {
+        const int a = sd.alias[k];
+        u64 x = 0;
+#pragma unroll
+        for (int q = 0; q < k; ++q)
+          if (q == a) x = s[q];
+        s[k] = a >= 0 ? x
+                      : (sd.stride[k] ? load_slot_value(sd.src[k], sd.type[k], sd.dtype[k],
+                                                        (const char*)sd.ptr[k] + (size_t)(row0 + v) * sd.stride[k], 0)
+                                      : load_slot_value(sd.src[k], sd.type[k], sd.dtype[k], sd.ptr[k], row0 + v));
+      }
+    }
+  }
 }
 

@@ -242,7 +242,7 @@ struct Engine {
   bool bk_ready = false;
   DevicePool dirpool;
   DevBuf tm_D, tm_P, tm_base, tm_status, tm_dirptrs, tm_scal, tm_gap, tm_tb;
-  i64* tm_base_pin = nullptr;
+  char* tm_base_pin = nullptr;   // pinned MergeSrc[k] of the current window
   size_t tm_base_cap = 0;
   size_t tm_status_bytes = 0;
   int64_t in_n = 0;                 // rows of the current execute's input
@@ -423,7 +423,8 @@ struct Engine {
                       &miss_list, &stg_lo[0], &stg_lo[1], &stg_hi[0], &stg_hi[1], &stg_st[0], &stg_st[1],
                       &runref_dev, &bounds_lo, &bounds_hi, &bounds_out, &out_tmp, &pk_hdr, &pk_sz,
                       &stg_pk[0], &stg_pk[1], &stg_desc[0], &stg_desc[1], &t_backup, &pk_status, &rec_buf,
-                      &tm_D, &tm_P, &tm_base, &tm_status, &tm_dirptrs, &tm_scal, &tm_gap, &tm_tb};
+                      &tm_D, &tm_P, &tm_base, &tm_status, &tm_dirptrs, &tm_scal, &tm_gap, &tm_tb,
+                      &hb_klo, &hb_khi, &hb_idx, &hot_hit};
     for (int i = 0; i < 2; ++i) {
       if (desc_pinned[i]) cudaFreeHost(desc_pinned[i]);
       if (desc_done[i]) cudaEventDestroy(desc_done[i]);
@@ -468,6 +469,7 @@ struct Engine {
     if (cfg.memory_budget > (int64_t)1 << 30)
       throw IsaError(ISA_ERR_INVALID_INPUT, "memory budget above 2^30 groups is not supported");
     if (cfg.preaggregate < 0 || cfg.preaggregate > 2) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown preaggregate mode");
+    if (cfg.hot_absorb < 0 || cfg.hot_absorb > 2) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown hot_absorb mode");
     if (cfg.merge_mode < ISA_MERGE_WIDE || cfg.merge_mode > ISA_MERGE_SEPARATE) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown merge mode");
     if (cfg.run_codec < 0 || cfg.run_codec > 2) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown run codec");
     if (cfg.run_tier != ISA_TIER_HOST && cfg.run_tier != ISA_TIER_HBM && cfg.run_tier != ISA_TIER_FILE &&
@@ -686,11 +688,14 @@ struct Engine {
 
   // Flush analysis on a sorted chunk of `span` rows: number of keys absent
   // from T; if |T| + new > M returns the chunk-relative flush row, else span.
-  u32 flush_point(int cur, u32 m, u32 span, const u32* firstpos = nullptr) {
+  // absent_from_T: the sorted keys are known not to be in T (hash-image
+  // misses), so no head needs the binary search over T
+  u32 flush_point(int cur, u32 m, u32 span, const u32* firstpos = nullptr, bool absent_from_T = false) {
+    const u32 tn_search = absent_from_T ? 0u : T.n;
     if (!firstpos && flush_small_ok(span)) {
       const u32 k = (u32)(cfg.memory_budget - (int64_t)T.n + 1);   // >= 1: |T| <= M
       ph_begin(ISA_PH_FLUSH);
-      flush_small(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, T.plo(), T.phi(), T.n, span,
+      flush_small(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, T.plo(), T.phi(), tn_search, span,
                   k, d_scal_mapped, st);
       ph_end(ISA_PH_FLUSH, m, 0);
       sync();
@@ -705,7 +710,7 @@ struct Engine {
     ph_begin(ISA_PH_FLUSH);
     CK(cudaMemsetAsync(bitmap.p, 0, (size_t)nw * 4, st));
     CK(cudaMemsetAsync(dscal32(0), 0, sizeof(u32), st));
-    new_heads(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, T.plo(), T.phi(), T.n,
+    new_heads(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, T.plo(), T.phi(), tn_search,
               bitmap.as<u32>(), dscal32(0), st, firstpos);
     const int64_t M = cfg.memory_budget;
     u32 k = (u32)(M - (int64_t)T.n + 1);   // >= 1: |T| <= M
@@ -734,6 +739,14 @@ struct Engine {
     return h_scal[0];
   }
   u32 last_new = 0;
+  // large-table absorb (isa_hot.cu): hash image of T, rebuilt when T changed
+  DevBuf hb_klo, hb_khi, hb_idx, hot_hit;
+  HotHash hh{};
+  u64 t_ver = 1, hash_ver = 0;   // T version (bumped on every change) / version the image was built from
+  int hot_mode = 0;              // per execute: -1 auto (undecided), 0 off, 1 on
+  double hot_miss_rate = 0;      // misses / rows of the last hot chunk
+  static constexpr u32 kHotMinT = 1u << 15;   // smallest table worth a hash image
+  bool hot_ready() const { return hot_mode == 1 && T.n > 8 && (cfg.hot_absorb == 1 || T.n >= kHotMinT); }
   // K1 tile pre-aggregation: slotted groups of the current chunk
   DevBuf g_lo, g_hi, g_first, g_st, g_count, g_off;
   Table U2;           // groups of the partial tile before a flush row
@@ -804,6 +817,7 @@ struct Engine {
   // T <- merge_combine(T, U)
   void merge_into_T() {
     if (U.n == 0) return;
+    ++t_ver;
     if (T.n == 0) { std::swap(T, U); U.n = 0; return; }
     T = merge_tables(T, U);
   }
@@ -1074,6 +1088,7 @@ struct Engine {
   bool dev_packed = false;   // a packed run of this execute went to HBM (spill_T: no busy table)
   void spill_T() {
     if (T.n == 0) return;
+    ++t_ver;
     if (cfg.run_tier == ISA_TIER_FILE) {
       Run r = spill_file(T);
       runs.push_back(r);
@@ -1138,6 +1153,7 @@ struct Engine {
     if (T.n > 0 && T.n <= 8 && tiny_ok && absorb_supported((int)T.n, S)) return absorb_chunk(kd, sd, row0, a, span);
     // tiny chunks are not worth the extra pass in auto mode; "always" keeps
     // it down to 4 tiles (also what the parity tests exercise)
+    if (hot_ready()) return hot_chunk(kd, sd, row0, a, span);
     const u32 k1_min = (cfg.preaggregate == 1 ? 4 : 64) * tile_rows();
     if (k1_mode != 0 && span >= k1_min) return k1_chunk(kd, sd, row0, a, span);
     int cur = sort_rows(kd, row0, nullptr, span);
@@ -1310,9 +1326,68 @@ struct Engine {
     return a + f;
   }
 
+  // Chunk with a large resident table: rows whose key is in T are absorbed
+  // through T's hash image (memindex.py:209-215), only the misses -- the
+  // chunk's new keys -- are sorted; the flush row comes from the sorted
+  // misses exactly as on the sort path, and only hits before it are absorbed.
+  int64_t hot_chunk(const KeyDesc& kd, const SlotDesc& sd, int64_t row0, int64_t a, u32 span) {
+    ph_begin(ISA_PH_HOT);
+    if (hash_ver != t_ver) {
+      const u32 cap = hot_hash_capacity(T.n);
+      hb_idx.ensure((size_t)cap * 4);
+      hb_klo.ensure((size_t)cap * 8);
+      if (KW == 2) hb_khi.ensure((size_t)cap * 8);
+      hh = HotHash{hb_klo.as<u64>(), KW == 2 ? hb_khi.as<u64>() : nullptr, hb_idx.as<u32>(), cap - 1};
+      hot_hash_build(KW, T.plo(), T.phi(), T.n, hh, st);
+      hash_ver = t_ver;
+    }
+    u32 grid, rpc;
+    hot_probe_geometry(span, num_sms, &grid, &rpc);
+    hot_hit.ensure((size_t)span * 4 + 64);
+    ab_miss_buf.ensure((size_t)grid * rpc * 4 + 64);
+    ab_miss_cnt.ensure((size_t)(grid + 1) * 4);
+    ab_miss_off.ensure((size_t)(grid + 1) * 4);
+    scan_tmp.ensure((scan_tmp_words(grid + 1) + 64) * 4);
+    kt_begin(KF_HOT_PROBE, st);
+    hot_probe(KW, kd, row0, span, hh, grid, rpc, hot_hit.as<u32>(), ab_miss_buf.as<u32>(), ab_miss_cnt.as<u32>(), st);
+    kt_end(KF_HOT_PROBE, (int64_t)span * (key_bits / 8 + 4), st);
+    CK(cudaMemcpyAsync(ab_miss_off.p, ab_miss_cnt.p, (size_t)grid * 4, cudaMemcpyDeviceToDevice, st));
+    scan_exclusive_u32(ab_miss_off.as<u32>(), grid, scan_tmp.as<u32>(), dscal32(3), st);
+    ph_end(ISA_PH_HOT, span, 0);
+    const u32 nmiss = read_u32(dscal32(3));
+    hot_miss_rate = (double)nmiss / (double)std::max<u32>(span, 1);
+    u32 f = span;
+    int cur = 0;
+    if (nmiss) {
+      miss_list.ensure((size_t)nmiss * 4 + 64);
+      compact_misses(ab_miss_buf.as<u32>(), ab_miss_cnt.as<u32>(), ab_miss_off.as<u32>(), grid, rpc,
+                     miss_list.as<u32>(), st);
+      cur = sort_rows(kd, row0, miss_list.as<u32>(), nmiss);
+      f = flush_point(cur, nmiss, span, nullptr, /*absent_from_T=*/true);
+    } else {
+      last_new = 0;
+    }
+    // hits before the flush row, into T (T's indices: before the merge)
+    ph_begin(ISA_PH_HOT);
+    kt_begin(KF_HOT_ABSORB, st);
+    hot_absorb(sd, row0, f, hot_hit.as<u32>(), T.pst(), num_sms, st);
+    kt_end(KF_HOT_ABSORB, (int64_t)f * (4 + value_row_bytes), st);
+    ph_end(ISA_PH_HOT, f, 0);
+    if (nmiss) {
+      collapse_chunk(cur, nmiss, f, sd, row0, nullptr, U, tcap);
+      merge_into_T();
+    }
+    if (f < span) {
+      spill_T();
+      return a + f;
+    }
+    refresh_tiny();
+    return a + span;
+  }
+
   // next chunk length (rows) for the sort path
   static constexpr int64_t kProbeRows = 4096;  // = one radix-sort tile (RS_TILE)
-  int64_t chunk_len(int64_t remaining, int64_t last_len, bool last_flushed, int64_t last_cycle) {
+  int64_t chunk_len(int64_t remaining, int64_t last_len, bool last_flushed, int64_t last_cycle, int64_t since_cycle) {
     const int64_t M = cfg.memory_budget;
     int64_t cmax = cfg.chunk_rows_max > 0 ? cfg.chunk_rows_max : ((int64_t)64 << 20);
     int64_t len;
@@ -1325,18 +1400,21 @@ struct Engine {
       // the new-group rate for the next chunk and, when the input has only
       // a handful of groups, hands the rest to the absorb kernel
       len = kProbeRows;
+    } else if (last_flushed && hot_mode == 1) {
+      // large-table absorb: sort the first eighth of the cycle (the table
+      // fills with the frequent keys), absorb the rest through its hash image
+      static int frac = -1;
+      if (frac < 0) { const char* e = getenv("ISA_HOT_FIRST"); frac = e ? std::max(2, atoi(e)) : 8; }
+      len = last_cycle / frac + 4096;
     } else if (last_flushed) {
       // the next flush ~ one fill cycle away; the margin follows how much
       // consecutive cycles have varied (rows past the flush are sorted for
       // nothing; a chunk that ends short costs an extra table merge)
-      double dev = 0.03;
-      if (cycles.size() >= 2) {
-        dev = 0;
-        for (size_t i = 1; i < cycles.size(); ++i)
-          dev = std::max(dev, std::fabs((double)cycles[i] / (double)std::max<int64_t>(cycles[i - 1], 1) - 1.0));
-      }
-      const double slack = std::min(0.125, 0.01 + 4.0 * dev);
-      len = last_cycle + (int64_t)((double)last_cycle * slack) + 4096;
+      len = last_cycle + (int64_t)((double)last_cycle * cycle_slack()) + 4096;
+    } else if (hot_ready() && !cycles.empty() && since_cycle < last_cycle) {
+      // the rest of the fill cycle in one hot chunk
+      const int64_t rest = last_cycle - since_cycle;
+      len = rest + (int64_t)((double)last_cycle * cycle_slack()) + 4096;
     } else if (last_new > 0) {
       double rate = (double)last_new / (double)last_len;
       double need = (double)(M - (int64_t)T.n + 1) / rate;
@@ -1348,6 +1426,19 @@ struct Engine {
     len = std::max<int64_t>(len, 4096);
     len = std::min(len, cmax);
     return std::min(len, remaining);
+  }
+
+  // relative margin past the predicted flush row: how much consecutive fill
+  // cycles have varied (rows past the flush are processed for nothing; a
+  // chunk that ends short costs an extra table merge)
+  double cycle_slack() const {
+    double dev = 0.03;
+    if (cycles.size() >= 2) {
+      dev = 0;
+      for (size_t i = 1; i < cycles.size(); ++i)
+        dev = std::max(dev, std::fabs((double)cycles[i] / (double)std::max<int64_t>(cycles[i - 1], 1) - 1.0));
+    }
+    return std::min(0.125, 0.01 + 4.0 * dev);
   }
 
   // ------------------------------------------------------- host windows --
@@ -1511,14 +1602,32 @@ struct Engine {
     if (tm_base_cap < (size_t)k) {
       if (tm_base_pin) CK(cudaFreeHost(tm_base_pin));
       tm_base_cap = (size_t)k + 64;
-      CK(cudaHostAlloc((void**)&tm_base_pin, tm_base_cap * 8, cudaHostAllocDefault));
+      CK(cudaHostAlloc((void**)&tm_base_pin, tm_base_cap * sizeof(MergeSrc), cudaHostAllocDefault));
     }
+    // run sources: HBM-resident runs in place (raw or bit-packed), the
+    // others from this window's staged slice (staged row = soff + (p - s0))
+    MergeSrc* msrc = (MergeSrc*)tm_base_pin;
     for (int r = 0; r < k; ++r) {
-      const i64 s0 = w == 0 ? 0 : (i64)tp.lb[(size_t)r * tp.nbound + (w - 1)];
-      tm_base_pin[r] = (i64)soff[r] - s0;
+      const Run& rn = runs[r];
+      MergeSrc q;
+      memset(&q, 0, sizeof(q));
+      if (!rn.host && rn.path.empty() && rn.pk_dev) {
+        q.pk = rn.pk_dev;
+        q.blk_off = rn.off_dev;
+      } else if (!rn.host && rn.path.empty()) {
+        q.lo = rn.lo; q.hi = rn.hi; q.st = rn.st;
+        q.off = 0;
+      } else {
+        const i64 s0 = w == 0 ? 0 : (i64)tp.lb[(size_t)r * tp.nbound + (w - 1)];
+        q.lo = stg_lo[slot].as<u64>();
+        q.hi = KW == 2 ? stg_hi[slot].as<u64>() : nullptr;
+        q.st = S ? stg_st[slot].as<u64>() : nullptr;
+        q.off = (i64)soff[r] - s0;
+      }
+      msrc[r] = q;
     }
-    tm_base.ensure((size_t)k * 8 + 16);
-    CK(cudaMemcpyAsync(tm_base.p, tm_base_pin, (size_t)k * 8, cudaMemcpyHostToDevice, st));
+    tm_base.ensure((size_t)k * sizeof(MergeSrc) + 16);
+    CK(cudaMemcpyAsync(tm_base.p, msrc, (size_t)k * sizeof(MergeSrc), cudaMemcpyHostToDevice, st));
     const u32 target = tp.cap / 2;
     const u64 rows = tp.pw[w + 1] - tp.pw[w];
     const u32 ntiles = (u32)((rows + target - 1) / target);
@@ -1533,16 +1642,14 @@ struct Engine {
     memset(&a, 0, sizeof(a));
     a.P = tm_P.as<u64>();
     a.D = tm_D.as<u32>();
-    a.base = (const i64*)tm_base.p;
+    a.src = (const MergeSrc*)tm_base.p;
+    a.fmask = fmask;
     a.k = k;
     a.b_lo = tp.wb[w];
     a.b_hi = tp.wb[w + 1];
     a.target = target;
     a.ntiles = ntiles;
     a.cap = tp.cap;
-    a.s_lo = stg_lo[slot].as<u64>();
-    a.s_hi = KW == 2 ? stg_hi[slot].as<u64>() : nullptr;
-    a.s_st = S ? stg_st[slot].as<u64>() : nullptr;
     a.sd = sd0;
     a.out_lo = result.plo() + result.n;
     a.out_hi = KW == 2 ? result.phi() + result.n : nullptr;
@@ -1716,8 +1823,15 @@ struct Engine {
     std::vector<int64_t> soffs[2];   // staged row of each run's slice, per staging slot
     soffs[0].assign(k, 0);
     soffs[1].assign(k, 0);
-    auto stage = [&](int w, int slot) -> int64_t {
-      CK(cudaStreamWaitEvent(h2d, stg_free[slot], 0));
+    // HBM-resident runs are read in place by the tile merge (no staging copy)
+    const bool inplace = tp && collapse;
+    auto resident = [&](const Run& r) { return !r.host && r.path.empty(); };
+    // mode 0: every run (h2d stream); 1: all but the HBM-resident runs (the
+    // tile merge reads those in place); 2: only the HBM-resident runs, on the
+    // compute stream (a window whose tiles overflowed goes to the radix path)
+    auto stage = [&](int w, int slot, int mode) -> int64_t {
+      cudaStream_t ss = mode == 2 ? st : h2d;
+      if (mode != 2) CK(cudaStreamWaitEvent(h2d, stg_free[slot], 0));
       int64_t off = 0;
       size_t poff = 0;
       auto& desc = desc_host[slot];
@@ -1732,6 +1846,10 @@ struct Engine {
         size_t cnt = s1 - s0;
         soffs[slot][r] = off;
         if (!cnt) continue;
+        if ((mode == 1 && resident(runs[r])) || (mode == 2 && !resident(runs[r]))) {
+          off += cnt;
+          continue;
+        }
         if (!runs[r].path.empty()) {
           // FileStore run: read the covering pages back from its file
           // (read_page / parse_page, runstore.py:132-142, 315-333)
@@ -1762,7 +1880,7 @@ struct Engine {
           const u32 o0 = runs[r].off_host[b0], o1 = runs[r].off_host[b1 + 1];
           const bool on_host = runs[r].pk_host != nullptr;
           if (on_host) {
-            CK(cudaMemcpyAsync(stg_pk[slot].as<char>() + poff, runs[r].pk_host + o0, o1 - o0, cudaMemcpyHostToDevice, h2d));
+            CK(cudaMemcpyAsync(stg_pk[slot].as<char>() + poff, runs[r].pk_host + o0, o1 - o0, cudaMemcpyHostToDevice, ss));
             led.bytes_h2d += o1 - o0;
           }
           const u64 src0 = on_host ? (u64)(uintptr_t)(stg_pk[slot].as<char>() + poff) : (u64)(uintptr_t)(runs[r].pk_dev + o0);
@@ -1782,14 +1900,14 @@ struct Engine {
           continue;
         }
         cudaMemcpyKind kind = runs[r].host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-        CK(cudaMemcpyAsync(stg_lo[slot].as<u64>() + off, runs[r].lo + s0, cnt * 8, cudaMemcpyDefault, h2d));
-        if (KW == 2) CK(cudaMemcpyAsync(stg_hi[slot].as<u64>() + off, runs[r].hi + s0, cnt * 8, cudaMemcpyDefault, h2d));
-        if (S) CK(cudaMemcpyAsync(stg_st[slot].as<u64>() + off * S, runs[r].st + (size_t)s0 * S, cnt * 8 * S, cudaMemcpyDefault, h2d));
+        CK(cudaMemcpyAsync(stg_lo[slot].as<u64>() + off, runs[r].lo + s0, cnt * 8, cudaMemcpyDefault, ss));
+        if (KW == 2) CK(cudaMemcpyAsync(stg_hi[slot].as<u64>() + off, runs[r].hi + s0, cnt * 8, cudaMemcpyDefault, ss));
+        if (S) CK(cudaMemcpyAsync(stg_st[slot].as<u64>() + off * S, runs[r].st + (size_t)s0 * S, cnt * 8 * S, cudaMemcpyDefault, ss));
         if (kind == cudaMemcpyHostToDevice) led.bytes_h2d += cnt * 8 * (KW + S);
         off += cnt;
       }
       if (!prefs.empty()) {
-        CK(cudaMemcpyAsync(stg_pk[slot].p, fstage[slot], fbytes, cudaMemcpyHostToDevice, h2d));
+        CK(cudaMemcpyAsync(stg_pk[slot].p, fstage[slot], fbytes, cudaMemcpyHostToDevice, ss));
         if (pref_cap[slot] < prefs.size()) {
           if (pref_pinned[slot]) CK(cudaFreeHost(pref_pinned[slot]));
           pref_cap[slot] = prefs.size() + prefs.size() / 2 + 64;
@@ -1798,10 +1916,10 @@ struct Engine {
         memcpy(pref_pinned[slot], prefs.data(), prefs.size() * sizeof(PageRef));
         stg_pref[slot].ensure(prefs.size() * sizeof(PageRef) + 16);
         CK(cudaMemcpyAsync(stg_pref[slot].p, pref_pinned[slot], prefs.size() * sizeof(PageRef),
-                           cudaMemcpyHostToDevice, h2d));
-        CK(cudaEventRecord(fstage_done[slot], h2d));
+                           cudaMemcpyHostToDevice, ss));
+        CK(cudaEventRecord(fstage_done[slot], ss));
         page_decode(ps0, stg_pref[slot].as<PageRef>(), (u32)prefs.size(), stg_pk[slot].as<char>(),
-                    stg_lo[slot].as<u64>(), stg_hi[slot].as<u64>(), stg_st[slot].as<u64>(), dscal32(12), h2d);
+                    stg_lo[slot].as<u64>(), stg_hi[slot].as<u64>(), stg_st[slot].as<u64>(), dscal32(12), ss);
       }
       if (!desc.empty()) {
         // descriptors through a pinned buffer (its previous copy must be done)
@@ -1814,29 +1932,33 @@ struct Engine {
         memcpy(desc_pinned[slot], desc.data(), desc.size() * sizeof(UnpackBlk));
         stg_desc[slot].ensure(desc.size() * sizeof(UnpackBlk) + 16);
         CK(cudaMemcpyAsync(stg_desc[slot].p, desc_pinned[slot], desc.size() * sizeof(UnpackBlk),
-                           cudaMemcpyHostToDevice, h2d));
-        CK(cudaEventRecord(desc_done[slot], h2d));
-        kt_begin(KF_UNPACK, h2d);
+                           cudaMemcpyHostToDevice, ss));
+        CK(cudaEventRecord(desc_done[slot], ss));
+        kt_begin(KF_UNPACK, ss);
         unpack_blocks(stg_desc[slot].as<UnpackBlk>(), (u32)desc.size(), stg_pk[slot].as<char>(), KW, S, fmask,
-                      stg_lo[slot].as<u64>(), stg_hi[slot].as<u64>(), stg_st[slot].as<u64>(), h2d);
-        kt_end(KF_UNPACK, unpack_bytes, h2d);
+                      stg_lo[slot].as<u64>(), stg_hi[slot].as<u64>(), stg_st[slot].as<u64>(), ss);
+        kt_end(KF_UNPACK, unpack_bytes, ss);
       }
-      CK(cudaEventRecord(stg_ready[slot], h2d));
+      if (mode != 2) CK(cudaEventRecord(stg_ready[slot], h2d));
       return off;
     };
     std::vector<int64_t> wrows(nwin);
-    wrows[0] = stage(0, 0);
+    const int smode = inplace ? 1 : 0;
+    wrows[0] = stage(0, 0, smode);
     for (int w = 0; w < nwin; ++w) {
       const int slot = w & 1;
-      if (w + 1 < nwin) wrows[w + 1] = stage(w + 1, slot ^ 1);
+      if (w + 1 < nwin) wrows[w + 1] = stage(w + 1, slot ^ 1, smode);
       CK(cudaStreamWaitEvent(st, stg_ready[slot], 0));
       const u32 m = (u32)wrows[w];
       led.rows_read_back += m;
       led.merge_windows++;
       if (m == 0) { CK(cudaEventRecord(stg_free[slot], st)); continue; }
-      if (tp && collapse && tile_window(*tp, w, m, slot, soffs[slot])) {
-        CK(cudaEventRecord(stg_free[slot], st));
-        continue;
+      if (inplace) {
+        if (tile_window(*tp, w, m, slot, soffs[slot])) {
+          CK(cudaEventRecord(stg_free[slot], st));
+          continue;
+        }
+        stage(w, slot, 2);   // the radix path below needs every row staged
       }
       // sort the window's rows by key: keys copied into sort buffers, value = staged row index
       ensure_sort(m);
@@ -2089,6 +2211,10 @@ struct Engine {
     // swapping tables never reallocates (cudaFree would synchronize)
     tcap = (size_t)std::min<int64_t>(cfg.memory_budget, n) + 1;
     k1_mode = cfg.preaggregate == 1 ? 1 : (cfg.preaggregate == 2 ? 0 : -1);
+    hot_mode = cfg.hot_absorb == 1 ? 1 : (cfg.hot_absorb == 2 ? 0 : -1);
+    if (const char* e = getenv("ISA_HOT")) hot_mode = e[0] == 'n' ? 0 : (e[0] == 'a' && e[1] == 'l' ? 1 : hot_mode);   // A/B
+    hash_ver = 0;
+    ++t_ver;
     U2.reserve(std::min<size_t>(tcap, tile_rows() + 1), KW, S);
     T.reserve(tcap, KW, S);
     U.reserve(tcap, KW, S);
@@ -2148,7 +2274,7 @@ struct Engine {
         // every row from here on, the probed ones included
         probe_chunk(kd, sd, a - base, (u32)std::min<int64_t>(probe_rows(), std::min(n, wend) - a));
       }
-      int64_t len = chunk_len(std::min(n, wend) - a, last_len, last_flushed, last_cycle);
+      int64_t len = chunk_len(std::min(n, wend) - a, last_len, last_flushed, last_cycle, a - cycle_start);
       int64_t b = a + len;
       int64_t nxt = process_chunk(kd, sd, base, a, b);
       last_flushed = nxt < b;
@@ -2156,6 +2282,12 @@ struct Engine {
         last_cycle = nxt - cycle_start;
         cycles.push_back(last_cycle);
         cycle_start = nxt;
+        // auto: the hash-image absorb is exact but measured no faster than
+        // sorting every row on config 3 (run generation 170 vs 162 ms: the
+        // cold hits' atomics miss L2 and the per-cycle table merge doubles,
+        // profiles/r2_ab_hot.txt), so auto keeps the sort path; "always"
+        // turns it on
+        if (hot_mode < 0) hot_mode = 0;
       }
       last_len = nxt - a;
       if (last_len == 0) last_len = 1;

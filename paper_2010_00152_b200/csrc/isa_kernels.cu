@@ -850,33 +850,6 @@ __global__ void k_head_flags(const u64* __restrict__ lo, const u64* __restrict__
   }
 }
 
-template <int MS>
-__device__ __forceinline__ void load_state_row(const SlotDesc& sd, i64 row0, const u64* __restrict__ st_in, u32 v,
-                                               u64 (&s)[MS]) {
-  const int S = sd.nslots;
-  if (st_in) {
-    const u64* p = st_in + (size_t)v * S;
-#pragma unroll
-    for (int k = 0; k < MS; ++k)
-      if (k < S) s[k] = p[k];
-  } else {
-#pragma unroll
-    for (int k = 0; k < MS; ++k) {
-      if (k < S) {
-        const int a = sd.alias[k];
-        u64 x = 0;
-#pragma unroll
-        for (int q = 0; q < k; ++q)
-          if (q == a) x = s[q];
-        s[k] = a >= 0 ? x
-                      : (sd.stride[k] ? load_slot_value(sd.src[k], sd.type[k], sd.dtype[k],
-                                                        (const char*)sd.ptr[k] + (size_t)(row0 + v) * sd.stride[k], 0)
-                                      : load_slot_value(sd.src[k], sd.type[k], sd.dtype[k], sd.ptr[k], row0 + v));
-      }
-    }
-  }
-}
-
 template <int KW, int MS>
 __global__ void k_seg_reduce(const u64* __restrict__ lo, const u64* __restrict__ hi, const u32* __restrict__ val,
                              u32 m, u32 limit, SlotDesc sd, i64 row0, const u64* __restrict__ st_in,

@@ -140,6 +140,18 @@ void fold_partials(int nt, const SlotDesc& sd, const u64* partials, u32 grid, u6
 void compact_misses(const u32* miss_buf, const u32* miss_cnt, const u32* miss_off, u32 grid,
                     u32 rows_per_cta, u32* out, cudaStream_t st);
 
+// ---- large-table absorb (isa_hot.cu) --------------------------------------
+// Hash image of the sorted resident table: slot -> table index, key copied.
+struct HotHash { u64* klo; u64* khi; u32* idx; u32 mask; };
+u32 hot_hash_capacity(u32 n);   // power of two >= 2n
+void hot_hash_build(int KW, const u64* t_lo, const u64* t_hi, u32 n, const HotHash& h, cudaStream_t st);
+void hot_probe_geometry(u32 n, int num_sms, u32* grid, u32* rows_per_cta);
+// hit[i] = table index of row row0 + i's key or ~0; misses listed per CTA in row order
+void hot_probe(int KW, const KeyDesc& kd, int64_t row0, u32 n, const HotHash& h, u32 grid, u32 rows_per_cta,
+               u32* hit, u32* miss_buf, u32* miss_cnt, cudaStream_t st);
+// states of rows row0 + i (i < n) with hit[i] != ~0 combined into t_st[hit[i]]
+void hot_absorb(const SlotDesc& sd, int64_t row0, u32 n, const u32* hit, u64* t_st, int num_sms, cudaStream_t st);
+
 // ---- runs / wide merge helpers ------------------------------------------
 // out[r * nb + b] = lower_bound(run r, bound b); run keys may be mapped host memory
 // A run for the wide merge's slice search: raw key words (lo/hi), or a
@@ -192,16 +204,24 @@ void dir_build(int KW, const u64* lo, const u64* hi, u32 n, const Bucketing& bk,
 void dir_transpose(u32* const* dirs_dev, int k, u32 nb1, u32* D, cudaStream_t st);
 // P[b] = sum_r D[b * k + r]
 void dir_rowsum(const u32* D, int k, u32 nb1, u64* P, cudaStream_t st);
+// Where the tile merge reads run r: raw rows (an HBM-resident run, or its
+// slice staged from host memory) at lo/hi/st[off + p] for run row p, or a
+// bit-packed HBM-resident run (pk != nullptr) decoded in place.
+struct MergeSrc {
+  const u64* lo; const u64* hi; const u64* st;
+  i64 off;
+  const char* pk; const u32* blk_off;
+};
 struct TileMergeArgs {
   const u64* P;            // [nb + 1] rows below bucket b (all runs)
   const u32* D;            // [nb + 1][k] first row of run r at bucket >= b
-  const i64* base;         // [k] staged row of run r's row 0 (staged position = base[r] + D[b][r])
+  const MergeSrc* src;     // [k] run sources
+  u32 fmask;               // f64 state slots (codec transform of packed runs)
   int k;
   u32 b_lo, b_hi;          // the window's buckets [b_lo, b_hi)
   u32 target;              // rows per tile (planned from P)
   u32 ntiles;
   u32 cap;                 // rows a tile may hold (tile_merge_cap)
-  const u64* s_lo; const u64* s_hi; const u64* s_st;   // staged window rows
   SlotDesc sd;             // nslots, op, type
   u64* out_lo; u64* out_hi; u64* out_st;                // first output group
   u64* status; u32 epoch; u32* ticket;                  // look-back words (ntiles, epoch-tagged), tile counter

@@ -170,8 +170,11 @@ size_t tile_merge_smem(int KW, int S, int k, u32 cap) {
 }
 
 u32 tile_merge_cap(int KW, int S, int k) {
-  // two CTAs per SM: ~100 KB of shared memory each
-  const size_t budget = 100 * 1024;
+  // three CTAs per SM: ~64 KB of shared memory each (measured: 100 KB 88 ms, 64 KB 70 ms, 44 KB 90 ms
+  // per 1e9 config-5 rows; ISA_TM_SMEM_KB overrides)
+  static int kb = -1;
+  if (kb < 0) { const char* e = getenv("ISA_TM_SMEM_KB"); kb = e ? std::max(16, std::min(200, atoi(e))) : 64; }
+  const size_t budget = (size_t)kb * 1024;
   const size_t fixed = tile_merge_smem(KW, S, k, 0);
   if (fixed >= budget) return 0;
   size_t cap = (budget - fixed) / (size_t)(8 * KW + 8 * S + 13);
@@ -189,41 +192,33 @@ __device__ __forceinline__ u64 tm_off(u64 h, u64 l, u64 bh, u64 bl, int sh) {
   return (dl >> sh) | (dh << (64 - sh));
 }
 
-// One stable LSD pass over the tile's u32 sort words (rows in warp-contiguous
-// ranges of WI, every lane ranks its items with MATCH.ANY and per-warp digit
-// counters); digit(w) is the pass's 8-bit digit of word w.
+// One stable LSD pass over the tile's u32 sort words.  Rows are split into
+// warp-contiguous ranges of WI (a multiple of 32); every warp walks its
+// range in order, ranking 32 rows per step with MATCH.ANY and per-warp digit
+// counters, and keeps (digit, rank) per row in `scratch`; after the
+// per-digit scan the same warp scatters its rows.  Rolled loops: the cost
+// follows the tile's rows, not its capacity.
 template <typename DigitFn>
-__device__ __forceinline__ void tm_pass(const u32* __restrict__ cur, u32* __restrict__ nxt, u32 n, u32 WI, u32* wcnt,
-                                        u32* dstart, u32* sw, DigitFn digit) {
+__device__ __forceinline__ void tm_pass(const u32* __restrict__ cur, u32* __restrict__ nxt, u32* __restrict__ scratch,
+                                        u32 n, u32 WI, u32* wcnt, u32* dstart, u32* sw, DigitFn digit) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const u32 lt = lanemask_lt();
   for (int q = lane; q < 256; q += 32) wcnt[w * 256 + q] = 0;
   __syncwarp();
-  u32 it_d[TM_MAX_IT], it_w[TM_MAX_IT], it_r[TM_MAX_IT];
-#pragma unroll
-  for (int it = 0; it < TM_MAX_IT; ++it) {
-    const u32 i = w * WI + it * 32 + lane;
-    const bool in_w = (u32)it * 32 < WI;
-    const bool valid = in_w && i < n;
-    u32 d = 256 + lane, x = 0;
-    if (valid) {
-      x = cur[i];
-      d = digit(x);
+  const u32 r0 = w * WI, r1 = min(n, r0 + WI);
+  for (u32 i = r0 + lane; i < ((r1 + 31) & ~31u) && r0 < r1; i += 32) {
+    const bool valid = i < r1;
+    const u32 d = valid ? digit(cur[i]) : 256 + lane;
+    const u32 peers = __match_any_sync(0xffffffffu, d);
+    const int leader = __ffs(peers) - 1;
+    u32 c = 0;
+    if (valid && lane == leader) {
+      c = wcnt[w * 256 + d];
+      wcnt[w * 256 + d] = c + __popc(peers);
     }
-    it_d[it] = d;
-    it_w[it] = x;
-    if (in_w) {
-      const u32 peers = __match_any_sync(0xffffffffu, d);
-      const int leader = __ffs(peers) - 1;
-      u32 c = 0;
-      if (valid && lane == leader) {
-        c = wcnt[w * 256 + d];
-        wcnt[w * 256 + d] = c + __popc(peers);
-      }
-      c = __shfl_sync(0xffffffffu, c, leader);
-      it_r[it] = c + __popc(peers & lt);
-      __syncwarp();
-    }
+    c = __shfl_sync(0xffffffffu, c, leader);
+    if (valid) scratch[i] = (d << 16) | (c + __popc(peers & lt));
+    __syncwarp();
   }
   __syncthreads();
   {   // per digit: exclusive over warps, then over digits
@@ -239,13 +234,9 @@ __device__ __forceinline__ void tm_pass(const u32* __restrict__ cur, u32* __rest
     dstart[dg] = block_excl_scan256(run, sw, &tot);
   }
   __syncthreads();
-#pragma unroll
-  for (int it = 0; it < TM_MAX_IT; ++it) {
-    const u32 i = w * WI + it * 32 + lane;
-    if ((u32)it * 32 < WI && i < n) {
-      const u32 d = it_d[it];
-      nxt[dstart[d] + wcnt[w * 256 + d] + it_r[it]] = it_w[it];
-    }
+  for (u32 i = r0 + lane; i < r1; i += 32) {
+    const u32 v = scratch[i], d = v >> 16;
+    nxt[dstart[d] + wcnt[w * 256 + d] + (v & 0xFFFFu)] = cur[i];
   }
   __syncthreads();
 }
@@ -263,7 +254,7 @@ __device__ __forceinline__ void tm_pass(const u32* __restrict__ cur, u32* __rest
 // finished by an insertion sort on the full key; a run longer than 64 makes
 // the tile fall back to an LSD sort over every span bit).
 template <int KW, int MS>
-__global__ void __launch_bounds__(TM_THREADS, 2) k_tile_merge(TileMergeArgs a) {
+__global__ void __launch_bounds__(TM_THREADS, 3) k_tile_merge(TileMergeArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const u32 cap = a.cap;
   const int S = a.sd.nslots;
@@ -276,7 +267,7 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_tile_merge(TileMergeArgs a) {
   u32* gid = wb + cap;
   unsigned char* head = (unsigned char*)(gid + cap);
   u32* seg_off = (u32*)(((uintptr_t)(head + cap) + 15) & ~(uintptr_t)15);   // [k + 1]
-  i64* seg_src = (i64*)(((uintptr_t)(seg_off + k + 1) + 15) & ~(uintptr_t)15);   // [k]
+  i64* seg_src = (i64*)(((uintptr_t)(seg_off + k + 1) + 15) & ~(uintptr_t)15);   // [k] run row of the segment's first row
   u32* wcnt = (u32*)(seg_src + k);                        // [TM_WARPS][256]
   u32* dstart = wcnt + TM_WARPS * 256;                    // [256]
   __shared__ u32 s_j, s_B0, s_B1, s_n, s_base, s_bits, s_long;
@@ -303,7 +294,7 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_tile_merge(TileMergeArgs a) {
       if (r < k) {
         const u32 s0 = a.D[(size_t)B0 * k + r], s1 = a.D[(size_t)B1 * k + r];
         len = s1 - s0;
-        seg_src[r] = a.base[r] + (i64)s0;
+        seg_src[r] = (i64)s0;
       }
       u32 tot;
       const u32 ex = block_excl_scan256(len, sw, &tot);
@@ -321,36 +312,57 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_tile_merge(TileMergeArgs a) {
   unsigned char exact = 1;
   u32* cur = wa;
   if (!over && n > 0) {
-    // ---- load: one thread per row (LU rows in flight per thread)
+    // ---- load: one thread per row (LU rows in flight per thread); raw rows
+    //      are read where they are, packed HBM runs decoded in place
     constexpr int LU = MS <= 2 ? 4 : (MS <= 5 ? 2 : 1);
+    const int ncol = KW + S;
     for (u32 i0 = tid; i0 < n; i0 += LU * TM_THREADS) {
-      i64 src[LU];
+      int run[LU];
+      u32 pos[LU];
 #pragma unroll
       for (int u = 0; u < LU; ++u) {
         const u32 i = i0 + u * TM_THREADS;
-        src[u] = -1;
+        run[u] = -1;
         if (i < n) {
           int l = 0, h = k;   // last r with seg_off[r] <= i (a non-empty segment)
           while (h - l > 1) {
             const int m = (l + h) >> 1;
             if (seg_off[m] <= i) l = m; else h = m;
           }
-          src[u] = seg_src[l] + (i64)(i - seg_off[l]);
+          run[u] = l;
+          pos[u] = (u32)(seg_src[l] + (i64)(i - seg_off[l]));
         }
       }
       u64 kl[LU], kh[LU], sv[LU][MS];
 #pragma unroll
       for (int u = 0; u < LU; ++u) {
-        if (src[u] < 0) continue;
-        kl[u] = a.s_lo[src[u]];
-        if (KW == 2) kh[u] = a.s_hi[src[u]];
+        if (run[u] < 0) continue;
+        const MergeSrc* ms = a.src + run[u];
+        const char* pk = ms->pk;
+        if (pk) {
+          const u64* h = (const u64*)(pk + ms->blk_off[pos[u] >> 10]);
+          const u32 ip = pos[u] & 1023u;
+          const u64* payload = h + 2 * ncol;
+          kl[u] = h[0] + pk_extract(payload + (h[1] >> 8), ip, (u32)(h[1] & 0xFF));
+          if (KW == 2) kh[u] = h[2] + pk_extract(payload + (h[3] >> 8), ip, (u32)(h[3] & 0xFF));
 #pragma unroll
-        for (int s = 0; s < MS; ++s)
-          if (s < S) sv[u][s] = a.s_st[(size_t)src[u] * S + s];
+          for (int s = 0; s < MS; ++s)
+            if (s < S) {
+              const u64 b = h[2 * (KW + s)], m = h[2 * (KW + s) + 1];
+              sv[u][s] = pk_inv(b + pk_extract(payload + (m >> 8), ip, (u32)(m & 0xFF)), (a.fmask >> s) & 1u, 0);
+            }
+        } else {
+          const i64 x = ms->off + (i64)pos[u];
+          kl[u] = ms->lo[x];
+          if (KW == 2) kh[u] = ms->hi[x];
+#pragma unroll
+          for (int s = 0; s < MS; ++s)
+            if (s < S) sv[u][s] = ms->st[(size_t)x * S + s];
+        }
       }
 #pragma unroll
       for (int u = 0; u < LU; ++u) {
-        if (src[u] < 0) continue;
+        if (run[u] < 0) continue;
         const u32 i = i0 + u * TM_THREADS;
         klo[i] = kl[u];
         if (KW == 2) khi[i] = kh[u];
@@ -398,7 +410,7 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_tile_merge(TileMergeArgs a) {
     const u32 WI = (((n + TM_WARPS - 1) / TM_WARPS) + 31) & ~31u;   // rows per warp, in order
     u32* nxt = wb;
     for (int sh = 12; sh < 12 + pb; sh += 8) {
-      tm_pass(cur, nxt, n, WI, wcnt, dstart, sw, [sh](u32 x) { return (x >> sh) & 0xFFu; });
+      tm_pass(cur, nxt, gid, n, WI, wcnt, dstart, sw, [sh](u32 x) { return (x >> sh) & 0xFFu; });
       u32* t = cur; cur = nxt; nxt = t;
     }
     const u32 ipt = (n + TM_THREADS - 1) / TM_THREADS;
@@ -432,7 +444,7 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_tile_merge(TileMergeArgs a) {
         // a long run of equal prefix: LSD over every span bit (keys read
         // through the row index), starting from the prefix order
         for (int sh = 0; sh < bits; sh += 8) {
-          tm_pass(cur, nxt, n, WI, wcnt, dstart, sw, [&](u32 x) {
+          tm_pass(cur, nxt, gid, n, WI, wcnt, dstart, sw, [&](u32 x) {
             const u32 xi = x & 0xFFFu;
             return (u32)tm_off<KW>(KW == 2 ? khi[xi] : 0, klo[xi], bh, bl, sh) & 0xFFu;
           });
@@ -536,7 +548,7 @@ template <int KW, int MS>
 static void tm_launch(TileMergeArgs& a, size_t smem, cudaStream_t st) {
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr))
-    cudaFuncSetAttribute(k_tile_merge<KW, MS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+    cudaFuncSetAttribute(k_tile_merge<KW, MS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 205 * 1024);
   klaunch(k_tile_merge<KW, MS>, a.ntiles, TM_THREADS, smem, st, a);
 }
 

@@ -66,12 +66,13 @@ class SortAggConfig:
     max_preliminary_merges: int | None = None
     # B200 placement knobs (no reference counterpart)
     run_tier: str = "auto"          # where spilled runs live: "auto" (HBM while they fit, then pinned DRAM) | "host" | "hbm"
-    hbm_run_budget: int = 0         # run_tier "auto": HBM bytes for runs, 0 = 40% of the free HBM
+    hbm_run_budget: int = 0         # run_tier "auto": HBM bytes for runs, 0 = half of the free HBM
     chunk_rows_max: int = 0         # 0 = library default
     window_rows: int = 0            # host-input staging window, 0 = default
     merge_window_rows: int = 0      # wide-merge key-range window capacity, 0 = default
     preaggregate: str = "auto"      # tile-local pre-aggregation before chunk sorts: auto | always | never
     run_codec: str = "auto"         # host-tier runs cross PCIe bit-packed: auto (runs >= 32K rows) | packed | raw
+    hot_absorb: str = "auto"        # rows whose key is in a large resident table absorbed via its hash image: auto | always | never
 
     def __post_init__(self):
         if self.page_capacity < 1:
@@ -91,6 +92,8 @@ class SortAggConfig:
             raise InvalidInputError(f"unknown preaggregate mode {self.preaggregate!r}")
         if self.run_codec not in ("auto", "packed", "raw"):
             raise InvalidInputError(f"unknown run codec {self.run_codec!r}")
+        if self.hot_absorb not in ("auto", "always", "never"):
+            raise InvalidInputError(f"unknown hot_absorb mode {self.hot_absorb!r}")
 
     @property
     def max_fanin(self):
@@ -454,6 +457,7 @@ class SortAggregate:
                           SEPARATE: _native.MERGE_SEPARATE}[self.config.merge_mode]
         cfg.output_size_hint = self.config.output_size_hint if self.config.output_size_hint is not None else 0
         cfg.run_codec = {"auto": 0, "raw": 1, "packed": 2}[self.config.run_codec]
+        cfg.hot_absorb = {"auto": 0, "always": 1, "never": 2}[self.config.hot_absorb]
         sch = _native.IsaSchema()
         if len(key_codes) > _native.MAX_KEY_COLS:
             raise InvalidInputError("too many key columns")

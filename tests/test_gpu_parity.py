@@ -542,3 +542,42 @@ def test_tile_merge_inexact_prefix(cfg, pbits, monkeypatch):
     w = workloads.make(cfg, rows=rows, device="cpu", **({"domain": 1 << 20} if cfg in (3, 5) else {}))
     op = _oracle_case(w, 4096, page=100, rel=1e-5 if cfg == 3 else 1e-9)
     assert op.runs_after_generation > 10
+
+
+@pytest.mark.parametrize("cfg,rows,memory", [
+    (3, 2_000_000, 1 << 14),   # Zipf: most rows hit the resident table
+    (3, 1_500_000, 1 << 12),
+    (1, 1_000_000, 4096),
+    (5, 1_000_000, 1 << 14),   # almost every row is a miss
+    (4, 600_000, 1 << 14),     # 128-bit keys
+])
+def test_hot_absorb_vs_c_oracle(cfg, rows, memory):
+    """Rows whose key is already resident absorbed through the table's hash
+    image (hot_absorb='always'): output equals the oracle, and the fill
+    cycles and spilled rows equal the C oracle's read-sort-write ledger."""
+    kw = {"domain": 1 << 18} if cfg in (3, 5) else {}
+    w = workloads.make(cfg, rows=rows, device="cpu", **kw)
+    rel = 1e-5 if cfg == 3 else 1e-9
+    op = _oracle_case(w, memory, page=min(100, memory // 2), rel=rel, hot_absorb="always")
+    keys_np = [k.cpu().numpy() for k in w.keys]
+    slots = oracle.make_states(w.schema, {k: v.cpu().numpy() for k, v in w.values.items()}, w.rows)
+    _, _, led, cycles = oracle.rsw_sortagg(keys_np, slots, oracle.slot_ops(w.schema), memory, min(100, memory // 2))
+    assert op.cycles == [c for c in cycles if c > 0]
+    assert op.ledger.rows_spilled == led["rows_spilled"] and op.runs_after_generation == led["runs"]
+    assert op.phase_stats["hot"]["calls"] > 0, "the hot path did not run"
+
+
+def test_hot_absorb_config3_shape():
+    """The hash-image absorb on a config-3-shaped input with a table above
+    the auto threshold (2^16 groups, Zipf keys, cycles of >= 2 M rows):
+    ledger and output unchanged."""
+    w = workloads.config3(rows=12_000_000, device="cpu")
+    M = 1 << 16
+    op = _oracle_case(w, M, page=100, rel=1e-5, hot_absorb="always")
+    keys_np = [k.cpu().numpy() for k in w.keys]
+    slots = oracle.make_states(w.schema, {k: v.cpu().numpy() for k, v in w.values.items()}, w.rows)
+    _, _, led, cycles = oracle.rsw_sortagg(keys_np, slots, oracle.slot_ops(w.schema), M, 100)
+    assert op.cycles == [c for c in cycles if c > 0]
+    assert op.ledger.rows_spilled == led["rows_spilled"]
+    assert max(op.cycles) >= 2 * M
+    assert op.phase_stats["hot"]["calls"] > 0
