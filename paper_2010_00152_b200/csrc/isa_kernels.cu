@@ -407,6 +407,193 @@ __global__ void __launch_bounds__(256) k_rs_hist_all(const u64* __restrict__ klo
     if (h[i]) atomicAdd(&ghist[i], h[i]);
 }
 
+// ---------------------------------------------------------------------------
+// Hybrid sort for wide keys: LSD passes over the top 16 bits of the sort
+// field only (two onesweep passes), then every run of equal top-16 bits (a
+// "bucket", ~n / 65536 rows for spread keys) is finished inside one CTA's
+// shared memory -- an LSD sort of the bucket rows over the field bits that
+// vary inside the CTA's range, keys read through a u16 row index.  Replaces
+// npass - 2 global passes (config 3's 64-bit keys: 8 -> 2 + 1 local) with
+// one read + write.  Stable: every pass is stable and the top-16 passes keep
+// equal keys in input order.  A bucket larger than a CTA's capacity
+// (clustered keys) sets *overflow; the caller then finishes with the plain
+// LSD passes from the top-16-sorted array (stable from any stable order).
+#define RL_THREADS 256
+#define RL_WARPS (RL_THREADS / 32)
+// rows one CTA sorts (template CAP: 4096 or 1024, ISA_RL_CAP); nominal rows
+// per CTA = CAP / 2 (ranges snap to bucket starts)
+
+// top-16 bucket of row i: field bits [bit_hi - 16, bit_hi) of the 128-bit key
+// (packed words: key bits [pk_lo, pk_lo + 32) sit in word bits 32..63)
+template <int KW, int PKIN>
+__device__ __forceinline__ u32 rl_top(const u64* __restrict__ lo, const u64* __restrict__ hi, u32 i, int bit_hi,
+                                      int pk_lo) {
+  if (PKIN) return (u32)(lo[i] >> (32 + bit_hi - 16 - pk_lo)) & 0xFFFFu;
+  const u64 h = KW == 2 ? hi[i] : 0, l = lo[i];
+  const int sft = bit_hi - 16;
+  u64 v;
+  if (sft >= 64) v = h >> (sft - 64);
+  else if (sft == 0) v = l;
+  else v = (l >> sft) | (sft > 48 ? (h << (64 - sft)) : 0ull);
+  return (u32)v & 0xFFFFu;
+}
+
+// CTA range starts: bnd[c] = first row of the bucket holding row c * RL_SPAN
+template <int KW, int PKIN>
+__global__ void k_rs_bounds(const u64* __restrict__ lo, const u64* __restrict__ hi, u32 n, u32 nctas, int bit_hi,
+                            int pk_lo, u32* __restrict__ bnd, u32* __restrict__ overflow, u32 RL_SPAN) {
+  const u32 c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > nctas) return;
+  if (c == 0) { bnd[0] = 0; return; }
+  if (c == nctas) { bnd[c] = n; return; }
+  const u32 x = c * RL_SPAN;
+  const u32 t = rl_top<KW, PKIN>(lo, hi, x, bit_hi, pk_lo);
+  u32 l = x > RL_SPAN ? x - RL_SPAN : 0, h = x;   // smallest j in [l, x] with top(j) == t
+  if (l > 0 && rl_top<KW, PKIN>(lo, hi, l, bit_hi, pk_lo) == t) atomicExch(overflow, 1u);   // bucket > RL_SPAN
+  while (l < h) {
+    const u32 m = (l + h) >> 1;
+    if (rl_top<KW, PKIN>(lo, hi, m, bit_hi, pk_lo) < t) l = m + 1; else h = m;
+  }
+  bnd[c] = l;
+}
+
+template <int KW, int PKIN, int RL_CAP>
+__global__ void __launch_bounds__(RL_THREADS, RL_CAP <= 1024 ? 6 : 2) k_rs_local(const u64* __restrict__ lo_in, const u64* __restrict__ hi_in,
+                                                             const u32* __restrict__ v_in, u64* __restrict__ lo_out,
+                                                             u64* __restrict__ hi_out, u32* __restrict__ v_out,
+                                                             const u32* __restrict__ bnd, int bit_lo, int bit_hi,
+                                                             int pk_lo, const u64* __restrict__ pk_const,
+                                                             u32* __restrict__ overflow) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  u64* k_lo = (u64*)smem;                         // [RL_CAP]
+  u64* k_hi = k_lo + RL_CAP;                      // [RL_CAP] (KW == 2)
+  u32* vv = (u32*)(k_lo + (size_t)KW * RL_CAP);   // [RL_CAP]
+  unsigned short* o0 = (unsigned short*)(vv + RL_CAP);
+  unsigned short* o1 = o0 + RL_CAP;
+  u32* scratch = (u32*)(o1 + RL_CAP);             // [RL_CAP] (digit, rank) per row
+  u32* wcnt = scratch + RL_CAP;                   // [RL_WARPS][256]
+  u32* dstart = wcnt + RL_WARPS * 256;            // [256]
+  __shared__ u32 sw[RL_WARPS];
+  __shared__ u64 s_or_lo[RL_WARPS], s_or_hi[RL_WARPS];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const u32 r0 = bnd[blockIdx.x], r1 = bnd[blockIdx.x + 1];
+  if (r1 <= r0) return;
+  const u32 n = r1 - r0;
+  if (n > RL_CAP) {   // a bucket too large for one CTA: the caller falls back
+    if (tid == 0) atomicExch(overflow, 1u);
+    return;
+  }
+  const u64 kc = PKIN ? *pk_const : 0;
+  // load (coalesced); packed words unpack here
+  u64 orl = 0, orh = 0;
+  for (u32 i = tid; i < n; i += RL_THREADS) {
+    u64 l, h = 0;
+    u32 v;
+    if (PKIN) {
+      const u64 wd = lo_in[r0 + i];
+      l = kc | ((wd >> 32) << pk_lo);
+      v = (u32)wd;
+    } else {
+      l = lo_in[r0 + i];
+      if (KW == 2) h = hi_in[r0 + i];
+      v = v_in[r0 + i];
+    }
+    k_lo[i] = l;
+    if (KW == 2) k_hi[i] = h;
+    vv[i] = v;
+    o0[i] = (unsigned short)i;
+  }
+  __syncthreads();
+  // field bits that vary inside the range (relative to its first row)
+  {
+    const u64 f_lo = k_lo[0], f_hi = KW == 2 ? k_hi[0] : 0;
+    for (u32 i = tid; i < n; i += RL_THREADS) {
+      orl |= k_lo[i] ^ f_lo;
+      if (KW == 2) orh |= k_hi[i] ^ f_hi;
+    }
+    for (int o = 16; o; o >>= 1) {
+      orl |= __shfl_xor_sync(0xffffffffu, orl, o);
+      orh |= __shfl_xor_sync(0xffffffffu, orh, o);
+    }
+    if (lane == 0) { s_or_lo[w] = orl; s_or_hi[w] = orh; }
+    __syncthreads();
+    orl = 0; orh = 0;
+    for (int q = 0; q < RL_WARPS; ++q) { orl |= s_or_lo[q]; orh |= s_or_hi[q]; }
+  }
+  // highest varying bit below bit_hi
+  int msb = -1;
+  {
+    u64 mh = orh, ml = orl;
+    if (bit_hi < 128) {
+      if (bit_hi >= 64) mh &= bit_hi == 64 ? 0ull : ((1ull << (bit_hi - 64)) - 1);
+      else { mh = 0; ml &= (1ull << bit_hi) - 1; }
+    }
+    if (mh) msb = 127 - __clzll((long long)mh);
+    else if (ml) msb = 63 - __clzll((long long)ml);
+  }
+  const int npass = msb < bit_lo ? 0 : (msb - bit_lo) / 8 + 1;
+  // LSD passes over [bit_lo, bit_lo + 8 npass): warp-contiguous rows in order
+  const u32 WI = (((n + RL_WARPS - 1) / RL_WARPS) + 31) & ~31u;
+  const u32 lt = lanemask_lt();
+  unsigned short* cur = o0;
+  unsigned short* nxt = o1;
+  for (int p = 0; p < npass; ++p) {
+    const int sft = bit_lo + 8 * p;
+    for (int q = lane; q < 256; q += 32) wcnt[w * 256 + q] = 0;
+    __syncwarp();
+    const u32 a0 = w * WI, a1 = min(n, a0 + WI);
+    for (u32 i = a0 + lane; i < ((a1 + 31) & ~31u) && a0 < a1; i += 32) {
+      const bool valid = i < a1;
+      u32 d = 256 + lane;
+      if (valid) {
+        const u32 x = cur[i];
+        d = digit_of(KW == 2 ? k_hi[x] : 0, k_lo[x], sft);
+      }
+      const u32 peers = __match_any_sync(0xffffffffu, d);
+      const int leader = __ffs(peers) - 1;
+      u32 c = 0;
+      if (valid && lane == leader) {
+        c = wcnt[w * 256 + d];
+        wcnt[w * 256 + d] = c + __popc(peers);
+      }
+      c = __shfl_sync(0xffffffffu, c, leader);
+      if (valid) scratch[i] = (d << 16) | (c + __popc(peers & lt));
+      __syncwarp();
+    }
+    __syncthreads();
+    {
+      const int dg = tid;
+      u32 run = 0;
+#pragma unroll
+      for (int ww = 0; ww < RL_WARPS; ++ww) {
+        const u32 c = wcnt[ww * 256 + dg];
+        wcnt[ww * 256 + dg] = run;
+        run += c;
+      }
+      u32 tot;
+      dstart[dg] = block_excl_scan256(run, sw, &tot);
+    }
+    __syncthreads();
+    for (u32 i = a0 + lane; i < a1; i += 32) {
+      const u32 v = scratch[i], d = v >> 16;
+      nxt[dstart[d] + wcnt[w * 256 + d] + (v & 0xFFFFu)] = cur[i];
+    }
+    __syncthreads();
+    unsigned short* t = cur; cur = nxt; nxt = t;
+  }
+  // write in sorted order (coalesced)
+  for (u32 i = tid; i < n; i += RL_THREADS) {
+    const u32 x = cur[i];
+    lo_out[r0 + i] = k_lo[x];
+    if (KW == 2) hi_out[r0 + i] = k_hi[x];
+    v_out[r0 + i] = vv[x];
+  }
+}
+
+static size_t rl_smem(int KW, int cap) {
+  return (size_t)cap * (8 * KW + 4 + 2 + 2 + 4) + (RL_WARPS * 256 + 256) * 4 + 64;
+}
+
 static size_t rs_scatter_smem(int KW, bool packed = false) {
   return (RS_WARPS * 256 + 256 + 256 + 8) * sizeof(u32) + (size_t)RS_TILE * (packed ? 8 : 8 * KW + 4);
 }
@@ -415,11 +602,18 @@ static size_t rs_scatter_smem(int KW, bool packed = false) {
 // The status words sit at a fixed offset and are only ever written as
 // status words (or zero), so no stale counter can alias a live epoch.
 #define RS_AUX_HDR 16640
-size_t sort_aux_bytes(u32 n) { return RS_AUX_HDR + (size_t)256 * ((n + RS_TILE - 1) / RS_TILE) * 8; }
+size_t sort_aux_bytes(u32 n) {
+  return RS_AUX_HDR + (size_t)256 * ((n + RS_TILE - 1) / RS_TILE) * 8 + ((size_t)n / 512 + 4) * 4 + 64;
+}
 static std::atomic<u32> g_rs_epoch{0};
 
-int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStream_t st, int64_t* launches,
-                     int start) {
+// LSD onesweep passes over [bit_lo, bit_hi).  pack_lo >= 0: pack (key bits
+// [pack_lo, pack_lo + 32) << 32 | row id) on the first pass whatever the
+// range; pack_lo == -2: never pack; -1: pack when the range fits 32 bits.
+// leave_packed: the last pass keeps the packed words (the local sort of the
+// hybrid path unpacks them).
+static int radix_lsd(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStream_t st, int64_t* launches, int start,
+                     int pack_lo, bool leave_packed) {
   int cur = start;
   if (n <= 1 || bit_hi <= bit_lo) return cur;
   static std::atomic<unsigned long long> attr_set[3];
@@ -451,7 +645,10 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
   // packed passes: one 8-byte word per row when the varying key bits fit 32
   static int pk_env = -1;
   if (pk_env < 0) { const char* e = getenv("ISA_PACKED"); pk_env = e && e[0] == '0' ? 0 : 1; }
-  const bool packed = pk_env && KW == 1 && b.pack_ok && ntiles > 1 && npass >= 2 && bit_hi - bit_lo <= 32;
+  const bool packed = pack_lo >= 0 ? true
+                                   : (pack_lo == -1 && pk_env && KW == 1 && b.pack_ok && ntiles > 1 && npass >= 2 &&
+                                      bit_hi - bit_lo <= 32);
+  const int pk_lo = pack_lo >= 0 ? pack_lo : bit_lo;
   const size_t psmem = rs_scatter_smem(1, true);
   static int lb_sleep = -1;   // look-back back-off (ns) while a predecessor has not published
   if (lb_sleep < 0) { const char* e = getenv("ISA_LB_SLEEP"); lb_sleep = e ? atoi(e) : 0; }
@@ -511,20 +708,21 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
   do {                                                                                                       \
     if (ballot[p])                                                                                           \
       klaunch(k_rs_scatter<1, true, PK>, ntiles, RS_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,      \
-              b.val[cur], b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - bit_lo, stt, gh, tc, ep, bit_lo, \
+              b.val[cur], b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - pk_lo, stt, gh, tc, ep, pk_lo,   \
               pk_const, lb_sleep);                                                                                     \
     else                                                                                                     \
       klaunch(k_rs_scatter<1, false, PK>, ntiles, RS_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,     \
-              b.val[cur], b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - bit_lo, stt, gh, tc, ep, bit_lo, \
+              b.val[cur], b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - pk_lo, stt, gh, tc, ep, pk_lo,   \
               pk_const, lb_sleep);                                                                                     \
   } while (0)
     // algorithmic bytes of the pass: every row's key words + row id read and written once
     // (packed passes: 8-byte words in the middle, 12 -> 8 / 8 -> 12 at the ends)
-    const int64_t pass_bytes = (int64_t)n * (packed ? (p == 0 || p == npass - 1 ? 20 : 16) : 2 * (8 * KW + 4));
+    const int64_t pass_bytes =
+        (int64_t)n * (packed ? (p == 0 || (p == npass - 1 && !leave_packed) ? 20 : 16) : 2 * (8 * KW + 4));
     kt_begin(KF_SCATTER, st);
     if (packed) {
       if (p == 0) RS_PK(1);
-      else if (p == npass - 1) RS_PK(3);
+      else if (p == npass - 1 && !leave_packed) RS_PK(3);
       else RS_PK(2);
     } else if (KW == 2) {
       if (ballot[p]) RS_GO(2, true, b.hi[cur], b.hi[nxt]);
@@ -540,6 +738,87 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
     cur = nxt;
   }
   return cur;
+}
+
+// unpack packed words (key bits << 32 | row id) into key / row-id columns
+__global__ void k_rs_unpack(const u64* __restrict__ w, u32 n, int pk_lo, const u64* __restrict__ pk_const,
+                            u64* __restrict__ lo, u32* __restrict__ val) {
+  const u64 kc = *pk_const;
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const u64 x = w[i];
+    lo[i] = kc | ((x >> 32) << pk_lo);
+    val[i] = (u32)x;
+  }
+}
+
+int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStream_t st, int64_t* launches,
+                     int start) {
+  // opt-in (ISA_HYBRID=1, read per sort): measured slower than plain
+  // onesweep LSD (config 5 sort 42 -> 58 ms, config 3 92 -> 143 ms per 1e9
+  // rows, profiles/r2_ab_hybrid.txt)
+  const char* he = getenv("ISA_HYBRID");
+  const int hyb_env = he && he[0] == '1' ? 1 : 0;
+  const int npass = (bit_hi - bit_lo + 7) / 8;
+  if (!(hyb_env && b.map_dev && npass >= 3 && n >= (1u << 16) && n <= 0x7FFFFFFFu))
+    return radix_lsd(KW, b, n, bit_lo, bit_hi, st, launches, start, -1, false);
+  const char* ce = getenv("ISA_RL_CAP");
+  const int cap_env = ce && atoi(ce) <= 1024 ? 1024 : 4096;
+  const u32 RL_CAP = (u32)cap_env, RL_SPAN = RL_CAP / 2;
+  static std::atomic<unsigned long long> attr_set[3];
+  if (first_on_device(attr_set[KW])) {
+    const int s4 = (int)rl_smem(KW, 4096), s1 = (int)rl_smem(KW, 1024);
+    if (KW == 2) {
+      cudaFuncSetAttribute(k_rs_local<2, 0, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, s4);
+      cudaFuncSetAttribute(k_rs_local<2, 0, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1);
+    } else {
+      cudaFuncSetAttribute(k_rs_local<1, 0, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, s4);
+      cudaFuncSetAttribute(k_rs_local<1, 1, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, s4);
+      cudaFuncSetAttribute(k_rs_local<1, 0, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1);
+      cudaFuncSetAttribute(k_rs_local<1, 1, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1);
+    }
+  }
+  static int pk_env = -1;
+  if (pk_env < 0) { const char* e = getenv("ISA_PACKED"); pk_env = e && e[0] == '0' ? 0 : 1; }
+  const bool packed = pk_env && KW == 1 && b.pack_ok && bit_hi - bit_lo <= 32;
+  // 1. the top 16 bits of the field
+  int cur = radix_lsd(KW, b, n, bit_hi - 16, bit_hi, st, launches, start, packed ? bit_lo : -2, packed);
+  const int nxt = cur ^ 1;
+  u64* pk_const = (u64*)((char*)b.aux + RS_AUX_HDR - 64);
+  u32* overflow = (u32*)((char*)b.aux + RS_AUX_HDR - 32);
+  const u32 ntiles = (n + RS_TILE - 1) / RS_TILE;
+  u32* bnd = (u32*)((char*)b.aux + RS_AUX_HDR + (size_t)256 * ntiles * 8);
+  const u32 nctas = (n + RL_SPAN - 1) / RL_SPAN;
+  cudaMemsetAsync(overflow, 0, sizeof(u32), st);
+  // 2. CTA ranges snapped to bucket starts, 3. local sort of every range
+  kt_begin(KF_SCATTER, st);
+  const int bg = (int)((nctas + 256) / 256);
+  if (KW == 2) klaunch(k_rs_bounds<2, 0>, bg, 256, 0, st, b.lo[cur], b.hi[cur], n, nctas, bit_hi, bit_lo, bnd, overflow, RL_SPAN);
+  else if (packed) klaunch(k_rs_bounds<1, 1>, bg, 256, 0, st, b.lo[cur], (const u64*)nullptr, n, nctas, bit_hi, bit_lo, bnd, overflow, RL_SPAN);
+  else klaunch(k_rs_bounds<1, 0>, bg, 256, 0, st, b.lo[cur], (const u64*)nullptr, n, nctas, bit_hi, bit_lo, bnd, overflow, RL_SPAN);
+  const size_t sm = rl_smem(KW, RL_CAP);
+#define RL_GO(K, P, C, HI_IN, HI_OUT)                                                                             \
+  klaunch(k_rs_local<K, P, C>, nctas, RL_THREADS, sm, st, b.lo[cur], HI_IN, b.val[cur], b.lo[nxt], HI_OUT, b.val[nxt], \
+          bnd, bit_lo, bit_hi, bit_lo, pk_const, overflow)
+#define RL_CAPS(K, P, HI_IN, HI_OUT) \
+  { if (RL_CAP == 1024) RL_GO(K, P, 1024, HI_IN, HI_OUT); else RL_GO(K, P, 4096, HI_IN, HI_OUT); }
+  if (KW == 2) RL_CAPS(2, 0, b.hi[cur], b.hi[nxt])
+  else if (packed) RL_CAPS(1, 1, (const u64*)nullptr, (u64*)nullptr)
+  else RL_CAPS(1, 0, (const u64*)nullptr, (u64*)nullptr)
+#undef RL_CAPS
+#undef RL_GO
+  kt_end(KF_SCATTER, (int64_t)n * (packed ? 20 : 2 * (8 * KW + 4)), st);
+  if (launches) *launches += 3;
+  // 4. a bucket too large for a CTA: plain LSD over every bit from the
+  //    top-16-sorted rows (stable from any stable order)
+  read_words(b.map_dev + 16 * 256 - 1, overflow, 1, st);
+  cudaStreamSynchronize(st);
+  if (((const volatile u32*)b.map_host)[16 * 256 - 1] == 0) return nxt;
+  if (packed) {
+    klaunch(k_rs_unpack, (int)std::min<u32>((n + 255) / 256, 148u * 16u), 256, 0, st, (const u64*)b.lo[cur], n, bit_lo, (const u64*)pk_const, b.lo[nxt],
+            b.val[nxt]);
+    cur = nxt;
+  }
+  return radix_lsd(KW, b, n, bit_lo, bit_hi, st, launches, cur, -2, false);
 }
 
 static int grid_for(u64 n, int threads, int cap = 148 * 16);

@@ -581,3 +581,39 @@ def test_hot_absorb_config3_shape():
     assert op.ledger.rows_spilled == led["rows_spilled"]
     assert max(op.cycles) >= 2 * M
     assert op.phase_stats["hot"]["calls"] > 0
+
+
+@pytest.mark.parametrize("cap", ["1024", "4096"])
+@pytest.mark.parametrize("on_host", [False, True])
+def test_hybrid_sort_clustered_bucket_falls_back(on_host, cap, monkeypatch):
+    """Half the rows share the top 16 bits of the sort field (a bucket far
+    larger than one CTA's local sort): the hybrid sort detects it and
+    finishes with plain LSD passes -- same result as the oracle."""
+    monkeypatch.setenv("ISA_HYBRID", "1")
+    monkeypatch.setenv("ISA_RL_CAP", cap)
+    g = torch.Generator().manual_seed(11)
+    n = 600_000
+    spread = torch.randint(0, 1 << 40, (n // 2,), generator=g, dtype=torch.int64)
+    dense = torch.randint(0, 1 << 20, (n - n // 2,), generator=g, dtype=torch.int64)
+    key = torch.cat([spread, dense])[torch.randperm(n, generator=g)]
+    val = torch.randint(-1000, 1000, (n,), generator=g, dtype=torch.int64)
+    w = _int_workload(key, val, 1 << 18)
+    slots = oracle.make_states(w.schema, {"v": val.numpy()}, n)
+    want_k, want_s = oracle.reference_aggregate([key.numpy()], slots, oracle.slot_ops(w.schema))
+    op = isa.SortAggregate(w.schema, _cfg(1 << 18, 100))
+    kk = [key.pin_memory()] if on_host else [key.cuda()]
+    vv = {"v": val.pin_memory() if on_host else val.cuda()}
+    _check(op.execute_columns(kk, vv), want_k, want_s)
+
+
+@pytest.mark.parametrize("cap", ["1024", "4096"])
+@pytest.mark.parametrize("cfg,rows,memory", [(3, 2_000_000, 1 << 20), (4, 1_000_000, 1 << 19), (5, 2_000_000, 1 << 20),
+                                             (1, 1_000_000, 1 << 19)])
+def test_hybrid_sort_vs_oracle(cfg, rows, memory, cap, monkeypatch):
+    """The hybrid sort (top-16 onesweep passes + CTA-local bucket sort) on
+    the config shapes: output and ledger equal the oracle's."""
+    monkeypatch.setenv("ISA_HYBRID", "1")
+    monkeypatch.setenv("ISA_RL_CAP", cap)
+    kw = {"domain": 1 << 24} if cfg in (3, 5) else {}
+    w = workloads.make(cfg, rows=rows, device="cpu", **kw)
+    _oracle_case(w, memory, page=100, rel=1e-5 if cfg == 3 else 1e-9)
