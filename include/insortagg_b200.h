@@ -96,7 +96,17 @@ typedef struct isa_config {
                                 it instead of being sorted (memindex.py:209-215): 0 auto (fill cycles of >= 2 M rows),
                                 1 always, 2 never */
   int64_t hbm_run_budget;    /* ISA_TIER_AUTO: bytes of HBM runs may use; 0 = half of the free HBM at execute start */
+  int32_t run_generation;    /* isa_run_generation (SortAggConfig.run_generation_mode) */
+  int32_t eviction_chunk;    /* replacement selection: rows evicted per step (SortAggConfig.eviction_chunk; 0 = page_capacity) */
 } isa_config;
+
+/* SortAggConfig.run_generation_mode (sortagg.py:43-44, 300-376):
+ * read-sort-write flushes the whole index when it is full; replacement
+ * selection evicts the eviction_chunk lowest keys of the current generation
+ * into the open run (generations + cursor, memindex.py:186-263).  Replacement
+ * selection runs in one persistent CTA (isa_seq.cu) and needs an integer key
+ * of <= 64 bits, <= 8 state slots and memory_budget <= 3500. */
+enum isa_run_generation { ISA_RUNGEN_RSW = 0, ISA_RUNGEN_RS = 1 };
 
 /* SortAggConfig.merge_mode (sortagg.py:45-47): wide = in-sort early
  * aggregation + one wide merge; traditional / separate = priority-queue run
@@ -153,6 +163,10 @@ typedef struct isa_ledger {
   double ms_wide_merge;
   double ms_host_sync;      /* host time blocked in stream synchronizations */
   double ms_spill_wait;     /* host-observed wait for table buffers still being spilled */
+  /* OutputEstimator.note_steady_probe totals (replacement selection, sortagg.py:113-119, 335-336) */
+  int64_t steady_probes;
+  int64_t steady_absorbs;
+  int64_t steady_resident_sum;
 } isa_ledger;
 
 /* device-time breakdown of the last execute (CUDA events on the caller's stream) */

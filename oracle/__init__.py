@@ -12,6 +12,11 @@ CPU restatements of the reference algorithm used only by tests/, by
 * ``rsw_sortagg`` — ctypes wrapper of rsw_oracle.c, the C restatement of
   ``index_run_generation`` (read-sort-write, sortagg.py:300-376) and
   ``wide_merge`` (sortagg.py:588-674) with the reference's spill ledger.
+* ``rs_run_generation`` — pure-Python restatement of replacement-selection
+  run generation with early aggregation (index_run_generation's RS branches,
+  sortagg.py:333-343, 356-369; OrderedIndex generations / cursor /
+  evict_range, memindex.py:186-263) for small inputs: run sizes, the
+  OutputEstimator's steady-probe totals (sortagg.py:113-119).
 * ``make_states`` / ``normalize_keys`` — Schema.make_state (core.py:162-182)
   over columns, and the order-preserving key image both oracles consume.
 
@@ -276,3 +281,73 @@ def parse_run_pages(data, arity, slots):
         off += 12 + length
     cat = lambda parts: np.concatenate(parts) if parts else np.zeros(0, dtype=np.int64)
     return [cat(k) for k in keys], [cat(s_) for s_ in states], counts
+
+
+# ------------------------------------------------- replacement selection ---
+
+def rs_run_generation(keys, memory_budget, chunk):
+    """Replacement selection with early aggregation over a sequence of
+    (hashable, orderable) keys; states are not tracked (the runs' rows are
+    what the ledger needs).  Returns (run sizes, (steady probes, steady
+    absorbs, steady resident sum)).
+
+    Follows sortagg.py:333-369 row by row: a key at or below the eviction
+    cursor lives in the next generation; a new key with the index full makes
+    the current generation evict its `chunk` lowest keys into the open run
+    (cursor = last evicted key); an exhausted generation closes the run and
+    the next one becomes current; the row is retried."""
+    import bisect
+    cur, nxt = [], []
+    cursor = None
+    runs, open_run = [], None
+    spilling = False
+    probes = absorbs = ressum = 0
+    for k in keys:
+        resident = len(cur) + len(nxt)
+        first = True
+        while True:
+            passed = cursor is not None and k <= cursor
+            tree = nxt if passed else cur
+            i = bisect.bisect_left(tree, k)
+            found = i < len(tree) and tree[i] == k
+            if found:
+                outcome = "absorbed"
+            elif len(cur) + len(nxt) >= memory_budget:
+                outcome = "evict"
+            else:
+                tree.insert(i, k)
+                outcome = "inserted"
+            if first and spilling:
+                probes += 1
+                ressum += resident
+                absorbs += outcome == "absorbed"
+            first = False
+            if outcome != "evict":
+                break
+            spilling = True
+            if open_run is None:
+                open_run = 0
+            ev = cur[:chunk]
+            del cur[:chunk]
+            open_run += len(ev)
+            if ev:
+                cursor = ev[-1]
+            if not cur:
+                runs.append(open_run)
+                open_run = None
+                cur, nxt = nxt, []
+                cursor = None
+    if runs or open_run is not None:
+        while True:
+            if cur:
+                open_run = (open_run or 0) + len(cur)
+                cur = []
+                continue
+            if open_run is not None:
+                runs.append(open_run)
+                open_run = None
+            if not nxt:
+                break
+            cur, nxt = nxt, []
+    return runs, (probes, absorbs, ressum)
+

@@ -85,6 +85,8 @@ class IsaConfig(ctypes.Structure):
         ("run_codec", ctypes.c_int32),
         ("hot_absorb", ctypes.c_int32),
         ("hbm_run_budget", ctypes.c_int64),
+        ("run_generation", ctypes.c_int32),
+        ("eviction_chunk", ctypes.c_int32),
     ]
 
 
@@ -122,6 +124,9 @@ class IsaLedger(ctypes.Structure):
         ("ms_wide_merge", ctypes.c_double),
         ("ms_host_sync", ctypes.c_double),
         ("ms_spill_wait", ctypes.c_double),
+        ("steady_probes", ctypes.c_int64),
+        ("steady_absorbs", ctypes.c_int64),
+        ("steady_resident_sum", ctypes.c_int64),
     ]
 
     def as_dict(self):

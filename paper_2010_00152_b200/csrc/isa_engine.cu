@@ -424,7 +424,9 @@ struct Engine {
                       &runref_dev, &bounds_lo, &bounds_hi, &bounds_out, &out_tmp, &pk_hdr, &pk_sz,
                       &stg_pk[0], &stg_pk[1], &stg_desc[0], &stg_desc[1], &t_backup, &pk_status, &rec_buf,
                       &tm_D, &tm_P, &tm_base, &tm_status, &tm_dirptrs, &tm_scal, &tm_gap, &tm_tb,
-                      &hb_klo, &hb_khi, &hb_idx, &hot_hit};
+                      &hb_klo, &hb_khi, &hb_idx, &hot_hit,
+                      &sq_st[0], &sq_st[1], &sq_st[2], &sq_st[3], &sq_grp, &sq_runlo, &sq_runst, &sq_off, &sq_len,
+                      &sq_cyc, &sq_keys, &sq_out};
     for (int i = 0; i < 2; ++i) {
       if (desc_pinned[i]) cudaFreeHost(desc_pinned[i]);
       if (desc_done[i]) cudaEventDestroy(desc_done[i]);
@@ -470,6 +472,9 @@ struct Engine {
       throw IsaError(ISA_ERR_INVALID_INPUT, "memory budget above 2^30 groups is not supported");
     if (cfg.preaggregate < 0 || cfg.preaggregate > 2) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown preaggregate mode");
     if (cfg.hot_absorb < 0 || cfg.hot_absorb > 2) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown hot_absorb mode");
+    if (cfg.run_generation != ISA_RUNGEN_RSW && cfg.run_generation != ISA_RUNGEN_RS)
+      throw IsaError(ISA_ERR_INVALID_INPUT, "unknown run generation mode");
+    if (cfg.eviction_chunk < 0) throw IsaError(ISA_ERR_INVALID_INPUT, "eviction chunk must be positive");
     if (cfg.merge_mode < ISA_MERGE_WIDE || cfg.merge_mode > ISA_MERGE_SEPARATE) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown merge mode");
     if (cfg.run_codec < 0 || cfg.run_codec > 2) throw IsaError(ISA_ERR_INVALID_INPUT, "unknown run codec");
     if (cfg.run_tier != ISA_TIER_HOST && cfg.run_tier != ISA_TIER_HBM && cfg.run_tier != ISA_TIER_FILE &&
@@ -559,6 +564,15 @@ struct Engine {
       const int64_t page_bound = pages * (12 + 8 * (int64_t)sch.n_key_cols) + M * 8 * (sch.n_key_cols + S);
       if (cfg.run_tier == ISA_TIER_FILE && page_bound >= (int64_t)0xF0000000ll)
         throw IsaError(ISA_ERR_INVALID_INPUT, "a run of memory_budget groups exceeds 4 GiB of pages; lower memory_budget");
+    }
+    if (cfg.run_generation == ISA_RUNGEN_RS) {
+      if (cfg.merge_mode != ISA_MERGE_WIDE)
+        throw IsaError(ISA_ERR_INVALID_INPUT, "replacement selection is supported with merge_mode 'wide'");
+      if (!seq_supported(KW, S, cfg.memory_budget, true))
+        throw IsaError(ISA_ERR_INVALID_INPUT,
+                       "replacement selection needs a key of <= 64 bits, <= 8 state slots and memory_budget <= 3500");
+      if (cfg.run_tier == ISA_TIER_FILE)
+        throw IsaError(ISA_ERR_INVALID_INPUT, "replacement selection keeps its runs in HBM (no FileStore tier)");
     }
     absorb_row_bytes = key_bits / 8;
     bool used[ISA_MAX_VAL_COLS] = {false};
@@ -2156,6 +2170,95 @@ struct Engine {
     nt.lo.p = nt.hi.p = nt.st.p = nullptr;
   }
 
+  // ------------------------------------------------ one-CTA run generation --
+  // Small budgets (isa_seq.cu): the whole read-sort-write run generation in
+  // one persistent CTA -- a fill cycle of a few thousand rows costs no launch
+  // and no host round trip -- and the only replacement-selection path.
+  DevBuf sq_st[4], sq_grp, sq_runlo, sq_runst, sq_off, sq_len, sq_cyc, sq_keys, sq_out;
+  bool seq_wanted(int64_t n) const {
+    if (cfg.run_generation == ISA_RUNGEN_RS) return true;
+    // read-sort-write: opt-in (ISA_SEQ=1, read per execute): config 1 measured
+    // 33.4 ms one-CTA vs 34.4 ms chunked -- one SM's memory latency per
+    // fill cycle costs what the chunked path spends in launches
+    const char* e = getenv("ISA_SEQ");
+    if (!e || e[0] != '1') return false;
+    return cfg.merge_mode == ISA_MERGE_WIDE && (cfg.run_tier == ISA_TIER_AUTO || cfg.run_tier == ISA_TIER_HBM) &&
+           cfg.chunk_rows_max == 0 && cfg.preaggregate == 0 && cfg.hot_absorb == 0 && n <= ((int64_t)1 << 22) &&
+           cfg.memory_budget <= 4096 && seq_supported(KW, S, cfg.memory_budget, false);
+  }
+  void execute_seq(int64_t n, const void* const* key_cols, const void* const* val_cols, bool on_host) {
+    if (n > ((int64_t)1 << 27))
+      throw IsaError(ISA_ERR_INVALID_INPUT, "replacement selection on the B200 operator takes at most 2^27 rows");
+    const bool rs = cfg.run_generation == ISA_RUNGEN_RS;
+    const u32 M = (u32)cfg.memory_budget;
+    const u32 P = (u32)(cfg.eviction_chunk > 0 ? cfg.eviction_chunk : cfg.page_capacity);
+    const void* kb[ISA_MAX_KEY_COLS];
+    const void* vb[ISA_MAX_VAL_COLS];
+    if (on_host) {
+      Window& w = win[0];
+      CK(cudaStreamSynchronize(h2d));
+      w.staged = false;
+      stage_window(w, key_cols, val_cols, 0, n);
+      CK(cudaStreamWaitEvent(st, w.ready, 0));
+      for (int c = 0; c < sch.n_key_cols; ++c) kb[c] = w.keys[c].p;
+      for (int j = 0; j < sch.n_val_cols; ++j) vb[j] = w.vals[j].p;
+      w.staged = false;
+    } else {
+      for (int c = 0; c < sch.n_key_cols; ++c) kb[c] = key_cols[c];
+      for (int j = 0; j < sch.n_val_cols; ++j) vb[j] = val_cols[j];
+    }
+    const int Sx = std::max(S, 1);
+    for (auto& b : sq_st) b.ensure((size_t)M * Sx * 8 + 64);
+    sq_grp.ensure((size_t)4096 * Sx * 8 + 64);
+    sq_runlo.ensure((size_t)n * 8 + 64);
+    sq_runst.ensure((size_t)n * Sx * 8 + 64);
+    const u32 max_runs = (u32)std::min<int64_t>(rs ? n + 16 : n / std::max<u32>(M, 1) + 16, (int64_t)1 << 24);
+    sq_off.ensure((size_t)max_runs * 4 + 64);
+    sq_len.ensure((size_t)max_runs * 4 + 64);
+    sq_cyc.ensure((size_t)max_runs * 4 + 64);
+    sq_keys.ensure((size_t)M * 8 + 64);
+    sq_out.ensure(256);
+    CK(cudaMemsetAsync(sq_out.p, 0, 256, st));
+    SeqBufs b{sq_st[0].as<u64>(), sq_st[1].as<u64>(), sq_st[2].as<u64>(), sq_st[3].as<u64>(), sq_grp.as<u64>(),
+              sq_runlo.as<u64>(), sq_runst.as<u64>(), sq_off.as<u32>(), sq_len.as<u32>(), sq_cyc.as<u32>(), max_runs,
+              sq_keys.as<u64>(), sq_out.p};
+    ph_begin(ISA_PH_SORT);
+    seq_rungen(rs, kd_at(kb), sd_at(vb), (u32)n, M, P, b, st);
+    ph_end(ISA_PH_SORT, n, 0);
+    struct { u32 nruns, ncycles, windows, epochs, cur_n, cur_buf, overflow, pad; u64 probes, absorbs, ressum; } o;
+    CK(cudaMemcpyAsync(&o, sq_out.p, sizeof(o), cudaMemcpyDeviceToHost, st));
+    sync();
+    if (o.overflow) throw IsaError(ISA_ERR_RESOURCE, "run directory of the one-CTA run generation overflowed");
+    std::vector<u32> off(o.nruns), len(o.nruns), cyc(o.ncycles);
+    if (o.nruns) {
+      CK(cudaMemcpyAsync(off.data(), sq_off.p, 4 * (size_t)o.nruns, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(len.data(), sq_len.p, 4 * (size_t)o.nruns, cudaMemcpyDeviceToHost, st));
+    }
+    if (o.ncycles) CK(cudaMemcpyAsync(cyc.data(), sq_cyc.p, 4 * (size_t)o.ncycles, cudaMemcpyDeviceToHost, st));
+    sync();
+    for (u32 r = 0; r < o.nruns; ++r) {
+      Run rr;
+      rr.host = false;
+      rr.rows = len[r];
+      rr.lo = sq_runlo.as<u64>() + off[r];
+      rr.hi = nullptr;
+      rr.st = S ? sq_runst.as<u64>() + (size_t)off[r] * S : nullptr;
+      runs.push_back(rr);
+      account_written(rr);
+    }
+    for (u32 c = 0; c < o.ncycles; ++c) cycles.push_back(cyc[c]);
+    led.chunks += o.epochs;
+    led.steady_probes = (int64_t)o.probes;
+    led.steady_absorbs = (int64_t)o.absorbs;
+    led.steady_resident_sum = (int64_t)o.ressum;
+    if (o.nruns == 0 && o.cur_n) {   // no spill: the index is the result
+      T.reserve(std::max<size_t>(tcap, o.cur_n + 1), KW, S);
+      CK(cudaMemcpyAsync(T.plo(), sq_keys.p, (size_t)o.cur_n * 8, cudaMemcpyDeviceToDevice, st));
+      if (S) CK(cudaMemcpyAsync(T.pst(), sq_st[o.cur_buf].p, (size_t)o.cur_n * 8 * S, cudaMemcpyDeviceToDevice, st));
+      T.n = o.cur_n;
+    }
+  }
+
   // ------------------------------------------------------------ execute --
   int64_t execute(int64_t n, const void* const* key_cols, const void* const* val_cols, bool on_host,
                   cudaStream_t stream) {
@@ -2222,11 +2325,13 @@ struct Engine {
     cudaEvent_t rg0 = ev_get(), rg1 = ev_get(), wm1 = ev_get();
     CK(cudaEventRecord(rg0, st));
 
+    const bool seq = seq_wanted(n);
+    if (seq) execute_seq(n, key_cols, val_cols, on_host);
     int64_t wrows = on_host ? (cfg.window_rows > 0 ? cfg.window_rows : ((int64_t)32 << 20)) : n;
-    int64_t a = 0, cycle_start = 0, last_len = 0, last_cycle = 0;
+    int64_t a = seq ? n : 0, cycle_start = 0, last_len = 0, last_cycle = 0;
     bool last_flushed = false;
     int wi = 0;
-    if (on_host) stage_window(win[0], key_cols, val_cols, 0, std::min(n, wrows));
+    if (on_host && !seq) stage_window(win[0], key_cols, val_cols, 0, std::min(n, wrows));
     while (a < n) {
       const void* kb[ISA_MAX_KEY_COLS];
       const void* vb[ISA_MAX_VAL_COLS];
@@ -2297,7 +2402,7 @@ struct Engine {
     // with host-tier runs it stays where it is (HBM): the wide merge reads it
     // next, so a PCIe round trip would buy nothing (the ledger counts it as
     // written like every run)
-    if (!runs.empty()) {
+    if (!runs.empty() && !seq) {
       if ((cfg.run_tier == ISA_TIER_HOST || cfg.run_tier == ISA_TIER_AUTO) && T.n > 0) {
         Run r;
         r.dir = make_dir();

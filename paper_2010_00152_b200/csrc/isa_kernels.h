@@ -152,6 +152,22 @@ void hot_probe(int KW, const KeyDesc& kd, int64_t row0, u32 n, const HotHash& h,
 // states of rows row0 + i (i < n) with hit[i] != ~0 combined into t_st[hit[i]]
 void hot_absorb(const SlotDesc& sd, int64_t row0, u32 n, const u32* hit, u64* t_st, int num_sms, cudaStream_t st);
 
+// ---- small-budget run generation in one persistent CTA (isa_seq.cu) -------
+#define SQ_MAX_M 4096
+struct SeqBufs {
+  u64 *st_a0, *st_a1, *st_b0, *st_b1;   // group states: current generation (ping-pong), next generation
+  u64* grp_tmp;                         // window groups' states (4096 x S)
+  u64 *run_lo, *run_st;                 // runs back to back (capacity: the input rows)
+  u32 *run_off, *run_len, *cycles;
+  u32 max_runs;
+  u64* cur_keys;                        // no spill: the index keys (the result)
+  void* out;                            // SeqOut counters (64 bytes)
+};
+bool seq_supported(int KW, int S, int64_t M, bool rs);
+// read-sort-write (rs = false) or replacement selection with eviction chunk P
+void seq_rungen(bool rs, const KeyDesc& kd, const SlotDesc& sd, u32 n, u32 M, u32 P, const SeqBufs& b,
+                cudaStream_t st);
+
 // ---- runs / wide merge helpers ------------------------------------------
 // out[r * nb + b] = lower_bound(run r, bound b); run keys may be mapped host memory
 // A run for the wide merge's slice search: raw key words (lo/hi), or a

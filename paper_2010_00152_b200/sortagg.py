@@ -406,10 +406,9 @@ class SortAggregate:
         if isinstance(store, FileStore):
             if config.merge_mode != WIDE:
                 raise InvalidInputError("the FileStore run tier supports merge_mode 'wide'")
-        if config.run_generation_mode != READ_SORT_WRITE:
-            raise InvalidInputError(
-                f"run_generation_mode {config.run_generation_mode!r} is not supported by the "
-                "B200 operator (read-sort-write only)")
+        if config.run_generation_mode == REPLACEMENT_SELECTION and config.merge_mode != WIDE:
+            raise InvalidInputError("replacement selection is supported with merge_mode 'wide' "
+                                    "(the traditional modes' tagged-run priority queue is not ported)")
         if any(c.kind != "int64" for c in schema.key_columns):
             raise InvalidInputError("utf8 key columns are not supported by the B200 operator")
         self.schema = schema
@@ -458,6 +457,8 @@ class SortAggregate:
         cfg.output_size_hint = self.config.output_size_hint if self.config.output_size_hint is not None else 0
         cfg.run_codec = {"auto": 0, "raw": 1, "packed": 2}[self.config.run_codec]
         cfg.hot_absorb = {"auto": 0, "always": 1, "never": 2}[self.config.hot_absorb]
+        cfg.run_generation = 1 if self.config.run_generation_mode == REPLACEMENT_SELECTION else 0
+        cfg.eviction_chunk = self.config.eviction_chunk or 0
         sch = _native.IsaSchema()
         if len(key_codes) > _native.MAX_KEY_COLS:
             raise InvalidInputError("too many key columns")
@@ -689,6 +690,10 @@ class SortAggregate:
                 est = OutputEstimator(self.config.memory_budget)
                 for c in cycles:
                     est.note_cycle(c)
+                # replacement selection: the steady-state probe totals (sortagg.py:335-336)
+                est.steady_probes = int(led.steady_probes)
+                est.steady_absorbs = int(led.steady_absorbs)
+                est.steady_resident_sum = int(led.steady_resident_sum)
                 est.note_runs(run_rows)
                 o_est = (self.config.output_size_hint if self.config.output_size_hint is not None
                          else est.estimate(n_rows))

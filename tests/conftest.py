@@ -21,9 +21,16 @@ def pytest_configure(config):
 
 def golden_names():
     """End-to-end operator fixtures (pages_* hold reference run files,
-    downstream_* the reference's sorted-output consumers)."""
+    downstream_* the reference's sorted-output consumers, rs_* replacement
+    selection)."""
     names = (os.path.splitext(os.path.basename(p))[0] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz")))
-    return sorted(n for n in names if not n.startswith(("pages_", "downstream_")))
+    return sorted(n for n in names if not n.startswith(("pages_", "downstream_", "rs_")))
+
+
+def rs_golden_names():
+    """Replacement-selection fixtures (tools/make_golden_rs.py)."""
+    names = (os.path.splitext(os.path.basename(p))[0] for p in glob.glob(os.path.join(GOLDEN_DIR, "rs_*.npz")))
+    return sorted(names)
 
 
 class Golden:

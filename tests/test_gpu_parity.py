@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import oracle
-from conftest import Golden, assert_slots_equal, golden_names
+from conftest import Golden, assert_slots_equal, golden_names, rs_golden_names
 
 pytestmark = pytest.mark.gpu
 
@@ -41,11 +41,13 @@ def _cfg(memory, page, **kw):
 
 @pytest.mark.parametrize("name", golden_names())
 @pytest.mark.parametrize("variant", ["device", "host_input", "hbm_runs", "packed_runs", "host_runs", "small_chunks",
-                                     "k1_always", "k1_never", "tile_merge", "radix_merge"])
+                                     "k1_always", "k1_never", "tile_merge", "radix_merge", "one_cta"])
 def test_golden_columns(name, variant, monkeypatch):
     g = Golden(name)
     if variant in ("tile_merge", "radix_merge"):   # force either wide-merge path
         monkeypatch.setenv("ISA_TILE_MERGE", "1" if variant == "tile_merge" else "0")
+    if variant == "one_cta":   # small budgets: the one-CTA read-sort-write run generation (isa_seq.cu)
+        monkeypatch.setenv("ISA_SEQ", "1")
     sch = g.schema()
     kw = {}
     if variant == "hbm_runs":
@@ -62,7 +64,7 @@ def test_golden_columns(name, variant, monkeypatch):
         kw.update(preaggregate="never")
     mode = str(g.z["merge_mode"]) if "merge_mode" in g.z else "wide"
     if mode != "wide" and variant in ("k1_always", "k1_never", "small_chunks", "packed_runs", "host_runs",
-                                      "tile_merge", "radix_merge"):
+                                      "tile_merge", "radix_merge", "one_cta"):
         pytest.skip("pre-aggregation / chunking knobs apply to the wide path only")
     op = isa.SortAggregate(sch, _cfg(g.memory, g.page, merge_mode=mode, **kw))
     n = len(g.keys[0])
@@ -617,3 +619,59 @@ def test_hybrid_sort_vs_oracle(cfg, rows, memory, cap, monkeypatch):
     kw = {"domain": 1 << 24} if cfg in (3, 5) else {}
     w = workloads.make(cfg, rows=rows, device="cpu", **kw)
     _oracle_case(w, memory, page=100, rel=1e-5 if cfg == 3 else 1e-9)
+
+
+
+@pytest.mark.parametrize("on_host", [False, True])
+@pytest.mark.parametrize("name", rs_golden_names())
+def test_replacement_selection_golden(name, on_host):
+    """Replacement selection (one persistent CTA, isa_seq.cu) against the
+    reference's own output, run sizes, steady-probe totals and merge plan
+    (tools/make_golden_rs.py)."""
+    g = Golden(name)
+    chunk = int(g.z["eviction_chunk"]) or None
+    cfg = _cfg(g.memory, g.page, run_generation_mode=isa.REPLACEMENT_SELECTION, eviction_chunk=chunk)
+    op = isa.SortAggregate(g.schema(), cfg)
+    if on_host:
+        keys = [torch.from_numpy(np.ascontiguousarray(k)).pin_memory() for k in g.keys]
+        vals = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in g.values.items()}
+    else:
+        keys = [_cuda(k) for k in g.keys]
+        vals = {k: _cuda(v) for k, v in g.values.items()}
+    _check(op.execute_columns(keys, vals), g.out_keys, g.out_slots)
+    assert op.run_rows == g.z["run_rows"].tolist()
+    assert op.cycles == []
+    d = op.device_ledger
+    assert [d["steady_probes"], d["steady_absorbs"], d["steady_resident_sum"]] == g.z["steady"].tolist()
+    assert op.ledger.rows_spilled == int(g.z["run_rows"].sum())
+    if len(g.z["run_rows"]):
+        assert [st.kind for st in op.initial_plan.steps] == g.z["plan_kinds"].tolist()
+    op.ledger.check_invariants()
+
+
+@pytest.mark.parametrize("rows,memory,chunk", [(50_000, 700, 33), (80_000, 2048, 100), (30_000, 64, 1)])
+def test_replacement_selection_vs_restatement(rows, memory, chunk):
+    """Larger random cases: run sizes and steady totals equal the Python
+    restatement's, output equals the numpy oracle's."""
+    w = workloads.make(3, rows=rows, device="cpu", domain=1 << 14)
+    op = _oracle_case(w, memory, page=max(2, min(100, memory // 2)), rel=1e-5,
+                      run_generation_mode=isa.REPLACEMENT_SELECTION, eviction_chunk=chunk)
+    keys = oracle.normalize_keys([k.numpy() for k in w.keys])[1].tolist()
+    runs, steady = oracle.rs_run_generation(keys, memory, chunk)
+    assert op.run_rows == runs
+    d = op.device_ledger
+    assert [d["steady_probes"], d["steady_absorbs"], d["steady_resident_sum"]] == list(steady)
+
+
+def test_config1_one_cta_run_generation_ledger(monkeypatch):
+    """BASELINE config 1 (1e6 rows, M = 4096) through the one-CTA run
+    generation: fill cycles and run sizes equal the C oracle's."""
+    monkeypatch.setenv("ISA_SEQ", "1")
+    w = workloads.config1(device="cpu")
+    keys_np = [k.numpy() for k in w.keys]
+    slots = oracle.make_states(w.schema, {k: v.numpy() for k, v in w.values.items()}, w.rows)
+    _, _, led, cycles = oracle.rsw_sortagg(keys_np, slots, oracle.slot_ops(w.schema), 4096, 100)
+    op = _oracle_case(w, 4096, page=100)
+    assert op.cycles == [c for c in cycles if c > 0]
+    assert op.ledger.rows_spilled == led["rows_spilled"] and op.runs_after_generation == led["runs"]
+    assert op.device_ledger["kernel_launches"] < 200   # no per-cycle launches

@@ -126,8 +126,9 @@ def test_compare_rows_and_ledger():
 
 def test_operator_rejects_out_of_scope_modes():
     sch = isa.Schema([isa.ColumnSpec("k")], [isa.AggregateSpec("n", isa.AggregateKind.COUNT)])
-    with pytest.raises(isa.InvalidInputError, match="run_generation_mode"):
-        isa.SortAggregate(sch, cfg(64, 8, run_generation_mode=isa.REPLACEMENT_SELECTION))
+    with pytest.raises(isa.InvalidInputError, match="replacement selection"):
+        isa.SortAggregate(sch, cfg(64, 8, run_generation_mode=isa.REPLACEMENT_SELECTION, merge_mode="traditional"))
+    isa.SortAggregate(sch, cfg(64, 8, run_generation_mode=isa.REPLACEMENT_SELECTION))   # wide: accepted
     with pytest.raises(isa.InvalidInputError, match="FileStore"):
         isa.SortAggregate(sch, cfg(64, 8, merge_mode="traditional"), isa.FileStore("/tmp/isa_fs_x"))
     isa.SortAggregate(sch, cfg(64, 8), isa.FileStore("/tmp/isa_fs_x"))   # wide: accepted

@@ -121,3 +121,17 @@ def test_page_parser_on_reference_run_files(name):
     # run rows are a subset of the groups (the final residue is the last run): every run key is an output key
     out_keys = set(zip(*[z[f"out_k{j}"].astype(np.int64).tolist() for j in range(arity)]))
     assert set(zip(*[k.tolist() for k in want_k])) <= out_keys
+
+
+@pytest.mark.parametrize("name", __import__("conftest").rs_golden_names())
+def test_rs_oracle_matches_reference(name):
+    """The replacement-selection restatement reproduces the reference's run
+    sizes and steady-probe totals on every rs_* fixture, and the numpy
+    oracle its output."""
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", name + ".npz"))
+    keys = z["in_k0"].astype(np.int64).tolist()
+    chunk = int(z["eviction_chunk"]) or int(z["page_capacity"])
+    runs, steady = oracle.rs_run_generation(keys, int(z["memory_budget"]), chunk)
+    assert runs == z["run_rows"].tolist()
+    assert list(steady) == z["steady"].tolist()
+    assert sorted(set(keys)) == z["out_k0"].tolist()
