@@ -1129,6 +1129,159 @@ __global__ void k_head_flags(const u64* __restrict__ lo, const u64* __restrict__
   }
 }
 
+// ---- collapse with block head counts (default): per 128-thread block of
+// the segmented reduce, the included heads are counted (keys + row ids read
+// once), the block counts scanned (one tiny kernel), and the reduce kernel
+// numbers its groups itself (block base + in-block prefix) -- instead of a
+// per-row head-flag array, a 3-kernel scan over it and a per-row read of the
+// scanned positions.
+#define CB_THREADS 128
+template <int KW, int MS>
+__global__ void __launch_bounds__(CB_THREADS) k_cl_count(const u64* __restrict__ lo, const u64* __restrict__ hi,
+                                                         const u32* __restrict__ val, u32 m, u32 limit,
+                                                         u32* __restrict__ counts) {
+  constexpr u32 CLI = (u32)cl_items(MS);
+  const u32 t = blockIdx.x * CB_THREADS + threadIdx.x;
+  const u32 i0 = t * CLI, i1 = min(i0 + CLI, m);
+  u32 c = 0;
+  if (i0 < m) {
+    u64 pl = i0 > 0 ? lo[i0 - 1] : 0, ph = (KW == 2 && i0 > 0) ? hi[i0 - 1] : 0;
+    for (u32 i = i0; i < i1; ++i) {
+      const u64 l = lo[i], h = KW == 2 ? hi[i] : 0;
+      c += (val[i] < limit && (i == 0 || !key_eq<KW>(h, l, ph, pl))) ? 1u : 0u;
+      pl = l; ph = h;
+    }
+  }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  __shared__ u32 ws[CB_THREADS / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u32 tot = 0;
+    for (int q = 0; q < CB_THREADS / 32; ++q) tot += ws[q];
+    counts[blockIdx.x] = tot;
+  }
+}
+
+// exclusive scan of nb block counts in one CTA (1024 threads, sequential per
+// thread chunk); *total = sum
+__global__ void __launch_bounds__(1024) k_cl_scan(u32* __restrict__ counts, u32 nb, u32* __restrict__ total) {
+  __shared__ u32 ws[32];
+  const u32 per = (nb + 1023) / 1024;
+  const u32 b0 = min(nb, threadIdx.x * per), b1 = min(nb, b0 + per);
+  u32 s = 0;
+  for (u32 b = b0; b < b1; ++b) s += counts[b];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  u32 x = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    u32 v = ws[lane];
+    u32 y = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 z = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += z;
+    }
+    ws[lane] = y - v;
+    if (lane == 31) *total = y;
+  }
+  __syncthreads();
+  u32 run = ws[w] + x - s;
+  for (u32 b = b0; b < b1; ++b) {
+    const u32 c = counts[b];
+    counts[b] = run;
+    run += c;
+  }
+}
+
+template <int KW, int MS>
+__global__ void __launch_bounds__(CB_THREADS) k_seg_reduce_b(const u64* __restrict__ lo, const u64* __restrict__ hi,
+                                                             const u32* __restrict__ val, u32 m, u32 limit, SlotDesc sd,
+                                                             i64 row0, const u64* __restrict__ st_in,
+                                                             const u32* __restrict__ bbase, u64* __restrict__ out_lo,
+                                                             u64* __restrict__ out_hi, u64* __restrict__ out_st,
+                                                             u64* __restrict__ partial, u32* __restrict__ partial_slot) {
+  const int S = sd.nslots;
+  constexpr u32 CLI = (u32)cl_items(MS);
+  const u32 t = blockIdx.x * CB_THREADS + threadIdx.x;
+  const u32 i0 = t * CLI, i1 = min(i0 + CLI, m);
+  // this thread's included heads -> its first group index (block scan)
+  u32 c = 0;
+  if (i0 < m) {
+    u64 pl = i0 > 0 ? lo[i0 - 1] : 0, ph = (KW == 2 && i0 > 0) ? hi[i0 - 1] : 0;
+    for (u32 i = i0; i < i1; ++i) {
+      const u64 l = lo[i], h = KW == 2 ? hi[i] : 0;
+      c += (val[i] < limit && (i == 0 || !key_eq<KW>(h, l, ph, pl))) ? 1u : 0u;
+      pl = l; ph = h;
+    }
+  }
+  __shared__ u32 ws[CB_THREADS / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  u32 x = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[w] = x;
+  __syncthreads();
+  u32 wpre = 0;
+  for (int q = 0; q < w; ++q) wpre += ws[q];
+  u32 hp = bbase[blockIdx.x] + wpre + x - c;   // group index of this thread's first head
+  if (i0 >= m) return;
+  u64 acc[MS];
+  u64 cur[MS];
+#pragma unroll
+  for (int k = 0; k < MS; ++k) acc[k] = cur[k] = 0;
+  bool have = false, lead = true;
+  u32 slot = 0;
+  u64 prev_lo = 0, prev_hi = 0;
+  if (i0 > 0) { prev_lo = lo[i0 - 1]; prev_hi = KW == 2 ? hi[i0 - 1] : 0; }
+  partial_slot[t] = 0xFFFFFFFFu;
+  const u32 lead_slot = hp - 1;
+  auto flush = [&]() {
+    if (lead) {
+#pragma unroll
+      for (int k = 0; k < MS; ++k)
+        if (k < S) partial[(size_t)t * S + k] = acc[k];
+      partial_slot[t] = lead_slot;
+    } else {
+#pragma unroll
+      for (int k = 0; k < MS; ++k)
+        if (k < S) out_st[(size_t)slot * S + k] = acc[k];
+    }
+  };
+  for (u32 i = i0; i < i1; ++i) {
+    u64 l = lo[i], h = KW == 2 ? hi[i] : 0;
+    u32 v = val[i];
+    bool head = (i == 0) || !key_eq<KW>(h, l, prev_hi, prev_lo);
+    prev_lo = l; prev_hi = h;
+    if (v >= limit) continue;
+    if (S) load_state_row<MS>(sd, row0, st_in, v, cur);
+    if (head) {
+      if (have) flush();
+      have = true; lead = false;
+      slot = hp++;
+      out_lo[slot] = l;
+      if (KW == 2) out_hi[slot] = h;
+#pragma unroll
+      for (int k = 0; k < MS; ++k) acc[k] = cur[k];
+    } else if (!have) {
+      have = true;
+#pragma unroll
+      for (int k = 0; k < MS; ++k) acc[k] = cur[k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < MS; ++k)
+        if (k < S) acc[k] = combine_slot(sd.op[k], sd.type[k], acc[k], cur[k]);
+    }
+  }
+  if (have) flush();
+}
+
 template <int KW, int MS>
 __global__ void k_seg_reduce(const u64* __restrict__ lo, const u64* __restrict__ hi, const u32* __restrict__ val,
                              u32 m, u32 limit, SlotDesc sd, i64 row0, const u64* __restrict__ st_in,
@@ -1550,13 +1703,32 @@ void collapse(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, u32 l
 #undef CF_LAUNCH
     return;
   }
+  u32 nthreads = collapse_threads(m, sd.nslots);
+  int blocks = (nthreads + 127) / 128;
+  const int S = sd.nslots;
+  // block head counts (default; config 5 collapse 35 -> 29 ms, window collapse
+  // 28 -> 22 ms per 1e9 rows, profiles/r2_ab_collapse.txt); ISA_COLLAPSE=rowflags:
+  // per-row head flags + full scan (round-1 path)
+  static int cb_env = -1;
+  if (cb_env < 0) { const char* e = getenv("ISA_COLLAPSE"); cb_env = (e && e[0] == 'r') ? 0 : 1; }
+  if (cb_env && (u32)blocks <= 1024u * 1024u) {
+    // block head counts -> one-CTA scan -> reduce numbering its own groups
+#define CB_CNT(K, M) klaunch(k_cl_count<K, M>, blocks, CB_THREADS, 0, st, lo, hi, val, m, limit, tmp.flags)
+#define CB_RED(K, M) klaunch(k_seg_reduce_b<K, M>, blocks, CB_THREADS, 0, st, lo, hi, val, m, limit, sd, (i64)row0, \
+                             st_in, (const u32*)tmp.flags, out_lo, out_hi, out_st, tmp.partial, tmp.partial_slot)
+#define CB_KW(K, X) { if (S <= 1) X(K, 1); else if (S <= 2) X(K, 2); else if (S <= 4) X(K, 4); \
+                      else if (S <= 5) X(K, 5); else if (S <= 8) X(K, 8); else X(K, 16); }
+    if (KW == 2) CB_KW(2, CB_CNT) else CB_KW(1, CB_CNT)
+    klaunch(k_cl_scan, 1, 1024, 0, st, tmp.flags, (u32)blocks, tmp.total);
+    if (KW == 2) CB_KW(2, CB_RED) else CB_KW(1, CB_RED)
+#undef CB_KW
+#undef CB_RED
+#undef CB_CNT
+  } else {
   int g = grid_for(m, 256);
   if (KW == 2) klaunch(k_head_flags<2>, g, 256, 0, st, lo, hi, val, m, limit, tmp.flags);
   else klaunch(k_head_flags<1>, g, 256, 0, st, lo, hi, val, m, limit, tmp.flags);
   scan_exclusive_u32(tmp.flags, m, tmp.scan_tmp, tmp.total, st);
-  u32 nthreads = collapse_threads(m, sd.nslots);
-  int blocks = (nthreads + 127) / 128;
-  const int S = sd.nslots;
 #define SR_LAUNCH(K, M) klaunch(k_seg_reduce<K, M>, blocks, 128, 0, st, lo, hi, val, m, limit, sd, row0, st_in, \
                                 tmp.flags, out_lo, out_hi, out_st, tmp.partial, tmp.partial_slot)
 #define SR_KW(K) { if (S <= 1) SR_LAUNCH(K, 1); else if (S <= 2) SR_LAUNCH(K, 2); else if (S <= 4) SR_LAUNCH(K, 4); \
@@ -1564,6 +1736,7 @@ void collapse(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, u32 l
   if (KW == 2) SR_KW(2) else SR_KW(1)
 #undef SR_KW
 #undef SR_LAUNCH
+  }
   if (S) {
     const int g = grid_for(nthreads, 256);
     if (S <= 2) klaunch(k_seg_fixup<2>, g, 256, 0, st, nthreads, sd, tmp.partial, tmp.partial_slot, out_st);
