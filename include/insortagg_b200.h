@@ -220,6 +220,13 @@ ISA_API int isa_execute(isa_handle* h, int64_t n_rows, const void* const* key_co
 ISA_API int isa_in_stream_aggregate(isa_handle* h, int64_t n_rows, const void* const* key_cols,
                                     const void* const* val_cols, int32_t input_on_host, void* stream,
                                     int64_t* n_groups_out);
+/* HashAggregate.execute (hashagg.py:73-198), the hash-aggregation baseline:
+ * same inputs as isa_execute; every group in one HBM hash table (no
+ * partitioning: the device holds the output), groups in first-arrival order
+ * (the reference's in-memory table order); read with isa_result_copy. */
+ISA_API int isa_hash_aggregate(isa_handle* h, int64_t n_rows, const void* const* key_cols,
+                               const void* const* val_cols, int32_t input_on_host, void* stream,
+                               int64_t* n_groups_out);
 /* bench.merge_intersect (bench.py:536-550): the keys present in both
  * strictly ascending key-column inputs (e.g. two SortAggregate outputs),
  * written to out_keys (device memory, or host memory with on_host = 1);

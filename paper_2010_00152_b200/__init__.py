@@ -41,6 +41,7 @@ from .sortagg import (
     SortAggregate,
     plan_merge,
 )
+from .hashagg import HashAggConfig, HashAggregate
 
 __all__ = [
     "AggregateKind", "AggregateSpec", "ColumnSpec", "INT64", "UTF8",
@@ -49,7 +50,7 @@ __all__ = [
     "CorruptionError", "ResourceError", "PlanningError",
     "FileStore", "MemoryStore",
     "SortAggConfig", "SortAggregate", "ColumnarResult", "OutputEstimator",
-    "PlanStep", "MergePlan", "plan_merge",
+    "PlanStep", "MergePlan", "plan_merge", "HashAggConfig", "HashAggregate",
     "WIDE", "TRADITIONAL", "SEPARATE", "READ_SORT_WRITE", "REPLACEMENT_SELECTION",
 ]
 

@@ -48,7 +48,7 @@ EXPORTED_SYMBOLS = (
     "isa_version", "isa_create", "isa_destroy", "isa_execute", "isa_result_copy",
     "isa_metrics", "isa_cycles", "isa_run_rows", "isa_last_error",
     "isa_sample_keys", "isa_partition", "isa_phase_stats", "isa_launch_count", "isa_steps",
-    "isa_set_spill_dir", "isa_in_stream_aggregate", "isa_merge_intersect", "isa_partition_counts",
+    "isa_set_spill_dir", "isa_in_stream_aggregate", "isa_hash_aggregate", "isa_merge_intersect", "isa_partition_counts",
     "isa_scatter_to_peers", "isa_ipc_handle", "isa_ipc_open", "isa_ipc_close",
     "isa_set_kernel_timing", "isa_kernel_stats",
 )
@@ -168,6 +168,8 @@ def load():
     lib.isa_result_copy.argtypes = [vp, pp, pp, ctypes.c_int32, vp]
     lib.isa_in_stream_aggregate.restype = ctypes.c_int
     lib.isa_in_stream_aggregate.argtypes = [vp, ctypes.c_int64, pp, pp, ctypes.c_int32, vp, i64p]
+    lib.isa_hash_aggregate.restype = ctypes.c_int
+    lib.isa_hash_aggregate.argtypes = [vp, ctypes.c_int64, pp, pp, ctypes.c_int32, vp, i64p]
     lib.isa_merge_intersect.restype = ctypes.c_int
     lib.isa_merge_intersect.argtypes = [vp, ctypes.c_int64, pp, ctypes.c_int64, pp, pp, ctypes.c_int32, vp, i64p]
     lib.isa_partition_counts.restype = ctypes.c_int
@@ -281,6 +283,12 @@ class Handle:
         out = ctypes.c_int64(0)
         self._check(self._lib.isa_in_stream_aggregate(self._h, n_rows, _ptr_array(key_ptrs), _ptr_array(val_ptrs),
                                                       1 if on_host else 0, stream, ctypes.byref(out)))
+        return out.value
+
+    def hash_aggregate(self, n_rows, key_ptrs, val_ptrs, on_host, stream):
+        out = ctypes.c_int64(0)
+        self._check(self._lib.isa_hash_aggregate(self._h, n_rows, _ptr_array(key_ptrs), _ptr_array(val_ptrs),
+                                                 1 if on_host else 0, stream, ctypes.byref(out)))
         return out.value
 
     def merge_intersect(self, n_a, a_ptrs, n_b, b_ptrs, out_ptrs, on_host, stream):

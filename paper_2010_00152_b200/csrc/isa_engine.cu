@@ -426,7 +426,7 @@ struct Engine {
                       &tm_D, &tm_P, &tm_base, &tm_status, &tm_dirptrs, &tm_scal, &tm_gap, &tm_tb,
                       &hb_klo, &hb_khi, &hb_idx, &hot_hit,
                       &sq_st[0], &sq_st[1], &sq_st[2], &sq_st[3], &sq_grp, &sq_runlo, &sq_runst, &sq_off, &sq_len,
-                      &sq_cyc, &sq_keys, &sq_out};
+                      &sq_cyc, &sq_keys, &sq_out, &ha_lo, &ha_hi, &ha_st, &ha_occ, &ha_first, &ha_slot};
     for (int i = 0; i < 2; ++i) {
       if (desc_pinned[i]) cudaFreeHost(desc_pinned[i]);
       if (desc_done[i]) cudaEventDestroy(desc_done[i]);
@@ -910,6 +910,24 @@ struct Engine {
   }
   static constexpr u32 kPackMinRows = 1u << 15;
 
+  // Auto tier: keep a run raw in HBM (no pack / unpack) when it fits next to
+  // the estimated packed size of everything still to spill (at most the input
+  // rows not yet read, at the packed/raw ratio measured on earlier runs); the
+  // first run is packed to learn the ratio.
+  int64_t rows_left = 0;              // input rows not yet consumed (updated per chunk)
+  double packed_ratio = -1;           // packed / raw bytes of the last packed run
+  // Opt-in (ISA_RAW_RUNS=1): measured config 5 at 1e9 rows 189 -> 192 ms (no
+  // pack, but the wide merge's D2D slice copies of raw runs cost more than
+  // unpacking) and out of memory at 4e9 rows (the result's growth no longer fits).
+  bool raw_fits_hbm(u32 rows) const {
+    static int env = -1;
+    if (env < 0) { const char* e = getenv("ISA_RAW_RUNS"); env = e && e[0] == '1' ? 1 : 0; }
+    if (!env || cfg.run_tier != ISA_TIER_AUTO || packed_ratio < 0) return false;
+    const double row_b = 8.0 * (KW + S);
+    const double need = (double)rows * row_b + (double)rows_left * row_b * packed_ratio;
+    return need <= (double)hbm_left;
+  }
+
   // T packed on the GPU (isa_codec.cu), then the packed bytes cross PCIe.
   // One host synchronization learns the packed size.
   Run spill_packed(Table& t) {
@@ -943,6 +961,7 @@ struct Engine {
       kt_end(KF_PACK, (int64_t)t.n * 8 * ncol * 2, st);
     }
     kt_add_bytes(KF_PACK, bytes);
+    packed_ratio = (double)bytes / std::max(1.0, (double)t.n * 8.0 * (KW + S));
     // packed blocks, then the block offsets: both owned by the table until
     // its D2H copies are done (pk_sz is reused by the next spill)
     CK(cudaMemcpyAsync(t.pk.as<char>() + off_at, pk_sz.p, (size_t)(nblk + 1) * 4, cudaMemcpyDeviceToDevice, st));
@@ -1110,7 +1129,7 @@ struct Engine {
       return;
     }
     u32* dir = make_dir();
-    if (pack_runs(T.n)) {
+    if (pack_runs(T.n) && !raw_fits_hbm(T.n)) {
       Run r = spill_packed(T);
       r.dir = dir;
       if (!r.host) {   // stream-ordered D2D copy: T's buffers are reusable right away
@@ -2285,6 +2304,8 @@ struct Engine {
     led.rows_seen = n;
     if (n == 0) { led.kernel_launches = 0; return 0; }
     dev_packed = false;
+    packed_ratio = -1;
+    rows_left = n;
     tm_mode = tile_merge_env();
     hbm_left = 0;
     bk_ready = false;
@@ -2381,6 +2402,7 @@ struct Engine {
       }
       int64_t len = chunk_len(std::min(n, wend) - a, last_len, last_flushed, last_cycle, a - cycle_start);
       int64_t b = a + len;
+      rows_left = n - a;
       int64_t nxt = process_chunk(kd, sd, base, a, b);
       last_flushed = nxt < b;
       if (last_flushed) {
@@ -2539,6 +2561,74 @@ struct Engine {
     led.n_groups = result.n;
     ph_collect();
     return result.n;
+  }
+
+  // HashAggregate baseline (hashagg.py:73-198): one hash table of every
+  // group in HBM, rows -> slots, states absorbed (k_hot_absorb), groups in
+  // first-arrival order (the reference's in-memory table order).  The
+  // result is read with isa_result_copy.
+  DevBuf ha_lo, ha_hi, ha_st, ha_occ, ha_first, ha_slot;
+  int64_t hash_aggregate(int64_t n, const void* const* key_cols, const void* const* val_cols, bool on_host,
+                         cudaStream_t stream) {
+    CK(cudaSetDevice(dev));
+    st = stream;
+    memset(&led, 0, sizeof(led));
+    memset(phases, 0, sizeof(phases));
+    runs.clear();
+    cycles.clear();
+    steps.clear();
+    result.n = 0;
+    if (n < 0) throw IsaError(ISA_ERR_INVALID_INPUT, "negative row count");
+    if (n > ((int64_t)1 << 30)) throw IsaError(ISA_ERR_INVALID_INPUT, "hash aggregation of more than 2^30 rows");
+    led.rows_seen = n;
+    if (n == 0) return 0;
+    std::vector<const void*> kb, vb;
+    if (on_host) to_device_cols(n, key_cols, val_cols, sch.n_val_cols, kb, vb);
+    const KeyDesc kd = kd_at(on_host ? kb.data() : key_cols);
+    const SlotDesc sd = sd_at(on_host ? vb.data() : val_cols);
+    u32 cap = 1024;
+    while ((int64_t)cap < 2 * n) cap <<= 1;
+    ha_lo.ensure((size_t)cap * 8);
+    if (KW == 2) ha_hi.ensure((size_t)cap * 8);
+    if (S) ha_st.ensure((size_t)cap * 8 * S);
+    ha_occ.ensure((size_t)cap * 4);
+    ha_first.ensure((size_t)cap * 4);
+    ha_slot.ensure((size_t)n * 4 + 64);
+    HashAggTable t{ha_lo.as<u64>(), ha_hi.as<u64>(), ha_st.as<u64>(), ha_occ.as<u32>(), ha_first.as<u32>(), cap - 1,
+                   dscal32(23)};
+    ph_begin(ISA_PH_HOT);
+    ha_insert(KW, kd, (u32)n, t, ha_slot.as<u32>(), st);
+    ha_init_states(t, sd, st);
+    hot_absorb(sd, 0, (u32)n, ha_slot.as<u32>(), t.st, num_sms, st);
+    cl_flags.ensure(((size_t)cap + 1) * 4);
+    scan_tmp.ensure((scan_tmp_words(cap + 1) + 64) * 4);
+    ha_flags(t, cl_flags.as<u32>(), st);
+    scan_exclusive_u32(cl_flags.as<u32>(), cap, scan_tmp.as<u32>(), dscal32(24), st);
+    ph_end(ISA_PH_HOT, n, 0);
+    const u32 g = read_u32(dscal32(24));
+    ensure_sort(g);
+    ha_compact(t, cl_flags.as<u32>(), s_lo[0].as<u64>(), s_val[0].as<u32>(), st);
+    // first-arrival order: sort the groups by their first row
+    SortBufs b;
+    for (int i = 0; i < 2; ++i) { b.lo[i] = s_lo[i].as<u64>(); b.hi[i] = nullptr; b.val[i] = s_val[i].as<u32>(); }
+    b.aux = tile_hist.p;
+    b.map_dev = d_hist_mapped;
+    b.map_host = h_hist;
+    b.pack_ok = true;
+    int bits = 1;
+    while (bits < 32 && ((int64_t)1 << bits) < n) ++bits;
+    const int cur = radix_sort_pairs(1, b, g, 0, bits, st, nullptr);
+    result.reserve(std::max<u32>(g, 1), KW, S);
+    ha_emit(t, s_val[cur].as<u32>(), g, KW, S, result.plo(), result.phi(), result.pst(), st);
+    result.n = g;
+    // hashagg.py accounting of an in-memory table: one hash + one access per
+    // key column per row, two accesses per key column per match
+    led.hash_computations = n;
+    led.column_value_accesses = n * sch.n_key_cols + 2 * (int64_t)sch.n_key_cols * (n - (int64_t)g);
+    led.n_groups = g;
+    sync();
+    ph_collect();
+    return g;
   }
 
   // bench.merge_intersect (bench.py:536-550): keys present in both inputs,
@@ -2743,6 +2833,18 @@ int isa_in_stream_aggregate(isa_handle* h, int64_t n_rows, const void* const* ke
   if (!h) return ISA_ERR_CONTRACT;
   try {
     int64_t g = h->eng->in_stream(n_rows, key_cols, val_cols, input_on_host != 0, (cudaStream_t)stream);
+    if (n_groups_out) *n_groups_out = g;
+    return ISA_OK;
+  } catch (const std::exception& e) {
+    return fail(h, e);
+  }
+}
+
+int isa_hash_aggregate(isa_handle* h, int64_t n_rows, const void* const* key_cols, const void* const* val_cols,
+                       int32_t input_on_host, void* stream, int64_t* n_groups_out) {
+  if (!h) return ISA_ERR_CONTRACT;
+  try {
+    int64_t g = h->eng->hash_aggregate(n_rows, key_cols, val_cols, input_on_host != 0, (cudaStream_t)stream);
     if (n_groups_out) *n_groups_out = g;
     return ISA_OK;
   } catch (const std::exception& e) {

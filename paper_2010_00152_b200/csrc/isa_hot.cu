@@ -224,3 +224,109 @@ void hot_absorb(const SlotDesc& sd, int64_t row0, u32 n, const u32* hit, u64* t_
 }
 
 }  // namespace isa
+
+// ============================================================================
+// Hash aggregation baseline (hashagg.py:73-198, the paper's like-for-like
+// comparison): one open-addressing table of every group in HBM (the GPU's
+// memory holds the whole output, so the reference's budget-driven
+// partitioning is never needed), rows mapped to their group's slot, states
+// combined by k_hot_absorb (shared-memory privatized), the groups emitted in
+// first-arrival order -- the reference's in-memory table order (dict
+// insertion order, hashagg.py:124-146).
+namespace isa {
+
+#define HT_FREE 0u
+#define HT_BUSY 1u
+#define HT_READY 2u
+
+template <int KW>
+__global__ void k_ha_insert(KeyDesc kd, u32 n, u64* __restrict__ tlo, u64* __restrict__ thi, u32* __restrict__ occ,
+                            u32* __restrict__ first, u32 mask, u32* __restrict__ slot_of, u32* __restrict__ ngroups) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    u64 hi, lo;
+    load_key(kd, (i64)i, hi, lo);
+    u32 s = hot_hash(hi, lo) & mask;
+    for (;;) {
+      u32 o = *(volatile u32*)(occ + s);
+      if (o == HT_FREE) {
+        o = atomicCAS(occ + s, HT_FREE, HT_BUSY);
+        if (o == HT_FREE) {   // claimed: publish the key
+          tlo[s] = lo;
+          if (KW == 2) thi[s] = hi;
+          __threadfence();
+          atomicExch(occ + s, HT_READY);
+          atomicAdd(ngroups, 1u);
+          break;
+        }
+      }
+      while (o == HT_BUSY) o = *(volatile u32*)(occ + s);   // another row is publishing this slot
+      if (*(volatile u64*)(tlo + s) == lo && (KW == 1 || *(volatile u64*)(thi + s) == hi)) break;
+      s = (s + 1) & mask;
+    }
+    slot_of[i] = s;
+    if (i < *(volatile u32*)(first + s)) atomicMin(first + s, i);
+  }
+}
+
+// occupied slots -> (first arrival row, slot) pairs, compacted through an exclusive scan of the flags
+__global__ void k_ha_flags(const u32* __restrict__ occ, u32 cap, u32* __restrict__ flag) {
+  for (u32 s = blockIdx.x * blockDim.x + threadIdx.x; s < cap; s += gridDim.x * blockDim.x)
+    flag[s] = occ[s] == HT_READY ? 1u : 0u;
+}
+__global__ void k_ha_compact(const u32* __restrict__ occ, const u32* __restrict__ pre, const u32* __restrict__ first,
+                             u32 cap, u64* __restrict__ key_first, u32* __restrict__ val_slot) {
+  for (u32 s = blockIdx.x * blockDim.x + threadIdx.x; s < cap; s += gridDim.x * blockDim.x)
+    if (occ[s] == HT_READY) {
+      key_first[pre[s]] = first[s];
+      val_slot[pre[s]] = s;
+    }
+}
+template <int MS>
+__global__ void k_ha_emit(const u32* __restrict__ order, u32 g, const u64* __restrict__ tlo,
+                          const u64* __restrict__ thi, const u64* __restrict__ tst, int S, u64* __restrict__ out_lo,
+                          u64* __restrict__ out_hi, u64* __restrict__ out_st) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < g; i += gridDim.x * blockDim.x) {
+    const u32 s = order[i];
+    out_lo[i] = tlo[s];
+    if (out_hi) out_hi[i] = thi[s];
+#pragma unroll
+    for (int k = 0; k < MS; ++k)
+      if (k < S) out_st[(size_t)i * S + k] = tst[(size_t)s * S + k];
+  }
+}
+__global__ void k_ha_init_states(u64* __restrict__ tst, u32 cap, SlotDesc sd) {
+  const int S = sd.nslots;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < (size_t)cap * S; q += (size_t)gridDim.x * blockDim.x)
+    tst[q] = identity_slot(sd.op[q % S], sd.type[q % S]);
+}
+
+void ha_insert(int KW, const KeyDesc& kd, u32 n, const HashAggTable& t, u32* slot_of, cudaStream_t st) {
+  cudaMemsetAsync(t.occ, 0, (size_t)(t.mask + 1) * 4, st);
+  cudaMemsetAsync(t.first, 0xFF, (size_t)(t.mask + 1) * 4, st);
+  cudaMemsetAsync(t.ngroups, 0, 4, st);
+  if (!n) return;
+  const int g = (int)std::min<u32>((n + 255) / 256, 148u * 16u);
+  if (KW == 2) klaunch(k_ha_insert<2>, g, 256, 0, st, kd, n, t.lo, t.hi, t.occ, t.first, t.mask, slot_of, t.ngroups);
+  else klaunch(k_ha_insert<1>, g, 256, 0, st, kd, n, t.lo, t.hi, t.occ, t.first, t.mask, slot_of, t.ngroups);
+}
+void ha_init_states(const HashAggTable& t, const SlotDesc& sd, cudaStream_t st) {
+  if (sd.nslots) klaunch(k_ha_init_states, 148 * 8, 256, 0, st, t.st, t.mask + 1, sd);
+}
+void ha_flags(const HashAggTable& t, u32* flag, cudaStream_t st) {
+  klaunch(k_ha_flags, (int)std::min<u32>((t.mask + 256) / 256, 148u * 16u), 256, 0, st, (const u32*)t.occ, t.mask + 1, flag);
+}
+void ha_compact(const HashAggTable& t, const u32* pre, u64* key_first, u32* val_slot, cudaStream_t st) {
+  klaunch(k_ha_compact, (int)std::min<u32>((t.mask + 256) / 256, 148u * 16u), 256, 0, st, (const u32*)t.occ, pre,
+          (const u32*)t.first, t.mask + 1, key_first, val_slot);
+}
+void ha_emit(const HashAggTable& t, const u32* order, u32 g, int KW, int S, u64* out_lo, u64* out_hi, u64* out_st,
+             cudaStream_t st) {
+  if (!g) return;
+  const int gr = (int)std::min<u32>((g + 255) / 256, 148u * 16u);
+#define HE(M) klaunch(k_ha_emit<M>, gr, 256, 0, st, order, g, (const u64*)t.lo, (const u64*)t.hi, (const u64*)t.st, S, \
+                      out_lo, KW == 2 ? out_hi : (u64*)nullptr, out_st)
+  if (S <= 1) HE(1); else if (S <= 2) HE(2); else if (S <= 4) HE(4); else if (S <= 8) HE(8); else HE(16);
+#undef HE
+}
+
+}  // namespace isa

@@ -152,6 +152,15 @@ void hot_probe(int KW, const KeyDesc& kd, int64_t row0, u32 n, const HotHash& h,
 // states of rows row0 + i (i < n) with hit[i] != ~0 combined into t_st[hit[i]]
 void hot_absorb(const SlotDesc& sd, int64_t row0, u32 n, const u32* hit, u64* t_st, int num_sms, cudaStream_t st);
 
+// ---- hash aggregation baseline (isa_hot.cu, hashagg.py:73-198) -------------
+struct HashAggTable { u64* lo; u64* hi; u64* st; u32* occ; u32* first; u32 mask; u32* ngroups; };
+void ha_insert(int KW, const KeyDesc& kd, u32 n, const HashAggTable& t, u32* slot_of, cudaStream_t st);
+void ha_init_states(const HashAggTable& t, const SlotDesc& sd, cudaStream_t st);
+void ha_flags(const HashAggTable& t, u32* flag, cudaStream_t st);
+void ha_compact(const HashAggTable& t, const u32* pre, u64* key_first, u32* val_slot, cudaStream_t st);
+void ha_emit(const HashAggTable& t, const u32* order, u32 g, int KW, int S, u64* out_lo, u64* out_hi, u64* out_st,
+             cudaStream_t st);
+
 // ---- small-budget run generation in one persistent CTA (isa_seq.cu) -------
 #define SQ_MAX_M 4096
 struct SeqBufs {

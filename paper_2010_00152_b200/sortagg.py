@@ -564,6 +564,14 @@ class SortAggregate:
         n_groups = h.in_stream(n, [k.data_ptr() for k in keys], [v.data_ptr() for v in vals], on_host, sptr)
         return self._collect(h, n, n_groups, keys, slots, on_host, sptr)
 
+    def hash_columns(self, keys, values=None, *, states=False, stream=None):
+        """The hash-aggregation baseline (hashagg.py:73-198) over the same
+        inputs as ``execute_columns``: groups in first-arrival order (the
+        reference's in-memory table order), not sorted."""
+        h, n, keys, vals, slots, on_host, sptr = self._prepare(keys, values, states, stream)
+        n_groups = h.hash_aggregate(n, [k.data_ptr() for k in keys], [v.data_ptr() for v in vals], on_host, sptr)
+        return self._collect(h, n, n_groups, keys, slots, on_host, sptr)
+
     def _prepare(self, keys, values, states, stream):
         torch = _torch()
         keys = list(keys)

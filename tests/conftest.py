@@ -22,9 +22,9 @@ def pytest_configure(config):
 def golden_names():
     """End-to-end operator fixtures (pages_* hold reference run files,
     downstream_* the reference's sorted-output consumers, rs_* replacement
-    selection)."""
+    selection, hash_* the HashAggregate baseline)."""
     names = (os.path.splitext(os.path.basename(p))[0] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz")))
-    return sorted(n for n in names if not n.startswith(("pages_", "downstream_", "rs_")))
+    return sorted(n for n in names if not n.startswith(("pages_", "downstream_", "rs_", "hash_")))
 
 
 def rs_golden_names():

@@ -225,3 +225,15 @@ def test_downstream_needs_the_gpu():
         downstream.merge_intersect(rows, rows)
     assert list(downstream.in_stream_aggregate([], sch)) == []
     assert downstream.merge_intersect([], rows) == []
+
+
+
+def test_hash_agg_config_validation():
+    """HashAggConfig validation mirrors hashagg.py:36-42."""
+    with pytest.raises(isa.InvalidInputError, match="page capacity"):
+        isa.HashAggConfig(memory_budget=10, page_capacity=0)
+    with pytest.raises(isa.InvalidInputError, match="exceed one page"):
+        isa.HashAggConfig(memory_budget=10, page_capacity=10)
+    with pytest.raises(isa.InvalidInputError, match="fan-out"):
+        isa.HashAggConfig(memory_budget=15, page_capacity=10)
+    assert isa.HashAggConfig(memory_budget=100, page_capacity=10).max_fanout == 10
