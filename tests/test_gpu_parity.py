@@ -727,3 +727,39 @@ def test_hash_aggregate_rows_and_large_random():
     assert np.array_equal(res.keys[0].cpu().numpy()[order], want_k[0])
     for s_, (gcol, wcol) in enumerate(zip(res.states, want_s)):
         assert_slots_equal(gcol.cpu().numpy()[order], wcol, rel=1e-5, what=f"slot {s_}")
+
+
+@pytest.mark.parametrize("case", ["rs", "rsw_chunks", "tile_merge", "hot", "hash", "one_cta"])
+def test_repeat_runs_bit_identical(case, monkeypatch):
+    """Race detector in place of compute-sanitizer (closed on this pool):
+    the same input run five times gives bit-identical integer outputs and
+    ledgers (a shared-memory race in the replacement-selection promotion was
+    found this way)."""
+    w = workloads.make(3 if case != "rsw_chunks" else 5, rows=300_000, device="cpu", domain=1 << 14)
+    keys = [k.cuda() for k in w.keys]
+    vals = {k: v.cuda() for k, v in w.values.items()}
+    kw = {}
+    if case == "rs":
+        kw = dict(run_generation_mode=isa.REPLACEMENT_SELECTION, eviction_chunk=8)
+    if case == "tile_merge":
+        monkeypatch.setenv("ISA_TILE_MERGE", "1")
+    if case == "hot":
+        kw = dict(hot_absorb="always")
+    if case == "one_cta":
+        monkeypatch.setenv("ISA_SEQ", "1")
+    outs = []
+    for _ in range(5):
+        if case == "hash":
+            op = isa.HashAggregate(w.schema, isa.HashAggConfig(memory_budget=4096, page_capacity=64))
+            r = op.execute_columns(keys, vals)
+            led = ()
+        else:
+            op = isa.SortAggregate(w.schema, _cfg(1024 if case in ("rs", "one_cta") else 4096, 100, **kw))
+            r = op.execute_columns(keys, vals)
+            led = (tuple(op.run_rows), tuple(op.cycles), op.ledger.rows_spilled)
+        ints = [t.cpu() for t in r.keys] + [t.cpu() for t in r.states if not t.dtype.is_floating_point]
+        outs.append((ints, led))
+    for ints, led in outs[1:]:
+        assert led == outs[0][1]
+        for a, b in zip(ints, outs[0][0]):
+            assert torch.equal(a, b)

@@ -51,4 +51,20 @@ os.environ["ISA_TILE_MERGE"] = "1"
 w = workloads.make(5, rows=300_000, device="cpu", domain=1 << 16)
 check(w, 4096)
 print("tile merge (config 5) OK", flush=True)
-os.environ["ISA_COLLAPSE"] = "fused"
+os.environ["ISA_TILE_MERGE"] = "0"
+w = workloads.make(3, rows=100_000, device="cpu", domain=1 << 14)
+check(w, 512, run_generation_mode=isa.REPLACEMENT_SELECTION, eviction_chunk=16)
+print("replacement selection OK", flush=True)
+check(w, 2048, hot_absorb="always")
+print("hash-image absorb OK", flush=True)
+os.environ["ISA_SEQ"] = "1"
+w = workloads.make(1, rows=100_000, device="cpu")
+check(w, 1024)
+print("one-CTA read-sort-write OK", flush=True)
+w = workloads.make(3, rows=200_000, device="cpu", domain=1 << 14)
+op = isa.HashAggregate(w.schema, isa.HashAggConfig(memory_budget=4096, page_capacity=64))
+res = op.execute_columns([k.cuda() for k in w.keys], {k: v.cuda() for k, v in w.values.items()})
+slots = oracle.make_states(w.schema, {k: v.numpy() for k, v in w.values.items()}, w.rows)
+want_k, _ = oracle.reference_aggregate([k.numpy() for k in w.keys], slots, oracle.slot_ops(w.schema))
+assert np.array_equal(np.sort(res.keys[0].cpu().numpy()), want_k[0])
+print("hash aggregate OK", flush=True)
