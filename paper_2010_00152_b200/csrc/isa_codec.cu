@@ -311,6 +311,52 @@ __global__ void __launch_bounds__(PK_THREADS) k_unpack(const UnpackBlk* __restri
   }
 }
 
+// Slices of HBM-resident packed runs: one descriptor per (run, window) --
+// the covering blocks are found on the device (CTA q -> slice by binary
+// search over the slices' first block numbers), so the host builds k
+// descriptors per window instead of one per 1,024-row block.
+__global__ void __launch_bounds__(PK_THREADS) k_unpack_slices(const UnpackSlice* __restrict__ sl, int ns, u32 nblk,
+                                                              int kw, int S, u32 fmask, u64* __restrict__ lo,
+                                                              u64* __restrict__ hi, u64* __restrict__ st) {
+  const int ncol = pk_ncol(kw, S);
+  for (u32 q = blockIdx.x; q < nblk; q += gridDim.x) {
+    int l = 0, h = ns;   // last slice with blk0 <= q
+    while (h - l > 1) {
+      const int m = (l + h) >> 1;
+      if (sl[m].blk0 <= q) l = m; else h = m;
+    }
+    const UnpackSlice u = sl[l];
+    const u32 b = u.s0 / PK_ROWS + (q - u.blk0);
+    const u32 r0 = b * PK_ROWS;
+    const u32 e0 = max(u.s0, r0) - r0, e1 = min(u.s1, r0 + PK_ROWS) - r0;
+    const u64* blk = (const u64*)(u.pk + u.off[b]);
+    const u64* payload = blk + ncol * 2;
+    for (int c = 0; c < ncol; ++c) {
+      const u64 base = blk[c * 2], meta = blk[c * 2 + 1];
+      const u32 width = (u32)(meta & 0xFF);
+      const u64* w = payload + (meta >> 8);
+      for (u32 i = e0 + threadIdx.x; i < e1; i += PK_THREADS) {
+        const u64 v = base + pk_extract(w, i, width);
+        const u32 o = u.dst + (r0 + i - u.s0);
+        if (c < kw) {
+          if (c == 0) lo[o] = v;
+          else hi[o] = v;
+        } else {
+          const int s_ = c - kw;
+          st[(size_t)o * S + s_] = pk_inv(v, (fmask >> s_) & 1u, 0);
+        }
+      }
+    }
+  }
+}
+
+void unpack_slices(const UnpackSlice* sl, int ns, u32 nblk, int kw, int S, u32 fmask, u64* lo, u64* hi, u64* st,
+                   cudaStream_t stream) {
+  if (ns && nblk)
+    klaunch(k_unpack_slices, (int)std::min<u32>(nblk, 148u * 16u), PK_THREADS, 0, stream, sl, ns, nblk, kw, S, fmask,
+            lo, hi, st);
+}
+
 void unpack_blocks(const UnpackBlk* d, u32 nd, const char* src, int kw, int S, u32 fmask, u64* lo, u64* hi, u64* st,
                    cudaStream_t stream) {
   if (nd) klaunch(k_unpack, nd, PK_THREADS, 0, stream, d, src, kw, S, fmask, lo, hi, st);

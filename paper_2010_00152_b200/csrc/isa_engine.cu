@@ -320,12 +320,18 @@ struct Engine {
     return d;
   }
   // wide merge
+  std::vector<std::pair<u64, u64>> sampled_bounds;   // (hi, lo) window bounds of the sampled plan
   DevBuf stg_lo[2], stg_hi[2], stg_st[2];
   cudaEvent_t stg_ready[2] = {nullptr, nullptr}, stg_free[2] = {nullptr, nullptr};
   DevBuf runref_dev, bounds_lo, bounds_hi, bounds_out;
   DevBuf pk_hdr, pk_sz, pk_status;          // codec: block headers, byte sizes -> offsets, look-back words
   DevBuf stg_pk[2], stg_desc[2];            // wide merge: packed bytes and unpack descriptors per slot
   std::vector<UnpackBlk> desc_host[2];
+  std::vector<UnpackSlice> slice_host[2];         // HBM-resident packed runs' slices per staging slot
+  UnpackSlice* slice_pinned[2] = {nullptr, nullptr};
+  size_t slice_cap[2] = {0, 0};
+  cudaEvent_t slice_done[2] = {nullptr, nullptr};
+  DevBuf stg_slices[2];
   UnpackBlk* desc_pinned[2] = {nullptr, nullptr};
   size_t desc_cap[2] = {0, 0};
   cudaEvent_t desc_done[2] = {nullptr, nullptr};
@@ -403,6 +409,8 @@ struct Engine {
       CK(cudaEventCreateWithFlags(&stg_free[i], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&desc_done[i], cudaEventDisableTiming));
       CK(cudaEventRecord(desc_done[i], 0));
+      CK(cudaEventCreateWithFlags(&slice_done[i], cudaEventDisableTiming));
+      CK(cudaEventRecord(slice_done[i], 0));
       CK(cudaEventCreateWithFlags(&fstage_done[i], cudaEventDisableTiming));
       CK(cudaEventRecord(fstage_done[i], 0));
       CK(cudaEventCreateWithFlags(&win[i].ready, cudaEventDisableTiming));
@@ -430,6 +438,9 @@ struct Engine {
     for (int i = 0; i < 2; ++i) {
       if (desc_pinned[i]) cudaFreeHost(desc_pinned[i]);
       if (desc_done[i]) cudaEventDestroy(desc_done[i]);
+      if (slice_pinned[i]) cudaFreeHost(slice_pinned[i]);
+      if (slice_done[i]) cudaEventDestroy(slice_done[i]);
+      stg_slices[i].release();
       if (fstage[i]) cudaFreeHost(fstage[i]);
       if (pref_pinned[i]) cudaFreeHost(pref_pinned[i]);
       if (fstage_done[i]) cudaEventDestroy(fstage_done[i]);
@@ -654,9 +665,14 @@ struct Engine {
     ph_end(ISA_PH_SORT, m, 0);
     return cur;
   }
-  int sort_built(u32 m) {
+  // known_v: the varying-bit mask is known on the host (a key-range window
+  // [L, U): every key shares the bits above L ^ (U - 1)), no read-back
+  int sort_built(u32 m, const u64* known_v = nullptr) {
     u64 vlo, vhi;
-    if (key_bits <= 16 || (key_bits <= 32 && m <= (1u << 20))) {
+    if (known_v) {
+      vlo = known_v[0];
+      vhi = known_v[1];
+    } else if (key_bits <= 16 || (key_bits <= 32 && m <= (1u << 20))) {
       // at most two 8-bit passes, or a small chunk of <= 32-bit keys: sort
       // every key bit instead of a host round trip for the varying bits
       vlo = key_bits == 64 ? ~0ull : ((1ull << key_bits) - 1);
@@ -1708,8 +1724,12 @@ struct Engine {
     return true;
   }
 
+  // direct != nullptr (wide merge, no tile plan): every window collapses
+  // straight into `direct`, numbered on the device after the groups of the
+  // windows before it -- no per-window host round trip; the host only reads
+  // the count when the rows staged so far could exceed direct's capacity.
   void merge_runs(std::vector<Run>& rs, bool collapse, const std::function<void(Table&, u32)>& emit,
-                  TilePlan* tp = nullptr) {
+                  TilePlan* tp = nullptr, Table* direct = nullptr) {
     auto& runs = rs;
     const int k = (int)runs.size();
     int64_t total = 0;
@@ -1772,7 +1792,8 @@ struct Engine {
         for (int64_t i = 0; i < total_s; ++i) samples.push_back({tmp_hi[i], tmp_lo[i]});
       }
       std::sort(samples.begin(), samples.end());
-      std::vector<std::pair<u64, u64>> bounds;
+      std::vector<std::pair<u64, u64>>& bounds = sampled_bounds;
+      bounds.clear();
       int64_t acc = (int64_t)k * F;
       for (auto& s : samples) {
         if (acc + F > W && (bounds.empty() || bounds.back() != s)) {
@@ -1873,6 +1894,9 @@ struct Engine {
       auto& prefs = pref_host[slot];
       prefs.clear();
       size_t fbytes = 0;
+      auto& slices = slice_host[slot];
+      slices.clear();
+      u32 slice_blocks = 0;
       for (int r = 0; r < k; ++r) {
         u32 s0, s1;
         slice(r, w, s0, s1);
@@ -1915,6 +1939,15 @@ struct Engine {
           if (on_host) {
             CK(cudaMemcpyAsync(stg_pk[slot].as<char>() + poff, runs[r].pk_host + o0, o1 - o0, cudaMemcpyHostToDevice, ss));
             led.bytes_h2d += o1 - o0;
+          }
+          if (!on_host) {
+            // HBM-resident: one slice descriptor, the blocks are found on the device
+            UnpackSlice sl{runs[r].pk_dev, runs[r].off_dev, s0, s1, (u32)off, slice_blocks};
+            slices.push_back(sl);
+            slice_blocks += b1 - b0 + 1;
+            unpack_bytes += (int64_t)(o1 - o0) + (int64_t)cnt * 8 * (KW + S);
+            off += cnt;
+            continue;
           }
           const u64 src0 = on_host ? (u64)(uintptr_t)(stg_pk[slot].as<char>() + poff) : (u64)(uintptr_t)(runs[r].pk_dev + o0);
           for (u32 b = b0; b <= b1; ++b) {
@@ -1972,10 +2005,52 @@ struct Engine {
                       stg_lo[slot].as<u64>(), stg_hi[slot].as<u64>(), stg_st[slot].as<u64>(), ss);
         kt_end(KF_UNPACK, unpack_bytes, ss);
       }
+      if (!slices.empty()) {
+        CK(cudaEventSynchronize(slice_done[slot]));   // the pinned buffer's previous copy is done
+        if (slice_cap[slot] < slices.size()) {
+          if (slice_pinned[slot]) CK(cudaFreeHost(slice_pinned[slot]));
+          slice_cap[slot] = slices.size() + slices.size() / 2 + 64;
+          CK(cudaHostAlloc((void**)&slice_pinned[slot], slice_cap[slot] * sizeof(UnpackSlice), cudaHostAllocDefault));
+        }
+        memcpy(slice_pinned[slot], slices.data(), slices.size() * sizeof(UnpackSlice));
+        stg_slices[slot].ensure(slices.size() * sizeof(UnpackSlice) + 16);
+        CK(cudaMemcpyAsync(stg_slices[slot].p, slice_pinned[slot], slices.size() * sizeof(UnpackSlice),
+                           cudaMemcpyHostToDevice, ss));
+        CK(cudaEventRecord(slice_done[slot], ss));
+        kt_begin(KF_UNPACK, ss);
+        unpack_slices(stg_slices[slot].as<UnpackSlice>(), (int)slices.size(), slice_blocks, KW, S, fmask,
+                      stg_lo[slot].as<u64>(), stg_hi[slot].as<u64>(), stg_st[slot].as<u64>(), ss);
+        kt_end(KF_UNPACK, unpack_bytes, ss);
+      }
       if (mode != 2) CK(cudaEventRecord(stg_ready[slot], h2d));
       return off;
     };
     std::vector<int64_t> wrows(nwin);
+    // sampled windows [bounds[w-1], bounds[w]) are sorted on key - bounds[w-1]
+    // (window 0: key - 0): with a known upper bound (every window but the
+    // last) the varying bits are those of the span, known on the host
+    auto window_low = [&](int w) -> std::pair<u64, u64> {
+      if (tp || w == 0 || w > nb) return {0ull, 0ull};
+      return sampled_bounds[w - 1];
+    };
+    auto window_mask = [&](int w, u64* v) -> bool {
+      if (tp || w >= nb) return false;
+      const auto L = window_low(w), U = sampled_bounds[w];   // (hi, lo), U exclusive
+      u64 uh = U.first, ul = U.second;
+      if (ul == 0) { if (uh == 0) return false; --uh; }
+      --ul;
+      const u64 sh = uh - L.first - (ul < L.second ? 1ull : 0ull), sl = ul - L.second;   // U - 1 - L
+      if (sh) { const int b = 63 - __builtin_clzll(sh); v[1] = b == 63 ? ~0ull : ((1ull << (b + 1)) - 1); v[0] = ~0ull; }
+      else { v[1] = 0; v[0] = sl ? (63 - __builtin_clzll(sl) == 63 ? ~0ull : ((1ull << (64 - __builtin_clzll(sl))) - 1)) : 1ull; }
+      return true;
+    };
+    const bool dir_mode = direct && collapse && !tp;
+    int64_t ub = 0;
+    if (dir_mode) {
+      ub = direct->n;
+      CK(cudaMemcpyAsync(dscal32(25), &direct->n, sizeof(u32), cudaMemcpyHostToDevice, st));
+      sync();
+    }
     const int smode = inplace ? 1 : 0;
     wrows[0] = stage(0, 0, smode);
     for (int w = 0; w < nwin; ++w) {
@@ -1995,15 +2070,31 @@ struct Engine {
       }
       // sort the window's rows by key: keys copied into sort buffers, value = staged row index
       ensure_sort(m);
-      CK(cudaMemcpyAsync(s_lo[0].p, stg_lo[slot].p, (size_t)m * 8, cudaMemcpyDeviceToDevice, st));
-      if (KW == 2) CK(cudaMemcpyAsync(s_hi[0].p, stg_hi[slot].p, (size_t)m * 8, cudaMemcpyDeviceToDevice, st));
-      iota_u32(s_val[0].as<u32>(), m, st);
+      const auto wl = dir_mode ? window_low(w) : std::pair<u64, u64>{0ull, 0ull};
+      window_keys(KW, stg_lo[slot].as<u64>(), stg_hi[slot].as<u64>(), m, wl.second, wl.first, s_lo[0].as<u64>(),
+                  s_hi[0].as<u64>(), s_val[0].as<u32>(), st);
       ph_begin(ISA_PH_WM_SORT);
-      CK(cudaMemsetAsync(dvary(), 0, 2 * sizeof(u64), st));
-      keys_varying(KW, s_lo[0].as<u64>(), s_hi[0].as<u64>(), m, dvary(), st);
-      int cur = sort_built(m);
+      u64 vm[2];
+      const bool known = dir_mode && window_mask(w, vm);
+      if (!known) {
+        CK(cudaMemsetAsync(dvary(), 0, 2 * sizeof(u64), st));
+        keys_varying(KW, s_lo[0].as<u64>(), s_hi[0].as<u64>(), m, dvary(), st);
+      }
+      int cur = sort_built(m, known ? vm : nullptr);
       ph_end(ISA_PH_WM_SORT, m, 0);
       u32 distinct;
+      if (dir_mode) {
+        // room for every row of this window after the groups so far
+        if (ub + m > (int64_t)(direct->lo.bytes / 8)) {
+          direct->n = read_u32(dscal32(25));
+          ub = direct->n;
+          if (ub + m > (int64_t)(direct->lo.bytes / 8)) grow_table(*direct, (size_t)ub + m);
+        }
+        collapse_direct(cur, m, stg_st[slot].as<u64>(), *direct, wl.second, wl.first);
+        ub += m;
+        CK(cudaEventRecord(stg_free[slot], st));
+        continue;
+      }
       if (collapse) {
         collapse_chunk(cur, m, 0xFFFFFFFFu, sd0, 0, stg_st[slot].as<u64>(), U, m);
         distinct = U.n;
@@ -2019,6 +2110,29 @@ struct Engine {
       emit(U, distinct);
     }
     U.n = 0;
+    if (dir_mode) direct->n = read_u32(dscal32(25));
+  }
+
+  // one window's collapse straight into t, numbered after *dscal32(25) groups
+  // (device count updated in place)
+  void collapse_direct(int cur, u32 m, const u64* st_in, Table& t, u64 add_lo, u64 add_hi) {
+    ensure_collapse(m);
+    CollapseTmp ct;
+    ct.flags = cl_flags.as<u32>();
+    ct.scan_tmp = scan_tmp.as<u32>();
+    ct.partial = cl_partial.as<u64>();
+    ct.partial_slot = cl_pslot.as<u32>();
+    ct.total = dscal32(26);
+    ct.dev_base = dscal32(25);
+    ct.key_add_lo = add_lo;
+    ct.key_add_hi = add_hi;
+    ph_begin(ISA_PH_WM_COLLAPSE);
+    kt_begin(KF_COLLAPSE, st);
+    collapse(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, 0xFFFFFFFFu, sd0, 0, st_in,
+             t.plo(), t.phi(), t.pst(), ct, st);
+    kt_end(KF_COLLAPSE, (int64_t)m * (8 * KW + 4 + 8 * S), st);
+    CK(cudaMemcpyAsync(dscal32(25), dscal32(26), sizeof(u32), cudaMemcpyDeviceToDevice, st));
+    ph_end(ISA_PH_WM_COLLAPSE, m, 0);
   }
 
   // Final wide merge of all runs into the result (sortagg.py:588-674)
@@ -2029,13 +2143,12 @@ struct Engine {
     result.n = 0;
     TilePlan tp;
     const bool tiles = build_tile_plan(tp);
-    if (tiles) {   // room for the estimated output (grown by a quarter if short)
+    {   // room for the estimated output (grown when short)
       const int64_t est = estimate_groups(total);
       result.reserve(std::max<int64_t>(1, std::min<int64_t>(total, est + est / 16 + W)), KW, S);
-    } else {
-      result.reserve(std::max<int64_t>(1, std::min<int64_t>(total, W)), KW, S);
     }
-    merge_runs(runs, true, [&](Table& w, u32) { append_result(w); }, tiles ? &tp : nullptr);
+    merge_runs(runs, true, [&](Table& w, u32) { append_result(w); }, tiles ? &tp : nullptr,
+               direct_merge_env() ? &result : nullptr);
     if (cfg.run_tier == ISA_TIER_FILE && read_u32(dscal32(12)))
       throw IsaError(ISA_ERR_CORRUPTION, "page checksum mismatch");   // parse_page, runstore.py:132-142
     led.pages_read = led.pages_written;
@@ -2044,6 +2157,10 @@ struct Engine {
     steps.push_back({ISA_STEP_WIDE, 1, (int64_t)runs.size(), total, (int64_t)result.n, 0});
   }
 
+  static bool direct_merge_env() {   // ISA_DIRECT_MERGE=0 (read per merge): per-window host round trips
+    const char* e = getenv("ISA_DIRECT_MERGE");
+    return !(e && e[0] == '0');
+  }
   void append_result(Table& w) {
     size_t need = (size_t)result.n + w.n;
     if (need > 0xFFFFFFFFull) throw IsaError(ISA_ERR_INVALID_INPUT, "more than 2^32-1 output groups are not supported");
@@ -2172,20 +2289,21 @@ struct Engine {
     return result.n;
   }
 
-  void grow_result(size_t need) {
-    const size_t have = result.lo.bytes / 8;
+  void grow_result(size_t need) { grow_table(result, need); }
+  void grow_table(Table& t, size_t need) {
+    const size_t have = t.lo.bytes / 8;
     size_t cap = std::max(need, have + have / 4);
     Table nt;
     nt.reserve(cap, KW, S);
-    if (result.n) {
-      CK(cudaMemcpyAsync(nt.plo(), result.plo(), (size_t)result.n * 8, cudaMemcpyDeviceToDevice, st));
-      if (KW == 2) CK(cudaMemcpyAsync(nt.phi(), result.phi(), (size_t)result.n * 8, cudaMemcpyDeviceToDevice, st));
-      if (S) CK(cudaMemcpyAsync(nt.pst(), result.pst(), (size_t)result.n * 8 * S, cudaMemcpyDeviceToDevice, st));
+    if (t.n) {
+      CK(cudaMemcpyAsync(nt.plo(), t.plo(), (size_t)t.n * 8, cudaMemcpyDeviceToDevice, st));
+      if (KW == 2) CK(cudaMemcpyAsync(nt.phi(), t.phi(), (size_t)t.n * 8, cudaMemcpyDeviceToDevice, st));
+      if (S) CK(cudaMemcpyAsync(nt.pst(), t.pst(), (size_t)t.n * 8 * S, cudaMemcpyDeviceToDevice, st));
     }
     sync();
-    nt.n = result.n;
-    result.release();
-    result = nt;
+    nt.n = t.n;
+    t.release();
+    t = nt;
     nt.lo.p = nt.hi.p = nt.st.p = nullptr;
   }
 

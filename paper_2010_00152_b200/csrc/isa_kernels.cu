@@ -185,6 +185,23 @@ __device__ __forceinline__ u32 digit_of(u64 hi, u64 lo, int shift) {
   return (u32)(v & 0xFFu);
 }
 
+// peers & (lanes whose digit bit `m` equals mine): the bit test feeds the
+// ballot as a predicate and the same predicate selects the replicated mask,
+// so the select folds into one LOP3 (4 instructions per bit instead of 6)
+__device__ __forceinline__ u32 ballot_same_bit(u32 peers, u32 d, u32 m) {
+  u32 r;
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 t, rep;\n\t"
+      "and.b32 t, %2, %3;\n\t"
+      "setp.ne.u32 p, t, 0;\n\t"
+      "vote.sync.ballot.b32 t, p, 0xffffffff;\n\t"
+      "selp.b32 rep, 0xffffffff, 0, p;\n\t"
+      "xor.b32 t, t, rep;\n\t"
+      "not.b32 t, t;\n\t"
+      "and.b32 %0, %1, t;\n\t}"
+      : "=r"(r) : "r"(peers), "r"(d), "r"(m));
+  return r;
+}
+
 // one key word: no cross-word digit (the hot loops of k_rs_scatter)
 template <int KW>
 __device__ __forceinline__ u32 digit_kw(u64 hi, u64 lo, int shift) {
@@ -283,11 +300,7 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 2 ? 4 : 3)) k
     } else {
       peers = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
 #pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const u32 bit = (d >> b) & 1u;
-        const u32 bits = __ballot_sync(0xffffffffu, bit);
-        peers &= ~(bits ^ (0u - bit));   // lanes whose bit b equals mine (one LOP3)
-      }
+      for (int b = 0; b < 8; ++b) peers = ballot_same_bit(peers, d, 1u << b);
       if (!FULL && !valid) peers = 1u << lane;
     }
     int leader = __ffs(peers) - 1;
@@ -935,6 +948,26 @@ void read_words(u32* dst_mapped, const u32* src, u32 nwords, cudaStream_t st) {
   klaunch(k_read_words, 1, 64, 0, st, dst_mapped, src, nwords);
 }
 
+// wide-merge window keys relative to the window's low bound (fewer varying
+// bits, exact pass count without a read-back) + the staged-row payload
+template <int KW>
+__global__ void k_window_keys(const u64* __restrict__ slo, const u64* __restrict__ shi, u32 m, u64 llo, u64 lhi,
+                              u64* __restrict__ dlo, u64* __restrict__ dhi, u32* __restrict__ val) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const u64 l = slo[i];
+    dlo[i] = l - llo;
+    if (KW == 2) dhi[i] = shi[i] - lhi - (l < llo ? 1ull : 0ull);
+    val[i] = i;
+  }
+}
+void window_keys(int KW, const u64* slo, const u64* shi, u32 m, u64 llo, u64 lhi, u64* dlo, u64* dhi, u32* val,
+                 cudaStream_t st) {
+  if (!m) return;
+  const int g = (int)std::min<u32>((m + 255) / 256, 148u * 16u);
+  if (KW == 2) klaunch(k_window_keys<2>, g, 256, 0, st, slo, shi, m, llo, lhi, dlo, dhi, val);
+  else klaunch(k_window_keys<1>, g, 256, 0, st, slo, (const u64*)nullptr, m, llo, lhi, dlo, (u64*)nullptr, val);
+}
+
 __global__ void k_iota(u32* v, u32 n) {
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = i;
 }
@@ -1165,7 +1198,12 @@ __global__ void __launch_bounds__(CB_THREADS) k_cl_count(const u64* __restrict__
 
 // exclusive scan of nb block counts in one CTA (1024 threads, sequential per
 // thread chunk); *total = sum
-__global__ void __launch_bounds__(1024) k_cl_scan(u32* __restrict__ counts, u32 nb, u32* __restrict__ total) {
+// base != nullptr: group numbers continue after *base (device-resident
+// output count, the wide merge appending window after window without a host
+// round trip); *total = *base + groups then
+__global__ void __launch_bounds__(1024) k_cl_scan(u32* __restrict__ counts, u32 nb, u32* __restrict__ total,
+                                                  const u32* __restrict__ base) {
+  const u32 b0v = base ? *base : 0u;
   __shared__ u32 ws[32];
   const u32 per = (nb + 1023) / 1024;
   const u32 b0 = min(nb, threadIdx.x * per), b1 = min(nb, b0 + per);
@@ -1187,10 +1225,10 @@ __global__ void __launch_bounds__(1024) k_cl_scan(u32* __restrict__ counts, u32 
       if (lane >= o) y += z;
     }
     ws[lane] = y - v;
-    if (lane == 31) *total = y;
+    if (lane == 31) *total = b0v + y;
   }
   __syncthreads();
-  u32 run = ws[w] + x - s;
+  u32 run = b0v + ws[w] + x - s;
   for (u32 b = b0; b < b1; ++b) {
     const u32 c = counts[b];
     counts[b] = run;
@@ -1204,7 +1242,8 @@ __global__ void __launch_bounds__(CB_THREADS) k_seg_reduce_b(const u64* __restri
                                                              i64 row0, const u64* __restrict__ st_in,
                                                              const u32* __restrict__ bbase, u64* __restrict__ out_lo,
                                                              u64* __restrict__ out_hi, u64* __restrict__ out_st,
-                                                             u64* __restrict__ partial, u32* __restrict__ partial_slot) {
+                                                             u64* __restrict__ partial, u32* __restrict__ partial_slot,
+                                                             u64 add_lo, u64 add_hi) {
   const int S = sd.nslots;
   constexpr u32 CLI = (u32)cl_items(MS);
   const u32 t = blockIdx.x * CB_THREADS + threadIdx.x;
@@ -1265,8 +1304,9 @@ __global__ void __launch_bounds__(CB_THREADS) k_seg_reduce_b(const u64* __restri
       if (have) flush();
       have = true; lead = false;
       slot = hp++;
-      out_lo[slot] = l;
-      if (KW == 2) out_hi[slot] = h;
+      const u64 ol = l + add_lo;   // keys were sorted relative to the window's low bound
+      out_lo[slot] = ol;
+      if (KW == 2) out_hi[slot] = h + add_hi + (ol < l ? 1ull : 0ull);
 #pragma unroll
       for (int k = 0; k < MS; ++k) acc[k] = cur[k];
     } else if (!have) {
@@ -1686,10 +1726,11 @@ void collapse(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, u32 l
               int64_t row0, const u64* st_in, u64* out_lo, u64* out_hi, u64* out_st, CollapseTmp& tmp,
               cudaStream_t st) {
   if (m == 0) {
-    cudaMemsetAsync(tmp.total, 0, sizeof(u32), st);
+    if (tmp.dev_base) cudaMemcpyAsync(tmp.total, tmp.dev_base, sizeof(u32), cudaMemcpyDeviceToDevice, st);
+    else cudaMemsetAsync(tmp.total, 0, sizeof(u32), st);
     return;
   }
-  if (tmp.status && collapse_fused_env()) {
+  if (tmp.status && collapse_fused_env() && !tmp.dev_base) {
     const int S = sd.nslots;
     const u32 nt = collapse_tiles(m, S);
     const u32 ep = (g_cf_epoch.fetch_add(1) % 0x3FFFFFFEu) + 1u;
@@ -1711,15 +1752,16 @@ void collapse(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, u32 l
   // per-row head flags + full scan (round-1 path)
   static int cb_env = -1;
   if (cb_env < 0) { const char* e = getenv("ISA_COLLAPSE"); cb_env = (e && e[0] == 'r') ? 0 : 1; }
-  if (cb_env && (u32)blocks <= 1024u * 1024u) {
+  if ((cb_env || tmp.dev_base) && (u32)blocks <= 1024u * 1024u) {
     // block head counts -> one-CTA scan -> reduce numbering its own groups
 #define CB_CNT(K, M) klaunch(k_cl_count<K, M>, blocks, CB_THREADS, 0, st, lo, hi, val, m, limit, tmp.flags)
 #define CB_RED(K, M) klaunch(k_seg_reduce_b<K, M>, blocks, CB_THREADS, 0, st, lo, hi, val, m, limit, sd, (i64)row0, \
-                             st_in, (const u32*)tmp.flags, out_lo, out_hi, out_st, tmp.partial, tmp.partial_slot)
+                             st_in, (const u32*)tmp.flags, out_lo, out_hi, out_st, tmp.partial, tmp.partial_slot, \
+                             tmp.key_add_lo, tmp.key_add_hi)
 #define CB_KW(K, X) { if (S <= 1) X(K, 1); else if (S <= 2) X(K, 2); else if (S <= 4) X(K, 4); \
                       else if (S <= 5) X(K, 5); else if (S <= 8) X(K, 8); else X(K, 16); }
     if (KW == 2) CB_KW(2, CB_CNT) else CB_KW(1, CB_CNT)
-    klaunch(k_cl_scan, 1, 1024, 0, st, tmp.flags, (u32)blocks, tmp.total);
+    klaunch(k_cl_scan, 1, 1024, 0, st, tmp.flags, (u32)blocks, tmp.total, (const u32*)tmp.dev_base);
     if (KW == 2) CB_KW(2, CB_RED) else CB_KW(1, CB_RED)
 #undef CB_KW
 #undef CB_RED

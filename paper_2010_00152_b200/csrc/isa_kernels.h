@@ -84,7 +84,14 @@ struct CollapseTmp {
   u64* status = nullptr;   // collapse_tiles(m, S) look-back words, zero when allocated (epoch-tagged after)
   u64* pay = nullptr;      // collapse_tiles(m, S) * 2 * S state words
   u32* ticket = nullptr;   // tile counter
+  // != nullptr: groups are numbered from *dev_base on (the outputs point at
+  // the table's row 0) and *total receives *dev_base + groups (block-count path)
+  const u32* dev_base = nullptr;
+  u64 key_add_lo = 0, key_add_hi = 0;   // added to every output key (block-count path; window-relative keys)
 };
+// s = window keys - (lhi:llo) (128-bit), val = 0..m-1
+void window_keys(int KW, const u64* slo, const u64* shi, u32 m, u64 llo, u64 lhi, u64* dlo, u64* dhi, u32* val,
+                 cudaStream_t st);
 u32 collapse_tiles(u32 m, int S);
 // value columns of rows [row0, row0 + n) interleaved into R-byte records
 struct RowPack { int nc; const void* src[ISA_MAX_SLOTS]; int elem[ISA_MAX_SLOTS]; int off[ISA_MAX_SLOTS]; int R; };
@@ -197,6 +204,11 @@ void pack_write(const PackSrc& p, const u64* hdr, const u32* blk_off, char* out,
 bool pack_fused_ok(const PackSrc& p);
 void pack_fused(const PackSrc& p, u64* status, u32* ticket, u32* blk_off, char* out, cudaStream_t st);
 void unpack_blocks(const UnpackBlk* d, u32 nd, const char* src, int kw, int S, u32 fmask, u64* lo, u64* hi, u64* st,
+                   cudaStream_t stream);
+// rows [s0, s1) of an HBM-resident packed run (blocks at pk + off[b]) -> staged rows from dst;
+// blk0 = number of covering blocks of the slices before this one
+struct UnpackSlice { const char* pk; const u32* off; u32 s0, s1, dst, blk0; };
+void unpack_slices(const UnpackSlice* sl, int ns, u32 nblk, int kw, int S, u32 fmask, u64* lo, u64* hi, u64* st,
                    cudaStream_t stream);
 
 // ---- reference page format (isa_pages.cu, runstore.py:1-20, 120-142) ----

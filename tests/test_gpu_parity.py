@@ -41,13 +41,16 @@ def _cfg(memory, page, **kw):
 
 @pytest.mark.parametrize("name", golden_names())
 @pytest.mark.parametrize("variant", ["device", "host_input", "hbm_runs", "packed_runs", "host_runs", "small_chunks",
-                                     "k1_always", "k1_never", "tile_merge", "radix_merge", "one_cta"])
+                                     "k1_always", "k1_never", "tile_merge", "radix_merge", "one_cta",
+                                     "window_round_trips"])
 def test_golden_columns(name, variant, monkeypatch):
     g = Golden(name)
     if variant in ("tile_merge", "radix_merge"):   # force either wide-merge path
         monkeypatch.setenv("ISA_TILE_MERGE", "1" if variant == "tile_merge" else "0")
     if variant == "one_cta":   # small budgets: the one-CTA read-sort-write run generation (isa_seq.cu)
         monkeypatch.setenv("ISA_SEQ", "1")
+    if variant == "window_round_trips":   # wide merge reading every window's group count back (no device base)
+        monkeypatch.setenv("ISA_DIRECT_MERGE", "0")
     sch = g.schema()
     kw = {}
     if variant == "hbm_runs":
@@ -64,7 +67,7 @@ def test_golden_columns(name, variant, monkeypatch):
         kw.update(preaggregate="never")
     mode = str(g.z["merge_mode"]) if "merge_mode" in g.z else "wide"
     if mode != "wide" and variant in ("k1_always", "k1_never", "small_chunks", "packed_runs", "host_runs",
-                                      "tile_merge", "radix_merge", "one_cta"):
+                                      "tile_merge", "radix_merge", "one_cta", "window_round_trips"):
         pytest.skip("pre-aggregation / chunking knobs apply to the wide path only")
     op = isa.SortAggregate(sch, _cfg(g.memory, g.page, merge_mode=mode, **kw))
     n = len(g.keys[0])
@@ -763,3 +766,17 @@ def test_repeat_runs_bit_identical(case, monkeypatch):
         assert led == outs[0][1]
         for a, b in zip(ints, outs[0][0]):
             assert torch.equal(a, b)
+
+
+
+@pytest.mark.parametrize("cfg,rows,memory,window", [(5, 3_000_000, 1 << 14, 50_000), (3, 2_000_000, 1 << 14, 40_000),
+                                                    (4, 1_000_000, 1 << 14, 30_000), (1, 1_000_000, 4096, 20_000)])
+def test_direct_window_merge_many_windows_vs_oracle(cfg, rows, memory, window, monkeypatch):
+    """Many small wide-merge windows appended on the device (group numbers
+    continue from a device-resident count, the result grows when the rows
+    staged so far could overflow it): equals the oracle."""
+    monkeypatch.setenv("ISA_TILE_MERGE", "0")   # the radix-window path (128-bit keys default to tiles)
+    kw = {"domain": 1 << 20} if cfg in (3, 5) else {}
+    w = workloads.make(cfg, rows=rows, device="cpu", **kw)
+    op = _oracle_case(w, memory, page=100, rel=1e-5 if cfg == 3 else 1e-9, merge_window_rows=window)
+    assert op.device_ledger["merge_windows"] > 10
