@@ -357,6 +357,25 @@ void unpack_slices(const UnpackSlice* sl, int ns, u32 nblk, int kw, int S, u32 f
             lo, hi, st);
 }
 
+// Raw (unpacked) HBM-resident run slices into a window's staging columns:
+// one CTA per piece of <= RAW_PIECE rows instead of one cudaMemcpy per
+// slice and column (a window over a few hundred small runs spent ~1 ms in
+// copy launches).
+__global__ void __launch_bounds__(256) k_gather_raw(const RawCopy* __restrict__ d, int kw, int S, u64* __restrict__ lo,
+                                                    u64* __restrict__ hi, u64* __restrict__ st) {
+  const RawCopy c = d[blockIdx.x];
+  for (u32 i = threadIdx.x; i < c.cnt; i += 256) {
+    lo[c.dst + i] = c.lo[i];
+    if (kw == 2) hi[c.dst + i] = c.hi[i];
+  }
+  const u32 ns = c.cnt * (u32)S;
+  for (u32 i = threadIdx.x; i < ns; i += 256) st[c.dst * S + i] = c.st[i];
+}
+
+void gather_raw(const RawCopy* d, u32 nd, int kw, int S, u64* lo, u64* hi, u64* st, cudaStream_t stream) {
+  if (nd) klaunch(k_gather_raw, nd, 256, 0, stream, d, kw, S, lo, hi, st);
+}
+
 void unpack_blocks(const UnpackBlk* d, u32 nd, const char* src, int kw, int S, u32 fmask, u64* lo, u64* hi, u64* st,
                    cudaStream_t stream) {
   if (nd) klaunch(k_unpack, nd, PK_THREADS, 0, stream, d, src, kw, S, fmask, lo, hi, st);

@@ -332,6 +332,11 @@ struct Engine {
   size_t slice_cap[2] = {0, 0};
   cudaEvent_t slice_done[2] = {nullptr, nullptr};
   DevBuf stg_slices[2];
+  std::vector<RawCopy> raw_host[2];             // HBM-resident raw runs' slice pieces per staging slot
+  RawCopy* raw_pinned[2] = {nullptr, nullptr};
+  size_t raw_cap[2] = {0, 0};
+  cudaEvent_t raw_done[2] = {nullptr, nullptr};
+  DevBuf stg_raw[2];
   UnpackBlk* desc_pinned[2] = {nullptr, nullptr};
   size_t desc_cap[2] = {0, 0};
   cudaEvent_t desc_done[2] = {nullptr, nullptr};
@@ -411,6 +416,8 @@ struct Engine {
       CK(cudaEventRecord(desc_done[i], 0));
       CK(cudaEventCreateWithFlags(&slice_done[i], cudaEventDisableTiming));
       CK(cudaEventRecord(slice_done[i], 0));
+      CK(cudaEventCreateWithFlags(&raw_done[i], cudaEventDisableTiming));
+      CK(cudaEventRecord(raw_done[i], 0));
       CK(cudaEventCreateWithFlags(&fstage_done[i], cudaEventDisableTiming));
       CK(cudaEventRecord(fstage_done[i], 0));
       CK(cudaEventCreateWithFlags(&win[i].ready, cudaEventDisableTiming));
@@ -432,7 +439,7 @@ struct Engine {
                       &runref_dev, &bounds_lo, &bounds_hi, &bounds_out, &out_tmp, &pk_hdr, &pk_sz,
                       &stg_pk[0], &stg_pk[1], &stg_desc[0], &stg_desc[1], &t_backup, &pk_status, &rec_buf,
                       &tm_D, &tm_P, &tm_base, &tm_status, &tm_dirptrs, &tm_scal, &tm_gap, &tm_tb,
-                      &hb_klo, &hb_khi, &hb_idx, &hot_hit,
+                      &hb_klo, &hb_khi, &hb_idx, &hot_hit, &ct_cuts, &ct_out, &ct_len, &ct_lo, &ct_st,
                       &sq_st[0], &sq_st[1], &sq_st[2], &sq_st[3], &sq_grp, &sq_runlo, &sq_runst, &sq_off, &sq_len,
                       &sq_cyc, &sq_keys, &sq_out, &ha_lo, &ha_hi, &ha_st, &ha_occ, &ha_first, &ha_slot};
     for (int i = 0; i < 2; ++i) {
@@ -441,6 +448,9 @@ struct Engine {
       if (slice_pinned[i]) cudaFreeHost(slice_pinned[i]);
       if (slice_done[i]) cudaEventDestroy(slice_done[i]);
       stg_slices[i].release();
+      if (raw_pinned[i]) cudaFreeHost(raw_pinned[i]);
+      if (raw_done[i]) cudaEventDestroy(raw_done[i]);
+      stg_raw[i].release();
       if (fstage[i]) cudaFreeHost(fstage[i]);
       if (pref_pinned[i]) cudaFreeHost(pref_pinned[i]);
       if (fstage_done[i]) cudaEventDestroy(fstage_done[i]);
@@ -1896,6 +1906,8 @@ struct Engine {
       size_t fbytes = 0;
       auto& slices = slice_host[slot];
       slices.clear();
+      auto& raws = raw_host[slot];
+      raws.clear();
       u32 slice_blocks = 0;
       for (int r = 0; r < k; ++r) {
         u32 s0, s1;
@@ -1965,6 +1977,20 @@ struct Engine {
           off += cnt;
           continue;
         }
+        if (!runs[r].host) {   // HBM-resident raw run: pieces for one gather kernel
+          for (u32 q = 0; q < cnt; q += RAW_PIECE) {
+            RawCopy rc;
+            rc.lo = runs[r].lo + s0 + q;
+            rc.hi = KW == 2 ? runs[r].hi + s0 + q : nullptr;
+            rc.st = S ? runs[r].st + (size_t)(s0 + q) * S : nullptr;
+            rc.dst = (u64)(off + q);
+            rc.cnt = std::min<u32>(RAW_PIECE, (u32)cnt - q);
+            rc.pad = 0;
+            raws.push_back(rc);
+          }
+          off += cnt;
+          continue;
+        }
         cudaMemcpyKind kind = runs[r].host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
         CK(cudaMemcpyAsync(stg_lo[slot].as<u64>() + off, runs[r].lo + s0, cnt * 8, cudaMemcpyDefault, ss));
         if (KW == 2) CK(cudaMemcpyAsync(stg_hi[slot].as<u64>() + off, runs[r].hi + s0, cnt * 8, cudaMemcpyDefault, ss));
@@ -2021,6 +2047,20 @@ struct Engine {
         unpack_slices(stg_slices[slot].as<UnpackSlice>(), (int)slices.size(), slice_blocks, KW, S, fmask,
                       stg_lo[slot].as<u64>(), stg_hi[slot].as<u64>(), stg_st[slot].as<u64>(), ss);
         kt_end(KF_UNPACK, unpack_bytes, ss);
+      }
+      if (!raws.empty()) {
+        CK(cudaEventSynchronize(raw_done[slot]));   // the pinned buffer's previous copy is done
+        if (raw_cap[slot] < raws.size()) {
+          if (raw_pinned[slot]) CK(cudaFreeHost(raw_pinned[slot]));
+          raw_cap[slot] = raws.size() + raws.size() / 2 + 64;
+          CK(cudaHostAlloc((void**)&raw_pinned[slot], raw_cap[slot] * sizeof(RawCopy), cudaHostAllocDefault));
+        }
+        memcpy(raw_pinned[slot], raws.data(), raws.size() * sizeof(RawCopy));
+        stg_raw[slot].ensure(raws.size() * sizeof(RawCopy) + 16);
+        CK(cudaMemcpyAsync(stg_raw[slot].p, raw_pinned[slot], raws.size() * sizeof(RawCopy), cudaMemcpyHostToDevice, ss));
+        CK(cudaEventRecord(raw_done[slot], ss));
+        gather_raw(stg_raw[slot].as<RawCopy>(), (u32)raws.size(), KW, S, stg_lo[slot].as<u64>(),
+                   stg_hi[slot].as<u64>(), stg_st[slot].as<u64>(), ss);
       }
       if (mode != 2) CK(cudaEventRecord(stg_ready[slot], h2d));
       return off;
@@ -2396,6 +2436,94 @@ struct Engine {
     }
   }
 
+  // ------------------------------------ cut-then-aggregate (isa_seq.cu) --
+  // Small budgets: every read-sort-write fill cycle starts from an empty
+  // table, so the cycle boundaries follow from the keys alone.  One CTA
+  // finds them (k_cut_scan), then every cycle's run is built in parallel
+  // (k_cut_runs): two launches and two host synchronizations for the whole
+  // run generation instead of a few launches and syncs per cycle.  The scan
+  // stops at the first cycle longer than it can sort in shared memory; the
+  // chunked loop continues from that cycle's first row (empty table: exact).
+  DevBuf ct_cuts, ct_out, ct_len, ct_lo, ct_st;
+  bool cut_staged = false;
+  int64_t host_window_rows() const { return cfg.window_rows > 0 ? cfg.window_rows : ((int64_t)32 << 20); }
+  bool cut_wanted(int64_t n, bool on_host) const {
+    const char* e = getenv("ISA_CUT");   // read per execute (A/B and tests)
+    if (e && e[0] == '0') return false;
+    if (cfg.run_generation != ISA_RUNGEN_RSW || cfg.merge_mode != ISA_MERGE_WIDE) return false;
+    if (cfg.run_tier != ISA_TIER_AUTO && cfg.run_tier != ISA_TIER_HBM) return false;
+    if (cfg.chunk_rows_max != 0 || cfg.preaggregate == 1 || cfg.hot_absorb == 1) return false;
+    if (!cut_supported(KW, S, cfg.memory_budget)) return false;
+    if (n <= cfg.memory_budget || n > ((int64_t)1 << 26)) return false;
+    if (on_host && n > host_window_rows()) return false;
+    return true;
+  }
+  // returns the first row the chunked loop still has to process
+  int64_t execute_cut(int64_t n, const void* const* key_cols, const void* const* val_cols, bool on_host) {
+    const u32 M = (u32)cfg.memory_budget;
+    const void* kb[ISA_MAX_KEY_COLS];
+    const void* vb[ISA_MAX_VAL_COLS];
+    if (on_host) {   // the whole input in one window; the chunked loop reuses it
+      Window& w = win[0];
+      CK(cudaStreamSynchronize(h2d));
+      stage_window(w, key_cols, val_cols, 0, n);
+      CK(cudaStreamWaitEvent(st, w.ready, 0));
+      for (int c = 0; c < sch.n_key_cols; ++c) kb[c] = w.keys[c].p;
+      for (int j = 0; j < sch.n_val_cols; ++j) vb[j] = w.vals[j].p;
+      cut_staged = true;
+    } else {
+      for (int c = 0; c < sch.n_key_cols; ++c) kb[c] = key_cols[c];
+      for (int j = 0; j < sch.n_val_cols; ++j) vb[j] = val_cols[j];
+    }
+    const KeyDesc kd = kd_at(kb);
+    const SlotDesc sd = sd_at(vb);
+    const u32 max_cuts = (u32)(n / M + 4);
+    ct_cuts.ensure((size_t)max_cuts * 4 + 64);
+    ct_out.ensure(64);
+    CK(cudaMemsetAsync(ct_out.p, 0, 64, st));
+    ph_begin(ISA_PH_FLUSH);
+    cut_scan(kd, (u32)n, M, ct_cuts.as<u32>(), max_cuts, ct_out.p, st);
+    ph_end(ISA_PH_FLUSH, n, n * (key_bits / 8));
+    struct { u32 ncuts, stop, batches, overflow; } o;
+    CK(cudaMemcpyAsync(&o, ct_out.p, sizeof(o), cudaMemcpyDeviceToHost, st));
+    sync();
+    if (o.overflow) throw IsaError(ISA_ERR_RESOURCE, "cut directory of the small-budget run generation overflowed");
+    const bool done = (int64_t)o.stop == n;
+    const u32 ncyc = o.ncuts + (done ? 1u : 0u);
+    if (ncyc == 0) return 0;
+    const int Sx = std::max(S, 1);
+    ct_lo.ensure((size_t)ncyc * M * 8 + 64);
+    ct_st.ensure((size_t)ncyc * M * 8 * Sx + 64);
+    ct_len.ensure((size_t)ncyc * 4 + 64);
+    ph_begin(ISA_PH_COLLAPSE);
+    cut_runs(kd, sd, ct_cuts.as<u32>(), ncyc, M, ct_lo.as<u64>(), ct_st.as<u64>(), ct_len.as<u32>(), st);
+    ph_end(ISA_PH_COLLAPSE, o.stop, 0);
+    std::vector<u32> cuts(o.ncuts + 2), len(ncyc);
+    CK(cudaMemcpyAsync(cuts.data(), ct_cuts.p, 4 * cuts.size(), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(len.data(), ct_len.p, 4 * (size_t)ncyc, cudaMemcpyDeviceToHost, st));
+    sync();
+    led.chunks += ncyc;
+    if (o.ncuts == 0) {   // done, no flush: the one cycle is the index, i.e. the result
+      T.reserve(std::max<size_t>(tcap, (size_t)len[0] + 1), KW, S);
+      CK(cudaMemcpyAsync(T.plo(), ct_lo.p, (size_t)len[0] * 8, cudaMemcpyDeviceToDevice, st));
+      if (S) CK(cudaMemcpyAsync(T.pst(), ct_st.p, (size_t)len[0] * 8 * S, cudaMemcpyDeviceToDevice, st));
+      T.n = len[0];
+      return n;
+    }
+    for (u32 c = 0; c < ncyc; ++c) {
+      Run rr;
+      rr.host = false;
+      rr.rows = len[c];
+      rr.lo = ct_lo.as<u64>() + (size_t)c * M;
+      rr.hi = nullptr;
+      rr.st = S ? ct_st.as<u64>() + (size_t)c * M * S : nullptr;
+      runs.push_back(rr);
+      account_written(rr);
+    }
+    for (u32 c = 0; c < o.ncuts; ++c) cycles.push_back(cuts[c + 1] - cuts[c]);
+    return o.stop;
+  }
+
   // ------------------------------------------------------------ execute --
   int64_t execute(int64_t n, const void* const* key_cols, const void* const* val_cols, bool on_host,
                   cudaStream_t stream) {
@@ -2466,11 +2594,15 @@ struct Engine {
 
     const bool seq = seq_wanted(n);
     if (seq) execute_seq(n, key_cols, val_cols, on_host);
-    int64_t wrows = on_host ? (cfg.window_rows > 0 ? cfg.window_rows : ((int64_t)32 << 20)) : n;
-    int64_t a = seq ? n : 0, cycle_start = 0, last_len = 0, last_cycle = 0;
-    bool last_flushed = false;
+    cut_staged = false;
+    for (auto& w : win) w.staged = false;   // never reuse a window staged from another execute's input
+    const int64_t cut_stop = !seq && cut_wanted(n, on_host) ? execute_cut(n, key_cols, val_cols, on_host) : 0;
+    int64_t wrows = on_host ? (cut_staged ? n : host_window_rows()) : n;
+    int64_t a = seq ? n : cut_stop, cycle_start = a, last_len = 0, last_cycle = 0;
+    bool last_flushed = !cycles.empty();
+    if (last_flushed) last_len = last_cycle = cycles.back();
     int wi = 0;
-    if (on_host && !seq) stage_window(win[0], key_cols, val_cols, 0, std::min(n, wrows));
+    if (on_host && !seq && !cut_staged) stage_window(win[0], key_cols, val_cols, 0, std::min(n, wrows));
     while (a < n) {
       const void* kb[ISA_MAX_KEY_COLS];
       const void* vb[ISA_MAX_VAL_COLS];
@@ -2542,7 +2674,7 @@ struct Engine {
     // with host-tier runs it stays where it is (HBM): the wide merge reads it
     // next, so a PCIe round trip would buy nothing (the ledger counts it as
     // written like every run)
-    if (!runs.empty() && !seq) {
+    if (!runs.empty() && !seq && T.n > 0) {
       if ((cfg.run_tier == ISA_TIER_HOST || cfg.run_tier == ISA_TIER_AUTO) && T.n > 0) {
         Run r;
         r.dir = make_dir();

@@ -184,6 +184,14 @@ bool seq_supported(int KW, int S, int64_t M, bool rs);
 void seq_rungen(bool rs, const KeyDesc& kd, const SlotDesc& sd, u32 n, u32 M, u32 P, const SeqBufs& b,
                 cudaStream_t st);
 
+// cut-then-aggregate read-sort-write for small budgets (isa_seq.cu): the
+// fill-cycle boundaries from the keys in one CTA, then every cycle's run in
+// parallel.  out: {ncuts, stop, batches, overflow}; cuts: max_cuts entries.
+bool cut_supported(int KW, int S, int64_t M);
+void cut_scan(const KeyDesc& kd, u32 n, u32 M, u32* cuts, u32 max_cuts, void* out, cudaStream_t st);
+void cut_runs(const KeyDesc& kd, const SlotDesc& sd, const u32* cuts, u32 ncycles, u32 M, u64* run_lo, u64* run_st,
+              u32* run_len, cudaStream_t st);
+
 // ---- runs / wide merge helpers ------------------------------------------
 // out[r * nb + b] = lower_bound(run r, bound b); run keys may be mapped host memory
 // A run for the wide merge's slice search: raw key words (lo/hi), or a
@@ -207,6 +215,10 @@ void unpack_blocks(const UnpackBlk* d, u32 nd, const char* src, int kw, int S, u
                    cudaStream_t stream);
 // rows [s0, s1) of an HBM-resident packed run (blocks at pk + off[b]) -> staged rows from dst;
 // blk0 = number of covering blocks of the slices before this one
+// raw HBM run slice pieces -> staging columns (isa_codec.cu)
+#define RAW_PIECE 8192
+struct RawCopy { const u64* lo; const u64* hi; const u64* st; u64 dst; u32 cnt, pad; };
+void gather_raw(const RawCopy* d, u32 nd, int kw, int S, u64* lo, u64* hi, u64* st, cudaStream_t stream);
 struct UnpackSlice { const char* pk; const u32* off; u32 s0, s1, dst, blk0; };
 void unpack_slices(const UnpackSlice* sl, int ns, u32 nblk, int kw, int S, u32 fmask, u64* lo, u64* hi, u64* st,
                    cudaStream_t stream);

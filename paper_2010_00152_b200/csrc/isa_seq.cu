@@ -463,6 +463,318 @@ __global__ void __launch_bounds__(SQ_THREADS, 1) k_seq_rungen(
   }
 }
 
+// ============================================ cut-then-aggregate RSW ====
+// Read-sort-write empties the index at every flush (evict_all,
+// sortagg.py:333-351), so every fill cycle starts from an empty table and
+// its end depends on the keys alone: cycle i is [f_i, f_{i+1}) where
+// f_{i+1} is the first row at which the (M + 1)-th distinct key of the
+// cycle appears (memindex.py:230-231).  With a small budget the cycles are
+// short, so instead of one host round trip per cycle:
+//
+//   k_cut_scan (one CTA): walks the keys in batches of 1,024 rows with a
+//     shared-memory hash set of the cycle's keys (slot -> first row, lowered
+//     with atomicMin, so a row is "new" iff it is its key's first row in the
+//     cycle), counts new keys in row order (block scan) and cuts at the
+//     (M - count + 1)-th new key of the batch; the table is then cleared and
+//     the scan resumes at the cut row.  It stops at the first cycle that
+//     grows past CUT_GIVEUP rows (the chunked path takes over from that
+//     cycle's first row, with an empty table: exact);
+//   k_cut_runs (one CTA per cycle, all cycles in parallel): sorts the
+//     cycle's rows by key in shared memory (stable LSD on the varying key
+//     bits, positions as payload), combines every key segment's rows in row
+//     order (the reference's combine order) and writes the run: exactly M
+//     groups for a flushed cycle, the residue for the last one.
+#define CUT_THREADS 1024
+#define CUT_WARPS (CUT_THREADS / 32)
+#define CUT_R 4                               // rows per thread per batch (contiguous: scan order = row order)
+#define CUT_B (CUT_THREADS * CUT_R)           // batch rows
+#define CUT_CAP 12288                         // rows of one cycle sorted in shared memory
+#define CUT_GIVEUP (CUT_CAP - CUT_B)          // a cycle longer than this hands over to the chunked path
+#define CR_THREADS 256
+#define CR_WARPS (CR_THREADS / 32)
+
+struct CutOut {
+  u32 ncuts;     // flushed cycles found
+  u32 stop;      // first row not covered (n: the scan reached the end)
+  u32 batches;   // batch passes (a batch holding a cut is passed again from the cut row)
+  u32 overflow;  // cut directory capacity exceeded
+};
+
+__device__ __forceinline__ u32 cut_hash(u64 k, int hbits) {
+  k ^= k >> 31;
+  k *= 0x9E3779B97F4A7C15ull;
+  return (u32)(k >> (64 - hbits));
+}
+
+// cuts[0] = 0, cuts[1..ncuts] = flush rows, cuts[ncuts + 1] = stop.  A
+// batch that holds a cut is passed again with the table cleared and only
+// its rows from the cut on (they are still in registers), so the batches
+// stay aligned and every row is loaded once.
+__global__ void __launch_bounds__(CUT_THREADS, 1) k_cut_scan(KeyDesc kd, u32 n, u32 M, int hbits,
+                                                             u32* __restrict__ cuts, u32 max_cuts,
+                                                             CutOut* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const u32 HS = 1u << hbits, mask = HS - 1;
+  unsigned long long* hkey = (unsigned long long*)smem;   // [HS + 1] (slot HS: the all-ones key)
+  u32* hfirst = (u32*)(hkey + HS + 1);                    // [HS + 1] first row of the slot's key
+  __shared__ u32 wsum[CUT_WARPS];
+  __shared__ u32 s_f;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const unsigned long long EMPTY = ~0ull;
+  for (u32 i = tid; i <= HS; i += CUT_THREADS) { hkey[i] = EMPTY; hfirst[i] = 0xFFFFFFFFu; }
+  __syncthreads();
+  u32 pos = 0, seg0 = 0, cnt = 0, ncuts = 0, batches = 0;
+  u64 nk[CUT_R];   // the next batch's keys (loaded one batch ahead)
+#pragma unroll
+  for (int j = 0; j < CUT_R; ++j) {
+    const u32 r = tid * CUT_R + j;
+    u64 hi;
+    nk[j] = 0;
+    if (r < n) load_key(kd, (i64)r, hi, nk[j]);
+  }
+  while (pos < n) {
+    u64 k[CUT_R];
+#pragma unroll
+    for (int j = 0; j < CUT_R; ++j) {
+      k[j] = nk[j];
+      const u32 r2 = pos + CUT_B + tid * CUT_R + j;
+      u64 hi;
+      if (r2 < n) load_key(kd, (i64)r2, hi, nk[j]);
+    }
+    const u32 r0 = pos + tid * CUT_R;   // this thread's first row
+    u32 lo_row = pos;                   // rows below it belong to the cycle closed in this batch
+    for (;;) {
+      ++batches;
+      u32 s[CUT_R];
+#pragma unroll
+      for (int j = 0; j < CUT_R; ++j) {
+        const u32 r = r0 + j;
+        s[j] = HS;
+        if (r < n && r >= lo_row) {
+          if (k[j] != EMPTY) {
+            u32 q = cut_hash(k[j], hbits);
+            for (;;) {
+              const unsigned long long old = atomicCAS(hkey + q, EMPTY, (unsigned long long)k[j]);
+              if (old == EMPTY || old == k[j]) break;
+              q = (q + 1) & mask;
+            }
+            s[j] = q;
+          }
+          atomicMin(hfirst + s[j], r);
+        }
+      }
+      __syncthreads();
+      u32 nm = 0;   // bit j: row r0 + j is its key's first row in the cycle
+#pragma unroll
+      for (int j = 0; j < CUT_R; ++j) {
+        const u32 r = r0 + j;
+        if (r < n && r >= lo_row && hfirst[s[j]] == r) nm |= 1u << j;
+      }
+      const u32 c = __popc(nm);
+      u32 x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) wsum[w] = x;
+      __syncthreads();
+      if (w == 0) {
+        u32 t = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const u32 y = __shfl_up_sync(0xffffffffu, t, o);
+          if (lane >= o) t += y;
+        }
+        wsum[lane] = t;   // inclusive over warps
+      }
+      __syncthreads();
+      const u32 total = wsum[CUT_WARPS - 1];
+      if (cnt + total <= M) {
+        cnt += total;
+        __syncthreads();   // wsum is rewritten by the next pass
+        break;
+      }
+      // the (M - cnt + 1)-th new key of the pass is the flush row
+      const u32 kth = M - cnt;
+      const u32 excl = (w ? wsum[w - 1] : 0) + x - c;
+      if (kth >= excl && kth < excl + c) {
+        u32 m = nm;
+        for (u32 q = excl; q < kth; ++q) m &= m - 1;
+        s_f = r0 + (__ffs(m) - 1);
+      }
+      __syncthreads();
+      const u32 f = s_f;
+      if (tid == 0) {
+        if (ncuts + 2 < max_cuts) cuts[ncuts + 1] = f;
+        else out->overflow = 1;
+      }
+      ++ncuts;
+      for (u32 i = tid; i <= HS; i += CUT_THREADS) { hkey[i] = EMPTY; hfirst[i] = 0xFFFFFFFFu; }
+      cnt = 0;
+      seg0 = f;
+      lo_row = f;
+      __syncthreads();
+    }
+    pos += CUT_B;
+    if (pos < n && pos - seg0 > CUT_GIVEUP) break;   // this cycle is long: the chunked path takes it
+  }
+  const u32 stop = pos >= n ? n : seg0;
+  if (tid == 0) {
+    cuts[0] = 0;
+    if (ncuts + 2 <= max_cuts) cuts[ncuts + 1] = stop;
+    out->ncuts = ncuts;
+    out->stop = stop;
+    out->batches = batches;
+  }
+}
+
+size_t cut_scan_smem(int hbits) { return ((size_t)1 << hbits) * 12 + 16 + 64; }
+
+// one CTA per cycle [cuts[c], cuts[c + 1]): sorted, combined run at run_lo/run_st + c * M
+template <int MS>
+__global__ void __launch_bounds__(CR_THREADS, 1) k_cut_runs(KeyDesc kd, SlotDesc sd, const u32* __restrict__ cuts,
+                                                            u32 M, u64* __restrict__ run_lo,
+                                                            u64* __restrict__ run_st, u32* __restrict__ run_len) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  u64* key = (u64*)smem;                                  // [CUT_CAP] row order
+  unsigned short* o0 = (unsigned short*)(key + CUT_CAP);  // [CUT_CAP]
+  unsigned short* o1 = o0 + CUT_CAP;                      // [CUT_CAP]
+  u32* scratch = (u32*)(o1 + CUT_CAP);                    // [CUT_CAP]
+  u32* wcnt = scratch + CUT_CAP;                          // [CR_WARPS][256]
+  u32* dstart = wcnt + CR_WARPS * 256;                    // [256]
+  __shared__ u32 sw[CR_WARPS + 1];
+  __shared__ unsigned long long s_or;
+  const int S = sd.nslots;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const u32 c = blockIdx.x;
+  const u32 r0 = cuts[c], n = cuts[c + 1] - r0;   // 1 <= n <= CUT_CAP
+  u64 kor = 0;
+  u64 k0;
+  {
+    u64 hi;
+    load_key(kd, (i64)r0, hi, k0);
+  }
+  for (u32 i = tid; i < n; i += CR_THREADS) {
+    u64 hi, lo;
+    load_key(kd, (i64)(r0 + i), hi, lo);
+    key[i] = lo;
+    o0[i] = (unsigned short)i;
+    kor |= lo ^ k0;
+  }
+  for (int o = 16; o; o >>= 1) kor |= __shfl_xor_sync(0xffffffffu, kor, o);
+  if (tid == 0) s_or = 0;
+  __syncthreads();
+  if (lane == 0 && kor) atomicOr(&s_or, (unsigned long long)kor);
+  __syncthreads();
+  const int bits = s_or ? 64 - __clzll((long long)s_or) : 0;
+  // stable LSD passes over the varying bits: positions move, keys stay
+  const u32 WI = (((n + CR_WARPS - 1) / CR_WARPS) + 31) & ~31u;
+  const u32 lt = lanemask_lt();
+  unsigned short* cur = o0;
+  unsigned short* nxt = o1;
+  const u32 a0 = w * WI, a1 = min(n, a0 + WI);
+  for (int sft = 0; sft < bits; sft += 8) {
+    for (int q = lane; q < 256; q += 32) wcnt[w * 256 + q] = 0;
+    __syncwarp();
+    for (u32 i = a0 + lane; a0 < a1 && i < ((a1 + 31) & ~31u); i += 32) {
+      const bool valid = i < a1;
+      const u32 d = valid ? (u32)(key[cur[i]] >> sft) & 0xFFu : 256 + lane;
+      const u32 peers = __match_any_sync(0xffffffffu, d);
+      const int leader = __ffs(peers) - 1;
+      u32 cn = 0;
+      if (valid && lane == leader) {
+        cn = wcnt[w * 256 + d];
+        wcnt[w * 256 + d] = cn + __popc(peers);
+      }
+      cn = __shfl_sync(0xffffffffu, cn, leader);
+      if (valid) scratch[i] = (d << 16) | (cn + __popc(peers & lt));
+      __syncwarp();
+    }
+    __syncthreads();
+    {
+      u32 run = 0;
+#pragma unroll
+      for (int ww = 0; ww < CR_WARPS; ++ww) {
+        const u32 x = wcnt[ww * 256 + tid];
+        wcnt[ww * 256 + tid] = run;
+        run += x;
+      }
+      u32 tot;
+      dstart[tid] = block_excl_scan256(run, sw, &tot);
+    }
+    __syncthreads();
+    for (u32 i = a0 + lane; i < a1; i += 32) {
+      const u32 v = scratch[i], d = v >> 16;
+      nxt[dstart[d] + wcnt[w * 256 + d] + (v & 0xFFFFu)] = cur[i];
+    }
+    __syncthreads();
+    unsigned short* t = cur; cur = nxt; nxt = t;
+  }
+  // group heads in sorted order; thread t owns sorted positions [i0, i1)
+  const u32 per = (n + CR_THREADS - 1) / CR_THREADS;
+  const u32 i0 = min(n, tid * per), i1 = min(n, i0 + per);
+  u32 heads = 0;
+  for (u32 i = i0; i < i1; ++i) heads += i == 0 || key[cur[i]] != key[cur[i - 1]];
+  u32 tot;
+  u32 g = block_excl_scan256(heads, sw, &tot);
+  u64* olo = run_lo + (size_t)c * M;
+  u64* ost = run_st + (size_t)c * M * S;
+  for (u32 i = i0; i < i1; ++i) {
+    const u64 k = key[cur[i]];
+    if (i != 0 && k == key[cur[i - 1]]) continue;
+    u64 acc[MS];
+    load_state_row<MS>(sd, (i64)r0, nullptr, cur[i], acc);
+    for (u32 j = i + 1; j < n && key[cur[j]] == k; ++j) {
+      u64 v[MS];
+      load_state_row<MS>(sd, (i64)r0, nullptr, cur[j], v);
+#pragma unroll
+      for (int q = 0; q < MS; ++q)
+        if (q < S) acc[q] = combine_slot(sd.op[q], sd.type[q], acc[q], v[q]);
+    }
+    olo[g] = k;
+#pragma unroll
+    for (int q = 0; q < MS; ++q)
+      if (q < S) ost[(size_t)g * S + q] = acc[q];
+    ++g;
+  }
+  if (tid == 0) run_len[c] = tot;
+}
+
+size_t cut_runs_smem() { return (size_t)CUT_CAP * (8 + 2 + 2 + 4) + (CR_WARPS * 256 + 256) * 4 + 64; }
+
+bool cut_supported(int KW, int S, int64_t M) { return KW == 1 && S <= 8 && M >= 1 && M <= SQ_MAX_M; }
+
+int cut_hash_bits(u32 M) {
+  int b = 10;
+  while (((u64)1 << b) < (u64)2 * (M + CUT_B)) ++b;   // load <= 1/2 with a full batch of new keys
+  return b;
+}
+
+void cut_scan(const KeyDesc& kd, u32 n, u32 M, u32* cuts, u32 max_cuts, void* out, cudaStream_t st) {
+  const int hb = cut_hash_bits(M);
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr))
+    cudaFuncSetAttribute(k_cut_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  klaunch(k_cut_scan, 1, CUT_THREADS, cut_scan_smem(hb), st, kd, n, M, hb, cuts, max_cuts, (CutOut*)out);
+}
+
+void cut_runs(const KeyDesc& kd, const SlotDesc& sd, const u32* cuts, u32 ncycles, u32 M, u64* run_lo, u64* run_st,
+              u32* run_len, cudaStream_t st) {
+  if (!ncycles) return;
+  const int S = sd.nslots;
+  const size_t smem = cut_runs_smem();
+#define CR_GO(MSV)                                                                                        \
+  do {                                                                                                    \
+    static std::atomic<unsigned long long> attr{0};                                                       \
+    if (first_on_device(attr))                                                                            \
+      cudaFuncSetAttribute(k_cut_runs<MSV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
+    klaunch(k_cut_runs<MSV>, ncycles, CR_THREADS, smem, st, kd, sd, cuts, M, run_lo, run_st, run_len);    \
+  } while (0)
+  if (S <= 1) CR_GO(1); else if (S <= 2) CR_GO(2); else if (S <= 4) CR_GO(4); else CR_GO(8);
+#undef CR_GO
+}
+
 size_t seq_smem(int M, bool rs) {
   return (size_t)SQ_CH * 8 * 2 + (size_t)M * 8 * (rs ? 3 : 2) + (size_t)SQ_CH * 2 * 2 + (size_t)SQ_CH * 4 * 2 +
          (size_t)SQ_WARPS * 256 * 4 + 256 * 4 + SQ_CH / 8 + 64;

@@ -42,7 +42,7 @@ def _cfg(memory, page, **kw):
 @pytest.mark.parametrize("name", golden_names())
 @pytest.mark.parametrize("variant", ["device", "host_input", "hbm_runs", "packed_runs", "host_runs", "small_chunks",
                                      "k1_always", "k1_never", "tile_merge", "radix_merge", "one_cta",
-                                     "window_round_trips"])
+                                     "window_round_trips", "chunk_loop"])
 def test_golden_columns(name, variant, monkeypatch):
     g = Golden(name)
     if variant in ("tile_merge", "radix_merge"):   # force either wide-merge path
@@ -51,6 +51,8 @@ def test_golden_columns(name, variant, monkeypatch):
         monkeypatch.setenv("ISA_SEQ", "1")
     if variant == "window_round_trips":   # wide merge reading every window's group count back (no device base)
         monkeypatch.setenv("ISA_DIRECT_MERGE", "0")
+    if variant == "chunk_loop":   # small budgets through the chunked loop instead of cut-then-aggregate
+        monkeypatch.setenv("ISA_CUT", "0")
     sch = g.schema()
     kw = {}
     if variant == "hbm_runs":
@@ -67,7 +69,8 @@ def test_golden_columns(name, variant, monkeypatch):
         kw.update(preaggregate="never")
     mode = str(g.z["merge_mode"]) if "merge_mode" in g.z else "wide"
     if mode != "wide" and variant in ("k1_always", "k1_never", "small_chunks", "packed_runs", "host_runs",
-                                      "tile_merge", "radix_merge", "one_cta", "window_round_trips"):
+                                      "tile_merge", "radix_merge", "one_cta", "window_round_trips",
+                                      "chunk_loop"):
         pytest.skip("pre-aggregation / chunking knobs apply to the wide path only")
     op = isa.SortAggregate(sch, _cfg(g.memory, g.page, merge_mode=mode, **kw))
     n = len(g.keys[0])
@@ -780,3 +783,69 @@ def test_direct_window_merge_many_windows_vs_oracle(cfg, rows, memory, window, m
     w = workloads.make(cfg, rows=rows, device="cpu", **kw)
     op = _oracle_case(w, memory, page=100, rel=1e-5 if cfg == 3 else 1e-9, merge_window_rows=window)
     assert op.device_ledger["merge_windows"] > 10
+
+
+def _mixed_cycles_input(n_short, n_long, short_domain, long_domain, seed, float_vals=False):
+    """Rows whose first part flushes every few thousand rows (large key
+    domain) and whose second part holds few keys (fill cycles far longer
+    than one CTA sorts): the cut-then-aggregate scan hands over to the
+    chunked loop at the first long cycle."""
+    rng = np.random.default_rng(seed)
+    k = np.concatenate([rng.integers(0, short_domain, n_short), rng.integers(0, long_domain, n_long)])
+    k = k.astype(np.uint32)
+    if float_vals:
+        v = rng.uniform(-1e5, 1e5, len(k))
+    else:
+        v = rng.integers(-1_000_000, 1_000_001, len(k)).astype(np.int64)
+    return k, v
+
+
+def _cut_schema(float_vals=False):
+    from paper_2010_00152_b200.core import AggregateKind, AggregateSpec, ColumnSpec, Schema
+    return Schema([ColumnSpec("k")], [AggregateSpec("n", AggregateKind.COUNT, None),
+                                      AggregateSpec("s", AggregateKind.SUM, "v"),
+                                      AggregateSpec("lo", AggregateKind.MIN, "v"),
+                                      AggregateSpec("hi", AggregateKind.MAX, "v")])
+
+
+@pytest.mark.parametrize("n_short,n_long,short_domain,long_domain,memory", [
+    (1_000_000, 0, 10_000, 1, 4096),          # config-1 shape: 190 short cycles, all through the cut scan
+    (300_000, 200_000, 50_000, 3000, 4096),   # short cycles, then one long cycle: hand-over to the chunked loop
+    (200_000, 0, 300, 1, 64),                 # tiny budget: a flush every ~70 rows
+    (100_000, 300_000, 20_000, 40, 1000),     # hand-over, then no further flush
+    (5000, 0, 100, 1, 4096),                  # no flush at all: the one cycle is the result
+    (50_000, 0, 1 << 31, 1, 2),               # distinct keys, M = 2: three rows per cycle
+])
+@pytest.mark.parametrize("on_host", [False, True])
+@pytest.mark.parametrize("float_vals", [False, True])
+def test_cut_then_aggregate_vs_c_oracle(n_short, n_long, short_domain, long_domain, memory, on_host, float_vals):
+    """Small-budget read-sort-write through the cut scan + per-cycle runs:
+    output, fill cycles, run sizes and spilled rows equal the C restatement
+    (oracle/rsw_oracle.c) on inputs with short cycles, long cycles and the
+    hand-over between them."""
+    k, v = _mixed_cycles_input(n_short, n_long, short_domain, long_domain, 7 + memory, float_vals)
+    sch = _cut_schema(float_vals)
+    slots = oracle.make_states(sch, {"v": v}, len(k))
+    ok, os_, led, cycles = oracle.rsw_sortagg([k], slots, oracle.slot_ops(sch), memory, min(100, memory // 2))
+    op = isa.SortAggregate(sch, _cfg(memory, min(100, memory // 2)))
+    if on_host:
+        res = op.execute_columns([torch.from_numpy(k).pin_memory()], {"v": torch.from_numpy(v).pin_memory()})
+    else:
+        res = op.execute_columns([_cuda(k)], {"v": _cuda(v)})
+    _check(res, ok, os_)
+    assert op.cycles == [c for c in cycles if c > 0]
+    assert op.ledger.rows_spilled == led["rows_spilled"] and op.runs_after_generation == led["runs"]
+
+
+def test_config1_cut_then_aggregate_launches():
+    """BASELINE config 1 through the default path: the whole run generation is
+    the cut scan + one per-cycle-run launch (plus the wide merge), not a few
+    launches per fill cycle; the ledger equals the C oracle's."""
+    w = workloads.config1(device="cpu")
+    keys_np = [k.numpy() for k in w.keys]
+    slots = oracle.make_states(w.schema, {k: v.numpy() for k, v in w.values.items()}, w.rows)
+    _, _, led, cycles = oracle.rsw_sortagg(keys_np, slots, oracle.slot_ops(w.schema), 4096, 100)
+    op = _oracle_case(w, 4096, page=100)
+    assert op.cycles == [c for c in cycles if c > 0]
+    assert op.ledger.rows_spilled == led["rows_spilled"] and op.runs_after_generation == led["runs"]
+    assert op.device_ledger["kernel_launches"] < 100
