@@ -270,6 +270,23 @@ ISA_API int isa_set_spill_dir(isa_handle* h, const char* dir, int64_t first_run_
 ISA_API int isa_result_copy(isa_handle* h, void* const* key_out, void* const* slot_out,
                     int32_t out_on_host, void* stream);
 
+/* Output allocator.  The reference hands the caller fresh result rows it owns
+ * (SortAggregate.execute, sortagg.py:744-757); here the caller owns the
+ * output columns too: `fn(user, capacity, key_out, slot_out)` is called at
+ * most once per isa_execute -- only with host input that spilled, right
+ * before the wide merge -- and fills key_out[i] / slot_out[s] with pinned
+ * host columns of `capacity` elements (key columns in their input dtype,
+ * slots 8 bytes), returning 0 (nonzero: decline).  The wide merge then writes
+ * every merged key-range window's groups straight into them over PCIe while
+ * the next window merges (sortagg.py:588-674 yields rows as the merge
+ * advances).  isa_result_streamed() == 1 after isa_execute means the columns
+ * hold rows [0, n_groups) and isa_result_copy is not needed; 0 (no spill,
+ * device input, declined, or more groups than `capacity`): read the result
+ * with isa_result_copy as usual.  fn = NULL removes the allocator. */
+typedef int (*isa_alloc_fn)(void* user, int64_t capacity, void** key_out, void** slot_out);
+ISA_API int isa_set_output_allocator(isa_handle* h, isa_alloc_fn fn, void* user);
+ISA_API int isa_result_streamed(isa_handle* h);
+
 ISA_API int isa_metrics(isa_handle* h, isa_ledger* out);
 /* Read-sort-write fill-cycle lengths of the last execute (rows per cycle). */
 ISA_API int64_t isa_cycles(isa_handle* h, int64_t* out, int64_t cap);

@@ -50,7 +50,7 @@ EXPORTED_SYMBOLS = (
     "isa_sample_keys", "isa_partition", "isa_phase_stats", "isa_launch_count", "isa_steps",
     "isa_set_spill_dir", "isa_in_stream_aggregate", "isa_hash_aggregate", "isa_merge_intersect", "isa_partition_counts",
     "isa_scatter_to_peers", "isa_ipc_handle", "isa_ipc_open", "isa_ipc_close",
-    "isa_set_kernel_timing", "isa_kernel_stats",
+    "isa_set_kernel_timing", "isa_kernel_stats", "isa_set_output_allocator", "isa_result_streamed",
 )
 
 # isa_kernel_family (kernel-true roofline families)
@@ -184,6 +184,10 @@ def load():
     lib.isa_ipc_close.argtypes = [vp]
     lib.isa_set_spill_dir.restype = ctypes.c_int
     lib.isa_set_spill_dir.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64]
+    lib.isa_set_output_allocator.restype = ctypes.c_int
+    lib.isa_set_output_allocator.argtypes = [vp, ALLOC_FN, vp]
+    lib.isa_result_streamed.restype = ctypes.c_int
+    lib.isa_result_streamed.argtypes = [vp]
     lib.isa_metrics.restype = ctypes.c_int
     lib.isa_metrics.argtypes = [vp, ctypes.POINTER(IsaLedger)]
     lib.isa_cycles.restype = ctypes.c_int64
@@ -236,6 +240,11 @@ def kernel_stats():
 def phases_dict(arr):
     return {name: {"ms": arr[i].ms, "calls": arr[i].calls, "rows": arr[i].rows, "bytes": arr[i].bytes}
             for i, name in enumerate(PHASES)}
+
+
+# isa_alloc_fn: int fn(void* user, int64_t capacity, void** key_out, void** slot_out)
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p),
+                            ctypes.POINTER(ctypes.c_void_p))
 
 
 def _ptr_array(ptrs):
@@ -311,6 +320,34 @@ class Handle:
 
     def set_spill_dir(self, directory, first_run_id):
         self._check(self._lib.isa_set_spill_dir(self._h, os.fsencode(directory), int(first_run_id)))
+
+    def set_output_allocator(self, fn):
+        """``fn(capacity) -> (key_ptrs, slot_ptrs)`` (or None to decline) is
+        called by the native wide merge for the caller-owned output columns;
+        ``None`` removes the allocator."""
+        if fn is None:
+            self._alloc_cb = None
+            self._check(self._lib.isa_set_output_allocator(self._h, ctypes.cast(None, ALLOC_FN), None))
+            return
+
+        def cb(_user, capacity, key_out, slot_out):
+            try:
+                ptrs = fn(int(capacity))
+                if ptrs is None:
+                    return 1
+                for i, p in enumerate(ptrs[0]):
+                    key_out[i] = p
+                for i, p in enumerate(ptrs[1]):
+                    slot_out[i] = p
+                return 0
+            except Exception:   # an allocation failure must not unwind through the C frames
+                return 1
+
+        self._alloc_cb = ALLOC_FN(cb)   # keep the thunk alive while the handle may call it
+        self._check(self._lib.isa_set_output_allocator(self._h, self._alloc_cb, None))
+
+    def result_streamed(self):
+        return bool(self._lib.isa_result_streamed(self._h))
 
     def result_copy(self, key_ptrs, slot_ptrs, on_host, stream):
         self._check(self._lib.isa_result_copy(self._h, _ptr_array(key_ptrs), _ptr_array(slot_ptrs),

@@ -401,6 +401,19 @@ struct Engine {
   isa_ledger led;
   std::vector<int64_t> cycles;
 
+  // Output columns allocated by the caller (isa_set_output_allocator): with
+  // host input the wide merge streams every window's groups into them over
+  // PCIe while the next window merges, instead of a device-side export and
+  // one device -> host copy per column after the merge.
+  isa_alloc_fn out_alloc = nullptr;
+  void* out_user = nullptr;
+  cudaStream_t xs = nullptr;
+  cudaEvent_t xs_ev = nullptr;
+  DevBuf exp_cnt;             // result row count after every exported window
+  ExportDesc stream_ed;
+  bool streaming = false, streamed_ok = false;
+  u32 stream_cap = 0, stream_w = 0;
+
   Engine(const isa_config& c, const isa_schema& s) : cfg(c), sch(s) {
     validate();
     CK(cudaSetDevice(cfg.device));
@@ -474,6 +487,9 @@ struct Engine {
     if (h_hist) cudaFreeHost(h_hist);
     if (h2d) cudaStreamDestroy(h2d);
     if (d2h) cudaStreamDestroy(d2h);
+    if (xs) cudaStreamDestroy(xs);
+    if (xs_ev) cudaEventDestroy(xs_ev);
+    exp_cnt.release();
     if (spill_done) cudaEventDestroy(spill_done);
     for (int i = 0; i < 2; ++i) {
       if (stg_ready[i]) cudaEventDestroy(stg_ready[i]);
@@ -2089,7 +2105,14 @@ struct Engine {
     if (dir_mode) {
       ub = direct->n;
       CK(cudaMemcpyAsync(dscal32(25), &direct->n, sizeof(u32), cudaMemcpyHostToDevice, st));
+      if (streaming) {
+        exp_cnt.ensure((size_t)(nwin + 2) * sizeof(u32));
+        CK(cudaMemcpyAsync(exp_cnt.p, &direct->n, sizeof(u32), cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(dscal32(30), 0, sizeof(u32), st));
+      }
       sync();
+    } else {
+      streaming = false;
     }
     const int smode = inplace ? 1 : 0;
     wrows[0] = stage(0, 0, smode);
@@ -2128,9 +2151,13 @@ struct Engine {
         if (ub + m > (int64_t)(direct->lo.bytes / 8)) {
           direct->n = read_u32(dscal32(25));
           ub = direct->n;
-          if (ub + m > (int64_t)(direct->lo.bytes / 8)) grow_table(*direct, (size_t)ub + m);
+          if (ub + m > (int64_t)(direct->lo.bytes / 8)) {
+            if (streaming) CK(cudaStreamSynchronize(xs));   // exports read the table that is about to move
+            grow_table(*direct, (size_t)ub + m);
+          }
         }
         collapse_direct(cur, m, stg_st[slot].as<u64>(), *direct, wl.second, wl.first);
+        if (streaming) stream_window(*direct);
         ub += m;
         CK(cudaEventRecord(stg_free[slot], st));
         continue;
@@ -2175,6 +2202,57 @@ struct Engine {
     ph_end(ISA_PH_WM_COLLAPSE, m, 0);
   }
 
+  // ---- streamed output (isa_set_output_allocator) ----
+  // The caller's allocator is asked once, before the first window, for
+  // columns of the estimated output size plus a margin (est = the
+  // OutputEstimator's inversion of the mean fill cycle, capped at the run
+  // rows); a result that outgrows them falls back to isa_result_copy.
+  void begin_stream(int64_t total, int64_t est) {
+    { const char* e = getenv("ISA_STREAM_OUT"); if (e && e[0] == '0') return; }   // A/B: isa_result_copy instead
+    const int64_t cap = std::min<int64_t>({total, est + est / 32 + 65536, (int64_t)0xFFFFFFF0ll});
+    void* kptr[ISA_MAX_KEY_COLS] = {nullptr};
+    void* sptr[ISA_MAX_SLOTS] = {nullptr};
+    if (out_alloc(out_user, cap, kptr, sptr) != 0) return;
+    memset(&stream_ed, 0, sizeof(stream_ed));
+    stream_ed.ncols = kd0.ncols;
+    stream_ed.nslots = S;
+    for (int c = 0; c < kd0.ncols; ++c) {
+      stream_ed.shift[c] = kd0.shift[c];
+      stream_ed.width[c] = kd0.width[c];
+      stream_ed.is_signed[c] = dtype_signed(kd0.dtype[c]) ? 1 : 0;
+      stream_ed.key_dst[c] = kptr[c];
+    }
+    for (int s = 0; s < S; ++s) stream_ed.slot_dst[s] = sptr[s];
+    if (!xs) {
+      int lo_pri = 0, hi_pri = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+      CK(cudaStreamCreateWithPriority(&xs, cudaStreamNonBlocking, hi_pri));
+      CK(cudaEventCreateWithFlags(&xs_ev, cudaEventDisableTiming));
+    }
+    stream_cap = (u32)cap;
+    stream_w = 0;
+    streaming = true;
+  }
+  // after a window collapsed into t (its new row count in *dscal32(26)):
+  // export rows [count before, count after) on the export stream
+  void stream_window(Table& t) {
+    CK(cudaMemcpyAsync(exp_cnt.as<u32>() + stream_w + 1, dscal32(26), sizeof(u32), cudaMemcpyDeviceToDevice, st));
+    CK(cudaEventRecord(xs_ev, st));
+    CK(cudaStreamWaitEvent(xs, xs_ev, 0));
+    kt_begin(KF_EXPORT, xs);
+    export_range(t.plo(), KW == 2 ? t.phi() : nullptr, t.pst(), exp_cnt.as<u32>() + stream_w,
+                 exp_cnt.as<u32>() + stream_w + 1, stream_cap, stream_ed, dscal32(30), 2 * num_sms, xs);
+    kt_end(KF_EXPORT, 0, xs);
+    ++stream_w;
+  }
+  void end_stream() {
+    CK(cudaStreamSynchronize(xs));
+    const u32 over = read_u32(dscal32(30));
+    streamed_ok = !over && result.n <= stream_cap;
+    if (streamed_ok) kt_add_bytes(KF_EXPORT, (int64_t)result.n * 2 * (8 * KW + 8 * S));
+    streaming = false;
+  }
+
   // Final wide merge of all runs into the result (sortagg.py:588-674)
   void wide_merge() {
     int64_t total = 0;
@@ -2186,9 +2264,11 @@ struct Engine {
     {   // room for the estimated output (grown when short)
       const int64_t est = estimate_groups(total);
       result.reserve(std::max<int64_t>(1, std::min<int64_t>(total, est + est / 16 + W)), KW, S);
+      if (out_alloc && in_on_host && !tiles && direct_merge_env()) begin_stream(total, est);
     }
     merge_runs(runs, true, [&](Table& w, u32) { append_result(w); }, tiles ? &tp : nullptr,
                direct_merge_env() ? &result : nullptr);
+    if (streaming) end_stream();
     if (cfg.run_tier == ISA_TIER_FILE && read_u32(dscal32(12)))
       throw IsaError(ISA_ERR_CORRUPTION, "page checksum mismatch");   // parse_page, runstore.py:132-142
     led.pages_read = led.pages_written;
@@ -2558,6 +2638,7 @@ struct Engine {
     dirpool.reset();
     in_n = n;
     in_on_host = on_host;
+    streaming = streamed_ok = false;
     for (int c = 0; c < sch.n_key_cols; ++c) in_keys[c] = key_cols[c];
     if (cfg.run_tier == ISA_TIER_AUTO) {
       size_t fr = 0, tot = 0;
@@ -2789,6 +2870,7 @@ struct Engine {
                     cudaStream_t stream) {
     CK(cudaSetDevice(dev));
     st = stream;
+    streaming = streamed_ok = false;
     memset(&led, 0, sizeof(led));
     memset(phases, 0, sizeof(phases));
     runs.clear();
@@ -2822,6 +2904,7 @@ struct Engine {
                          cudaStream_t stream) {
     CK(cudaSetDevice(dev));
     st = stream;
+    streaming = streamed_ok = false;
     memset(&led, 0, sizeof(led));
     memset(phases, 0, sizeof(phases));
     runs.clear();
@@ -3201,6 +3284,18 @@ int isa_result_copy(isa_handle* h, void* const* key_out, void* const* slot_out, 
   } catch (const std::exception& e) {
     return fail(h, e);
   }
+}
+
+int isa_set_output_allocator(isa_handle* h, isa_alloc_fn fn, void* user) {
+  if (!h) return ISA_ERR_CONTRACT;
+  h->eng->out_alloc = fn;
+  h->eng->out_user = user;
+  return ISA_OK;
+}
+
+int isa_result_streamed(isa_handle* h) {
+  if (!h) return 0;
+  return h->eng->streamed_ok ? 1 : 0;
 }
 
 int isa_metrics(isa_handle* h, isa_ledger* out) {

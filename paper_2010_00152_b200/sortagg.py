@@ -549,10 +549,35 @@ class SortAggregate:
         file_store = isinstance(self.store, FileStore)
         if file_store:
             h.set_spill_dir(self.store.directory, self.store._next)
-        # the native side selects the device itself; outputs name it explicitly
-        n_groups = h.execute(n, [k.data_ptr() for k in keys], [v.data_ptr() for v in vals], on_host, sptr)
+        # host input: the wide merge streams its windows into output columns
+        # this call allocates on request (isa_set_output_allocator), so the
+        # device -> host transfer overlaps the merge; the caller owns them
+        streamed = {}
+        if on_host:
+            torch = _torch()
+
+            def alloc(capacity):
+                ok = [torch.empty(capacity, dtype=k.dtype, pin_memory=True) for k in keys]
+                os_ = [torch.empty(capacity, dtype=torch.float64 if ty == _native.SLOT_F64 else torch.int64,
+                                   pin_memory=True) for (_, ty, _, _) in slots]
+                streamed["keys"], streamed["states"] = ok, os_
+                return [t.data_ptr() for t in ok], [t.data_ptr() for t in os_]
+
+            h.set_output_allocator(alloc)
+        try:
+            # the native side selects the device itself; outputs name it explicitly
+            n_groups = h.execute(n, [k.data_ptr() for k in keys], [v.data_ptr() for v in vals], on_host, sptr)
+        finally:
+            if on_host:
+                h.set_output_allocator(None)
         if file_store:
             self.run_ids = self.store._adopt(h.run_rows(), len(keys), len(slots), self.config.page_capacity)
+        self.streamed_output = bool(streamed) and h.result_streamed()
+        if self.streamed_output:
+            self._record(h, n, n_groups)
+            return ColumnarResult([t[:n_groups] for t in streamed["keys"]],
+                                  [t[:n_groups] for t in streamed["states"]])
+        streamed.clear()
         return self._collect(h, n, n_groups, keys, slots, on_host, sptr)
 
     def in_stream_columns(self, keys, values=None, *, states=False, stream=None):

@@ -849,3 +849,55 @@ def test_config1_cut_then_aggregate_launches():
     assert op.cycles == [c for c in cycles if c > 0]
     assert op.ledger.rows_spilled == led["rows_spilled"] and op.runs_after_generation == led["runs"]
     assert op.device_ledger["kernel_launches"] < 100
+
+
+@pytest.mark.parametrize("cfg,rows,memory,window", [(5, 3_000_000, 1 << 14, 50_000), (3, 2_000_000, 1 << 14, 40_000),
+                                                    (1, 1_000_000, 4096, 20_000), (5, 3_000_000, 1 << 18, 0)])
+def test_streamed_host_output_vs_oracle(cfg, rows, memory, window, monkeypatch):
+    """Host input that spills: the wide merge writes every window's groups
+    into caller-owned pinned columns (isa_set_output_allocator) while the next
+    window merges; the columns equal the oracle and the device-input result,
+    and the result is reported as streamed."""
+    monkeypatch.setenv("ISA_TILE_MERGE", "0")
+    kw = {"domain": 1 << 20} if cfg in (3, 5) else {}
+    w = workloads.make(cfg, rows=rows, device="cpu", **kw)
+    keys_np = [k.numpy() for k in w.keys]
+    slots = oracle.make_states(w.schema, {k: v.numpy() for k, v in w.values.items()}, w.rows)
+    want_keys, want_slots = oracle.reference_aggregate(keys_np, slots, oracle.slot_ops(w.schema))
+    op = isa.SortAggregate(w.schema, _cfg(memory, 100, merge_window_rows=window))
+    first = None
+    for _ in range(2):   # the second execute reuses the handle (fresh columns each time)
+        res = op.execute_columns([k.pin_memory() for k in w.keys], {k: v.pin_memory() for k, v in w.values.items()})
+        assert op.streamed_output
+        assert all(t.device.type == "cpu" and t.is_pinned() for t in list(res.keys) + list(res.states))
+        _check(res, want_keys, want_slots, rel=1e-5 if cfg == 3 else 1e-9)
+        if first is not None:   # the caller owns the first result: not overwritten by the second execute
+            assert all(a.data_ptr() != b.data_ptr() for a, b in zip(first.keys, res.keys))
+            _check(first, want_keys, want_slots, rel=1e-5 if cfg == 3 else 1e-9)
+        first = res
+    res = op.execute_columns([k.cuda() for k in w.keys], {k: v.cuda() for k, v in w.values.items()})
+    assert not op.streamed_output
+    _check(res, want_keys, want_slots, rel=1e-5 if cfg == 3 else 1e-9)
+
+
+def test_streamed_host_output_falls_back_when_the_estimate_is_short(monkeypatch):
+    """Long fill cycles first (few keys), then all-distinct keys: the output
+    estimate from the mean fill cycle is far below the real group count, the
+    streamed columns are too small, and the operator falls back to
+    isa_result_copy -- same result."""
+    monkeypatch.setenv("ISA_TILE_MERGE", "0")
+    rng = np.random.default_rng(11)
+    n1, n2, memory = 2_000_000, 400_000, 1 << 12
+    k = np.concatenate([rng.integers(0, memory + 40, n1), (1 << 20) + rng.permutation(n2)]).astype(np.int64)
+    v = rng.integers(0, 1000, len(k)).astype(np.int64)
+    sch = _cut_schema()
+    slots = oracle.make_states(sch, {"v": v}, len(k))
+    want_keys, want_slots = oracle.reference_aggregate([k], slots, oracle.slot_ops(sch))
+    op = isa.SortAggregate(sch, _cfg(memory, 100, merge_window_rows=30_000))
+    res = op.execute_columns([torch.from_numpy(k).pin_memory()], {"v": torch.from_numpy(v).pin_memory()})
+    _check(res, want_keys, want_slots)
+    assert not op.streamed_output
+    monkeypatch.setenv("ISA_STREAM_OUT", "0")   # the allocator path switched off: identical
+    op2 = isa.SortAggregate(sch, _cfg(memory, 100, merge_window_rows=30_000))
+    res2 = op2.execute_columns([torch.from_numpy(k).pin_memory()], {"v": torch.from_numpy(v).pin_memory()})
+    _check(res2, want_keys, want_slots)
