@@ -413,10 +413,14 @@ def measure(torch, dist, cfgno, rows_total, run_tier, steps, warmup, world, rank
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             secs = float(t.item())
         d2h = sum(o.numel() * o.element_size() for o in outs)
+        raw = op_e2e.phase_snapshot()
+        e2e_ph = {k: round(v["ms"], 2) for k, v in _native.phases_dict(raw).items() if v["ms"]} if raw is not None else {}
         out["e2e"] = {"value": rows * world / secs, "unit": "rows/s",
                       "h2d_bytes_per_step": rows * in_row_bytes,
                       "d2h_bytes_per_step": d2h, "ms_per_step": secs * 1e3,
-                      "timing": "CUDA events on the launching stream around synchronous execute_columns calls"}
+                      "timing": "CUDA events on the launching stream around synchronous execute_columns calls",
+                      "phases_ms_last_step": e2e_ph,
+                      "streamed_output": bool(getattr(op_e2e, "streamed_output", False))}
         outs = None
         del host_keys, host_vals
         op_e2e.close()

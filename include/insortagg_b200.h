@@ -273,13 +273,13 @@ ISA_API int isa_result_copy(isa_handle* h, void* const* key_out, void* const* sl
 /* Output allocator.  The reference hands the caller fresh result rows it owns
  * (SortAggregate.execute, sortagg.py:744-757); here the caller owns the
  * output columns too: `fn(user, capacity, key_out, slot_out)` is called at
- * most once per isa_execute -- only with host input that spilled, right
- * before the wide merge -- and fills key_out[i] / slot_out[s] with pinned
- * host columns of `capacity` elements (key columns in their input dtype,
- * slots 8 bytes), returning 0 (nonzero: decline).  The wide merge then writes
- * every merged key-range window's groups straight into them over PCIe while
- * the next window merges (sortagg.py:588-674 yields rows as the merge
- * advances).  isa_result_streamed() == 1 after isa_execute means the columns
+ * most once per isa_execute -- only with host input that spilled, once the
+ * wide merge's first key-range window is merged (capacity = the estimated
+ * output size plus a margin) -- and fills key_out[i] / slot_out[s] with
+ * pinned host columns of `capacity` elements (key columns in their input
+ * dtype, slots 8 bytes), returning 0 (nonzero: decline).  The wide merge then
+ * copies every merged window's groups into them while the next window merges
+ * (sortagg.py:588-674 yields rows as the merge advances).  isa_result_streamed() == 1 after isa_execute means the columns
  * hold rows [0, n_groups) and isa_result_copy is not needed; 0 (no spill,
  * device input, declined, or more groups than `capacity`): read the result
  * with isa_result_copy as usual.  fn = NULL removes the allocator. */

@@ -409,10 +409,9 @@ struct Engine {
   void* out_user = nullptr;
   cudaStream_t xs = nullptr;
   cudaEvent_t xs_ev = nullptr;
-  DevBuf exp_cnt;             // result row count after every exported window
   ExportDesc stream_ed;
   bool streaming = false, streamed_ok = false;
-  u32 stream_cap = 0, stream_w = 0;
+  u32 stream_cap = 0;
 
   Engine(const isa_config& c, const isa_schema& s) : cfg(c), sch(s) {
     validate();
@@ -489,7 +488,7 @@ struct Engine {
     if (d2h) cudaStreamDestroy(d2h);
     if (xs) cudaStreamDestroy(xs);
     if (xs_ev) cudaEventDestroy(xs_ev);
-    exp_cnt.release();
+    for (auto e : stream_cnt_ev) if (e) cudaEventDestroy(e);
     if (spill_done) cudaEventDestroy(spill_done);
     for (int i = 0; i < 2; ++i) {
       if (stg_ready[i]) cudaEventDestroy(stg_ready[i]);
@@ -2105,14 +2104,8 @@ struct Engine {
     if (dir_mode) {
       ub = direct->n;
       CK(cudaMemcpyAsync(dscal32(25), &direct->n, sizeof(u32), cudaMemcpyHostToDevice, st));
-      if (streaming) {
-        exp_cnt.ensure((size_t)(nwin + 2) * sizeof(u32));
-        CK(cudaMemcpyAsync(exp_cnt.p, &direct->n, sizeof(u32), cudaMemcpyHostToDevice, st));
-        CK(cudaMemsetAsync(dscal32(30), 0, sizeof(u32), st));
-      }
       sync();
-    } else {
-      streaming = false;
+      if (stream_want && direct->n == 0) stream_setup();
     }
     const int smode = inplace ? 1 : 0;
     wrows[0] = stage(0, 0, smode);
@@ -2152,12 +2145,12 @@ struct Engine {
           direct->n = read_u32(dscal32(25));
           ub = direct->n;
           if (ub + m > (int64_t)(direct->lo.bytes / 8)) {
-            if (streaming) CK(cudaStreamSynchronize(xs));   // exports read the table that is about to move
+            if (streaming) { stream_flush(nullptr); CK(cudaStreamSynchronize(xs)); }   // exports read the table that is about to move
             grow_table(*direct, (size_t)ub + m);
           }
         }
         collapse_direct(cur, m, stg_st[slot].as<u64>(), *direct, wl.second, wl.first);
-        if (streaming) stream_window(*direct);
+        if (streaming) stream_window(m);
         ub += m;
         CK(cudaEventRecord(stg_free[slot], st));
         continue;
@@ -2203,16 +2196,41 @@ struct Engine {
   }
 
   // ---- streamed output (isa_set_output_allocator) ----
-  // The caller's allocator is asked once, before the first window, for
-  // columns of the estimated output size plus a margin (est = the
-  // OutputEstimator's inversion of the mean fill cycle, capped at the run
-  // rows); a result that outgrows them falls back to isa_result_copy.
-  void begin_stream(int64_t total, int64_t est) {
-    { const char* e = getenv("ISA_STREAM_OUT"); if (e && e[0] == '0') return; }   // A/B: isa_result_copy instead
-    const int64_t cap = std::min<int64_t>({total, est + est / 32 + 65536, (int64_t)0xFFFFFFF0ll});
+  // Window w's groups leave for the caller's pinned columns while window
+  // w + 1 merges: its group count goes to mapped host memory right after its
+  // collapse (one word, written by a kernel), the host -- one window ahead
+  // with its enqueues, so the GPU never waits for it -- reads it once the
+  // collapse's event completed, and the export stream converts rows
+  // [count before, count after) into column slices (device staging) and
+  // copies them out with the copy engine.  The allocator is asked after the
+  // first window, for max(the OutputEstimator's inversion of the mean fill
+  // cycle, total run rows x the first window's groups / rows) plus a margin;
+  // a result that outgrows the columns falls back to isa_result_copy.
+  bool stream_want = false;
+  int64_t stream_total = 0, stream_est = 0, stream_rows0 = 0;
+  u32 stream_prev = 0;          // groups exported so far
+  int stream_pending = -1;      // h_scal slot of the window whose export is still to be issued
+  cudaEvent_t stream_cnt_ev[2] = {nullptr, nullptr};
+  void stream_setup() {
+    if (!xs) {
+      CK(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&xs_ev, cudaEventDisableTiming));
+      for (auto& e : stream_cnt_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    stream_prev = 0;
+    stream_pending = -1;
+    stream_rows0 = 0;
+    streaming = true;
+    stream_cap = 0;
+  }
+  bool stream_alloc(u32 groups0) {
+    int64_t est = stream_est;
+    if (stream_rows0 > 0)
+      est = std::max<int64_t>(est, (int64_t)((double)stream_total * (double)groups0 / (double)stream_rows0));
+    const int64_t cap = std::min<int64_t>({stream_total, est + est / 32 + 65536, (int64_t)0xFFFFFFF0ll});
     void* kptr[ISA_MAX_KEY_COLS] = {nullptr};
     void* sptr[ISA_MAX_SLOTS] = {nullptr};
-    if (out_alloc(out_user, cap, kptr, sptr) != 0) return;
+    if (out_alloc(out_user, cap, kptr, sptr) != 0) return false;
     memset(&stream_ed, 0, sizeof(stream_ed));
     stream_ed.ncols = kd0.ncols;
     stream_ed.nslots = S;
@@ -2223,33 +2241,57 @@ struct Engine {
       stream_ed.key_dst[c] = kptr[c];
     }
     for (int s = 0; s < S; ++s) stream_ed.slot_dst[s] = sptr[s];
-    if (!xs) {
-      int lo_pri = 0, hi_pri = 0;
-      CK(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
-      CK(cudaStreamCreateWithPriority(&xs, cudaStreamNonBlocking, hi_pri));
-      CK(cudaEventCreateWithFlags(&xs_ev, cudaEventDisableTiming));
-    }
     stream_cap = (u32)cap;
-    stream_w = 0;
-    streaming = true;
+    return true;
   }
-  // after a window collapsed into t (its new row count in *dscal32(26)):
-  // export rows [count before, count after) on the export stream
-  void stream_window(Table& t) {
-    CK(cudaMemcpyAsync(exp_cnt.as<u32>() + stream_w + 1, dscal32(26), sizeof(u32), cudaMemcpyDeviceToDevice, st));
-    CK(cudaEventRecord(xs_ev, st));
-    CK(cudaStreamWaitEvent(xs, xs_ev, 0));
+  // the window that just collapsed into the table: publish its count
+  void stream_window(u32 m) {
+    if (stream_rows0 == 0) stream_rows0 = m;
+    const int slot = stream_pending < 0 ? 0 : (stream_pending ^ 1);
+    stream_flush(nullptr);                        // the window before it (its count is complete by now)
+    to_host(dscal32(26), sizeof(u32), 100 + slot);
+    CK(cudaEventRecord(stream_cnt_ev[slot], st));
+    stream_pending = slot;
+  }
+  // issue the pending window's export; t: the table when it may have moved
+  void stream_flush(Table* moved) {
+    (void)moved;
+    if (stream_pending < 0 || !streaming) return;
+    const int slot = stream_pending;
+    stream_pending = -1;
+    CK(cudaEventSynchronize(stream_cnt_ev[slot]));
+    const u32 c1 = ((volatile u32*)h_scal)[100 + slot], c0 = stream_prev;
+    if (stream_cap == 0 && !stream_alloc(c1)) { streaming = false; return; }
+    if (c1 > stream_cap) { streaming = false; return; }   // the columns are too small: isa_result_copy
+    const u32 n = c1 - c0;
+    if (n == 0) return;
+    size_t off = 0;
+    ExportDesc ed = stream_ed;
+    std::vector<size_t> koff(kd0.ncols), soff(S);
+    for (int c = 0; c < kd0.ncols; ++c) { koff[c] = off; off += (((size_t)n * key_elem(c)) + 255) & ~(size_t)255; }
+    for (int s = 0; s < S; ++s) { soff[s] = off; off += (((size_t)n * 8) + 255) & ~(size_t)255; }
+    if (off + 256 > out_tmp.bytes) {
+      CK(cudaStreamSynchronize(xs));   // copies out of the staging area still in flight
+      out_tmp.ensure(off + off / 4 + 256);
+    }
+    for (int c = 0; c < kd0.ncols; ++c) ed.key_dst[c] = out_tmp.as<char>() + koff[c];
+    for (int s = 0; s < S; ++s) ed.slot_dst[s] = out_tmp.as<char>() + soff[s];
+    CK(cudaStreamWaitEvent(xs, stream_cnt_ev[slot], 0));
     kt_begin(KF_EXPORT, xs);
-    export_range(t.plo(), KW == 2 ? t.phi() : nullptr, t.pst(), exp_cnt.as<u32>() + stream_w,
-                 exp_cnt.as<u32>() + stream_w + 1, stream_cap, stream_ed, dscal32(30), 2 * num_sms, xs);
-    kt_end(KF_EXPORT, 0, xs);
-    ++stream_w;
+    export_all(result.plo() + c0, KW == 2 ? result.phi() + c0 : nullptr, result.pst() + (size_t)c0 * S, n, ed, xs);
+    kt_end(KF_EXPORT, (int64_t)n * 2 * (8 * KW + 8 * S), xs);
+    for (int c = 0; c < kd0.ncols; ++c)
+      CK(cudaMemcpyAsync((char*)stream_ed.key_dst[c] + (size_t)c0 * key_elem(c), out_tmp.as<char>() + koff[c],
+                         (size_t)n * key_elem(c), cudaMemcpyDeviceToHost, xs));
+    for (int s = 0; s < S; ++s)
+      CK(cudaMemcpyAsync((char*)stream_ed.slot_dst[s] + (size_t)c0 * 8, out_tmp.as<char>() + soff[s], (size_t)n * 8,
+                         cudaMemcpyDeviceToHost, xs));
+    stream_prev = c1;
   }
   void end_stream() {
+    stream_flush(nullptr);
     CK(cudaStreamSynchronize(xs));
-    const u32 over = read_u32(dscal32(30));
-    streamed_ok = !over && result.n <= stream_cap;
-    if (streamed_ok) kt_add_bytes(KF_EXPORT, (int64_t)result.n * 2 * (8 * KW + 8 * S));
+    streamed_ok = streaming && stream_cap > 0 && stream_prev == result.n;
     streaming = false;
   }
 
@@ -2264,11 +2306,15 @@ struct Engine {
     {   // room for the estimated output (grown when short)
       const int64_t est = estimate_groups(total);
       result.reserve(std::max<int64_t>(1, std::min<int64_t>(total, est + est / 16 + W)), KW, S);
-      if (out_alloc && in_on_host && !tiles && direct_merge_env()) begin_stream(total, est);
+      stream_want = out_alloc && in_on_host && !tiles && direct_merge_env();
+      { const char* e = getenv("ISA_STREAM_OUT"); if (e && e[0] == '0') stream_want = false; }   // A/B: isa_result_copy
+      stream_total = total;
+      stream_est = est;
     }
     merge_runs(runs, true, [&](Table& w, u32) { append_result(w); }, tiles ? &tp : nullptr,
                direct_merge_env() ? &result : nullptr);
     if (streaming) end_stream();
+    stream_want = false;
     if (cfg.run_tier == ISA_TIER_FILE && read_u32(dscal32(12)))
       throw IsaError(ISA_ERR_CORRUPTION, "page checksum mismatch");   // parse_page, runstore.py:132-142
     led.pages_read = led.pages_written;

@@ -2034,42 +2034,6 @@ void export_all(const u64* lo, const u64* hi, const u64* stt, u32 n, const Expor
   if (n) klaunch(k_export_all, grid_for(n, 256), 256, 0, st, lo, hi, stt, n, ed);
 }
 
-// Rows [*c0p, *c1p) of a result that grows window by window on the device
-// (both counts device-resident: no host round trip) into the caller's output
-// columns -- pinned host memory written from the SMs over PCIe (zero copy;
-// each warp stores 32 consecutive elements of a column), so the device ->
-// host transfer of window i overlaps the merge of window i + 1.  Rows at or
-// beyond `cap` (the output columns' capacity) are not written; *over is set.
-__global__ void __launch_bounds__(256) k_export_range(const u64* __restrict__ lo, const u64* __restrict__ hi,
-                                                      const u64* __restrict__ stt, const u32* __restrict__ c0p,
-                                                      const u32* __restrict__ c1p, u32 cap, ExportDesc ed,
-                                                      u32* __restrict__ over) {
-  const u32 c0 = *c0p, c1r = *c1p, c1 = min(c1r, cap);
-  if (c1r > cap && blockIdx.x == 0 && threadIdx.x == 0) *over = 1u;
-  for (u64 i = (u64)c0 + blockIdx.x * blockDim.x + threadIdx.x; i < c1; i += (u64)gridDim.x * blockDim.x) {
-    const u64 l = lo[i], h = hi ? hi[i] : 0;
-    for (int c = 0; c < ed.ncols; ++c) {
-      if (!ed.key_dst[c]) continue;
-      const int w = ed.width[c];
-      u64 f = key_field(h, l, ed.shift[c], w);
-      if (ed.is_signed[c]) f ^= (1ull << (w - 1));
-      switch (w) {
-        case 8: ((unsigned char*)ed.key_dst[c])[i] = (unsigned char)f; break;
-        case 16: ((unsigned short*)ed.key_dst[c])[i] = (unsigned short)f; break;
-        case 32: ((unsigned int*)ed.key_dst[c])[i] = (unsigned int)f; break;
-        default: ((u64*)ed.key_dst[c])[i] = f; break;
-      }
-    }
-    for (int s = 0; s < ed.nslots; ++s)
-      if (ed.slot_dst[s]) ((u64*)ed.slot_dst[s])[i] = stt[(size_t)i * ed.nslots + s];
-  }
-}
-
-void export_range(const u64* lo, const u64* hi, const u64* stt, const u32* c0p, const u32* c1p, u32 cap,
-                  const ExportDesc& ed, u32* over, int ctas, cudaStream_t st) {
-  klaunch(k_export_range, ctas, 256, 0, st, lo, hi, stt, c0p, c1p, cap, ed, over);
-}
-
 __global__ void k_export_slot(const u64* __restrict__ stt, int S, int s, u32 n, u64* __restrict__ out) {
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = stt[(size_t)i * S + s];
 }

@@ -296,9 +296,6 @@ struct ExportDesc {
 };
 // all key columns + all slots in one kernel (null destinations are skipped)
 void export_all(const u64* lo, const u64* hi, const u64* states, u32 n, const ExportDesc& ed, cudaStream_t st);
-// rows [*c0p, min(*c1p, cap)) (device-resident counts) into host-mapped columns; *over = 1 when *c1p > cap
-void export_range(const u64* lo, const u64* hi, const u64* states, const u32* c0p, const u32* c1p, u32 cap,
-                  const ExportDesc& ed, u32* over, int ctas, cudaStream_t st);
 
 // ---- partition (multi-GPU range split) -----------------------------------
 void sample_keys(const KeyDesc& kd, int64_t n, int64_t stride, u64* out_lo, u64* out_hi, cudaStream_t st);
