@@ -127,49 +127,41 @@ __device__ __forceinline__ void pkf_st(u64* p, u64 v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// NC = kw + S columns (template: the per-column min / max live in registers,
+// the staging loops carry no division by a runtime column count).
+template <int NC>
 __global__ void __launch_bounds__(PK_THREADS) k_pack_fused(PackSrc p, u64* __restrict__ status, u32 epoch,
                                                            u32* __restrict__ ticket, u32* __restrict__ blk_off,
                                                            char* __restrict__ out) {
-  extern __shared__ __align__(16) u64 stage[];   // [ncol][PK_ROWS]
-  __shared__ u64 s_mn[PK_THREADS / 32][PKF_MAXC], s_mx[PK_THREADS / 32][PKF_MAXC];
-  __shared__ u64 s_base[PKF_MAXC];
-  __shared__ u32 s_width[PKF_MAXC], s_woff[PKF_MAXC], s_b, s_off, s_bytes;
-  const int ncol = pk_ncol(p.kw, p.S);
+  extern __shared__ __align__(16) u64 stage[];   // [NC][PK_ROWS]
+  __shared__ u64 s_mn[PK_THREADS / 32][NC], s_mx[PK_THREADS / 32][NC];
+  __shared__ u64 s_base[NC];
+  __shared__ u32 s_width[NC], s_woff[NC], s_b, s_off, s_bytes;
+  const int kw = p.kw, S = NC - kw;
   const u32 nblk = (p.n + PK_ROWS - 1) / PK_ROWS;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) s_b = atomicAdd(ticket, 1u);
   __syncthreads();
   const u32 b = s_b, r0 = b * PK_ROWS;
   const u32 rows = min((u32)PK_ROWS, p.n - r0);
-  // 1. stage (transformed values)
-  for (u32 i = tid; i < rows; i += PK_THREADS) {
-    stage[i] = p.lo[r0 + i];
-    if (p.kw == 2) stage[PK_ROWS + i] = p.hi[r0 + i];
-  }
-  if (p.S) {
-    const u64* src = p.st + (size_t)r0 * p.S;
-    for (u32 j = tid; j < rows * (u32)p.S; j += PK_THREADS) {
-      const u32 i = j / p.S, s_ = j % p.S;
-      stage[(size_t)(p.kw + s_) * PK_ROWS + i] = pk_fwd(src[j], (p.fmask >> s_) & 1u, 0);
-    }
-  }
-  __syncthreads();
-  // 2. min / max of every column
-  u64 mn[PKF_MAXC], mx[PKF_MAXC];
+  // 1. stage the transformed values of every column, min / max on the way
+  u64 mn[NC], mx[NC];
 #pragma unroll
-  for (int c = 0; c < PKF_MAXC; ++c) { mn[c] = ~0ull; mx[c] = 0; }
+  for (int c = 0; c < NC; ++c) { mn[c] = ~0ull; mx[c] = 0; }
+  const u64* src = p.st + (size_t)r0 * S;
   for (u32 i = tid; i < rows; i += PK_THREADS) {
 #pragma unroll
-    for (int c = 0; c < PKF_MAXC; ++c) {
-      if (c < ncol) {
-        const u64 v = stage[(size_t)c * PK_ROWS + i];
-        mn[c] = v < mn[c] ? v : mn[c];
-        mx[c] = v > mx[c] ? v : mx[c];
-      }
+    for (int c = 0; c < NC; ++c) {
+      u64 v;
+      if (c < kw) v = c == 0 ? p.lo[r0 + i] : p.hi[r0 + i];
+      else v = pk_fwd(src[(size_t)i * S + (c - kw)], (p.fmask >> (c - kw)) & 1u, 0);
+      stage[c * PK_ROWS + i] = v;
+      mn[c] = v < mn[c] ? v : mn[c];
+      mx[c] = v > mx[c] ? v : mx[c];
     }
   }
 #pragma unroll
-  for (int c = 0; c < PKF_MAXC; ++c) {
+  for (int c = 0; c < NC; ++c) {
     for (int o = 16; o; o >>= 1) {
       const u64 a = __shfl_xor_sync(0xffffffffu, mn[c], o), z = __shfl_xor_sync(0xffffffffu, mx[c], o);
       mn[c] = a < mn[c] ? a : mn[c];
@@ -179,8 +171,8 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack_fused(PackSrc p, u64* __res
   }
   __syncthreads();
   if (tid == 0) {
-    u64 woff = 0;
-    for (int c = 0; c < ncol; ++c) {
+    u32 woff = 0;
+    for (int c = 0; c < NC; ++c) {
       u64 a = s_mn[0][c], z = s_mx[0][c];
       for (int ww = 1; ww < PK_THREADS / 32; ++ww) {
         a = s_mn[ww][c] < a ? s_mn[ww][c] : a;
@@ -189,13 +181,13 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack_fused(PackSrc p, u64* __res
       const u32 width = z == a ? 0u : (u32)(64 - __clzll((long long)(z - a)));
       s_base[c] = a;
       s_width[c] = width;
-      s_woff[c] = (u32)woff;
-      woff += ((u64)rows * width + 63) / 64;
+      s_woff[c] = woff;
+      woff += (rows * width + 63) / 64;
     }
-    s_bytes = (u32)((ncol * 2 + woff) * 8);
+    s_bytes = (NC * 2 + woff) * 8;
   }
   __syncthreads();
-  // 3. decoupled look-back over the previous blocks' byte counts, one warp:
+  // 2. decoupled look-back over the previous blocks' byte counts, one warp:
   //    32 predecessors per round trip
   if (w == 0) {
     const u32 bytes = s_bytes;
@@ -227,30 +219,30 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack_fused(PackSrc p, u64* __res
     }
   }
   __syncthreads();
-  // 4. header + payload at the block's offset
+  // 3. header + payload at the block's offset; one payload word per thread
+  //    step, bit positions in 32-bit arithmetic (rows * width <= 2^16)
   u64* blk = (u64*)(out + s_off);
-  if (tid < ncol) {
+  if (tid < NC) {
     blk[tid * 2] = s_base[tid];
     blk[tid * 2 + 1] = (u64)s_width[tid] | ((u64)s_woff[tid] << 8);
   }
-  u64* payload = blk + ncol * 2;
-  for (int c = 0; c < ncol; ++c) {
+  u64* payload = blk + NC * 2;
+#pragma unroll 1
+  for (int c = 0; c < NC; ++c) {
     const u32 width = s_width[c];
     if (width == 0) continue;
     const u64 base = s_base[c];
-    const u64* vals = stage + (size_t)c * PK_ROWS;
+    const u64* vals = stage + c * PK_ROWS;
     u64* wout = payload + s_woff[c];
-    const u32 nwords = (u32)(((u64)rows * width + 63) / 64);
+    const u32 nwords = (rows * width + 63) / 64;
     for (u32 q = tid; q < nwords; q += PK_THREADS) {
-      const u64 lo_bit = (u64)q * 64;
-      const u32 i0 = (u32)(lo_bit / width);
-      const u32 i1 = min(rows - 1, (u32)((lo_bit + 63) / width));
-      u64 word = 0;
-      for (u32 i = i0; i <= i1; ++i) {
-        const long long pos = (long long)((u64)i * width) - (long long)lo_bit;
-        const u64 v = vals[i] - base;
-        word |= pos >= 0 ? (v << pos) : (v >> (-pos));
-      }
+      const u32 lo_bit = q * 64;
+      const u32 i0 = lo_bit / width;
+      const u32 i1 = min(rows - 1, (lo_bit + 63) / width);
+      int pos = (int)(i0 * width) - (int)lo_bit;   // bit of value i0 in this word (<= 0)
+      u64 word = (vals[i0] - base) >> (-pos);
+      pos += (int)width;
+      for (u32 i = i0 + 1; i <= i1; ++i, pos += (int)width) word |= (vals[i] - base) << pos;
       wout[q] = word;
     }
   }
@@ -265,11 +257,19 @@ void pack_fused(const PackSrc& p, u64* status, u32* ticket, u32* blk_off, char* 
   if (!nb) return;
   const size_t smem = (size_t)pk_ncol(p.kw, p.S) * PK_ROWS * 8;
   static std::atomic<unsigned long long> attr{0};
-  if (first_on_device(attr))
-    cudaFuncSetAttribute(k_pack_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, PKF_MAXC * PK_ROWS * 8);
+  if (first_on_device(attr)) {
+#define PKF_ATTR(N) cudaFuncSetAttribute(k_pack_fused<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, N * PK_ROWS * 8)
+    PKF_ATTR(1); PKF_ATTR(2); PKF_ATTR(3); PKF_ATTR(4); PKF_ATTR(5); PKF_ATTR(6); PKF_ATTR(7); PKF_ATTR(8);
+#undef PKF_ATTR
+  }
   const u32 ep = (g_pk_epoch.fetch_add(1) % 0x3FFFFFFEu) + 1u;
   cudaMemsetAsync(ticket, 0, sizeof(u32), st);
-  klaunch(k_pack_fused, nb, PK_THREADS, smem, st, p, status, ep, ticket, blk_off, out);
+#define PKF_GO(N) case N: klaunch(k_pack_fused<N>, nb, PK_THREADS, smem, st, p, status, ep, ticket, blk_off, out); break
+  switch (pk_ncol(p.kw, p.S)) {
+    PKF_GO(1); PKF_GO(2); PKF_GO(3); PKF_GO(4); PKF_GO(5); PKF_GO(6); PKF_GO(7); PKF_GO(8);
+    default: break;
+  }
+#undef PKF_GO
 }
 
 u32 pack_blocks(u32 n) { return (n + PK_ROWS - 1) / PK_ROWS; }
@@ -319,12 +319,19 @@ __global__ void __launch_bounds__(PK_THREADS) k_unpack_slices(const UnpackSlice*
                                                               int kw, int S, u32 fmask, u64* __restrict__ lo,
                                                               u64* __restrict__ hi, u64* __restrict__ st) {
   const int ncol = pk_ncol(kw, S);
+  __shared__ u32 s_cnt;
   for (u32 q = blockIdx.x; q < nblk; q += gridDim.x) {
-    int l = 0, h = ns;   // last slice with blk0 <= q
-    while (h - l > 1) {
-      const int m = (l + h) >> 1;
-      if (sl[m].blk0 <= q) l = m; else h = m;
-    }
+    // last slice with blk0 <= q: counted by all threads at once (one memory
+    // round trip instead of a binary search's dependent chain)
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    u32 below = 0;
+    for (int t = threadIdx.x; t < ns; t += PK_THREADS) below += sl[t].blk0 <= q ? 1u : 0u;
+    for (int o = 16; o; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+    if ((threadIdx.x & 31) == 0 && below) atomicAdd(&s_cnt, below);
+    __syncthreads();
+    const int l = (int)s_cnt - 1;
+    __syncthreads();   // everyone has read the count before the next block resets it
     const UnpackSlice u = sl[l];
     const u32 b = u.s0 / PK_ROWS + (q - u.blk0);
     const u32 r0 = b * PK_ROWS;
@@ -381,6 +388,169 @@ void unpack_blocks(const UnpackBlk* d, u32 nd, const char* src, int kw, int S, u
   if (nd) klaunch(k_unpack, nd, PK_THREADS, 0, stream, d, src, kw, S, fmask, lo, hi, st);
 }
 
+// ---------------------------------------------------------------------------
+// Dense-window wide merge (sortagg.py:588-674 on a dense integer key domain).
+// When the runs' keys are dense in their range (a few run rows per possible
+// key), a key-range window of D consecutive keys is merged by direct
+// addressing: every run row of the window combines its state into entry
+// (key - window low) of a D-entry state array that stays in L2 -- no sort,
+// no staging of the rows -- and the occupied entries, in index order, are the
+// window's groups in key order.  Runs hold unique keys, so an entry receives
+// at most one row per run: contention is bounded by the run count whatever
+// the key skew.  Integer slots only (atomics commute exactly).
+//
+// k_dense_accum: one CTA per 1,024-row block of a (run, window) slice, read
+// in place from the HBM-resident run (bit-packed blocks decoded on the fly,
+// or raw columns); the key pass keeps each row's entry index in registers,
+// then one pass per state column issues the reductions.
+template <int IT>
+__global__ void __launch_bounds__(PK_THREADS) k_dense_accum(const DenseSlice* __restrict__ sl, int ns, u32 nblk, SlotDesc sd,
+                                                            u64 key_lo, u32 D, u64* __restrict__ dense,
+                                                            unsigned char* __restrict__ occ) {
+  static_assert(IT * PK_THREADS == PK_ROWS, "one block of run rows per CTA step");
+  const int S = sd.nslots;
+  __shared__ u32 s_cnt;
+  for (u32 q = blockIdx.x; q < nblk; q += gridDim.x) {
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    u32 below = 0;
+    for (int t = threadIdx.x; t < ns; t += PK_THREADS) below += sl[t].blk0 <= q ? 1u : 0u;
+    for (int o = 16; o; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+    if ((threadIdx.x & 31) == 0 && below) atomicAdd(&s_cnt, below);
+    __syncthreads();
+    const int l = (int)s_cnt - 1;
+    __syncthreads();
+    const DenseSlice u = sl[l];
+    u32 idx[IT];
+    if (u.pk) {
+      const u32 b = u.s0 / PK_ROWS + (q - u.blk0);
+      const u32 r0 = b * PK_ROWS;
+      const u32 e0 = max(u.s0, r0) - r0, e1 = min(u.s1, r0 + PK_ROWS) - r0;
+      const u64* blk = (const u64*)(u.pk + u.off[b]);
+      const u64* payload = blk + (1 + S) * 2;
+      {
+        const u64 base = blk[0], meta = blk[1];
+        const u32 width = (u32)(meta & 0xFF);
+        const u64* w = payload + (meta >> 8);
+#pragma unroll
+        for (int j = 0; j < IT; ++j) {
+          const u32 i = e0 + threadIdx.x + j * PK_THREADS;
+          const u64 k = i < e1 ? base + pk_extract(w, i, width) - key_lo : ~0ull;
+          idx[j] = k < (u64)D ? (u32)k : 0xFFFFFFFFu;
+          if (occ && idx[j] != 0xFFFFFFFFu) occ[idx[j]] = 1;
+        }
+      }
+      for (int c = 0; c < S; ++c) {
+        const u64 base = blk[(1 + c) * 2], meta = blk[(1 + c) * 2 + 1];
+        const u32 width = (u32)(meta & 0xFF);
+        const u64* w = payload + (meta >> 8);
+        const int op = sd.op[c];
+#pragma unroll
+        for (int j = 0; j < IT; ++j) {
+          if (idx[j] == 0xFFFFFFFFu) continue;
+          const u32 i = e0 + threadIdx.x + j * PK_THREADS;
+          const u64 v = pk_inv(base + pk_extract(w, i, width), 0, 0);
+          atomic_combine(dense + (size_t)idx[j] * S + c, op, ST_I64, v);
+        }
+      }
+    } else {
+      const u32 r0 = u.s0 + (q - u.blk0) * PK_ROWS, r1 = min(u.s1, r0 + PK_ROWS);
+#pragma unroll
+      for (int j = 0; j < IT; ++j) {
+        const u32 i = r0 + threadIdx.x + j * PK_THREADS;
+        const u64 k = i < r1 ? u.lo[i] - key_lo : ~0ull;
+        idx[j] = k < (u64)D ? (u32)k : 0xFFFFFFFFu;
+        if (idx[j] == 0xFFFFFFFFu) continue;
+        if (occ) occ[idx[j]] = 1;
+        for (int c = 0; c < S; ++c)
+          atomic_combine(dense + (size_t)idx[j] * S + c, sd.op[c], ST_I64, u.st[(size_t)i * S + c]);
+      }
+    }
+  }
+}
+
+// identity states (and cleared occupancy) for entries [0, D)
+__global__ void k_dense_init(u64* __restrict__ dense, unsigned char* __restrict__ occ, SlotDesc sd, u32 D) {
+  const int S = sd.nslots;
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < D; i += gridDim.x * blockDim.x) {
+    for (int c = 0; c < S; ++c) dense[(size_t)i * S + c] = identity_slot(sd.op[c], ST_I64);
+    if (occ) occ[i] = 0;
+  }
+}
+
+#define DN_ITEMS 4
+__device__ __forceinline__ bool dense_present(const u64* dense, const unsigned char* occ, int S, int cnt_slot, u32 i) {
+  return occ ? occ[i] != 0 : dense[(size_t)i * S + cnt_slot] != 0;
+}
+
+// occupied entries per 1,024-entry block
+__global__ void __launch_bounds__(256) k_dense_count(const u64* __restrict__ dense, const unsigned char* __restrict__ occ,
+                                                     int S, int cnt_slot, u32 D, u32* __restrict__ counts) {
+  __shared__ u32 ws[8];
+  const u32 i0 = (blockIdx.x * 256 + threadIdx.x) * DN_ITEMS;
+  u32 c = 0;
+#pragma unroll
+  for (int j = 0; j < DN_ITEMS; ++j)
+    if (i0 + j < D && dense_present(dense, occ, S, cnt_slot, i0 + j)) ++c;
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u32 t = 0;
+    for (int q = 0; q < 8; ++q) t += ws[q];
+    counts[blockIdx.x] = t;
+  }
+}
+
+// occupied entries -> result rows bbase[block] + rank (key = key_lo + entry),
+// every entry read is put back to its identity for the next window
+__global__ void __launch_bounds__(256) k_dense_emit(u64* __restrict__ dense, unsigned char* __restrict__ occ, SlotDesc sd,
+                                                    int cnt_slot, u32 D, u64 key_lo, const u32* __restrict__ bbase,
+                                                    u64* __restrict__ out_lo, u64* __restrict__ out_st) {
+  __shared__ u32 sw[8];
+  const int S = sd.nslots;
+  const u32 i0 = (blockIdx.x * 256 + threadIdx.x) * DN_ITEMS;
+  bool pres[DN_ITEMS];
+  u32 c = 0;
+#pragma unroll
+  for (int j = 0; j < DN_ITEMS; ++j) {
+    pres[j] = i0 + j < D && dense_present(dense, occ, S, cnt_slot, i0 + j);
+    c += pres[j] ? 1u : 0u;
+  }
+  u32 tot;
+  u32 pos = bbase[blockIdx.x] + block_excl_scan256(c, sw, &tot);
+#pragma unroll
+  for (int j = 0; j < DN_ITEMS; ++j) {
+    if (!pres[j]) continue;
+    const u32 i = i0 + j;
+    out_lo[pos] = key_lo + i;
+    for (int s = 0; s < S; ++s) {
+      out_st[(size_t)pos * S + s] = dense[(size_t)i * S + s];
+      dense[(size_t)i * S + s] = identity_slot(sd.op[s], ST_I64);
+    }
+    if (occ) occ[i] = 0;
+    ++pos;
+  }
+}
+
+void dense_init(u64* dense, unsigned char* occ, const SlotDesc& sd, u32 D, cudaStream_t st) {
+  if (D) klaunch(k_dense_init, (int)std::min<u32>((D + 255) / 256, 148u * 8u), 256, 0, st, dense, occ, sd, D);
+}
+void dense_accum(const DenseSlice* sl, int ns, u32 nblk, const SlotDesc& sd, u64 key_lo, u32 D, u64* dense,
+                 unsigned char* occ, cudaStream_t st) {
+  if (ns && nblk)
+    klaunch(k_dense_accum<PK_ROWS / PK_THREADS>, (int)std::min<u32>(nblk, 148u * 8u), PK_THREADS, 0, st, sl, ns, nblk, sd,
+            key_lo, D, dense, occ);
+}
+u32 dense_blocks(u32 D) { return (D + 256 * DN_ITEMS - 1) / (256 * DN_ITEMS); }
+void dense_count(const u64* dense, const unsigned char* occ, int S, int cnt_slot, u32 D, u32* counts, cudaStream_t st) {
+  klaunch(k_dense_count, (int)dense_blocks(D), 256, 0, st, dense, occ, S, cnt_slot, D, counts);
+}
+void dense_emit(u64* dense, unsigned char* occ, const SlotDesc& sd, int cnt_slot, u32 D, u64 key_lo, const u32* bbase,
+                u64* out_lo, u64* out_st, cudaStream_t st) {
+  klaunch(k_dense_emit, (int)dense_blocks(D), 256, 0, st, dense, occ, sd, cnt_slot, D, key_lo, bbase, out_lo, out_st);
+}
+
 // key of `row` of a packed run, read in place (mapped host memory)
 template <int KW>
 __device__ __forceinline__ void pk_key_at(const RunRef& r, u32 row, u64& khi, u64& klo) {
@@ -391,6 +561,21 @@ __device__ __forceinline__ void pk_key_at(const RunRef& r, u32 row, u64& khi, u6
   klo = blk[0] + pk_extract(payload + (blk[1] >> 8), i, (u32)(blk[1] & 0xFF));
   khi = 0;
   if (KW == 2) khi = blk[2] + pk_extract(payload + (blk[3] >> 8), i, (u32)(blk[3] & 0xFF));
+}
+
+// first and last key of every run (KW == 1): out[2r], out[2r + 1]
+__global__ void k_run_key_range(const RunRef* __restrict__ runs, int nruns, u64* __restrict__ out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= 2 * nruns) return;
+  const RunRef rr = runs[q >> 1];
+  const u32 row = (q & 1) ? rr.rows - 1 : 0u;
+  u64 khi = 0, klo;
+  if (rr.pk) pk_key_at<1>(rr, row, khi, klo);
+  else klo = rr.lo[row];
+  out[q] = klo;
+}
+void run_key_range(const RunRef* runs, int nruns, u64* out, cudaStream_t st) {
+  if (nruns) klaunch(k_run_key_range, (2 * nruns + 127) / 128, 128, 0, st, runs, nruns, out);
 }
 
 template <int KW>

@@ -453,7 +453,8 @@ struct Engine {
                       &tm_D, &tm_P, &tm_base, &tm_status, &tm_dirptrs, &tm_scal, &tm_gap, &tm_tb,
                       &hb_klo, &hb_khi, &hb_idx, &hot_hit, &ct_cuts, &ct_out, &ct_len, &ct_lo, &ct_st,
                       &sq_st[0], &sq_st[1], &sq_st[2], &sq_st[3], &sq_grp, &sq_runlo, &sq_runst, &sq_off, &sq_len,
-                      &sq_cyc, &sq_keys, &sq_out, &ha_lo, &ha_hi, &ha_st, &ha_occ, &ha_first, &ha_slot};
+                      &sq_cyc, &sq_keys, &sq_out, &ha_lo, &ha_hi, &ha_st, &ha_occ, &ha_first, &ha_slot,
+                      &dn_state, &dn_occ, &dn_counts, &dn_slices};
     for (int i = 0; i < 2; ++i) {
       if (desc_pinned[i]) cudaFreeHost(desc_pinned[i]);
       if (desc_done[i]) cudaEventDestroy(desc_done[i]);
@@ -1232,13 +1233,29 @@ struct Engine {
     if (k1_mode != 0 && span >= k1_min) return k1_chunk(kd, sd, row0, a, span);
     int cur = sort_rows(kd, row0, nullptr, span);
     const bool t_empty = T.n == 0;
+    // one int64 value column: an int32 copy of the chunk's values (L2-sized)
+    // for the collapse's random gather; the fit check rides on the flush
+    // analysis's host round trip
+    const void* ncol = span >= (1u << 20) ? narrow_candidate(sd) : nullptr;
+    if (ncol) {
+      rec_buf.ensure((size_t)span * 4 + 64);
+      ((volatile u32*)h_scal)[110] = 0;
+      narrow_i64(ncol, row0, span, rec_buf.as<int>(), d_scal_mapped + 110, st);
+    }
     u32 f = flush_point(cur, span, span);
     // with T empty every group of the chunk before f is new: M of them on a
     // flush, else the new-key count the flush analysis already returned
     const int64_t known = t_empty ? (f < span ? cfg.memory_budget : (int64_t)last_new) : -1;
     SlotDesc sdc = sd;
     int64_t r0c = row0;
-    if (f >= (1u << 20) && pack_records(sd, sdc, f)) {
+    if (ncol && ((volatile u32*)h_scal)[110] == 0) {
+      for (int s = 0; s < S; ++s)
+        if (sd.src[s] == SRC_COL && sd.ptr[s] == ncol) {
+          sdc.ptr[s] = rec_buf.p;
+          sdc.dtype[s] = ISA_I32;
+        }
+      r0c = 0;
+    } else if (f >= (1u << 20) && pack_records(sd, sdc, f)) {
       // >= 2 value columns: one record per row, so the collapse's random
       // gather touches one sector per row instead of one per column
       row_pack(rpk, row0, f, rec_buf.as<char>(), st);
@@ -1540,6 +1557,20 @@ struct Engine {
     }
     CK(cudaEventRecord(w.ready, h2d));
     w.staged = true;
+  }
+
+  // the one int64 value column every column-fed slot reads (null: none, or
+  // several columns / another dtype / strided records)
+  const void* narrow_candidate(const SlotDesc& sd) const {
+    { const char* e = getenv("ISA_NARROW"); if (e && e[0] == '0') return nullptr; }   // A/B
+    const void* col = nullptr;
+    for (int s = 0; s < S; ++s) {
+      if (sd.src[s] != SRC_COL) continue;
+      if (sd.dtype[s] != ISA_I64 || sd.stride[s] != 0) return nullptr;
+      if (col && sd.ptr[s] != col) return nullptr;
+      col = sd.ptr[s];
+    }
+    return col;
   }
 
   // Row-record layout for the collapse of a large sort-path chunk: true
@@ -2295,6 +2326,144 @@ struct Engine {
     streaming = false;
   }
 
+  // ---- dense-window wide merge (isa_codec.cu) ----
+  // Applies when every run is HBM-resident, the key is one word, every slot
+  // is an integer aggregate and the runs' key range holds at most 4 possible
+  // keys per run row.  Windows are equal key slabs of D keys (state array of
+  // ~40 MB: it lives in L2); slice bounds come from one batched lower-bound
+  // search, every window's slice descriptors are built and uploaded once.
+  DevBuf dn_state, dn_occ, dn_counts, dn_slices;
+  bool dense_merge(int64_t total) {
+    { const char* e = getenv("ISA_DENSE"); if (e && e[0] == '0') return false; }   // A/B: sort-based windows
+    const int k = (int)runs.size();
+    if (KW != 1 || k < 1 || total < 1) return false;
+    for (int s = 0; s < S; ++s)
+      if (sd0.type[s] != ST_I64) return false;
+    for (auto& r : runs)
+      if (r.host || !r.path.empty() || r.rows == 0) return false;
+    // key range of the runs
+    std::vector<RunRef> refs(k);
+    for (int i = 0; i < k; ++i) refs[i] = RunRef{runs[i].lo, runs[i].hi, runs[i].rows, S, runs[i].pk_dev, runs[i].off_dev};
+    runref_dev.ensure(sizeof(RunRef) * k);
+    bounds_lo.ensure(8 * (size_t)2 * k);
+    CK(cudaMemcpyAsync(runref_dev.p, refs.data(), sizeof(RunRef) * k, cudaMemcpyHostToDevice, st));
+    run_key_range(runref_dev.as<RunRef>(), k, bounds_lo.as<u64>(), st);
+    std::vector<u64> kr(2 * (size_t)k);
+    CK(cudaMemcpyAsync(kr.data(), bounds_lo.p, 8 * kr.size(), cudaMemcpyDeviceToHost, st));
+    sync();
+    u64 kmin = ~0ull, kmax = 0;
+    for (int i = 0; i < k; ++i) { kmin = std::min(kmin, kr[2 * i]); kmax = std::max(kmax, kr[2 * i + 1]); }
+    const u64 span = kmax - kmin;   // keys kmin .. kmin + span
+    if (span >= (u64)total * 4) return false;
+    const int cnt_slot = dense_count_slot();
+    const size_t entry = (size_t)8 * S + (cnt_slot < 0 ? 1 : 0);
+    u32 D = 1u << 12;
+    while (D < (1u << 26) && (size_t)(2 * D) * std::max<size_t>(entry, 1) <= ((size_t)40 << 20)) D *= 2;
+    while (D > (1u << 12) && (u64)(D / 2) > span) D /= 2;
+    if (const char* e = getenv("ISA_DENSE_D")) D = std::max<u32>(64u, (u32)atoi(e));   // tests: many small windows
+    const u64 nwin64 = span / D + 1;
+    if (nwin64 > (1u << 16)) return false;
+    const int nwin = (int)nwin64, nb = nwin - 1;
+    // exact slice bounds: lower_bound of every window boundary in every run
+    std::vector<u32> lb((size_t)k * std::max(nb, 1), 0u);
+    if (nb > 0) {
+      std::vector<u64> blo(nb), bhi(nb, 0ull);
+      for (int i = 0; i < nb; ++i) blo[i] = kmin + (u64)(i + 1) * D;
+      bounds_lo.ensure(8 * (size_t)nb);
+      bounds_hi.ensure(8 * (size_t)nb);
+      bounds_out.ensure(4 * (size_t)k * nb);
+      CK(cudaMemcpyAsync(bounds_lo.p, blo.data(), 8 * (size_t)nb, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(bounds_hi.p, bhi.data(), 8 * (size_t)nb, cudaMemcpyHostToDevice, st));
+      run_lower_bounds(KW, runref_dev.as<RunRef>(), k, bounds_lo.as<u64>(), bounds_hi.as<u64>(), nb,
+                       bounds_out.as<u32>(), st);
+      CK(cudaMemcpyAsync(lb.data(), bounds_out.p, 4 * (size_t)k * nb, cudaMemcpyDeviceToHost, st));
+      sync();
+    }
+    // every window's slices, uploaded once
+    std::vector<DenseSlice> slices;
+    std::vector<size_t> soff(nwin + 1, 0);
+    std::vector<u32> wblk(nwin, 0);
+    std::vector<int64_t> wrows(nwin, 0), wbytes(nwin, 0);
+    slices.reserve((size_t)k * nwin);
+    for (int w = 0; w < nwin; ++w) {
+      u32 blocks = 0;
+      for (int r = 0; r < k; ++r) {
+        const u32 s0 = w == 0 ? 0u : lb[(size_t)r * nb + (w - 1)];
+        const u32 s1 = w == nwin - 1 ? runs[r].rows : lb[(size_t)r * nb + w];
+        if (s1 <= s0) continue;
+        DenseSlice d{};
+        d.s0 = s0; d.s1 = s1; d.blk0 = blocks;
+        if (runs[r].pk_dev) {
+          d.pk = runs[r].pk_dev;
+          d.off = runs[r].off_dev;
+          const u32 b0 = s0 / PK_ROWS, b1 = (s1 - 1) / PK_ROWS;
+          blocks += b1 - b0 + 1;
+          wbytes[w] += (int64_t)(runs[r].off_host[b1 + 1] - runs[r].off_host[b0]);
+        } else {
+          d.lo = runs[r].lo;
+          d.st = runs[r].st;
+          blocks += (s1 - s0 + PK_ROWS - 1) / PK_ROWS;
+          wbytes[w] += (int64_t)(s1 - s0) * 8 * (KW + S);
+        }
+        slices.push_back(d);
+        wrows[w] += s1 - s0;
+      }
+      wblk[w] = blocks;
+      soff[w + 1] = slices.size();
+    }
+    dn_slices.ensure(slices.size() * sizeof(DenseSlice) + 64);
+    CK(cudaMemcpyAsync(dn_slices.p, slices.data(), slices.size() * sizeof(DenseSlice), cudaMemcpyHostToDevice, st));
+    dn_state.ensure((size_t)D * 8 * std::max(S, 1) + 64);
+    if (cnt_slot < 0) dn_occ.ensure((size_t)D + 64);
+    const u32 nblocks = dense_blocks(D);
+    dn_counts.ensure((size_t)(nblocks + 1) * 4);
+    u64* dstate = dn_state.as<u64>();
+    unsigned char* occ = cnt_slot < 0 ? dn_occ.as<unsigned char>() : nullptr;
+    dense_init(dstate, occ, sd0, D, st);
+    u32 zero = 0;
+    CK(cudaMemcpyAsync(dscal32(25), &zero, sizeof(u32), cudaMemcpyHostToDevice, st));
+    sync();   // the descriptor vectors are pageable host memory
+    result.n = 0;
+    if (stream_want) stream_setup();
+    int64_t ub = 0;
+    for (int w = 0; w < nwin; ++w) {
+      const int64_t m = wrows[w];
+      led.rows_read_back += m;
+      led.merge_windows++;
+      if (m == 0) continue;
+      const int64_t most = std::min<int64_t>(m, D);
+      if (ub + most > (int64_t)(result.lo.bytes / 8)) {
+        result.n = read_u32(dscal32(25));
+        ub = result.n;
+        if (ub + most > (int64_t)(result.lo.bytes / 8)) {
+          if (streaming) { stream_flush(nullptr); CK(cudaStreamSynchronize(xs)); }
+          grow_table(result, (size_t)ub + most);
+        }
+      }
+      ph_begin(ISA_PH_WM_COLLAPSE);
+      kt_begin(KF_MERGE, st);
+      dense_accum(dn_slices.as<DenseSlice>() + soff[w], (int)(soff[w + 1] - soff[w]), wblk[w], sd0, kmin + (u64)w * D, D,
+                  dstate, occ, st);
+      kt_end(KF_MERGE, wbytes[w] + m * 8 * S, st);
+      dense_count(dstate, occ, S, cnt_slot, D, dn_counts.as<u32>(), st);
+      block_counts_scan(dn_counts.as<u32>(), nblocks, dscal32(26), dscal32(25), st);
+      dense_emit(dstate, occ, sd0, cnt_slot, D, kmin + (u64)w * D, dn_counts.as<u32>(), result.plo(), result.pst(), st);
+      CK(cudaMemcpyAsync(dscal32(25), dscal32(26), sizeof(u32), cudaMemcpyDeviceToDevice, st));
+      ph_end(ISA_PH_WM_COLLAPSE, m, 0);
+      if (streaming) stream_window((u32)std::min<int64_t>(m, 0xFFFFFFFFll));
+      ub += most;
+    }
+    result.n = read_u32(dscal32(25));
+    if (result.n > 0xFFFFFFF0u) throw IsaError(ISA_ERR_INVALID_INPUT, "more than 2^32-1 output groups are not supported");
+    return true;
+  }
+  // a COUNT-like slot (int64 sum of ones): nonzero exactly for occupied entries
+  int dense_count_slot() const {
+    for (int s = 0; s < S; ++s)
+      if (sd0.src[s] == SRC_ONE && sd0.op[s] == OP_ADD && sd0.type[s] == ST_I64) return s;
+    return -1;
+  }
+
   // Final wide merge of all runs into the result (sortagg.py:588-674)
   void wide_merge() {
     int64_t total = 0;
@@ -2311,8 +2480,9 @@ struct Engine {
       stream_total = total;
       stream_est = est;
     }
-    merge_runs(runs, true, [&](Table& w, u32) { append_result(w); }, tiles ? &tp : nullptr,
-               direct_merge_env() ? &result : nullptr);
+    if (tiles || !dense_merge(total))
+      merge_runs(runs, true, [&](Table& w, u32) { append_result(w); }, tiles ? &tp : nullptr,
+                 direct_merge_env() ? &result : nullptr);
     if (streaming) end_stream();
     stream_want = false;
     if (cfg.run_tier == ISA_TIER_FILE && read_u32(dscal32(12)))

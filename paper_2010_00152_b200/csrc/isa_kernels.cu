@@ -1141,6 +1141,28 @@ void row_pack(const RowPack& rp, int64_t row0, u32 n, char* out, cudaStream_t st
   if (n) klaunch(k_row_pack, grid_for(n, 256), 256, 0, st, rp, (i64)row0, n, out);
 }
 
+// One int64 value column narrowed to int32 for rows [row0, row0 + n): the
+// collapse gathers values by pre-sort row position (random reads), and a
+// 4-byte record per row of a fill cycle mostly stays in the 126 MB L2 where
+// the 8-byte column does not.  *bad_mapped (mapped host memory, zeroed by the
+// host) is set when a value does not fit int32: the caller then keeps the
+// column.
+__global__ void __launch_bounds__(256) k_narrow_i64(const i64* __restrict__ src, u32 n, int* __restrict__ out,
+                                                    u32* __restrict__ bad_mapped) {
+  bool bad = false;
+  for (u32 i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+    const i64 v = src[i];
+    const int x = (int)v;
+    out[i] = x;
+    bad |= (i64)x != v;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *bad_mapped = 1u;
+}
+
+void narrow_i64(const void* src, int64_t row0, u32 n, int* out, u32* bad_mapped, cudaStream_t st) {
+  if (n) klaunch(k_narrow_i64, grid_for(n, 256), 256, 0, st, (const i64*)src + row0, n, out, bad_mapped);
+}
+
 // ========================================================== collapse ====
 // Consecutive sorted items per segmented-reduce thread: 4 for states of
 // <= 2 slots (measured: config 5's collapse 51 -> 35 ms; more threads keep
@@ -1234,6 +1256,10 @@ __global__ void __launch_bounds__(1024) k_cl_scan(u32* __restrict__ counts, u32 
     counts[b] = run;
     run += c;
   }
+}
+
+void block_counts_scan(u32* counts, u32 nb, u32* total, const u32* base, cudaStream_t st) {
+  klaunch(k_cl_scan, 1, 1024, 0, st, counts, nb, total, base);
 }
 
 template <int KW, int MS>

@@ -95,6 +95,8 @@ void window_keys(int KW, const u64* slo, const u64* shi, u32 m, u64 llo, u64 lhi
 u32 collapse_tiles(u32 m, int S);
 // value columns of rows [row0, row0 + n) interleaved into R-byte records
 struct RowPack { int nc; const void* src[ISA_MAX_SLOTS]; int elem[ISA_MAX_SLOTS]; int off[ISA_MAX_SLOTS]; int R; };
+// int64 column rows [row0, +n) -> int32 records; *bad_mapped = 1 when a value does not fit
+void narrow_i64(const void* src, int64_t row0, u32 n, int* out, u32* bad_mapped, cudaStream_t st);
 void row_pack(const RowPack& rp, int64_t row0, u32 n, char* out, cudaStream_t st);
 // segmented-reduce threads for m items (per-thread partial-state buffers)
 u32 collapse_threads(u32 m, int S);
@@ -222,6 +224,22 @@ void gather_raw(const RawCopy* d, u32 nd, int kw, int S, u64* lo, u64* hi, u64* 
 struct UnpackSlice { const char* pk; const u32* off; u32 s0, s1, dst, blk0; };
 void unpack_slices(const UnpackSlice* sl, int ns, u32 nblk, int kw, int S, u32 fmask, u64* lo, u64* hi, u64* st,
                    cudaStream_t stream);
+
+// exclusive scan of nb per-block counts in place, starting at *base (null: 0); *total = *base + sum
+void block_counts_scan(u32* counts, u32 nb, u32* total, const u32* base, cudaStream_t st);
+// ---- dense-window wide merge (isa_codec.cu) -------------------------------
+// a (run, window) slice: rows [s0, s1) of an HBM-resident run, bit-packed
+// (pk, off) or raw (lo, st); blk0 = its first 1,024-row block in the window's
+// block numbering
+struct DenseSlice { const char* pk; const u32* off; const u64* lo; const u64* st; u32 s0, s1, blk0, pad; };
+void dense_init(u64* dense, unsigned char* occ, const SlotDesc& sd, u32 D, cudaStream_t st);
+void dense_accum(const DenseSlice* sl, int ns, u32 nblk, const SlotDesc& sd, u64 key_lo, u32 D, u64* dense,
+                 unsigned char* occ, cudaStream_t st);
+u32 dense_blocks(u32 D);
+void dense_count(const u64* dense, const unsigned char* occ, int S, int cnt_slot, u32 D, u32* counts, cudaStream_t st);
+void dense_emit(u64* dense, unsigned char* occ, const SlotDesc& sd, int cnt_slot, u32 D, u64 key_lo, const u32* bbase,
+                u64* out_lo, u64* out_st, cudaStream_t st);
+void run_key_range(const RunRef* runs, int nruns, u64* out, cudaStream_t st);
 
 // ---- reference page format (isa_pages.cu, runstore.py:1-20, 120-142) ----
 struct PageSpec {

@@ -42,11 +42,15 @@ def _cfg(memory, page, **kw):
 @pytest.mark.parametrize("name", golden_names())
 @pytest.mark.parametrize("variant", ["device", "host_input", "hbm_runs", "packed_runs", "host_runs", "small_chunks",
                                      "k1_always", "k1_never", "tile_merge", "radix_merge", "one_cta",
-                                     "window_round_trips", "chunk_loop"])
+                                     "window_round_trips", "chunk_loop", "dense_small_windows"])
 def test_golden_columns(name, variant, monkeypatch):
     g = Golden(name)
     if variant in ("tile_merge", "radix_merge"):   # force either wide-merge path
         monkeypatch.setenv("ISA_TILE_MERGE", "1" if variant == "tile_merge" else "0")
+    if variant in ("radix_merge", "window_round_trips"):   # not the dense-window merge (dense integer keys)
+        monkeypatch.setenv("ISA_DENSE", "0")
+    if variant == "dense_small_windows":   # dense keys: direct-addressed windows of 256 keys
+        monkeypatch.setenv("ISA_DENSE_D", "256")
     if variant == "one_cta":   # small budgets: the one-CTA read-sort-write run generation (isa_seq.cu)
         monkeypatch.setenv("ISA_SEQ", "1")
     if variant == "window_round_trips":   # wide merge reading every window's group count back (no device base)
@@ -70,7 +74,7 @@ def test_golden_columns(name, variant, monkeypatch):
     mode = str(g.z["merge_mode"]) if "merge_mode" in g.z else "wide"
     if mode != "wide" and variant in ("k1_always", "k1_never", "small_chunks", "packed_runs", "host_runs",
                                       "tile_merge", "radix_merge", "one_cta", "window_round_trips",
-                                      "chunk_loop"):
+                                      "chunk_loop", "dense_small_windows"):
         pytest.skip("pre-aggregation / chunking knobs apply to the wide path only")
     op = isa.SortAggregate(sch, _cfg(g.memory, g.page, merge_mode=mode, **kw))
     n = len(g.keys[0])
@@ -779,6 +783,7 @@ def test_direct_window_merge_many_windows_vs_oracle(cfg, rows, memory, window, m
     continue from a device-resident count, the result grows when the rows
     staged so far could overflow it): equals the oracle."""
     monkeypatch.setenv("ISA_TILE_MERGE", "0")   # the radix-window path (128-bit keys default to tiles)
+    monkeypatch.setenv("ISA_DENSE", "0")        # ... and not the dense-window merge
     kw = {"domain": 1 << 20} if cfg in (3, 5) else {}
     w = workloads.make(cfg, rows=rows, device="cpu", **kw)
     op = _oracle_case(w, memory, page=100, rel=1e-5 if cfg == 3 else 1e-9, merge_window_rows=window)
@@ -853,12 +858,16 @@ def test_config1_cut_then_aggregate_launches():
 
 @pytest.mark.parametrize("cfg,rows,memory,window", [(5, 3_000_000, 1 << 14, 50_000), (3, 2_000_000, 1 << 14, 40_000),
                                                     (1, 1_000_000, 4096, 20_000), (5, 3_000_000, 1 << 18, 0)])
-def test_streamed_host_output_vs_oracle(cfg, rows, memory, window, monkeypatch):
+@pytest.mark.parametrize("dense", ["0", "1"])
+def test_streamed_host_output_vs_oracle(cfg, rows, memory, window, dense, monkeypatch):
     """Host input that spills: the wide merge writes every window's groups
     into caller-owned pinned columns (isa_set_output_allocator) while the next
     window merges; the columns equal the oracle and the device-input result,
     and the result is reported as streamed."""
     monkeypatch.setenv("ISA_TILE_MERGE", "0")
+    monkeypatch.setenv("ISA_DENSE", dense)
+    if dense == "1" and window:
+        monkeypatch.setenv("ISA_DENSE_D", "8192")
     kw = {"domain": 1 << 20} if cfg in (3, 5) else {}
     w = workloads.make(cfg, rows=rows, device="cpu", **kw)
     keys_np = [k.numpy() for k in w.keys]
@@ -886,6 +895,7 @@ def test_streamed_host_output_falls_back_when_the_estimate_is_short(monkeypatch)
     streamed columns are too small, and the operator falls back to
     isa_result_copy -- same result."""
     monkeypatch.setenv("ISA_TILE_MERGE", "0")
+    monkeypatch.setenv("ISA_DENSE", "0")
     rng = np.random.default_rng(11)
     n1, n2, memory = 2_000_000, 400_000, 1 << 12
     k = np.concatenate([rng.integers(0, memory + 40, n1), (1 << 20) + rng.permutation(n2)]).astype(np.int64)
@@ -901,3 +911,70 @@ def test_streamed_host_output_falls_back_when_the_estimate_is_short(monkeypatch)
     op2 = isa.SortAggregate(sch, _cfg(memory, 100, merge_window_rows=30_000))
     res2 = op2.execute_columns([torch.from_numpy(k).pin_memory()], {"v": torch.from_numpy(v).pin_memory()})
     _check(res2, want_keys, want_slots)
+
+
+def _phase_ms(op, name):
+    from paper_2010_00152_b200 import _native
+    return _native.phases_dict(op.phase_snapshot())[name]["ms"]
+
+
+@pytest.mark.parametrize("case", ["cfg5", "cfg5_small_windows", "signed_minmax", "sum_only", "distinct", "raw_hbm_runs",
+                                  "one_window"])
+def test_dense_window_merge_vs_oracle(case, monkeypatch):
+    """Dense integer keys: the wide merge accumulates every run row into a
+    direct-addressed window of the key range (integer atomics) instead of
+    sorting the window; groups, states and the ledger equal the oracle's, and
+    no window sort runs."""
+    from paper_2010_00152_b200.core import AggregateKind, AggregateSpec, ColumnSpec, Schema
+    rng = np.random.default_rng(5)
+    kw = {}
+    if case in ("cfg5", "cfg5_small_windows", "raw_hbm_runs", "one_window"):
+        w = workloads.make(5, rows=3_000_000, device="cpu", domain=1 << 20)
+        sch, keys_np = w.schema, [k.numpy() for k in w.keys]
+        vals_np = {k: v.numpy() for k, v in w.values.items()}
+        memory = 1 << 14
+        if case == "cfg5_small_windows":
+            monkeypatch.setenv("ISA_DENSE_D", "4096")
+        if case == "raw_hbm_runs":
+            kw.update(run_tier="hbm", run_codec="raw")
+        if case == "one_window":
+            memory = 1 << 19
+    else:
+        n = 1_500_000
+        k = rng.integers(-300_000, 300_000, n).astype(np.int64)
+        v = rng.integers(-1_000_000, 1_000_001, n).astype(np.int64)
+        keys_np, vals_np, memory = [k], {"v": v}, 1 << 13
+        if case == "signed_minmax":
+            sch = _cut_schema()
+        elif case == "sum_only":   # no COUNT slot: occupancy bytes
+            sch = Schema([ColumnSpec("k")], [AggregateSpec("s", AggregateKind.SUM, "v"),
+                                             AggregateSpec("hi", AggregateKind.MAX, "v")])
+        else:                      # DISTINCT: no slots at all
+            sch, vals_np = Schema([ColumnSpec("k")], []), {}
+        monkeypatch.setenv("ISA_DENSE_D", "16384")
+    slots = oracle.make_states(sch, vals_np, len(keys_np[0]))
+    want_keys, want_slots = oracle.reference_aggregate(keys_np, slots, oracle.slot_ops(sch))
+    _, _, led, cycles = oracle.rsw_sortagg(keys_np, slots, oracle.slot_ops(sch), memory, 100)
+    op = isa.SortAggregate(sch, _cfg(memory, 100, **kw))
+    res = op.execute_columns([_cuda(k) for k in keys_np], {n_: _cuda(v) for n_, v in vals_np.items()})
+    _check(res, want_keys, want_slots)
+    assert op.ledger.rows_spilled == led["rows_spilled"] and op.ledger.rows_read_back == led["rows_spilled"]
+    assert op.runs_after_generation == led["runs"] and op.runs_after_generation > 1
+    assert _phase_ms(op, "wm_sort") == 0 and _phase_ms(op, "wm_collapse") > 0
+    if case == "cfg5_small_windows":
+        assert op.device_ledger["merge_windows"] >= 200
+    if case == "one_window":
+        assert op.device_ledger["merge_windows"] == 1
+    monkeypatch.setenv("ISA_DENSE", "0")   # the sort-based windows give the same columns
+    op2 = isa.SortAggregate(sch, _cfg(memory, 100, **kw))
+    res2 = op2.execute_columns([_cuda(k) for k in keys_np], {n_: _cuda(v) for n_, v in vals_np.items()})
+    for a, b in zip(list(res.keys) + list(res.states), list(res2.keys) + list(res2.states)):
+        assert torch.equal(a, b)
+    assert _phase_ms(op2, "wm_sort") > 0
+
+
+def test_dense_window_merge_not_for_sparse_or_float(monkeypatch):
+    """Sparse keys (hashed) and float aggregates keep the sort-based windows."""
+    w = workloads.make(3, rows=1_000_000, device="cpu", domain=1 << 20)   # hashed int64 keys, float sums
+    op = _oracle_case(w, 1 << 14, page=100, rel=1e-5)
+    assert _phase_ms(op, "wm_sort") > 0
