@@ -686,6 +686,7 @@ struct Engine {
     CK(cudaMemsetAsync(dvary(), 0, 2 * sizeof(u64), st));
     build_keys(KW, kd, row0, pos, m, s_lo[0].as<u64>(), s_hi[0].as<u64>(), s_val[0].as<u32>(), dvary(), st);
     sort_ctx = 0;
+    sort_val_iota = pos == nullptr;
     int cur = sort_built(m);
     sort_ctx = 1;
     ph_end(ISA_PH_SORT, m, 0);
@@ -693,7 +694,10 @@ struct Engine {
   }
   // known_v: the varying-bit mask is known on the host (a key-range window
   // [L, U): every key shares the bits above L ^ (U - 1)), no read-back
+  bool sort_val_iota = false;   // the pending sort's payload is 0..m-1 (consumed by the next sort_built)
   int sort_built(u32 m, const u64* known_v = nullptr) {
+    const bool iota = sort_val_iota;
+    sort_val_iota = false;
     u64 vlo, vhi;
     if (known_v) {
       vlo = known_v[0];
@@ -721,6 +725,7 @@ struct Engine {
     b.map_dev = d_hist_mapped;
     b.map_host = h_hist;
     b.pack_ok = true;   // bits outside [lb, hb] do not vary (see above)
+    b.val_iota = iota;
     RankHint& rh = rank_hint[sort_ctx];
     b.hint = rh.h;
     b.hint_bit_lo = rh.bit_lo;
@@ -2167,6 +2172,7 @@ struct Engine {
         CK(cudaMemsetAsync(dvary(), 0, 2 * sizeof(u64), st));
         keys_varying(KW, s_lo[0].as<u64>(), s_hi[0].as<u64>(), m, dvary(), st);
       }
+      sort_val_iota = true;   // window_keys numbered the staged rows
       int cur = sort_built(m, known ? vm : nullptr);
       ph_end(ISA_PH_WM_SORT, m, 0);
       u32 distinct;

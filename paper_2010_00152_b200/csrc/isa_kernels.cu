@@ -242,7 +242,7 @@ __device__ __forceinline__ void st_relaxed_gpu(u64* p, u64 v) {
 // the usual (key, row id) columns.  `shift` is then the digit's position
 // in the packed word.
 template <int KW, bool BALLOT, int PK = 0>
-__global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 2 ? 4 : 3)) k_rs_scatter(const u64* __restrict__ lo_in, const u64* __restrict__ hi_in,
+__global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 1 ? 4 : 3)) k_rs_scatter(const u64* __restrict__ lo_in, const u64* __restrict__ hi_in,
                                                          const u32* __restrict__ v_in, u64* __restrict__ lo_out,
                                                          u64* __restrict__ hi_out, u32* __restrict__ v_out, u32 n,
                                                          int shift, u64* __restrict__ status,
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 2 ? 4 : 3)) k
     u32 gi = base + li;
     lo[it] = valid ? lo_in[gi] : 0;
     hi[it] = (KW == 2 && valid) ? hi_in[gi] : 0;
-    v[it] = (PK <= 1 && valid) ? v_in[gi] : 0;
+    v[it] = (PK <= 1 && valid) ? ((PK == 1 && !v_in) ? gi : v_in[gi]) : 0;   // PK 1, null v_in: row ids 0..n-1
     if (PK == 1) {
       if (gi == 0 && valid) *pk_const = lo[it] & ~(0xFFFFFFFFull << pk_lo);
       lo[it] = (((lo[it] >> pk_lo) & 0xFFFFFFFFull) << 32) | v[it];
@@ -734,7 +734,16 @@ static int radix_lsd(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
         (int64_t)n * (packed ? (p == 0 || (p == npass - 1 && !leave_packed) ? 20 : 16) : 2 * (8 * KW + 4));
     kt_begin(KF_SCATTER, st);
     if (packed) {
-      if (p == 0) RS_PK(1);
+      if (p == 0 && b.val_iota) {   // row ids 0..n-1: the pass numbers the rows itself (no row-id read)
+        if (ballot[p])
+          klaunch(k_rs_scatter<1, true, 1>, ntiles, RS_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,
+                  (const u32*)nullptr, b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - pk_lo, stt, gh, tc, ep, pk_lo,
+                  pk_const, lb_sleep);
+        else
+          klaunch(k_rs_scatter<1, false, 1>, ntiles, RS_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,
+                  (const u32*)nullptr, b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - pk_lo, stt, gh, tc, ep, pk_lo,
+                  pk_const, lb_sleep);
+      } else if (p == 0) RS_PK(1);
       else if (p == npass - 1 && !leave_packed) RS_PK(3);
       else RS_PK(2);
     } else if (KW == 2) {

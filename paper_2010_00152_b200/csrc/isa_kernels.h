@@ -25,6 +25,7 @@ struct SortBufs {
   signed char* hint = nullptr;     // [16] cached ranking choice per pass (hint[0] < 0: none yet)
   int hint_bit_lo = -1, hint_npass = 0;
   bool pack_ok = false;   // key bits outside [bit_lo, bit_hi) are equal in every key (packed passes allowed)
+  bool val_iota = false;  // val[0][i] == i (row ids 0..n-1): a packing first pass numbers the rows itself
 };
 size_t sort_aux_bytes(u32 n);
 int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStream_t st, int64_t* launches,
