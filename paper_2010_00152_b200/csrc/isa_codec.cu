@@ -170,21 +170,30 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack_fused(PackSrc p, u64* __res
     if (lane == 0) { s_mn[w][c] = mn[c]; s_mx[w][c] = mx[c]; }
   }
   __syncthreads();
-  if (tid == 0) {
-    u32 woff = 0;
-    for (int c = 0; c < NC; ++c) {
-      u64 a = s_mn[0][c], z = s_mx[0][c];
+  if (w == 0) {
+    // lane c reduces column c over the warps; the payload word offsets are a
+    // prefix over the columns (shuffle scan)
+    u32 words = 0, width = 0;
+    if (lane < NC) {
+      u64 a = s_mn[0][lane], z = s_mx[0][lane];
+#pragma unroll
       for (int ww = 1; ww < PK_THREADS / 32; ++ww) {
-        a = s_mn[ww][c] < a ? s_mn[ww][c] : a;
-        z = s_mx[ww][c] > z ? s_mx[ww][c] : z;
+        a = s_mn[ww][lane] < a ? s_mn[ww][lane] : a;
+        z = s_mx[ww][lane] > z ? s_mx[ww][lane] : z;
       }
-      const u32 width = z == a ? 0u : (u32)(64 - __clzll((long long)(z - a)));
-      s_base[c] = a;
-      s_width[c] = width;
-      s_woff[c] = woff;
-      woff += (rows * width + 63) / 64;
+      width = z == a ? 0u : (u32)(64 - __clzll((long long)(z - a)));
+      words = (rows * width + 63) / 64;
+      s_base[lane] = a;
+      s_width[lane] = width;
     }
-    s_bytes = (NC * 2 + woff) * 8;
+    u32 incl = words;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane < NC) s_woff[lane] = incl - words;
+    if (lane == NC - 1) s_bytes = (NC * 2 + incl) * 8;
   }
   __syncthreads();
   // 2. decoupled look-back over the previous blocks' byte counts, one warp:

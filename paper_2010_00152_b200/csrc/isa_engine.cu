@@ -454,7 +454,7 @@ struct Engine {
                       &hb_klo, &hb_khi, &hb_idx, &hot_hit, &ct_cuts, &ct_out, &ct_len, &ct_lo, &ct_st,
                       &sq_st[0], &sq_st[1], &sq_st[2], &sq_st[3], &sq_grp, &sq_runlo, &sq_runst, &sq_off, &sq_len,
                       &sq_cyc, &sq_keys, &sq_out, &ha_lo, &ha_hi, &ha_st, &ha_occ, &ha_first, &ha_slot,
-                      &dn_state, &dn_occ, &dn_counts, &dn_slices};
+                      &dn_state, &dn_occ, &dn_counts, &dn_slices, &rec_sorted};
     for (int i = 0; i < 2; ++i) {
       if (desc_pinned[i]) cudaFreeHost(desc_pinned[i]);
       if (desc_done[i]) cudaEventDestroy(desc_done[i]);
@@ -488,6 +488,8 @@ struct Engine {
     if (h2d) cudaStreamDestroy(h2d);
     if (d2h) cudaStreamDestroy(d2h);
     if (xs) cudaStreamDestroy(xs);
+    if (dn_emit) cudaStreamDestroy(dn_emit);
+    for (int i = 0; i < 2; ++i) { if (dn_acc_done[i]) cudaEventDestroy(dn_acc_done[i]); if (dn_emit_done[i]) cudaEventDestroy(dn_emit_done[i]); }
     if (xs_ev) cudaEventDestroy(xs_ev);
     for (auto e : stream_cnt_ev) if (e) cudaEventDestroy(e);
     if (spill_done) cudaEventDestroy(spill_done);
@@ -695,9 +697,19 @@ struct Engine {
   // known_v: the varying-bit mask is known on the host (a key-range window
   // [L, U): every key shares the bits above L ^ (U - 1)), no read-back
   bool sort_val_iota = false;   // the pending sort's payload is 0..m-1 (consumed by the next sort_built)
+  // the pending sort may carry a 4-byte value per row (in row order) with the keys and leave it in sorted
+  // order in sort_carry_out; sort_carried tells whether it did (packed passes only)
+  const u32* sort_carry_in = nullptr;
+  u32* sort_carry_out = nullptr;
+  bool sort_carried = false;
   int sort_built(u32 m, const u64* known_v = nullptr) {
     const bool iota = sort_val_iota;
     sort_val_iota = false;
+    const u32* cin = sort_carry_in;
+    u32* cout = sort_carry_out;
+    sort_carry_in = nullptr;
+    sort_carry_out = nullptr;
+    sort_carried = false;
     u64 vlo, vhi;
     if (known_v) {
       vlo = known_v[0];
@@ -726,6 +738,9 @@ struct Engine {
     b.map_host = h_hist;
     b.pack_ok = true;   // bits outside [lb, hb] do not vary (see above)
     b.val_iota = iota;
+    b.carry_in = cin;
+    b.carry_out = cout;
+    struct CarryBack { bool& f; SortBufs& b; ~CarryBack() { f = b.carried; } } carry_back{sort_carried, b};
     RankHint& rh = rank_hint[sort_ctx];
     b.hint = rh.h;
     b.hint_bit_lo = rh.bit_lo;
@@ -816,6 +831,7 @@ struct Engine {
 
   // U <- collapse(sorted chunk restricted to positions < limit)
   // known_n >= 0: the caller knows the group count (no host round trip)
+  bool collapse_by_pos = false;   // the next collapse_chunk reads value columns by sorted position (carried values)
   void collapse_chunk(int cur, u32 m, u32 limit, const SlotDesc& sd, int64_t row0, const u64* st_in, Table& out,
                       size_t out_cap, bool merge_phase = true, int64_t known_n = -1) {
     ensure_collapse(m);
@@ -829,6 +845,8 @@ struct Engine {
     ct.status = cl_status.as<u64>();
     ct.pay = cl_pay.as<u64>();
     ct.ticket = dscal32(22);
+    ct.by_pos = collapse_by_pos;
+    collapse_by_pos = false;
     const int phc = (st_in && merge_phase) ? ISA_PH_WM_COLLAPSE : ISA_PH_COLLAPSE;
     ph_begin(phc);
     kt_begin(KF_COLLAPSE, st);
@@ -1236,17 +1254,26 @@ struct Engine {
     if (hot_ready()) return hot_chunk(kd, sd, row0, a, span);
     const u32 k1_min = (cfg.preaggregate == 1 ? 4 : 64) * tile_rows();
     if (k1_mode != 0 && span >= k1_min) return k1_chunk(kd, sd, row0, a, span);
-    int cur = sort_rows(kd, row0, nullptr, span);
-    const bool t_empty = T.n == 0;
-    // one int64 value column: an int32 copy of the chunk's values (L2-sized)
-    // for the collapse's random gather; the fit check rides on the flush
-    // analysis's host round trip
+    // one int64 value column: an int32 copy of the chunk's values, carried
+    // through the packed sort passes as the payload so that the collapse
+    // reads every row's value at its sorted position (no random gather); when
+    // the sort cannot carry it (key bits spanning more than 32) the collapse
+    // gathers from the int32 copy.  The fit check rides on the flush
+    // analysis's host round trip.
     const void* ncol = span >= (1u << 20) ? narrow_candidate(sd) : nullptr;
     if (ncol) {
       rec_buf.ensure((size_t)span * 4 + 64);
       ((volatile u32*)h_scal)[110] = 0;
       narrow_i64(ncol, row0, span, rec_buf.as<int>(), d_scal_mapped + 110, st);
+      if (collapse_by_pos_ok(span, S)) {
+        rec_sorted.ensure((size_t)span * 4 + 64);
+        sort_carry_in = rec_buf.as<u32>();
+        sort_carry_out = rec_sorted.as<u32>();
+      }
     }
+    int cur = sort_rows(kd, row0, nullptr, span);
+    const bool carried = sort_carried;
+    const bool t_empty = T.n == 0;
     u32 f = flush_point(cur, span, span);
     // with T empty every group of the chunk before f is new: M of them on a
     // flush, else the new-key count the flush analysis already returned
@@ -1256,10 +1283,11 @@ struct Engine {
     if (ncol && ((volatile u32*)h_scal)[110] == 0) {
       for (int s = 0; s < S; ++s)
         if (sd.src[s] == SRC_COL && sd.ptr[s] == ncol) {
-          sdc.ptr[s] = rec_buf.p;
+          sdc.ptr[s] = carried ? rec_sorted.p : rec_buf.p;
           sdc.dtype[s] = ISA_I32;
         }
       r0c = 0;
+      collapse_by_pos = carried;
     } else if (f >= (1u << 20) && pack_records(sd, sdc, f)) {
       // >= 2 value columns: one record per row, so the collapse's random
       // gather touches one sector per row instead of one per column
@@ -1582,7 +1610,7 @@ struct Engine {
   // (and sdc pointing into rec_buf) when the slots read >= 2 distinct
   // value columns that fit a 16-byte record.
   RowPack rpk;
-  DevBuf rec_buf;
+  DevBuf rec_buf, rec_sorted;
   bool pack_records(const SlotDesc& sd, SlotDesc& sdc, u32 rows) {
     memset(&rpk, 0, sizeof(rpk));
     int off = 0;
@@ -2339,6 +2367,8 @@ struct Engine {
   // ~40 MB: it lives in L2); slice bounds come from one batched lower-bound
   // search, every window's slice descriptors are built and uploaded once.
   DevBuf dn_state, dn_occ, dn_counts, dn_slices;
+  cudaStream_t dn_emit = nullptr;
+  cudaEvent_t dn_acc_done[2] = {nullptr, nullptr}, dn_emit_done[2] = {nullptr, nullptr};
   bool dense_merge(int64_t total) {
     { const char* e = getenv("ISA_DENSE"); if (e && e[0] == '0') return false; }   // A/B: sort-based windows
     const int k = (int)runs.size();
@@ -2419,26 +2449,44 @@ struct Engine {
     }
     dn_slices.ensure(slices.size() * sizeof(DenseSlice) + 64);
     CK(cudaMemcpyAsync(dn_slices.p, slices.data(), slices.size() * sizeof(DenseSlice), cudaMemcpyHostToDevice, st));
-    dn_state.ensure((size_t)D * 8 * std::max(S, 1) + 64);
-    if (cnt_slot < 0) dn_occ.ensure((size_t)D + 64);
     const u32 nblocks = dense_blocks(D);
     dn_counts.ensure((size_t)(nblocks + 1) * 4);
-    u64* dstate = dn_state.as<u64>();
-    unsigned char* occ = cnt_slot < 0 ? dn_occ.as<unsigned char>() : nullptr;
-    dense_init(dstate, occ, sd0, D, st);
+    // two state arrays: window w + 1 accumulates on the compute stream while
+    // window w's entries are emitted (and reset) on a second stream
+    dn_state.ensure((size_t)2 * D * 8 * std::max(S, 1) + 64);
+    if (cnt_slot < 0) dn_occ.ensure((size_t)2 * D + 64);
+    u64* dstate2[2] = {dn_state.as<u64>(), dn_state.as<u64>() + (size_t)D * std::max(S, 1)};
+    unsigned char* occ2[2] = {cnt_slot < 0 ? dn_occ.as<unsigned char>() : nullptr,
+                              cnt_slot < 0 ? dn_occ.as<unsigned char>() + D : nullptr};
+    if (!dn_emit) {
+      CK(cudaStreamCreateWithFlags(&dn_emit, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        CK(cudaEventCreateWithFlags(&dn_acc_done[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&dn_emit_done[i], cudaEventDisableTiming));
+      }
+    }
+    for (int i = 0; i < 2; ++i) {
+      dense_init(dstate2[i], occ2[i], sd0, D, st);
+      CK(cudaEventRecord(dn_emit_done[i], st));
+    }
     u32 zero = 0;
     CK(cudaMemcpyAsync(dscal32(25), &zero, sizeof(u32), cudaMemcpyHostToDevice, st));
     sync();   // the descriptor vectors are pageable host memory
     result.n = 0;
     if (stream_want) stream_setup();
     int64_t ub = 0;
+    cudaStream_t main_st = st;
+    int nact = 0;
+    ph_begin(ISA_PH_WM_COLLAPSE);
     for (int w = 0; w < nwin; ++w) {
       const int64_t m = wrows[w];
       led.rows_read_back += m;
       led.merge_windows++;
       if (m == 0) continue;
+      const int buf = nact++ & 1;
       const int64_t most = std::min<int64_t>(m, D);
       if (ub + most > (int64_t)(result.lo.bytes / 8)) {
+        CK(cudaStreamSynchronize(dn_emit));
         result.n = read_u32(dscal32(25));
         ub = result.n;
         if (ub + most > (int64_t)(result.lo.bytes / 8)) {
@@ -2446,19 +2494,28 @@ struct Engine {
           grow_table(result, (size_t)ub + most);
         }
       }
-      ph_begin(ISA_PH_WM_COLLAPSE);
+      // accumulate on the compute stream once this array's previous window was emitted
+      CK(cudaStreamWaitEvent(st, dn_emit_done[buf], 0));
       kt_begin(KF_MERGE, st);
       dense_accum(dn_slices.as<DenseSlice>() + soff[w], (int)(soff[w + 1] - soff[w]), wblk[w], sd0, kmin + (u64)w * D, D,
-                  dstate, occ, st);
+                  dstate2[buf], occ2[buf], st);
       kt_end(KF_MERGE, wbytes[w] + m * 8 * S, st);
-      dense_count(dstate, occ, S, cnt_slot, D, dn_counts.as<u32>(), st);
+      CK(cudaEventRecord(dn_acc_done[buf], st));
+      // count, number and emit on the second stream (the helpers launch on `st`)
+      st = dn_emit;
+      CK(cudaStreamWaitEvent(st, dn_acc_done[buf], 0));
+      dense_count(dstate2[buf], occ2[buf], S, cnt_slot, D, dn_counts.as<u32>(), st);
       block_counts_scan(dn_counts.as<u32>(), nblocks, dscal32(26), dscal32(25), st);
-      dense_emit(dstate, occ, sd0, cnt_slot, D, kmin + (u64)w * D, dn_counts.as<u32>(), result.plo(), result.pst(), st);
+      dense_emit(dstate2[buf], occ2[buf], sd0, cnt_slot, D, kmin + (u64)w * D, dn_counts.as<u32>(), result.plo(),
+                 result.pst(), st);
       CK(cudaMemcpyAsync(dscal32(25), dscal32(26), sizeof(u32), cudaMemcpyDeviceToDevice, st));
-      ph_end(ISA_PH_WM_COLLAPSE, m, 0);
+      CK(cudaEventRecord(dn_emit_done[buf], st));
       if (streaming) stream_window((u32)std::min<int64_t>(m, 0xFFFFFFFFll));
+      st = main_st;
       ub += most;
     }
+    for (int i = 0; i < 2; ++i) CK(cudaStreamWaitEvent(st, dn_emit_done[i], 0));
+    ph_end(ISA_PH_WM_COLLAPSE, total, 0);
     result.n = read_u32(dscal32(25));
     if (result.n > 0xFFFFFFF0u) throw IsaError(ISA_ERR_INVALID_INPUT, "more than 2^32-1 output groups are not supported");
     return true;

@@ -241,15 +241,24 @@ __device__ __forceinline__ void st_relaxed_gpu(u64* p, u64 v) {
 // in *pk_const), PK 2 moves packed words, PK 3 unpacks on the way out to
 // the usual (key, row id) columns.  `shift` is then the digit's position
 // in the packed word.
+//
+// Carried values (PK 4 / 5, with plain PK 0 passes over the packed words in
+// between): the payload column holds a 4-byte value per row instead of the
+// row id, which sits in the packed word's low half.  PK 4 packs like PK 1
+// (row ids 0..n-1) and takes the payload from v_in = the values in row order;
+// PK 5 unpacks like PK 3 and also writes the payload, now in sorted order, to
+// carry_out -- the collapse then reads every row's value at its sorted
+// position instead of gathering it by row id.
 template <int KW, bool BALLOT, int PK = 0>
-__global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 1 ? 4 : 3)) k_rs_scatter(const u64* __restrict__ lo_in, const u64* __restrict__ hi_in,
+__global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : ((PK >= 1 && PK <= 3) ? 4 : 3)) k_rs_scatter(const u64* __restrict__ lo_in, const u64* __restrict__ hi_in,
                                                          const u32* __restrict__ v_in, u64* __restrict__ lo_out,
                                                          u64* __restrict__ hi_out, u32* __restrict__ v_out, u32 n,
                                                          int shift, u64* __restrict__ status,
                                                          const u32* __restrict__ ghist, u32* __restrict__ tile_ctr,
                                                          u32 epoch, int pk_lo, u64* __restrict__ pk_const,
-                                                         int lb_sleep) {
+                                                         int lb_sleep, u32* __restrict__ carry_out) {
   static_assert(PK == 0 || KW == 1, "packed passes carry one key word");
+  constexpr bool HASV = PK == 0 || PK >= 4;   // a payload column moves with the key words
   extern __shared__ __align__(16) unsigned char smem[];
   u32* wcnt = (u32*)smem;               // [RS_WARPS][256]
   u32* dstart = wcnt + RS_WARPS * 256;  // [256]
@@ -280,10 +289,10 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 1 ? 4 : 3)) k
     u32 gi = base + li;
     lo[it] = valid ? lo_in[gi] : 0;
     hi[it] = (KW == 2 && valid) ? hi_in[gi] : 0;
-    v[it] = (PK <= 1 && valid) ? ((PK == 1 && !v_in) ? gi : v_in[gi]) : 0;   // PK 1, null v_in: row ids 0..n-1
-    if (PK == 1) {
+    v[it] = ((PK <= 1 || PK >= 4) && valid) ? ((PK == 1 && !v_in) ? gi : v_in[gi]) : 0;   // PK 1, null v_in: row ids 0..n-1
+    if (PK == 1 || PK == 4) {
       if (gi == 0 && valid) *pk_const = lo[it] & ~(0xFFFFFFFFull << pk_lo);
-      lo[it] = (((lo[it] >> pk_lo) & 0xFFFFFFFFull) << 32) | v[it];
+      lo[it] = (((lo[it] >> pk_lo) & 0xFFFFFFFFull) << 32) | (PK == 4 ? gi : v[it]);
     }
   }
 #pragma unroll
@@ -348,7 +357,7 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 1 ? 4 : 3)) k
       u32 p = dstart[d] + wcnt[w * 256 + d] + (off[it] & 0xFFFFu);
       s_lo[p] = lo[it];
       if (KW == 2) s_hi[p] = hi[it];
-      if (!PK) s_v[p] = v[it];
+      if (HASV) s_v[p] = v[it];
     }
   }
   if (!status) {
@@ -380,7 +389,7 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 1 ? 4 : 3)) k
     }
     gbase[dg] = gs + excl - ds;
   }
-  const u64 kc = PK == 3 ? *pk_const : 0;
+  const u64 kc = (PK == 3 || PK == 5) ? *pk_const : 0;
   __syncthreads();
 #pragma unroll kRsWriteUnroll
   for (int it = 0; it < RS_ITEMS; ++it) {
@@ -390,13 +399,14 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : (PK >= 1 ? 4 : 3)) k
       u64 h = KW == 2 ? s_hi[p] : 0;
       u32 d = digit_kw<KW>(h, l, shift);
       u32 dst = gbase[d] + p;
-      if (PK == 3) {
+      if (PK == 3 || PK == 5) {
         lo_out[dst] = kc | ((l >> 32) << pk_lo);
         v_out[dst] = (u32)l;
+        if (PK == 5) carry_out[dst] = s_v[p];
       } else {
         lo_out[dst] = l;
         if (KW == 2) hi_out[dst] = h;
-        if (!PK) v_out[dst] = s_v[p];
+        if (HASV) v_out[dst] = s_v[p];
       }
     }
   }
@@ -639,6 +649,11 @@ static int radix_lsd(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
       cudaFuncSetAttribute(k_rs_scatter<1, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ps);
       cudaFuncSetAttribute(k_rs_scatter<1, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ps);
       cudaFuncSetAttribute(k_rs_scatter<1, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ps);
+      const int fs = (int)rs_scatter_smem(1);
+      cudaFuncSetAttribute(k_rs_scatter<1, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
+      cudaFuncSetAttribute(k_rs_scatter<1, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
+      cudaFuncSetAttribute(k_rs_scatter<1, false, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
+      cudaFuncSetAttribute(k_rs_scatter<1, true, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
     }
     if (KW == 2) {
       cudaFuncSetAttribute(k_rs_scatter<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_scatter_smem(2));
@@ -662,6 +677,14 @@ static int radix_lsd(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
                                    : (pack_lo == -1 && pk_env && KW == 1 && b.pack_ok && ntiles > 1 && npass >= 2 &&
                                       bit_hi - bit_lo <= 32);
   const int pk_lo = pack_lo >= 0 ? pack_lo : bit_lo;
+  // values carried through the sort as the payload (see k_rs_scatter, PK 4 / 5): opt-in (ISA_CARRY=1, read
+  // per sort) -- measured on config 5 at 4e9 rows the collapse without the gather saves 19 ms and the
+  // 12-byte passes at 3 CTAs/SM cost 24 ms (sort 154 -> 177 ms, collapse 98 -> 80 ms)
+  const char* ce = getenv("ISA_CARRY");
+  const int carry_env = ce && ce[0] == '1' ? 1 : 0;
+  const bool carry = carry_env && packed && pack_lo == -1 && !leave_packed && b.val_iota && b.carry_in && b.carry_out &&
+                     npass >= 2;
+  b.carried = carry;
   const size_t psmem = rs_scatter_smem(1, true);
   static int lb_sleep = -1;   // look-back back-off (ns) while a predecessor has not published
   if (lb_sleep < 0) { const char* e = getenv("ISA_LB_SLEEP"); lb_sleep = e ? atoi(e) : 0; }
@@ -716,33 +739,45 @@ static int radix_lsd(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
     const u32 ep = one ? 0u : ((g_rs_epoch.fetch_add(1) % 0x3FFFFFFEu) + 1u);
 #define RS_GO(K, BL, HI_IN, HI_OUT)                                                                          \
   klaunch(k_rs_scatter<K, BL>, ntiles, RS_THREADS, smem, st, b.lo[cur], HI_IN, b.val[cur], b.lo[nxt], HI_OUT, \
-          b.val[nxt], n, shift, stt, gh, tc, ep, 0, (u64*)nullptr, lb_sleep)
+          b.val[nxt], n, shift, stt, gh, tc, ep, 0, (u64*)nullptr, lb_sleep, (u32*)nullptr)
 #define RS_PK(PK)                                                                                            \
   do {                                                                                                       \
     if (ballot[p])                                                                                           \
       klaunch(k_rs_scatter<1, true, PK>, ntiles, RS_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,      \
               b.val[cur], b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - pk_lo, stt, gh, tc, ep, pk_lo,   \
-              pk_const, lb_sleep);                                                                                     \
+              pk_const, lb_sleep, (u32*)nullptr);                                                                      \
     else                                                                                                     \
       klaunch(k_rs_scatter<1, false, PK>, ntiles, RS_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,     \
               b.val[cur], b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - pk_lo, stt, gh, tc, ep, pk_lo,   \
-              pk_const, lb_sleep);                                                                                     \
+              pk_const, lb_sleep, (u32*)nullptr);                                                                      \
   } while (0)
     // algorithmic bytes of the pass: every row's key words + row id read and written once
     // (packed passes: 8-byte words in the middle, 12 -> 8 / 8 -> 12 at the ends)
     const int64_t pass_bytes =
-        (int64_t)n * (packed ? (p == 0 || (p == npass - 1 && !leave_packed) ? 20 : 16) : 2 * (8 * KW + 4));
+        (int64_t)n * (carry ? (p == npass - 1 ? 28 : 24)
+                            : packed ? (p == 0 || (p == npass - 1 && !leave_packed) ? 20 : 16) : 2 * (8 * KW + 4));
     kt_begin(KF_SCATTER, st);
-    if (packed) {
+    if (carry) {
+      // (packed word, value) pairs: PK 4 in, plain passes over the word's key half, PK 5 out
+      const int wshift = 32 + shift - pk_lo;
+      const u32* vin = p == 0 ? b.carry_in : b.val[cur];
+#define RS_CARRY(BL, PKM)                                                                                       \
+  klaunch(k_rs_scatter<1, BL, PKM>, ntiles, RS_THREADS, smem, st, b.lo[cur], (const u64*)nullptr, vin, b.lo[nxt], \
+          (u64*)nullptr, b.val[nxt], n, wshift, stt, gh, tc, ep, pk_lo, pk_const, lb_sleep, b.carry_out)
+      if (p == 0) { if (ballot[p]) RS_CARRY(true, 4); else RS_CARRY(false, 4); }
+      else if (p == npass - 1) { if (ballot[p]) RS_CARRY(true, 5); else RS_CARRY(false, 5); }
+      else { if (ballot[p]) RS_CARRY(true, 0); else RS_CARRY(false, 0); }
+#undef RS_CARRY
+    } else if (packed) {
       if (p == 0 && b.val_iota) {   // row ids 0..n-1: the pass numbers the rows itself (no row-id read)
         if (ballot[p])
           klaunch(k_rs_scatter<1, true, 1>, ntiles, RS_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,
                   (const u32*)nullptr, b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - pk_lo, stt, gh, tc, ep, pk_lo,
-                  pk_const, lb_sleep);
+                  pk_const, lb_sleep, (u32*)nullptr);
         else
           klaunch(k_rs_scatter<1, false, 1>, ntiles, RS_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,
                   (const u32*)nullptr, b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - pk_lo, stt, gh, tc, ep, pk_lo,
-                  pk_const, lb_sleep);
+                  pk_const, lb_sleep, (u32*)nullptr);
       } else if (p == 0) RS_PK(1);
       else if (p == npass - 1 && !leave_packed) RS_PK(3);
       else RS_PK(2);
@@ -1278,7 +1313,7 @@ __global__ void __launch_bounds__(CB_THREADS) k_seg_reduce_b(const u64* __restri
                                                              const u32* __restrict__ bbase, u64* __restrict__ out_lo,
                                                              u64* __restrict__ out_hi, u64* __restrict__ out_st,
                                                              u64* __restrict__ partial, u32* __restrict__ partial_slot,
-                                                             u64 add_lo, u64 add_hi) {
+                                                             u64 add_lo, u64 add_hi, int by_pos) {
   const int S = sd.nslots;
   constexpr u32 CLI = (u32)cl_items(MS);
   const u32 t = blockIdx.x * CB_THREADS + threadIdx.x;
@@ -1334,7 +1369,7 @@ __global__ void __launch_bounds__(CB_THREADS) k_seg_reduce_b(const u64* __restri
     bool head = (i == 0) || !key_eq<KW>(h, l, prev_hi, prev_lo);
     prev_lo = l; prev_hi = h;
     if (v >= limit) continue;
-    if (S) load_state_row<MS>(sd, row0, st_in, v, cur);
+    if (S) load_state_row<MS>(sd, by_pos ? (i64)0 : row0, st_in, by_pos ? i : v, cur);   // by_pos: values in sorted order
     if (head) {
       if (have) flush();
       have = true; lead = false;
@@ -1757,6 +1792,13 @@ u32 collapse_tiles(u32 m, int S) {
   return (m + tile - 1) / tile;
 }
 
+// value columns addressed by sorted position (CollapseTmp::by_pos) need the block-count path
+bool collapse_by_pos_ok(u32 m, int S) {
+  const char* e = getenv("ISA_COLLAPSE");
+  if (e && (e[0] == 'r' || e[0] == 'f')) return false;
+  return (collapse_threads(m, S) + 127) / 128 <= 1024u * 1024u;
+}
+
 void collapse(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, u32 limit, const SlotDesc& sd,
               int64_t row0, const u64* st_in, u64* out_lo, u64* out_hi, u64* out_st, CollapseTmp& tmp,
               cudaStream_t st) {
@@ -1792,7 +1834,7 @@ void collapse(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, u32 l
 #define CB_CNT(K, M) klaunch(k_cl_count<K, M>, blocks, CB_THREADS, 0, st, lo, hi, val, m, limit, tmp.flags)
 #define CB_RED(K, M) klaunch(k_seg_reduce_b<K, M>, blocks, CB_THREADS, 0, st, lo, hi, val, m, limit, sd, (i64)row0, \
                              st_in, (const u32*)tmp.flags, out_lo, out_hi, out_st, tmp.partial, tmp.partial_slot, \
-                             tmp.key_add_lo, tmp.key_add_hi)
+                             tmp.key_add_lo, tmp.key_add_hi, tmp.by_pos ? 1 : 0)
 #define CB_KW(K, X) { if (S <= 1) X(K, 1); else if (S <= 2) X(K, 2); else if (S <= 4) X(K, 4); \
                       else if (S <= 5) X(K, 5); else if (S <= 8) X(K, 8); else X(K, 16); }
     if (KW == 2) CB_KW(2, CB_CNT) else CB_KW(1, CB_CNT)

@@ -26,6 +26,11 @@ struct SortBufs {
   int hint_bit_lo = -1, hint_npass = 0;
   bool pack_ok = false;   // key bits outside [bit_lo, bit_hi) are equal in every key (packed passes allowed)
   bool val_iota = false;  // val[0][i] == i (row ids 0..n-1): a packing first pass numbers the rows itself
+  // carried values: carry_in[i] = a 4-byte value of row i; when the sort runs packed passes it moves the
+  // values with the keys and leaves them in sorted order in carry_out (carried = true on return)
+  const u32* carry_in = nullptr;
+  u32* carry_out = nullptr;
+  bool carried = false;
 };
 size_t sort_aux_bytes(u32 n);
 int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStream_t st, int64_t* launches,
@@ -89,7 +94,9 @@ struct CollapseTmp {
   // the table's row 0) and *total receives *dev_base + groups (block-count path)
   const u32* dev_base = nullptr;
   u64 key_add_lo = 0, key_add_hi = 0;   // added to every output key (block-count path; window-relative keys)
+  bool by_pos = false;   // value columns are addressed by sorted position, not by val[i] (carried values)
 };
+bool collapse_by_pos_ok(u32 m, int S);
 // s = window keys - (lhi:llo) (128-bit), val = 0..m-1
 void window_keys(int KW, const u64* slo, const u64* shi, u32 m, u64 llo, u64 lhi, u64* dlo, u64* dhi, u32* val,
                  cudaStream_t st);

@@ -978,3 +978,30 @@ def test_dense_window_merge_not_for_sparse_or_float(monkeypatch):
     w = workloads.make(3, rows=1_000_000, device="cpu", domain=1 << 20)   # hashed int64 keys, float sums
     op = _oracle_case(w, 1 << 14, page=100, rel=1e-5)
     assert _phase_ms(op, "wm_sort") > 0
+
+
+@pytest.mark.parametrize("case", ["fits_int32", "one_wide_value", "carry_off", "wide_keys"])
+def test_carried_values_through_the_sort(case, monkeypatch):
+    """Fill cycles above 2^20 rows with one int64 value column: the values
+    (narrowed to int32) ride through the packed radix passes and the collapse
+    reads them in sorted order; a value outside int32 falls back to the
+    gather from the column, keys spanning more than 32 bits to the gather from
+    the int32 copy.  Output and ledger equal the oracles either way."""
+    rng = np.random.default_rng(21)
+    n, memory = 5_000_000, 1 << 21
+    k = rng.integers(0, 1 << 22, n).astype(np.int64)
+    if case == "wide_keys":
+        k = k * ((1 << 40) + 12345)   # order-preserving spread: 62 varying bits, no packed passes
+    v = rng.integers(-1_000_000, 1_000_001, n).astype(np.int64)
+    if case == "one_wide_value":
+        v[n // 3] = 1 << 40
+    monkeypatch.setenv("ISA_CARRY", "0" if case == "carry_off" else "1")   # opt-in path under test
+    sch = _cut_schema()
+    slots = oracle.make_states(sch, {"v": v}, n)
+    want_keys, want_slots = oracle.reference_aggregate([k], slots, oracle.slot_ops(sch))
+    _, _, led, cycles = oracle.rsw_sortagg([k], slots, oracle.slot_ops(sch), memory, 100)
+    op = isa.SortAggregate(sch, _cfg(memory, 100))
+    res = op.execute_columns([_cuda(k)], {"v": _cuda(v)})
+    _check(res, want_keys, want_slots)
+    assert op.cycles == [c for c in cycles if c > 0] and min(op.cycles) > (1 << 20)
+    assert op.ledger.rows_spilled == led["rows_spilled"] and op.runs_after_generation == led["runs"]
