@@ -981,16 +981,40 @@ struct Engine {
   // first run is packed to learn the ratio.
   int64_t rows_left = 0;              // input rows not yet consumed (updated per chunk)
   double packed_ratio = -1;           // packed / raw bytes of the last packed run
-  // Opt-in (ISA_RAW_RUNS=1): measured config 5 at 1e9 rows 189 -> 192 ms (no
-  // pack, but the wide merge's D2D slice copies of raw runs cost more than
-  // unpacking) and out of memory at 4e9 rows (the result's growth no longer fits).
-  bool raw_fits_hbm(u32 rows) const {
-    static int env = -1;
-    if (env < 0) { const char* e = getenv("ISA_RAW_RUNS"); env = e && e[0] == '1' ? 1 : 0; }
-    if (!env || cfg.run_tier != ISA_TIER_AUTO || packed_ratio < 0) return false;
+  // Raw runs pay off when the wide merge reads them in place -- the
+  // dense-window merge (predicted from the first run: one key word, integer
+  // slots, a key span of at most 4 keys per input row): no pack, and the
+  // accumulate kernel reads 8 * (KW + S) bytes per row instead of decoding.
+  // For the sort-based windows they do not (config 5 at 1e9 rows 189 -> 192
+  // ms: the D2D slice copies cost more than unpacking).  Raw runs take at most
+  // 30% of the memory free at the start of the execute (packed runs up to
+  // 50%, hbm_left): the result and the caller's output columns still have to
+  // fit.  ISA_RAW_RUNS=1 / 0 forces raw runs whenever they fit hbm_left / off.
+  int dense_pred = -1;     // per execute: -1 unknown, 0 / 1 the dense-window merge is expected
+  double raw_left = 0;     // bytes of raw runs still allowed
+  bool raw_fits_hbm(u32 rows) {
+    const char* e = getenv("ISA_RAW_RUNS");
+    if ((e && e[0] == '0') || cfg.run_tier != ISA_TIER_AUTO || packed_ratio < 0) return false;
     const double row_b = 8.0 * (KW + S);
     const double need = (double)rows * row_b + (double)rows_left * row_b * packed_ratio;
-    return need <= (double)hbm_left;
+    if (need > (double)hbm_left) return false;
+    if (e && e[0] == '1') return true;
+    if (dense_pred != 1 || (double)rows * row_b > raw_left) return false;
+    raw_left -= (double)rows * row_b;
+    return true;
+  }
+  // first run: is the dense-window merge likely (see dense_merge)?
+  void predict_dense() {
+    if (dense_pred >= 0) return;
+    dense_pred = 0;
+    if (KW != 1 || T.n < 2 || cfg.run_tier != ISA_TIER_AUTO) return;
+    for (int s = 0; s < S; ++s)
+      if (sd0.type[s] != ST_I64) return;
+    u64 ends[2];
+    CK(cudaMemcpyAsync(&ends[0], T.plo(), 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&ends[1], T.plo() + (T.n - 1), 8, cudaMemcpyDeviceToHost, st));
+    sync();
+    dense_pred = (double)(ends[1] - ends[0]) < 4.0 * (double)in_n ? 1 : 0;
   }
 
   // T packed on the GPU (isa_codec.cu), then the packed bytes cross PCIe.
@@ -1194,6 +1218,7 @@ struct Engine {
       return;
     }
     u32* dir = make_dir();
+    predict_dense();
     if (pack_runs(T.n) && !raw_fits_hbm(T.n)) {
       Run r = spill_packed(T);
       r.dir = dir;
@@ -2918,6 +2943,8 @@ struct Engine {
     in_n = n;
     in_on_host = on_host;
     streaming = streamed_ok = false;
+    dense_pred = -1;
+    raw_left = 0;
     for (int c = 0; c < sch.n_key_cols; ++c) in_keys[c] = key_cols[c];
     if (cfg.run_tier == ISA_TIER_AUTO) {
       size_t fr = 0, tot = 0;
@@ -2926,6 +2953,7 @@ struct Engine {
       // from the previous execute, reused before anything new is allocated)
       hbm_left = cfg.hbm_run_budget > 0 ? cfg.hbm_run_budget
                                         : (int64_t)(0.5 * ((double)fr + (double)devpool.capacity()));
+      raw_left = 0.6 * (double)hbm_left;
     }
     if (cfg.merge_mode != ISA_MERGE_WIDE) {
       auto t0p = std::chrono::steady_clock::now();
