@@ -184,12 +184,22 @@ def _cpu_baseline(w, sample_rows, threads):
     return n / secs, n, secs, len(out_keys[0])
 
 
-def _traffic(cfgno, fam):
-    """ncu dram bytes per launch of a kernel family (profiles/ncu_traffic.json)."""
+def _traffic(cfgno, fam, alg_bytes_per_launch=None):
+    """ncu dram bytes per launch of a kernel family (profiles/ncu_traffic.json):
+    a captured per-launch figure, or -- launches of a family differ in size --
+    the captured DRAM bytes per algorithmic byte times this run's mean
+    algorithmic bytes per launch."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            t = json.load(f).get(f"config{cfgno}", {}).get(fam)
-        return t.get("dram_bytes_per_launch") if t else None
+            d = json.load(f).get(f"config{cfgno}", {})
+        t = d.get(fam) or (d if d.get("phase") == fam else None)
+        if not t:
+            return None
+        if "dram_bytes_per_launch" in t:
+            return t["dram_bytes_per_launch"]
+        if "dram_bytes_per_alg_byte" in t and alg_bytes_per_launch:
+            return t["dram_bytes_per_alg_byte"] * alg_bytes_per_launch
+        return None
     except Exception:
         return None
 
@@ -204,7 +214,7 @@ def _kernel_roofline(ks, steps, peak, peak_src, cfgno):
     per_launch_ms = d["ms"] / d["launches"]
     achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": _traffic(cfgno, dom),
+            "frac": achieved / peak, "traffic": _traffic(cfgno, dom, per_launch_bytes),
             "alg_bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
             "launches_per_step": d["launches"] / max(1, steps), "peak_source": peak_src,
             "timing": "CUDA events around every launch of the family on its stream, timed region"}

@@ -1,37 +1,45 @@
-"""One-screen summary of an ncu --set full report's raw CSV (duration, DRAM
-bytes and throughput, occupancy, IPC, instructions, top stall reasons)."""
+#!/usr/bin/env python
+"""Text summary of an .ncu-rep (one block per profiled launch): duration,
+DRAM bytes, occupancy, IPC, instruction count, registers, grid and the top
+warp-stall reasons -- the lines committed under profiles/.
+usage: python tools/ncu_summary.py gpurun_out/x.ncu-rep [...]"""
 import csv
+import subprocess
 import sys
 
-WANT = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "dram read"),
-        ("dram__bytes_write.sum", "dram write"),
-        ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram % of peak"),
-        ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
-        ("sm__maximum_warps_per_active_cycle_pct", "theoretical occupancy %"),
-        ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
-        ("sm__inst_executed.avg.per_cycle_active", "IPC"), ("smsp__inst_executed.sum", "warp instructions"),
-        ("launch__registers_per_thread", "registers"), ("launch__grid_size", "grid"),
-        ("launch__block_size", "block")]
+KEYS = [("duration us", "gpu__time_duration.sum"), ("dram read MB", "dram__bytes_read.sum"),
+        ("dram write MB", "dram__bytes_write.sum"), ("dram % of peak", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+        ("L2 hit %", "lts__t_sector_hit_rate.pct"),
+        ("achieved occupancy %", "sm__warps_active.avg.pct_of_peak_sustained_active"),
+        ("IPC", "sm__inst_executed.avg.per_cycle_elapsed"), ("warp instructions", "smsp__inst_executed.sum"),
+        ("registers", "launch__registers_per_thread"), ("grid", "launch__grid_size"), ("block", "launch__block_size")]
 
 
-def main(path):
-    r = list(csv.reader(open(path)))
-    hdr, units = r[0], r[1]
-    for row in r[2:]:
-        name = row[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
-        print(f"kernel: {name}")
-        for key, label in WANT:
-            if key in hdr:
-                i = hdr.index(key)
-                print(f"  {label:26s} {row[i]} {units[i]}")
-        st = [(h, row[i]) for i, h in enumerate(hdr) if h.startswith("smsp__pcsamp_warps_issue_stalled_")
-              and not h.endswith("not_issued") and row[i]]
-        tot = sum(float(v.replace(",", "")) for _, v in st) or 1
-        top = sorted(st, key=lambda x: -float(x[1].replace(",", "")))[:6]
-        print("  stalls: " + ", ".join(f"{h.replace('smsp__pcsamp_warps_issue_stalled_', '')} "
-                                       f"{float(v.replace(',', '')) / tot * 100:.0f}%" for h, v in top))
+def main():
+    for path in sys.argv[1:]:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(out.splitlines()))
+        if len(rows) < 3:
+            print(f"# {path}: no launches")
+            continue
+        h, units = rows[0], rows[1]
+        print(f"# {path}")
+        for row in rows[2:]:
+            print("kernel:", row[h.index("Kernel Name")])
+            for label, k in KEYS:
+                if k in h:
+                    print(f"  {label:<22} {row[h.index(k)]} {units[h.index(k)] if 'bytes' in k else ''}".rstrip())
+            st = {}
+            for i, k in enumerate(h):
+                if k.startswith("smsp__average_warps_issue_stalled") and k.endswith("per_issue_active.ratio"):
+                    try:
+                        st[k.split("stalled_")[1].split("_per")[0]] = float(row[i])
+                    except ValueError:
+                        pass
+            tot = sum(st.values()) or 1.0
+            top = sorted(st.items(), key=lambda x: -x[1])[:6]
+            print("  stalls:", ", ".join(f"{k} {100 * v / tot:.0f}%" for k, v in top))
 
 
 if __name__ == "__main__":
-    for p in sys.argv[1:]:
-        main(p)
+    main()
