@@ -108,7 +108,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
         except Exception:
@@ -324,6 +324,13 @@ def measure(torch, dist, cfgno, rows_total, run_tier, steps, warmup, world, rank
             torch.cuda.synchronize(dev)
     barrier()
     stream = torch.cuda.current_stream(dev)
+    # kernel timing records two CUDA events per timed launch: create them all
+    # now (one untimed step counts the launches), not inside the timed region
+    l0 = _native.launch_count()
+    res = None
+    res = step()
+    torch.cuda.synchronize(dev)
+    _native.kernel_timing_reserve(2 * (steps + 1) * (_native.launch_count() - l0) + 64)
     _native.set_kernel_timing(True)
     _native.kernel_stats()          # drop anything recorded before the timed region
     launches0 = _native.launch_count()

@@ -323,6 +323,10 @@ typedef struct isa_kstat {
   int64_t bytes;
 } isa_kstat;
 ISA_API void isa_set_kernel_timing(int32_t on);
+/* Create `events` timing events now (this host thread), so that a timed
+ * region with kernel timing on creates none (cudaEventCreate costs a few
+ * microseconds each; two events per timed launch). */
+ISA_API void isa_kernel_timing_reserve(int64_t events);
 ISA_API int isa_kernel_stats(isa_kstat* out, int cap);
 
 /* --- multi-GPU range partitioning primitives -------------------------- */

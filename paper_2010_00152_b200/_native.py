@@ -50,7 +50,8 @@ EXPORTED_SYMBOLS = (
     "isa_sample_keys", "isa_partition", "isa_phase_stats", "isa_launch_count", "isa_steps",
     "isa_set_spill_dir", "isa_in_stream_aggregate", "isa_hash_aggregate", "isa_merge_intersect", "isa_partition_counts",
     "isa_scatter_to_peers", "isa_ipc_handle", "isa_ipc_open", "isa_ipc_close",
-    "isa_set_kernel_timing", "isa_kernel_stats", "isa_set_output_allocator", "isa_result_streamed",
+    "isa_set_kernel_timing", "isa_kernel_stats", "isa_kernel_timing_reserve", "isa_set_output_allocator",
+    "isa_result_streamed",
 )
 
 # isa_kernel_family (kernel-true roofline families)
@@ -204,6 +205,8 @@ def load():
     lib.isa_launch_count.argtypes = []
     lib.isa_set_kernel_timing.restype = None
     lib.isa_set_kernel_timing.argtypes = [ctypes.c_int32]
+    lib.isa_kernel_timing_reserve.restype = None
+    lib.isa_kernel_timing_reserve.argtypes = [ctypes.c_int64]
     lib.isa_kernel_stats.restype = ctypes.c_int
     lib.isa_kernel_stats.argtypes = [ctypes.POINTER(IsaKstat), ctypes.c_int]
     lib.isa_sample_keys.restype = ctypes.c_int
@@ -226,6 +229,11 @@ def launch_count():
 def set_kernel_timing(on):
     """CUDA-event timing of the library's main kernels (this host thread)."""
     load().isa_set_kernel_timing(1 if on else 0)
+
+
+def kernel_timing_reserve(events):
+    """Pre-create CUDA events for kernel timing (two per timed launch)."""
+    load().isa_kernel_timing_reserve(int(events))
 
 
 def kernel_stats():

@@ -28,6 +28,7 @@ enum KFam { KF_SCATTER = 0, KF_HIST, KF_COLLAPSE, KF_PACK, KF_UNPACK, KF_ABSORB,
             KF_HOT_PROBE, KF_HOT_ABSORB, KF_COUNT };
 bool kt_enabled();
 void kt_set(bool on);
+void kt_reserve(int64_t events);
 void kt_begin(int fam, cudaStream_t st);
 void kt_end(int fam, int64_t alg_bytes, cudaStream_t st);
 void kt_add_bytes(int fam, int64_t alg_bytes);   // to the family's last record (bytes known after the launch)

@@ -3634,6 +3634,7 @@ int isa_phase_stats(isa_handle* h, isa_phase* out, int cap) {
 int64_t isa_launch_count(void) { return (int64_t)isa::g_launches.load(); }
 
 void isa_set_kernel_timing(int32_t on) { isa::kt_set(on != 0); }
+void isa_kernel_timing_reserve(int64_t events) { isa::kt_reserve(events); }
 
 int isa_kernel_stats(isa_kstat* out, int cap) {
   double ms[isa::KF_COUNT];

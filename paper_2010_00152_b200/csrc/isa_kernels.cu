@@ -39,6 +39,13 @@ thread_local KTimer g_kt;
 
 bool kt_enabled() { return g_kt.on; }
 void kt_set(bool on) { g_kt.on = on; }
+void kt_reserve(int64_t events) {   // create the timing events ahead of a timed region
+  while ((int64_t)g_kt.pool.size() < events) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) break;
+    g_kt.pool.push_back(e);
+  }
+}
 void kt_begin(int fam, cudaStream_t st) {
   if (!g_kt.on) return;
   cudaEvent_t e = g_kt.get();
