@@ -786,19 +786,23 @@ struct Engine {
     ph_begin(ISA_PH_FLUSH);
     CK(cudaMemsetAsync(bitmap.p, 0, (size_t)nw * 4, st));
     CK(cudaMemsetAsync(dscal32(0), 0, sizeof(u32), st));
+    // chunks of mostly new keys (the previous chunk tells) mark the rows that
+    // are not new heads and select in the complement: far fewer bitmap atomics
+    const bool invert = !firstpos && m == span && new_frac_hint > 0.5 && flush_invert_env();
     new_heads(KW, s_lo[cur].as<u64>(), s_hi[cur].as<u64>(), s_val[cur].as<u32>(), m, T.plo(), T.phi(), tn_search,
-              bitmap.as<u32>(), dscal32(0), st, firstpos);
+              bitmap.as<u32>(), dscal32(0), st, firstpos, invert);
     const int64_t M = cfg.memory_budget;
     u32 k = (u32)(M - (int64_t)T.n + 1);   // >= 1: |T| <= M
     if (span <= (1u << 20)) {
       // small chunks: select the k-th new head speculatively and read both
       // numbers with one synchronization (the select is cheap here)
-      select_kth_bit(bitmap.as<u32>(), span, k, word_tmp.as<u32>(), scan_tmp.as<u32>(), dscal32(1), st);
+      select_kth_bit(bitmap.as<u32>(), span, k, word_tmp.as<u32>(), scan_tmp.as<u32>(), dscal32(1), st, invert);
       to_host(dscal32(0), 2 * sizeof(u32));
       ph_end(ISA_PH_FLUSH, m, 0);
       sync();
       const u32 n_new = h_scal[0], f = h_scal[1];
       last_new = n_new;
+      new_frac_hint = (double)n_new / (double)std::max<u32>(m, 1);
       return (int64_t)T.n + n_new <= M ? span : f;
     }
     to_host(dscal32(0), sizeof(u32));
@@ -806,15 +810,21 @@ struct Engine {
     sync();
     u32 n_new = h_scal[0];
     last_new = n_new;
+    new_frac_hint = (double)n_new / (double)std::max<u32>(m, 1);
     if ((int64_t)T.n + n_new <= M) return span;
     ph_begin(ISA_PH_FLUSH);
-    select_kth_bit(bitmap.as<u32>(), span, k, word_tmp.as<u32>(), scan_tmp.as<u32>(), dscal32(1), st);
+    select_kth_bit(bitmap.as<u32>(), span, k, word_tmp.as<u32>(), scan_tmp.as<u32>(), dscal32(1), st, invert);
     to_host(dscal32(1), sizeof(u32));
     ph_end(ISA_PH_FLUSH, 0, 0);
     sync();
     return h_scal[0];
   }
   u32 last_new = 0;
+  double new_frac_hint = 0;   // new keys / rows of the last large flush analysis (per execute)
+  static bool flush_invert_env() {   // ISA_FLUSH_INVERT=0 (read per call): always mark the new heads
+    const char* e = getenv("ISA_FLUSH_INVERT");
+    return !(e && e[0] == '0');
+  }
   // large-table absorb (isa_hot.cu): hash image of T, rebuilt when T changed
   DevBuf hb_klo, hb_khi, hb_idx, hot_hit;
   HotHash hh{};
@@ -2945,6 +2955,7 @@ struct Engine {
     streaming = streamed_ok = false;
     dense_pred = -1;
     raw_left = 0;
+    new_frac_hint = 0;
     for (int c = 0; c < sch.n_key_cols; ++c) in_keys[c] = key_cols[c];
     if (cfg.run_tier == ISA_TIER_AUTO) {
       size_t fr = 0, tot = 0;

@@ -1030,21 +1030,24 @@ void iota_u32(u32* v, u32 n, cudaStream_t st) {
 template <int KW>
 __global__ void k_new_heads(const u64* __restrict__ lo, const u64* __restrict__ hi, const u32* __restrict__ val,
                             u32 m, const u64* __restrict__ T_lo, const u64* __restrict__ T_hi, u32 t,
-                            u32* __restrict__ bitmap, u32* __restrict__ n_new, const u32* __restrict__ firstpos) {
+                            u32* __restrict__ bitmap, u32* __restrict__ n_new, const u32* __restrict__ firstpos,
+                            int invert) {
+  // invert (val[] is a permutation of the bitmap's positions): the rows that
+  // are NOT first occurrences of a new key set their bit instead -- the few
+  // duplicates of a chunk of mostly new keys rather than every row
   u32 cnt = 0;
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
     u64 l = lo[i], h = KW == 2 ? hi[i] : 0;
     bool head = (i == 0) || !key_eq<KW>(h, l, KW == 2 ? hi[i - 1] : 0, lo[i - 1]);
-    if (!head) continue;
-    bool in_t = false;
-    if (t) {
+    bool is_new = head;
+    if (head && t) {
       u32 p = lower_bound_key<KW>(T_lo, T_hi, t, h, l);
-      in_t = p < t && key_eq<KW>(KW == 2 ? T_hi[p] : 0, T_lo[p], h, l);
+      is_new = !(p < t && key_eq<KW>(KW == 2 ? T_hi[p] : 0, T_lo[p], h, l));
     }
-    if (!in_t) {
+    if (is_new) ++cnt;
+    if (is_new != (invert != 0)) {
       u32 pos = firstpos ? firstpos[val[i]] : val[i];
       atomicOr(&bitmap[pos >> 5], 1u << (pos & 31));
-      ++cnt;
     }
   }
   for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
@@ -1135,20 +1138,32 @@ void flush_small(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, co
 }
 
 void new_heads(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, const u64* T_lo, const u64* T_hi,
-               u32 t, u32* bitmap, u32* n_new, cudaStream_t st, const u32* firstpos) {
+               u32 t, u32* bitmap, u32* n_new, cudaStream_t st, const u32* firstpos, bool invert) {
   if (m == 0) return;
   int g = grid_for(m, 256);
-  if (KW == 2) klaunch(k_new_heads<2>, g, 256, 0, st, lo, hi, val, m, T_lo, T_hi, t, bitmap, n_new, firstpos);
-  else klaunch(k_new_heads<1>, g, 256, 0, st, lo, hi, val, m, T_lo, T_hi, t, bitmap, n_new, firstpos);
+  const int inv = invert ? 1 : 0;
+  if (KW == 2) klaunch(k_new_heads<2>, g, 256, 0, st, lo, hi, val, m, T_lo, T_hi, t, bitmap, n_new, firstpos, inv);
+  else klaunch(k_new_heads<1>, g, 256, 0, st, lo, hi, val, m, T_lo, T_hi, t, bitmap, n_new, firstpos, inv);
 }
 
-__global__ void k_popc_words(const u32* __restrict__ bm, u32 nw, u32* __restrict__ cnt) {
-  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x) cnt[i] = __popc(bm[i]);
+// word w of the bitmap as the selection sees it: complemented (bits beyond
+// nbits cleared) when the bitmap marks the rows that are not new heads
+__device__ __forceinline__ u32 sel_word(const u32* __restrict__ bm, u32 w, u32 nw, u32 nbits, int invert) {
+  u32 x = bm[w];
+  if (invert) {
+    x = ~x;
+    if (w == nw - 1 && (nbits & 31)) x &= (1u << (nbits & 31)) - 1;
+  }
+  return x;
 }
-__global__ void k_find_kth(const u32* __restrict__ bm, const u32* __restrict__ pre, u32 nw, u32 k,
+__global__ void k_popc_words(const u32* __restrict__ bm, u32 nw, u32 nbits, int invert, u32* __restrict__ cnt) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x)
+    cnt[i] = __popc(sel_word(bm, i, nw, nbits, invert));
+}
+__global__ void k_find_kth(const u32* __restrict__ bm, const u32* __restrict__ pre, u32 nw, u32 nbits, int invert, u32 k,
                            u32* __restrict__ out) {
   for (u32 w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) {
-    u32 word = bm[w];
+    u32 word = sel_word(bm, w, nw, nbits, invert);
     u32 p = pre[w], c = __popc(word);
     if (p < k && p + c >= k) {
       u32 need = k - p;  // 1-based within word
@@ -1161,12 +1176,14 @@ __global__ void k_find_kth(const u32* __restrict__ bm, const u32* __restrict__ p
   }
 }
 
-void select_kth_bit(const u32* bitmap, u32 nbits, u32 k, u32* word_tmp, u32* scan_tmp, u32* out, cudaStream_t st) {
+void select_kth_bit(const u32* bitmap, u32 nbits, u32 k, u32* word_tmp, u32* scan_tmp, u32* out, cudaStream_t st,
+                    bool invert) {
   u32 nw = (nbits + 31) / 32;
   int g = grid_for(nw, 256);
-  klaunch(k_popc_words, g, 256, 0, st, bitmap, nw, word_tmp);
+  const int inv = invert ? 1 : 0;
+  klaunch(k_popc_words, g, 256, 0, st, bitmap, nw, nbits, inv, word_tmp);
   scan_exclusive_u32(word_tmp, nw, scan_tmp, nullptr, st);
-  klaunch(k_find_kth, g, 256, 0, st, bitmap, word_tmp, nw, k, out);
+  klaunch(k_find_kth, g, 256, 0, st, bitmap, word_tmp, nw, nbits, inv, k, out);
 }
 
 // ====================================================== row records ====

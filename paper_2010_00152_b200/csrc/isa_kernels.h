@@ -65,7 +65,10 @@ void compact_groups(int KW, const u64* g_lo, const u64* g_hi, const u32* g_count
 // firstpos != nullptr: val[i] indexes firstpos[] (tile groups) for the row position
 void new_heads(int KW, const u64* lo, const u64* hi, const u32* val, u32 m,
                const u64* T_lo, const u64* T_hi, u32 t, u32* bitmap, u32* n_new,
-               cudaStream_t st, const u32* firstpos = nullptr);
+               cudaStream_t st, const u32* firstpos = nullptr, bool invert = false);
+// invert (val[] must be a permutation of 0..nbits-1): the bitmap marks the
+// rows that are not first occurrences of a new key; select_kth_bit with the
+// same flag selects in its complement
 // position of the k-th (1-based) set bit of bitmap (nbits bits) -> *out
 // whole flush analysis of a small chunk in one CTA: out_mapped[0] = new
 // keys, [1] = row of the k-th new key's first occurrence (span if fewer)
@@ -73,7 +76,7 @@ bool flush_small_ok(u32 span);
 void flush_small(int KW, const u64* lo, const u64* hi, const u32* val, u32 m, const u64* T_lo, const u64* T_hi, u32 t,
                  u32 span, u32 k, u32* out_mapped, cudaStream_t st);
 void select_kth_bit(const u32* bitmap, u32 nbits, u32 k, u32* word_tmp, u32* scan_tmp,
-                    u32* out, cudaStream_t st);
+                    u32* out, cudaStream_t st, bool invert = false);
 
 // ---- collapse (segmented reduce of a sorted sequence) -------------------
 // Elements i < m with val[i] < limit are grouped by equal key; each group
