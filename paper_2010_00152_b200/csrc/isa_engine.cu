@@ -682,7 +682,14 @@ struct Engine {
 
   // Sort (key, pos) pairs of rows row0 + pos[i] (pos == nullptr: row0 + i),
   // i < m.  Returns the buffer index holding the sorted result.
-  int sort_rows(const KeyDesc& kd, int64_t row0, const u32* pos, u32 m) {
+  // assume: sort on the varying-bit mask of the execute's earlier chunks
+  // instead of reading this chunk's mask back first (one host round trip
+  // less); the caller then verifies it at its next synchronization
+  // (sort_assumed, verify_assumed_mask)
+  u64 sticky_vlo = 0, sticky_vhi = 0;
+  bool sticky_ok = false, sort_assume = false, sort_assumed = false;
+  int sort_rows(const KeyDesc& kd, int64_t row0, const u32* pos, u32 m, bool assume = false) {
+    sort_assume = assume && sticky_ok && assume_env();
     ensure_sort(m);
     ph_begin(ISA_PH_SORT);
     CK(cudaMemsetAsync(dvary(), 0, 2 * sizeof(u64), st));
@@ -697,6 +704,19 @@ struct Engine {
   // known_v: the varying-bit mask is known on the host (a key-range window
   // [L, U): every key shares the bits above L ^ (U - 1)), no read-back
   bool sort_val_iota = false;   // the pending sort's payload is 0..m-1 (consumed by the next sort_built)
+  static bool assume_env() {   // ISA_ASSUME_MASK=0 (read per sort): always read the chunk's mask back
+    const char* e = getenv("ISA_ASSUME_MASK");
+    return !(e && e[0] == '0');
+  }
+  // after a synchronization that followed to_host(dvary(), 16, 104): did the
+  // chunk's varying bits stay inside the assumed mask?  (widens the mask if not)
+  bool verify_assumed_mask() {
+    const u64 alo = ((volatile u64*)h_scal)[52], ahi = ((volatile u64*)h_scal)[53];
+    const bool ok = !(alo & ~sticky_vlo) && !(ahi & ~sticky_vhi);
+    sticky_vlo |= alo;
+    sticky_vhi |= ahi;
+    return ok;
+  }
   // the pending sort may carry a 4-byte value per row (in row order) with the keys and leave it in sorted
   // order in sort_carry_out; sort_carried tells whether it did (packed passes only)
   const u32* sort_carry_in = nullptr;
@@ -705,6 +725,7 @@ struct Engine {
   int sort_built(u32 m, const u64* known_v = nullptr) {
     const bool iota = sort_val_iota;
     sort_val_iota = false;
+    sort_assumed = false;
     const u32* cin = sort_carry_in;
     u32* cout = sort_carry_out;
     sort_carry_in = nullptr;
@@ -719,12 +740,20 @@ struct Engine {
       // every key bit instead of a host round trip for the varying bits
       vlo = key_bits == 64 ? ~0ull : ((1ull << key_bits) - 1);
       vhi = 0;
+    } else if (sort_assume) {
+      vlo = sticky_vlo;
+      vhi = sticky_vhi;
+      sort_assumed = true;
     } else {
       to_host(dvary(), 2 * sizeof(u64));
       sync();
       vlo = ((u64*)h_scal)[0];
       vhi = ((u64*)h_scal)[1];
+      sticky_vlo |= vlo;
+      sticky_vhi |= vhi;
+      sticky_ok = true;
     }
+    sort_assume = false;
     int hb = -1, lb = 128;
     if (vhi) { hb = 127 - __builtin_clzll(vhi); }
     else if (vlo) { hb = 63 - __builtin_clzll(vlo); }
@@ -793,9 +822,10 @@ struct Engine {
               bitmap.as<u32>(), dscal32(0), st, firstpos, invert);
     const int64_t M = cfg.memory_budget;
     u32 k = (u32)(M - (int64_t)T.n + 1);   // >= 1: |T| <= M
-    if (span <= (1u << 20)) {
-      // small chunks: select the k-th new head speculatively and read both
-      // numbers with one synchronization (the select is cheap here)
+    if (span <= (1u << 20) || expect_flush) {
+      // small chunks, and chunks sized to end just past the next flush (the
+      // previous chunk flushed): select the k-th new head speculatively and
+      // read both numbers with one synchronization
       select_kth_bit(bitmap.as<u32>(), span, k, word_tmp.as<u32>(), scan_tmp.as<u32>(), dscal32(1), st, invert);
       to_host(dscal32(0), 2 * sizeof(u32));
       ph_end(ISA_PH_FLUSH, m, 0);
@@ -820,6 +850,7 @@ struct Engine {
     return h_scal[0];
   }
   u32 last_new = 0;
+  bool expect_flush = false;   // the current chunk was sized from the last fill cycle: a flush is likely
   double new_frac_hint = 0;   // new keys / rows of the last large flush analysis (per execute)
   static bool flush_invert_env() {   // ISA_FLUSH_INVERT=0 (read per call): always mark the new heads
     const char* e = getenv("ISA_FLUSH_INVERT");
@@ -1306,10 +1337,18 @@ struct Engine {
         sort_carry_out = rec_sorted.as<u32>();
       }
     }
-    int cur = sort_rows(kd, row0, nullptr, span);
-    const bool carried = sort_carried;
+    int cur = sort_rows(kd, row0, nullptr, span, /*assume=*/true);
+    bool carried = sort_carried;
+    const bool assumed = sort_assumed;
+    if (assumed) to_host(dvary(), 2 * sizeof(u64), 104);
     const bool t_empty = T.n == 0;
     u32 f = flush_point(cur, span, span);
+    if (assumed && !verify_assumed_mask()) {
+      // key bits outside the assumed mask vary in this chunk: sort again on its own mask
+      cur = sort_rows(kd, row0, nullptr, span);
+      carried = sort_carried;
+      f = flush_point(cur, span, span);
+    }
     // with T empty every group of the chunk before f is new: M of them on a
     // flush, else the new-key count the flush analysis already returned
     const int64_t known = t_empty ? (f < span ? cfg.memory_budget : (int64_t)last_new) : -1;
@@ -2956,6 +2995,8 @@ struct Engine {
     dense_pred = -1;
     raw_left = 0;
     new_frac_hint = 0;
+    sticky_vlo = sticky_vhi = 0;
+    sticky_ok = false;
     for (int c = 0; c < sch.n_key_cols; ++c) in_keys[c] = key_cols[c];
     if (cfg.run_tier == ISA_TIER_AUTO) {
       size_t fr = 0, tot = 0;
@@ -3052,7 +3093,9 @@ struct Engine {
       int64_t len = chunk_len(std::min(n, wend) - a, last_len, last_flushed, last_cycle, a - cycle_start);
       int64_t b = a + len;
       rows_left = n - a;
+      expect_flush = last_flushed;
       int64_t nxt = process_chunk(kd, sd, base, a, b);
+      expect_flush = false;
       last_flushed = nxt < b;
       if (last_flushed) {
         last_cycle = nxt - cycle_start;

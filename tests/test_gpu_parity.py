@@ -1005,3 +1005,26 @@ def test_carried_values_through_the_sort(case, monkeypatch):
     _check(res, want_keys, want_slots)
     assert op.cycles == [c for c in cycles if c > 0] and min(op.cycles) > (1 << 20)
     assert op.ledger.rows_spilled == led["rows_spilled"] and op.runs_after_generation == led["runs"]
+
+
+@pytest.mark.parametrize("memory", [64, 4096])
+def test_assumed_sort_mask_widens_mid_input(memory):
+    """Chunks are sorted on the varying key bits of the execute's earlier
+    chunks without reading their own mask back first; a chunk whose keys vary
+    in further bits (here: the key range jumps by 2^40, twice) is detected at
+    the flush analysis's synchronization and sorted again.  Output and ledger
+    equal the oracles."""
+    rng = np.random.default_rng(3)
+    parts = [rng.integers(0, 1 << 12, 150_000), (1 << 40) + rng.integers(0, 1 << 12, 150_000),
+             rng.integers(0, 1 << 50, 100_000), rng.integers(0, 1 << 12, 100_000)]
+    k = np.concatenate(parts).astype(np.int64)
+    v = rng.integers(-1000, 1000, len(k)).astype(np.int64)
+    sch = _cut_schema()
+    slots = oracle.make_states(sch, {"v": v}, len(k))
+    want_keys, want_slots = oracle.reference_aggregate([k], slots, oracle.slot_ops(sch))
+    _, _, led, cycles = oracle.rsw_sortagg([k], slots, oracle.slot_ops(sch), memory, min(100, memory // 2))
+    op = isa.SortAggregate(sch, _cfg(memory, min(100, memory // 2)))
+    res = op.execute_columns([_cuda(k)], {"v": _cuda(v)})
+    _check(res, want_keys, want_slots)
+    assert op.cycles == [c for c in cycles if c > 0]
+    assert op.ledger.rows_spilled == led["rows_spilled"] and op.runs_after_generation == led["runs"]
