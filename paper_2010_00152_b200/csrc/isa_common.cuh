@@ -269,6 +269,25 @@ __device__ __forceinline__ u32 block_excl_scan256(u32 v, u32* sw, u32* total) {
   return pre + x - v;
 }
 
+// exclusive scan across a block of NW warps; *total = block sum (sw: NW words)
+template <int NW>
+__device__ __forceinline__ u32 block_excl_scan_nw(u32 v, u32* sw, u32* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  u32 x = warp_incl_scan(v);
+  if (lane == 31) sw[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    u32 s = lane < NW ? sw[lane] : 0;
+    s = warp_incl_scan(s);
+    if (lane < NW) sw[lane] = s;
+  }
+  __syncthreads();
+  u32 pre = w ? sw[w - 1] : 0;
+  *total = sw[NW - 1];
+  __syncthreads();
+  return pre + x - v;
+}
+
 // ---- run codec value transforms (isa_codec.cu; shared with the tile merge's in-place decode)
 __device__ __forceinline__ u64 pk_fwd(u64 bits, int is_f64, int is_key) {
   if (is_key) return bits;

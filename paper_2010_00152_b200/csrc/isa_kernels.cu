@@ -178,8 +178,10 @@ void scan_exclusive_u32(u32* data, u32 n, u32* tmp, u32* total, cudaStream_t st)
 }
 
 // ======================================================== radix sort ====
-#define RS_THREADS 256
-#define RS_ITEMS 16
+#ifndef RS_THREADS
+#define RS_THREADS 256   // x 16 rows per thread; -DRS_THREADS=512 (x 8 rows, 48 instead of 32 warps/SM on the packed
+#endif                   // passes) measured no faster: config 5 scatter 113 = 113 ms, config 3 81 -> 89, config 4 54 -> 67
+#define RS_ITEMS (4096 / RS_THREADS)
 #define RS_TILE (RS_THREADS * RS_ITEMS)
 #define RS_WARPS (RS_THREADS / 32)
 #define RS_WARP_ITEMS (RS_TILE / RS_WARPS)
@@ -257,7 +259,7 @@ __device__ __forceinline__ void st_relaxed_gpu(u64* p, u64 v) {
 // carry_out -- the collapse then reads every row's value at its sorted
 // position instead of gathering it by row id.
 template <int KW, bool BALLOT, int PK = 0>
-__global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : ((PK >= 1 && PK <= 3) ? 4 : 3)) k_rs_scatter(const u64* __restrict__ lo_in, const u64* __restrict__ hi_in,
+__global__ void __launch_bounds__(RS_THREADS, (RS_THREADS == 256 ? (KW == 2 ? 2 : ((PK >= 1 && PK <= 3) ? 4 : 3)) : (KW == 2 ? 1 : ((PK >= 1 && PK <= 3) ? 3 : 2)))) k_rs_scatter(const u64* __restrict__ lo_in, const u64* __restrict__ hi_in,
                                                          const u32* __restrict__ v_in, u64* __restrict__ lo_out,
                                                          u64* __restrict__ hi_out, u32* __restrict__ v_out, u32 n,
                                                          int shift, u64* __restrict__ status,
@@ -270,8 +272,8 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : ((PK >= 1 && PK <= 3
   u32* wcnt = (u32*)smem;               // [RS_WARPS][256]
   u32* dstart = wcnt + RS_WARPS * 256;  // [256]
   u32* gbase = dstart + 256;            // [256]
-  u32* sw = gbase + 256;                // [8]
-  u64* s_lo = (u64*)(sw + 8);           // [RS_TILE]
+  u32* sw = gbase + 256;                // [RS_WARPS]
+  u64* s_lo = (u64*)(sw + RS_WARPS);    // [RS_TILE]
   u64* s_hi = s_lo + RS_TILE;           // [RS_TILE] (KW == 2)
   u32* s_v = (u32*)(s_lo + KW * RS_TILE);
 
@@ -337,22 +339,25 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : ((PK >= 1 && PK <= 3
   // aggregate is published now, but the look-back for its exclusive prefix
   // waits until the rows are staged, so predecessors have had that long to
   // publish (fewer spinning reloads)
-  const int dg = tid;  // RS_THREADS == 256: thread = digit
+  const int dg = tid;  // threads 0..255 own one digit each
+  const bool isd = dg < 256;
   u32 run = 0, ds, gs = 0;
   {
+    if (isd) {
 #pragma unroll
-    for (int ww = 0; ww < RS_WARPS; ++ww) {
-      u32 c = wcnt[ww * 256 + dg];
-      wcnt[ww * 256 + dg] = run;
-      run += c;
+      for (int ww = 0; ww < RS_WARPS; ++ww) {
+        u32 c = wcnt[ww * 256 + dg];
+        wcnt[ww * 256 + dg] = run;
+        run += c;
+      }
     }
     u32 tot;
-    ds = block_excl_scan256(run, sw, &tot);
-    dstart[dg] = ds;
+    ds = block_excl_scan_nw<RS_WARPS>(run, sw, &tot);
+    if (isd) dstart[dg] = ds;
     if (status) {
-      gs = block_excl_scan256(ghist[dg], sw, &tot);   // global start of digit dg
+      gs = block_excl_scan_nw<RS_WARPS>(isd ? ghist[dg] : 0u, sw, &tot);   // global start of digit dg
       const u64 E = (u64)epoch << 34;
-      st_relaxed_gpu(status + (size_t)tile * 256 + dg, E | ((tile == 0 ? 2ull : 1ull) << 32) | run);
+      if (isd) st_relaxed_gpu(status + (size_t)tile * 256 + dg, E | ((tile == 0 ? 2ull : 1ull) << 32) | run);
     }
   }
   __syncthreads();
@@ -367,7 +372,9 @@ __global__ void __launch_bounds__(RS_THREADS, KW == 2 ? 2 : ((PK >= 1 && PK <= 3
       if (HASV) s_v[p] = v[it];
     }
   }
-  if (!status) {
+  if (!isd) {
+    // no digit of its own
+  } else if (!status) {
     gbase[dg] = 0u;   // one tile: in-tile offsets are global
   } else {
     const u64 E = (u64)epoch << 34;
@@ -625,7 +632,7 @@ static size_t rl_smem(int KW, int cap) {
 }
 
 static size_t rs_scatter_smem(int KW, bool packed = false) {
-  return (RS_WARPS * 256 + 256 + 256 + 8) * sizeof(u32) + (size_t)RS_TILE * (packed ? 8 : 8 * KW + 4);
+  return (RS_WARPS * 256 + 256 + 256 + RS_WARPS) * sizeof(u32) + (size_t)RS_TILE * (packed ? 8 : 8 * KW + 4);
 }
 
 // aux layout: [ghist: RS_MAX_PASS * 256 u32][tile counters: RS_MAX_PASS u32][pad][status: 256 * ntiles u64].
