@@ -178,13 +178,25 @@ void scan_exclusive_u32(u32* data, u32 n, u32* tmp, u32* total, cudaStream_t st)
 }
 
 // ======================================================== radix sort ====
-#ifndef RS_THREADS
-#define RS_THREADS 256   // x 16 rows per thread; -DRS_THREADS=512 (x 8 rows, 48 instead of 32 warps/SM on the packed
-#endif                   // passes) measured no faster: config 5 scatter 113 = 113 ms, config 3 81 -> 89, config 4 54 -> 67
-#define RS_ITEMS (4096 / RS_THREADS)
+#define RS_THREADS 256   // x 16 rows per thread (512 x 8 measured no faster: config 5 scatter 113 = 113 ms, config 3
+                         // 81 -> 89, config 4 54 -> 67)
+#ifndef RS_PK_THREADS
+#define RS_PK_THREADS 512   // packed passes: 512 x 16 rows per tile
+#endif
+#define RS_ITEMS 16
 #define RS_TILE (RS_THREADS * RS_ITEMS)
 #define RS_WARPS (RS_THREADS / 32)
 #define RS_WARP_ITEMS (RS_TILE / RS_WARPS)
+// Packed passes (one 8-byte word per row) run 512-thread tiles of 8,192 rows
+// at 2 CTAs/SM -- the same 32 warps/SM as 4 tiles of 4,096, but the per-tile
+// work (digit scan, publish, look-back: a third of the pass's instructions)
+// is paid half as often; the other passes' tiles (12-20 bytes of shared
+// memory per row) stay at 256 threads.
+__host__ __device__ constexpr int rs_threads(int PK) { return (PK >= 1 && PK <= 3) ? RS_PK_THREADS : RS_THREADS; }
+__host__ __device__ constexpr int rs_min_ctas(int KW, int PK) {
+  return (PK >= 1 && PK <= 3) ? (RS_PK_THREADS == 512 ? 2 : 4) : (KW == 2 ? 2 : 3);
+}
+__host__ __device__ constexpr int rs_tile(int PK) { return rs_threads(PK) * RS_ITEMS; }
 
 __device__ __forceinline__ u32 digit_of(u64 hi, u64 lo, int shift) {
   u64 v;
@@ -259,7 +271,7 @@ __device__ __forceinline__ void st_relaxed_gpu(u64* p, u64 v) {
 // carry_out -- the collapse then reads every row's value at its sorted
 // position instead of gathering it by row id.
 template <int KW, bool BALLOT, int PK = 0>
-__global__ void __launch_bounds__(RS_THREADS, (RS_THREADS == 256 ? (KW == 2 ? 2 : ((PK >= 1 && PK <= 3) ? 4 : 3)) : (KW == 2 ? 1 : ((PK >= 1 && PK <= 3) ? 3 : 2)))) k_rs_scatter(const u64* __restrict__ lo_in, const u64* __restrict__ hi_in,
+__global__ void __launch_bounds__(rs_threads(PK), rs_min_ctas(KW, PK)) k_rs_scatter(const u64* __restrict__ lo_in, const u64* __restrict__ hi_in,
                                                          const u32* __restrict__ v_in, u64* __restrict__ lo_out,
                                                          u64* __restrict__ hi_out, u32* __restrict__ v_out, u32 n,
                                                          int shift, u64* __restrict__ status,
@@ -268,32 +280,34 @@ __global__ void __launch_bounds__(RS_THREADS, (RS_THREADS == 256 ? (KW == 2 ? 2 
                                                          int lb_sleep, u32* __restrict__ carry_out) {
   static_assert(PK == 0 || KW == 1, "packed passes carry one key word");
   constexpr bool HASV = PK == 0 || PK >= 4;   // a payload column moves with the key words
+  constexpr int THREADS = rs_threads(PK), ITEMS = RS_ITEMS, TILE = THREADS * ITEMS, WARPS = THREADS / 32,
+                WARP_ITEMS = TILE / WARPS;
   extern __shared__ __align__(16) unsigned char smem[];
-  u32* wcnt = (u32*)smem;               // [RS_WARPS][256]
-  u32* dstart = wcnt + RS_WARPS * 256;  // [256]
+  u32* wcnt = (u32*)smem;               // [WARPS][256]
+  u32* dstart = wcnt + WARPS * 256;  // [256]
   u32* gbase = dstart + 256;            // [256]
-  u32* sw = gbase + 256;                // [RS_WARPS]
-  u64* s_lo = (u64*)(sw + RS_WARPS);    // [RS_TILE]
-  u64* s_hi = s_lo + RS_TILE;           // [RS_TILE] (KW == 2)
-  u32* s_v = (u32*)(s_lo + KW * RS_TILE);
+  u32* sw = gbase + 256;                // [WARPS]
+  u64* s_lo = (u64*)(sw + WARPS);    // [TILE]
+  u64* s_hi = s_lo + TILE;           // [TILE] (KW == 2)
+  u32* s_v = (u32*)(s_lo + KW * TILE);
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (status && tid == 0) sw[0] = atomicAdd(tile_ctr, 1u);
   __syncthreads();
-  const u32 tile = status ? sw[0] : blockIdx.x, base = tile * RS_TILE;
-  const u32 tile_n = min((u32)RS_TILE, n - base);
-  for (int i = tid; i < RS_WARPS * 256; i += RS_THREADS) wcnt[i] = 0;
+  const u32 tile = status ? sw[0] : blockIdx.x, base = tile * TILE;
+  const u32 tile_n = min((u32)TILE, n - base);
+  for (int i = tid; i < WARPS * 256; i += THREADS) wcnt[i] = 0;
   __syncthreads();
 
-  u64 lo[RS_ITEMS], hi[RS_ITEMS];
-  u32 v[RS_ITEMS], off[RS_ITEMS];
+  u64 lo[ITEMS], hi[ITEMS];
+  u32 v[ITEMS], off[ITEMS];
   const u32 lt = lanemask_lt();
   // load + rank; full tiles (all but the last) drop every bounds test
   auto load_rank = [&](auto full_tag) {
   constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-  for (int it = 0; it < RS_ITEMS; ++it) {
-    u32 li = w * RS_WARP_ITEMS + it * 32 + lane;
+  for (int it = 0; it < ITEMS; ++it) {
+    u32 li = w * WARP_ITEMS + it * 32 + lane;
     const bool valid = FULL || li < tile_n;
     u32 gi = base + li;
     lo[it] = valid ? lo_in[gi] : 0;
@@ -305,8 +319,8 @@ __global__ void __launch_bounds__(RS_THREADS, (RS_THREADS == 256 ? (KW == 2 ? 2 
     }
   }
 #pragma unroll
-  for (int it = 0; it < RS_ITEMS; ++it) {
-    u32 li = w * RS_WARP_ITEMS + it * 32 + lane;
+  for (int it = 0; it < ITEMS; ++it) {
+    u32 li = w * WARP_ITEMS + it * 32 + lane;
     const bool valid = FULL || li < tile_n;
     u32 d = valid ? digit_kw<KW>(hi[it], lo[it], shift) : 256 + lane;
     // lanes holding the same digit: MATCH.ANY, or (BALLOT: chosen by the
@@ -332,7 +346,7 @@ __global__ void __launch_bounds__(RS_THREADS, (RS_THREADS == 256 ? (KW == 2 ? 2 
     __syncwarp();
   }
   };
-  if (tile_n == RS_TILE) load_rank(std::true_type{});
+  if (tile_n == TILE) load_rank(std::true_type{});
   else load_rank(std::false_type{});
   __syncthreads();
   // per-digit exclusive prefix over warps, then over digits; the tile's
@@ -345,25 +359,25 @@ __global__ void __launch_bounds__(RS_THREADS, (RS_THREADS == 256 ? (KW == 2 ? 2 
   {
     if (isd) {
 #pragma unroll
-      for (int ww = 0; ww < RS_WARPS; ++ww) {
+      for (int ww = 0; ww < WARPS; ++ww) {
         u32 c = wcnt[ww * 256 + dg];
         wcnt[ww * 256 + dg] = run;
         run += c;
       }
     }
     u32 tot;
-    ds = block_excl_scan_nw<RS_WARPS>(run, sw, &tot);
+    ds = block_excl_scan_nw<WARPS>(run, sw, &tot);
     if (isd) dstart[dg] = ds;
     if (status) {
-      gs = block_excl_scan_nw<RS_WARPS>(isd ? ghist[dg] : 0u, sw, &tot);   // global start of digit dg
+      gs = block_excl_scan_nw<WARPS>(isd ? ghist[dg] : 0u, sw, &tot);   // global start of digit dg
       const u64 E = (u64)epoch << 34;
       if (isd) st_relaxed_gpu(status + (size_t)tile * 256 + dg, E | ((tile == 0 ? 2ull : 1ull) << 32) | run);
     }
   }
   __syncthreads();
 #pragma unroll
-  for (int it = 0; it < RS_ITEMS; ++it) {
-    u32 li = w * RS_WARP_ITEMS + it * 32 + lane;
+  for (int it = 0; it < ITEMS; ++it) {
+    u32 li = w * WARP_ITEMS + it * 32 + lane;
     if (li < tile_n) {
       const u32 d = off[it] >> 16;
       u32 p = dstart[d] + wcnt[w * 256 + d] + (off[it] & 0xFFFFu);
@@ -406,8 +420,8 @@ __global__ void __launch_bounds__(RS_THREADS, (RS_THREADS == 256 ? (KW == 2 ? 2 
   const u64 kc = (PK == 3 || PK == 5) ? *pk_const : 0;
   __syncthreads();
 #pragma unroll kRsWriteUnroll
-  for (int it = 0; it < RS_ITEMS; ++it) {
-    u32 p = it * RS_THREADS + tid;
+  for (int it = 0; it < ITEMS; ++it) {
+    u32 p = it * THREADS + tid;
     if (p < tile_n) {
       u64 l = s_lo[p];
       u64 h = KW == 2 ? s_hi[p] : 0;
@@ -632,7 +646,8 @@ static size_t rl_smem(int KW, int cap) {
 }
 
 static size_t rs_scatter_smem(int KW, bool packed = false) {
-  return (RS_WARPS * 256 + 256 + 256 + RS_WARPS) * sizeof(u32) + (size_t)RS_TILE * (packed ? 8 : 8 * KW + 4);
+  const int threads = packed ? RS_PK_THREADS : RS_THREADS, warps = threads / 32;
+  return (warps * 256 + 256 + 256 + warps) * sizeof(u32) + (size_t)threads * RS_ITEMS * (packed ? 8 : 8 * KW + 4);
 }
 
 // aux layout: [ghist: RS_MAX_PASS * 256 u32][tile counters: RS_MAX_PASS u32][pad][status: 256 * ntiles u64].
@@ -678,6 +693,7 @@ static int radix_lsd(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
     }
   }
   const u32 ntiles = (n + RS_TILE - 1) / RS_TILE;
+  const u32 pk_tiles = (n + rs_tile(1) - 1) / rs_tile(1);   // packed passes run larger tiles
   const size_t smem = rs_scatter_smem(KW);
   const int npass = (bit_hi - bit_lo + 7) / 8;
   u32* ghist = (u32*)b.aux;
@@ -757,11 +773,11 @@ static int radix_lsd(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
 #define RS_PK(PK)                                                                                            \
   do {                                                                                                       \
     if (ballot[p])                                                                                           \
-      klaunch(k_rs_scatter<1, true, PK>, ntiles, RS_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,      \
+      klaunch(k_rs_scatter<1, true, PK>, pk_tiles, RS_PK_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr, \
               b.val[cur], b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - pk_lo, stt, gh, tc, ep, pk_lo,   \
               pk_const, lb_sleep, (u32*)nullptr);                                                                      \
     else                                                                                                     \
-      klaunch(k_rs_scatter<1, false, PK>, ntiles, RS_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,     \
+      klaunch(k_rs_scatter<1, false, PK>, pk_tiles, RS_PK_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr, \
               b.val[cur], b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - pk_lo, stt, gh, tc, ep, pk_lo,   \
               pk_const, lb_sleep, (u32*)nullptr);                                                                      \
   } while (0)
@@ -785,11 +801,11 @@ static int radix_lsd(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
     } else if (packed) {
       if (p == 0 && b.val_iota) {   // row ids 0..n-1: the pass numbers the rows itself (no row-id read)
         if (ballot[p])
-          klaunch(k_rs_scatter<1, true, 1>, ntiles, RS_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,
+          klaunch(k_rs_scatter<1, true, 1>, pk_tiles, RS_PK_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,
                   (const u32*)nullptr, b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - pk_lo, stt, gh, tc, ep, pk_lo,
                   pk_const, lb_sleep, (u32*)nullptr);
         else
-          klaunch(k_rs_scatter<1, false, 1>, ntiles, RS_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,
+          klaunch(k_rs_scatter<1, false, 1>, pk_tiles, RS_PK_THREADS, psmem, st, b.lo[cur], (const u64*)nullptr,
                   (const u32*)nullptr, b.lo[nxt], (u64*)nullptr, b.val[nxt], n, 32 + shift - pk_lo, stt, gh, tc, ep, pk_lo,
                   pk_const, lb_sleep, (u32*)nullptr);
       } else if (p == 0) RS_PK(1);
