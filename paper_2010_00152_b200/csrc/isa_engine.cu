@@ -1368,6 +1368,23 @@ struct Engine {
       row_pack(rpk, row0, f, rec_buf.as<char>(), st);
       r0c = 0;
     }
+    // a flush into an empty table whose run stays raw in HBM: the collapse
+    // writes the run's rows in place (no table, no device-to-device copy)
+    if (t_empty && f < span && cfg.run_tier == ISA_TIER_AUTO && dense_pred == 1 && !dirs_wanted() &&
+        pack_runs((u32)cfg.memory_budget) && raw_fits_hbm((u32)cfg.memory_budget)) {
+      Run r = alloc_run((u32)cfg.memory_budget);
+      if (!r.host) {
+        Table view;   // borrows the run's storage (DevBuf owns nothing by itself)
+        view.lo.p = r.lo; view.lo.bytes = (size_t)r.rows * 8;
+        view.st.p = r.st; view.st.bytes = (size_t)r.rows * 8 * S;
+        collapse_chunk(cur, span, f, sdc, r0c, nullptr, view, r.rows, true, known);
+        ++t_ver;
+        runs.push_back(r);
+        account_written(r);
+        return a + f;
+      }
+      // (not reached: raw_fits_hbm reserved the space) fall through with the host run unused
+    }
     collapse_chunk(cur, span, f, sdc, r0c, nullptr, U, tcap, true, known);
     merge_into_T();
     if (f < span) {
