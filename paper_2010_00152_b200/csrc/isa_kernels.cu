@@ -1365,13 +1365,42 @@ __global__ void __launch_bounds__(CB_THREADS) k_seg_reduce_b(const u64* __restri
   constexpr u32 CLI = (u32)cl_items(MS);
   const u32 t = blockIdx.x * CB_THREADS + threadIdx.x;
   const u32 i0 = t * CLI, i1 = min(i0 + CLI, m);
+  // States of <= 2 slots: the thread's items are read once into registers and
+  // every item's state row is requested before any is combined (CLI random
+  // gathers in flight per thread instead of one).
+  constexpr bool PF = MS <= 2;
+  constexpr u32 NPF = PF ? CLI : 1;
+  u64 L[NPF], Hh[NPF], C[NPF][MS];
+  u32 V[NPF];
+  if (PF && i0 < m) {
+#pragma unroll
+    for (u32 j = 0; j < NPF; ++j) {
+      const u32 i = i0 + j;
+      const bool ok = i < i1;
+      L[j] = ok ? lo[i] : 0;
+      Hh[j] = (KW == 2 && ok) ? hi[i] : 0;
+      V[j] = ok ? val[i] : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (u32 j = 0; j < NPF; ++j) {
+#pragma unroll
+      for (int k = 0; k < MS; ++k) C[j][k] = 0;
+      if (S && i0 + j < i1 && V[j] < limit)
+        load_state_row<MS>(sd, by_pos ? (i64)0 : row0, st_in, by_pos ? i0 + j : V[j], C[j]);
+    }
+  }
   // this thread's included heads -> its first group index (block scan)
   u32 c = 0;
   if (i0 < m) {
     u64 pl = i0 > 0 ? lo[i0 - 1] : 0, ph = (KW == 2 && i0 > 0) ? hi[i0 - 1] : 0;
-    for (u32 i = i0; i < i1; ++i) {
-      const u64 l = lo[i], h = KW == 2 ? hi[i] : 0;
-      c += (val[i] < limit && (i == 0 || !key_eq<KW>(h, l, ph, pl))) ? 1u : 0u;
+#pragma unroll(PF ? CLI : 1)
+    for (u32 jj = 0; jj < CLI; ++jj) {
+      const u32 i = i0 + jj;
+      if (i >= i1) break;
+      const u32 pj = PF ? jj : 0;
+      const u64 l = PF ? L[pj] : lo[i], h = KW == 2 ? (PF ? Hh[pj] : hi[i]) : 0;
+      const u32 vv = PF ? V[pj] : val[i];
+      c += (vv < limit && (i == 0 || !key_eq<KW>(h, l, ph, pl))) ? 1u : 0u;
       pl = l; ph = h;
     }
   }
@@ -1410,13 +1439,22 @@ __global__ void __launch_bounds__(CB_THREADS) k_seg_reduce_b(const u64* __restri
         if (k < S) out_st[(size_t)slot * S + k] = acc[k];
     }
   };
-  for (u32 i = i0; i < i1; ++i) {
-    u64 l = lo[i], h = KW == 2 ? hi[i] : 0;
-    u32 v = val[i];
+#pragma unroll(PF ? CLI : 1)
+  for (u32 jj = 0; jj < CLI; ++jj) {
+    const u32 i = i0 + jj;
+    if (i >= i1) break;
+    const u32 pj = PF ? jj : 0;
+    u64 l = PF ? L[pj] : lo[i], h = KW == 2 ? (PF ? Hh[pj] : hi[i]) : 0;
+    u32 v = PF ? V[pj] : val[i];
     bool head = (i == 0) || !key_eq<KW>(h, l, prev_hi, prev_lo);
     prev_lo = l; prev_hi = h;
     if (v >= limit) continue;
-    if (S) load_state_row<MS>(sd, by_pos ? (i64)0 : row0, st_in, by_pos ? i : v, cur);   // by_pos: values in sorted order
+    if (PF) {
+#pragma unroll
+      for (int k = 0; k < MS; ++k) cur[k] = C[pj][k];
+    } else if (S) {
+      load_state_row<MS>(sd, by_pos ? (i64)0 : row0, st_in, by_pos ? i : v, cur);   // by_pos: values in sorted order
+    }
     if (head) {
       if (have) flush();
       have = true; lead = false;
