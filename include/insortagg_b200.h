@@ -273,16 +273,23 @@ ISA_API int isa_result_copy(isa_handle* h, void* const* key_out, void* const* sl
 /* Output allocator.  The reference hands the caller fresh result rows it owns
  * (SortAggregate.execute, sortagg.py:744-757); here the caller owns the
  * output columns too: `fn(user, capacity, key_out, slot_out)` is called at
- * most once per isa_execute -- only with host input that spilled, once the
- * wide merge's first key-range window is merged (capacity = the estimated
- * output size plus a margin) -- and fills key_out[i] / slot_out[s] with
- * pinned host columns of `capacity` elements (key columns in their input
- * dtype, slots 8 bytes), returning 0 (nonzero: decline).  The wide merge then
- * copies every merged window's groups into them while the next window merges
- * (sortagg.py:588-674 yields rows as the merge advances).  isa_result_streamed() == 1 after isa_execute means the columns
- * hold rows [0, n_groups) and isa_result_copy is not needed; 0 (no spill,
- * device input, declined, or more groups than `capacity`): read the result
- * with isa_result_copy as usual.  fn = NULL removes the allocator. */
+ * most once per isa_execute and fills key_out[i] / slot_out[s] with columns
+ * of `capacity` elements (key columns in their input dtype, slots 8 bytes) in
+ * the input's memory space -- device memory for device input, pinned host
+ * memory for host input -- returning 0 (nonzero: decline).
+ *  - Host input that spilled: the call comes once the wide merge's first
+ *    key-range window is merged, with capacity = the estimated output size
+ *    plus a margin, and the wide merge copies every merged window's groups
+ *    into the columns while the next window merges (sortagg.py:588-674 yields
+ *    rows as the merge advances).
+ *  - Otherwise (device input, or nothing spilled): the call comes at the end
+ *    of isa_execute with capacity = n_groups exactly and the columns are
+ *    filled before it returns.
+ * isa_result_streamed() != 0 after isa_execute means the columns hold rows
+ * [0, n_groups) and isa_result_copy is not needed (2: filled while the wide
+ * merge ran, 1: at the end of the call); 0 (declined, no groups, or
+ * more groups than the streamed capacity): read the result with
+ * isa_result_copy as usual.  fn = NULL removes the allocator. */
 typedef int (*isa_alloc_fn)(void* user, int64_t capacity, void** key_out, void** slot_out);
 ISA_API int isa_set_output_allocator(isa_handle* h, isa_alloc_fn fn, void* user);
 ISA_API int isa_result_streamed(isa_handle* h);

@@ -355,7 +355,9 @@ class Handle:
         self._check(self._lib.isa_set_output_allocator(self._h, self._alloc_cb, None))
 
     def result_streamed(self):
-        return bool(self._lib.isa_result_streamed(self._h))
+        """0: read with result_copy; 1: the allocator's columns were filled at
+        the end of the execute; 2: while the wide merge ran."""
+        return int(self._lib.isa_result_streamed(self._h))
 
     def result_copy(self, key_ptrs, slot_ptrs, on_host, stream):
         self._check(self._lib.isa_result_copy(self._h, _ptr_array(key_ptrs), _ptr_array(slot_ptrs),

@@ -2363,6 +2363,8 @@ struct Engine {
   // cycle, total run rows x the first window's groups / rows) plus a margin;
   // a result that outgrows the columns falls back to isa_result_copy.
   bool stream_want = false;
+  bool stream_alloc_called = false;   // the allocator is asked at most once per execute
+  bool streamed_during_merge = false;
   int64_t stream_total = 0, stream_est = 0, stream_rows0 = 0;
   u32 stream_prev = 0;          // groups exported so far
   int stream_pending = -1;      // h_scal slot of the window whose export is still to be issued
@@ -2386,6 +2388,7 @@ struct Engine {
     const int64_t cap = std::min<int64_t>({stream_total, est + est / 32 + 65536, (int64_t)0xFFFFFFF0ll});
     void* kptr[ISA_MAX_KEY_COLS] = {nullptr};
     void* sptr[ISA_MAX_SLOTS] = {nullptr};
+    stream_alloc_called = true;
     if (out_alloc(out_user, cap, kptr, sptr) != 0) return false;
     memset(&stream_ed, 0, sizeof(stream_ed));
     stream_ed.ncols = kd0.ncols;
@@ -2448,6 +2451,7 @@ struct Engine {
     stream_flush(nullptr);
     CK(cudaStreamSynchronize(xs));
     streamed_ok = streaming && stream_cap > 0 && stream_prev == result.n;
+    streamed_during_merge = streamed_ok;
     streaming = false;
   }
 
@@ -3009,6 +3013,8 @@ struct Engine {
     in_n = n;
     in_on_host = on_host;
     streaming = streamed_ok = false;
+    stream_alloc_called = false;
+    streamed_during_merge = false;
     dense_pred = -1;
     raw_left = 0;
     new_frac_hint = 0;
@@ -3176,6 +3182,18 @@ struct Engine {
     ev_pool.push_back(rg0); ev_pool.push_back(rg1); ev_pool.push_back(wm1);
     ph_collect();
     led.n_groups = result.n;
+    // output allocator, nothing streamed (device input, no spill, or the
+    // streamed columns were too small and none were handed out): the caller's
+    // columns are allocated now, at the exact group count, and filled directly
+    if (out_alloc && !streamed_ok && !stream_alloc_called && result.n > 0) {
+      void* kptr[ISA_MAX_KEY_COLS] = {nullptr};
+      void* sptr[ISA_MAX_SLOTS] = {nullptr};
+      if (out_alloc(out_user, (int64_t)result.n, kptr, sptr) == 0) {
+        result_copy(kptr, sptr, in_on_host, st);
+        streamed_ok = true;
+        streamed_during_merge = false;
+      }
+    }
     led.kernel_launches = g_launches.load() - launch0;
     CK(cudaGetLastError());
     return result.n;
@@ -3673,7 +3691,7 @@ int isa_set_output_allocator(isa_handle* h, isa_alloc_fn fn, void* user) {
 
 int isa_result_streamed(isa_handle* h) {
   if (!h) return 0;
-  return h->eng->streamed_ok ? 1 : 0;
+  return h->eng->streamed_ok ? (h->eng->streamed_during_merge ? 2 : 1) : 0;
 }
 
 int isa_metrics(isa_handle* h, isa_ledger* out) {

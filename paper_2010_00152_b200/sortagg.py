@@ -549,31 +549,32 @@ class SortAggregate:
         file_store = isinstance(self.store, FileStore)
         if file_store:
             h.set_spill_dir(self.store.directory, self.store._next)
-        # host input: the wide merge streams its windows into output columns
-        # this call allocates on request (isa_set_output_allocator), so the
-        # device -> host transfer overlaps the merge; the caller owns them
+        # the caller owns the output columns: the native side asks for them
+        # (isa_set_output_allocator) -- during the wide merge with host input
+        # that spilled (the device -> host transfer then overlaps the merge),
+        # else at the end of the execute at the exact group count
         streamed = {}
-        if on_host:
-            torch = _torch()
+        torch = _torch()
+        out_dev = torch.device("cpu") if on_host else keys[0].device
 
-            def alloc(capacity):
-                ok = [torch.empty(capacity, dtype=k.dtype, pin_memory=True) for k in keys]
-                os_ = [torch.empty(capacity, dtype=torch.float64 if ty == _native.SLOT_F64 else torch.int64,
-                                   pin_memory=True) for (_, ty, _, _) in slots]
-                streamed["keys"], streamed["states"] = ok, os_
-                return [t.data_ptr() for t in ok], [t.data_ptr() for t in os_]
+        def alloc(capacity):
+            ok = [torch.empty(capacity, dtype=k.dtype, device=out_dev, pin_memory=on_host) for k in keys]
+            os_ = [torch.empty(capacity, dtype=torch.float64 if ty == _native.SLOT_F64 else torch.int64,
+                               device=out_dev, pin_memory=on_host) for (_, ty, _, _) in slots]
+            streamed["keys"], streamed["states"] = ok, os_
+            return [t.data_ptr() for t in ok], [t.data_ptr() for t in os_]
 
-            h.set_output_allocator(alloc)
+        h.set_output_allocator(alloc)
         try:
             # the native side selects the device itself; outputs name it explicitly
             n_groups = h.execute(n, [k.data_ptr() for k in keys], [v.data_ptr() for v in vals], on_host, sptr)
         finally:
-            if on_host:
-                h.set_output_allocator(None)
+            h.set_output_allocator(None)
         if file_store:
             self.run_ids = self.store._adopt(h.run_rows(), len(keys), len(slots), self.config.page_capacity)
-        self.streamed_output = bool(streamed) and h.result_streamed()
-        if self.streamed_output:
+        mode = h.result_streamed() if streamed else 0
+        self.streamed_output = mode == 2   # the columns were filled while the wide merge ran
+        if mode:
             self._record(h, n, n_groups)
             return ColumnarResult([t[:n_groups] for t in streamed["keys"]],
                                   [t[:n_groups] for t in streamed["states"]])
