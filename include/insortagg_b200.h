@@ -250,6 +250,20 @@ ISA_API int isa_partition_counts(isa_handle* h, int64_t n_rows, const void* cons
 ISA_API int isa_scatter_to_peers(isa_handle* h, int64_t n_rows, const void* const* key_cols,
                                  const void* const* val_cols, void* const* peer_cols,
                                  const int64_t* peer_offsets, void* stream);
+/* Multi-GPU execute in one process: handles[g] was
+ * created with isa_config.device = its GPU and holds shard g of the input in
+ * that GPU's memory (key_cols[g][i] / val_cols[g][j], n_rows[g] rows, < 2^31).
+ * Sampled splitters cut the key space into n_devices ranges of about equal row
+ * counts, every shard is partitioned by range and its rows are stored
+ * straight into the destination GPUs' receive columns over NVLink peer access
+ * (isa_partition_counts + isa_scatter_to_peers on plain device pointers), then
+ * every GPU runs its operator on its range (one host thread per GPU).
+ * n_groups_out[g] = groups of range g; its result is read from handles[g]
+ * (isa_result_copy), and the results in g order are the globally sorted
+ * output.  streams[g] (or NULL) is the cudaStream_t used on device g. */
+ISA_API int isa_execute_multi(isa_handle* const* handles, int32_t n_devices, const int64_t* n_rows,
+                              const void* const* const* key_cols, const void* const* const* val_cols,
+                              void* const* streams, int64_t* n_groups_out);
 /* CUDA IPC plumbing for the receive columns: 72-byte handles (allocation
  * handle + the pointer's offset inside the allocation); open returns the
  * mapped allocation base (for isa_ipc_close) and the pointer. */

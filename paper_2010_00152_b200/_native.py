@@ -51,7 +51,7 @@ EXPORTED_SYMBOLS = (
     "isa_set_spill_dir", "isa_in_stream_aggregate", "isa_hash_aggregate", "isa_merge_intersect", "isa_partition_counts",
     "isa_scatter_to_peers", "isa_ipc_handle", "isa_ipc_open", "isa_ipc_close",
     "isa_set_kernel_timing", "isa_kernel_stats", "isa_kernel_timing_reserve", "isa_set_output_allocator",
-    "isa_result_streamed",
+    "isa_result_streamed", "isa_execute_multi",
 )
 
 # isa_kernel_family (kernel-true roofline families)
@@ -173,6 +173,9 @@ def load():
     lib.isa_hash_aggregate.argtypes = [vp, ctypes.c_int64, pp, pp, ctypes.c_int32, vp, i64p]
     lib.isa_merge_intersect.restype = ctypes.c_int
     lib.isa_merge_intersect.argtypes = [vp, ctypes.c_int64, pp, ctypes.c_int64, pp, pp, ctypes.c_int32, vp, i64p]
+    lib.isa_execute_multi.restype = ctypes.c_int
+    lib.isa_execute_multi.argtypes = [ctypes.POINTER(vp), ctypes.c_int32, i64p, ctypes.POINTER(pp), ctypes.POINTER(pp),
+                                      pp, i64p]
     lib.isa_partition_counts.restype = ctypes.c_int
     lib.isa_partition_counts.argtypes = [vp, ctypes.c_int64, pp, vp, vp, ctypes.c_int32, i64p, vp]
     lib.isa_scatter_to_peers.restype = ctypes.c_int
@@ -404,6 +407,28 @@ class Handle:
                                             split_lo, split_hi, n_split, _ptr_array(key_out),
                                             _ptr_array(val_out), counts, stream))
         return [counts[i] for i in range(n_split + 1)]
+
+
+def execute_multi(handles, n_rows, key_ptrs, val_ptrs, streams=None):
+    """isa_execute_multi over ``handles`` (one per device): shard g has
+    ``n_rows[g]`` rows in the device columns ``key_ptrs[g]`` / ``val_ptrs[g]``.
+    Returns the group count of every key range."""
+    g = len(handles)
+    lib = load()
+    hs = (ctypes.c_void_p * g)(*[h._h for h in handles])
+    rows = (ctypes.c_int64 * g)(*[int(x) for x in n_rows])
+    karr = [_ptr_array(k) for k in key_ptrs]
+    varr = [_ptr_array(v) for v in val_ptrs]
+    pp_t = ctypes.POINTER(ctypes.c_void_p)
+    kk = (pp_t * g)(*[ctypes.cast(a, pp_t) for a in karr])
+    vv = (pp_t * g)(*[ctypes.cast(a, pp_t) for a in varr])
+    st = _ptr_array(streams) if streams else None
+    out = (ctypes.c_int64 * g)()
+    status = lib.isa_execute_multi(hs, g, rows, kk, vv, st, out)
+    if status != 0:
+        msg = lib.isa_last_error(handles[0]._h).decode()
+        raise _STATUS_ERRORS.get(status, ResourceError)(msg)
+    return [int(x) for x in out]
 
 
 def ipc_handle(ptr):

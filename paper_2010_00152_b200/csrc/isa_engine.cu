@@ -35,6 +35,7 @@
 #include <unistd.h>
 #include <deque>
 #include <functional>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -3614,6 +3615,145 @@ int isa_scatter_to_peers(isa_handle* h, int64_t n_rows, const void* const* key_c
     return ISA_OK;
   } catch (const std::exception& e) {
     return fail(h, e);
+  }
+}
+
+// Multi-GPU execute in one process: handles[g] lives
+// on its own device (isa_config.device) and holds shard g of the input in
+// device memory.  Sampled splitters cut the key space into n_devices ranges
+// of about equal row counts; every device partitions its shard by range and
+// the fused scatter kernel stores the rows straight into the destination
+// devices' receive columns over NVLink peer access (one process: plain
+// device pointers, no IPC); then every device runs its operator on its range,
+// one host thread per device.  Range g's result is held by handles[g].
+int isa_execute_multi(isa_handle* const* handles, int32_t n_devices, const int64_t* n_rows,
+                      const void* const* const* key_cols, const void* const* const* val_cols, void* const* streams,
+                      int64_t* n_groups_out) {
+  if (!handles || n_devices < 1 || n_devices > 256 || !n_rows || !key_cols || !val_cols) return ISA_ERR_CONTRACT;
+  const int G = n_devices;
+  for (int g = 0; g < G; ++g)
+    if (!handles[g] || !handles[g]->eng) return ISA_ERR_CONTRACT;
+  isa_handle* h0 = handles[0];
+  std::vector<std::vector<void*>> recv(G);   // receive columns of every device (freed on every path)
+  auto free_recv = [&]() {
+    for (int d = 0; d < G; ++d) {
+      cudaSetDevice(handles[d]->eng->dev);
+      for (void* p : recv[d]) if (p) cudaFree(p);
+      recv[d].clear();
+    }
+  };
+  try {
+    Engine* e0 = h0->eng;
+    const int nk = e0->sch.n_key_cols, nv = e0->sch.n_val_cols, ncol = nk + nv;
+    auto stream_of = [&](int g) { return streams ? (cudaStream_t)streams[g] : (cudaStream_t) nullptr; };
+    if (G == 1) {
+      int64_t ng = e0->execute(n_rows[0], key_cols[0], val_cols[0], false, stream_of(0));
+      if (n_groups_out) n_groups_out[0] = ng;
+      return ISA_OK;
+    }
+    // peer access between every pair of distinct devices
+    for (int a = 0; a < G; ++a)
+      for (int b = 0; b < G; ++b) {
+        const int da = handles[a]->eng->dev, db = handles[b]->eng->dev;
+        if (da == db) continue;
+        int can = 0;
+        CK(cudaDeviceCanAccessPeer(&can, da, db));
+        if (!can) throw IsaError(ISA_ERR_RESOURCE, "isa_execute_multi needs peer access between the devices");
+        CK(cudaSetDevice(da));
+        const cudaError_t pe = cudaDeviceEnablePeerAccess(db, 0);
+        if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) CK(pe);
+        (void)cudaGetLastError();
+      }
+    // 1. sampled normalized keys of every shard -> G - 1 splitters at equal-count quantiles
+    const int64_t per = 1 << 16;
+    std::vector<std::pair<u64, u64>> samples;   // (hi, lo)
+    for (int g = 0; g < G; ++g) {
+      Engine* e = handles[g]->eng;
+      if (n_rows[g] <= 0) continue;
+      CK(cudaSetDevice(e->dev));
+      const int64_t stride = std::max<int64_t>(1, n_rows[g] / per), ns = (n_rows[g] + stride - 1) / stride;
+      u64 *dlo = nullptr, *dhi = nullptr;
+      CK(cudaMalloc(&dlo, 8 * (size_t)ns));
+      CK(cudaMalloc(&dhi, 8 * (size_t)ns));
+      isa::sample_keys(e->kd_at(key_cols[g]), n_rows[g], stride, dlo, dhi, stream_of(g));
+      std::vector<u64> lo(ns), hi(ns);
+      CK(cudaMemcpyAsync(lo.data(), dlo, 8 * (size_t)ns, cudaMemcpyDeviceToHost, stream_of(g)));
+      CK(cudaMemcpyAsync(hi.data(), dhi, 8 * (size_t)ns, cudaMemcpyDeviceToHost, stream_of(g)));
+      CK(cudaStreamSynchronize(stream_of(g)));
+      cudaFree(dlo);
+      cudaFree(dhi);
+      for (int64_t i = 0; i < ns; ++i) samples.push_back({hi[i], lo[i]});
+    }
+    std::sort(samples.begin(), samples.end());
+    std::vector<u64> sp_lo(G - 1, ~0ull), sp_hi(G - 1, ~0ull);
+    if (!samples.empty())
+      for (int r = 0; r + 1 < G; ++r) {
+        const size_t pos = std::min(samples.size() - 1, samples.size() * (size_t)(r + 1) / (size_t)G);
+        sp_hi[r] = samples[pos].first;
+        sp_lo[r] = samples[pos].second;
+      }
+    // 2. every shard: destinations by splitter + per-destination counts (the permutation stays in the handle)
+    std::vector<std::vector<int64_t>> counts(G, std::vector<int64_t>(G, 0));
+    for (int g = 0; g < G; ++g) {
+      Engine* e = handles[g]->eng;
+      CK(cudaSetDevice(e->dev));
+      u64 *dlo = nullptr, *dhi = nullptr;
+      CK(cudaMalloc(&dlo, 8 * (size_t)G));
+      CK(cudaMalloc(&dhi, 8 * (size_t)G));
+      CK(cudaMemcpy(dlo, sp_lo.data(), 8 * (size_t)(G - 1), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(dhi, sp_hi.data(), 8 * (size_t)(G - 1), cudaMemcpyHostToDevice));
+      e->partition_counts(n_rows[g], key_cols[g], dlo, dhi, G - 1, counts[g].data(), stream_of(g));
+      cudaFree(dlo);
+      cudaFree(dhi);
+    }
+    // 3. receive columns on every destination; source g's block lands at sum of counts[q][d], q < g
+    std::vector<int64_t> recv_n(G, 0);
+    for (int d = 0; d < G; ++d) {
+      for (int g = 0; g < G; ++g) recv_n[d] += counts[g][d];
+      Engine* e = handles[d]->eng;
+      CK(cudaSetDevice(e->dev));
+      recv[d].assign(ncol, nullptr);
+      for (int c = 0; c < ncol; ++c) {
+        const size_t el = c < nk ? e->key_elem(c) : e->val_elem(c - nk);
+        CK(cudaMalloc(&recv[d][c], std::max<size_t>((size_t)recv_n[d] * el, 256)));
+      }
+    }
+    std::vector<void*> table((size_t)G * ncol);
+    for (int d = 0; d < G; ++d)
+      for (int c = 0; c < ncol; ++c) table[(size_t)d * ncol + c] = recv[d][c];
+    for (int g = 0; g < G; ++g) {
+      std::vector<int64_t> offs(G, 0);
+      for (int d = 0; d < G; ++d)
+        for (int q = 0; q < g; ++q) offs[d] += counts[q][d];
+      handles[g]->eng->scatter_to_peers(n_rows[g], key_cols[g], val_cols[g], table.data(), offs.data(), stream_of(g));
+    }
+    for (int g = 0; g < G; ++g) {   // every store landed before anyone reads
+      CK(cudaSetDevice(handles[g]->eng->dev));
+      CK(cudaDeviceSynchronize());
+    }
+    // 4. the local operator on every range, one host thread per device
+    std::vector<int> rc(G, ISA_OK);
+    std::vector<int64_t> ng(G, 0);
+    std::vector<std::thread> th;
+    for (int d = 0; d < G; ++d)
+      th.emplace_back([&, d]() {
+        std::vector<const void*> kc(recv[d].begin(), recv[d].begin() + nk), vc(recv[d].begin() + nk, recv[d].end());
+        if (vc.empty()) vc.push_back(nullptr);
+        rc[d] = isa_execute(handles[d], recv_n[d], kc.data(), vc.data(), 0, streams ? streams[d] : nullptr, &ng[d]);
+      });
+    for (auto& t : th) t.join();
+    free_recv();
+    for (int d = 0; d < G; ++d) {
+      if (rc[d] != ISA_OK) {
+        if (d) h0->eng->err = handles[d]->eng->err;
+        return rc[d];
+      }
+      if (n_groups_out) n_groups_out[d] = ng[d];
+    }
+    return ISA_OK;
+  } catch (const std::exception& e) {
+    free_recv();
+    return fail(h0, e);
   }
 }
 

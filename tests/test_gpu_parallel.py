@@ -128,3 +128,46 @@ def test_ipc_handle_carries_the_offset_in_its_allocation():
     assert len(ha) == 72 and ha[:64] == hb[:64]
     off_a, off_b = struct.unpack("<Q", ha[64:])[0], struct.unpack("<Q", hb[64:])[0]
     assert off_b - off_a == 65536 - 4096
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,rows,memory", [(5, 2_000_000, 1 << 14), (3, 1_000_000, 1 << 14), (1, 600_000, 4096)])
+def test_execute_multi_two_ranges_on_one_gpu(cfg, rows, memory):
+    """isa_execute_multi with two handles standing in for two GPUs (both on
+    cuda:0: the same splitter, partition and peer-store kernels, plain device
+    pointers): two shards in, two key ranges out; their concatenation is the
+    single-operator result and the ranges do not overlap."""
+    import numpy as np
+    import oracle
+    import paper_2010_00152_b200 as isa
+    from paper_2010_00152_b200 import _native, workloads
+    kw = {"domain": 1 << 20} if cfg in (3, 5) else {}
+    w = workloads.make(cfg, rows=rows, device="cpu", **kw)
+    keys_np = [k.numpy() for k in w.keys]
+    slots = oracle.make_states(w.schema, {k: v.numpy() for k, v in w.values.items()}, w.rows)
+    want_keys, want_slots = oracle.reference_aggregate(keys_np, slots, oracle.slot_ops(w.schema))
+    cut = (rows * 2) // 5   # unequal shards
+    ops, prepared = [], []
+    for a, b in ((0, cut), (cut, rows)):
+        op = isa.SortAggregate(w.schema, isa.SortAggConfig(memory_budget=memory, page_capacity=100, ovc_enabled=False))
+        ops.append(op)
+        prepared.append(op._prepare([k[a:b].cuda() for k in w.keys], {n: v[a:b].cuda() for n, v in w.values.items()},
+                                    False, None))
+    # two native handles, one per "device"
+    assert prepared[0][0] is not prepared[1][0]
+    counts = _native.execute_multi([p[0] for p in prepared], [p[1] for p in prepared],
+                                   [[k.data_ptr() for k in p[2]] for p in prepared],
+                                   [[v.data_ptr() for v in p[3]] for p in prepared])
+    outs = [op._collect(p[0], p[1], ng, p[2], p[4], False, p[6]) for op, p, ng in zip(ops, prepared, counts)]
+    assert sum(counts) == len(want_keys[0]) and min(counts) > 0
+    # roughly equal ranges from the sampled splitters
+    assert max(counts) < 0.75 * sum(counts)
+    for j, wk in enumerate(want_keys):
+        got = np.concatenate([o.keys[j].cpu().numpy() for o in outs])
+        assert np.array_equal(got, wk)
+    for s, ws in enumerate(want_slots):
+        got = np.concatenate([o.states[s].cpu().numpy() for o in outs])
+        if got.dtype.kind == "f":
+            assert np.allclose(got, ws, rtol=1e-5 if cfg == 3 else 1e-9, atol=1e-9)
+        else:
+            assert np.array_equal(got, ws)
