@@ -727,6 +727,9 @@ struct Engine {
     const bool iota = sort_val_iota;
     sort_val_iota = false;
     sort_assumed = false;
+    sort_partial_used = false;
+    const bool partial_ok = sort_partial_ok;
+    sort_partial_ok = false;
     const u32* cin = sort_carry_in;
     u32* cout = sort_carry_out;
     sort_carry_in = nullptr;
@@ -789,7 +792,27 @@ struct Engine {
       if (read_u32(dscal32(5)) == 0) return cur;
       return radix_sort_pairs(KW, b, m, lb, hb + 1, st, nullptr, cur);
     }
+    // Wide one-word keys (hashed 64-bit keys: every bit varies): sort on the
+    // top 48 varying bits only -- 6 passes instead of 8.  Equal keys keep
+    // their row order (stable), and two distinct keys that share 48 bits are
+    // rare (about one pair per eight chunks of 2^23 distinct keys); a check
+    // pass over the sorted keys reports an inversion to the caller's next
+    // synchronization, which then sorts the chunk again on every bit.
+    if (partial_ok && KW == 1 && hb - lb + 1 > 48 && m >= (1u << 20) && partial_env()) {
+      const int cur = radix_sort_pairs(KW, b, m, hb - 47, hb + 1, st, nullptr);
+      ((volatile u32*)h_scal)[111] = 0;
+      check_sorted(b.lo[cur], m, d_scal_mapped + 111, st);
+      sort_partial_used = true;
+      return cur;
+    }
     return radix_sort_pairs(KW, b, m, lb, hb + 1, st, nullptr);
+  }
+  // sort_partial_ok: the caller of the next sort can verify a partial-key
+  // sort at its next synchronization (sort_partial_used, h_scal[111])
+  bool sort_partial_ok = false, sort_partial_used = false;
+  static bool partial_env() {   // ISA_PARTIAL_SORT=0 (read per sort): always sort every varying bit
+    const char* e = getenv("ISA_PARTIAL_SORT");
+    return !(e && e[0] == '0');
   }
 
   // Flush analysis on a sorted chunk of `span` rows: number of keys absent
@@ -1338,14 +1361,18 @@ struct Engine {
         sort_carry_out = rec_sorted.as<u32>();
       }
     }
+    sort_partial_ok = true;
     int cur = sort_rows(kd, row0, nullptr, span, /*assume=*/true);
     bool carried = sort_carried;
-    const bool assumed = sort_assumed;
+    const bool assumed = sort_assumed, partial = sort_partial_used;
     if (assumed) to_host(dvary(), 2 * sizeof(u64), 104);
     const bool t_empty = T.n == 0;
     u32 f = flush_point(cur, span, span);
-    if (assumed && !verify_assumed_mask()) {
-      // key bits outside the assumed mask vary in this chunk: sort again on its own mask
+    const bool mask_ok = !assumed || verify_assumed_mask();
+    if (!mask_ok || (partial && ((volatile u32*)h_scal)[111] != 0)) {
+      // key bits outside the assumed mask vary in this chunk, or two keys
+      // that share the sorted top bits came out of order: sort again on the
+      // chunk's own mask, every bit
       cur = sort_rows(kd, row0, nullptr, span);
       carried = sort_carried;
       f = flush_point(cur, span, span);

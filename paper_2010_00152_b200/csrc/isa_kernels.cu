@@ -944,6 +944,18 @@ void sort_small_segments(u64* lo, const u64* hi, u32* val, u32 n, u32 maxlen, u3
   if (n) klaunch(k_sort_small_segments, grid_for(n, 256), 256, 0, st, lo, hi, val, n, maxlen, too_long);
 }
 
+// one-word keys sorted on their top bits only: is the full key order
+// non-decreasing?  (*bad_mapped: mapped host word, zeroed by the host, set on
+// an inversion -- two distinct keys that share the sorted bits, out of order)
+__global__ void __launch_bounds__(256) k_check_sorted(const u64* __restrict__ lo, u32 n, u32* __restrict__ bad_mapped) {
+  bool bad = false;
+  for (u32 i = blockIdx.x * 256 + threadIdx.x + 1; i < n; i += gridDim.x * 256) bad |= lo[i] < lo[i - 1];
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *bad_mapped = 1u;
+}
+void check_sorted(const u64* lo, u32 n, u32* bad_mapped, cudaStream_t st) {
+  if (n > 1) klaunch(k_check_sorted, grid_for(n, 256), 256, 0, st, lo, n, bad_mapped);
+}
+
 // ======================================================= key building ====
 template <int KW>
 __global__ void k_build_keys(KeyDesc kd, i64 row0, const u32* __restrict__ pos, u32 n, u64* __restrict__ lo,

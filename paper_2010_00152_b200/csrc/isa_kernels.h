@@ -35,6 +35,8 @@ struct SortBufs {
 size_t sort_aux_bytes(u32 n);
 int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStream_t st, int64_t* launches,
                      int start = 0);
+// *bad_mapped = 1 when lo[0..n) is not non-decreasing (one-word keys sorted on their top bits only)
+void check_sorted(const u64* lo, u32 n, u32* bad_mapped, cudaStream_t st);
 // stable insertion sort by the low word of every run of equal high words
 // (length <= maxlen; longer runs set *too_long)
 void sort_small_segments(u64* lo, const u64* hi, u32* val, u32 n, u32 maxlen, u32* too_long, cudaStream_t st);

@@ -1028,3 +1028,29 @@ def test_assumed_sort_mask_widens_mid_input(memory):
     _check(res, want_keys, want_slots)
     assert op.cycles == [c for c in cycles if c > 0]
     assert op.ledger.rows_spilled == led["rows_spilled"] and op.runs_after_generation == led["runs"]
+
+
+@pytest.mark.parametrize("collide", [False, True])
+def test_partial_key_sort_of_wide_keys(collide):
+    """64-bit keys whose every bit varies are sorted on their top 48 bits in
+    chunks of >= 2^20 rows; distinct keys that share those bits and arrive out
+    of order (planted here: pairs differing in the low 16 bits only) are caught
+    by the check pass and the chunk is sorted again on every bit."""
+    rng = np.random.default_rng(17)
+    n, memory = 3_000_000, 1 << 21
+    base = rng.integers(-(1 << 62), 1 << 62, 400_000).astype(np.int64)
+    k = base[rng.integers(0, len(base), n)]
+    if collide:
+        idx = rng.integers(0, n, 5000)
+        k[idx] = (k[idx] & ~np.int64(0xFFFF)) | rng.integers(0, 1 << 16, len(idx)).astype(np.int64)
+        k[(idx + 7) % n] = (k[idx] & ~np.int64(0xFFFF)) | rng.integers(0, 1 << 16, len(idx)).astype(np.int64)
+    v = rng.integers(-1000, 1000, n).astype(np.int64)
+    sch = _cut_schema()
+    slots = oracle.make_states(sch, {"v": v}, n)
+    want_keys, want_slots = oracle.reference_aggregate([k], slots, oracle.slot_ops(sch))
+    _, _, led, cycles = oracle.rsw_sortagg([k], slots, oracle.slot_ops(sch), memory, 100)
+    op = isa.SortAggregate(sch, _cfg(memory, 100))
+    res = op.execute_columns([_cuda(k)], {"v": _cuda(v)})
+    _check(res, want_keys, want_slots)
+    assert op.cycles == [c for c in cycles if c > 0]
+    assert op.ledger.rows_spilled == led["rows_spilled"] and op.runs_after_generation == led["runs"]
