@@ -786,9 +786,13 @@ struct Engine {
       // 128-bit keys whose high word varies: sort on the high word, then
       // finish runs of equal high words with a stable sort on the low word
       // (half the radix passes when high words are nearly unique)
-      int cur = radix_sort_pairs(KW, b, m, std::max(lb, 64), hb + 1, st, nullptr);
+      // ... and at most the top 48 bits of it (6 passes): keys sharing those
+      // bits are rare and land in the same small run
+      int lo_bit = std::max(lb, 64);
+      if (hb - lo_bit + 1 > 48 && partial_env()) lo_bit = hb - 47;
+      int cur = radix_sort_pairs(KW, b, m, lo_bit, hb + 1, st, nullptr);
       CK(cudaMemsetAsync(dscal32(5), 0, sizeof(u32), st));
-      sort_small_segments(b.lo[cur], b.hi[cur], b.val[cur], m, 64, dscal32(5), st);
+      sort_small_segments(b.lo[cur], b.hi[cur], b.val[cur], m, 64, lo_bit > 64 ? lo_bit - 64 : 0, dscal32(5), st);
       if (read_u32(dscal32(5)) == 0) return cur;
       return radix_sort_pairs(KW, b, m, lb, hb + 1, st, nullptr, cur);
     }

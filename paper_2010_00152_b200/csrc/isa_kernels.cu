@@ -914,34 +914,38 @@ static int grid_for(u64 n, int threads, int cap = 148 * 16);
 // high words (usually exact duplicates or rare collisions) with a stable
 // insertion sort on the low word.  A run longer than maxlen sets *too_long
 // (the caller then completes the sort with full LSD passes).
-__global__ void k_sort_small_segments(u64* __restrict__ lo, const u64* __restrict__ hi, u32* __restrict__ val, u32 n,
-                                      u32 maxlen, u32* __restrict__ too_long) {
+__global__ void k_sort_small_segments(u64* __restrict__ lo, u64* __restrict__ hi, u32* __restrict__ val, u32 n,
+                                      u32 maxlen, int shift, u32* __restrict__ too_long) {
+  // shift > 0: the rows were sorted on hi >> shift only; a run = equal
+  // hi >> shift, ordered by (hi, lo)
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const u64 h = hi[i];
-    if (i > 0 && hi[i - 1] == h) continue;   // not the first element of a run
+    const u64 h = hi[i] >> shift;
+    if (i > 0 && (hi[i - 1] >> shift) == h) continue;   // not the first element of a run
     u32 j = i + 1;
-    while (j < n && hi[j] == h) {
+    while (j < n && (hi[j] >> shift) == h) {
       ++j;
       if (j - i > maxlen) break;
     }
     if (j - i > maxlen) { *too_long = 1u; continue; }
     for (u32 a = i + 1; a < j; ++a) {
-      const u64 kl = lo[a];
+      const u64 kl = lo[a], kh = hi[a];
       const u32 kv = val[a];
       u32 p = a;
-      while (p > i && lo[p - 1] > kl) {
+      while (p > i && (hi[p - 1] > kh || (hi[p - 1] == kh && lo[p - 1] > kl))) {
         lo[p] = lo[p - 1];
+        if (shift) hi[p] = hi[p - 1];
         val[p] = val[p - 1];
         --p;
       }
       lo[p] = kl;
+      if (shift) hi[p] = kh;
       val[p] = kv;
     }
   }
 }
 
-void sort_small_segments(u64* lo, const u64* hi, u32* val, u32 n, u32 maxlen, u32* too_long, cudaStream_t st) {
-  if (n) klaunch(k_sort_small_segments, grid_for(n, 256), 256, 0, st, lo, hi, val, n, maxlen, too_long);
+void sort_small_segments(u64* lo, u64* hi, u32* val, u32 n, u32 maxlen, int shift, u32* too_long, cudaStream_t st) {
+  if (n) klaunch(k_sort_small_segments, grid_for(n, 256), 256, 0, st, lo, hi, val, n, maxlen, shift, too_long);
 }
 
 // one-word keys sorted on their top bits only: is the full key order

@@ -39,7 +39,8 @@ int radix_sort_pairs(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
 void check_sorted(const u64* lo, u32 n, u32* bad_mapped, cudaStream_t st);
 // stable insertion sort by the low word of every run of equal high words
 // (length <= maxlen; longer runs set *too_long)
-void sort_small_segments(u64* lo, const u64* hi, u32* val, u32 n, u32 maxlen, u32* too_long, cudaStream_t st);
+// shift > 0: runs of equal hi >> shift (the rows were sorted on those bits only), ordered by (hi, lo)
+void sort_small_segments(u64* lo, u64* hi, u32* val, u32 n, u32 maxlen, int shift, u32* too_long, cudaStream_t st);
 
 // ---- key building -------------------------------------------------------
 // keys of rows row0 + (pos ? pos[i] : i), i < n  ->  lo/hi/val(=pos or i);
