@@ -243,6 +243,61 @@ def _step_roofline(w, rows, n_groups, dled, ms_step, peak, link, run_tier):
             "t_hbm_ms": t_hbm * 1e3, "frac_hbm_only": t_hbm * 1e3 / ms_step, "run_tier": run_tier}
 
 
+def _check_result(torch, dist, res, schema, rows_total, world, rank, dev):
+    """Outside the timed region: every rank's keys strictly ascending, the
+    ranks' key ranges in rank order, and -- when the schema counts rows -- the
+    counts of all groups summing to the input rows."""
+    from paper_2010_00152_b200.core import AggregateKind
+    def ordered_view(k):   # torch compares neither uint16/32 nor uint64: order-preserving int64 views
+        if k.dtype in (torch.uint16, torch.uint32):
+            return k.to(torch.int64)
+        if k.dtype == torch.uint64:
+            return k.view(torch.int64) ^ torch.tensor(-(1 << 63), dtype=torch.int64, device=k.device)
+        return k
+
+    keys = [ordered_view(k) for k in res.keys]
+    n = int(keys[0].shape[0]) if keys else 0
+    ok_sorted = True
+    if n > 1:
+        gt = torch.zeros(n - 1, dtype=torch.bool, device=keys[0].device)
+        eq = torch.ones(n - 1, dtype=torch.bool, device=keys[0].device)
+        for k in keys:   # lexicographic, most significant column first
+            gt |= eq & (k[1:] > k[:-1])
+            eq &= k[1:] == k[:-1]
+        ok_sorted = bool(gt.all().item())
+    slot = 0
+    count_slot = None
+    for agg in schema.aggregates:
+        if agg.kind == AggregateKind.COUNT and count_slot is None:
+            count_slot = slot
+        slot += 2 if agg.kind == AggregateKind.AVG else 1
+    cnt = int(res.states[count_slot].sum().item()) if count_slot is not None and n else (0 if count_slot is not None else None)
+    ordered = True
+    if world > 1:
+        first = torch.stack([k[0] if n else torch.zeros((), dtype=k.dtype, device=dev) for k in keys]).to(torch.int64)
+        last = torch.stack([k[-1] if n else torch.zeros((), dtype=k.dtype, device=dev) for k in keys]).to(torch.int64)
+        info = torch.cat([first, last, torch.tensor([n, cnt or 0], dtype=torch.int64, device=dev)])
+        every = [torch.empty_like(info) for _ in range(world)]
+        dist.all_gather(every, info)
+        nk = len(keys)
+        prev = None
+        cnt = 0 if count_slot is not None else None
+        for e in every:
+            e = e.tolist()
+            if count_slot is not None:
+                cnt += e[2 * nk + 1]
+            if e[2 * nk] == 0:
+                continue
+            if prev is not None and not (tuple(prev) < tuple(e[:nk])):
+                ordered = False
+            prev = e[nk:2 * nk]
+        flag = torch.tensor([1 if ok_sorted else 0], dtype=torch.int64, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        ok_sorted = bool(flag.item())
+    return {"keys_strictly_ascending": ok_sorted, "rank_ranges_in_order": ordered,
+            "count_sum": cnt, "count_sum_equals_rows": (cnt == rows_total) if cnt is not None else None}
+
+
 def run_reference(args):
     """--impl reference: the reference algorithm on the host cores."""
     world, rank, _ = _dist()
@@ -364,6 +419,7 @@ def measure(torch, dist, cfgno, rows_total, run_tier, steps, warmup, world, rank
     ms_step = ms_total / max(1, steps)
     value = rows * world / (ms_step / 1e3)
     n_groups = res.n_groups if hasattr(res, "n_groups") else None
+    check = _check_result(torch, dist, res, w.schema, rows * world, world, rank, dev)
     if world > 1 and n_groups is not None:
         t = torch.tensor([n_groups], dtype=torch.int64, device=dev)
         dist.all_reduce(t)
@@ -389,6 +445,7 @@ def measure(torch, dist, cfgno, rows_total, run_tier, steps, warmup, world, rank
                             "merge_windows": dled.get("merge_windows"), "chunks": dled.get("chunks")},
         "gpu_launches": launches,
         "clocks": clk,
+        "check": check,
     }
     res = None
 
@@ -478,7 +535,7 @@ def main():
                                                        "generated on device)",
     }
     for k in ("config", "roofline", "kernels", "step_roofline", "phases_ms_per_step", "ledger_per_step",
-              "gpu_launches", "clocks", "e2e"):
+              "gpu_launches", "clocks", "check", "e2e"):
         if k in m:
             line[k] = m[k]
     if cfgno == 5 and world == 1 and not args.no_cfg3:

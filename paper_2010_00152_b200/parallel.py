@@ -239,8 +239,10 @@ def distributed_execute(op, keys, values=None, *, mode="partition", group=None, 
         rk, rc = exchange_p2p(op, keys, cols, split_hi, split_lo, group)
     elif exchange == "nccl":
         pk, pc, counts = partitioner(keys, cols, split_hi, split_lo)
+        nk = len(pk)
         recv, _ = exchange_columns(pk + pc, counts, group)
-        rk, rc = recv[: len(pk)], recv[len(pk):]
+        del pk, pc   # the partitioned copy is not needed any more: its memory goes to the local operator's runs
+        rk, rc = recv[:nk], recv[nk:]
     else:
         raise InvalidInputError(f"unknown exchange {exchange!r}")
     if mode == "preaggregate":

@@ -79,8 +79,10 @@ def _worker(rank, world, port, cfg, rows, mode, q):
         res = parallel.distributed_execute(None, w.keys, w.values, mode=mode, sampler=_sampler,
                                            partitioner=_partitioner, local_execute=local_execute,
                                            merge_execute=merge_execute)
+        import bench   # the bench's multi-rank result check, over the same process group
+        chk = bench._check_result(torch, dist, res, w.schema, rows * world, world, rank, torch.device("cpu"))
         out = ([k.numpy() for k in res.keys], [s.numpy() for s in res.states],
-               [k.numpy() for k in w.keys], {n: v.numpy() for n, v in w.values.items()})
+               [k.numpy() for k in w.keys], {n: v.numpy() for n, v in w.values.items()}, chk)
         gathered = [None] * world
         dist.all_gather_object(gathered, out)
         if rank == 0:
@@ -120,6 +122,11 @@ def test_two_rank_range_partition_matches_oracle(cfg, rows, mode):
             np.testing.assert_allclose(g, e, rtol=1e-9)
         else:
             assert np.array_equal(g, e)
+    # bench.py's own check agrees on every rank
+    for g in gathered:
+        assert g[4]["keys_strictly_ascending"] and g[4]["rank_ranges_in_order"]
+        if g[4]["count_sum"] is not None:
+            assert g[4]["count_sum_equals_rows"], g[4]
     # both ranks received work (range partition actually split the keys)
     if cfg != 2:
         assert all(len(g[0][0]) > 0 for g in gathered)
