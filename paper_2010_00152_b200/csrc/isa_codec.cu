@@ -542,6 +542,58 @@ __global__ void __launch_bounds__(256) k_dense_emit(u64* __restrict__ dense, uns
   }
 }
 
+// the same, straight into the caller's output columns (isa_set_output_allocator
+// with device input): keys denormalized per column, one column per state slot;
+// rows at or beyond `cap` are not written (*over = 1: the columns were too small)
+__global__ void __launch_bounds__(256) k_dense_emit_cols(u64* __restrict__ dense, unsigned char* __restrict__ occ,
+                                                         SlotDesc sd, int cnt_slot, u32 D, u64 key_lo,
+                                                         const u32* __restrict__ bbase, ExportDesc ed, u32 cap,
+                                                         u32* __restrict__ over) {
+  __shared__ u32 sw[8];
+  const int S = sd.nslots;
+  const u32 i0 = (blockIdx.x * 256 + threadIdx.x) * DN_ITEMS;
+  bool pres[DN_ITEMS];
+  u32 c = 0;
+#pragma unroll
+  for (int j = 0; j < DN_ITEMS; ++j) {
+    pres[j] = i0 + j < D && dense_present(dense, occ, S, cnt_slot, i0 + j);
+    c += pres[j] ? 1u : 0u;
+  }
+  u32 tot;
+  u32 pos = bbase[blockIdx.x] + block_excl_scan256(c, sw, &tot);
+#pragma unroll
+  for (int j = 0; j < DN_ITEMS; ++j) {
+    if (!pres[j]) continue;
+    const u32 i = i0 + j;
+    if (pos < cap) {
+      const u64 nk = key_lo + i;
+      for (int q = 0; q < ed.ncols; ++q) {
+        const int w = ed.width[q];
+        u64 f = key_field(0, nk, ed.shift[q], w);
+        if (ed.is_signed[q]) f ^= (1ull << (w - 1));
+        switch (w) {
+          case 8: ((unsigned char*)ed.key_dst[q])[pos] = (unsigned char)f; break;
+          case 16: ((unsigned short*)ed.key_dst[q])[pos] = (unsigned short)f; break;
+          case 32: ((unsigned int*)ed.key_dst[q])[pos] = (unsigned int)f; break;
+          default: ((u64*)ed.key_dst[q])[pos] = f; break;
+        }
+      }
+      for (int s = 0; s < S; ++s) ((u64*)ed.slot_dst[s])[pos] = dense[(size_t)i * S + s];
+    } else {
+      *over = 1u;
+    }
+    for (int s = 0; s < S; ++s) dense[(size_t)i * S + s] = identity_slot(sd.op[s], ST_I64);
+    if (occ) occ[i] = 0;
+    ++pos;
+  }
+}
+
+void dense_emit_cols(u64* dense, unsigned char* occ, const SlotDesc& sd, int cnt_slot, u32 D, u64 key_lo,
+                     const u32* bbase, const ExportDesc& ed, u32 cap, u32* over, cudaStream_t st) {
+  klaunch(k_dense_emit_cols, (int)((D + 256 * DN_ITEMS - 1) / (256 * DN_ITEMS)), 256, 0, st, dense, occ, sd, cnt_slot, D,
+          key_lo, bbase, ed, cap, over);
+}
+
 void dense_init(u64* dense, unsigned char* occ, const SlotDesc& sd, u32 D, cudaStream_t st) {
   if (D) klaunch(k_dense_init, (int)std::min<u32>((D + 255) / 256, 148u * 8u), 256, 0, st, dense, occ, sd, D);
 }

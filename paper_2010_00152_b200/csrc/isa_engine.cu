@@ -2496,7 +2496,12 @@ struct Engine {
   DevBuf dn_state, dn_occ, dn_counts, dn_slices;
   cudaStream_t dn_emit = nullptr;
   cudaEvent_t dn_acc_done[2] = {nullptr, nullptr}, dn_emit_done[2] = {nullptr, nullptr};
-  bool dense_merge(int64_t total) {
+  // allow_direct: with an output allocator and device input the occupied
+  // entries are emitted straight into the caller's columns (no result table,
+  // no export pass); a result larger than the columns' capacity -- the
+  // estimate after the first window was short -- merges again into the table
+  bool result_in_caller = false;
+  bool dense_merge(int64_t total, int64_t est, bool allow_direct = true) {
     { const char* e = getenv("ISA_DENSE"); if (e && e[0] == '0') return false; }   // A/B: sort-based windows
     const int k = (int)runs.size();
     if (KW != 1 || k < 1 || total < 1) return false;
@@ -2600,6 +2605,54 @@ struct Engine {
     CK(cudaMemcpyAsync(dscal32(25), &zero, sizeof(u32), cudaMemcpyHostToDevice, st));
     sync();   // the descriptor vectors are pageable host memory
     result.n = 0;
+    bool direct = allow_direct && out_alloc && !in_on_host && !stream_alloc_called;
+    { const char* e = getenv("ISA_DIRECT_OUT"); if (e && e[0] == '0') direct = false; }   // A/B: result table + export
+    ExportDesc ded;
+    u32 dcap = 0;
+    const int64_t led_rb0 = led.rows_read_back, led_mw0 = led.merge_windows;
+    if (direct) {
+      // the first non-empty window is accumulated and counted before anything
+      // is emitted: its groups / rows ratio sizes the caller's columns
+      int w0 = 0;
+      while (w0 < nwin && wrows[w0] == 0) ++w0;
+      u32 g0 = 0;
+      if (w0 < nwin) {
+        dense_accum(dn_slices.as<DenseSlice>() + soff[w0], (int)(soff[w0 + 1] - soff[w0]), wblk[w0], sd0,
+                    kmin + (u64)w0 * D, D, dstate2[0], occ2[0], st);
+        dense_count(dstate2[0], occ2[0], S, cnt_slot, D, dn_counts.as<u32>(), st);
+        block_counts_scan(dn_counts.as<u32>(), nblocks, dscal32(26), dscal32(25), st);
+        g0 = read_u32(dscal32(26));
+        // put the probed window back: the loop below accumulates it again
+        dense_init(dstate2[0], occ2[0], sd0, D, st);
+      }
+      int64_t e2 = est;
+      if (w0 < nwin) e2 = std::max<int64_t>(e2, (int64_t)((double)total * (double)g0 / (double)wrows[w0]));
+      const int64_t cap = std::min<int64_t>({total, e2 + e2 / 32 + (int64_t)D + 65536, (int64_t)0xFFFFFFF0ll});
+      void* kptr[ISA_MAX_KEY_COLS] = {nullptr};
+      void* sptr[ISA_MAX_SLOTS] = {nullptr};
+      stream_alloc_called = true;
+      if (out_alloc(out_user, cap, kptr, sptr) != 0) {
+        direct = false;
+      } else {
+        memset(&ded, 0, sizeof(ded));
+        ded.ncols = kd0.ncols;
+        ded.nslots = S;
+        for (int c = 0; c < kd0.ncols; ++c) {
+          ded.shift[c] = kd0.shift[c];
+          ded.width[c] = kd0.width[c];
+          ded.is_signed[c] = dtype_signed(kd0.dtype[c]) ? 1 : 0;
+          ded.key_dst[c] = kptr[c];
+        }
+        for (int s = 0; s < S; ++s) ded.slot_dst[s] = sptr[s];
+        dcap = (u32)cap;
+        CK(cudaMemsetAsync(dscal32(31), 0, sizeof(u32), st));
+        CK(cudaEventRecord(dn_emit_done[0], st));
+      }
+    }
+    if (!direct) {   // room for the estimated output in the result table (grown when short)
+      const int64_t W = cfg.merge_window_rows > 0 ? cfg.merge_window_rows : ((int64_t)48 << 20);
+      result.reserve(std::max<int64_t>(1, std::min<int64_t>(total, est + est / 16 + W)), KW, S);
+    }
     if (stream_want) stream_setup();
     int64_t ub = 0;
     cudaStream_t main_st = st;
@@ -2612,7 +2665,7 @@ struct Engine {
       if (m == 0) continue;
       const int buf = nact++ & 1;
       const int64_t most = std::min<int64_t>(m, D);
-      if (ub + most > (int64_t)(result.lo.bytes / 8)) {
+      if (!direct && ub + most > (int64_t)(result.lo.bytes / 8)) {
         CK(cudaStreamSynchronize(dn_emit));
         result.n = read_u32(dscal32(25));
         ub = result.n;
@@ -2633,8 +2686,12 @@ struct Engine {
       CK(cudaStreamWaitEvent(st, dn_acc_done[buf], 0));
       dense_count(dstate2[buf], occ2[buf], S, cnt_slot, D, dn_counts.as<u32>(), st);
       block_counts_scan(dn_counts.as<u32>(), nblocks, dscal32(26), dscal32(25), st);
-      dense_emit(dstate2[buf], occ2[buf], sd0, cnt_slot, D, kmin + (u64)w * D, dn_counts.as<u32>(), result.plo(),
-                 result.pst(), st);
+      if (direct)
+        dense_emit_cols(dstate2[buf], occ2[buf], sd0, cnt_slot, D, kmin + (u64)w * D, dn_counts.as<u32>(), ded, dcap,
+                        dscal32(31), st);
+      else
+        dense_emit(dstate2[buf], occ2[buf], sd0, cnt_slot, D, kmin + (u64)w * D, dn_counts.as<u32>(), result.plo(),
+                   result.pst(), st);
       CK(cudaMemcpyAsync(dscal32(25), dscal32(26), sizeof(u32), cudaMemcpyDeviceToDevice, st));
       CK(cudaEventRecord(dn_emit_done[buf], st));
       if (streaming) stream_window((u32)std::min<int64_t>(m, 0xFFFFFFFFll));
@@ -2645,6 +2702,19 @@ struct Engine {
     ph_end(ISA_PH_WM_COLLAPSE, total, 0);
     result.n = read_u32(dscal32(25));
     if (result.n > 0xFFFFFFF0u) throw IsaError(ISA_ERR_INVALID_INPUT, "more than 2^32-1 output groups are not supported");
+    if (direct) {
+      if (read_u32(dscal32(31)) || result.n > dcap) {
+        // the caller's columns were too small: merge again, into the result
+        // table (the caller then reads it with isa_result_copy)
+        led.rows_read_back = led_rb0;
+        led.merge_windows = led_mw0;
+        return dense_merge(total, est, false);
+      }
+      result_in_caller = true;
+      streamed_ok = true;
+      streamed_during_merge = false;
+      kt_add_bytes(KF_MERGE, (int64_t)result.n * (8 * KW + 8 * S));
+    }
     return true;
   }
   // a COUNT-like slot (int64 sum of ones): nonzero exactly for occupied entries
@@ -2662,17 +2732,17 @@ struct Engine {
     result.n = 0;
     TilePlan tp;
     const bool tiles = build_tile_plan(tp);
-    {   // room for the estimated output (grown when short)
-      const int64_t est = estimate_groups(total);
+    const int64_t est = estimate_groups(total);
+    stream_want = out_alloc && in_on_host && !tiles && direct_merge_env();
+    { const char* e = getenv("ISA_STREAM_OUT"); if (e && e[0] == '0') stream_want = false; }   // A/B: isa_result_copy
+    stream_total = total;
+    stream_est = est;
+    if (tiles || !dense_merge(total, est)) {
+      // room for the estimated output (grown when short)
       result.reserve(std::max<int64_t>(1, std::min<int64_t>(total, est + est / 16 + W)), KW, S);
-      stream_want = out_alloc && in_on_host && !tiles && direct_merge_env();
-      { const char* e = getenv("ISA_STREAM_OUT"); if (e && e[0] == '0') stream_want = false; }   // A/B: isa_result_copy
-      stream_total = total;
-      stream_est = est;
-    }
-    if (tiles || !dense_merge(total))
       merge_runs(runs, true, [&](Table& w, u32) { append_result(w); }, tiles ? &tp : nullptr,
                  direct_merge_env() ? &result : nullptr);
+    }
     if (streaming) end_stream();
     stream_want = false;
     if (cfg.run_tier == ISA_TIER_FILE && read_u32(dscal32(12)))
@@ -3047,6 +3117,7 @@ struct Engine {
     streaming = streamed_ok = false;
     stream_alloc_called = false;
     streamed_during_merge = false;
+    result_in_caller = false;
     dense_pred = -1;
     raw_left = 0;
     new_frac_hint = 0;
@@ -3238,6 +3309,8 @@ struct Engine {
   void result_copy(void* const* key_out, void* const* slot_out, bool out_on_host, cudaStream_t stream) {
     CK(cudaSetDevice(dev));
     st = stream;
+    if (result_in_caller)
+      throw IsaError(ISA_ERR_CONTRACT, "the result of the last execute was written to the output allocator's columns");
     const u32 n = result.n;
     if (n == 0) return;
     ExportDesc ed;
@@ -3299,6 +3372,7 @@ struct Engine {
     CK(cudaSetDevice(dev));
     st = stream;
     streaming = streamed_ok = false;
+    result_in_caller = false;
     memset(&led, 0, sizeof(led));
     memset(phases, 0, sizeof(phases));
     runs.clear();
@@ -3333,6 +3407,7 @@ struct Engine {
     CK(cudaSetDevice(dev));
     st = stream;
     streaming = streamed_ok = false;
+    result_in_caller = false;
     memset(&led, 0, sizeof(led));
     memset(phases, 0, sizeof(phases));
     runs.clear();

@@ -328,6 +328,9 @@ struct ExportDesc {
 };
 // all key columns + all slots in one kernel (null destinations are skipped)
 void export_all(const u64* lo, const u64* hi, const u64* states, u32 n, const ExportDesc& ed, cudaStream_t st);
+// dense-window merge emitting straight into the caller's columns (see dense_emit): rows >= cap set *over
+void dense_emit_cols(u64* dense, unsigned char* occ, const SlotDesc& sd, int cnt_slot, u32 D, u64 key_lo,
+                     const u32* bbase, const ExportDesc& ed, u32 cap, u32* over, cudaStream_t st);
 
 // ---- partition (multi-GPU range split) -----------------------------------
 void sample_keys(const KeyDesc& kd, int64_t n, int64_t stride, u64* out_lo, u64* out_hi, cudaStream_t st);

@@ -1054,3 +1054,30 @@ def test_partial_key_sort_of_wide_keys(collide):
     _check(res, want_keys, want_slots)
     assert op.cycles == [c for c in cycles if c > 0]
     assert op.ledger.rows_spilled == led["rows_spilled"] and op.runs_after_generation == led["runs"]
+
+
+def test_dense_merge_direct_output_falls_back_when_the_estimate_is_short(monkeypatch):
+    """Device input, dense keys: the dense-window merge emits into the
+    caller's columns, sized after the first window.  Here the first window is
+    nearly empty and the rest of the key range is full, so the columns are too
+    small: the merge runs again into the result table and the result is read
+    with isa_result_copy -- same groups."""
+    monkeypatch.setenv("ISA_DENSE_D", "4096")
+    rng = np.random.default_rng(9)
+    n, memory = 1_200_000, 1 << 13
+    lowk = rng.integers(0, 4096, 8).astype(np.int64)   # 8 keys in the first window
+    k = np.concatenate([lowk, rng.integers(4096, 4096 + (1 << 18), n)]).astype(np.int64)
+    k = k[rng.permutation(len(k))]
+    v = rng.integers(-1000, 1000, len(k)).astype(np.int64)
+    sch = _cut_schema()
+    slots = oracle.make_states(sch, {"v": v}, len(k))
+    want_keys, want_slots = oracle.reference_aggregate([k], slots, oracle.slot_ops(sch))
+    op = isa.SortAggregate(sch, _cfg(memory, 100))
+    res = op.execute_columns([_cuda(k)], {"v": _cuda(v)})
+    _check(res, want_keys, want_slots)
+    assert _phase_ms(op, "wm_sort") == 0
+    monkeypatch.setenv("ISA_DIRECT_OUT", "0")   # result table + export: identical
+    op2 = isa.SortAggregate(sch, _cfg(memory, 100))
+    res2 = op2.execute_columns([_cuda(k)], {"v": _cuda(v)})
+    for a, b in zip(list(res.keys) + list(res.states), list(res2.keys) + list(res2.states)):
+        assert torch.equal(a, b)
