@@ -1056,9 +1056,10 @@ struct Engine {
   // accumulate kernel reads 8 * (KW + S) bytes per row instead of decoding.
   // For the sort-based windows they do not (config 5 at 1e9 rows 189 -> 192
   // ms: the D2D slice copies cost more than unpacking).  Raw runs take at most
-  // 30% of the memory free at the start of the execute (packed runs up to
-  // 50%, hbm_left): the result and the caller's output columns still have to
-  // fit.  ISA_RAW_RUNS=1 / 0 forces raw runs whenever they fit hbm_left / off.
+  // 45% of the memory free at the start of the execute (all runs together up
+  // to 50%, hbm_left): the caller's output columns, and a result table when
+  // the merge needs one, still have to fit.  ISA_RAW_RUNS=1 / 0 forces raw
+  // runs whenever they fit hbm_left / off.
   int dense_pred = -1;     // per execute: -1 unknown, 0 / 1 the dense-window merge is expected
   double raw_left = 0;     // bytes of raw runs still allowed
   bool raw_fits_hbm(u32 rows) {
@@ -3131,7 +3132,7 @@ struct Engine {
       // from the previous execute, reused before anything new is allocated)
       hbm_left = cfg.hbm_run_budget > 0 ? cfg.hbm_run_budget
                                         : (int64_t)(0.5 * ((double)fr + (double)devpool.capacity()));
-      raw_left = 0.6 * (double)hbm_left;
+      raw_left = 0.9 * (double)hbm_left;
     }
     if (cfg.merge_mode != ISA_MERGE_WIDE) {
       auto t0p = std::chrono::steady_clock::now();
