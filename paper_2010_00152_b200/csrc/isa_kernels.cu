@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(256) k_rs_hist_all(const u64* __restrict__ klo
   __syncthreads();
   for (u32 i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
     const u64 lo = klo[i], hi = KW == 2 ? khi[i] : 0;
-    for (int p = 0; p < npass; ++p) atomicAdd(&h[p * 256 + digit_of(hi, lo, bit_lo + 8 * p)], 1u);
+    for (int p = 0; p < npass; ++p) atomicAdd(&h[p * 256 + digit_kw<KW>(hi, lo, bit_lo + 8 * p)], 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < npass * 256; i += 256)
@@ -967,6 +967,31 @@ __global__ void k_build_keys(KeyDesc kd, i64 row0, const u32* __restrict__ pos, 
   u64 r_hi, r_lo;
   load_key(kd, row0 + (pos ? pos[0] : 0), r_hi, r_lo);
   u64 acc_lo = 0, acc_hi = 0;
+  if (KW == 1 && !pos && kd.ncols == 1 && kd.shift[0] == 0 && (kd.dtype[0] == DT_I64 || kd.dtype[0] == DT_U64)) {
+    // one 64-bit key column, rows in order (configs 3 and 5): no per-row
+    // dtype dispatch, four independent loads in flight per thread
+    const u64* col = (const u64*)kd.ptr[0] + row0;
+    const u64 flip = kd.dtype[0] == DT_I64 ? 0x8000000000000000ull : 0ull;
+    const u32 stride = gridDim.x * blockDim.x;
+    u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * (u64)stride < n; i += 4 * stride) {
+      u64 l[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) l[j] = __ldg(col + i + j * stride) ^ flip;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        lo[i + j * stride] = l[j];
+        val[i + j * stride] = i + j * stride;
+        acc_lo |= l[j] ^ r_lo;
+      }
+    }
+    for (; i < n; i += stride) {
+      const u64 l = __ldg(col + i) ^ flip;
+      lo[i] = l;
+      val[i] = i;
+      acc_lo |= l ^ r_lo;
+    }
+  } else
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     u32 r = pos ? pos[i] : i;
     u64 h, l;
