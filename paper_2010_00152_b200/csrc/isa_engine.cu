@@ -689,12 +689,36 @@ struct Engine {
   // (sort_assumed, verify_assumed_mask)
   u64 sticky_vlo = 0, sticky_vhi = 0;
   bool sticky_ok = false, sort_assume = false, sort_assumed = false;
+  int pend_hist_lo = -1, pend_hist_np = 0;   // histograms counted by build_keys for the pending sort
+  static bool hist_fuse_env() {   // ISA_HIST_FUSE=0 (read per sort): the histogram kernel always runs
+    const char* e = getenv("ISA_HIST_FUSE");
+    return !(e && e[0] == '0');
+  }
   int sort_rows(const KeyDesc& kd, int64_t row0, const u32* pos, u32 m, bool assume = false) {
     sort_assume = assume && sticky_ok && assume_env();
     ensure_sort(m);
     ph_begin(ISA_PH_SORT);
     CK(cudaMemsetAsync(dvary(), 0, 2 * sizeof(u64), st));
-    build_keys(KW, kd, row0, pos, m, s_lo[0].as<u64>(), s_hi[0].as<u64>(), s_val[0].as<u32>(), dvary(), st);
+    // with the mask assumed the sort's bit range is known here: the key-building
+    // pass counts the all-pass histograms itself (one read of the keys less)
+    pend_hist_lo = -1;
+    pend_hist_np = 0;
+    u32* gh = nullptr;
+    if (sort_assume && sticky_vhi == 0 && sticky_vlo != 0 && build_keys_counts_histograms(KW, kd, pos) &&
+        hist_fuse_env()) {
+      const int hb = 63 - __builtin_clzll(sticky_vlo);
+      int lb = __builtin_ctzll(sticky_vlo);
+      if (sort_partial_ok && hb - lb + 1 > 48 && m >= (1u << 20) && partial_env()) lb = hb - 47;   // as sort_built
+      const int np = (hb + 1 - lb + 7) / 8;
+      if (np >= 1 && np <= 16) {
+        gh = sort_aux_hist(tile_hist.p);
+        CK(cudaMemsetAsync(gh, 0, sort_aux_hist_bytes(), st));
+        pend_hist_lo = lb;
+        pend_hist_np = np;
+      }
+    }
+    build_keys(KW, kd, row0, pos, m, s_lo[0].as<u64>(), s_hi[0].as<u64>(), s_val[0].as<u32>(), dvary(), st, gh,
+               pend_hist_lo, pend_hist_np);
     sort_ctx = 0;
     sort_val_iota = pos == nullptr;
     int cur = sort_built(m);
@@ -726,6 +750,9 @@ struct Engine {
   int sort_built(u32 m, const u64* known_v = nullptr) {
     const bool iota = sort_val_iota;
     sort_val_iota = false;
+    const int ph_lo = pend_hist_lo, ph_np = pend_hist_np;   // consumed by this sort on every path
+    pend_hist_lo = -1;
+    pend_hist_np = 0;
     sort_assumed = false;
     sort_partial_used = false;
     const bool partial_ok = sort_partial_ok;
@@ -771,6 +798,8 @@ struct Engine {
     b.map_host = h_hist;
     b.pack_ok = true;   // bits outside [lb, hb] do not vary (see above)
     b.val_iota = iota;
+    b.hist_bit_lo = ph_lo;
+    b.hist_npass = ph_np;
     b.carry_in = cin;
     b.carry_out = cout;
     struct CarryBack { bool& f; SortBufs& b; ~CarryBack() { f = b.carried; } } carry_back{sort_carried, b};

@@ -718,14 +718,21 @@ static int radix_lsd(int KW, SortBufs& b, u32 n, int bit_lo, int bit_hi, cudaStr
   const size_t psmem = rs_scatter_smem(1, true);
   static int lb_sleep = -1;   // look-back back-off (ns) while a predecessor has not published
   if (lb_sleep < 0) { const char* e = getenv("ISA_LB_SLEEP"); lb_sleep = e ? atoi(e) : 0; }
+  const bool hist_ready = b.hist_npass == npass && b.hist_bit_lo == bit_lo && start == 0;
+  b.hist_npass = 0;   // consumed (a second sort on these buffers counts for itself)
   if (ntiles > 1) {
     if (npass > RS_MAX_PASS) throw std::runtime_error("radix sort: too many passes");
-    cudaMemsetAsync(ghist, 0, (RS_MAX_PASS * 256 + RS_MAX_PASS) * 4, st);
-    const u32 g = std::min<u32>(ntiles, 148u * 8u);
-    kt_begin(KF_HIST, st);
-    if (KW == 2) klaunch(k_rs_hist_all<2>, g, 256, 0, st, b.lo[cur], b.hi[cur], n, bit_lo, npass, ghist);
-    else klaunch(k_rs_hist_all<1>, g, 256, 0, st, b.lo[cur], (const u64*)nullptr, n, bit_lo, npass, ghist);
-    kt_end(KF_HIST, (int64_t)n * 8 * KW, st);
+    if (hist_ready) {
+      // counted by the key-building pass: only the tile counters are reset
+      cudaMemsetAsync(tctr, 0, RS_MAX_PASS * 4, st);
+    } else {
+      cudaMemsetAsync(ghist, 0, (RS_MAX_PASS * 256 + RS_MAX_PASS) * 4, st);
+      const u32 g = std::min<u32>(ntiles, 148u * 8u);
+      kt_begin(KF_HIST, st);
+      if (KW == 2) klaunch(k_rs_hist_all<2>, g, 256, 0, st, b.lo[cur], b.hi[cur], n, bit_lo, npass, ghist);
+      else klaunch(k_rs_hist_all<1>, g, 256, 0, st, b.lo[cur], (const u64*)nullptr, n, bit_lo, npass, ghist);
+      kt_end(KF_HIST, (int64_t)n * 8 * KW, st);
+    }
   }
   // ranking per pass: ballots for large passes without heavy digits (one
   // small read-back of the histograms; MATCH.ANY otherwise)
@@ -963,7 +970,16 @@ void check_sorted(const u64* lo, u32 n, u32* bad_mapped, cudaStream_t st) {
 // ======================================================= key building ====
 template <int KW>
 __global__ void k_build_keys(KeyDesc kd, i64 row0, const u32* __restrict__ pos, u32 n, u64* __restrict__ lo,
-                             u64* __restrict__ hi, u32* __restrict__ val, u64* __restrict__ varying) {
+                             u64* __restrict__ hi, u32* __restrict__ val, u64* __restrict__ varying,
+                             u32* __restrict__ ghist, int h_bit_lo, int h_npass) {
+  // ghist != nullptr (fast path only): the all-pass digit histograms of the
+  // sort that follows (bits [h_bit_lo, h_bit_lo + 8 * h_npass)) are counted
+  // here, while the keys are in registers, instead of a pass of their own
+  __shared__ u32 hsm[KW == 1 ? RS_MAX_PASS * 256 : 1];
+  if (KW == 1 && ghist) {
+    for (int i = threadIdx.x; i < h_npass * 256; i += blockDim.x) hsm[i] = 0;
+    __syncthreads();
+  }
   u64 r_hi, r_lo;
   load_key(kd, row0 + (pos ? pos[0] : 0), r_hi, r_lo);
   u64 acc_lo = 0, acc_hi = 0;
@@ -983,6 +999,8 @@ __global__ void k_build_keys(KeyDesc kd, i64 row0, const u32* __restrict__ pos, 
         lo[i + j * stride] = l[j];
         val[i + j * stride] = i + j * stride;
         acc_lo |= l[j] ^ r_lo;
+        if (ghist)
+          for (int p = 0; p < h_npass; ++p) atomicAdd(&hsm[p * 256 + ((u32)(l[j] >> (h_bit_lo + 8 * p)) & 0xFFu)], 1u);
       }
     }
     for (; i < n; i += stride) {
@@ -990,6 +1008,13 @@ __global__ void k_build_keys(KeyDesc kd, i64 row0, const u32* __restrict__ pos, 
       lo[i] = l;
       val[i] = i;
       acc_lo |= l ^ r_lo;
+      if (ghist)
+        for (int p = 0; p < h_npass; ++p) atomicAdd(&hsm[p * 256 + ((u32)(l >> (h_bit_lo + 8 * p)) & 0xFFu)], 1u);
+    }
+    if (ghist) {
+      __syncthreads();
+      for (int q = threadIdx.x; q < h_npass * 256; q += blockDim.x)
+        if (hsm[q]) atomicAdd(&ghist[q], hsm[q]);
     }
   } else
   for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -1020,13 +1045,21 @@ static int grid_for(u64 n, int threads, int cap) {
   return (int)g;
 }
 
+// the kernel's fast path (one 64-bit key column in row order): it can count the sort's histograms on the way
+bool build_keys_counts_histograms(int KW, const KeyDesc& kd, const u32* pos) {
+  return KW == 1 && !pos && kd.ncols == 1 && kd.shift[0] == 0 && (kd.dtype[0] == DT_I64 || kd.dtype[0] == DT_U64);
+}
 void build_keys(int KW, const KeyDesc& kd, int64_t row0, const u32* pos, u32 n, u64* lo, u64* hi, u32* val,
-                u64* varying, cudaStream_t st) {
+                u64* varying, cudaStream_t st, u32* ghist, int h_bit_lo, int h_npass) {
   if (n == 0) return;
   int g = grid_for(n, 256);
-  if (KW == 2) klaunch(k_build_keys<2>, g, 256, 0, st, kd, row0, pos, n, lo, hi, val, varying);
-  else klaunch(k_build_keys<1>, g, 256, 0, st, kd, row0, pos, n, lo, hi, val, varying);
+  if (!build_keys_counts_histograms(KW, kd, pos) || h_npass < 1 || h_npass > RS_MAX_PASS) ghist = nullptr;
+  if (KW == 2) klaunch(k_build_keys<2>, g, 256, 0, st, kd, row0, pos, n, lo, hi, val, varying, (u32*)nullptr, 0, 0);
+  else klaunch(k_build_keys<1>, g, 256, 0, st, kd, row0, pos, n, lo, hi, val, varying, ghist, h_bit_lo, h_npass);
 }
+// the histogram area of a sort's aux buffer (zeroed by whoever counts into it)
+u32* sort_aux_hist(void* aux) { return (u32*)aux; }
+size_t sort_aux_hist_bytes() { return (size_t)RS_MAX_PASS * 256 * 4; }
 
 template <int KW>
 __global__ void k_keys_varying(const u64* __restrict__ lo, const u64* __restrict__ hi, u32 n, u64* varying) {

@@ -26,6 +26,9 @@ struct SortBufs {
   int hint_bit_lo = -1, hint_npass = 0;
   bool pack_ok = false;   // key bits outside [bit_lo, bit_hi) are equal in every key (packed passes allowed)
   bool val_iota = false;  // val[0][i] == i (row ids 0..n-1): a packing first pass numbers the rows itself
+  // the all-pass histograms of bits [hist_bit_lo, hist_bit_lo + 8 * hist_npass) are already in the aux buffer
+  // (counted by build_keys); used when the sort's first radix_lsd call covers exactly those passes
+  int hist_bit_lo = -1, hist_npass = 0;
   // carried values: carry_in[i] = a 4-byte value of row i; when the sort runs packed passes it moves the
   // values with the keys and leaves them in sorted order in carry_out (carried = true on return)
   const u32* carry_in = nullptr;
@@ -46,7 +49,13 @@ void sort_small_segments(u64* lo, u64* hi, u32* val, u32 n, u32 maxlen, int shif
 // keys of rows row0 + (pos ? pos[i] : i), i < n  ->  lo/hi/val(=pos or i);
 // varying[0..1] |= key ^ key_of_first (lo, hi).
 void build_keys(int KW, const KeyDesc& kd, int64_t row0, const u32* pos, u32 n,
-                u64* lo, u64* hi, u32* val, u64* varying, cudaStream_t st);
+                    u64* lo, u64* hi, u32* val, u64* varying, cudaStream_t st,
+                    u32* ghist = nullptr, int h_bit_lo = 0, int h_npass = 0);
+// ghist (the zeroed histogram area of the sort's aux buffer): also count the all-pass digit histograms of bits
+// [h_bit_lo, h_bit_lo + 8 * h_npass) -- only when build_keys_counts_histograms(...)
+bool build_keys_counts_histograms(int KW, const KeyDesc& kd, const u32* pos);
+u32* sort_aux_hist(void* aux);
+size_t sort_aux_hist_bytes();
 // varying |= key ^ key[0] for an existing SoA key array
 void keys_varying(int KW, const u64* lo, const u64* hi, u32 n, u64* varying, cudaStream_t st);
 void iota_u32(u32* v, u32 n, cudaStream_t st);
