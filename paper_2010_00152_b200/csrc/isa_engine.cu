@@ -24,7 +24,13 @@
 //     advanced past it; on the GPU this is a partition of the key space into
 //     windows: window [s_i, s_{i+1}) is final as soon as every run's slice of
 //     it has been read.  Each window's slices are staged (H2D for host-tier
-//     runs), radix-sorted and collapsed.
+//     runs), radix-sorted and collapsed; 128-bit keys merge their windows
+//     tile by tile in shared memory (isa_merge.cu); dense integer key
+//     domains accumulate every window by direct addressing into an
+//     L2-resident state array, reading the HBM-resident runs in place
+//     (dense_merge, isa_codec.cu).  With an output allocator the groups go
+//     straight to the caller's columns (device input) or leave for the
+//     caller's pinned host columns window by window while the merge runs.
 #include "isa_kernels.h"
 #include "../../include/insortagg_b200.h"
 
